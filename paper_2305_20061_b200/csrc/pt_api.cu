@@ -1,0 +1,520 @@
+// pt_api.cu -- C-ABI of libpt_b200 (include/pt.h) and the wavefront render loop.
+//
+// Per wave of k consecutive samples x all pixels (SURVEY.md 8a "Wave"):
+//   raygen -> for depth 1..max_depth { traverse -> shade (scatter, RR, compaction) } -> NIF -> accumulate.
+// All queue lengths live in device counters, so the host never synchronises inside a wave; kernels
+// size their grids to the SM count and read their work counts on the device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "pt_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CU(expr)                                                                                   \
+    do {                                                                                           \
+        cudaError_t _e = (expr);                                                                   \
+        if (_e != cudaSuccess) {                                                                   \
+            return fail(_e == cudaErrorMemoryAllocation ? PT_ERR_OOM : PT_ERR_CUDA,                \
+                        std::string(#expr) + ": " + cudaGetErrorString(_e));                       \
+        }                                                                                          \
+    } while (0)
+
+int check_device() {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return fail(PT_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (major != 10) return fail(PT_ERR_CUDA, "libpt_b200 requires an sm_100 (B200) device");
+    return PT_OK;
+}
+
+bool finite3(const float* v) { return std::isfinite(v[0]) && std::isfinite(v[1]) && std::isfinite(v[2]); }
+
+void free_ws(pt::Workspace& ws) {
+    cudaFree(ws.ray_o); cudaFree(ws.ray_d); cudaFree(ws.beta);
+    cudaFree(ws.queue[0]); cudaFree(ws.queue[1]); cudaFree(ws.hit);
+    cudaFree(ws.esc); cudaFree(ws.esc_beta); cudaFree(ws.wave_buf); cudaFree(ws.counters);
+    cudaFree(ws.fb);
+    cudaFree(ws.d_stats);
+    if (ws.own_stream) cudaStreamDestroy(ws.own_stream);
+    ws = pt::Workspace();
+}
+
+int ensure_ws(pt::Workspace& ws, int64_t cap) {
+    if (!ws.counters) {
+        CU(cudaMalloc(&ws.counters, sizeof(uint32_t) * pt::kCounters));
+        CU(cudaMalloc(&ws.d_stats, sizeof(unsigned long long) * 4));
+        CU(cudaMemset(ws.d_stats, 0, sizeof(unsigned long long) * 4));
+        CU(cudaStreamCreateWithFlags(&ws.own_stream, cudaStreamNonBlocking));
+    }
+    if (cap <= ws.capacity) return PT_OK;
+    cudaFree(ws.ray_o); cudaFree(ws.ray_d); cudaFree(ws.beta);
+    cudaFree(ws.queue[0]); cudaFree(ws.queue[1]); cudaFree(ws.hit);
+    cudaFree(ws.esc); cudaFree(ws.esc_beta); cudaFree(ws.wave_buf);
+    ws.capacity = 0;
+    CU(cudaMalloc(&ws.ray_o, sizeof(float4) * cap));
+    CU(cudaMalloc(&ws.ray_d, sizeof(float4) * cap));
+    CU(cudaMalloc(&ws.beta, sizeof(float4) * cap));
+    CU(cudaMalloc(&ws.queue[0], sizeof(uint32_t) * cap));
+    CU(cudaMalloc(&ws.queue[1], sizeof(uint32_t) * cap));
+    CU(cudaMalloc(&ws.hit, sizeof(float4) * cap));
+    CU(cudaMalloc(&ws.esc, sizeof(float4) * cap));
+    CU(cudaMalloc(&ws.esc_beta, sizeof(float4) * cap));
+    CU(cudaMalloc(&ws.wave_buf, sizeof(float) * 3 * cap));
+    ws.capacity = cap;
+    return PT_OK;
+}
+
+pt::TraceParams trace_params(const pt_scene* sc) {
+    pt::TraceParams tp;
+    tp.pool = sc->d_pool;
+    tp.empty = sc->empty ? 1 : 0;
+    tp.tri_v = sc->d_tri_v;
+    tp.sph = sc->d_sph;
+    tp.sph_mat = sc->d_sph_mat;
+    tp.mats = sc->d_mats;
+    tp.n_tris = sc->n_tris;
+    return tp;
+}
+
+// kernel-class timers for profiling (CUDA events on the launching stream)
+enum { T_RAYGEN, T_TRAVERSE, T_SHADE, T_NIF, T_ACCUM, T_N };
+
+struct Timer {
+    bool on;
+    cudaStream_t st;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> rec;
+    void begin(int, cudaEvent_t* a) {
+        if (!on) return;
+        cudaEventCreate(a);
+        cudaEventRecord(*a, st);
+    }
+    void end(int cls, cudaEvent_t a) {
+        if (!on) return;
+        cudaEvent_t b;
+        cudaEventCreate(&b);
+        cudaEventRecord(b, st);
+        rec.push_back({cls, {a, b}});
+    }
+    void collect(pt_stats& s) {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        for (auto& r : rec) {
+            float ms = 0.0f;
+            cudaEventElapsedTime(&ms, r.second.first, r.second.second);
+            double* dst = r.first == T_RAYGEN ? &s.t_raygen_ms
+                        : r.first == T_TRAVERSE ? &s.t_traverse_ms
+                        : r.first == T_SHADE ? &s.t_shade_ms
+                        : r.first == T_NIF ? &s.t_nif_ms : &s.t_accum_ms;
+            *dst += ms;
+            cudaEventDestroy(r.second.first);
+            cudaEventDestroy(r.second.second);
+        }
+        rec.clear();
+    }
+};
+
+__global__ void stats_kernel(const uint32_t* counters, int max_depth, unsigned long long* acc) {
+    unsigned long long seg = 0;
+    for (int d = 0; d < max_depth; ++d) seg += counters[d];
+    acc[0] += counters[0];
+    acc[1] += seg;
+    acc[2] += counters[pt::kCounterEsc];
+}
+
+__global__ void set_count_kernel(uint32_t* c, uint32_t v) { *c = v; }
+
+int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, int W, int H, int first_sample,
+                        int n_samples, int max_depth, uint64_t seed, int wave_samples, float* d_accum,
+                        cudaStream_t st) {
+    if (W < 1 || H < 1 || n_samples < 1 || max_depth < 1 || first_sample < 0)
+        return fail(PT_ERR_INVALID_ARG, "width, height, n_samples, max_depth must be >= 1");
+    if (max_depth >= pt::kCounterEsc - 1) return fail(PT_ERR_INVALID_ARG, "max_depth too large (<= 60)");
+    if (!nif && !env_rgb) return fail(PT_ERR_INVALID_ARG, "env_rgb must be given when nif is NULL");
+    if (!d_accum) return fail(PT_ERR_INVALID_ARG, "d_accum is NULL");
+    const int64_t np = (int64_t)W * H;
+    if (np > (1ll << 31) / 2) return fail(PT_ERR_INVALID_ARG, "frame too large");
+    int64_t k = wave_samples;
+    if (k <= 0) k = std::max<int64_t>(1, std::min<int64_t>(n_samples, (int64_t)(8 << 20) / np));
+    k = std::min<int64_t>(k, n_samples);
+    while (k > 1 && k * np > (1ll << 31)) --k;
+    int rc = ensure_ws(sc->ws, k * np);
+    if (rc) return rc;
+    pt::Workspace& ws = sc->ws;
+    unsigned long long* d_stats = ws.d_stats;
+    CU(cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * 4, st));
+    const pt::Cam32 cam = pt::make_cam32(sc->cam, W, H);
+    const pt::TraceParams tp = trace_params(sc);
+    const float3 env = env_rgb ? make_float3(env_rgb[0], env_rgb[1], env_rgb[2]) : make_float3(0, 0, 0);
+    const int use_nif = nif ? 1 : 0;
+    Timer tm{sc->profiling, st, {}};
+    pt_stats stats{};
+    for (int64_t w0 = first_sample; w0 < (int64_t)first_sample + n_samples; w0 += k) {
+        const int64_t kk = std::min<int64_t>(k, (int64_t)first_sample + n_samples - w0);
+        const int64_t slots = kk * np;
+        CU(cudaMemsetAsync(ws.counters, 0, sizeof(uint32_t) * pt::kCounters, st));
+        set_count_kernel<<<1, 1, 0, st>>>(ws.counters + 0, (uint32_t)slots);
+        cudaEvent_t e0;
+        tm.begin(T_RAYGEN, &e0);
+        pt::launch_raygen(cam, W, H, (int)w0, (int)slots, seed, ws, st);
+        tm.end(T_RAYGEN, e0);
+        for (int d = 1; d <= max_depth; ++d) {
+            const int identity = d == 1;
+            const uint32_t* qin = identity ? nullptr : ws.queue[d & 1];
+            uint32_t* qout = ws.queue[(d + 1) & 1];
+            tm.begin(T_TRAVERSE, &e0);
+            pt::launch_traverse(tp, qin, ws.counters + (d - 1), identity, ws, st);
+            tm.end(T_TRAVERSE, e0);
+            tm.begin(T_SHADE, &e0);
+            pt::launch_shade(tp, W, H, (int)w0, d, max_depth, seed, qin, ws.counters + (d - 1), identity, qout,
+                             ws.counters + d, use_nif, env, ws, st);
+            tm.end(T_SHADE, e0);
+            stats.launches += 2;
+            stats.traverse_launches += 1;
+        }
+        if (use_nif) {
+            tm.begin(T_NIF, &e0);
+            cudaError_t e = pt::launch_nif(nif, ws.esc, ws.esc_beta, ws.counters + pt::kCounterEsc, slots, ws.wave_buf, st);
+            tm.end(T_NIF, e0);
+            if (e != cudaSuccess) return fail(PT_ERR_CUDA, std::string("nif launch: ") + cudaGetErrorString(e));
+            stats.launches += 1;
+            stats.nif_launches += 1;
+        }
+        tm.begin(T_ACCUM, &e0);
+        pt::launch_accumulate(ws.wave_buf, (int)np, (int)kk, d_accum, st);
+        tm.end(T_ACCUM, e0);
+        stats_kernel<<<1, 1, 0, st>>>(ws.counters, max_depth, d_stats);
+        stats.launches += 2;
+        stats.waves += 1;
+    }
+    CU(cudaGetLastError());
+    tm.collect(stats);   // synchronises only while profiling is on
+    sc->stats = stats;   // paths/segments/escaped are read from ws.d_stats by pt_get_stats
+    return PT_OK;
+}
+
+}  // namespace
+
+namespace pt {
+
+Cam32 make_cam32(const pt_camera& c, int W, int H) {
+    // fp64 on the host, rounded once to fp32 (reading R22)
+    double f[3], r[3], u[3];
+    for (int a = 0; a < 3; ++a) f[a] = (double)c.look_at[a] - (double)c.eye[a];
+    const double lf = std::sqrt((f[0] * f[0] + f[1] * f[1]) + f[2] * f[2]);
+    for (int a = 0; a < 3; ++a) f[a] /= lf;
+    const double up[3] = {c.up[0], c.up[1], c.up[2]};
+    r[0] = f[1] * up[2] - f[2] * up[1];
+    r[1] = f[2] * up[0] - f[0] * up[2];
+    r[2] = f[0] * up[1] - f[1] * up[0];
+    const double lr = std::sqrt((r[0] * r[0] + r[1] * r[1]) + r[2] * r[2]);
+    for (int a = 0; a < 3; ++a) r[a] /= lr;
+    u[0] = r[1] * f[2] - r[2] * f[1];
+    u[1] = r[2] * f[0] - r[0] * f[2];
+    u[2] = r[0] * f[1] - r[1] * f[0];
+    const double t = std::tan(0.5 * (double)c.vfov_deg * 3.14159265358979323846 / 180.0);
+    Cam32 k;
+    for (int a = 0; a < 3; ++a) {
+        k.f[a] = (float)f[a];
+        k.r[a] = (float)r[a];
+        k.u[a] = (float)u[a];
+        k.eye[a] = c.eye[a];
+    }
+    k.ta = (float)(t * ((double)W / (double)H));
+    k.t = (float)t;
+    return k;
+}
+
+cudaError_t launch_nif_debug(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,
+                             int64_t rows, float* out, float* dbg, cudaStream_t st);
+
+}  // namespace pt
+
+extern "C" {
+
+const char* pt_last_error(void) { return g_err.c_str(); }
+const char* pt_version(void) { return "pt_b200 0.1 sm_100a"; }
+
+int pt_scene_create(const pt_triangle* tris, int64_t n_tris, const pt_sphere* spheres, int64_t n_spheres,
+                    const pt_material* mats, int32_t n_mats, const pt_camera* cam, pt_scene** out) {
+    if (!out || !cam || n_tris < 0 || n_spheres < 0 || n_mats < 0) return fail(PT_ERR_INVALID_ARG, "bad argument");
+    if ((n_tris > 0 && !tris) || (n_spheres > 0 && !spheres) || (n_mats > 0 && !mats))
+        return fail(PT_ERR_INVALID_ARG, "null array with positive count");
+    if (n_tris + n_spheres >= (1ll << 31) - 1) return fail(PT_ERR_INVALID_ARG, "too many primitives");
+    *out = nullptr;
+    for (int64_t i = 0; i < n_tris; ++i) {
+        if (!finite3(tris[i].v0) || !finite3(tris[i].v1) || !finite3(tris[i].v2))
+            return fail(PT_ERR_DOMAIN, "non-finite triangle vertex");
+        if (tris[i].material >= (uint32_t)n_mats) return fail(PT_ERR_INVALID_ARG, "triangle material out of range");
+    }
+    for (int64_t i = 0; i < n_spheres; ++i) {
+        if (!finite3(spheres[i].center) || !std::isfinite(spheres[i].radius) || !(spheres[i].radius > 0.0f))
+            return fail(PT_ERR_DOMAIN, "non-finite sphere or radius <= 0");
+        if (spheres[i].material >= (uint32_t)n_mats) return fail(PT_ERR_INVALID_ARG, "sphere material out of range");
+    }
+    for (int32_t i = 0; i < n_mats; ++i)
+        if (mats[i].kind > PT_EMISSIVE) return fail(PT_ERR_INVALID_ARG, "unknown material kind");
+    int rc = check_device();
+    if (rc) return rc;
+    pt::HostBvh bvh;
+    std::string msg;
+    rc = pt::build_wide_bvh(tris, n_tris, spheres, n_spheres, &bvh, &msg);
+    if (rc) return fail(rc, msg);
+    pt_scene* sc = new pt_scene();
+    cudaGetDevice(&sc->device);
+    sc->n_tris = n_tris;
+    sc->n_sph = n_spheres;
+    sc->n_mats = n_mats;
+    sc->cam = *cam;
+    sc->empty = bvh.empty;
+    sc->bvh_nodes = bvh.n_nodes;
+    sc->bvh_leaves = bvh.n_leaves;
+    sc->bvh_depth = bvh.max_depth;
+    auto cleanup = [&](int code, const std::string& m) {
+        pt_scene_destroy(sc);
+        return fail(code, m);
+    };
+#define CUS(expr)                                                                                        \
+    do {                                                                                                 \
+        cudaError_t _e = (expr);                                                                         \
+        if (_e != cudaSuccess)                                                                           \
+            return cleanup(_e == cudaErrorMemoryAllocation ? PT_ERR_OOM : PT_ERR_CUDA, cudaGetErrorString(_e)); \
+    } while (0)
+    sc->pool_units = (int64_t)bvh.pool.size();
+    if (sc->pool_units > 0) {
+        CUS(cudaMalloc(&sc->d_pool, sizeof(uint4) * sc->pool_units));
+        CUS(cudaMemcpy(sc->d_pool, bvh.pool.data(), sizeof(uint4) * sc->pool_units, cudaMemcpyHostToDevice));
+    }
+    if (n_tris > 0) {
+        std::vector<float4> tv(3 * n_tris);
+        for (int64_t i = 0; i < n_tris; ++i) {
+            uint32_t mb = tris[i].material;
+            float mf;
+            std::memcpy(&mf, &mb, 4);
+            tv[3 * i + 0] = make_float4(tris[i].v0[0], tris[i].v0[1], tris[i].v0[2], mf);
+            tv[3 * i + 1] = make_float4(tris[i].v1[0], tris[i].v1[1], tris[i].v1[2], 0.0f);
+            tv[3 * i + 2] = make_float4(tris[i].v2[0], tris[i].v2[1], tris[i].v2[2], 0.0f);
+        }
+        CUS(cudaMalloc(&sc->d_tri_v, sizeof(float4) * tv.size()));
+        CUS(cudaMemcpy(sc->d_tri_v, tv.data(), sizeof(float4) * tv.size(), cudaMemcpyHostToDevice));
+    }
+    if (n_spheres > 0) {
+        std::vector<float4> sv(n_spheres);
+        std::vector<uint32_t> sm(n_spheres);
+        for (int64_t i = 0; i < n_spheres; ++i) {
+            sv[i] = make_float4(spheres[i].center[0], spheres[i].center[1], spheres[i].center[2], spheres[i].radius);
+            sm[i] = spheres[i].material;
+        }
+        CUS(cudaMalloc(&sc->d_sph, sizeof(float4) * n_spheres));
+        CUS(cudaMemcpy(sc->d_sph, sv.data(), sizeof(float4) * n_spheres, cudaMemcpyHostToDevice));
+        CUS(cudaMalloc(&sc->d_sph_mat, sizeof(uint32_t) * n_spheres));
+        CUS(cudaMemcpy(sc->d_sph_mat, sm.data(), sizeof(uint32_t) * n_spheres, cudaMemcpyHostToDevice));
+    }
+    if (n_mats > 0) {
+        static_assert(sizeof(pt::DevMaterial) == sizeof(pt_material), "material layout");
+        CUS(cudaMalloc(&sc->d_mats, sizeof(pt_material) * n_mats));
+        CUS(cudaMemcpy(sc->d_mats, mats, sizeof(pt_material) * n_mats, cudaMemcpyHostToDevice));
+    }
+#undef CUS
+    *out = sc;
+    return PT_OK;
+}
+
+int pt_scene_destroy(pt_scene* sc) {
+    if (!sc) return PT_OK;
+    {
+        std::lock_guard<std::mutex> lk(sc->mu);
+        cudaFree(sc->d_pool); cudaFree(sc->d_tri_v); cudaFree(sc->d_sph); cudaFree(sc->d_sph_mat); cudaFree(sc->d_mats);
+        free_ws(sc->ws);
+    }
+    delete sc;
+    return PT_OK;
+}
+
+int pt_nif_load(const uint16_t* blob, int64_t n_halves, pt_nif** out) {
+    if (!blob || !out) return fail(PT_ERR_INVALID_ARG, "null argument");
+    *out = nullptr;
+    if (n_halves != 50307) return fail(PT_ERR_FORMAT, "NIF blob must hold 50307 fp16 values (SIREN 2-128x4-3)");
+    for (int64_t i = 0; i < n_halves; ++i)
+        if ((blob[i] & 0x7C00u) == 0x7C00u) return fail(PT_ERR_DOMAIN, "non-finite NIF weight");
+    int rc = check_device();
+    if (rc) return rc;
+    std::vector<uint8_t> img;
+    pt::nif_build_smem_image(blob, &img);
+    pt_nif* n = new pt_nif();
+    cudaGetDevice(&n->device);
+    n->smem_bytes = (int64_t)img.size();
+    cudaError_t e = cudaMalloc(&n->d_smem_image, img.size());
+    if (e == cudaSuccess) e = cudaMemcpy(n->d_smem_image, img.data(), img.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&n->d_blob, sizeof(uint16_t) * n_halves);
+    if (e == cudaSuccess) e = cudaMemcpy(n->d_blob, blob, sizeof(uint16_t) * n_halves, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        pt_nif_destroy(n);
+        return fail(e == cudaErrorMemoryAllocation ? PT_ERR_OOM : PT_ERR_CUDA, cudaGetErrorString(e));
+    }
+    *out = n;
+    return PT_OK;
+}
+
+int pt_nif_destroy(pt_nif* n) {
+    if (!n) return PT_OK;
+    cudaFree(n->d_smem_image);
+    cudaFree(n->d_blob);
+    delete n;
+    return PT_OK;
+}
+
+int pt_render_samples(const pt_scene* scene, const pt_nif* nif, const float env_rgb[3], int32_t width, int32_t height,
+                      int32_t first_sample, int32_t n_samples, int32_t max_depth, uint64_t seed, int32_t wave_samples,
+                      float* d_accum, void* stream) {
+    if (!scene) return fail(PT_ERR_INVALID_ARG, "scene is NULL");
+    pt_scene* sc = const_cast<pt_scene*>(scene);
+    std::lock_guard<std::mutex> lk(sc->mu);
+    return render_samples_impl(sc, nif, env_rgb, width, height, first_sample, n_samples, max_depth, seed,
+                               wave_samples, d_accum, (cudaStream_t)stream);
+}
+
+int pt_render(const pt_scene* scene, const pt_nif* nif, const float env_rgb[3], int32_t width, int32_t height,
+              int32_t spp, int32_t max_depth, uint64_t seed, float* out_rgb) {
+    if (!scene || !out_rgb) return fail(PT_ERR_INVALID_ARG, "null argument");
+    if (width < 1 || height < 1 || spp < 1 || max_depth < 1) return fail(PT_ERR_INVALID_ARG, "W, H, spp, max_depth >= 1");
+    pt_scene* sc = const_cast<pt_scene*>(scene);
+    std::lock_guard<std::mutex> lk(sc->mu);
+    int rc = ensure_ws(sc->ws, 1);
+    if (rc) return rc;
+    const int64_t n = (int64_t)width * height * 3;
+    if (sc->ws.fb_capacity < n) {
+        cudaFree(sc->ws.fb);
+        sc->ws.fb = nullptr;
+        sc->ws.fb_capacity = 0;
+        CU(cudaMalloc(&sc->ws.fb, sizeof(float) * n));
+        sc->ws.fb_capacity = n;
+    }
+    cudaStream_t st = sc->ws.own_stream;
+    CU(cudaMemsetAsync(sc->ws.fb, 0, sizeof(float) * n, st));
+    rc = render_samples_impl(sc, nif, env_rgb, width, height, 0, spp, max_depth, seed, 0, sc->ws.fb, st);
+    if (rc) return rc;
+    pt::launch_scale(sc->ws.fb, n, 1.0f / (float)spp, st);
+    CU(cudaMemcpyAsync(out_rgb, sc->ws.fb, sizeof(float) * n, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    return PT_OK;
+}
+
+int pt_trace_primary(const pt_scene* scene, int32_t width, int32_t height, uint64_t seed, int32_t sample,
+                     int32_t* d_prim, float* d_t, void* stream) {
+    if (!scene || !d_prim || !d_t || width < 1 || height < 1 || sample < 0)
+        return fail(PT_ERR_INVALID_ARG, "bad argument");
+    const pt::Cam32 cam = pt::make_cam32(scene->cam, width, height);
+    pt::launch_primary(trace_params(scene), cam, width, height, sample, seed, d_prim, d_t, (cudaStream_t)stream);
+    CU(cudaGetLastError());
+    return PT_OK;
+}
+
+int pt_trace_rays(const pt_scene* scene, const float* d_o, const float* d_d, int64_t n, int32_t* d_prim, float* d_t,
+                  void* stream) {
+    if (!scene || n < 0 || (n > 0 && (!d_o || !d_d || !d_prim || !d_t))) return fail(PT_ERR_INVALID_ARG, "bad argument");
+    if (n == 0) return PT_OK;
+    pt::launch_trace_rays(trace_params(scene), d_o, d_d, n, d_prim, d_t, (cudaStream_t)stream);
+    CU(cudaGetLastError());
+    return PT_OK;
+}
+
+static int nif_infer_impl(const pt_nif* nif, const float* d_uv, int64_t n, float* d_rgb, float* d_dbg, void* stream) {
+    if (!nif || n < 0 || (n > 0 && (!d_uv || !d_rgb))) return fail(PT_ERR_INVALID_ARG, "bad argument");
+    if (n == 0) return PT_OK;
+    if (n > (1ll << 31)) return fail(PT_ERR_INVALID_ARG, "too many queries");
+    cudaStream_t st = (cudaStream_t)stream;
+    // scratch queue (test/bench hook): cached per process, grown on demand
+    static float4* esc = nullptr;
+    static float4* esc_beta = nullptr;
+    static uint32_t* cnt = nullptr;
+    static int64_t cap = 0;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    if (n > cap) {
+        CU(cudaStreamSynchronize(st));
+        cudaFree(esc); cudaFree(esc_beta);
+        esc = esc_beta = nullptr;
+        cap = 0;
+        CU(cudaMalloc(&esc, sizeof(float4) * n));
+        CU(cudaMalloc(&esc_beta, sizeof(float4) * n));
+        cap = n;
+    }
+    if (!cnt) CU(cudaMalloc(&cnt, sizeof(uint32_t)));
+    pt::launch_pack_queries(d_uv, n, esc, esc_beta, cnt, st);
+    cudaError_t e = d_dbg ? pt::launch_nif_debug(nif, esc, esc_beta, cnt, n, d_rgb, d_dbg, st)
+                          : pt::launch_nif(nif, esc, esc_beta, cnt, n, d_rgb, st);
+    if (e != cudaSuccess) return fail(PT_ERR_CUDA, std::string("nif launch: ") + cudaGetErrorString(e));
+    return PT_OK;
+}
+
+int pt_nif_infer(const pt_nif* nif, const float* d_uv, int64_t n, float* d_rgb, void* stream) {
+    return nif_infer_impl(nif, d_uv, n, d_rgb, nullptr, stream);
+}
+
+// test hook (not in pt.h): raw accumulators of every layer, d_dbg[5][n][128] fp32
+PT_API int pt_debug_nif_layers(const pt_nif* nif, const float* d_uv, int64_t n, float* d_rgb, float* d_dbg, void* stream) {
+    if (!d_dbg) return fail(PT_ERR_INVALID_ARG, "d_dbg is NULL");
+    return nif_infer_impl(nif, d_uv, n, d_rgb, d_dbg, stream);
+}
+
+int pt_get_stats(const pt_scene* scene, pt_stats* out) {
+    if (!scene || !out) return fail(PT_ERR_INVALID_ARG, "null argument");
+    pt_scene* sc = const_cast<pt_scene*>(scene);
+    std::lock_guard<std::mutex> lk(sc->mu);
+    *out = sc->stats;
+    if (sc->ws.d_stats) {
+        unsigned long long h[4] = {0, 0, 0, 0};
+        CU(cudaDeviceSynchronize());
+        CU(cudaMemcpy(h, sc->ws.d_stats, sizeof(h), cudaMemcpyDeviceToHost));
+        out->paths = (int64_t)h[0];
+        out->segments = (int64_t)h[1];
+        out->escaped = (int64_t)h[2];
+    }
+    return PT_OK;
+}
+
+int pt_set_profiling(pt_scene* scene, int32_t enabled) {
+    if (!scene) return fail(PT_ERR_INVALID_ARG, "null argument");
+    std::lock_guard<std::mutex> lk(scene->mu);
+    scene->profiling = enabled != 0;
+    return PT_OK;
+}
+
+// host-only test hooks of the BVH builder (no GPU needed; not in pt.h)
+PT_API int pt_debug_build_bvh(const pt_triangle* tris, int64_t n_tris, const pt_sphere* spheres, int64_t n_spheres,
+                       int64_t* stats /* [4]: nodes, leaves, depth, pool units */, uint32_t* pool_out,
+                       int64_t pool_cap_units) {
+    pt::HostBvh bvh;
+    std::string msg;
+    int rc = pt::build_wide_bvh(tris, n_tris, spheres, n_spheres, &bvh, &msg);
+    if (rc) return fail(rc, msg);
+    if (stats) {
+        stats[0] = bvh.n_nodes;
+        stats[1] = bvh.n_leaves;
+        stats[2] = bvh.max_depth;
+        stats[3] = (int64_t)bvh.pool.size();
+    }
+    if (pool_out && pool_cap_units >= (int64_t)bvh.pool.size())
+        std::memcpy(pool_out, bvh.pool.data(), sizeof(uint4) * bvh.pool.size());
+    return PT_OK;
+}
+
+PT_API uint16_t pt_debug_f16_round(double x, int32_t up) { return up ? pt::f16_round_up(x) : pt::f16_round_down(x); }
+
+}  // extern "C"

@@ -1,0 +1,147 @@
+// pt_internal.h -- private declarations of libpt_b200 (CUDA path). Not shared with oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "pt.h"
+
+namespace pt {
+
+// ---------------------------------------------------------------------------------------------
+// Wide BVH, device layout:
+//   a pool of 16-byte units. An interior node is 4 units (64 B, 64-B aligned):
+//     unit 0: float O.x, O.y, O.z (node origin = box min, fp32), uint32 base (unit index of the child block)
+//     units 1-3: 4 child boxes x 12 B: f16 lo.x, lo.y, lo.z, hi.x, hi.y, hi.z = offsets from O,
+//                lo rounded down / hi rounded up so fp32(O + lo) <= exact lo, fp32(O + hi) >= exact hi
+//                (the paper's "round-to-nearest-not-lower", made exact for the decode).
+//                The offsets are >= 0, so their sign bits carry the child meta:
+//                lo.x sign = valid, lo.y sign = leaf, {lo.z, hi.x} signs = prim count - 1.
+//   A child block holds the node's children contiguously (first child implicit at `base`, like the
+//   paper's "first child is implicitly stored next"): interior children first (4 units
+//   each), then the leaves' primitives inline, 3 units (48 B) per primitive:
+//     triangle: (v0.xyz, id) (v1.xyz, 0) (v2.xyz, 0); sphere: (c.xyz, id | SPHERE_FLAG) (r, 0, 0, 0) (0)
+// ---------------------------------------------------------------------------------------------
+constexpr uint32_t kSphereFlag = 0x80000000u;
+constexpr int kNodeUnits = 4;
+constexpr int kPrimUnits = 3;
+constexpr int kMaxLeafPrims = 4;
+constexpr int kStackSize = 64;
+
+struct DevMaterial {        // 32 B, same field order as pt_material
+    uint32_t kind;
+    float albedo[3];
+    float emission[3];
+    float ior;
+};
+
+struct HostBvh {
+    std::vector<uint4> pool;  // 16-B units
+    int64_t n_nodes = 0, n_leaves = 0, max_depth = 0;
+    bool empty = true;
+};
+
+// Builds the 4-wide compressed BVH; returns PT_OK or PT_ERR_DOMAIN with msg filled.
+int build_wide_bvh(const pt_triangle* tris, int64_t n_tris, const pt_sphere* sph, int64_t n_sph, HostBvh* out,
+                   std::string* msg);
+// f16 helpers of the conservative quantiser (exposed for tests of the host builder)
+uint16_t f16_round_down(double x);
+uint16_t f16_round_up(double x);
+double f16_value(uint16_t h);
+
+struct Workspace {
+    int64_t capacity = 0;      // path slots
+    float4* ray_o = nullptr;   // [cap] origin (w unused)
+    float4* ray_d = nullptr;   // [cap] direction (w unused)
+    float4* beta = nullptr;    // [cap] throughput (w unused)
+    uint32_t* queue[2] = {nullptr, nullptr};  // alive slot queues (ping-pong)
+    float4* hit = nullptr;     // [cap] per queue entry: (t, prim bits, 0, 0)
+    float4* esc = nullptr;     // [cap] escaped-ray queue: (u, v, slot bits, 0)
+    float4* esc_beta = nullptr;// [cap] escaped-ray throughput
+    float* wave_buf = nullptr; // [cap][3] radiance per slot, written exactly once per path
+    uint32_t* counters = nullptr;  // [kCounters]
+    int64_t fb_capacity = 0;
+    float* fb = nullptr;       // scratch framebuffer for pt_render (host-output path)
+    cudaStream_t own_stream = nullptr;
+    unsigned long long* d_stats = nullptr;  // [paths, segments, escaped, -] accumulated per call
+};
+constexpr int kCounters = 64;   // [d] = alive count produced at depth d (d = 0 raygen), [62] = escaped, [63] = error flags
+constexpr int kCounterEsc = 62;
+constexpr int kCounterErr = 63;
+
+}  // namespace pt
+
+struct pt_scene {
+    int device = 0;
+    int64_t n_tris = 0, n_sph = 0;
+    int32_t n_mats = 0;
+    pt_camera cam{};
+    uint4* d_pool = nullptr;          // wide BVH + inline primitives
+    int64_t pool_units = 0;
+    bool empty = true;
+    float4* d_tri_v = nullptr;        // [n_tris*3] vertices (shading), .w of vertex 0 = material bits
+    float4* d_sph = nullptr;          // [n_sph] (c, r)
+    uint32_t* d_sph_mat = nullptr;    // [n_sph]
+    pt::DevMaterial* d_mats = nullptr;
+    int64_t bvh_nodes = 0, bvh_leaves = 0, bvh_depth = 0;
+    std::mutex mu;                    // guards ws + stats
+    pt::Workspace ws;
+    pt_stats stats{};
+    bool profiling = false;
+};
+
+struct pt_nif {
+    int device = 0;
+    void* d_smem_image = nullptr;     // pre-laid-out shared-memory image of the fused kernel
+    int64_t smem_bytes = 0;
+    uint16_t* d_blob = nullptr;       // raw fp16 blob (reference SIMT kernel)
+};
+
+namespace pt {
+
+// camera constants in fp32 (host computes in fp64, rounds once; reading R22)
+struct Cam32 {
+    float f[3], r[3], u[3], eye[3];
+    float ta, t;
+};
+Cam32 make_cam32(const pt_camera& c, int W, int H);
+
+struct TraceParams {
+    const uint4* pool;
+    int empty;
+    const float4* tri_v;
+    const float4* sph;
+    const uint32_t* sph_mat;
+    const DevMaterial* mats;
+    int64_t n_tris;
+};
+
+// kernel launchers (trace_kernels.cu)
+void launch_raygen(const Cam32& cam, int W, int H, int first_sample, int n_slots, uint64_t seed, Workspace& ws,
+                   cudaStream_t st);
+void launch_traverse(const TraceParams& tp, const uint32_t* queue_in, const uint32_t* count_in, int identity,
+                     Workspace& ws, cudaStream_t st);
+void launch_shade(const TraceParams& tp, int W, int H, int first_sample, int depth, int max_depth, uint64_t seed,
+                  const uint32_t* queue_in, const uint32_t* count_in, int identity, uint32_t* queue_out,
+                  uint32_t* count_out, int use_nif, float3 env, Workspace& ws, cudaStream_t st);
+void launch_accumulate(const float* wave_buf, int n_pix, int k, float* fb, cudaStream_t st);
+void launch_primary(const TraceParams& tp, const Cam32& cam, int W, int H, int sample, uint64_t seed,
+                    int32_t* prim, float* t, cudaStream_t st);
+void launch_trace_rays(const TraceParams& tp, const float* o, const float* d, int64_t n, int32_t* prim, float* t,
+                       cudaStream_t st);
+void launch_scale(float* fb, int64_t n, float s, cudaStream_t st);
+void launch_pack_queries(const float* uv, int64_t n, float4* esc, float4* esc_beta, uint32_t* count,
+                         cudaStream_t st);
+
+// NIF (nif_kernel.cu)
+int64_t nif_smem_image_bytes();
+void nif_build_smem_image(const uint16_t* blob, std::vector<uint8_t>* image);
+cudaError_t launch_nif(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,
+                       int64_t max_rows, float* out, cudaStream_t st);
+int num_sms();
+
+}  // namespace pt

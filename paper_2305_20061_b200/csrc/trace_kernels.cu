@@ -1,0 +1,586 @@
+// trace_kernels.cu -- wavefront path-tracing kernels for sm_100a: raygen, traverse, shade (scatter +
+// Russian roulette + warp-aggregated compaction of alive and escaped paths), accumulate.
+//
+// Method (PAPER.md = /root/reference/PAPER.md line): no light sampling, contributions from emitters
+// hit by chance and from escaped rays; escaped rays are queued for the batched HDR-NIF
+// ("we need to run inference on large batches of ray queries"); Russian roulette from
+// depth 3 with survival proportional to throughput. Wide compressed BVH with
+// conservative fp16 child boxes. Readings R1-R22 in DESIGN.md.
+//
+// Exactness contract with the fp64 oracle: camera rays are computed with
+// explicitly rounded fp32 intrinsics (no contraction), primitive tests run in fp64 with explicitly
+// rounded intrinsics in the oracle's operation order, so primary hits are bit-identical.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include "pt_internal.h"
+
+namespace pt {
+
+// ---------------------------------------------------------------------------------------------
+// Philox-4x32-10 (Salmon et al. SC'11), counter (pixel, sample, slot, stream), key = seed (R13)
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint4 philox10(uint4 c, uint2 k) {
+#pragma unroll
+    for (int i = 0; i < 10; ++i) {
+        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+        k.x += 0x9E3779B9u;
+        k.y += 0xBB67AE85u;
+    }
+    return c;
+}
+__device__ __forceinline__ float u01f(uint32_t x) { return (float)(x >> 8) * 0x1p-24f; }  // exact
+
+// ---------------------------------------------------------------------------------------------
+// Camera (fp32, explicitly rounded, reading R22)
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ float3 cam_dir(const Cam32& k, int W, int H, int x, int y, float xi0, float xi1) {
+    const float px = __fadd_rn((float)x, xi0);
+    const float py = __fadd_rn((float)y, xi1);
+    const float sx = __fsub_rn(__fdiv_rn(__fmul_rn(2.0f, px), (float)W), 1.0f);
+    const float sy = __fsub_rn(1.0f, __fdiv_rn(__fmul_rn(2.0f, py), (float)H));
+    const float cx = __fmul_rn(sx, k.ta);
+    const float cy = __fmul_rn(sy, k.t);
+    float v[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) v[a] = __fadd_rn(__fadd_rn(k.f[a], __fmul_rn(cx, k.r[a])), __fmul_rn(cy, k.u[a]));
+    const float l2 = __fadd_rn(__fadd_rn(__fmul_rn(v[0], v[0]), __fmul_rn(v[1], v[1])), __fmul_rn(v[2], v[2]));
+    const float l = __fsqrt_rn(l2);
+    return make_float3(__fdiv_rn(v[0], l), __fdiv_rn(v[1], l), __fdiv_rn(v[2], l));
+}
+
+// ---------------------------------------------------------------------------------------------
+// fp64 primitive tests, oracle operation order (watertight: Woop/Benthin/Wald 2013)
+// ---------------------------------------------------------------------------------------------
+struct Ray64 {
+    double o[3];   // origin permuted to (kx, ky, kz)
+    double dkz;    // d[kz]
+    double Sx, Sy, Sz;
+    double d[3];   // unpermuted direction (sphere test)
+    double ou[3];  // unpermuted origin
+    int kx, ky, kz;
+};
+
+__device__ __forceinline__ double sel3(double a, double b, double c, int k) { return k == 0 ? a : (k == 1 ? b : c); }
+
+__device__ __forceinline__ void ray64_prepare(float3 o, float3 d, Ray64& r) {
+    const double dx = d.x, dy = d.y, dz = d.z;
+    int kz = 0;
+    if (fabs(dy) > fabs(dx)) kz = 1;
+    if (fabs(dz) > fabs(sel3(dx, dy, dz, kz))) kz = 2;
+    int kx = kz + 1; if (kx == 3) kx = 0;
+    int ky = kx + 1; if (ky == 3) ky = 0;
+    const double dkz = sel3(dx, dy, dz, kz);
+    if (dkz < 0.0) { int t = kx; kx = ky; ky = t; }
+    r.kx = kx; r.ky = ky; r.kz = kz;
+    r.Sx = __ddiv_rn(sel3(dx, dy, dz, kx), dkz);
+    r.Sy = __ddiv_rn(sel3(dx, dy, dz, ky), dkz);
+    r.Sz = __ddiv_rn(1.0, dkz);
+    r.dkz = dkz;
+    r.ou[0] = o.x; r.ou[1] = o.y; r.ou[2] = o.z;
+    r.d[0] = dx; r.d[1] = dy; r.d[2] = dz;
+    r.o[0] = sel3(o.x, o.y, o.z, kx);
+    r.o[1] = sel3(o.x, o.y, o.z, ky);
+    r.o[2] = sel3(o.x, o.y, o.z, kz);
+}
+
+// returns true and t if the watertight test hits with t > 0
+__device__ __forceinline__ bool tri_test64(const Ray64& r, float3 v0, float3 v1, float3 v2, double& t_out) {
+    const double A0 = __dsub_rn(sel3(v0.x, v0.y, v0.z, r.kx), r.o[0]);
+    const double A1 = __dsub_rn(sel3(v0.x, v0.y, v0.z, r.ky), r.o[1]);
+    const double A2 = __dsub_rn(sel3(v0.x, v0.y, v0.z, r.kz), r.o[2]);
+    const double B0 = __dsub_rn(sel3(v1.x, v1.y, v1.z, r.kx), r.o[0]);
+    const double B1 = __dsub_rn(sel3(v1.x, v1.y, v1.z, r.ky), r.o[1]);
+    const double B2 = __dsub_rn(sel3(v1.x, v1.y, v1.z, r.kz), r.o[2]);
+    const double C0 = __dsub_rn(sel3(v2.x, v2.y, v2.z, r.kx), r.o[0]);
+    const double C1 = __dsub_rn(sel3(v2.x, v2.y, v2.z, r.ky), r.o[1]);
+    const double C2 = __dsub_rn(sel3(v2.x, v2.y, v2.z, r.kz), r.o[2]);
+    const double Ax = __dsub_rn(A0, __dmul_rn(r.Sx, A2));
+    const double Ay = __dsub_rn(A1, __dmul_rn(r.Sy, A2));
+    const double Bx = __dsub_rn(B0, __dmul_rn(r.Sx, B2));
+    const double By = __dsub_rn(B1, __dmul_rn(r.Sy, B2));
+    const double Cx = __dsub_rn(C0, __dmul_rn(r.Sx, C2));
+    const double Cy = __dsub_rn(C1, __dmul_rn(r.Sy, C2));
+    const double U = __dsub_rn(__dmul_rn(Cx, By), __dmul_rn(Cy, Bx));
+    const double V = __dsub_rn(__dmul_rn(Ax, Cy), __dmul_rn(Ay, Cx));
+    const double Wt = __dsub_rn(__dmul_rn(Bx, Ay), __dmul_rn(By, Ax));
+    if ((U < 0.0 || V < 0.0 || Wt < 0.0) && (U > 0.0 || V > 0.0 || Wt > 0.0)) return false;
+    const double det = __dadd_rn(__dadd_rn(U, V), Wt);
+    if (det == 0.0) return false;
+    const double Az = __dmul_rn(r.Sz, A2);
+    const double Bz = __dmul_rn(r.Sz, B2);
+    const double Cz = __dmul_rn(r.Sz, C2);
+    const double T = __dadd_rn(__dadd_rn(__dmul_rn(U, Az), __dmul_rn(V, Bz)), __dmul_rn(Wt, Cz));
+    if (det < 0.0 && T >= 0.0) return false;
+    if (det > 0.0 && T <= 0.0) return false;
+    t_out = __ddiv_rn(T, det);
+    return true;
+}
+
+__device__ __forceinline__ bool sph_test64(const Ray64& r, float3 c, float rad, double& t_out) {
+    const double oc0 = __dsub_rn(r.ou[0], (double)c.x);
+    const double oc1 = __dsub_rn(r.ou[1], (double)c.y);
+    const double oc2 = __dsub_rn(r.ou[2], (double)c.z);
+    const double a = __dadd_rn(__dadd_rn(__dmul_rn(r.d[0], r.d[0]), __dmul_rn(r.d[1], r.d[1])), __dmul_rn(r.d[2], r.d[2]));
+    const double b = __dadd_rn(__dadd_rn(__dmul_rn(oc0, r.d[0]), __dmul_rn(oc1, r.d[1])), __dmul_rn(oc2, r.d[2]));
+    const double cc = __dsub_rn(__dadd_rn(__dadd_rn(__dmul_rn(oc0, oc0), __dmul_rn(oc1, oc1)), __dmul_rn(oc2, oc2)),
+                                __dmul_rn((double)rad, (double)rad));
+    const double disc = __dsub_rn(__dmul_rn(b, b), __dmul_rn(a, cc));
+    if (disc < 0.0) return false;
+    const double sq = __dsqrt_rn(disc);
+    const double t0 = __ddiv_rn(__dsub_rn(-b, sq), a);
+    const double t1 = __ddiv_rn(__dadd_rn(-b, sq), a);
+    if (t0 > 0.0) { t_out = t0; return true; }
+    if (t1 > 0.0) { t_out = t1; return true; }
+    return false;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Wide-BVH closest hit: (t, id) lexicographic minimum over all primitives (reading R11)
+// ---------------------------------------------------------------------------------------------
+struct Hit { double t; int32_t prim; };
+
+__device__ __forceinline__ float half_bits_to_float(uint32_t h) {
+    return __half2float(__ushort_as_half((unsigned short)(h & 0x7FFFu)));
+}
+
+__device__ __forceinline__ void test_leaf(const uint4* __restrict__ pool, uint32_t off, int cnt, const Ray64& r64,
+                                          Hit& best) {
+    for (int k = 0; k < cnt; ++k) {
+        const uint4 u0 = __ldg(pool + off + 3 * k);
+        const uint32_t idw = u0.w;
+        const int32_t id = (int32_t)(idw & ~kSphereFlag);
+        double t;
+        bool h;
+        if (idw & kSphereFlag) {
+            const uint4 u1 = __ldg(pool + off + 3 * k + 1);
+            h = sph_test64(r64, make_float3(__uint_as_float(u0.x), __uint_as_float(u0.y), __uint_as_float(u0.z)),
+                           __uint_as_float(u1.x), t);
+        } else {
+            const uint4 u1 = __ldg(pool + off + 3 * k + 1);
+            const uint4 u2 = __ldg(pool + off + 3 * k + 2);
+            h = tri_test64(r64, make_float3(__uint_as_float(u0.x), __uint_as_float(u0.y), __uint_as_float(u0.z)),
+                           make_float3(__uint_as_float(u1.x), __uint_as_float(u1.y), __uint_as_float(u1.z)),
+                           make_float3(__uint_as_float(u2.x), __uint_as_float(u2.y), __uint_as_float(u2.z)), t);
+        }
+        if (h && (best.prim < 0 || t < best.t || (t == best.t && id < best.prim))) {
+            best.t = t;
+            best.prim = id;
+        }
+    }
+}
+
+__device__ __forceinline__ float cull_bound(const Hit& best) {
+    // fp32 upper bound of the best t with margin for the slab rounding
+    return best.prim < 0 ? CUDART_INF_F : __fmul_ru(__double2float_ru(best.t), 1.0000005f);
+}
+
+__device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
+    Hit best{CUDART_INF, -1};
+    if (tp.empty) return best;
+    Ray64 r64;
+    ray64_prepare(o, d, r64);
+    const float inv[3] = {1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
+    const float og[3] = {o.x, o.y, o.z};
+    const bool neg[3] = {signbit(d.x) != 0, signbit(d.y) != 0, signbit(d.z) != 0};
+    constexpr float kGrow = 1.0f + 2.0f * (3.0f * 0x1p-24f) / (1.0f - 3.0f * 0x1p-24f);   // 1 + 2 gamma_3
+    uint2 stack[kStackSize];
+    int sp = 0;
+    uint32_t cur = 0;
+    const uint4* __restrict__ pool = tp.pool;
+    for (;;) {
+        const uint4 h = __ldg(pool + cur);
+        const uint4 q0 = __ldg(pool + cur + 1), q1 = __ldg(pool + cur + 2), q2 = __ldg(pool + cur + 3);
+        const uint32_t w[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
+        const float O[3] = {__uint_as_float(h.x), __uint_as_float(h.y), __uint_as_float(h.z)};
+        uint32_t off = h.w;
+        uint32_t c_off[4];
+        float c_tn[4];
+        int nc = 0;
+        float tcull = cull_bound(best);
+#pragma unroll
+        for (int ci = 0; ci < 4; ++ci) {
+            const uint32_t w0 = w[3 * ci], w1 = w[3 * ci + 1], w2 = w[3 * ci + 2];
+            if (w0 & 0x8000u) {
+                const bool leaf = (w0 & 0x80000000u) != 0;
+                const int cnt = (int)(((w1 >> 15) & 1u) | ((w1 >> 30) & 2u)) + 1;
+                const float lo[3] = {half_bits_to_float(w0), half_bits_to_float(w0 >> 16), half_bits_to_float(w1)};
+                const float hi[3] = {half_bits_to_float(w1 >> 16), half_bits_to_float(w2), half_bits_to_float(w2 >> 16)};
+                float tn = 0.0f, tf = CUDART_INF_F;
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const float bl = __fadd_rn(O[a], lo[a]);
+                    const float bh = __fadd_rn(O[a], hi[a]);
+                    const float t0 = __fmul_rn(__fsub_rn(bl, og[a]), inv[a]);
+                    const float t1 = __fmul_rn(__fsub_rn(bh, og[a]), inv[a]);
+                    tn = fmaxf(tn, neg[a] ? t1 : t0);
+                    tf = fminf(tf, neg[a] ? t0 : t1);
+                }
+                tf = tf * kGrow;
+                if (tn <= tf && tn <= tcull) {
+                    if (leaf) {
+                        test_leaf(pool, off, cnt, r64, best);
+                        tcull = cull_bound(best);
+                    } else {
+                        c_off[nc] = off;
+                        c_tn[nc] = tn;
+                        ++nc;
+                    }
+                }
+                off += leaf ? (uint32_t)(kPrimUnits * cnt) : (uint32_t)kNodeUnits;
+            }
+        }
+        // keep interior children still in front of the (possibly updated) best hit; sort by entry
+        int m = 0;
+        for (int i = 0; i < nc; ++i)
+            if (c_tn[i] <= tcull) { c_off[m] = c_off[i]; c_tn[m] = c_tn[i]; ++m; }
+        for (int i = 1; i < m; ++i)
+            for (int j = i; j > 0 && c_tn[j] < c_tn[j - 1]; --j) {
+                float tt = c_tn[j]; c_tn[j] = c_tn[j - 1]; c_tn[j - 1] = tt;
+                uint32_t oo = c_off[j]; c_off[j] = c_off[j - 1]; c_off[j - 1] = oo;
+            }
+        if (m > 0) {
+            for (int i = m - 1; i >= 1; --i) stack[sp++] = make_uint2(c_off[i], __float_as_uint(c_tn[i]));
+            cur = c_off[0];
+            continue;
+        }
+        bool found = false;
+        while (sp > 0) {
+            const uint2 e = stack[--sp];
+            if (__uint_as_float(e.y) <= tcull) { cur = e.x; found = true; break; }
+        }
+        if (!found) break;
+    }
+    return best;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Kernels
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) raygen_kernel(Cam32 cam, int W, int H, int first_sample, int n_slots, uint2 key,
+                                                     float4* __restrict__ ray_o, float4* __restrict__ ray_d,
+                                                     float4* __restrict__ beta) {
+    const int np = W * H;
+    for (int slot = blockIdx.x * blockDim.x + threadIdx.x; slot < n_slots; slot += gridDim.x * blockDim.x) {
+        const int p = slot % np;
+        const int s = first_sample + slot / np;
+        const uint4 r = philox10(make_uint4((uint32_t)p, (uint32_t)s, 0u, 0u), key);
+        const float3 d = cam_dir(cam, W, H, p % W, p / W, u01f(r.x), u01f(r.y));
+        ray_o[slot] = make_float4(cam.eye[0], cam.eye[1], cam.eye[2], 0.0f);
+        ray_d[slot] = make_float4(d.x, d.y, d.z, 0.0f);
+        beta[slot] = make_float4(1.0f, 1.0f, 1.0f, 0.0f);
+    }
+}
+
+__global__ void __launch_bounds__(128) traverse_kernel(TraceParams tp, const uint32_t* __restrict__ q_in,
+                                                       const uint32_t* __restrict__ cnt_in, int identity,
+                                                       const float4* __restrict__ ray_o,
+                                                       const float4* __restrict__ ray_d, float4* __restrict__ hit) {
+    const uint32_t n = *cnt_in;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t slot = identity ? i : __ldg(q_in + i);
+        const float4 o = __ldg(ray_o + slot), d = __ldg(ray_d + slot);
+        const Hit h = closest_hit(tp, make_float3(o.x, o.y, o.z), make_float3(d.x, d.y, d.z));
+        hit[i] = make_float4((float)h.t, __int_as_float(h.prim), 0.0f, 0.0f);
+    }
+}
+
+__device__ __forceinline__ void equirect_f32(float3 d, float& u, float& v) {
+    // SPEC.md:438 convention (reading R14): u = 0.5 + atan2(d.x, -d.z)/2pi wrapped to [0,1); v = acos(d.y)/pi
+    const float len = sqrtf(d.x * d.x + d.y * d.y + d.z * d.z);
+    float uu;
+    if (d.x == 0.0f && d.z == 0.0f) uu = 0.5f;
+    else {
+        uu = 0.5f + atan2f(d.x, -d.z) * (0.5f / CUDART_PI_F);
+        if (uu >= 1.0f) uu -= 1.0f;
+    }
+    const float y = fminf(1.0f, fmaxf(-1.0f, d.y / len));
+    u = uu;
+    v = acosf(y) * (1.0f / CUDART_PI_F);
+}
+
+// warp-aggregated append: one atomic per warp (Guideline 12), returns this lane's slot
+__device__ __forceinline__ uint32_t warp_append(bool pred, uint32_t* counter) {
+    const uint32_t mask = __ballot_sync(0xFFFFFFFFu, pred);
+    if (mask == 0) return 0;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(mask) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(counter, (uint32_t)__popc(mask));
+    base = __shfl_sync(0xFFFFFFFFu, base, leader);
+    return base + (uint32_t)__popc(mask & ((1u << lane) - 1u));
+}
+
+struct ShadeArgs {
+    TraceParams tp;
+    int W, H, first_sample, depth, max_depth;
+    uint2 key;
+    const uint32_t* q_in;
+    const uint32_t* cnt_in;
+    int identity;
+    uint32_t* q_out;
+    uint32_t* cnt_out;
+    uint32_t* cnt_esc;
+    int use_nif;
+    float3 env;
+    float4* ray_o;
+    float4* ray_d;
+    float4* beta;
+    const float4* hit;
+    float4* esc;
+    float4* esc_beta;
+    float* wave_buf;
+};
+
+__global__ void __launch_bounds__(256) shade_kernel(ShadeArgs a) {
+    const uint32_t n = *a.cnt_in;
+    const int np = a.W * a.H;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    // warp-uniform trip count so every lane reaches the ballots
+    const uint32_t n_round = (n + 31u) & ~31u;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += stride) {
+        const bool active = i < n;
+        bool alive = false, escaped = false;
+        uint32_t slot = 0;
+        float3 o3 = make_float3(0, 0, 0), wi = make_float3(0, 0, 0), bt = make_float3(0, 0, 0);
+        float eu = 0.0f, ev = 0.0f;
+        if (active) {
+            slot = a.identity ? i : __ldg(a.q_in + i);
+            const float4 hv = __ldg(a.hit + i);
+            const int32_t prim = __float_as_int(hv.y);
+            const float4 o = a.ray_o[slot], d4 = a.ray_d[slot], b4 = a.beta[slot];
+            const float3 d = make_float3(d4.x, d4.y, d4.z);
+            bt = make_float3(b4.x, b4.y, b4.z);
+            float3 L = make_float3(0, 0, 0);
+            bool done = true;
+            if (prim < 0) {                                   // escaped: environment light
+                if (a.use_nif) {
+                    equirect_f32(d, eu, ev);
+                    escaped = true;
+                    done = false;
+                } else {
+                    L = make_float3(bt.x * a.env.x, bt.y * a.env.y, bt.z * a.env.z);
+                }
+            } else {
+                const float t = hv.x;
+                const float3 P = make_float3(fmaf(t, d.x, o.x), fmaf(t, d.y, o.y), fmaf(t, d.z, o.z));
+                float3 ng;
+                uint32_t mi;
+                if (prim < a.tp.n_tris) {
+                    const float4 v0 = __ldg(a.tp.tri_v + 3 * prim), v1 = __ldg(a.tp.tri_v + 3 * prim + 1),
+                                 v2 = __ldg(a.tp.tri_v + 3 * prim + 2);
+                    const float3 e1 = make_float3(v1.x - v0.x, v1.y - v0.y, v1.z - v0.z);
+                    const float3 e2 = make_float3(v2.x - v0.x, v2.y - v0.y, v2.z - v0.z);
+                    ng = make_float3(e1.y * e2.z - e1.z * e2.y, e1.z * e2.x - e1.x * e2.z, e1.x * e2.y - e1.y * e2.x);
+                    const float il = rsqrtf(ng.x * ng.x + ng.y * ng.y + ng.z * ng.z);
+                    ng = make_float3(ng.x * il, ng.y * il, ng.z * il);
+                    mi = __float_as_uint(v0.w);
+                } else {
+                    const int si = prim - (int)a.tp.n_tris;
+                    const float4 s = __ldg(a.tp.sph + si);
+                    const float ir = 1.0f / s.w;
+                    ng = make_float3((P.x - s.x) * ir, (P.y - s.y) * ir, (P.z - s.z) * ir);
+                    mi = __ldg(a.tp.sph_mat + si);
+                }
+                const DevMaterial m = a.tp.mats[mi];
+                const float cosd = d.x * ng.x + d.y * ng.y + d.z * ng.z;
+                if (m.kind == PT_EMISSIVE) {
+                    if (cosd < 0.0f) L = make_float3(bt.x * m.emission[0], bt.y * m.emission[1], bt.z * m.emission[2]);
+                } else if (a.depth < a.max_depth) {
+                    const int p = (int)(slot % (uint32_t)np);
+                    const int s = a.first_sample + (int)(slot / (uint32_t)np);
+                    const uint4 rr = philox10(make_uint4((uint32_t)p, (uint32_t)s, (uint32_t)a.depth, 0u), a.key);
+                    const float xi0 = u01f(rr.x), xi1 = u01f(rr.y), xi2 = u01f(rr.z), xi3 = u01f(rr.w);
+                    const bool entering = cosd < 0.0f;
+                    const float3 n = entering ? ng : make_float3(-ng.x, -ng.y, -ng.z);
+                    float side = 1.0f;
+                    if (m.kind == PT_LAMBERT) {
+                        // cosine-weighted hemisphere, ONB of Duff et al. 2017 (reading R9)
+                        const float sg = copysignf(1.0f, n.z);
+                        const float aa = -1.0f / (sg + n.z);
+                        const float bb = n.x * n.y * aa;
+                        const float3 t1 = make_float3(1.0f + sg * n.x * n.x * aa, sg * bb, -sg * n.x);
+                        const float3 t2 = make_float3(bb, sg + n.y * n.y * aa, -n.y);
+                        float sphi, cphi;
+                        sincosf(2.0f * CUDART_PI_F * xi1, &sphi, &cphi);
+                        const float rho = sqrtf(xi0), c3 = sqrtf(1.0f - xi0);
+                        const float c1 = rho * cphi, c2 = rho * sphi;
+                        wi = make_float3(c1 * t1.x + c2 * t2.x + c3 * n.x, c1 * t1.y + c2 * t2.y + c3 * n.y,
+                                         c1 * t1.z + c2 * t2.z + c3 * n.z);
+                        bt = make_float3(bt.x * m.albedo[0], bt.y * m.albedo[1], bt.z * m.albedo[2]);
+                    } else if (m.kind == PT_MIRROR) {
+                        const float dn = d.x * n.x + d.y * n.y + d.z * n.z;
+                        wi = make_float3(d.x - 2.0f * dn * n.x, d.y - 2.0f * dn * n.y, d.z - 2.0f * dn * n.z);
+                        bt = make_float3(bt.x * m.albedo[0], bt.y * m.albedo[1], bt.z * m.albedo[2]);
+                    } else {
+                        // dielectric, Schlick Fresnel, TIR -> F = 1 (reading R9)
+                        const float eta = entering ? 1.0f / m.ior : m.ior;
+                        const float cosi = -(d.x * n.x + d.y * n.y + d.z * n.z);
+                        const float sin2t = eta * eta * (1.0f - cosi * cosi);
+                        float F = 1.0f, cost = 0.0f;
+                        if (sin2t <= 1.0f) {
+                            cost = sqrtf(1.0f - sin2t);
+                            const float c = entering ? cosi : cost;
+                            float r0 = (1.0f - m.ior) / (1.0f + m.ior);
+                            r0 = r0 * r0;
+                            const float mm = 1.0f - c;
+                            F = r0 + (1.0f - r0) * (mm * mm * mm * mm * mm);
+                        }
+                        if (xi2 < F) {
+                            wi = make_float3(d.x + 2.0f * cosi * n.x, d.y + 2.0f * cosi * n.y, d.z + 2.0f * cosi * n.z);
+                        } else {
+                            const float k = eta * cosi - cost;
+                            wi = make_float3(eta * d.x + k * n.x, eta * d.y + k * n.y, eta * d.z + k * n.z);
+                            side = -1.0f;
+                        }
+                    }
+                    const float il = rsqrtf(wi.x * wi.x + wi.y * wi.y + wi.z * wi.z);
+                    wi = make_float3(wi.x * il, wi.y * il, wi.z * il);
+                    // spawn with normal offset on the side wi leaves to (reading R10)
+                    const float pm = fmaxf(1.0f, fmaxf(fabsf(P.x), fmaxf(fabsf(P.y), fabsf(P.z))));
+                    const float eps = 1e-4f * pm * side;
+                    o3 = make_float3(P.x + eps * n.x, P.y + eps * n.y, P.z + eps * n.z);
+                    alive = true;
+                    done = false;
+                    // Russian roulette from depth 3, q = min(1, max beta) (reading R8)
+                    if (a.depth >= 3) {
+                        const float q = fminf(1.0f, fmaxf(bt.x, fmaxf(bt.y, bt.z)));
+                        if (xi3 >= q) {
+                            alive = false;
+                            done = true;
+                        } else {
+                            bt = make_float3(bt.x / q, bt.y / q, bt.z / q);
+                        }
+                    }
+                }
+            }
+            if (done) {
+                a.wave_buf[3 * (size_t)slot + 0] = L.x;
+                a.wave_buf[3 * (size_t)slot + 1] = L.y;
+                a.wave_buf[3 * (size_t)slot + 2] = L.z;
+            }
+        }
+        const uint32_t pos_a = warp_append(alive, a.cnt_out);
+        const uint32_t pos_e = warp_append(escaped, a.cnt_esc);
+        if (alive) {
+            a.ray_o[slot] = make_float4(o3.x, o3.y, o3.z, 0.0f);
+            a.ray_d[slot] = make_float4(wi.x, wi.y, wi.z, 0.0f);
+            a.beta[slot] = make_float4(bt.x, bt.y, bt.z, 0.0f);
+            a.q_out[pos_a] = slot;
+        }
+        if (escaped) {
+            a.esc[pos_e] = make_float4(eu, ev, __uint_as_float(slot), 0.0f);
+            a.esc_beta[pos_e] = make_float4(bt.x, bt.y, bt.z, 0.0f);
+        }
+    }
+}
+
+__global__ void accumulate_kernel(const float* __restrict__ wave_buf, int n_elems, int k, float* __restrict__ fb) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n_elems; e += gridDim.x * blockDim.x) {
+        float s = fb[e];
+        for (int j = 0; j < k; ++j) s += __ldg(wave_buf + (size_t)j * n_elems + e);   // fixed sample order
+        fb[e] = s;
+    }
+}
+
+__global__ void primary_kernel(TraceParams tp, Cam32 cam, int W, int H, int sample, uint2 key, int32_t* prim,
+                               float* tout) {
+    const int np = W * H;
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < np; p += gridDim.x * blockDim.x) {
+        const uint4 r = philox10(make_uint4((uint32_t)p, (uint32_t)sample, 0u, 0u), key);
+        const float3 d = cam_dir(cam, W, H, p % W, p / W, u01f(r.x), u01f(r.y));
+        const Hit h = closest_hit(tp, make_float3(cam.eye[0], cam.eye[1], cam.eye[2]), d);
+        prim[p] = h.prim;
+        tout[p] = (float)h.t;
+    }
+}
+
+__global__ void trace_rays_kernel(TraceParams tp, const float* o, const float* d, int64_t n, int32_t* prim, float* tout) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const Hit h = closest_hit(tp, make_float3(o[3 * i], o[3 * i + 1], o[3 * i + 2]),
+                                  make_float3(d[3 * i], d[3 * i + 1], d[3 * i + 2]));
+        prim[i] = h.prim;
+        tout[i] = (float)h.t;
+    }
+}
+
+__global__ void scale_kernel(float* fb, int64_t n, float s) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        fb[i] *= s;
+}
+
+__global__ void pack_queries_kernel(const float* uv, int64_t n, float4* esc, float4* esc_beta, uint32_t* count) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        esc[i] = make_float4(uv[2 * i], uv[2 * i + 1], __uint_as_float((uint32_t)i), 0.0f);
+        esc_beta[i] = make_float4(1.0f, 1.0f, 1.0f, 0.0f);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *count = (uint32_t)n;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Launchers: persistent-style grids sized to the SM count (Guideline 11); counts read on device.
+// ---------------------------------------------------------------------------------------------
+static int grid_for(int64_t n, int block, int per_sm) {
+    int64_t g = (n + block - 1) / block;
+    int64_t cap = (int64_t)num_sms() * per_sm;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+void launch_raygen(const Cam32& cam, int W, int H, int first_sample, int n_slots, uint64_t seed, Workspace& ws,
+                   cudaStream_t st) {
+    const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+    raygen_kernel<<<grid_for(n_slots, 256, 8), 256, 0, st>>>(cam, W, H, first_sample, n_slots, key, ws.ray_o,
+                                                             ws.ray_d, ws.beta);
+}
+
+void launch_traverse(const TraceParams& tp, const uint32_t* queue_in, const uint32_t* count_in, int identity,
+                     Workspace& ws, cudaStream_t st) {
+    traverse_kernel<<<num_sms() * 8, 128, 0, st>>>(tp, queue_in, count_in, identity, ws.ray_o, ws.ray_d, ws.hit);
+}
+
+void launch_shade(const TraceParams& tp, int W, int H, int first_sample, int depth, int max_depth, uint64_t seed,
+                  const uint32_t* queue_in, const uint32_t* count_in, int identity, uint32_t* queue_out,
+                  uint32_t* count_out, int use_nif, float3 env, Workspace& ws, cudaStream_t st) {
+    ShadeArgs a;
+    a.tp = tp;
+    a.W = W; a.H = H; a.first_sample = first_sample; a.depth = depth; a.max_depth = max_depth;
+    a.key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+    a.q_in = queue_in; a.cnt_in = count_in; a.identity = identity;
+    a.q_out = queue_out; a.cnt_out = count_out; a.cnt_esc = ws.counters + kCounterEsc;
+    a.use_nif = use_nif; a.env = env;
+    a.ray_o = ws.ray_o; a.ray_d = ws.ray_d; a.beta = ws.beta; a.hit = ws.hit;
+    a.esc = ws.esc; a.esc_beta = ws.esc_beta; a.wave_buf = ws.wave_buf;
+    shade_kernel<<<num_sms() * 8, 256, 0, st>>>(a);
+}
+
+void launch_accumulate(const float* wave_buf, int n_pix, int k, float* fb, cudaStream_t st) {
+    const int n = 3 * n_pix;
+    accumulate_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(wave_buf, n, k, fb);
+}
+
+void launch_primary(const TraceParams& tp, const Cam32& cam, int W, int H, int sample, uint64_t seed, int32_t* prim,
+                    float* t, cudaStream_t st) {
+    const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+    primary_kernel<<<grid_for((int64_t)W * H, 128, 8), 128, 0, st>>>(tp, cam, W, H, sample, key, prim, t);
+}
+
+void launch_trace_rays(const TraceParams& tp, const float* o, const float* d, int64_t n, int32_t* prim, float* t,
+                       cudaStream_t st) {
+    trace_rays_kernel<<<grid_for(n, 128, 8), 128, 0, st>>>(tp, o, d, n, prim, t);
+}
+
+void launch_scale(float* fb, int64_t n, float s, cudaStream_t st) {
+    scale_kernel<<<grid_for(n, 256, 4), 256, 0, st>>>(fb, n, s);
+}
+
+void launch_pack_queries(const float* uv, int64_t n, float4* esc, float4* esc_beta, uint32_t* count, cudaStream_t st) {
+    pack_queries_kernel<<<grid_for(n, 256, 4), 256, 0, st>>>(uv, n, esc, esc_beta, count);
+}
+
+}  // namespace pt

@@ -1,0 +1,187 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the fp64 oracle on the same seeded inputs.
+
+Gates (BASELINE.json north_star):
+  * primary-hit primitive ids bit-exact on >= 99.99 % of pixels, any remainder at <= 1e-5 barycentric
+    edges (the design makes them 100 % equal: fp32 camera rays are bit-identical, tests run in fp64);
+  * NIF: max relative error of exp(y) <= 1e-2 and |dy| <= 1e-3 in log space (SURVEY 8c caution);
+  * framebuffer relative RMSE <= 2e-3.
+"""
+import numpy as np
+import pytest
+
+from paper_2305_20061_b200 import scenes
+
+pytestmark = pytest.mark.gpu
+
+REL_RMSE_GATE = 2e-3
+NIF_REL_GATE = 1e-2
+NIF_LOG_GATE = 1e-3
+
+
+@pytest.fixture(scope="module")
+def ptm():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2305_20061_b200 import _build, pt
+    _build.build()
+    pt.lib()
+    return pt
+
+
+@pytest.fixture(scope="module")
+def blob():
+    return scenes.siren_blob(0)
+
+
+def _uv_cases(n, seed):
+    uv = scenes.query_uv(n, seed)
+    edge = np.array([[0, 0], [1, 1], [0.5, 0.5], [0, 1], [1, 0], [1e-7, 0.5], [1 - 2 ** -24, 0.25]], np.float32)
+    return np.concatenate([edge, uv])[:n] if n >= len(edge) else uv
+
+
+@pytest.mark.parametrize("n", [1, 127, 128, 129, 1000, 4 * 148 * 128 + 77])
+@pytest.mark.parametrize("scale", [1.0, 30.0])
+def test_nif_vs_oracle(ptm, orc, n, scale):
+    import torch
+    blob = scenes.siren_blob(0, out_scale=scale)
+    nif = ptm.Nif(blob)
+    uv = _uv_cases(n, seed=n)
+    got = ptm.nif_infer(nif, torch.from_numpy(uv).cuda()).cpu().numpy().astype(np.float64)
+    y = orc.nif_eval(blob, uv.astype(np.float64))
+    ref = np.exp(y)
+    assert np.isfinite(got).all()
+    # log-space gate: 1e-3 for the BASELINE network; for the x30 test network the bound of one fp16
+    # rounding of the last hidden activations, 2^-11 * max_j sum_k |W5_jk|, exceeds it
+    W5 = scenes.nif_layers_from_blob(blob)[4][0]
+    log_gate = max(NIF_LOG_GATE, 2.0 ** -11 * np.abs(W5).sum(1).max())
+    assert np.abs(np.log(got) - y).max() <= log_gate
+    assert (np.abs(got - ref) / ref).max() <= NIF_REL_GATE
+
+
+def test_nif_layer_accumulators(ptm, blob):
+    """Debug view: every layer's fp32 accumulator against an independent float64 evaluation of the
+    same fp16 activations (isolates MMA layout bugs from the sine epilogue)."""
+    import torch
+    uv = _uv_cases(512, 3)
+    nif = ptm.Nif(blob)
+    out, dbg = ptm.nif_debug_layers(nif, torch.from_numpy(uv).cuda())
+    dbg = dbg.cpu().numpy().astype(np.float64)
+    L = scenes.nif_layers_from_blob(blob)
+    x = np.stack([2 * uv[:, 0].astype(np.float64) - 1, 2 * uv[:, 1].astype(np.float64) - 1], 1)
+    pre = x @ L[0][0].T + L[0][1]
+    assert np.abs(dbg[0] - pre).max() < 1e-3 * max(1.0, np.abs(pre).max())
+    h = np.sin(dbg[0]).astype(np.float16).astype(np.float64)     # what the kernel feeds forward
+    for li in (1, 2, 3):
+        pre = h @ L[li][0].T + L[li][1]
+        assert np.abs(dbg[li] - pre).max() < 2e-3, li
+        h = np.sin(dbg[li]).astype(np.float16).astype(np.float64)
+    y = h @ L[4][0].T + L[4][1]
+    assert np.abs(dbg[4][:, :3] - y).max() < 1e-3
+
+
+def _primary_check(ptm, orc, sc, W, H, pix, seed=0, sample=0):
+    prim_g, t_g = ptm.trace_primary(ptm.Scene(sc), W, H, seed, sample)
+    prim_g = prim_g.cpu().numpy()[pix]
+    t_g = t_g.cpu().numpy()[pix]
+    prim_o, t_o, edge = orc.OracleScene(sc).primary(W, H, seed, sample, pix)
+    eq = prim_g == prim_o
+    frac = eq.mean()
+    mism = ~eq
+    assert frac >= 0.9999, f"primary-hit agreement {frac}"
+    assert (edge[mism] <= 1e-5).all(), f"mismatches off the edge band: {edge[mism]}"
+    hit = prim_o >= 0
+    assert np.array_equal(t_g[hit & eq], t_o[hit & eq].astype(np.float32))
+    return frac
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2])
+def test_primary_hits_full_frame(ptm, orc, cfg):
+    c = scenes.CONFIGS[cfg]
+    sc = scenes.scene_for_config(cfg)
+    pix = np.arange(c.n_pix, dtype=np.int64)
+    assert _primary_check(ptm, orc, sc, c.width, c.height, pix) == 1.0
+
+
+def test_primary_hits_small_bvh_sampled(ptm, orc):
+    c = scenes.CONFIGS[3]
+    sc = scenes.scene_for_config(3)
+    rows = np.arange(0, c.height, 8)
+    pix = (rows[:, None] * c.width + np.arange(c.width)[None, :]).reshape(-1).astype(np.int64)
+    assert _primary_check(ptm, orc, sc, c.width, c.height, pix, sample=3) == 1.0
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_trace_rays_random_soup_vs_brute_force(ptm, orc, seed):
+    import torch
+    sc = scenes.random_soup(2000, 64, seed)
+    rng = np.random.default_rng(seed)
+    n = 20000
+    o = rng.uniform(-2, 2, size=(n, 3)).astype(np.float32)
+    tgt = rng.uniform(-0.7, 0.7, size=(n, 3)).astype(np.float32)
+    d = (tgt - o).astype(np.float32)
+    d[:100] = np.eye(3, dtype=np.float32)[rng.integers(0, 3, 100)]       # axis-aligned rays
+    prim_g, t_g = ptm.trace_rays(ptm.Scene(sc), torch.from_numpy(o).cuda(), torch.from_numpy(d).cuda())
+    prim_o, t_o, _, _ = orc.OracleScene(sc).closest_hit(o.astype(np.float64), d.astype(np.float64), brute=True)
+    assert np.array_equal(prim_g.cpu().numpy(), prim_o)
+    hit = prim_o >= 0
+    assert np.array_equal(t_g.cpu().numpy()[hit], t_o[hit].astype(np.float32))
+
+
+def test_furnace_empty_scene_exact(ptm):
+    img = ptm.render(ptm.Scene(scenes.empty_scene()), None, 37, 23, 3, 4, seed=1, env_rgb=(0.3, 0.7, 1.9))
+    assert np.array_equal(img, np.broadcast_to(np.array([0.3, 0.7, 1.9], np.float32), img.shape))
+
+
+def test_furnace_lambert_sphere(ptm, orc):
+    rho = (0.25, 0.5, 0.75)
+    sc = scenes.single_sphere_scene(kind=scenes.LAMBERT, albedo=rho)
+    W = H = 48
+    spp = 8
+    img = ptm.render(ptm.Scene(sc), None, W, H, spp, 4, seed=7, env_rgb=(1, 1, 1)).reshape(-1, 3).astype(np.float64)
+    k = (img[:, 0] - 1) * spp / (rho[0] - 1)
+    assert np.allclose(k, np.round(k), atol=1e-4)
+    ref, _ = orc.OracleScene(sc).render(W, H, 4, 7, s0=0, s1=spp)
+    assert np.allclose(img, ref / spp, rtol=0, atol=1e-6)
+
+
+def _rel_rmse(a, b):
+    return float(np.sqrt(((a - b) ** 2).sum() / (b ** 2).sum()))
+
+
+def test_render_config0_full_vs_oracle(ptm, orc, blob):
+    c = scenes.CONFIGS[0]
+    sc = scenes.scene_for_config(0)
+    img = ptm.render(ptm.Scene(sc), ptm.Nif(blob), c.width, c.height, c.spp, c.max_depth, seed=c.seed)
+    ref, _ = orc.OracleScene(sc).render(c.width, c.height, c.max_depth, c.seed, s0=0, s1=c.spp, nif_blob=blob)
+    ref = ref.reshape(c.height, c.width, 3) / c.spp
+    assert _rel_rmse(img, ref) <= REL_RMSE_GATE
+
+
+def test_render_config1_rows_vs_oracle(ptm, orc, blob):
+    """Config 1 at full size in the bench launch configuration; oracle on every 16th row."""
+    c = scenes.CONFIGS[1]
+    sc = scenes.scene_for_config(1)
+    img = ptm.render(ptm.Scene(sc), ptm.Nif(blob), c.width, c.height, c.spp, c.max_depth, seed=c.seed)
+    rows = np.arange(0, c.height, 16)
+    pix = (rows[:, None] * c.width + np.arange(c.width)[None, :]).reshape(-1).astype(np.int64)
+    ref, _ = orc.OracleScene(sc).render(c.width, c.height, c.max_depth, c.seed, pix=pix, s0=0, s1=c.spp,
+                                        nif_blob=blob)
+    got = img.reshape(-1, 3)[pix]
+    assert _rel_rmse(got, ref / c.spp) <= REL_RMSE_GATE
+
+
+def test_render_deterministic_and_wave_invariant(ptm, blob):
+    import torch
+    c = scenes.CONFIGS[0]
+    s = ptm.Scene(scenes.scene_for_config(0))
+    nif = ptm.Nif(blob)
+    a = ptm.render(s, nif, c.width, c.height, 4, 4, seed=5)
+    b = ptm.render(s, nif, c.width, c.height, 4, 4, seed=5)
+    assert np.array_equal(a, b)
+    acc = torch.zeros(c.width * c.height * 3, device="cuda")
+    for first in range(4):            # one sample per wave, four calls
+        ptm.render_samples(s, nif, c.width, c.height, first, 1, 4, 5, acc, wave_samples=1)
+    torch.cuda.synchronize()
+    d = acc.cpu().numpy().reshape(a.shape) / 4
+    assert np.allclose(d, a, rtol=1e-6, atol=1e-7)
