@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 neural path tracer hot path (BASELINE.json metric: samples/sec and NIF
+inferences/sec; % tensor roofline for the NIF kernel).
+
+One step = one full frame of BASELINE.json configs[1] ("Box+NIF": 512x512, 16 spp per GPU, max_depth 8,
+RR from depth 3, SIREN HDR-NIF) through the whole wavefront hot path -- raygen, traverse, shade
+(scatter + RR + compaction), fused tcgen05 NIF, accumulate -- plus, for N > 1, the NCCL framebuffer
+reduce to rank 0. Inputs (scene BVH, NIF weights) are resident in HBM when the timed region starts.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1] [--impl ours|reference]
+
+Launch for N > 1: python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N.
+--impl reference times the fp64 CPU oracle (the reference arm of this tier) on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2305_20061_b200 import scenes  # noqa: E402
+
+HIDDEN_FLOP_PER_INF = 3 * 2 * 128 * 128          # tensor-counted FLOPs per NIF inference
+TOTAL_FLOP_PER_INF = 2 * (2 * 128 + 3 * 128 * 128 + 128 * 3)
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def load_peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            p = json.load(f)
+        return {"hbm_gbs": float(p["hbm_gbs"]), "bf16_tflops": float(p["bf16_tflops"]),
+                "bf16_tflops_sustained": float(p.get("bf16_tflops_sustained", p["bf16_tflops"])),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.lines: list[str] = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def oracle_sample(cfg, rows_every: int):
+    rows = np.arange(0, cfg.height, rows_every)
+    pix = (rows[:, None] * cfg.width + np.arange(cfg.width)[None, :]).reshape(-1).astype(np.int64)
+    return pix, f"rows 0::{rows_every} ({len(rows)} of {cfg.height}) x {cfg.width} px x {cfg.spp} spp"
+
+
+def run_oracle(cfg, steps: int, warmup: int, rows_every: int):
+    """Time the fp64 CPU oracle (as it stands) on a bounded sample of the workload."""
+    import oracle
+    sc = oracle.OracleScene(scenes.scene_for_config(cfg.index))
+    blob = scenes.siren_blob(0) if cfg.use_nif else None
+    pix, desc = oracle_sample(cfg, rows_every)
+    cores = os.cpu_count() or 1
+    for _ in range(warmup):
+        sc.render(cfg.width, cfg.height, cfg.max_depth, cfg.seed, pix=pix, s0=0, s1=cfg.spp, nif_blob=blob,
+                  env_rgb=cfg.env_rgb, nthreads=cores)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        sc.render(cfg.width, cfg.height, cfg.max_depth, cfg.seed, pix=pix, s0=0, s1=cfg.spp, nif_blob=blob,
+                  env_rgb=cfg.env_rgb, nthreads=cores)
+    dt = time.perf_counter() - t0
+    samples = len(pix) * cfg.spp * steps
+    return {"value": samples / dt, "unit": "samples/s", "cores": cores, "kind": "oracle",
+            "sample": desc, "seconds": dt, "cpu": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for l in open("/proc/cpuinfo"):
+            if l.startswith("model name"):
+                return l.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def workload_config(cfg, world):
+    return {"workload": f"configs[{cfg.index}] {cfg.name}: {cfg.width}x{cfg.height}, {cfg.spp} spp per GPU, "
+                        f"max_depth {cfg.max_depth}, RR>=3, {'SIREN HDR-NIF' if cfg.use_nif else 'constant env'}",
+            "width": cfg.width, "height": cfg.height, "spp_per_gpu": cfg.spp, "max_depth": cfg.max_depth,
+            "wave_samples": cfg.wave_samples, "frame_spp_total": cfg.spp * world, "seed": cfg.seed,
+            "parallelism": f"sample-partitioned x{world} + NCCL framebuffer reduce" if world > 1 else "1 GPU",
+            "l2": "L2 flushed (512 MiB memset) between timed steps, untimed; wave state 0.55 GB > L2"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--oracle-rows-every", type=int, default=8)
+    args = ap.parse_args()
+    cfg = scenes.CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        r = run_oracle(cfg, args.steps, args.warmup, rows_every=64)
+        line = {"metric": "samples/sec", "value": r["value"], "unit": "samples/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * r["seconds"] / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "impl": "reference", "config": workload_config(cfg, 1),
+                "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": r["value"], "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        line["config"]["reference_sample"] = r["sample"]
+        print(json.dumps(line))
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2305_20061_b200 import _build, pt
+    from paper_2305_20061_b200.dist import render_partitioned
+
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    if rank == 0:
+        _build.build()
+    if world > 1:
+        dist.barrier()
+    pt.lib()
+
+    W, H, spp, depth = cfg.width, cfg.height, cfg.spp, cfg.max_depth
+    env = None if cfg.use_nif else cfg.env_rgb
+    src = scenes.scene_for_config(cfg.index)
+    blob = scenes.siren_blob(0) if cfg.use_nif else None
+    S = pt.Scene(src)
+    N = pt.Nif(blob) if cfg.use_nif else None
+    accum = torch.zeros(W * H * 3, dtype=torch.float32, device="cuda")
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    n_total = spp * world                       # weak scaling: spp samples per GPU, disjoint index blocks
+    stream = torch.cuda.current_stream()
+
+    def block(f, c, acc):
+        pt.render_samples(S, N, W, H, f, c, depth, cfg.seed, acc, env_rgb=env, wave_samples=cfg.wave_samples,
+                          stream=stream)
+
+    def step():
+        accum.zero_()
+        render_partitioned(block, n_total, accum, rank, world)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, per-step CUDA events on the launching stream, L2 flush untimed ----
+    S.set_profiling(True)
+    kt = {"raygen": 0.0, "traverse": 0.0, "shade": 0.0, "nif": 0.0, "accum": 0.0}
+    escaped = segments = paths = launches = nif_launches = trav_launches = 0
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_wall0 = time.perf_counter()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            evs[k][0].record(stream)
+            step()
+            evs[k][1].record(stream)
+            st = S.stats()
+            for key in kt:
+                kt[key] += st[f"t_{key}_ms"]
+            escaped += st["escaped"]
+            segments += st["segments"]
+            paths += st["paths"]
+            launches += st["launches"]
+            nif_launches += st["nif_launches"]
+            trav_launches += st["traverse_launches"]
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_wall = time.perf_counter() - t_wall0
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    S.set_profiling(False)
+
+    samples_per_step = W * H * spp * world
+    value = samples_per_step * args.steps / (ms_max / 1e3)
+
+    # ---- end-to-end through the public API: host arrays in, host framebuffer out ----
+    e2e_steps = max(3, min(args.steps, 20))
+    host_fb = torch.empty(W * H * 3, dtype=torch.float32, pin_memory=True)
+    h2d = src.tris.nbytes + src.spheres.nbytes + src.materials.nbytes + src.camera.nbytes + (blob.nbytes if blob is not None else 0)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    te0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        S2 = pt.Scene(src)
+        N2 = pt.Nif(blob) if cfg.use_nif else None
+        acc2 = torch.zeros(W * H * 3, dtype=torch.float32, device="cuda")
+
+        def block2(f, c, acc, S2=S2, N2=N2):
+            pt.render_samples(S2, N2, W, H, f, c, depth, cfg.seed, acc, env_rgb=env, wave_samples=cfg.wave_samples)
+
+        render_partitioned(block2, n_total, acc2, rank, world)
+        if rank == 0:
+            host_fb.copy_(acc2.mul_(1.0 / n_total), non_blocking=False)
+        torch.cuda.synchronize()
+        S2.close()
+        if N2:
+            N2.close()
+    te = torch.tensor([time.perf_counter() - te0], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = samples_per_step * e2e_steps / float(te.item())
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks = load_peaks()
+    K = args.steps
+    nif_ms = kt["nif"]
+    infers = escaped
+    kernels = {
+        "traverse": {"ms_per_step": kt["traverse"] / K, "launches_per_step": trav_launches / K,
+                     "bytes_alg": (4 + 32 + 16) * segments},
+        "shade": {"ms_per_step": kt["shade"] / K, "bytes_alg": 120 * segments},
+        "nif": {"ms_per_step": nif_ms / K, "launches_per_step": nif_launches / K,
+                "flops_alg": HIDDEN_FLOP_PER_INF * infers},
+        "raygen": {"ms_per_step": kt["raygen"] / K, "bytes_alg": 48 * paths},
+        "accumulate": {"ms_per_step": kt["accum"] / K},
+    }
+    dominant = max(kernels, key=lambda n: kernels[n]["ms_per_step"])
+    nif_tflops = (HIDDEN_FLOP_PER_INF * infers) / (nif_ms / 1e3) / 1e12 if nif_ms > 0 else 0.0
+    nif_roof = {"bound": "tensor", "achieved": nif_tflops, "peak": peaks["bf16_tflops_sustained"],
+                "unit": "TFLOP/s", "frac": nif_tflops / peaks["bf16_tflops_sustained"], "traffic": None,
+                "kernel": "nif_fused_kernel", "flop_per_inference": HIDDEN_FLOP_PER_INF,
+                "inferences_per_launch": infers / max(1, nif_launches),
+                "peak_source": peaks["source"] + " bf16 sustained (fp16 same rate)"}
+    if dominant in ("traverse", "shade", "raygen"):
+        ms_k = kt[dominant if dominant != "raygen" else "raygen"]
+        byts = kernels[dominant]["bytes_alg"]
+        gbs = byts / (ms_k / 1e3) / 1e9 if ms_k > 0 else 0.0
+        roof = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": gbs / peaks["hbm_gbs"], "traffic": None, "kernel": f"{dominant}_kernel",
+                "peak_source": peaks["source"]}
+    else:
+        roof = nif_roof
+    clocks = clk.summary()
+    line = {
+        "metric": "samples/sec", "value": value, "unit": "samples/s", "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 trace / f64 prim tests / f16-in f32-acc NIF",
+        "data": "synthetic (seeded scene generator + seeded untrained SIREN weights)",
+        "config": workload_config(cfg, world),
+        "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(host_fb.numel() * 4),
+                "what": "pt_scene_create + pt_nif_load from host arrays, render, reduce, framebuffer to pinned host"},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "nif": {"inferences_per_s": infers / (nif_ms / 1e3) if nif_ms > 0 else None,
+                "inferences_per_step": infers / K, "roofline": nif_roof},
+        "kernels_ms_per_step": {k: v["ms_per_step"] for k, v in kernels.items()},
+        "paths_per_step": paths / K, "segments_per_step": segments / K,
+        "wall_s_timed_region": t_wall,
+        "clocks": clocks,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        r = run_oracle(cfg, 1, 0, rows_every=args.oracle_rows_every)
+        line["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        line["cpu_baseline"]["cpu"] = r["cpu"]
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -98,7 +98,7 @@ enum { T_RAYGEN, T_TRAVERSE, T_SHADE, T_NIF, T_ACCUM, T_N };
 struct Timer {
     bool on;
     cudaStream_t st;
-    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> rec;
+    std::vector<pt::TimedLaunch>* rec;
     void begin(int, cudaEvent_t* a) {
         if (!on) return;
         cudaEventCreate(a);
@@ -109,25 +109,26 @@ struct Timer {
         cudaEvent_t b;
         cudaEventCreate(&b);
         cudaEventRecord(b, st);
-        rec.push_back({cls, {a, b}});
-    }
-    void collect(pt_stats& s) {
-        if (!on) return;
-        cudaStreamSynchronize(st);
-        for (auto& r : rec) {
-            float ms = 0.0f;
-            cudaEventElapsedTime(&ms, r.second.first, r.second.second);
-            double* dst = r.first == T_RAYGEN ? &s.t_raygen_ms
-                        : r.first == T_TRAVERSE ? &s.t_traverse_ms
-                        : r.first == T_SHADE ? &s.t_shade_ms
-                        : r.first == T_NIF ? &s.t_nif_ms : &s.t_accum_ms;
-            *dst += ms;
-            cudaEventDestroy(r.second.first);
-            cudaEventDestroy(r.second.second);
-        }
-        rec.clear();
+        rec->push_back({cls, a, b});
     }
 };
+
+// sum the pending launch timers into stats (synchronises on the recorded events)
+void collect_timers(pt_scene* sc) {
+    for (auto& r : sc->pending) {
+        float ms = 0.0f;
+        cudaEventSynchronize(r.b);
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        double* dst = r.cls == T_RAYGEN ? &sc->stats.t_raygen_ms
+                    : r.cls == T_TRAVERSE ? &sc->stats.t_traverse_ms
+                    : r.cls == T_SHADE ? &sc->stats.t_shade_ms
+                    : r.cls == T_NIF ? &sc->stats.t_nif_ms : &sc->stats.t_accum_ms;
+        *dst += ms;
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    sc->pending.clear();
+}
 
 __global__ void stats_kernel(const uint32_t* counters, int max_depth, unsigned long long* acc) {
     unsigned long long seg = 0;
@@ -162,7 +163,8 @@ int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, i
     const pt::TraceParams tp = trace_params(sc);
     const float3 env = env_rgb ? make_float3(env_rgb[0], env_rgb[1], env_rgb[2]) : make_float3(0, 0, 0);
     const int use_nif = nif ? 1 : 0;
-    Timer tm{sc->profiling, st, {}};
+    collect_timers(sc);                  // drop timers of a previous call
+    Timer tm{sc->profiling, st, &sc->pending};
     pt_stats stats{};
     for (int64_t w0 = first_sample; w0 < (int64_t)first_sample + n_samples; w0 += k) {
         const int64_t kk = std::min<int64_t>(k, (int64_t)first_sample + n_samples - w0);
@@ -199,12 +201,11 @@ int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, i
         pt::launch_accumulate(ws.wave_buf, (int)np, (int)kk, d_accum, st);
         tm.end(T_ACCUM, e0);
         stats_kernel<<<1, 1, 0, st>>>(ws.counters, max_depth, d_stats);
-        stats.launches += 2;
+        stats.launches += 4;   // set_count, raygen, accumulate, stats
         stats.waves += 1;
     }
     CU(cudaGetLastError());
-    tm.collect(stats);   // synchronises only while profiling is on
-    sc->stats = stats;   // paths/segments/escaped are read from ws.d_stats by pt_get_stats
+    sc->stats = stats;   // kernel times and paths/segments/escaped are resolved by pt_get_stats
     return PT_OK;
 }
 
@@ -339,6 +340,7 @@ int pt_scene_destroy(pt_scene* sc) {
     if (!sc) return PT_OK;
     {
         std::lock_guard<std::mutex> lk(sc->mu);
+        collect_timers(sc);
         cudaFree(sc->d_pool); cudaFree(sc->d_tri_v); cudaFree(sc->d_sph); cudaFree(sc->d_sph_mat); cudaFree(sc->d_mats);
         free_ws(sc->ws);
     }
@@ -477,6 +479,7 @@ int pt_get_stats(const pt_scene* scene, pt_stats* out) {
     if (!scene || !out) return fail(PT_ERR_INVALID_ARG, "null argument");
     pt_scene* sc = const_cast<pt_scene*>(scene);
     std::lock_guard<std::mutex> lk(sc->mu);
+    collect_timers(sc);
     *out = sc->stats;
     if (sc->ws.d_stats) {
         unsigned long long h[4] = {0, 0, 0, 0};

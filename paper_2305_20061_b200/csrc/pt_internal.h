@@ -69,6 +69,10 @@ struct Workspace {
     cudaStream_t own_stream = nullptr;
     unsigned long long* d_stats = nullptr;  // [paths, segments, escaped, -] accumulated per call
 };
+struct TimedLaunch {
+    int cls;
+    cudaEvent_t a, b;
+};
 constexpr int kCounters = 64;   // [d] = alive count produced at depth d (d = 0 raygen), [62] = escaped, [63] = error flags
 constexpr int kCounterEsc = 62;
 constexpr int kCounterErr = 63;
@@ -92,6 +96,7 @@ struct pt_scene {
     pt::Workspace ws;
     pt_stats stats{};
     bool profiling = false;
+    std::vector<pt::TimedLaunch> pending;   // launch timers awaiting pt_get_stats
 };
 
 struct pt_nif {
