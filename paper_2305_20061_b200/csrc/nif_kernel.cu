@@ -36,22 +36,24 @@ constexpr int kB5Bytes = 16 * 144 * 2;        // layer 5: N=16 (3 used), K=144
 constexpr int kOffB1 = 0;
 constexpr int kOffB2 = kOffB1 + kB1Bytes;
 constexpr int kOffB5 = kOffB2 + 3 * kBHBytes;
-constexpr int kImageBytes = kOffB5 + kB5Bytes;   // 119,296
-constexpr int kBarBytes = 64;
+constexpr int kOffOnes = kOffB5 + kB5Bytes;      // A operand of the bias K step: [128][16], row = (1, 0, ...)
+constexpr int kOnesBytes = 128 * 16 * 2;
+constexpr int kImageBytes = kOffOnes + kOnesBytes;   // 123,392
+constexpr int kBarBytes = 80;
 constexpr int kSmemBytes = kImageBytes + kBarBytes + 128;
 
-constexpr int kSplit = 2;                          // epilogue warps per TMEM lane quarter per slot
-constexpr int kEpiWarpsPerSlot = 4 * kSplit;       // 8
-constexpr int kNumEpiWarps = 2 * kEpiWarpsPerSlot; // 16
+constexpr int kNumEpiWarps = 16;                   // 4 per TMEM lane quarter, 32 columns each
+constexpr int kEpiArrivals = kNumEpiWarps;         // arrivals per a_ready phase
 constexpr int kFirstEpiWarp = 4;
 constexpr int kThreads = 32 * (kFirstEpiWarp + kNumEpiWarps);   // 640
-constexpr int kColsPerWarp = kHid / kSplit;        // 64
 
-// TMEM columns (512 allocated): slot s: D at 256 s (128 cols), A at 256 s + 128 (64 cols of h, then
-// the 8-column constant-1 bias chunk at +64). The layer-1 input (K=16) reuses the first 8 A columns.
+// TMEM columns (512 allocated): slot s: D at 256 s (128 fp32 columns), then two 64-column fp16 A
+// buffers (layer l reads buffer l % 2 while its epilogue writes buffer (l+1) % 2, so no epilogue write
+// can race an MMA still reading A). The layer-1 input (K=16) is the first 8 columns of buffer 0.
+// The bias K step reads its A operand (a constant-1 column) from shared memory instead of TMEM.
 constexpr uint32_t kTmemCols = 512;
 __host__ __device__ constexpr uint32_t d_col(int s) { return 256u * s; }
-__host__ __device__ constexpr uint32_t a_col(int s) { return 256u * s + 128u; }
+__host__ __device__ constexpr uint32_t a_col(int s, int buf) { return 256u * s + 128u + 64u * buf; }
 
 // instruction descriptor: D f32, A/B f16, K-major both, M=128, N given
 __host__ __device__ constexpr uint32_t idesc(int n) {
@@ -103,6 +105,8 @@ void nif_build_smem_image(const uint16_t* blob, std::vector<uint8_t>* image) {
         for (int k = 0; k < 128; ++k) put_core(img, kOffB5, 16, n, k, W5[n * 128 + k]);
         put_core(img, kOffB5, 16, n, 128, b5[n]);
     }
+    // constant-1 A tile of the bias step (M = 128 rows, K = 16)
+    for (int m = 0; m < 128; ++m) put_core(img, kOffOnes, 128, m, 0, 0x3C00);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -139,6 +143,16 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
     }
 }
 
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -158,6 +172,14 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
         ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(id), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void mma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t id, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(id), "r"(acc)
         : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
@@ -199,9 +221,71 @@ __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
     return *reinterpret_cast<const uint32_t*>(&h);
 }
 
+// wait for all prior tcgen05.ld of this thread; the register operands pin later uses of v after it
+__device__ __forceinline__ void tmem_wait_ld_dep(uint32_t* v) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                   "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]),
+                   "+r"(v[15]), "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]),
+                   "+r"(v[22]), "+r"(v[23]), "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]),
+                   "+r"(v[29]), "+r"(v[30]), "+r"(v[31])
+                 :
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_wait_ld_dep4(uint32_t* v) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]) : : "memory");
+}
+
+// Sine epilogue, split between two pipes: the SFU (MUFU.SIN, 16 lanes/clk/SM) and
+// the FMA pipe, where sin runs as an fp16x2 odd polynomial after an fp32 quarter-period reduction
+// w = |frac(x/2pi + 1/4)| - 1/4, sin(x) = sin(2 pi w), |w| <= 1/4 (max abs error 1.1e-3 in fp16).
+#ifndef PT_NIF_MUFU_PAIRS
+#define PT_NIF_MUFU_PAIRS 9   // of the 16 column pairs of a 32-column chunk, on the SFU
+#endif
+__device__ __forceinline__ uint32_t sin2_poly(float a, float b) {
+    // packed fp32x2 range reduction (FFMA2/FADD2, sm_100), then an fp16x2 odd polynomial
+    constexpr float kInv2Pi = 0.15915494309189535f;
+    constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23: x + magic - magic = rint(x)
+    const float2 sv = __ffma2_rn(make_float2(a, b), make_float2(kInv2Pi, kInv2Pi), make_float2(0.25f, 0.25f));
+    const float2 tv = __fadd2_rn(sv, make_float2(kMagic, kMagic));
+    const float2 kv = __fadd2_rn(tv, make_float2(-kMagic, -kMagic));
+    const float2 uv = __fadd2_rn(sv, make_float2(-kv.x, -kv.y));
+    const float2 wv = __fadd2_rn(make_float2(fabsf(uv.x), fabsf(uv.y)), make_float2(-0.25f, -0.25f));
+    const __half2 w = __floats2half2_rn(wv.x, wv.y);
+    const __half2 w2 = __hmul2(w, w);
+    const __half2 c1 = __halves2half2(__ushort_as_half(0x4648), __ushort_as_half(0x4648));   //  6.28125
+    const __half2 c3 = __halves2half2(__ushort_as_half(0xD123), __ushort_as_half(0xD123));   // -41.09375
+    const __half2 c5 = __halves2half2(__ushort_as_half(0x5499), __ushort_as_half(0x5499));   //  73.5625
+    __half2 p = __hfma2(w2, c5, c3);
+    p = __hfma2(p, w2, c1);
+    const __half2 r = __hmul2(p, w);
+    return *reinterpret_cast<const uint32_t*>(&r);
+}
+__device__ __forceinline__ void sine_chunk(const uint32_t* v, uint32_t* p) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const float a = __uint_as_float(v[2 * j]), b = __uint_as_float(v[2 * j + 1]);
+        p[j] = j < PT_NIF_MUFU_PAIRS ? pack_half2(__sinf(a), __sinf(b)) : sin2_poly(a, b);
+    }
+}
+
 // ---------------------------------------------------------------------------------------------
 // The fused kernel
 // ---------------------------------------------------------------------------------------------
+#ifdef PT_NIF_TRACE
+// timing trace of CTA 0 (variant builds only): [role][record][2] clock64 stamps
+__device__ unsigned long long g_nif_trace[3 * 4096 * 2];
+#define NIF_TRACE(role, rec, k)                                                                  \
+    do {                                                                                         \
+        if (blockIdx.x == 0 && (rec) < 4096) g_nif_trace[((role) * 4096 + (rec)) * 2 + (k)] = clock64(); \
+    } while (0)
+#else
+#define NIF_TRACE(role, rec, k) \
+    do {                        \
+    } while (0)
+#endif
+
 template <bool kDebug>
 __global__ void __launch_bounds__(nif::kThreads, 1)
     nif_fused_kernel(const uint8_t* __restrict__ g_image, const float4* __restrict__ esc,
@@ -210,8 +294,9 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
     using namespace nif;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* image = smem;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kImageBytes);   // [0] weights, [1,2] a_ready, [3,4] d_full
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kImageBytes + 48);
+    // [0] weights, [1..4] a_ready[slot][column half], [5..8] d_full[slot][column half]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kImageBytes);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kImageBytes + 72);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -221,10 +306,8 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
 
     if (warp == 1 && lane == 0) {
         mbar_init(bar_w, 1);
-        mbar_init(smem_u32(&bars[1]), kEpiWarpsPerSlot);
-        mbar_init(smem_u32(&bars[2]), kEpiWarpsPerSlot);
-        mbar_init(smem_u32(&bars[3]), 1);
-        mbar_init(smem_u32(&bars[4]), 1);
+        for (int b = 1; b < 5; ++b) mbar_init(smem_u32(&bars[b]), kEpiArrivals / 2);
+        for (int b = 5; b < 9; ++b) mbar_init(smem_u32(&bars[b]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
@@ -252,10 +335,14 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
     }
 
     if (warp == 0) {
-        if (lane == 0 && blockIdx.x < n_tiles) {
-            // ===== MMA issuer (single thread) =====
+        if (blockIdx.x < n_tiles) {
+            // ===== MMA issuer: warp 0 walks the schedule, one elected lane issues =====
+            // Layer l reads A buffer l % 2. Each layer runs as two N=64 column halves with their own
+            // commit barrier; the low half's K steps 0-3 (A columns 0-31, written by the low-half
+            // epilogue warps) start before the high half of A is ready.
             mbar_wait(bar_w, 0);
             const uint32_t img = smem_u32(image);
+            const uint64_t ones = smem_desc(img + kOffOnes, 2048, 128);
             uint32_t a_phase[2] = {0, 0};
             for (uint32_t i = 0;; i += 2) {
                 const uint32_t t0 = blockIdx.x + i * gridDim.x;
@@ -263,115 +350,178 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
                 const int nslots = (t0 + gridDim.x < n_tiles) ? 2 : 1;
                 for (int layer = 0; layer < 5; ++layer) {
                     for (int s = 0; s < nslots; ++s) {
-                        mbar_wait(smem_u32(&bars[1 + s]), a_phase[s]);
-                        a_phase[s] ^= 1;
-                        tc_fence_after();
+                        const uint32_t bar_alo = smem_u32(&bars[1 + 2 * s]), bar_ahi = smem_u32(&bars[2 + 2 * s]);
+                        const uint32_t bar_lo = smem_u32(&bars[5 + 2 * s]), bar_hi = smem_u32(&bars[6 + 2 * s]);
                         const uint32_t dt = tmem + d_col(s);
-                        const uint32_t at = tmem + a_col(s);
+                        const uint32_t at = tmem + a_col(s, layer & 1);
+                        mbar_wait(bar_alo, a_phase[s]);
+                        if (lane == 0) NIF_TRACE(0, ((i / 2) * 5 + layer) * 2 + s, 0);
+                        tc_fence_after();
                         if (layer == 0) {
-                            mma_ts(dt, at, smem_desc(img + kOffB1, 128 * 16, 128), idesc(128), 0);
-                        } else if (layer < 4) {
-                            const uint32_t base = img + kOffB2 + (layer - 1) * kBHBytes;
-#pragma unroll
-                            for (int k = 0; k < 9; ++k)
-                                mma_ts(dt, at + 8 * k, smem_desc(base + k * 2 * 2048, 2048, 128), idesc(128), k > 0);
+                            mbar_wait(bar_ahi, a_phase[s]);
+                            tc_fence_after();
+                            if (elect_one()) {
+                                mma_ts(dt, at, smem_desc(img + kOffB1, 2048, 128), idesc(64), 0);
+                                mma_commit(bar_lo);
+                                mma_ts(dt + 64, at, smem_desc(img + kOffB1 + 1024, 2048, 128), idesc(64), 0);
+                                mma_commit(bar_hi);
+                            }
                         } else {
-                            const uint32_t base = img + kOffB5;
+                            const bool out_layer = layer == 4;
+                            const uint32_t base = out_layer ? img + kOffB5 : img + kOffB2 + (layer - 1) * kBHBytes;
+                            const uint32_t lbo = out_layer ? 256 : 2048;       // K-direction core-matrix stride
+                            const uint32_t id = idesc(out_layer ? 16 : 64);
+                            if (elect_one()) {
 #pragma unroll
-                            for (int k = 0; k < 9; ++k)
-                                mma_ts(dt, at + 8 * k, smem_desc(base + k * 2 * 256, 256, 128), idesc(16), k > 0);
+                                for (int k = 0; k < 4; ++k)
+                                    mma_ts(dt, at + 8 * k, smem_desc(base + k * 2 * lbo, lbo, 128), id, k > 0);
+                            }
+                            __syncwarp();
+                            mbar_wait(bar_ahi, a_phase[s]);
+                            tc_fence_after();
+                            if (elect_one()) {
+#pragma unroll
+                                for (int k = 4; k < 8; ++k)
+                                    mma_ts(dt, at + 8 * k, smem_desc(base + k * 2 * lbo, lbo, 128), id, 1);
+                                mma_ss(dt, ones, smem_desc(base + 16 * lbo, lbo, 128), id, 1);   // + bias
+                                if (out_layer) {
+                                    mma_commit(bar_lo);
+                                    mma_commit(bar_hi);
+                                } else {
+                                    mma_commit(bar_lo);
+#pragma unroll
+                                    for (int k = 0; k < 8; ++k)
+                                        mma_ts(dt + 64, at + 8 * k, smem_desc(base + 1024 + k * 2 * lbo, lbo, 128), id,
+                                               k > 0);
+                                    mma_ss(dt + 64, ones, smem_desc(base + 1024 + 16 * lbo, lbo, 128), id, 1);
+                                    mma_commit(bar_hi);
+                                }
+                            }
                         }
-                        mma_commit(smem_u32(&bars[3 + s]));
+                        a_phase[s] ^= 1;
+                        __syncwarp();
+                        if (lane == 0) NIF_TRACE(0, ((i / 2) * 5 + layer) * 2 + s, 1);
                     }
                 }
             }
         }
     } else if (warp >= kFirstEpiWarp) {
         // ===== epilogue warps =====
+        // All 16 epilogue warps work on one (slot, layer) at a time, in the MMA's issue order, so the
+        // tensor core runs the other slot's layer while the sines of this one are computed. Warp w
+        // owns TMEM lane quarter w % 4 (hardware rule) and the 32-column block cb of the 128 columns.
         const int e = warp - kFirstEpiWarp;
-        const int s = e / kEpiWarpsPerSlot;
-        const int h = (e / 4) % kSplit;
-        const int q = warp & 3;                       // TMEM lane quarter (hardware: warp id % 4)
+        const int cb = e >> 2;                        // column block 0..3
+        const int q = warp & 3;                       // TMEM lane quarter
         const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
-        const uint32_t dt = tmem + d_col(s) + lane_addr;
-        const uint32_t at = tmem + a_col(s) + lane_addr;
-        const uint32_t bar_a = smem_u32(&bars[1 + s]);
-        const uint32_t bar_d = smem_u32(&bars[3 + s]);
-        uint32_t d_phase = 0;
-        // constant-1 bias chunk (A columns 64..71): row = (1.0h, 0 ...)
-        if (h == 0) {
-            uint32_t v[8] = {0x00003C00u, 0, 0, 0, 0, 0, 0, 0};
-            tmem_st8(at + 64, v);
+        uint32_t d_phase[2] = {0, 0};
+        // the per-row work (layer-1 input, output) is done by the cb == 0 warps
+        float4 ent[2] = {make_float4(0.5f, 0.5f, 0.0f, 0.0f), make_float4(0.5f, 0.5f, 0.0f, 0.0f)};
+        auto row_of = [&](uint32_t tile) { return tile * kTileM + 32 * q + lane; };
+        auto write_a0 = [&](int s, float4 en) {
+            // layer-1 A tile: (x_hi, y_hi, x_lo, y_lo, 1, 0 ...), x0 = (2u-1, 2v-1) (reading R15)
+            const float x = 2.0f * en.x - 1.0f, y = 2.0f * en.y - 1.0f;
+            const __half xh = __float2half_rn(x), yh = __float2half_rn(y);
+            const __half xl = __float2half_rn(x - __half2float(xh)), yl = __float2half_rn(y - __half2float(yh));
+            uint32_t v[8];
+            v[0] = (uint32_t)__half_as_ushort(xh) | ((uint32_t)__half_as_ushort(yh) << 16);
+            v[1] = (uint32_t)__half_as_ushort(xl) | ((uint32_t)__half_as_ushort(yl) << 16);
+            v[2] = 0x00003C00u;
+            v[3] = v[4] = v[5] = v[6] = v[7] = 0;
+            tmem_st8(tmem + a_col(s, 0) + lane_addr, v);
+        };
+        auto load_ent = [&](uint32_t tile) {
+            const uint32_t row = row_of(tile);
+            return (tile < n_tiles && row < n_rows) ? __ldg(esc + row) : make_float4(0.5f, 0.5f, 0.0f, 0.0f);
+        };
+        // prologue: constant-1 bias chunks and the layer-1 inputs of the first tile pair
+        for (int s = 0; s < 2; ++s) {
+            const uint32_t tile = blockIdx.x + s * gridDim.x;
+            if (cb == 0) {
+                ent[s] = load_ent(tile);
+                if (tile < n_tiles) write_a0(s, ent[s]);
+            }
         }
-        for (uint32_t i = s;; i += 2) {
-            const uint32_t tile = blockIdx.x + i * gridDim.x;
-            if (tile >= n_tiles) break;
-            const uint32_t row = tile * kTileM + 32 * q + lane;
-            const bool valid = row < n_rows;
-            float4 ent = make_float4(0.5f, 0.5f, 0.0f, 0.0f);
-            if (valid) ent = __ldg(esc + row);
-            if (h == 0) {
-                // layer-1 A tile: (x_hi, y_hi, x_lo, y_lo, 1, 0 ...), x0 = (2u-1, 2v-1) (reading R15)
-                const float x = 2.0f * ent.x - 1.0f, y = 2.0f * ent.y - 1.0f;
-                const __half xh = __float2half_rn(x), yh = __float2half_rn(y);
-                const __half xl = __float2half_rn(x - __half2float(xh)), yl = __float2half_rn(y - __half2float(yh));
-                uint32_t v[8];
-                v[0] = (uint32_t)__half_as_ushort(xh) | ((uint32_t)__half_as_ushort(yh) << 16);
-                v[1] = (uint32_t)__half_as_ushort(xl) | ((uint32_t)__half_as_ushort(yl) << 16);
-                v[2] = 0x00003C00u;
-                v[3] = v[4] = v[5] = v[6] = v[7] = 0;
-                tmem_st8(at, v);
-                tmem_wait_st();
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar_a);
-            // hidden layers: D (fp32) -> sin -> fp16 -> A
-            for (int layer = 0; layer < 4; ++layer) {
-                mbar_wait(bar_d, d_phase);
-                d_phase ^= 1;
-                tc_fence_after();
-#pragma unroll
-                for (int c = 0; c < kColsPerWarp / 32; ++c) {
-                    const int col = h * kColsPerWarp + 32 * c;
-                    uint32_t v[32];
-                    TMEM_LD32(dt + col, v);
-                    tmem_wait_ld();
-                    if (kDebug && valid) {
-                        for (int j = 0; j < 32; ++j)
-                            dbg[((size_t)layer * n_rows + row) * kHid + col + j] = __uint_as_float(v[j]);
-                    }
-                    uint32_t p[16];
-#pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        p[j] = pack_half2(__sinf(__uint_as_float(v[2 * j])), __sinf(__uint_as_float(v[2 * j + 1])));
-                    TMEM_ST16(at + col / 2, p);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+            if (blockIdx.x < n_tiles) mbar_arrive(smem_u32(&bars[1 + (cb >> 1)]));
+            if (blockIdx.x + gridDim.x < n_tiles) mbar_arrive(smem_u32(&bars[3 + (cb >> 1)]));
+        }
+        for (uint32_t i = 0;; i += 2) {
+            const uint32_t t0 = blockIdx.x + i * gridDim.x;
+            if (t0 >= n_tiles) break;
+            const int nslots = (t0 + gridDim.x < n_tiles) ? 2 : 1;
+            // prefetch: this pair's throughputs and the next pair's queue entries (cb == 0 warps)
+            float4 beta[2] = {make_float4(0, 0, 0, 0), make_float4(0, 0, 0, 0)};
+            float4 ent_next[2] = {ent[0], ent[1]};
+            if (cb == 0) {
+                for (int s = 0; s < nslots; ++s) {
+                    const uint32_t tile = t0 + s * gridDim.x;
+                    const uint32_t row = row_of(tile);
+                    if (row < n_rows) beta[s] = __ldg(esc_beta + row);
+                    ent_next[s] = load_ent(tile + 2 * gridDim.x);
                 }
-                tmem_wait_st();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(bar_a);
             }
-            // output layer: y = D[:, 0:3]; radiance = beta * exp(y)
-            mbar_wait(bar_d, d_phase);
-            d_phase ^= 1;
-            tc_fence_after();
-            if (h == 0) {
-                uint32_t v[4];
-                tmem_ld4(dt, v);
-                tmem_wait_ld();
-                if (valid) {
-                    const float4 b = __ldg(esc_beta + row);
-                    const uint32_t slot = __float_as_uint(ent.z);
-                    const float y0 = __uint_as_float(v[0]), y1 = __uint_as_float(v[1]), y2 = __uint_as_float(v[2]);
-                    if (kDebug) {
-                        dbg[((size_t)4 * n_rows + row) * kHid + 0] = y0;
-                        dbg[((size_t)4 * n_rows + row) * kHid + 1] = y1;
-                        dbg[((size_t)4 * n_rows + row) * kHid + 2] = y2;
+            for (int layer = 0; layer < 5; ++layer) {
+                for (int s = 0; s < nslots; ++s) {
+                    const uint32_t tile = t0 + s * gridDim.x;
+                    const uint32_t row = row_of(tile);
+                    const bool valid = row < n_rows;
+                    const uint32_t dt = tmem + d_col(s) + lane_addr;
+                    const uint32_t at = tmem + a_col(s, (layer + 1) & 1) + lane_addr;   // next layer's A
+                    const uint32_t dph = d_phase[s];
+                    d_phase[s] ^= 1;
+                    mbar_wait(smem_u32(&bars[5 + 2 * s + (cb >> 1)]), dph);
+                    const int trole = (warp == kFirstEpiWarp) ? 1 : (warp == kFirstEpiWarp + kNumEpiWarps - 1 ? 2 : -1);
+                    if (trole > 0 && lane == 0) NIF_TRACE(trole, ((i / 2) * 5 + layer) * 2 + s, 0);
+                    tc_fence_after();
+                    bool arrive = true;
+                    if (layer < 4) {
+                        // hidden layer: D (fp32) -> sin -> fp16 -> A (this warp's 32 columns)
+                        const int col = 32 * cb;
+                        uint32_t v[32];
+                        TMEM_LD32(dt + col, v);
+                        tmem_wait_ld_dep(v);
+                        if (kDebug && valid) {
+                            for (int j = 0; j < 32; ++j)
+                                dbg[((size_t)layer * n_rows + row) * kHid + col + j] = __uint_as_float(v[j]);
+                        }
+                        uint32_t p[16];
+                        sine_chunk(v, p);
+                        TMEM_ST16(at + col / 2, p);
+                    } else {
+                        // output layer: y = D[:, 0:3]; radiance = beta * exp(y); then the layer-1
+                        // input of this slot's next tile (if any) into the A region
+                        const uint32_t next = tile + 2 * gridDim.x;
+                        if (cb == 0) {
+                            uint32_t v[4];
+                            tmem_ld4(dt, v);
+                            tmem_wait_ld_dep4(v);
+                            if (valid) {
+                                const uint32_t slot = __float_as_uint(ent[s].z);
+                                const float y0 = __uint_as_float(v[0]), y1 = __uint_as_float(v[1]),
+                                            y2 = __uint_as_float(v[2]);
+                                if (kDebug) {
+                                    dbg[((size_t)4 * n_rows + row) * kHid + 0] = y0;
+                                    dbg[((size_t)4 * n_rows + row) * kHid + 1] = y1;
+                                    dbg[((size_t)4 * n_rows + row) * kHid + 2] = y2;
+                                }
+                                out[3 * (size_t)slot + 0] = beta[s].x * __expf(y0);
+                                out[3 * (size_t)slot + 1] = beta[s].y * __expf(y1);
+                                out[3 * (size_t)slot + 2] = beta[s].z * __expf(y2);
+                            }
+                            ent[s] = ent_next[s];
+                            if (next < n_tiles) write_a0(s, ent[s]);
+                        }
+                        arrive = next < n_tiles;
                     }
-                    out[3 * (size_t)slot + 0] = b.x * __expf(y0);
-                    out[3 * (size_t)slot + 1] = b.y * __expf(y1);
-                    out[3 * (size_t)slot + 2] = b.z * __expf(y2);
+                    tmem_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (trole > 0 && lane == 0) NIF_TRACE(trole, ((i / 2) * 5 + layer) * 2 + s, 1);
+                    if (lane == 0 && arrive) mbar_arrive(smem_u32(&bars[1 + 2 * s + (cb >> 1)]));
                 }
             }
         }
@@ -431,3 +581,9 @@ cudaError_t launch_nif_debug(const pt_nif* nif, const float4* esc, const float4*
 }
 
 }  // namespace pt
+
+#ifdef PT_NIF_TRACE
+extern "C" __attribute__((visibility("default"))) int pt_debug_nif_trace(unsigned long long* host_out) {
+    return (int)cudaMemcpyFromSymbol(host_out, pt::g_nif_trace, sizeof(pt::g_nif_trace));
+}
+#endif

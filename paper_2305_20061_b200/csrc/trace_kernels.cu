@@ -54,66 +54,94 @@ __device__ __forceinline__ float3 cam_dir(const Cam32& k, int W, int H, int x, i
 }
 
 // ---------------------------------------------------------------------------------------------
-// fp64 primitive tests, oracle operation order (watertight: Woop/Benthin/Wald 2013)
+// Primitive tests. Decisions are exactly those of the fp64 oracle (watertight: Woop/Benthin/Wald
+// 2013): a conservative fp32 pre-test rejects only triangles whose edge functions have
+// mixed signs by more than a proven fp32 error bound; every remaining candidate is decided in fp64
+// with explicitly rounded intrinsics in the oracle's operation order (R22).
 // ---------------------------------------------------------------------------------------------
-struct Ray64 {
-    double o[3];   // origin permuted to (kx, ky, kz)
-    double dkz;    // d[kz]
-    double Sx, Sy, Sz;
-    double d[3];   // unpermuted direction (sphere test)
-    double ou[3];  // unpermuted origin
+struct RayT {
+    float o[3], d[3], inv[3];   // slab test, sphere test
+    float ok[3];          // origin permuted to (kx, ky, kz)
+    float Sx, Sy, Sz;     // fp32 shear (pre-test only)
+    double Sx64, Sy64, Sz64;
     int kx, ky, kz;
+    unsigned negmask;     // bit a: d[a] has its sign bit set
 };
 
-__device__ __forceinline__ double sel3(double a, double b, double c, int k) { return k == 0 ? a : (k == 1 ? b : c); }
+__device__ __forceinline__ float self3(float3 v, int k) { return k == 0 ? v.x : (k == 1 ? v.y : v.z); }
 
-__device__ __forceinline__ void ray64_prepare(float3 o, float3 d, Ray64& r) {
-    const double dx = d.x, dy = d.y, dz = d.z;
+__device__ __forceinline__ void ray_prepare(float3 o, float3 d, RayT& r) {
     int kz = 0;
-    if (fabs(dy) > fabs(dx)) kz = 1;
-    if (fabs(dz) > fabs(sel3(dx, dy, dz, kz))) kz = 2;
+    if (fabsf(d.y) > fabsf(d.x)) kz = 1;
+    if (fabsf(d.z) > fabsf(self3(d, kz))) kz = 2;
     int kx = kz + 1; if (kx == 3) kx = 0;
     int ky = kx + 1; if (ky == 3) ky = 0;
-    const double dkz = sel3(dx, dy, dz, kz);
-    if (dkz < 0.0) { int t = kx; kx = ky; ky = t; }
+    const float dkz = self3(d, kz);
+    if (dkz < 0.0f) { int t = kx; kx = ky; ky = t; }
     r.kx = kx; r.ky = ky; r.kz = kz;
-    r.Sx = __ddiv_rn(sel3(dx, dy, dz, kx), dkz);
-    r.Sy = __ddiv_rn(sel3(dx, dy, dz, ky), dkz);
-    r.Sz = __ddiv_rn(1.0, dkz);
-    r.dkz = dkz;
-    r.ou[0] = o.x; r.ou[1] = o.y; r.ou[2] = o.z;
-    r.d[0] = dx; r.d[1] = dy; r.d[2] = dz;
-    r.o[0] = sel3(o.x, o.y, o.z, kx);
-    r.o[1] = sel3(o.x, o.y, o.z, ky);
-    r.o[2] = sel3(o.x, o.y, o.z, kz);
+    const double dkz64 = (double)dkz;
+    r.Sx64 = __ddiv_rn((double)self3(d, kx), dkz64);
+    r.Sy64 = __ddiv_rn((double)self3(d, ky), dkz64);
+    r.Sz64 = __ddiv_rn(1.0, dkz64);
+    r.Sx = self3(d, kx) / dkz;
+    r.Sy = self3(d, ky) / dkz;
+    r.Sz = 1.0f / dkz;
+    r.o[0] = o.x; r.o[1] = o.y; r.o[2] = o.z;
+    r.d[0] = d.x; r.d[1] = d.y; r.d[2] = d.z;
+    r.ok[0] = self3(o, kx); r.ok[1] = self3(o, ky); r.ok[2] = self3(o, kz);
+    r.inv[0] = 1.0f / d.x; r.inv[1] = 1.0f / d.y; r.inv[2] = 1.0f / d.z;
+    r.negmask = (signbit(d.x) ? 1u : 0u) | (signbit(d.y) ? 2u : 0u) | (signbit(d.z) ? 4u : 0u);
 }
 
-// returns true and t if the watertight test hits with t > 0
-__device__ __forceinline__ bool tri_test64(const Ray64& r, float3 v0, float3 v1, float3 v2, double& t_out) {
-    const double A0 = __dsub_rn(sel3(v0.x, v0.y, v0.z, r.kx), r.o[0]);
-    const double A1 = __dsub_rn(sel3(v0.x, v0.y, v0.z, r.ky), r.o[1]);
-    const double A2 = __dsub_rn(sel3(v0.x, v0.y, v0.z, r.kz), r.o[2]);
-    const double B0 = __dsub_rn(sel3(v1.x, v1.y, v1.z, r.kx), r.o[0]);
-    const double B1 = __dsub_rn(sel3(v1.x, v1.y, v1.z, r.ky), r.o[1]);
-    const double B2 = __dsub_rn(sel3(v1.x, v1.y, v1.z, r.kz), r.o[2]);
-    const double C0 = __dsub_rn(sel3(v2.x, v2.y, v2.z, r.kx), r.o[0]);
-    const double C1 = __dsub_rn(sel3(v2.x, v2.y, v2.z, r.ky), r.o[1]);
-    const double C2 = __dsub_rn(sel3(v2.x, v2.y, v2.z, r.kz), r.o[2]);
-    const double Ax = __dsub_rn(A0, __dmul_rn(r.Sx, A2));
-    const double Ay = __dsub_rn(A1, __dmul_rn(r.Sy, A2));
-    const double Bx = __dsub_rn(B0, __dmul_rn(r.Sx, B2));
-    const double By = __dsub_rn(B1, __dmul_rn(r.Sy, B2));
-    const double Cx = __dsub_rn(C0, __dmul_rn(r.Sx, C2));
-    const double Cy = __dsub_rn(C1, __dmul_rn(r.Sy, C2));
+// fp32 pre-test: false only if the fp64 edge functions certainly have mixed signs.
+// |U32 - U64| <= 20 eps M^2 with M the largest |A[kx]| + |S||A[kz]| term.
+__device__ __forceinline__ bool tri_maybe32(const RayT& r, float3 v0, float3 v1, float3 v2) {
+    const float A0 = self3(v0, r.kx) - r.ok[0], A1 = self3(v0, r.ky) - r.ok[1], A2 = self3(v0, r.kz) - r.ok[2];
+    const float B0 = self3(v1, r.kx) - r.ok[0], B1 = self3(v1, r.ky) - r.ok[1], B2 = self3(v1, r.kz) - r.ok[2];
+    const float C0 = self3(v2, r.kx) - r.ok[0], C1 = self3(v2, r.ky) - r.ok[1], C2 = self3(v2, r.kz) - r.ok[2];
+    const float Ax = fmaf(-r.Sx, A2, A0), Ay = fmaf(-r.Sy, A2, A1);
+    const float Bx = fmaf(-r.Sx, B2, B0), By = fmaf(-r.Sy, B2, B1);
+    const float Cx = fmaf(-r.Sx, C2, C0), Cy = fmaf(-r.Sy, C2, C1);
+    const float U = fmaf(Cx, By, -Cy * Bx);
+    const float V = fmaf(Ax, Cy, -Ay * Cx);
+    const float W = fmaf(Bx, Ay, -By * Ax);
+    const float asx = fabsf(r.Sx), asy = fabsf(r.Sy);
+    const float M = fmaxf(fmaxf(fmaxf(fmaf(asx, fabsf(A2), fabsf(A0)), fmaf(asy, fabsf(A2), fabsf(A1))),
+                                fmaxf(fmaf(asx, fabsf(B2), fabsf(B0)), fmaf(asy, fabsf(B2), fabsf(B1)))),
+                          fmaxf(fmaf(asx, fabsf(C2), fabsf(C0)), fmaf(asy, fabsf(C2), fabsf(C1))));
+    const float bound = (32.0f * 0x1p-24f) * M * M + 1e-30f;
+    const bool neg = U < -bound || V < -bound || W < -bound;
+    const bool pos = U > bound || V > bound || W > bound;
+    return !(neg && pos);
+}
+
+// fp64 watertight test in the oracle's operation order; true and t if hit with t > 0
+__device__ __forceinline__ bool tri_test64(const RayT& r, float3 v0, float3 v1, float3 v2, double& t_out) {
+    const double ox = r.ok[0], oy = r.ok[1], oz = r.ok[2];
+    const double A0 = __dsub_rn((double)self3(v0, r.kx), ox);
+    const double A1 = __dsub_rn((double)self3(v0, r.ky), oy);
+    const double A2 = __dsub_rn((double)self3(v0, r.kz), oz);
+    const double B0 = __dsub_rn((double)self3(v1, r.kx), ox);
+    const double B1 = __dsub_rn((double)self3(v1, r.ky), oy);
+    const double B2 = __dsub_rn((double)self3(v1, r.kz), oz);
+    const double C0 = __dsub_rn((double)self3(v2, r.kx), ox);
+    const double C1 = __dsub_rn((double)self3(v2, r.ky), oy);
+    const double C2 = __dsub_rn((double)self3(v2, r.kz), oz);
+    const double Ax = __dsub_rn(A0, __dmul_rn(r.Sx64, A2));
+    const double Ay = __dsub_rn(A1, __dmul_rn(r.Sy64, A2));
+    const double Bx = __dsub_rn(B0, __dmul_rn(r.Sx64, B2));
+    const double By = __dsub_rn(B1, __dmul_rn(r.Sy64, B2));
+    const double Cx = __dsub_rn(C0, __dmul_rn(r.Sx64, C2));
+    const double Cy = __dsub_rn(C1, __dmul_rn(r.Sy64, C2));
     const double U = __dsub_rn(__dmul_rn(Cx, By), __dmul_rn(Cy, Bx));
     const double V = __dsub_rn(__dmul_rn(Ax, Cy), __dmul_rn(Ay, Cx));
     const double Wt = __dsub_rn(__dmul_rn(Bx, Ay), __dmul_rn(By, Ax));
     if ((U < 0.0 || V < 0.0 || Wt < 0.0) && (U > 0.0 || V > 0.0 || Wt > 0.0)) return false;
     const double det = __dadd_rn(__dadd_rn(U, V), Wt);
     if (det == 0.0) return false;
-    const double Az = __dmul_rn(r.Sz, A2);
-    const double Bz = __dmul_rn(r.Sz, B2);
-    const double Cz = __dmul_rn(r.Sz, C2);
+    const double Az = __dmul_rn(r.Sz64, A2);
+    const double Bz = __dmul_rn(r.Sz64, B2);
+    const double Cz = __dmul_rn(r.Sz64, C2);
     const double T = __dadd_rn(__dadd_rn(__dmul_rn(U, Az), __dmul_rn(V, Bz)), __dmul_rn(Wt, Cz));
     if (det < 0.0 && T >= 0.0) return false;
     if (det > 0.0 && T <= 0.0) return false;
@@ -121,12 +149,13 @@ __device__ __forceinline__ bool tri_test64(const Ray64& r, float3 v0, float3 v1,
     return true;
 }
 
-__device__ __forceinline__ bool sph_test64(const Ray64& r, float3 c, float rad, double& t_out) {
-    const double oc0 = __dsub_rn(r.ou[0], (double)c.x);
-    const double oc1 = __dsub_rn(r.ou[1], (double)c.y);
-    const double oc2 = __dsub_rn(r.ou[2], (double)c.z);
-    const double a = __dadd_rn(__dadd_rn(__dmul_rn(r.d[0], r.d[0]), __dmul_rn(r.d[1], r.d[1])), __dmul_rn(r.d[2], r.d[2]));
-    const double b = __dadd_rn(__dadd_rn(__dmul_rn(oc0, r.d[0]), __dmul_rn(oc1, r.d[1])), __dmul_rn(oc2, r.d[2]));
+__device__ __forceinline__ bool sph_test64(const RayT& r, float3 c, float rad, double& t_out) {
+    const double d0 = r.d[0], d1 = r.d[1], d2 = r.d[2];
+    const double oc0 = __dsub_rn((double)r.o[0], (double)c.x);
+    const double oc1 = __dsub_rn((double)r.o[1], (double)c.y);
+    const double oc2 = __dsub_rn((double)r.o[2], (double)c.z);
+    const double a = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
+    const double b = __dadd_rn(__dadd_rn(__dmul_rn(oc0, d0), __dmul_rn(oc1, d1)), __dmul_rn(oc2, d2));
     const double cc = __dsub_rn(__dadd_rn(__dadd_rn(__dmul_rn(oc0, oc0), __dmul_rn(oc1, oc1)), __dmul_rn(oc2, oc2)),
                                 __dmul_rn((double)rad, (double)rad));
     const double disc = __dsub_rn(__dmul_rn(b, b), __dmul_rn(a, cc));
@@ -148,45 +177,37 @@ __device__ __forceinline__ float half_bits_to_float(uint32_t h) {
     return __half2float(__ushort_as_half((unsigned short)(h & 0x7FFFu)));
 }
 
-__device__ __forceinline__ void test_leaf(const uint4* __restrict__ pool, uint32_t off, int cnt, const Ray64& r64,
-                                          Hit& best) {
-    for (int k = 0; k < cnt; ++k) {
-        const uint4 u0 = __ldg(pool + off + 3 * k);
-        const uint32_t idw = u0.w;
-        const int32_t id = (int32_t)(idw & ~kSphereFlag);
-        double t;
-        bool h;
-        if (idw & kSphereFlag) {
-            const uint4 u1 = __ldg(pool + off + 3 * k + 1);
-            h = sph_test64(r64, make_float3(__uint_as_float(u0.x), __uint_as_float(u0.y), __uint_as_float(u0.z)),
-                           __uint_as_float(u1.x), t);
-        } else {
-            const uint4 u1 = __ldg(pool + off + 3 * k + 1);
-            const uint4 u2 = __ldg(pool + off + 3 * k + 2);
-            h = tri_test64(r64, make_float3(__uint_as_float(u0.x), __uint_as_float(u0.y), __uint_as_float(u0.z)),
-                           make_float3(__uint_as_float(u1.x), __uint_as_float(u1.y), __uint_as_float(u1.z)),
-                           make_float3(__uint_as_float(u2.x), __uint_as_float(u2.y), __uint_as_float(u2.z)), t);
-        }
-        if (h && (best.prim < 0 || t < best.t || (t == best.t && id < best.prim))) {
-            best.t = t;
-            best.prim = id;
-        }
-    }
-}
-
 __device__ __forceinline__ float cull_bound(const Hit& best) {
-    // fp32 upper bound of the best t with margin for the slab rounding (see DESIGN.md "Traversal")
+    // fp32 upper bound of the best t with margin for the slab rounding (DESIGN.md "Traversal")
     return best.prim < 0 ? CUDART_INF_F : __fmul_ru(__double2float_ru(best.t), 1.0000005f);
+}
+__device__ __forceinline__ void test_prim(const uint4* __restrict__ pool, uint32_t unit, const RayT& r, Hit& best) {
+    const uint4 u0 = __ldg(pool + unit);
+    const uint4 u1 = __ldg(pool + unit + 1);
+    const uint32_t idw = u0.w;
+    const int32_t id = (int32_t)(idw & ~kSphereFlag);
+    const float3 p0 = make_float3(__uint_as_float(u0.x), __uint_as_float(u0.y), __uint_as_float(u0.z));
+    double t;
+    bool h;
+    if (idw & kSphereFlag) {
+        h = sph_test64(r, p0, __uint_as_float(u1.x), t);
+    } else {
+        const uint4 u2 = __ldg(pool + unit + 2);
+        const float3 p1 = make_float3(__uint_as_float(u1.x), __uint_as_float(u1.y), __uint_as_float(u1.z));
+        const float3 p2 = make_float3(__uint_as_float(u2.x), __uint_as_float(u2.y), __uint_as_float(u2.z));
+        h = tri_maybe32(r, p0, p1, p2) && tri_test64(r, p0, p1, p2, t);
+    }
+    if (h && (best.prim < 0 || t < best.t || (t == best.t && id < best.prim))) {
+        best.t = t;
+        best.prim = id;
+    }
 }
 
 __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
     Hit best{CUDART_INF, -1};
     if (tp.empty) return best;
-    Ray64 r64;
-    ray64_prepare(o, d, r64);
-    const float inv[3] = {1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
-    const float og[3] = {o.x, o.y, o.z};
-    const bool neg[3] = {signbit(d.x) != 0, signbit(d.y) != 0, signbit(d.z) != 0};
+    RayT r;
+    ray_prepare(o, d, r);
     constexpr float kGrow = 1.0f + 2.0f * (3.0f * 0x1p-24f) / (1.0f - 3.0f * 0x1p-24f);   // 1 + 2 gamma_3
     uint2 stack[kStackSize];
     int sp = 0;
@@ -201,7 +222,10 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
         uint32_t c_off[4];
         float c_tn[4];
         int nc = 0;
-        float tcull = cull_bound(best);
+        uint32_t leaf_unit[4];
+        int leaf_cnt[4];
+        int nl = 0;
+        const float tcull0 = cull_bound(best);
 #pragma unroll
         for (int ci = 0; ci < 4; ++ci) {
             const uint32_t w0 = w[3 * ci], w1 = w[3 * ci + 1], w2 = w[3 * ci + 2];
@@ -215,16 +239,18 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
                 for (int a = 0; a < 3; ++a) {
                     const float bl = __fadd_rn(O[a], lo[a]);
                     const float bh = __fadd_rn(O[a], hi[a]);
-                    const float t0 = __fmul_rn(__fsub_rn(bl, og[a]), inv[a]);
-                    const float t1 = __fmul_rn(__fsub_rn(bh, og[a]), inv[a]);
-                    tn = fmaxf(tn, neg[a] ? t1 : t0);
-                    tf = fminf(tf, neg[a] ? t0 : t1);
+                    const float t0 = __fmul_rn(__fsub_rn(bl, r.o[a]), r.inv[a]);
+                    const float t1 = __fmul_rn(__fsub_rn(bh, r.o[a]), r.inv[a]);
+                    const bool ng = (r.negmask >> a) & 1u;
+                    tn = fmaxf(tn, ng ? t1 : t0);
+                    tf = fminf(tf, ng ? t0 : t1);
                 }
                 tf = tf * kGrow;
-                if (tn <= tf && tn <= tcull) {
+                if (tn <= tf && tn <= tcull0) {
                     if (leaf) {
-                        test_leaf(pool, off, cnt, r64, best);
-                        tcull = cull_bound(best);
+                        leaf_unit[nl] = off;
+                        leaf_cnt[nl] = cnt;
+                        ++nl;
                     } else {
                         c_off[nc] = off;
                         c_tn[nc] = tn;
@@ -234,6 +260,13 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
                 off += leaf ? (uint32_t)(kPrimUnits * cnt) : (uint32_t)kNodeUnits;
             }
         }
+        // all primitives of the hit leaves in one loop (one code path for the divergent tests)
+        int li = 0, lk = 0;
+        while (li < nl) {
+            test_prim(pool, leaf_unit[li] + kPrimUnits * lk, r, best);
+            if (++lk == leaf_cnt[li]) { lk = 0; ++li; }
+        }
+        const float tcull = cull_bound(best);
         // keep interior children still in front of the (possibly updated) best hit; sort by entry
         int m = 0;
         for (int i = 0; i < nc; ++i)

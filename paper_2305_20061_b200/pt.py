@@ -13,7 +13,7 @@ import numpy as np
 from . import scenes
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libpt_b200.so")
+LIB_PATH = os.environ.get("PT_B200_LIB") or os.path.join(_PKG, "libpt_b200.so")   # override: tuning experiments
 _lib = None
 _lock = threading.Lock()
 
@@ -60,6 +60,8 @@ def lib():
             L.pt_debug_build_bvh.argtypes = [P, I64, P, I64, P, P, I64]
             L.pt_debug_f16_round.restype = C.c_uint16
             L.pt_debug_f16_round.argtypes = [C.c_double, I32]
+            if hasattr(L, "pt_debug_nif_trace"):
+                L.pt_debug_nif_trace.argtypes = [P]
             _lib = L
     return _lib
 
