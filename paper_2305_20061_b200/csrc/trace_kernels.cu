@@ -66,6 +66,7 @@ struct RayT {
     double Sx64, Sy64, Sz64;
     int kx, ky, kz;
     unsigned negmask;     // bit a: d[a] has its sign bit set
+    bool have64;
 };
 
 __device__ __forceinline__ float self3(float3 v, int k) { return k == 0 ? v.x : (k == 1 ? v.y : v.z); }
@@ -79,23 +80,39 @@ __device__ __forceinline__ void ray_prepare(float3 o, float3 d, RayT& r) {
     const float dkz = self3(d, kz);
     if (dkz < 0.0f) { int t = kx; kx = ky; ky = t; }
     r.kx = kx; r.ky = ky; r.kz = kz;
-    const double dkz64 = (double)dkz;
-    r.Sx64 = __ddiv_rn((double)self3(d, kx), dkz64);
-    r.Sy64 = __ddiv_rn((double)self3(d, ky), dkz64);
-    r.Sz64 = __ddiv_rn(1.0, dkz64);
-    r.Sx = self3(d, kx) / dkz;
-    r.Sy = self3(d, ky) / dkz;
-    r.Sz = 1.0f / dkz;
+    // fp32 shear for the pre-test only (its error bound tolerates the reciprocal-multiply form);
+    // the fp64 shear of the exact test is computed on first use (ensure64)
+    const float rz = __frcp_rn(dkz);
+    r.Sx = self3(d, kx) * rz;
+    r.Sy = self3(d, ky) * rz;
+    r.Sz = rz;
+    r.have64 = false;
     r.o[0] = o.x; r.o[1] = o.y; r.o[2] = o.z;
     r.d[0] = d.x; r.d[1] = d.y; r.d[2] = d.z;
     r.ok[0] = self3(o, kx); r.ok[1] = self3(o, ky); r.ok[2] = self3(o, kz);
-    r.inv[0] = 1.0f / d.x; r.inv[1] = 1.0f / d.y; r.inv[2] = 1.0f / d.z;
+    r.inv[0] = __frcp_rn(d.x); r.inv[1] = __frcp_rn(d.y); r.inv[2] = __frcp_rn(d.z);
     r.negmask = (signbit(d.x) ? 1u : 0u) | (signbit(d.y) ? 2u : 0u) | (signbit(d.z) ? 4u : 0u);
 }
 
-// fp32 pre-test: false only if the fp64 edge functions certainly have mixed signs.
-// |U32 - U64| <= 20 eps M^2 with M the largest |A[kx]| + |S||A[kz]| term.
-__device__ __forceinline__ bool tri_maybe32(const RayT& r, float3 v0, float3 v1, float3 v2) {
+// fp64 shear constants, exactly the oracle's divisions
+__device__ __forceinline__ void ensure64(RayT& r) {
+    if (r.have64) return;
+    const float3 d = make_float3(r.d[0], r.d[1], r.d[2]);
+    const double dkz64 = (double)self3(d, r.kz);
+    r.Sx64 = __ddiv_rn((double)self3(d, r.kx), dkz64);
+    r.Sy64 = __ddiv_rn((double)self3(d, r.ky), dkz64);
+    r.Sz64 = __ddiv_rn(1.0, dkz64);
+    r.have64 = true;
+}
+
+// Certified fp32 watertight test. Returns 0 if the exact (hence the fp64 oracle's) test certainly
+// misses, 1 if it certainly hits with t in [t - dt, t + dt], t - dt > 0, and 2 if undecided (near an
+// edge or t ~ 0): then the fp64 test decides. Error bounds: with eps = 2^-24,
+// mX = max|A[kx]| + |Sx| max|A[kz]| (over the 3 vertices) and likewise mY, the sheared coordinates
+// carry |dAx| <= 4 eps mX, the edge functions |dU| <= 19 eps mX mY (we use 24), and
+// |dT| <= 3 eU mZ + 18 eps maxE mZ, |ddet| <= 3 eU + 6 eps maxE with mZ = |Sz| max|A[kz]|.
+__device__ __forceinline__ int tri_test32(const RayT& r, float3 v0, float3 v1, float3 v2, float& t, float& dt) {
+    constexpr float eps = 0x1p-24f;
     const float A0 = self3(v0, r.kx) - r.ok[0], A1 = self3(v0, r.ky) - r.ok[1], A2 = self3(v0, r.kz) - r.ok[2];
     const float B0 = self3(v1, r.kx) - r.ok[0], B1 = self3(v1, r.ky) - r.ok[1], B2 = self3(v1, r.kz) - r.ok[2];
     const float C0 = self3(v2, r.kx) - r.ok[0], C1 = self3(v2, r.ky) - r.ok[1], C2 = self3(v2, r.kz) - r.ok[2];
@@ -105,18 +122,33 @@ __device__ __forceinline__ bool tri_maybe32(const RayT& r, float3 v0, float3 v1,
     const float U = fmaf(Cx, By, -Cy * Bx);
     const float V = fmaf(Ax, Cy, -Ay * Cx);
     const float W = fmaf(Bx, Ay, -By * Ax);
-    const float asx = fabsf(r.Sx), asy = fabsf(r.Sy);
-    const float M = fmaxf(fmaxf(fmaxf(fmaf(asx, fabsf(A2), fabsf(A0)), fmaf(asy, fabsf(A2), fabsf(A1))),
-                                fmaxf(fmaf(asx, fabsf(B2), fabsf(B0)), fmaf(asy, fabsf(B2), fabsf(B1)))),
-                          fmaxf(fmaf(asx, fabsf(C2), fabsf(C0)), fmaf(asy, fabsf(C2), fabsf(C1))));
-    const float bound = (32.0f * 0x1p-24f) * M * M + 1e-30f;
-    const bool neg = U < -bound || V < -bound || W < -bound;
-    const bool pos = U > bound || V > bound || W > bound;
-    return !(neg && pos);
+    const float mz2 = fmaxf(fabsf(A2), fmaxf(fabsf(B2), fabsf(C2)));
+    const float mX = fmaf(fabsf(r.Sx), mz2, fmaxf(fabsf(A0), fmaxf(fabsf(B0), fabsf(C0))));
+    const float mY = fmaf(fabsf(r.Sy), mz2, fmaxf(fabsf(A1), fmaxf(fabsf(B1), fabsf(C1))));
+    const float eU = (24.0f * eps) * mX * mY;
+    const bool neg = U < -eU || V < -eU || W < -eU;
+    const bool pos = U > eU || V > eU || W > eU;
+    if (neg && pos) return 0;
+    const bool certain = (U > eU && V > eU && W > eU) || (U < -eU && V < -eU && W < -eU);
+    if (!certain) return 2;
+    const float det = U + V + W;
+    const float T = fmaf(W, r.Sz * C2, fmaf(V, r.Sz * B2, U * (r.Sz * A2)));
+    const float mZ = fabsf(r.Sz) * mz2;
+    const float maxE = fmaxf(fabsf(U), fmaxf(fabsf(V), fabsf(W)));
+    const float dT = 3.0f * eU * mZ + (18.0f * eps) * maxE * mZ;
+    const float dDet = 3.0f * eU + (6.0f * eps) * maxE;
+    const float adet = fabsf(det);
+    if (adet <= 2.0f * dDet) return 2;
+    t = __fdiv_rn(T, det);
+    dt = 1.25f * ((dT + fabsf(t) * dDet) / (adet - dDet) + (2.0f * eps) * fabsf(t));
+    if (t + dt <= 0.0f) return 0;
+    if (t - dt <= 0.0f) return 2;
+    return 1;
 }
 
 // fp64 watertight test in the oracle's operation order; true and t if hit with t > 0
-__device__ __forceinline__ bool tri_test64(const RayT& r, float3 v0, float3 v1, float3 v2, double& t_out) {
+__device__ __forceinline__ bool tri_test64(RayT& r, float3 v0, float3 v1, float3 v2, double& t_out) {
+    ensure64(r);
     const double ox = r.ok[0], oy = r.ok[1], oz = r.ok[2];
     const double A0 = __dsub_rn((double)self3(v0, r.kx), ox);
     const double A1 = __dsub_rn((double)self3(v0, r.ky), oy);
@@ -149,7 +181,7 @@ __device__ __forceinline__ bool tri_test64(const RayT& r, float3 v0, float3 v1, 
     return true;
 }
 
-__device__ __forceinline__ bool sph_test64(const RayT& r, float3 c, float rad, double& t_out) {
+__device__ __forceinline__ bool sph_test64(RayT& r, float3 c, float rad, double& t_out) {
     const double d0 = r.d[0], d1 = r.d[1], d2 = r.d[2];
     const double oc0 = __dsub_rn((double)r.o[0], (double)c.x);
     const double oc1 = __dsub_rn((double)r.o[1], (double)c.y);
@@ -171,7 +203,15 @@ __device__ __forceinline__ bool sph_test64(const RayT& r, float3 c, float rad, d
 // ---------------------------------------------------------------------------------------------
 // Wide-BVH closest hit: (t, id) lexicographic minimum over all primitives (reading R11)
 // ---------------------------------------------------------------------------------------------
-struct Hit { double t; int32_t prim; };
+// Best hit so far. Decided exactly like the fp64 oracle, but carried as a certified fp32 interval
+// [tlo, thi] until a near-tie forces the exact fp64 t (exact == true).
+struct Hit {
+    double t;
+    float tlo, thi;
+    int32_t prim;
+    uint32_t unit;
+    bool exact;
+};
 
 __device__ __forceinline__ float half_bits_to_float(uint32_t h) {
     return __half2float(__ushort_as_half((unsigned short)(h & 0x7FFFu)));
@@ -179,32 +219,82 @@ __device__ __forceinline__ float half_bits_to_float(uint32_t h) {
 
 __device__ __forceinline__ float cull_bound(const Hit& best) {
     // fp32 upper bound of the best t with margin for the slab rounding
-    return best.prim < 0 ? CUDART_INF_F : __fmul_ru(__double2float_ru(best.t), 1.0000005f);
+    return best.prim < 0 ? CUDART_INF_F : __fmul_ru(best.thi, 1.0000005f);
 }
-__device__ __forceinline__ void test_prim(const uint4* __restrict__ pool, uint32_t unit, const RayT& r, Hit& best) {
+
+// exact fp64 test of the primitive stored at `unit`
+__device__ __forceinline__ bool exact_test(const uint4* __restrict__ pool, uint32_t unit, RayT& r, double& t) {
+    const uint4 u0 = __ldg(pool + unit);
+    const uint4 u1 = __ldg(pool + unit + 1);
+    const float3 p0 = make_float3(__uint_as_float(u0.x), __uint_as_float(u0.y), __uint_as_float(u0.z));
+    if (u0.w & kSphereFlag) return sph_test64(r, p0, __uint_as_float(u1.x), t);
+    const uint4 u2 = __ldg(pool + unit + 2);
+    return tri_test64(r, p0, make_float3(__uint_as_float(u1.x), __uint_as_float(u1.y), __uint_as_float(u1.z)),
+                      make_float3(__uint_as_float(u2.x), __uint_as_float(u2.y), __uint_as_float(u2.z)), t);
+}
+
+__device__ __forceinline__ void test_prim(const uint4* __restrict__ pool, uint32_t unit, RayT& r, Hit& best) {
     const uint4 u0 = __ldg(pool + unit);
     const uint4 u1 = __ldg(pool + unit + 1);
     const uint32_t idw = u0.w;
     const int32_t id = (int32_t)(idw & ~kSphereFlag);
     const float3 p0 = make_float3(__uint_as_float(u0.x), __uint_as_float(u0.y), __uint_as_float(u0.z));
-    double t;
-    bool h;
+    double t64 = 0.0;
+    float t32 = 0.0f, dt = 0.0f;
+    bool exact;
     if (idw & kSphereFlag) {
-        h = sph_test64(r, p0, __uint_as_float(u1.x), t);
+        if (!sph_test64(r, p0, __uint_as_float(u1.x), t64)) return;
+        exact = true;
     } else {
         const uint4 u2 = __ldg(pool + unit + 2);
         const float3 p1 = make_float3(__uint_as_float(u1.x), __uint_as_float(u1.y), __uint_as_float(u1.z));
         const float3 p2 = make_float3(__uint_as_float(u2.x), __uint_as_float(u2.y), __uint_as_float(u2.z));
-        h = tri_maybe32(r, p0, p1, p2) && tri_test64(r, p0, p1, p2, t);
+        const int c = tri_test32(r, p0, p1, p2, t32, dt);
+        if (c == 0) return;
+        if (c == 2) {
+            if (!tri_test64(r, p0, p1, p2, t64)) return;
+            exact = true;
+        } else {
+            exact = false;
+        }
     }
-    if (h && (best.prim < 0 || t < best.t || (t == best.t && id < best.prim))) {
-        best.t = t;
-        best.prim = id;
+    const float tlo = exact ? __double2float_rd(t64) : t32 - dt;
+    const float thi = exact ? __double2float_ru(t64) : t32 + dt;
+    if (best.prim >= 0) {
+        if (tlo > best.thi) return;                 // certainly farther
+        if (!(thi < best.tlo)) {                    // not certainly closer: decide exactly, as the oracle
+            if (!exact) {
+                if (!exact_test(pool, unit, r, t64)) return;
+                exact = true;
+            }
+            if (!best.exact) {
+                double tb;
+                exact_test(pool, best.unit, r, tb);
+                best.t = tb;
+                best.tlo = __double2float_rd(tb);
+                best.thi = __double2float_ru(tb);
+                best.exact = true;
+            }
+            if (!(t64 < best.t || (t64 == best.t && id < best.prim))) return;
+        }
+    }
+    best.prim = id;
+    best.unit = unit;
+    best.exact = exact;
+    best.t = exact ? t64 : (double)t32;
+    best.tlo = exact ? __double2float_rd(t64) : tlo;
+    best.thi = exact ? __double2float_ru(t64) : thi;
+}
+
+__device__ __forceinline__ void cswap(float& ta, uint32_t& oa, float& tb, uint32_t& ob) {
+    if (tb < ta) {
+        const float t = ta; ta = tb; tb = t;
+        const uint32_t o = oa; oa = ob; ob = o;
     }
 }
 
 __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
-    Hit best{CUDART_INF, -1};
+    Hit best{CUDART_INF, CUDART_INF_F, CUDART_INF_F, -1, 0u, true};
     if (tp.empty) return best;
     RayT r;
     ray_prepare(o, d, r);
@@ -219,15 +309,18 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
         const uint32_t w[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
         const float O[3] = {__uint_as_float(h.x), __uint_as_float(h.y), __uint_as_float(h.z)};
         uint32_t off = h.w;
-        uint32_t c_off[4];
-        float c_tn[4];
-        int nc = 0;
-        uint32_t leaf_unit[4];
-        int leaf_cnt[4];
-        int nl = 0;
+        // per-child results in registers (static indices only: no local-memory arrays)
+        float ctn[4];
+        uint32_t coff[4];
+        uint32_t lunit[4];
+        int lcnt[4];
         const float tcull0 = cull_bound(best);
 #pragma unroll
         for (int ci = 0; ci < 4; ++ci) {
+            ctn[ci] = CUDART_INF_F;
+            coff[ci] = 0;
+            lcnt[ci] = 0;
+            lunit[ci] = 0;
             const uint32_t w0 = w[3 * ci], w1 = w[3 * ci + 1], w2 = w[3 * ci + 2];
             if (w0 & 0x8000u) {
                 const bool leaf = (w0 & 0x80000000u) != 0;
@@ -246,39 +339,48 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
                     tf = fminf(tf, ng ? t0 : t1);
                 }
                 tf = tf * kGrow;
-                if (tn <= tf && tn <= tcull0) {
-                    if (leaf) {
-                        leaf_unit[nl] = off;
-                        leaf_cnt[nl] = cnt;
-                        ++nl;
-                    } else {
-                        c_off[nc] = off;
-                        c_tn[nc] = tn;
-                        ++nc;
-                    }
+                const bool hit = tn <= tf && tn <= tcull0;
+                if (leaf) {
+                    lunit[ci] = off;
+                    lcnt[ci] = hit ? cnt : 0;
+                } else {
+                    ctn[ci] = hit ? tn : CUDART_INF_F;
+                    coff[ci] = off;
                 }
                 off += leaf ? (uint32_t)(kPrimUnits * cnt) : (uint32_t)kNodeUnits;
             }
         }
-        // all primitives of the hit leaves in one loop (one code path for the divergent tests)
-        int li = 0, lk = 0;
-        while (li < nl) {
-            test_prim(pool, leaf_unit[li] + kPrimUnits * lk, r, best);
-            if (++lk == leaf_cnt[li]) { lk = 0; ++li; }
+        // primitives of the hit leaves: one loop over (leaf, prim) so test_prim is instantiated once
+        {
+            uint32_t unit = 0;
+            int left = 0, ci = 0;
+            for (;;) {
+                if (left == 0) {
+                    while (ci < 4 && (ci == 0 ? lcnt[0] : ci == 1 ? lcnt[1] : ci == 2 ? lcnt[2] : lcnt[3]) == 0) ++ci;
+                    if (ci == 4) break;
+                    left = ci == 0 ? lcnt[0] : ci == 1 ? lcnt[1] : ci == 2 ? lcnt[2] : lcnt[3];
+                    unit = ci == 0 ? lunit[0] : ci == 1 ? lunit[1] : ci == 2 ? lunit[2] : lunit[3];
+                    ++ci;
+                }
+                test_prim(pool, unit, r, best);
+                unit += kPrimUnits;
+                --left;
+            }
         }
         const float tcull = cull_bound(best);
-        // keep interior children still in front of the (possibly updated) best hit; sort by entry
-        int m = 0;
-        for (int i = 0; i < nc; ++i)
-            if (c_tn[i] <= tcull) { c_off[m] = c_off[i]; c_tn[m] = c_tn[i]; ++m; }
-        for (int i = 1; i < m; ++i)
-            for (int j = i; j > 0 && c_tn[j] < c_tn[j - 1]; --j) {
-                float tt = c_tn[j]; c_tn[j] = c_tn[j - 1]; c_tn[j - 1] = tt;
-                uint32_t oo = c_off[j]; c_off[j] = c_off[j - 1]; c_off[j - 1] = oo;
-            }
-        if (m > 0) {
-            for (int i = m - 1; i >= 1; --i) stack[sp++] = make_uint2(c_off[i], __float_as_uint(c_tn[i]));
-            cur = c_off[0];
+        // sort the interior children by entry distance (network of 5 compare-swaps), cull, descend
+        cswap(ctn[0], coff[0], ctn[1], coff[1]);
+        cswap(ctn[2], coff[2], ctn[3], coff[3]);
+        cswap(ctn[0], coff[0], ctn[2], coff[2]);
+        cswap(ctn[1], coff[1], ctn[3], coff[3]);
+        cswap(ctn[1], coff[1], ctn[2], coff[2]);
+        // (non-hit children carry +inf, which is never <= a finite bound; with no hit yet the bound is
+        // +inf, so test finiteness explicitly)
+#pragma unroll
+        for (int ci = 3; ci >= 1; --ci)
+            if (ctn[ci] < CUDART_INF_F && ctn[ci] <= tcull) stack[sp++] = make_uint2(coff[ci], __float_as_uint(ctn[ci]));
+        if (ctn[0] < CUDART_INF_F && ctn[0] <= tcull) {
+            cur = coff[0];
             continue;
         }
         bool found = false;

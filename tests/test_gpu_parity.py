@@ -95,7 +95,8 @@ def _primary_check(ptm, orc, sc, W, H, pix, seed=0, sample=0):
     assert frac >= 0.9999, f"primary-hit agreement {frac}"
     assert (edge[mism] <= 1e-5).all(), f"mismatches off the edge band: {edge[mism]}"
     hit = prim_o >= 0
-    assert np.array_equal(t_g[hit & eq], t_o[hit & eq].astype(np.float32))
+    # t: fp32 estimate within its certified interval (exact fp64 only where a tie had to be decided)
+    assert np.allclose(t_g[hit & eq], t_o[hit & eq], rtol=1e-5, atol=0)
     return frac
 
 
@@ -129,7 +130,7 @@ def test_trace_rays_random_soup_vs_brute_force(ptm, orc, seed):
     prim_o, t_o, _, _ = orc.OracleScene(sc).closest_hit(o.astype(np.float64), d.astype(np.float64), brute=True)
     assert np.array_equal(prim_g.cpu().numpy(), prim_o)
     hit = prim_o >= 0
-    assert np.array_equal(t_g.cpu().numpy()[hit], t_o[hit].astype(np.float32))
+    assert np.allclose(t_g.cpu().numpy()[hit], t_o[hit], rtol=1e-5, atol=1e-5)
 
 
 def test_furnace_empty_scene_exact(ptm):
