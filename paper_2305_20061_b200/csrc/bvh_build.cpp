@@ -112,7 +112,10 @@ struct Builder {
                     double cost = acc.area() * (double)c + rarea[k + 1] * (double)rcnt[k + 1];
                     if (cost < best) { best = cost; best_k = k; }
                 }
+                // SAH with a node-traversal cost of kTraversalCost primitive tests (per unit area)
+                constexpr double kTraversalCost = 1.5;
                 double leaf_cost = bb.area() * (double)it.count;
+                best += kTraversalCost * bb.area();
                 if (best_k >= 0 && (best < leaf_cost || it.count > kMaxLeafPrims)) {
                     auto mid = std::partition(order.begin() + it.first, order.begin() + it.first + it.count,
                                               [&](int64_t id) { return bin_of(id) <= best_k; });

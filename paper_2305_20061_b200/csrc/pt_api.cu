@@ -45,10 +45,19 @@ int check_device() {
 
 bool finite3(const float* v) { return std::isfinite(v[0]) && std::isfinite(v[1]) && std::isfinite(v[2]); }
 
+void free_path_state(pt::Workspace& ws) {
+    for (int b = 0; b < 2; ++b) {
+        cudaFree(ws.rayA[b]); cudaFree(ws.rayB[b]); cudaFree(ws.rayC[b]);
+        ws.rayA[b] = ws.rayB[b] = nullptr;
+        ws.rayC[b] = nullptr;
+    }
+    cudaFree(ws.hit); cudaFree(ws.esc); cudaFree(ws.esc_beta); cudaFree(ws.wave_buf);
+    ws.hit = nullptr; ws.esc = ws.esc_beta = nullptr; ws.wave_buf = nullptr;
+}
+
 void free_ws(pt::Workspace& ws) {
-    cudaFree(ws.ray_o); cudaFree(ws.ray_d); cudaFree(ws.beta);
-    cudaFree(ws.queue[0]); cudaFree(ws.queue[1]); cudaFree(ws.hit);
-    cudaFree(ws.esc); cudaFree(ws.esc_beta); cudaFree(ws.wave_buf); cudaFree(ws.counters);
+    free_path_state(ws);
+    cudaFree(ws.counters);
     cudaFree(ws.fb);
     cudaFree(ws.d_stats);
     if (ws.own_stream) cudaStreamDestroy(ws.own_stream);
@@ -63,16 +72,14 @@ int ensure_ws(pt::Workspace& ws, int64_t cap) {
         CU(cudaStreamCreateWithFlags(&ws.own_stream, cudaStreamNonBlocking));
     }
     if (cap <= ws.capacity) return PT_OK;
-    cudaFree(ws.ray_o); cudaFree(ws.ray_d); cudaFree(ws.beta);
-    cudaFree(ws.queue[0]); cudaFree(ws.queue[1]); cudaFree(ws.hit);
-    cudaFree(ws.esc); cudaFree(ws.esc_beta); cudaFree(ws.wave_buf);
+    free_path_state(ws);
     ws.capacity = 0;
-    CU(cudaMalloc(&ws.ray_o, sizeof(float4) * cap));
-    CU(cudaMalloc(&ws.ray_d, sizeof(float4) * cap));
-    CU(cudaMalloc(&ws.beta, sizeof(float4) * cap));
-    CU(cudaMalloc(&ws.queue[0], sizeof(uint32_t) * cap));
-    CU(cudaMalloc(&ws.queue[1], sizeof(uint32_t) * cap));
-    CU(cudaMalloc(&ws.hit, sizeof(float4) * cap));
+    for (int b = 0; b < 2; ++b) {
+        CU(cudaMalloc(&ws.rayA[b], sizeof(float4) * cap));
+        CU(cudaMalloc(&ws.rayB[b], sizeof(float4) * cap));
+        CU(cudaMalloc(&ws.rayC[b], sizeof(float2) * cap));
+    }
+    CU(cudaMalloc(&ws.hit, sizeof(float2) * cap));
     CU(cudaMalloc(&ws.esc, sizeof(float4) * cap));
     CU(cudaMalloc(&ws.esc_beta, sizeof(float4) * cap));
     CU(cudaMalloc(&ws.wave_buf, sizeof(float) * 3 * cap));
@@ -176,15 +183,13 @@ int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, i
         pt::launch_raygen(cam, W, H, (int)w0, (int)slots, seed, ws, st);
         tm.end(T_RAYGEN, e0);
         for (int d = 1; d <= max_depth; ++d) {
-            const int identity = d == 1;
-            const uint32_t* qin = identity ? nullptr : ws.queue[d & 1];
-            uint32_t* qout = ws.queue[(d + 1) & 1];
+            const int buf = (d - 1) & 1;       // bounce d reads state buffer buf, shade writes buf ^ 1
             tm.begin(T_TRAVERSE, &e0);
-            pt::launch_traverse(tp, qin, ws.counters + (d - 1), identity, ws, st);
+            pt::launch_traverse(tp, buf, ws.counters + (d - 1), ws, st);
             tm.end(T_TRAVERSE, e0);
             tm.begin(T_SHADE, &e0);
-            pt::launch_shade(tp, W, H, (int)w0, d, max_depth, seed, qin, ws.counters + (d - 1), identity, qout,
-                             ws.counters + d, use_nif, env, ws, st);
+            pt::launch_shade(tp, W, H, (int)w0, d, max_depth, seed, buf, ws.counters + (d - 1), ws.counters + d,
+                             use_nif, env, ws, st);
             tm.end(T_SHADE, e0);
             stats.launches += 2;
             stats.traverse_launches += 1;

@@ -55,11 +55,11 @@ double f16_value(uint16_t h);
 
 struct Workspace {
     int64_t capacity = 0;      // path slots
-    float4* ray_o = nullptr;   // [cap] origin (w unused)
-    float4* ray_d = nullptr;   // [cap] direction (w unused)
-    float4* beta = nullptr;    // [cap] throughput (w unused)
-    uint32_t* queue[2] = {nullptr, nullptr};  // alive slot queues (ping-pong)
-    float4* hit = nullptr;     // [cap] per queue entry: (t, prim bits, 0, 0)
+    // live-path state in queue order, double buffered (in/out of each bounce):
+    float4* rayA[2] = {nullptr, nullptr};   // (o.xyz, slot bits)
+    float4* rayB[2] = {nullptr, nullptr};   // (d.xyz, beta.x)
+    float2* rayC[2] = {nullptr, nullptr};   // (beta.y, beta.z)
+    float2* hit = nullptr;     // [cap] per queue entry: (t, prim bits)
     float4* esc = nullptr;     // [cap] escaped-ray queue: (u, v, slot bits, 0)
     float4* esc_beta = nullptr;// [cap] escaped-ray throughput
     float* wave_buf = nullptr; // [cap][3] radiance per slot, written exactly once per path
@@ -128,11 +128,10 @@ struct TraceParams {
 // kernel launchers (trace_kernels.cu)
 void launch_raygen(const Cam32& cam, int W, int H, int first_sample, int n_slots, uint64_t seed, Workspace& ws,
                    cudaStream_t st);
-void launch_traverse(const TraceParams& tp, const uint32_t* queue_in, const uint32_t* count_in, int identity,
-                     Workspace& ws, cudaStream_t st);
+void launch_traverse(const TraceParams& tp, int buf, const uint32_t* count_in, Workspace& ws, cudaStream_t st);
 void launch_shade(const TraceParams& tp, int W, int H, int first_sample, int depth, int max_depth, uint64_t seed,
-                  const uint32_t* queue_in, const uint32_t* count_in, int identity, uint32_t* queue_out,
-                  uint32_t* count_out, int use_nif, float3 env, Workspace& ws, cudaStream_t st);
+                  int buf, const uint32_t* count_in, uint32_t* count_out, int use_nif, float3 env, Workspace& ws,
+                  cudaStream_t st);
 void launch_accumulate(const float* wave_buf, int n_pix, int k, float* fb, cudaStream_t st);
 void launch_primary(const TraceParams& tp, const Cam32& cam, int W, int H, int sample, uint64_t seed,
                     int32_t* prim, float* t, cudaStream_t st);

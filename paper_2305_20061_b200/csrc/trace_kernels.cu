@@ -312,60 +312,50 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
         // per-child results in registers (static indices only: no local-memory arrays)
         float ctn[4];
         uint32_t coff[4];
-        uint32_t lunit[4];
-        int lcnt[4];
+        uint32_t lu[4];
+        uint32_t leafmask = 0, cntpack = 0;
         const float tcull0 = cull_bound(best);
 #pragma unroll
         for (int ci = 0; ci < 4; ++ci) {
             ctn[ci] = CUDART_INF_F;
             coff[ci] = 0;
-            lcnt[ci] = 0;
-            lunit[ci] = 0;
+            lu[ci] = off;
             const uint32_t w0 = w[3 * ci], w1 = w[3 * ci + 1], w2 = w[3 * ci + 2];
-            if (w0 & 0x8000u) {
-                const bool leaf = (w0 & 0x80000000u) != 0;
-                const int cnt = (int)(((w1 >> 15) & 1u) | ((w1 >> 30) & 2u)) + 1;
-                const float lo[3] = {half_bits_to_float(w0), half_bits_to_float(w0 >> 16), half_bits_to_float(w1)};
-                const float hi[3] = {half_bits_to_float(w1 >> 16), half_bits_to_float(w2), half_bits_to_float(w2 >> 16)};
-                float tn = 0.0f, tf = CUDART_INF_F;
+            const bool valid = (w0 & 0x8000u) != 0;
+            const bool leaf = (w0 & 0x80000000u) != 0;
+            const uint32_t cnt = (((w1 >> 15) & 1u) | ((w1 >> 30) & 2u)) + 1u;
+            const float lo[3] = {half_bits_to_float(w0), half_bits_to_float(w0 >> 16), half_bits_to_float(w1)};
+            const float hi[3] = {half_bits_to_float(w1 >> 16), half_bits_to_float(w2), half_bits_to_float(w2 >> 16)};
+            float tn = 0.0f, tf = CUDART_INF_F;
 #pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    const float bl = __fadd_rn(O[a], lo[a]);
-                    const float bh = __fadd_rn(O[a], hi[a]);
-                    const float t0 = __fmul_rn(__fsub_rn(bl, r.o[a]), r.inv[a]);
-                    const float t1 = __fmul_rn(__fsub_rn(bh, r.o[a]), r.inv[a]);
-                    const bool ng = (r.negmask >> a) & 1u;
-                    tn = fmaxf(tn, ng ? t1 : t0);
-                    tf = fminf(tf, ng ? t0 : t1);
-                }
-                tf = tf * kGrow;
-                const bool hit = tn <= tf && tn <= tcull0;
-                if (leaf) {
-                    lunit[ci] = off;
-                    lcnt[ci] = hit ? cnt : 0;
-                } else {
-                    ctn[ci] = hit ? tn : CUDART_INF_F;
-                    coff[ci] = off;
-                }
-                off += leaf ? (uint32_t)(kPrimUnits * cnt) : (uint32_t)kNodeUnits;
+            for (int a = 0; a < 3; ++a) {
+                const float bl = __fadd_rn(O[a], lo[a]);
+                const float bh = __fadd_rn(O[a], hi[a]);
+                const float t0 = __fmul_rn(__fsub_rn(bl, r.o[a]), r.inv[a]);
+                const float t1 = __fmul_rn(__fsub_rn(bh, r.o[a]), r.inv[a]);
+                const bool ng = (r.negmask >> a) & 1u;
+                tn = fmaxf(tn, ng ? t1 : t0);
+                tf = fminf(tf, ng ? t0 : t1);
             }
+            tf = tf * kGrow;
+            const bool hit = valid && tn <= tf && tn <= tcull0;
+            if (hit && leaf) {
+                leafmask |= 1u << ci;
+                cntpack |= cnt << (4 * ci);
+            }
+            if (hit && !leaf) {
+                ctn[ci] = tn;
+                coff[ci] = off;
+            }
+            off += valid ? (leaf ? kPrimUnits * cnt : (uint32_t)kNodeUnits) : 0u;
         }
-        // primitives of the hit leaves: one loop over (leaf, prim) so test_prim is instantiated once
-        {
-            uint32_t unit = 0;
-            int left = 0, ci = 0;
-            for (;;) {
-                if (left == 0) {
-                    while (ci < 4 && (ci == 0 ? lcnt[0] : ci == 1 ? lcnt[1] : ci == 2 ? lcnt[2] : lcnt[3]) == 0) ++ci;
-                    if (ci == 4) break;
-                    left = ci == 0 ? lcnt[0] : ci == 1 ? lcnt[1] : ci == 2 ? lcnt[2] : lcnt[3];
-                    unit = ci == 0 ? lunit[0] : ci == 1 ? lunit[1] : ci == 2 ? lunit[2] : lunit[3];
-                    ++ci;
-                }
-                test_prim(pool, unit, r, best);
-                unit += kPrimUnits;
-                --left;
-            }
+        // primitives of the hit leaves (one instantiation of test_prim)
+        while (leafmask) {
+            const int ci = __ffs(leafmask) - 1;
+            leafmask &= leafmask - 1;
+            uint32_t unit = ci == 0 ? lu[0] : ci == 1 ? lu[1] : ci == 2 ? lu[2] : lu[3];
+            const uint32_t cnt = (cntpack >> (4 * ci)) & 15u;
+            for (uint32_t k = 0; k < cnt; ++k, unit += kPrimUnits) test_prim(pool, unit, r, best);
         }
         const float tcull = cull_bound(best);
         // sort the interior children by entry distance (network of 5 compare-swaps), cull, descend
@@ -396,31 +386,31 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
 // ---------------------------------------------------------------------------------------------
 // Kernels
 // ---------------------------------------------------------------------------------------------
+// Ray state is kept in queue order (compacted every bounce) so every kernel reads and writes it
+// coalesced: A = (o.xyz, slot), B = (d.xyz, beta.x), C = (beta.y, beta.z)  -- 40 B per live path.
 __global__ void __launch_bounds__(256) raygen_kernel(Cam32 cam, int W, int H, int first_sample, int n_slots, uint2 key,
-                                                     float4* __restrict__ ray_o, float4* __restrict__ ray_d,
-                                                     float4* __restrict__ beta) {
+                                                     float4* __restrict__ A, float4* __restrict__ B,
+                                                     float2* __restrict__ C) {
     const int np = W * H;
     for (int slot = blockIdx.x * blockDim.x + threadIdx.x; slot < n_slots; slot += gridDim.x * blockDim.x) {
         const int p = slot % np;
         const int s = first_sample + slot / np;
         const uint4 r = philox10(make_uint4((uint32_t)p, (uint32_t)s, 0u, 0u), key);
         const float3 d = cam_dir(cam, W, H, p % W, p / W, u01f(r.x), u01f(r.y));
-        ray_o[slot] = make_float4(cam.eye[0], cam.eye[1], cam.eye[2], 0.0f);
-        ray_d[slot] = make_float4(d.x, d.y, d.z, 0.0f);
-        beta[slot] = make_float4(1.0f, 1.0f, 1.0f, 0.0f);
+        A[slot] = make_float4(cam.eye[0], cam.eye[1], cam.eye[2], __uint_as_float((uint32_t)slot));
+        B[slot] = make_float4(d.x, d.y, d.z, 1.0f);
+        C[slot] = make_float2(1.0f, 1.0f);
     }
 }
 
-__global__ void __launch_bounds__(128) traverse_kernel(TraceParams tp, const uint32_t* __restrict__ q_in,
-                                                       const uint32_t* __restrict__ cnt_in, int identity,
-                                                       const float4* __restrict__ ray_o,
-                                                       const float4* __restrict__ ray_d, float4* __restrict__ hit) {
+__global__ void __launch_bounds__(128) traverse_kernel(TraceParams tp, const uint32_t* __restrict__ cnt_in,
+                                                       const float4* __restrict__ A, const float4* __restrict__ B,
+                                                       float2* __restrict__ hit) {
     const uint32_t n = *cnt_in;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint32_t slot = identity ? i : __ldg(q_in + i);
-        const float4 o = __ldg(ray_o + slot), d = __ldg(ray_d + slot);
+        const float4 o = __ldg(A + i), d = __ldg(B + i);
         const Hit h = closest_hit(tp, make_float3(o.x, o.y, o.z), make_float3(d.x, d.y, d.z));
-        hit[i] = make_float4((float)h.t, __int_as_float(h.prim), 0.0f, 0.0f);
+        hit[i] = make_float2((float)h.t, __int_as_float(h.prim));
     }
 }
 
@@ -454,18 +444,18 @@ struct ShadeArgs {
     TraceParams tp;
     int W, H, first_sample, depth, max_depth;
     uint2 key;
-    const uint32_t* q_in;
     const uint32_t* cnt_in;
-    int identity;
-    uint32_t* q_out;
     uint32_t* cnt_out;
     uint32_t* cnt_esc;
     int use_nif;
     float3 env;
-    float4* ray_o;
-    float4* ray_d;
-    float4* beta;
-    const float4* hit;
+    const float4* A_in;
+    const float4* B_in;
+    const float2* C_in;
+    float4* A_out;
+    float4* B_out;
+    float2* C_out;
+    const float2* hit;
     float4* esc;
     float4* esc_beta;
     float* wave_buf;
@@ -484,12 +474,13 @@ __global__ void __launch_bounds__(256) shade_kernel(ShadeArgs a) {
         float3 o3 = make_float3(0, 0, 0), wi = make_float3(0, 0, 0), bt = make_float3(0, 0, 0);
         float eu = 0.0f, ev = 0.0f;
         if (active) {
-            slot = a.identity ? i : __ldg(a.q_in + i);
-            const float4 hv = __ldg(a.hit + i);
+            const float2 hv = __ldg(a.hit + i);
             const int32_t prim = __float_as_int(hv.y);
-            const float4 o = a.ray_o[slot], d4 = a.ray_d[slot], b4 = a.beta[slot];
+            const float4 o = __ldg(a.A_in + i), d4 = __ldg(a.B_in + i);
+            const float2 c2 = __ldg(a.C_in + i);
+            slot = __float_as_uint(o.w);
             const float3 d = make_float3(d4.x, d4.y, d4.z);
-            bt = make_float3(b4.x, b4.y, b4.z);
+            bt = make_float3(d4.w, c2.x, c2.y);
             float3 L = make_float3(0, 0, 0);
             bool done = true;
             if (prim < 0) {                                   // escaped: environment light
@@ -602,10 +593,9 @@ __global__ void __launch_bounds__(256) shade_kernel(ShadeArgs a) {
         const uint32_t pos_a = warp_append(alive, a.cnt_out);
         const uint32_t pos_e = warp_append(escaped, a.cnt_esc);
         if (alive) {
-            a.ray_o[slot] = make_float4(o3.x, o3.y, o3.z, 0.0f);
-            a.ray_d[slot] = make_float4(wi.x, wi.y, wi.z, 0.0f);
-            a.beta[slot] = make_float4(bt.x, bt.y, bt.z, 0.0f);
-            a.q_out[pos_a] = slot;
+            a.A_out[pos_a] = make_float4(o3.x, o3.y, o3.z, __uint_as_float(slot));
+            a.B_out[pos_a] = make_float4(wi.x, wi.y, wi.z, bt.x);
+            a.C_out[pos_a] = make_float2(bt.y, bt.z);
         }
         if (escaped) {
             a.esc[pos_e] = make_float4(eu, ev, __uint_as_float(slot), 0.0f);
@@ -670,26 +660,26 @@ static int grid_for(int64_t n, int block, int per_sm) {
 void launch_raygen(const Cam32& cam, int W, int H, int first_sample, int n_slots, uint64_t seed, Workspace& ws,
                    cudaStream_t st) {
     const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
-    raygen_kernel<<<grid_for(n_slots, 256, 8), 256, 0, st>>>(cam, W, H, first_sample, n_slots, key, ws.ray_o,
-                                                             ws.ray_d, ws.beta);
+    raygen_kernel<<<grid_for(n_slots, 256, 8), 256, 0, st>>>(cam, W, H, first_sample, n_slots, key, ws.rayA[0],
+                                                             ws.rayB[0], ws.rayC[0]);
 }
 
-void launch_traverse(const TraceParams& tp, const uint32_t* queue_in, const uint32_t* count_in, int identity,
-                     Workspace& ws, cudaStream_t st) {
-    traverse_kernel<<<num_sms() * 8, 128, 0, st>>>(tp, queue_in, count_in, identity, ws.ray_o, ws.ray_d, ws.hit);
+void launch_traverse(const TraceParams& tp, int buf, const uint32_t* count_in, Workspace& ws, cudaStream_t st) {
+    traverse_kernel<<<num_sms() * 8, 128, 0, st>>>(tp, count_in, ws.rayA[buf], ws.rayB[buf], ws.hit);
 }
 
 void launch_shade(const TraceParams& tp, int W, int H, int first_sample, int depth, int max_depth, uint64_t seed,
-                  const uint32_t* queue_in, const uint32_t* count_in, int identity, uint32_t* queue_out,
-                  uint32_t* count_out, int use_nif, float3 env, Workspace& ws, cudaStream_t st) {
+                  int buf, const uint32_t* count_in, uint32_t* count_out, int use_nif, float3 env, Workspace& ws,
+                  cudaStream_t st) {
     ShadeArgs a;
     a.tp = tp;
     a.W = W; a.H = H; a.first_sample = first_sample; a.depth = depth; a.max_depth = max_depth;
     a.key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
-    a.q_in = queue_in; a.cnt_in = count_in; a.identity = identity;
-    a.q_out = queue_out; a.cnt_out = count_out; a.cnt_esc = ws.counters + kCounterEsc;
+    a.cnt_in = count_in; a.cnt_out = count_out; a.cnt_esc = ws.counters + kCounterEsc;
     a.use_nif = use_nif; a.env = env;
-    a.ray_o = ws.ray_o; a.ray_d = ws.ray_d; a.beta = ws.beta; a.hit = ws.hit;
+    a.A_in = ws.rayA[buf]; a.B_in = ws.rayB[buf]; a.C_in = ws.rayC[buf];
+    a.A_out = ws.rayA[buf ^ 1]; a.B_out = ws.rayB[buf ^ 1]; a.C_out = ws.rayC[buf ^ 1];
+    a.hit = ws.hit;
     a.esc = ws.esc; a.esc_beta = ws.esc_beta; a.wave_buf = ws.wave_buf;
     shade_kernel<<<num_sms() * 8, 256, 0, st>>>(a);
 }
