@@ -292,9 +292,8 @@ def main():
     nif_ms = kt["nif"]
     infers = escaped
     kernels = {
-        "traverse": {"ms_per_step": kt["traverse"] / K, "launches_per_step": trav_launches / K,
-                     "bytes_alg": (4 + 32 + 16) * segments},
-        "shade": {"ms_per_step": kt["shade"] / K, "bytes_alg": 120 * segments},
+        "trace_shade": {"ms_per_step": kt["traverse"] / K, "launches_per_step": trav_launches / K,
+                        "bytes_alg": 80 * segments},
         "nif": {"ms_per_step": nif_ms / K, "launches_per_step": nif_launches / K,
                 "flops_alg": HIDDEN_FLOP_PER_INF * infers},
         "raygen": {"ms_per_step": kt["raygen"] / K, "bytes_alg": 48 * paths},
@@ -307,8 +306,8 @@ def main():
                 "kernel": "nif_fused_kernel", "flop_per_inference": HIDDEN_FLOP_PER_INF,
                 "inferences_per_launch": infers / max(1, nif_launches),
                 "peak_source": peaks["source"] + " bf16 sustained (fp16 same rate)"}
-    if dominant in ("traverse", "shade", "raygen"):
-        ms_k = kt[dominant if dominant != "raygen" else "raygen"]
+    if dominant in ("trace_shade", "raygen"):
+        ms_k = kt["traverse" if dominant == "trace_shade" else "raygen"]
         byts = kernels[dominant]["bytes_alg"]
         gbs = byts / (ms_k / 1e3) / 1e9 if ms_k > 0 else 0.0
         roof = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",

@@ -51,8 +51,8 @@ void free_path_state(pt::Workspace& ws) {
         ws.rayA[b] = ws.rayB[b] = nullptr;
         ws.rayC[b] = nullptr;
     }
-    cudaFree(ws.hit); cudaFree(ws.esc); cudaFree(ws.esc_beta); cudaFree(ws.wave_buf);
-    ws.hit = nullptr; ws.esc = ws.esc_beta = nullptr; ws.wave_buf = nullptr;
+    cudaFree(ws.esc); cudaFree(ws.esc_beta); cudaFree(ws.wave_buf);
+    ws.esc = ws.esc_beta = nullptr; ws.wave_buf = nullptr;
 }
 
 void free_ws(pt::Workspace& ws) {
@@ -79,7 +79,6 @@ int ensure_ws(pt::Workspace& ws, int64_t cap) {
         CU(cudaMalloc(&ws.rayB[b], sizeof(float4) * cap));
         CU(cudaMalloc(&ws.rayC[b], sizeof(float2) * cap));
     }
-    CU(cudaMalloc(&ws.hit, sizeof(float2) * cap));
     CU(cudaMalloc(&ws.esc, sizeof(float4) * cap));
     CU(cudaMalloc(&ws.esc_beta, sizeof(float4) * cap));
     CU(cudaMalloc(&ws.wave_buf, sizeof(float) * 3 * cap));
@@ -185,13 +184,10 @@ int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, i
         for (int d = 1; d <= max_depth; ++d) {
             const int buf = (d - 1) & 1;       // bounce d reads state buffer buf, shade writes buf ^ 1
             tm.begin(T_TRAVERSE, &e0);
-            pt::launch_traverse(tp, buf, ws.counters + (d - 1), ws, st);
+            pt::launch_trace_shade(tp, W, H, (int)w0, d, max_depth, seed, buf, ws.counters + (d - 1),
+                                   ws.counters + d, use_nif, env, ws, st);
             tm.end(T_TRAVERSE, e0);
-            tm.begin(T_SHADE, &e0);
-            pt::launch_shade(tp, W, H, (int)w0, d, max_depth, seed, buf, ws.counters + (d - 1), ws.counters + d,
-                             use_nif, env, ws, st);
-            tm.end(T_SHADE, e0);
-            stats.launches += 2;
+            stats.launches += 1;
             stats.traverse_launches += 1;
         }
         if (use_nif) {

@@ -59,7 +59,6 @@ struct Workspace {
     float4* rayA[2] = {nullptr, nullptr};   // (o.xyz, slot bits)
     float4* rayB[2] = {nullptr, nullptr};   // (d.xyz, beta.x)
     float2* rayC[2] = {nullptr, nullptr};   // (beta.y, beta.z)
-    float2* hit = nullptr;     // [cap] per queue entry: (t, prim bits)
     float4* esc = nullptr;     // [cap] escaped-ray queue: (u, v, slot bits, 0)
     float4* esc_beta = nullptr;// [cap] escaped-ray throughput
     float* wave_buf = nullptr; // [cap][3] radiance per slot, written exactly once per path
@@ -128,8 +127,7 @@ struct TraceParams {
 // kernel launchers (trace_kernels.cu)
 void launch_raygen(const Cam32& cam, int W, int H, int first_sample, int n_slots, uint64_t seed, Workspace& ws,
                    cudaStream_t st);
-void launch_traverse(const TraceParams& tp, int buf, const uint32_t* count_in, Workspace& ws, cudaStream_t st);
-void launch_shade(const TraceParams& tp, int W, int H, int first_sample, int depth, int max_depth, uint64_t seed,
+void launch_trace_shade(const TraceParams& tp, int W, int H, int first_sample, int depth, int max_depth, uint64_t seed,
                   int buf, const uint32_t* count_in, uint32_t* count_out, int use_nif, float3 env, Workspace& ws,
                   cudaStream_t st);
 void launch_accumulate(const float* wave_buf, int n_pix, int k, float* fb, cudaStream_t st);

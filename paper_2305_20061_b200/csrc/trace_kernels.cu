@@ -403,17 +403,6 @@ __global__ void __launch_bounds__(256) raygen_kernel(Cam32 cam, int W, int H, in
     }
 }
 
-__global__ void __launch_bounds__(128) traverse_kernel(TraceParams tp, const uint32_t* __restrict__ cnt_in,
-                                                       const float4* __restrict__ A, const float4* __restrict__ B,
-                                                       float2* __restrict__ hit) {
-    const uint32_t n = *cnt_in;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const float4 o = __ldg(A + i), d = __ldg(B + i);
-        const Hit h = closest_hit(tp, make_float3(o.x, o.y, o.z), make_float3(d.x, d.y, d.z));
-        hit[i] = make_float2((float)h.t, __int_as_float(h.prim));
-    }
-}
-
 __device__ __forceinline__ void equirect_f32(float3 d, float& u, float& v) {
     // SPEC.md:438 convention (reading R14): u = 0.5 + atan2(d.x, -d.z)/2pi wrapped to [0,1); v = acos(d.y)/pi
     const float len = sqrtf(d.x * d.x + d.y * d.y + d.z * d.z);
@@ -455,13 +444,15 @@ struct ShadeArgs {
     float4* A_out;
     float4* B_out;
     float2* C_out;
-    const float2* hit;
     float4* esc;
     float4* esc_beta;
     float* wave_buf;
 };
 
-__global__ void __launch_bounds__(256) shade_kernel(ShadeArgs a) {
+// One bounce of the wavefront for every live path: closest hit over the wide BVH (S2), then emission,
+// BSDF sampling, Russian roulette (S3) and warp-aggregated compaction into the next live queue or
+// the escaped-ray queue of the NIF (S4). Fused so the path state is read once and written once.
+__global__ void __launch_bounds__(128) trace_shade_kernel(ShadeArgs a) {
     const uint32_t n = *a.cnt_in;
     const int np = a.W * a.H;
     const uint32_t stride = gridDim.x * blockDim.x;
@@ -474,10 +465,10 @@ __global__ void __launch_bounds__(256) shade_kernel(ShadeArgs a) {
         float3 o3 = make_float3(0, 0, 0), wi = make_float3(0, 0, 0), bt = make_float3(0, 0, 0);
         float eu = 0.0f, ev = 0.0f;
         if (active) {
-            const float2 hv = __ldg(a.hit + i);
-            const int32_t prim = __float_as_int(hv.y);
             const float4 o = __ldg(a.A_in + i), d4 = __ldg(a.B_in + i);
             const float2 c2 = __ldg(a.C_in + i);
+            const Hit hh = closest_hit(a.tp, make_float3(o.x, o.y, o.z), make_float3(d4.x, d4.y, d4.z));
+            const int32_t prim = hh.prim;
             slot = __float_as_uint(o.w);
             const float3 d = make_float3(d4.x, d4.y, d4.z);
             bt = make_float3(d4.w, c2.x, c2.y);
@@ -492,7 +483,7 @@ __global__ void __launch_bounds__(256) shade_kernel(ShadeArgs a) {
                     L = make_float3(bt.x * a.env.x, bt.y * a.env.y, bt.z * a.env.z);
                 }
             } else {
-                const float t = hv.x;
+                const float t = (float)hh.t;
                 const float3 P = make_float3(fmaf(t, d.x, o.x), fmaf(t, d.y, o.y), fmaf(t, d.z, o.z));
                 float3 ng;
                 uint32_t mi;
@@ -664,11 +655,15 @@ void launch_raygen(const Cam32& cam, int W, int H, int first_sample, int n_slots
                                                              ws.rayB[0], ws.rayC[0]);
 }
 
-void launch_traverse(const TraceParams& tp, int buf, const uint32_t* count_in, Workspace& ws, cudaStream_t st) {
-    traverse_kernel<<<num_sms() * 8, 128, 0, st>>>(tp, count_in, ws.rayA[buf], ws.rayB[buf], ws.hit);
+// persistent grids: exactly the resident block count (one wave), so no SM idles behind a partial wave
+template <typename K>
+static int resident_grid(K kernel, int block) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0);
+    return num_sms() * (per_sm > 0 ? per_sm : 1);
 }
 
-void launch_shade(const TraceParams& tp, int W, int H, int first_sample, int depth, int max_depth, uint64_t seed,
+void launch_trace_shade(const TraceParams& tp, int W, int H, int first_sample, int depth, int max_depth, uint64_t seed,
                   int buf, const uint32_t* count_in, uint32_t* count_out, int use_nif, float3 env, Workspace& ws,
                   cudaStream_t st) {
     ShadeArgs a;
@@ -679,9 +674,9 @@ void launch_shade(const TraceParams& tp, int W, int H, int first_sample, int dep
     a.use_nif = use_nif; a.env = env;
     a.A_in = ws.rayA[buf]; a.B_in = ws.rayB[buf]; a.C_in = ws.rayC[buf];
     a.A_out = ws.rayA[buf ^ 1]; a.B_out = ws.rayB[buf ^ 1]; a.C_out = ws.rayC[buf ^ 1];
-    a.hit = ws.hit;
     a.esc = ws.esc; a.esc_beta = ws.esc_beta; a.wave_buf = ws.wave_buf;
-    shade_kernel<<<num_sms() * 8, 256, 0, st>>>(a);
+    static const int grid = resident_grid(trace_shade_kernel, 128);
+    trace_shade_kernel<<<grid, 128, 0, st>>>(a);
 }
 
 void launch_accumulate(const float* wave_buf, int n_pix, int k, float* fb, cudaStream_t st) {
