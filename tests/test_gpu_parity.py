@@ -190,3 +190,49 @@ def test_render_deterministic_and_wave_invariant(ptm, blob):
     torch.cuda.synchronize()
     d = acc.cpu().numpy().reshape(a.shape) / 4
     assert np.allclose(d, a, rtol=1e-6, atol=1e-7)
+
+
+def _rows_pix(c, n_rows):
+    rows = np.linspace(0, c.height - 1, n_rows).astype(np.int64)
+    return (rows[:, None] * c.width + np.arange(c.width)[None, :]).reshape(-1).astype(np.int64)
+
+
+@pytest.mark.parametrize("cfg,n_rows", [(2, 12), (3, 6), (4, 4)])
+def test_render_full_size_rows_vs_oracle(ptm, orc, blob, cfg, n_rows):
+    """Configs 2-4 at full resolution and full spp (config 4: 5.08 M triangles, constant env);
+    the oracle evaluates evenly spaced full rows of the same frame."""
+    c = scenes.CONFIGS[cfg]
+    sc = scenes.scene_for_config(cfg)
+    nif = ptm.Nif(blob) if c.use_nif else None
+    img = ptm.render(ptm.Scene(sc), nif, c.width, c.height, c.spp, c.max_depth, seed=c.seed,
+                     env_rgb=None if c.use_nif else c.env_rgb)
+    pix = _rows_pix(c, n_rows)
+    ref, _ = orc.OracleScene(sc).render(c.width, c.height, c.max_depth, c.seed, pix=pix, s0=0, s1=c.spp,
+                                        nif_blob=blob if c.use_nif else None, env_rgb=c.env_rgb)
+    got = img.reshape(-1, 3)[pix].astype(np.float64)
+    rel = _rel_rmse(got, ref / c.spp)
+    assert rel <= REL_RMSE_GATE, rel
+
+
+@pytest.mark.parametrize("W,H,spp,depth", [(1, 1, 1, 1), (7, 3, 1, 1), (33, 17, 3, 2), (64, 64, 5, 12)])
+def test_render_edge_sizes(ptm, orc, blob, W, H, spp, depth):
+    """Odd/tiny frames, single sample, depth 1 (direct only) and a deep cap: exact agreement in the
+    direct-only case (primary hits are bit-exact, NIF within its gate), rel-RMSE otherwise."""
+    sc = scenes.box_scene()
+    img = ptm.render(ptm.Scene(sc), ptm.Nif(blob), W, H, spp, depth, seed=11)
+    ref, _ = orc.OracleScene(sc).render(W, H, depth, 11, s0=0, s1=spp, nif_blob=blob)
+    ref = ref.reshape(H, W, 3) / spp
+    assert np.isfinite(img).all()
+    assert _rel_rmse(img, ref) <= REL_RMSE_GATE
+    if depth == 1:
+        assert np.allclose(img, ref, rtol=1e-2, atol=1e-6)
+
+
+def test_invalid_arguments_raise(ptm, blob):
+    s = ptm.Scene(scenes.box_scene())
+    with pytest.raises(ptm.PtError):
+        ptm.render(s, ptm.Nif(blob), 0, 4, 1, 1)
+    with pytest.raises(ptm.PtError):
+        ptm.render(s, ptm.Nif(blob), 4, 4, 1, 0)
+    with pytest.raises(ptm.PtError):
+        ptm.Nif(blob[:-1])
