@@ -325,12 +325,11 @@ int build_wide_bvh(const pt_triangle* tris, int64_t n_tris, const pt_sphere* sph
                 off += kNodeUnits;
             }
         }
-        // pack the 4 x 12-B child records into units 1..3 (= 12 uint16 pairs)
-        uint16_t flat[24];
-        for (int ci = 0; ci < 4; ++ci)
-            for (int k = 0; k < 6; ++k) flat[6 * ci + k] = q[ci][k];
+        // pack the 4 x 12-B child records into units 1..3: one word per axis, (lo | hi << 16), so the
+        // kernel decodes both bounds of an axis with one packed fp16x2 -> fp32x2 conversion
         uint32_t words[12];
-        for (int w = 0; w < 12; ++w) words[w] = (uint32_t)flat[2 * w] | ((uint32_t)flat[2 * w + 1] << 16);
+        for (int ci = 0; ci < 4; ++ci)
+            for (int a = 0; a < 3; ++a) words[3 * ci + a] = (uint32_t)q[ci][a] | ((uint32_t)q[ci][3 + a] << 16);
         pool[pnd.unit + 1] = make_uint4(words[0], words[1], words[2], words[3]);
         pool[pnd.unit + 2] = make_uint4(words[4], words[5], words[6], words[7]);
         pool[pnd.unit + 3] = make_uint4(words[8], words[9], words[10], words[11]);

@@ -16,7 +16,7 @@ namespace pt {
 // Wide BVH, device layout:
 //   a pool of 16-byte units. An interior node is 4 units (64 B, 64-B aligned):
 //     unit 0: float O.x, O.y, O.z (node origin = box min, fp32), uint32 base (unit index of the child block)
-//     units 1-3: 4 child boxes x 12 B: f16 lo.x, lo.y, lo.z, hi.x, hi.y, hi.z = offsets from O,
+//     units 1-3: 4 child boxes x 12 B: words (lo.x|hi.x) (lo.y|hi.y) (lo.z|hi.z), f16 offsets from O,
 //                lo rounded down / hi rounded up so fp32(O + lo) <= exact lo, fp32(O + hi) >= exact hi
 //                (the paper's "round-to-nearest-not-lower", made exact for the decode).
 //                The offsets are >= 0, so their sign bits carry the child meta:

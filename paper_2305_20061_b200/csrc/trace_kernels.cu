@@ -200,6 +200,35 @@ __device__ __forceinline__ bool sph_test64(RayT& r, float3 c, float rad, double&
     return false;
 }
 
+// Certified fp32 ray/sphere test (same contract as tri_test32): with a = d.d, q = |oc|^2 + r^2 the
+// discriminant carries |d disc| <= 24 eps a q (we use 32), b <= 5 eps |oc||d|, and the roots inherit
+// |dt| <= (db + d sqrt(disc)) / a + 5 eps |t|. Grazing rays and roots near 0 defer to fp64.
+__device__ __forceinline__ int sph_test32(const RayT& r, float3 c, float rad, float& t, float& dt) {
+    constexpr float eps = 0x1p-24f;
+    const float ox = r.o[0] - c.x, oy = r.o[1] - c.y, oz = r.o[2] - c.z;
+    const float a = fmaf(r.d[0], r.d[0], fmaf(r.d[1], r.d[1], r.d[2] * r.d[2]));
+    const float b = fmaf(ox, r.d[0], fmaf(oy, r.d[1], oz * r.d[2]));
+    const float oc2 = fmaf(ox, ox, fmaf(oy, oy, oz * oz));
+    const float cc = oc2 - rad * rad;
+    const float disc = fmaf(b, b, -a * cc);
+    const float q = oc2 + rad * rad;
+    const float ddisc = (32.0f * eps) * a * q;
+    if (disc < -ddisc) return 0;
+    if (disc <= ddisc) return 2;
+    const float sq = sqrtf(disc);
+    const float dsq = ddisc / (sqrtf(disc - ddisc) + sq) + 2.0f * eps * sq;
+    const float db = (5.0f * eps) * sqrtf(oc2 * a);
+    const float ia = 1.0f / a;
+    const float t0 = (-b - sq) * ia, t1 = (-b + sq) * ia;
+    const float e0 = (db + dsq) * ia + (5.0f * eps) * fabsf(t0);
+    const float e1 = (db + dsq) * ia + (5.0f * eps) * fabsf(t1);
+    if (t0 - e0 > 0.0f) { t = t0; dt = 1.25f * e0; return 1; }
+    if (t0 + e0 > 0.0f) return 2;                 // smaller root near 0: undecided
+    if (t1 - e1 > 0.0f) { t = t1; dt = 1.25f * e1; return 1; }
+    if (t1 + e1 > 0.0f) return 2;
+    return 0;
+}
+
 // ---------------------------------------------------------------------------------------------
 // Wide-BVH closest hit: (t, id) lexicographic minimum over all primitives (reading R11)
 // ---------------------------------------------------------------------------------------------
@@ -243,8 +272,14 @@ __device__ __forceinline__ void test_prim(const uint4* __restrict__ pool, uint32
     float t32 = 0.0f, dt = 0.0f;
     bool exact;
     if (idw & kSphereFlag) {
-        if (!sph_test64(r, p0, __uint_as_float(u1.x), t64)) return;
-        exact = true;
+        const int c = sph_test32(r, p0, __uint_as_float(u1.x), t32, dt);
+        if (c == 0) return;
+        if (c == 2) {
+            if (!sph_test64(r, p0, __uint_as_float(u1.x), t64)) return;
+            exact = true;
+        } else {
+            exact = false;
+        }
     } else {
         const uint4 u2 = __ldg(pool + unit + 2);
         const float3 p1 = make_float3(__uint_as_float(u1.x), __uint_as_float(u1.y), __uint_as_float(u1.z));
@@ -322,20 +357,20 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
             lu[ci] = off;
             const uint32_t w0 = w[3 * ci], w1 = w[3 * ci + 1], w2 = w[3 * ci + 2];
             const bool valid = (w0 & 0x8000u) != 0;
-            const bool leaf = (w0 & 0x80000000u) != 0;
-            const uint32_t cnt = (((w1 >> 15) & 1u) | ((w1 >> 30) & 2u)) + 1u;
-            const float lo[3] = {half_bits_to_float(w0), half_bits_to_float(w0 >> 16), half_bits_to_float(w1)};
-            const float hi[3] = {half_bits_to_float(w1 >> 16), half_bits_to_float(w2), half_bits_to_float(w2 >> 16)};
+            const bool leaf = (w1 & 0x8000u) != 0;
+            const uint32_t cnt = (((w2 >> 15) & 1u) | ((w0 >> 30) & 2u)) + 1u;
+            const uint32_t wa[3] = {w0 & 0x7FFF7FFFu, w1 & 0x7FFF7FFFu, w2 & 0x7FFF7FFFu};
             float tn = 0.0f, tf = CUDART_INF_F;
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-                const float bl = __fadd_rn(O[a], lo[a]);
-                const float bh = __fadd_rn(O[a], hi[a]);
-                const float t0 = __fmul_rn(__fsub_rn(bl, r.o[a]), r.inv[a]);
-                const float t1 = __fmul_rn(__fsub_rn(bh, r.o[a]), r.inv[a]);
+                // (lo, hi) of this axis: exact fp16 -> fp32, then the same rn ops as the builder's check
+                const float2 lh = __half22float2(*reinterpret_cast<const __half2*>(&wa[a]));
+                const float2 b = __fadd2_rn(make_float2(O[a], O[a]), lh);
+                const float2 t = __fmul2_rn(__fadd2_rn(b, make_float2(-r.o[a], -r.o[a])),
+                                            make_float2(r.inv[a], r.inv[a]));
                 const bool ng = (r.negmask >> a) & 1u;
-                tn = fmaxf(tn, ng ? t1 : t0);
-                tf = fminf(tf, ng ? t0 : t1);
+                tn = fmaxf(tn, ng ? t.y : t.x);
+                tf = fminf(tf, ng ? t.x : t.y);
             }
             tf = tf * kGrow;
             const bool hit = valid && tn <= tf && tn <= tcull0;
@@ -379,6 +414,12 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
             if (__uint_as_float(e.y) <= tcull) { cur = e.x; found = true; break; }
         }
         if (!found) break;
+    }
+    // the fp32 sphere t can lose ~1e-5 (disc cancellation): refine the winner's t in fp64 so the
+    // spawn point stays well inside the 1e-4 self-intersection offset (reading R10)
+    if (best.prim >= 0 && !best.exact && best.prim >= (int32_t)tp.n_tris) {
+        double t64;
+        if (exact_test(pool, best.unit, r, t64)) best.t = t64;
     }
     return best;
 }

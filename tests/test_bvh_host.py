@@ -61,9 +61,9 @@ def _check_pool(sc, pool):
             w0, w1, w2 = int(words[3 * ci]), int(words[3 * ci + 1]), int(words[3 * ci + 2])
             if not (w0 & 0x8000):
                 continue
-            leaf = bool(w0 & 0x80000000)
-            cnt = (((w1 >> 15) & 1) | ((w1 >> 30) & 2)) + 1
-            qs = [w0, w0 >> 16, w1, w1 >> 16, w2, w2 >> 16]
+            leaf = bool(w1 & 0x8000)
+            cnt = (((w2 >> 15) & 1) | ((w0 >> 30) & 2)) + 1
+            qs = [w0, w1, w2, w0 >> 16, w1 >> 16, w2 >> 16]      # lo.x lo.y lo.z hi.x hi.y hi.z
             dlo = np.array([np.float32(O[a] + _f16(qs[a])) for a in range(3)], np.float64)
             dhi = np.array([np.float32(O[a] + _f16(qs[3 + a])) for a in range(3)], np.float64)
             if leaf:
