@@ -33,6 +33,10 @@ from paper_2305_20061_b200 import scenes  # noqa: E402
 HIDDEN_FLOP_PER_INF = 3 * 2 * 128 * 128          # tensor-counted FLOPs per NIF inference
 TOTAL_FLOP_PER_INF = 2 * (2 * 128 + 3 * 128 * 128 + 128 * 3)
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+L2_READ_GBS = 16409.6                       # tools/l2_bench.cu on this pool's B200 (profiles/round1/l2_bench.json)
+# algorithmic traversal bytes per traced segment, per config (counting build: 64 B x node visits +
+# 48 B x primitive tests + 80 B path state; profiles/round1/trace_count.json)
+TRACE_BYTES_PER_SEGMENT = {1: 300.0}
 
 
 def load_peaks():
@@ -296,7 +300,7 @@ def main():
                         "bytes_alg": 80 * segments},
         "nif": {"ms_per_step": nif_ms / K, "launches_per_step": nif_launches / K,
                 "flops_alg": HIDDEN_FLOP_PER_INF * infers},
-        "raygen": {"ms_per_step": kt["raygen"] / K, "bytes_alg": 48 * paths},
+        "raygen": {"ms_per_step": kt["raygen"] / K, "bytes_alg": 40 * paths},
         "accumulate": {"ms_per_step": kt["accum"] / K},
     }
     dominant = max(kernels, key=lambda n: kernels[n]["ms_per_step"])
@@ -306,13 +310,24 @@ def main():
                 "kernel": "nif_fused_kernel", "flop_per_inference": HIDDEN_FLOP_PER_INF,
                 "inferences_per_launch": infers / max(1, nif_launches),
                 "peak_source": peaks["source"] + " bf16 sustained (fp16 same rate)"}
-    if dominant in ("trace_shade", "raygen"):
-        ms_k = kt["traverse" if dominant == "trace_shade" else "raygen"]
-        byts = kernels[dominant]["bytes_alg"]
+    if dominant == "trace_shade":
+        # traversal + shading: algorithmic L2 bytes per segment (counting build, tools/trace_count.py,
+        # profiles/round1/trace_count.json): node visits x 64 B + primitive tests x 48 B + 80 B of path
+        # state, against the measured L2 read bandwidth (tools/l2_bench.cu, profiles/round1/l2_bench.json)
+        ms_k = kt["traverse"]
+        byts = TRACE_BYTES_PER_SEGMENT.get(cfg.index, 300.0) * segments
         gbs = byts / (ms_k / 1e3) / 1e9 if ms_k > 0 else 0.0
+        roof = {"bound": "l2", "achieved": gbs, "peak": L2_READ_GBS, "unit": "GB/s", "frac": gbs / L2_READ_GBS,
+                "traffic": None, "kernel": "trace_shade_kernel",
+                "bytes_per_segment": TRACE_BYTES_PER_SEGMENT.get(cfg.index, 300.0),
+                "segments_per_launch": segments / max(1, trav_launches),
+                "peak_source": "measured L2 read bandwidth, tools/l2_bench.cu (MEASURED_PEAKS.json has none)",
+                "hbm_frac": (80.0 * segments / (ms_k / 1e3) / 1e9) / peaks["hbm_gbs"] if ms_k > 0 else 0.0}
+    elif dominant == "raygen":
+        ms_k = kt["raygen"]
+        gbs = 40 * paths / (ms_k / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": gbs / peaks["hbm_gbs"], "traffic": None, "kernel": f"{dominant}_kernel",
-                "peak_source": peaks["source"]}
+                "frac": gbs / peaks["hbm_gbs"], "traffic": None, "kernel": "raygen_kernel"}
     else:
         roof = nif_roof
     clocks = clk.summary()

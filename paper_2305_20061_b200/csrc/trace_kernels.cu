@@ -234,6 +234,14 @@ __device__ __forceinline__ int sph_test32(const RayT& r, float3 c, float rad, fl
 // ---------------------------------------------------------------------------------------------
 // Best hit so far. Decided exactly like the fp64 oracle, but carried as a certified fp32 interval
 // [tlo, thi] until a near-tie forces the exact fp64 t (exact == true).
+#ifdef PT_COUNT
+// counting build (tools/trace_count.py): node visits, box tests, primitive tests, fp64 tests, rays
+__device__ unsigned long long g_trav_count[8];
+#define TCOUNT(i, v) atomicAdd(&g_trav_count[i], (unsigned long long)(v))
+#else
+#define TCOUNT(i, v) do { } while (0)
+#endif
+
 struct Hit {
     double t;
     float tlo, thi;
@@ -271,6 +279,7 @@ __device__ __forceinline__ void test_prim(const uint4* __restrict__ pool, uint32
     double t64 = 0.0;
     float t32 = 0.0f, dt = 0.0f;
     bool exact;
+    TCOUNT(2, 1);
     if (idw & kSphereFlag) {
         const int c = sph_test32(r, p0, __uint_as_float(u1.x), t32, dt);
         if (c == 0) return;
@@ -287,6 +296,7 @@ __device__ __forceinline__ void test_prim(const uint4* __restrict__ pool, uint32
         const int c = tri_test32(r, p0, p1, p2, t32, dt);
         if (c == 0) return;
         if (c == 2) {
+            TCOUNT(3, 1);
             if (!tri_test64(r, p0, p1, p2, t64)) return;
             exact = true;
         } else {
@@ -338,7 +348,9 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
     int sp = 0;
     uint32_t cur = 0;
     const uint4* __restrict__ pool = tp.pool;
+    TCOUNT(4, 1);
     for (;;) {
+        TCOUNT(0, 1);
         const uint4 h = __ldg(pool + cur);
         const uint4 q0 = __ldg(pool + cur + 1), q1 = __ldg(pool + cur + 2), q2 = __ldg(pool + cur + 3);
         const uint32_t w[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
@@ -745,3 +757,14 @@ void launch_pack_queries(const float* uv, int64_t n, float4* esc, float4* esc_be
 }
 
 }  // namespace pt
+
+#ifdef PT_COUNT
+extern "C" __attribute__((visibility("default"))) int pt_debug_trav_counts(unsigned long long* host, int reset) {
+    cudaMemcpyFromSymbol(host, pt::g_trav_count, sizeof(pt::g_trav_count));
+    if (reset) {
+        unsigned long long z[8] = {0};
+        cudaMemcpyToSymbol(pt::g_trav_count, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

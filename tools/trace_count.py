@@ -1,0 +1,55 @@
+#!/usr/bin/env python
+"""Counting build (PT_COUNT): node visits and primitive tests per traced segment for the bench
+workload and the primary rays of configs 1-3, i.e. the algorithmic traversal bytes of SURVEY 8d:
+bytes/segment = visits * 64 B + prim tests * 48 B + 40 B state in + ~40 B state out."""
+import ctypes as C
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+lib = os.path.join(ROOT, "build/variants/libpt_count.so")
+if not os.path.exists(lib):
+    from paper_2305_20061_b200 import _build
+    _build.build(out=lib, defines=["PT_COUNT"])
+os.environ["PT_B200_LIB"] = lib
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2305_20061_b200 import pt, scenes  # noqa: E402
+
+L = pt.lib()
+L.pt_debug_trav_counts.argtypes = [C.c_void_p, C.c_int]
+
+
+def counts(reset=True):
+    h = np.zeros(8, np.uint64)
+    torch.cuda.synchronize()
+    L.pt_debug_trav_counts(C.c_void_p(h.ctypes.data), int(reset))
+    return {"node_visits": int(h[0]), "prim_tests": int(h[2]), "fp64_tests": int(h[3]), "rays": int(h[4])}
+
+
+out = {}
+for cfg in (1, 2, 3):
+    c = scenes.CONFIGS[cfg]
+    S = pt.Scene(scenes.scene_for_config(cfg))
+    counts()
+    pt.trace_primary(S, c.width, c.height, 0, 0)
+    k = counts()
+    k["per_ray"] = {"visits": k["node_visits"] / k["rays"], "prims": k["prim_tests"] / k["rays"],
+                    "fp64": k["fp64_tests"] / k["rays"]}
+    out[f"primary_c{cfg}"] = k
+# bench workload (config 1 render), all bounces
+c = scenes.CONFIGS[1]
+S = pt.Scene(scenes.scene_for_config(1))
+N = pt.Nif(scenes.siren_blob(0))
+acc = torch.zeros(c.width * c.height * 3, device="cuda")
+counts()
+pt.render_samples(S, N, c.width, c.height, 0, c.spp, c.max_depth, 0, acc, wave_samples=c.wave_samples)
+k = counts()
+k["per_segment"] = {"visits": k["node_visits"] / k["rays"], "prims": k["prim_tests"] / k["rays"],
+                    "fp64": k["fp64_tests"] / k["rays"]}
+k["alg_bytes_per_segment"] = 64 * k["per_segment"]["visits"] + 48 * k["per_segment"]["prims"] + 80
+out["render_c1"] = k
+print(json.dumps(out, indent=1))
