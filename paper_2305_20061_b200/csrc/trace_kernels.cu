@@ -505,7 +505,10 @@ struct ShadeArgs {
 // One bounce of the wavefront for every live path: closest hit over the wide BVH (S2), then emission,
 // BSDF sampling, Russian roulette (S3) and warp-aggregated compaction into the next live queue or
 // the escaped-ray queue of the NIF (S4). Fused so the path state is read once and written once.
-__global__ void __launch_bounds__(128) trace_shade_kernel(ShadeArgs a) {
+#ifndef PT_TS_MINB
+#define PT_TS_MINB 8   // min resident blocks per SM for trace_shade: 64-register cap; tools/ts_tune.sh on B200
+#endif
+__global__ void __launch_bounds__(128, PT_TS_MINB) trace_shade_kernel(ShadeArgs a) {
     const uint32_t n = *a.cnt_in;
     const int np = a.W * a.H;
     const uint32_t stride = gridDim.x * blockDim.x;
