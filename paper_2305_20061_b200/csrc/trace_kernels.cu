@@ -579,7 +579,7 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) trace_shade_kernel(ShadeArgs 
                         const float3 t1 = make_float3(1.0f + sg * n.x * n.x * aa, sg * bb, -sg * n.x);
                         const float3 t2 = make_float3(bb, sg + n.y * n.y * aa, -n.y);
                         float sphi, cphi;
-                        sincosf(2.0f * CUDART_PI_F * xi1, &sphi, &cphi);
+                        sincospif(2.0f * xi1, &sphi, &cphi);   // sin/cos(2 pi xi1), cheap exact-argument reduction
                         const float rho = sqrtf(xi0), c3 = sqrtf(1.0f - xi0);
                         const float c1 = rho * cphi, c2 = rho * sphi;
                         wi = make_float3(c1 * t1.x + c2 * t2.x + c3 * n.x, c1 * t1.y + c2 * t2.y + c3 * n.y,
