@@ -45,18 +45,52 @@ int check_device() {
 
 bool finite3(const float* v) { return std::isfinite(v[0]) && std::isfinite(v[1]) && std::isfinite(v[2]); }
 
-void free_path_state(pt::Workspace& ws) {
+// Path-state buffers (the large per-wave arrays) are pooled per device and shared by all scene handles:
+// re-creating a scene does not reallocate ~0.5 GB of wave state. Reuse across streams is ordered by
+// an event recorded after each render's last use (the next user's stream waits on it).
+struct PathPool {
+    std::mutex mu;
+    int64_t capacity = 0;
+    float4* rayA[2] = {nullptr, nullptr};
+    float4* rayB[2] = {nullptr, nullptr};
+    float2* rayC[2] = {nullptr, nullptr};
+    float4* esc = nullptr;
+    float4* esc_beta = nullptr;
+    float* wave_buf = nullptr;
+    cudaEvent_t last_use = nullptr;
+};
+
+PathPool& path_pool(int dev) {
+    static PathPool pools[64];
+    return pools[dev & 63];
+}
+
+int ensure_pool(PathPool& pp, int64_t cap) {
+    if (!pp.last_use) CU(cudaEventCreateWithFlags(&pp.last_use, cudaEventDisableTiming));
+    if (cap <= pp.capacity) return PT_OK;
+    CU(cudaEventSynchronize(pp.last_use));           // no render may still use the old buffers
     for (int b = 0; b < 2; ++b) {
-        cudaFree(ws.rayA[b]); cudaFree(ws.rayB[b]); cudaFree(ws.rayC[b]);
-        ws.rayA[b] = ws.rayB[b] = nullptr;
-        ws.rayC[b] = nullptr;
+        cudaFree(pp.rayA[b]); cudaFree(pp.rayB[b]); cudaFree(pp.rayC[b]);
+        pp.rayA[b] = pp.rayB[b] = nullptr;
+        pp.rayC[b] = nullptr;
     }
-    cudaFree(ws.esc); cudaFree(ws.esc_beta); cudaFree(ws.wave_buf);
-    ws.esc = ws.esc_beta = nullptr; ws.wave_buf = nullptr;
+    cudaFree(pp.esc); cudaFree(pp.esc_beta); cudaFree(pp.wave_buf);
+    pp.esc = pp.esc_beta = nullptr;
+    pp.wave_buf = nullptr;
+    pp.capacity = 0;
+    for (int b = 0; b < 2; ++b) {
+        CU(cudaMalloc(&pp.rayA[b], sizeof(float4) * cap));
+        CU(cudaMalloc(&pp.rayB[b], sizeof(float4) * cap));
+        CU(cudaMalloc(&pp.rayC[b], sizeof(float2) * cap));
+    }
+    CU(cudaMalloc(&pp.esc, sizeof(float4) * cap));
+    CU(cudaMalloc(&pp.esc_beta, sizeof(float4) * cap));
+    CU(cudaMalloc(&pp.wave_buf, sizeof(float) * 3 * cap));
+    pp.capacity = cap;
+    return PT_OK;
 }
 
 void free_ws(pt::Workspace& ws) {
-    free_path_state(ws);
     cudaFree(ws.counters);
     cudaFree(ws.fb);
     cudaFree(ws.d_stats);
@@ -64,25 +98,14 @@ void free_ws(pt::Workspace& ws) {
     ws = pt::Workspace();
 }
 
-int ensure_ws(pt::Workspace& ws, int64_t cap) {
+// per-scene small state: counters, stats, scratch framebuffer stream
+int ensure_ws(pt::Workspace& ws) {
     if (!ws.counters) {
         CU(cudaMalloc(&ws.counters, sizeof(uint32_t) * pt::kCounters));
         CU(cudaMalloc(&ws.d_stats, sizeof(unsigned long long) * 4));
         CU(cudaMemset(ws.d_stats, 0, sizeof(unsigned long long) * 4));
         CU(cudaStreamCreateWithFlags(&ws.own_stream, cudaStreamNonBlocking));
     }
-    if (cap <= ws.capacity) return PT_OK;
-    free_path_state(ws);
-    ws.capacity = 0;
-    for (int b = 0; b < 2; ++b) {
-        CU(cudaMalloc(&ws.rayA[b], sizeof(float4) * cap));
-        CU(cudaMalloc(&ws.rayB[b], sizeof(float4) * cap));
-        CU(cudaMalloc(&ws.rayC[b], sizeof(float2) * cap));
-    }
-    CU(cudaMalloc(&ws.esc, sizeof(float4) * cap));
-    CU(cudaMalloc(&ws.esc_beta, sizeof(float4) * cap));
-    CU(cudaMalloc(&ws.wave_buf, sizeof(float) * 3 * cap));
-    ws.capacity = cap;
     return PT_OK;
 }
 
@@ -160,9 +183,23 @@ int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, i
     if (k <= 0) k = std::max<int64_t>(1, std::min<int64_t>(n_samples, (int64_t)(8 << 20) / np));
     k = std::min<int64_t>(k, n_samples);
     while (k > 1 && k * np > (1ll << 31)) --k;
-    int rc = ensure_ws(sc->ws, k * np);
+    int rc = ensure_ws(sc->ws);
     if (rc) return rc;
+    PathPool& pp = path_pool(sc->device);
+    std::lock_guard<std::mutex> pool_lock(pp.mu);
+    rc = ensure_pool(pp, k * np);
+    if (rc) return rc;
+    CU(cudaStreamWaitEvent(st, pp.last_use, 0));   // previous user of the pooled buffers is done
     pt::Workspace& ws = sc->ws;
+    for (int b = 0; b < 2; ++b) {
+        ws.rayA[b] = pp.rayA[b];
+        ws.rayB[b] = pp.rayB[b];
+        ws.rayC[b] = pp.rayC[b];
+    }
+    ws.esc = pp.esc;
+    ws.esc_beta = pp.esc_beta;
+    ws.wave_buf = pp.wave_buf;
+    ws.capacity = pp.capacity;
     unsigned long long* d_stats = ws.d_stats;
     CU(cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * 4, st));
     const pt::Cam32 cam = pt::make_cam32(sc->cam, W, H);
@@ -206,6 +243,7 @@ int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, i
         stats.waves += 1;
     }
     CU(cudaGetLastError());
+    CU(cudaEventRecord(pp.last_use, st));
     sc->stats = stats;   // kernel times and paths/segments/escaped are resolved by pt_get_stats
     return PT_OK;
 }
@@ -398,7 +436,7 @@ int pt_render(const pt_scene* scene, const pt_nif* nif, const float env_rgb[3], 
     if (width < 1 || height < 1 || spp < 1 || max_depth < 1) return fail(PT_ERR_INVALID_ARG, "W, H, spp, max_depth >= 1");
     pt_scene* sc = const_cast<pt_scene*>(scene);
     std::lock_guard<std::mutex> lk(sc->mu);
-    int rc = ensure_ws(sc->ws, 1);
+    int rc = ensure_ws(sc->ws);
     if (rc) return rc;
     const int64_t n = (int64_t)width * height * 3;
     if (sc->ws.fb_capacity < n) {
