@@ -12,6 +12,8 @@ Parity status per function:
   camera_rays       pinned: centre-pixel/forward-axis identity, corner symmetry
   equirect          pinned: SPEC.md:441-443 worked values, inverse round trip
   nif_eval          pinned: zero net (exp(b5)), hand-computed one-unit nets, torch.float64 full SIREN
+  fr_eval           pinned: zero net (M b4), single-frequency closed form through the concat skip,
+                    torch.float64 full network (the paper's Fourier/ReLU/YUV NIF, reading R4)
   scatter           pinned: cosine moments E[cos]=2/3, E[cos^2]=1/2; mirror; Fresnel(0)=0.04; Snell; TIR
   render            pinned: furnace 1 (empty scene == c exactly), furnace 2 (convex sphere == rho*c),
                     furnace 3 (dielectric: L in {0, c}), emitter front/back, RR unbiasedness
@@ -62,6 +64,7 @@ def lib():
             L.orc_roulette.restype = C.c_int
             L.orc_roulette.argtypes = [P, I32, D]
             L.orc_nif_eval.argtypes = [P, P, I64, P]
+            L.orc_fr_eval.argtypes = [P, P, I64, P]
             L.orc_scatter.argtypes = [C.c_int, P, P, D, P, P, P, P]
             L.orc_render.restype = C.c_int
             L.orc_render.argtypes = [P, P, P, I32, I32, I32, U64, P, I64, I32, I32, I32, P, P]
@@ -184,6 +187,15 @@ def nif_eval(blob, uv):
     uv = np.ascontiguousarray(uv, dtype=np.float64).reshape(-1, 2)
     y = np.empty((uv.shape[0], 3), np.float64)
     lib().orc_nif_eval(_p(blob), _p(uv), uv.shape[0], _p(y))
+    return y
+
+
+def fr_eval(blob, uv):
+    """The paper's Fourier/ReLU/YUV NIF in fp64: RGB log radiance [n][3] (env = exp)."""
+    blob = np.ascontiguousarray(blob, dtype=np.uint16)
+    uv = np.ascontiguousarray(uv, dtype=np.float64).reshape(-1, 2)
+    y = np.empty((uv.shape[0], 3), np.float64)
+    lib().orc_fr_eval(_p(blob), _p(uv), uv.shape[0], _p(y))
     return y
 
 

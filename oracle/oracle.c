@@ -565,6 +565,64 @@ EXPORT void orc_nif_eval(const uint16_t* blob, const double* uv, int64_t n, doub
     nif_free(&net);
 }
 
+/* The paper's own NIF (reading R4): Fourier features of x = (u, v),
+   gamma = [sin(2 pi B x) (20), cos(2 pi B x) (20)]; h0 = relu(W0 gamma + b0) (128); h1 = relu(W1 h0 + b1)
+   (88); h2 = relu(W2 [h1, gamma] + b2) (concat skip, 128); h3 = relu(W3 h2 + b3); yuv = W4 h3 + b4;
+   rgb_log = M yuv with M the fixed BT.601 YUV->RGB matrix. Returns rgb_log (the env is exp). */
+static const int FR_IN[5] = {40, 128, 128, 128, 128};
+static const int FR_OUT[5] = {128, 88, 128, 128, 3};
+
+static void fr_eval(const double* B, double* const W[5], double* const b[5], double u, double v, double y[3]) {
+    const double PI = 3.14159265358979323846;
+    double g[40], a[128], h[128];
+    for (int j = 0; j < 20; ++j) {
+        double p = 2.0 * PI * (B[2 * j] * u + B[2 * j + 1] * v);
+        g[j] = sin(p);
+        g[20 + j] = cos(p);
+    }
+    memcpy(a, g, sizeof(double) * 40);
+    for (int l = 0; l < 4; ++l) {
+        int fi = FR_IN[l], fo = FR_OUT[l];
+        for (int o = 0; o < fo; ++o) {
+            double s = 0.0;
+            for (int i = 0; i < fi; ++i) s += W[l][o * fi + i] * a[i];
+            s += b[l][o];
+            h[o] = s > 0.0 ? s : 0.0;
+        }
+        if (l == 1) {                     /* concat skip: [h1 (88), gamma (40)] */
+            memcpy(a, h, sizeof(double) * 88);
+            memcpy(a + 88, g, sizeof(double) * 40);
+        } else {
+            memcpy(a, h, sizeof(double) * fo);
+        }
+    }
+    double yuv[3];
+    for (int o = 0; o < 3; ++o) {
+        double s = 0.0;
+        for (int i = 0; i < 128; ++i) s += W[4][o * 128 + i] * a[i];
+        yuv[o] = s + b[4][o];
+    }
+    y[0] = yuv[0] + 1.13983 * yuv[2];
+    y[1] = yuv[0] - 0.39465 * yuv[1] - 0.58060 * yuv[2];
+    y[2] = yuv[0] + 2.03211 * yuv[1];
+}
+
+EXPORT void orc_fr_eval(const uint16_t* blob, const double* uv, int64_t n, double* y_out) {
+    double B[40];
+    double* W[5];
+    double* b[5];
+    int64_t off = 0;
+    for (int i = 0; i < 40; ++i) B[i] = half_to_double(blob[off++]);
+    for (int l = 0; l < 5; ++l) {
+        W[l] = (double*)malloc(sizeof(double) * FR_IN[l] * FR_OUT[l]);
+        b[l] = (double*)malloc(sizeof(double) * FR_OUT[l]);
+        for (int i = 0; i < FR_IN[l] * FR_OUT[l]; ++i) W[l][i] = half_to_double(blob[off++]);
+        for (int i = 0; i < FR_OUT[l]; ++i) b[l][i] = half_to_double(blob[off++]);
+    }
+    for (int64_t i = 0; i < n; ++i) fr_eval(B, W, b, uv[2 * i], uv[2 * i + 1], y_out + 3 * i);
+    for (int l = 0; l < 5; ++l) { free(W[l]); free(b[l]); }
+}
+
 /* ---------------------------------------------------------------------------------------------- */
 /* Scattering (readings R9, R10)                                        */
 /* ---------------------------------------------------------------------------------------------- */

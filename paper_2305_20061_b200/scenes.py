@@ -381,6 +381,59 @@ def siren_blob(seed: int = 0, out_scale: float = 1.0) -> np.ndarray:
     return flat.view(np.uint16).copy()
 
 
+# The paper's own HDR-NIF (Sec. 3.2; reading R4):
+# Fourier features (F = 40: sin and cos of 2 pi B x for 20 frequency rows B, x = (u, v)) -> 4 dense ReLU
+# layers of width H = 128, where layer 1 ("the last odd layer before the middle") outputs H - F = 88
+# units and is concatenated with the 40 Fourier features -> linear 128 -> 3 (YUV, log space) -> fixed
+# YUV -> RGB matrix -> exp. 50,011 trainable parameters (97.7 KiB in fp16, "97 KiB")
+# plus the 20 x 2 frequency matrix.
+FR_FREQS = 20
+FR_FEATURES = 2 * FR_FREQS
+FR_LAYERS = [(FR_FEATURES, 128), (128, 128 - FR_FEATURES), (128, 128), (128, 128), (128, 3)]
+FR_N_HALVES = 2 * FR_FREQS + sum(o * i + o for i, o in FR_LAYERS)   # 50,051
+assert FR_N_HALVES == 50051
+# BT.601 YUV -> RGB ("The network's final layer is a static colour-conversion matrix (defaulting to YUV
+# to RGB)"): rows R, G, B; columns Y, U, V
+YUV_TO_RGB = np.array([[1.0, 0.0, 1.13983],
+                       [1.0, -0.39465, -0.58060],
+                       [1.0, 2.03211, 0.0]])
+
+
+def fourier_relu_blob(seed: int = 0, sigma: float = 6.0) -> np.ndarray:
+    """fp16 blob of the paper's NIF, 50,051 halves: B[20][2] (frequencies, cycles per unit of u/v),
+    then for each of the 5 layers W[out][in], b[out]. Untrained seeded init: B ~ N(0, sigma^2), ReLU
+    layers He-uniform, biases U(+-0.05), output layer scaled by 0.1 with b = (0.5, 0, 0) (Y offset)."""
+    rng = np.random.default_rng([seed, 7])
+    parts = [rng.normal(0.0, sigma, size=(FR_FREQS, 2)).reshape(-1)]
+    for li, (fin, fout) in enumerate(FR_LAYERS):
+        bound = math.sqrt(6.0 / fin)
+        W = rng.uniform(-bound, bound, size=(fout, fin))
+        b = rng.uniform(-0.05, 0.05, size=fout)
+        if li == len(FR_LAYERS) - 1:
+            W = 0.1 * W
+            b = np.array([0.5, 0.0, 0.0])
+        parts.append(W.reshape(-1))
+        parts.append(b)
+    flat = np.concatenate(parts).astype(np.float16)
+    assert flat.size == FR_N_HALVES
+    return flat.view(np.uint16).copy()
+
+
+def fourier_relu_from_blob(blob: np.ndarray):
+    """(B [20][2], [(W, b)] x 5) as float64 arrays (exact widening)."""
+    h = np.asarray(blob, dtype=np.uint16).view(np.float16).astype(np.float64)
+    B = h[:2 * FR_FREQS].reshape(FR_FREQS, 2)
+    off = 2 * FR_FREQS
+    out = []
+    for fin, fout in FR_LAYERS:
+        W = h[off:off + fin * fout].reshape(fout, fin)
+        off += fin * fout
+        b = h[off:off + fout]
+        off += fout
+        out.append((W, b))
+    return B, out
+
+
 def nif_layers_from_blob(blob: np.ndarray):
     """Split a blob into [(W[out][in], b[out])] as float64 arrays (exact widening)."""
     h = np.asarray(blob, dtype=np.uint16).view(np.float16).astype(np.float64)
