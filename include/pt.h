@@ -82,6 +82,15 @@ PT_API int pt_scene_destroy(pt_scene* scene);
    the fused kernel (tcgen05 K-major operand tiles) and kept resident on the device.
    Errors: INVALID_ARG, FORMAT (n_halves != 50307), CUDA, OOM. */
 PT_API int pt_nif_load(const uint16_t* fp16_blob, int64_t n_halves, pt_nif** out);
+
+/* NIF kinds for pt_nif_load_ex. PT_NIF_SIREN: as pt_nif_load. PT_NIF_FOURIER_RELU: the paper's own
+   HDR-NIF (Sec. 3.2; reading R4): Fourier features gamma = (sin 2 pi B x,
+   cos 2 pi B x) of x = (u, v) with B [20][2], dense ReLU layers 40->128->88 (+ concat of gamma)->128->128,
+   linear 128->3 (YUV, log space), fixed BT.601 YUV->RGB matrix, exp. fp16_blob: n_halves = 50,051 =
+   B (40) then W_l [out][in], b_l [out] for the 5 layers. Errors as pt_nif_load. */
+#define PT_NIF_SIREN 0
+#define PT_NIF_FOURIER_RELU 1
+PT_API int pt_nif_load_ex(int32_t kind, const uint16_t* fp16_blob, int64_t n_halves, pt_nif** out);
 PT_API int pt_nif_destroy(pt_nif* nif);
 
 /* Render a full frame. env: nif != NULL -> HDR-NIF environment; nif == NULL -> constant env_rgb

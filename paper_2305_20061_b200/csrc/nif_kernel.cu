@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cmath>
 #include <cstring>
 #include <vector>
 
@@ -39,8 +40,21 @@ constexpr int kOffB5 = kOffB2 + 3 * kBHBytes;
 constexpr int kOffOnes = kOffB5 + kB5Bytes;      // A operand of the bias K step: [128][16], row = (1, 0, ...)
 constexpr int kOnesBytes = 128 * 16 * 2;
 constexpr int kImageBytes = kOffOnes + kOnesBytes;   // 123,392
+// The paper's own NIF (kind 1: Fourier features + ReLU + concat skip + YUV->RGB, reading R4):
+//   B0: N=128, K=48 (+16 bias) -- K' 0..7 zero, K' 8+2j / 9+2j = weights of sin_j / cos_j
+//   B1: N=96 (88 used), K=128 (+16); B2: N=128, K = [h1 (88), (sin_j, cos_j) interleaved (40)] (+16)
+//   B3: N=128, K=128 (+16); B4: N=16 (3 used: Y, U, V), K=128 (+16); frequencies as fp32 [20][2]
+constexpr int kFrOffB0 = 0;
+constexpr int kFrOffB1 = kFrOffB0 + 128 * 64 * 2;
+constexpr int kFrOffB2 = kFrOffB1 + 96 * 144 * 2;
+constexpr int kFrOffB3 = kFrOffB2 + 128 * 144 * 2;
+constexpr int kFrOffB4 = kFrOffB3 + 128 * 144 * 2;
+constexpr int kFrOffOnes = kFrOffB4 + 16 * 144 * 2;
+constexpr int kFrOffFreq = kFrOffOnes + kOnesBytes;
+constexpr int kFrImageBytes = kFrOffFreq + 20 * 2 * 4;   // 126,624
+constexpr int kImageMax = kFrImageBytes > kImageBytes ? kFrImageBytes : kImageBytes;
 constexpr int kBarBytes = 80;
-constexpr int kSmemBytes = kImageBytes + kBarBytes + 128;
+constexpr int kSmemBytes = kImageMax + kBarBytes + 128;
 
 constexpr int kNumEpiWarps = 16;                   // 4 per TMEM lane quarter, 32 columns each
 constexpr int kEpiArrivals = kNumEpiWarps;         // arrivals per a_ready phase
@@ -107,6 +121,65 @@ void nif_build_smem_image(const uint16_t* blob, std::vector<uint8_t>* image) {
     }
     // constant-1 A tile of the bias step (M = 128 rows, K = 16)
     for (int m = 0; m < 128; ++m) put_core(img, kOffOnes, 128, m, 0, 0x3C00);
+}
+
+// The paper's NIF (blob: B[20][2], then W[out][in], b[out] of the 5 layers) -> kind-1 smem image.
+void nif_build_smem_image_fr(const uint16_t* blob, std::vector<uint8_t>* image) {
+    using namespace nif;
+    std::vector<uint8_t>& img = *image;
+    img.assign(kFrImageBytes, 0);
+    size_t off = 0;
+    float freq[40];
+    for (int i = 0; i < 40; ++i) {
+        const uint16_t h = blob[off++];
+        const int e = (h >> 10) & 31, m = h & 1023;
+        double v = e == 0 ? std::ldexp((double)m, -24) : std::ldexp((double)(m | 1024), e - 25);
+        freq[i] = (float)((h & 0x8000) ? -v : v);
+    }
+    std::memcpy(&img[kFrOffFreq], freq, sizeof(freq));
+    // layer 0: W0 [128][40] (inputs sin_0..19, cos_0..19), b0
+    const uint16_t* W0 = blob + off; off += 128 * 40;
+    const uint16_t* b0 = blob + off; off += 128;
+    for (int n = 0; n < 128; ++n) {
+        for (int j = 0; j < 20; ++j) {
+            put_core(img, kFrOffB0, 128, n, 8 + 2 * j, W0[n * 40 + j]);
+            put_core(img, kFrOffB0, 128, n, 9 + 2 * j, W0[n * 40 + 20 + j]);
+        }
+        put_core(img, kFrOffB0, 128, n, 48, b0[n]);
+    }
+    // layer 1: W1 [88][128], b1 -> N padded to 96
+    const uint16_t* W1 = blob + off; off += 88 * 128;
+    const uint16_t* b1 = blob + off; off += 88;
+    for (int n = 0; n < 88; ++n) {
+        for (int k = 0; k < 128; ++k) put_core(img, kFrOffB1, 96, n, k, W1[n * 128 + k]);
+        put_core(img, kFrOffB1, 96, n, 128, b1[n]);
+    }
+    // layer 2: W2 [128][128] over [h1 (88), sin (20), cos (20)] -> Fourier inputs interleaved
+    const uint16_t* W2 = blob + off; off += 128 * 128;
+    const uint16_t* b2 = blob + off; off += 128;
+    for (int n = 0; n < 128; ++n) {
+        for (int k = 0; k < 88; ++k) put_core(img, kFrOffB2, 128, n, k, W2[n * 128 + k]);
+        for (int j = 0; j < 20; ++j) {
+            put_core(img, kFrOffB2, 128, n, 88 + 2 * j, W2[n * 128 + 88 + j]);
+            put_core(img, kFrOffB2, 128, n, 89 + 2 * j, W2[n * 128 + 108 + j]);
+        }
+        put_core(img, kFrOffB2, 128, n, 128, b2[n]);
+    }
+    // layer 3
+    const uint16_t* W3 = blob + off; off += 128 * 128;
+    const uint16_t* b3 = blob + off; off += 128;
+    for (int n = 0; n < 128; ++n) {
+        for (int k = 0; k < 128; ++k) put_core(img, kFrOffB3, 128, n, k, W3[n * 128 + k]);
+        put_core(img, kFrOffB3, 128, n, 128, b3[n]);
+    }
+    // layer 4: W4 [3][128] -> N padded to 16
+    const uint16_t* W4 = blob + off; off += 3 * 128;
+    const uint16_t* b4 = blob + off; off += 3;
+    for (int n = 0; n < 3; ++n) {
+        for (int k = 0; k < 128; ++k) put_core(img, kFrOffB4, 16, n, k, W4[n * 128 + k]);
+        put_core(img, kFrOffB4, 16, n, 128, b4[n]);
+    }
+    for (int m = 0; m < 128; ++m) put_core(img, kFrOffOnes, 128, m, 0, 0x3C00);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -286,17 +359,46 @@ __device__ unsigned long long g_nif_trace[3 * 4096 * 2];
     } while (0)
 #endif
 
-template <bool kDebug>
+// ReLU epilogue of the paper's NIF: relu + fp16x2 pack in one cvt per pair
+__device__ __forceinline__ uint32_t relu_pack(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
+// Per-layer MMA layout of a kind (SIREN 0 / paper NIF 1): B tile base, K-direction core-matrix stride
+// (LBO = N/8 * 128 B), N of the low and high column halves.
+struct LayerDesc {
+    uint32_t base, lbo;
+    int n_lo, n_hi;
+};
+template <int kKind>
+__device__ __forceinline__ LayerDesc layer_desc(int layer) {
+    using namespace nif;
+    if (kKind == 0) {
+        if (layer == 4) return {(uint32_t)kOffB5, 256u, 16, 0};
+        return {(uint32_t)(kOffB2 + (layer - 1) * kBHBytes), 2048u, 64, 64};
+    } else {
+        if (layer == 1) return {(uint32_t)kFrOffB1, 1536u, 64, 32};
+        if (layer == 2) return {(uint32_t)kFrOffB2, 2048u, 64, 64};
+        if (layer == 3) return {(uint32_t)kFrOffB3, 2048u, 64, 64};
+        return {(uint32_t)kFrOffB4, 256u, 16, 0};
+    }
+}
+
+template <int kKind, bool kDebug>
 __global__ void __launch_bounds__(nif::kThreads, 1)
     nif_fused_kernel(const uint8_t* __restrict__ g_image, const float4* __restrict__ esc,
                      const float4* __restrict__ esc_beta, const uint32_t* __restrict__ count, float* __restrict__ out,
                      float* __restrict__ dbg) {
     using namespace nif;
+    constexpr int kImg = kKind == 0 ? kImageBytes : kFrImageBytes;
+    constexpr uint32_t kOnesOff = kKind == 0 ? kOffOnes : kFrOffOnes;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* image = smem;
     // [0] weights, [1..4] a_ready[slot][column half], [5..8] d_full[slot][column half]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kImageBytes);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kImageBytes + 72);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kImageMax);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kImageMax + 72);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -322,10 +424,10 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
 
     if (warp == 1 && lane == 0 && blockIdx.x < n_tiles) {
         // stage the whole weight image once (bulk TMA copy, complete_tx on bar_w)
-        mbar_expect_tx(bar_w, (uint32_t)kImageBytes);
+        mbar_expect_tx(bar_w, (uint32_t)kImg);
         constexpr int kChunk = 16384;
-        for (int off = 0; off < kImageBytes; off += kChunk) {
-            const int bytes = (kImageBytes - off) < kChunk ? (kImageBytes - off) : kChunk;
+        for (int off = 0; off < kImg; off += kChunk) {
+            const int bytes = (kImg - off) < kChunk ? (kImg - off) : kChunk;
             asm volatile(
                 "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                     smem_u32(image + off)),
@@ -337,12 +439,12 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
     if (warp == 0) {
         if (blockIdx.x < n_tiles) {
             // ===== MMA issuer: warp 0 walks the schedule, one elected lane issues =====
-            // Layer l reads A buffer l % 2. Each layer runs as two N=64 column halves with their own
-            // commit barrier; the low half's K steps 0-3 (A columns 0-31, written by the low-half
-            // epilogue warps) start before the high half of A is ready.
+            // Layer l reads A buffer l % 2. Each layer runs as two column halves with their own commit
+            // barrier; the low half's K steps 0-3 (A columns 0-31, written by the low-half epilogue
+            // warps) start before the high half of A is ready.
             mbar_wait(bar_w, 0);
             const uint32_t img = smem_u32(image);
-            const uint64_t ones = smem_desc(img + kOffOnes, 2048, 128);
+            const uint64_t ones = smem_desc(img + kOnesOff, 2048, 128);
             uint32_t a_phase[2] = {0, 0};
             for (uint32_t i = 0;; i += 2) {
                 const uint32_t t0 = blockIdx.x + i * gridDim.x;
@@ -361,20 +463,34 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
                             mbar_wait(bar_ahi, a_phase[s]);
                             tc_fence_after();
                             if (elect_one()) {
-                                mma_ts(dt, at, smem_desc(img + kOffB1, 2048, 128), idesc(64), 0);
-                                mma_commit(bar_lo);
-                                mma_ts(dt + 64, at, smem_desc(img + kOffB1 + 1024, 2048, 128), idesc(64), 0);
-                                mma_commit(bar_hi);
+                                if (kKind == 0) {
+                                    // x0 hi/lo + constant-1 bias column in one K=16 step
+                                    mma_ts(dt, at, smem_desc(img + kOffB1, 2048, 128), idesc(64), 0);
+                                    mma_commit(bar_lo);
+                                    mma_ts(dt + 64, at, smem_desc(img + kOffB1 + 1024, 2048, 128), idesc(64), 0);
+                                    mma_commit(bar_hi);
+                                } else {
+                                    // Fourier features in A columns 40..63 (K' 0..47) + bias step
+#pragma unroll
+                                    for (int half = 0; half < 2; ++half) {
+                                        const uint32_t b0 = img + kFrOffB0 + 1024 * half;
+#pragma unroll
+                                        for (int k = 0; k < 3; ++k)
+                                            mma_ts(dt + 64 * half, at + 40 + 8 * k, smem_desc(b0 + k * 2 * 2048, 2048, 128),
+                                                   idesc(64), k > 0);
+                                        mma_ss(dt + 64 * half, ones, smem_desc(b0 + 6 * 2048, 2048, 128), idesc(64), 1);
+                                        mma_commit(half ? bar_hi : bar_lo);
+                                    }
+                                }
                             }
                         } else {
-                            const bool out_layer = layer == 4;
-                            const uint32_t base = out_layer ? img + kOffB5 : img + kOffB2 + (layer - 1) * kBHBytes;
-                            const uint32_t lbo = out_layer ? 256 : 2048;       // K-direction core-matrix stride
-                            const uint32_t id = idesc(out_layer ? 16 : 64);
+                            const LayerDesc L = layer_desc<kKind>(layer);
+                            const uint32_t base = img + L.base, lbo = L.lbo;
+                            const uint32_t id_lo = idesc(L.n_lo);
                             if (elect_one()) {
 #pragma unroll
                                 for (int k = 0; k < 4; ++k)
-                                    mma_ts(dt, at + 8 * k, smem_desc(base + k * 2 * lbo, lbo, 128), id, k > 0);
+                                    mma_ts(dt, at + 8 * k, smem_desc(base + k * 2 * lbo, lbo, 128), id_lo, k > 0);
                             }
                             __syncwarp();
                             mbar_wait(bar_ahi, a_phase[s]);
@@ -382,20 +498,18 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
                             if (elect_one()) {
 #pragma unroll
                                 for (int k = 4; k < 8; ++k)
-                                    mma_ts(dt, at + 8 * k, smem_desc(base + k * 2 * lbo, lbo, 128), id, 1);
-                                mma_ss(dt, ones, smem_desc(base + 16 * lbo, lbo, 128), id, 1);   // + bias
-                                if (out_layer) {
-                                    mma_commit(bar_lo);
-                                    mma_commit(bar_hi);
-                                } else {
-                                    mma_commit(bar_lo);
+                                    mma_ts(dt, at + 8 * k, smem_desc(base + k * 2 * lbo, lbo, 128), id_lo, 1);
+                                mma_ss(dt, ones, smem_desc(base + 16 * lbo, lbo, 128), id_lo, 1);   // + bias
+                                mma_commit(bar_lo);
+                                if (L.n_hi > 0) {
+                                    const uint32_t id_hi = idesc(L.n_hi);
 #pragma unroll
                                     for (int k = 0; k < 8; ++k)
-                                        mma_ts(dt + 64, at + 8 * k, smem_desc(base + 1024 + k * 2 * lbo, lbo, 128), id,
+                                        mma_ts(dt + 64, at + 8 * k, smem_desc(base + 1024 + k * 2 * lbo, lbo, 128), id_hi,
                                                k > 0);
-                                    mma_ss(dt + 64, ones, smem_desc(base + 1024 + 16 * lbo, lbo, 128), id, 1);
-                                    mma_commit(bar_hi);
+                                    mma_ss(dt + 64, ones, smem_desc(base + 1024 + 16 * lbo, lbo, 128), id_hi, 1);
                                 }
+                                mma_commit(bar_hi);
                             }
                         }
                         a_phase[s] ^= 1;
@@ -408,36 +522,68 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
     } else if (warp >= kFirstEpiWarp) {
         // ===== epilogue warps =====
         // All 16 epilogue warps work on one (slot, layer) at a time, in the MMA's issue order, so the
-        // tensor core runs the other slot's layer while the sines of this one are computed. Warp w
+        // tensor core runs the other slot's layer while this one's activations are computed. Warp w
         // owns TMEM lane quarter w % 4 (hardware rule) and the 32-column block cb of the 128 columns.
         const int e = warp - kFirstEpiWarp;
         const int cb = e >> 2;                        // column block 0..3
         const int q = warp & 3;                       // TMEM lane quarter
         const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
+        const bool row_warp = kKind == 1 || cb == 0;  // warps that need the queue entry of their rows
+        const float* freq = reinterpret_cast<const float*>(image + kFrOffFreq);
         uint32_t d_phase[2] = {0, 0};
-        // the per-row work (layer-1 input, output) is done by the cb == 0 warps
         float4 ent[2] = {make_float4(0.5f, 0.5f, 0.0f, 0.0f), make_float4(0.5f, 0.5f, 0.0f, 0.0f)};
         auto row_of = [&](uint32_t tile) { return tile * kTileM + 32 * q + lane; };
         auto write_a0 = [&](int s, float4 en) {
-            // layer-1 A tile: (x_hi, y_hi, x_lo, y_lo, 1, 0 ...), x0 = (2u-1, 2v-1) (reading R15)
-            const float x = 2.0f * en.x - 1.0f, y = 2.0f * en.y - 1.0f;
-            const __half xh = __float2half_rn(x), yh = __float2half_rn(y);
-            const __half xl = __float2half_rn(x - __half2float(xh)), yl = __float2half_rn(y - __half2float(yh));
-            uint32_t v[8];
-            v[0] = (uint32_t)__half_as_ushort(xh) | ((uint32_t)__half_as_ushort(yh) << 16);
-            v[1] = (uint32_t)__half_as_ushort(xl) | ((uint32_t)__half_as_ushort(yl) << 16);
-            v[2] = 0x00003C00u;
-            v[3] = v[4] = v[5] = v[6] = v[7] = 0;
-            tmem_st8(tmem + a_col(s, 0) + lane_addr, v);
+            const uint32_t a0 = tmem + a_col(s, 0) + lane_addr;
+            if (kKind == 0) {
+                if (cb != 0) return;
+                // layer-1 A tile: (x_hi, y_hi, x_lo, y_lo, 1, 0 ...), x0 = (2u-1, 2v-1) (reading R15)
+                const float x = 2.0f * en.x - 1.0f, y = 2.0f * en.y - 1.0f;
+                const __half xh = __float2half_rn(x), yh = __float2half_rn(y);
+                const __half xl = __float2half_rn(x - __half2float(xh)), yl = __float2half_rn(y - __half2float(yh));
+                uint32_t v[8];
+                v[0] = (uint32_t)__half_as_ushort(xh) | ((uint32_t)__half_as_ushort(yh) << 16);
+                v[1] = (uint32_t)__half_as_ushort(xl) | ((uint32_t)__half_as_ushort(yl) << 16);
+                v[2] = 0x00003C00u;
+                v[3] = v[4] = v[5] = v[6] = v[7] = 0;
+                tmem_st8(a0, v);
+            } else {
+                // Fourier features (sin_j, cos_j) of 2 pi B_j.(u, v) into A column 44 + j; the four warps
+                // of a lane quarter split the 20 frequencies (4 / 8 / 8) and zero columns 40..43
+                auto feat = [&](int j) {
+                    const float p = fmaf(freq[2 * j], en.x, freq[2 * j + 1] * en.y);
+                    const float r = p - rintf(p);                  // exact-range turns in [-1/2, 1/2]
+                    float sn, cs;
+                    __sincosf(6.28318530717958647692f * r, &sn, &cs);
+                    return pack_half2(sn, cs);
+                };
+                uint32_t v[8];
+                if (cb == 0) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) v[j] = feat(j);
+                    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a0 + 44), "r"(v[0]),
+                                 "r"(v[1]), "r"(v[2]), "r"(v[3])
+                                 : "memory");
+                } else if (cb == 3) {
+                    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%1,%1,%1};" ::"r"(a0 + 40), "r"(0u)
+                                 : "memory");
+                } else {
+                    const int j0 = cb == 1 ? 4 : 12;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) v[j] = feat(j0 + j);
+                    tmem_st8(a0 + 44 + j0, v);
+                }
+            }
         };
         auto load_ent = [&](uint32_t tile) {
             const uint32_t row = row_of(tile);
             return (tile < n_tiles && row < n_rows) ? __ldg(esc + row) : make_float4(0.5f, 0.5f, 0.0f, 0.0f);
         };
-        // prologue: constant-1 bias chunks and the layer-1 inputs of the first tile pair
+        // prologue: layer-1 inputs of the first tile pair (weights must be resident for kind 1)
+        if (kKind == 1 && blockIdx.x < n_tiles) mbar_wait(bar_w, 0);
         for (int s = 0; s < 2; ++s) {
             const uint32_t tile = blockIdx.x + s * gridDim.x;
-            if (cb == 0) {
+            if (row_warp) {
                 ent[s] = load_ent(tile);
                 if (tile < n_tiles) write_a0(s, ent[s]);
             }
@@ -453,14 +599,14 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
             const uint32_t t0 = blockIdx.x + i * gridDim.x;
             if (t0 >= n_tiles) break;
             const int nslots = (t0 + gridDim.x < n_tiles) ? 2 : 1;
-            // prefetch: this pair's throughputs and the next pair's queue entries (cb == 0 warps)
+            // prefetch: this pair's throughputs (cb == 0) and the next pair's queue entries
             float4 beta[2] = {make_float4(0, 0, 0, 0), make_float4(0, 0, 0, 0)};
             float4 ent_next[2] = {ent[0], ent[1]};
-            if (cb == 0) {
+            if (row_warp) {
                 for (int s = 0; s < nslots; ++s) {
                     const uint32_t tile = t0 + s * gridDim.x;
                     const uint32_t row = row_of(tile);
-                    if (row < n_rows) beta[s] = __ldg(esc_beta + row);
+                    if (cb == 0 && row < n_rows) beta[s] = __ldg(esc_beta + row);
                     ent_next[s] = load_ent(tile + 2 * gridDim.x);
                 }
             }
@@ -479,18 +625,36 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
                     tc_fence_after();
                     bool arrive = true;
                     if (layer < 4) {
-                        // hidden layer: D (fp32) -> sin -> fp16 -> A (this warp's 32 columns)
+                        // hidden layer: D (fp32) -> activation -> fp16 -> A (this warp's 32 columns).
+                        // Paper NIF layer 1: only D columns 0..87 are units (A columns 0..43); A columns
+                        // 44..63 keep the Fourier features for the concat skip.
                         const int col = 32 * cb;
-                        uint32_t v[32];
-                        TMEM_LD32(dt + col, v);
-                        tmem_wait_ld_dep(v);
-                        if (kDebug && valid) {
-                            for (int j = 0; j < 32; ++j)
-                                dbg[((size_t)layer * n_rows + row) * kHid + col + j] = __uint_as_float(v[j]);
+                        const bool skip = kKind == 1 && layer == 1 && cb == 3;
+                        if (!skip) {
+                            uint32_t v[32];
+                            TMEM_LD32(dt + col, v);
+                            tmem_wait_ld_dep(v);
+                            if (kDebug && valid) {
+                                for (int j = 0; j < 32; ++j)
+                                    dbg[((size_t)layer * n_rows + row) * kHid + col + j] = __uint_as_float(v[j]);
+                            }
+                            uint32_t p[16];
+                            if (kKind == 0) {
+                                sine_chunk(v, p);
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < 16; ++j)
+                                    p[j] = relu_pack(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+                            }
+                            if (kKind == 1 && layer == 1 && cb == 2) {
+                                tmem_st8(at + 32, p);        // units 64..79
+                                asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(at + 40),
+                                             "r"(p[8]), "r"(p[9]), "r"(p[10]), "r"(p[11])
+                                             : "memory");   // units 80..87
+                            } else {
+                                TMEM_ST16(at + col / 2, p);
+                            }
                         }
-                        uint32_t p[16];
-                        sine_chunk(v, p);
-                        TMEM_ST16(at + col / 2, p);
                     } else {
                         // output layer: y = D[:, 0:3]; radiance = beta * exp(y); then the layer-1
                         // input of this slot's next tile (if any) into the A region
@@ -501,17 +665,25 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
                             tmem_wait_ld_dep4(v);
                             if (valid) {
                                 const uint32_t slot = __float_as_uint(ent[s].z);
-                                const float y0 = __uint_as_float(v[0]), y1 = __uint_as_float(v[1]),
-                                            y2 = __uint_as_float(v[2]);
+                                float y0 = __uint_as_float(v[0]), y1 = __uint_as_float(v[1]), y2 = __uint_as_float(v[2]);
                                 if (kDebug) {
                                     dbg[((size_t)4 * n_rows + row) * kHid + 0] = y0;
                                     dbg[((size_t)4 * n_rows + row) * kHid + 1] = y1;
                                     dbg[((size_t)4 * n_rows + row) * kHid + 2] = y2;
                                 }
+                                if (kKind == 1) {
+                                    // fixed BT.601 YUV -> RGB colour layer, log space
+                                    const float Y = y0, U = y1, V = y2;
+                                    y0 = fmaf(1.13983f, V, Y);
+                                    y1 = fmaf(-0.58060f, V, fmaf(-0.39465f, U, Y));
+                                    y2 = fmaf(2.03211f, U, Y);
+                                }
                                 out[3 * (size_t)slot + 0] = beta[s].x * __expf(y0);
                                 out[3 * (size_t)slot + 1] = beta[s].y * __expf(y1);
                                 out[3 * (size_t)slot + 2] = beta[s].z * __expf(y2);
                             }
+                        }
+                        if (row_warp) {
                             ent[s] = ent_next[s];
                             if (next < n_tiles) write_a0(s, ent[s]);
                         }
@@ -545,29 +717,33 @@ int num_sms() {
     return n;
 }
 
+template <int kKind, bool kDebug>
+static cudaError_t nif_launch_t(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,
+                                int grid, float* out, float* dbg, cudaStream_t st) {
+    using namespace nif;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(nif_fused_kernel<kKind, kDebug>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    nif_fused_kernel<kKind, kDebug><<<grid, kThreads, kSmemBytes, st>>>((const uint8_t*)nif->d_smem_image, esc,
+                                                                        esc_beta, count, out, dbg);
+    return cudaGetLastError();
+}
+
 static cudaError_t nif_launch_impl(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,
                                    int64_t max_rows, float* out, float* dbg, cudaStream_t st) {
     using namespace nif;
-    static bool configured[2] = {false, false};
-    const int which = dbg ? 1 : 0;
-    if (!configured[which]) {
-        cudaError_t e = dbg ? cudaFuncSetAttribute(nif_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   kSmemBytes)
-                            : cudaFuncSetAttribute(nif_fused_kernel<false>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        if (e != cudaSuccess) return e;
-        configured[which] = true;
-    }
     int64_t tiles = (max_rows + kTileM - 1) / kTileM;
     int grid = num_sms();
     if (tiles < grid) grid = (int)(tiles > 0 ? tiles : 1);
-    if (dbg)
-        nif_fused_kernel<true><<<grid, kThreads, kSmemBytes, st>>>((const uint8_t*)nif->d_smem_image, esc, esc_beta,
-                                                                   count, out, dbg);
-    else
-        nif_fused_kernel<false><<<grid, kThreads, kSmemBytes, st>>>((const uint8_t*)nif->d_smem_image, esc, esc_beta,
-                                                                    count, out, nullptr);
-    return cudaGetLastError();
+    if (nif->kind == PT_NIF_FOURIER_RELU)
+        return dbg ? nif_launch_t<1, true>(nif, esc, esc_beta, count, grid, out, dbg, st)
+                   : nif_launch_t<1, false>(nif, esc, esc_beta, count, grid, out, dbg, st);
+    return dbg ? nif_launch_t<0, true>(nif, esc, esc_beta, count, grid, out, dbg, st)
+               : nif_launch_t<0, false>(nif, esc, esc_beta, count, grid, out, dbg, st);
 }
 
 cudaError_t launch_nif(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,

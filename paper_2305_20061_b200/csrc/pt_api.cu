@@ -387,17 +387,23 @@ int pt_scene_destroy(pt_scene* sc) {
     return PT_OK;
 }
 
-int pt_nif_load(const uint16_t* blob, int64_t n_halves, pt_nif** out) {
+int pt_nif_load_ex(int32_t kind, const uint16_t* blob, int64_t n_halves, pt_nif** out) {
     if (!blob || !out) return fail(PT_ERR_INVALID_ARG, "null argument");
     *out = nullptr;
-    if (n_halves != 50307) return fail(PT_ERR_FORMAT, "NIF blob must hold 50307 fp16 values (SIREN 2-128x4-3)");
+    if (kind != PT_NIF_SIREN && kind != PT_NIF_FOURIER_RELU) return fail(PT_ERR_INVALID_ARG, "unknown NIF kind");
+    const int64_t want = kind == PT_NIF_SIREN ? 50307 : 50051;
+    if (n_halves != want)
+        return fail(PT_ERR_FORMAT, kind == PT_NIF_SIREN ? "NIF blob must hold 50307 fp16 values (SIREN 2-128x4-3)"
+                                                        : "NIF blob must hold 50051 fp16 values (Fourier/ReLU NIF)");
     for (int64_t i = 0; i < n_halves; ++i)
         if ((blob[i] & 0x7C00u) == 0x7C00u) return fail(PT_ERR_DOMAIN, "non-finite NIF weight");
     int rc = check_device();
     if (rc) return rc;
     std::vector<uint8_t> img;
-    pt::nif_build_smem_image(blob, &img);
+    if (kind == PT_NIF_SIREN) pt::nif_build_smem_image(blob, &img);
+    else pt::nif_build_smem_image_fr(blob, &img);
     pt_nif* n = new pt_nif();
+    n->kind = kind;
     cudaGetDevice(&n->device);
     n->smem_bytes = (int64_t)img.size();
     cudaError_t e = cudaMalloc(&n->d_smem_image, img.size());
@@ -410,6 +416,10 @@ int pt_nif_load(const uint16_t* blob, int64_t n_halves, pt_nif** out) {
     }
     *out = n;
     return PT_OK;
+}
+
+int pt_nif_load(const uint16_t* blob, int64_t n_halves, pt_nif** out) {
+    return pt_nif_load_ex(PT_NIF_SIREN, blob, n_halves, out);
 }
 
 int pt_nif_destroy(pt_nif* n) {

@@ -100,6 +100,7 @@ struct pt_scene {
 
 struct pt_nif {
     int device = 0;
+    int kind = PT_NIF_SIREN;
     void* d_smem_image = nullptr;     // pre-laid-out shared-memory image of the fused kernel
     int64_t smem_bytes = 0;
     uint16_t* d_blob = nullptr;       // raw fp16 blob (reference SIMT kernel)
@@ -142,6 +143,7 @@ void launch_pack_queries(const float* uv, int64_t n, float4* esc, float4* esc_be
 // NIF (nif_kernel.cu)
 int64_t nif_smem_image_bytes();
 void nif_build_smem_image(const uint16_t* blob, std::vector<uint8_t>* image);
+void nif_build_smem_image_fr(const uint16_t* blob, std::vector<uint8_t>* image);
 cudaError_t launch_nif(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,
                        int64_t max_rows, float* out, cudaStream_t st);
 int num_sms();

@@ -29,7 +29,7 @@ class PtStats(C.Structure):
                 ("nif_launches", C.c_int64), ("traverse_launches", C.c_int64)]
 
 
-EXPORTED = ["pt_scene_create", "pt_scene_destroy", "pt_nif_load", "pt_nif_destroy", "pt_render",
+EXPORTED = ["pt_scene_create", "pt_scene_destroy", "pt_nif_load", "pt_nif_load_ex", "pt_nif_destroy", "pt_render",
             "pt_render_samples", "pt_trace_primary", "pt_trace_rays", "pt_nif_infer", "pt_get_stats",
             "pt_set_profiling", "pt_last_error", "pt_version"]
 
@@ -46,6 +46,7 @@ def lib():
             L.pt_scene_create.argtypes = [P, I64, P, I64, P, I32, P, C.POINTER(P)]
             L.pt_scene_destroy.argtypes = [P]
             L.pt_nif_load.argtypes = [P, I64, C.POINTER(P)]
+            L.pt_nif_load_ex.argtypes = [I32, P, I64, C.POINTER(P)]
             L.pt_nif_destroy.argtypes = [P]
             L.pt_render.argtypes = [P, P, P, I32, I32, I32, I32, U64, P]
             L.pt_render_samples.argtypes = [P, P, P, I32, I32, I32, I32, I32, U64, I32, P, P]
@@ -99,11 +100,13 @@ class Scene:
         c = np.ascontiguousarray(sc.camera)
         h = C.c_void_p()
         _check(lib().pt_scene_create(_p(t), t.shape[0], _p(s), s.shape[0], _p(m), m.shape[0], _p(c), C.byref(h)))
+        self._lib = lib()
         self.h = h
 
     def close(self):
+        # the library handle is held by the object: module globals may be gone at interpreter exit
         if getattr(self, "h", None):
-            lib().pt_scene_destroy(self.h)
+            self._lib.pt_scene_destroy(self.h)
             self.h = None
 
     __del__ = close
@@ -117,16 +120,23 @@ class Scene:
         return {k: getattr(st, k) for k, _ in PtStats._fields_}
 
 
+NIF_SIREN = 0          # PT_NIF_SIREN: SIREN 2-128x4-3 (scenes.siren_blob)
+NIF_FOURIER_RELU = 1   # PT_NIF_FOURIER_RELU: the paper's Fourier/ReLU/YUV NIF (scenes.fourier_relu_blob)
+
+
 class Nif:
-    def __init__(self, blob: np.ndarray):
+    def __init__(self, blob: np.ndarray, kind: int = NIF_SIREN):
         b = np.ascontiguousarray(blob, dtype=np.uint16)
         h = C.c_void_p()
-        _check(lib().pt_nif_load(_p(b), b.size, C.byref(h)))
+        _check(lib().pt_nif_load_ex(int(kind), _p(b), b.size, C.byref(h)))
+        self._lib = lib()
         self.h = h
+        self.kind = int(kind)
 
     def close(self):
+        # the library handle is held by the object: module globals may be gone at interpreter exit
         if getattr(self, "h", None):
-            lib().pt_nif_destroy(self.h)
+            self._lib.pt_nif_destroy(self.h)
             self.h = None
 
     __del__ = close

@@ -84,6 +84,73 @@ def test_nif_layer_accumulators(ptm, blob):
     assert np.abs(dbg[4][:, :3] - y).max() < sin_err * np.abs(L[4][0]).sum(1).max() + 1e-4
 
 
+@pytest.fixture(scope="module")
+def fr_blob():
+    return scenes.fourier_relu_blob(0)
+
+
+def _fr_features(uv, B):
+    p = 2 * np.pi * (uv.astype(np.float64) @ B.T)
+    return np.concatenate([np.sin(p), np.cos(p)], 1)
+
+
+@pytest.mark.parametrize("n", [1, 127, 129, 1000, 4 * 148 * 128 + 77])
+def test_fr_nif_vs_oracle(ptm, orc, fr_blob, n):
+    """The paper's own HDR-NIF (Fourier features, ReLU, concat skip, YUV->RGB; PT_NIF_FOURIER_RELU)
+    on the tcgen05 kernel against oracle.fr_eval, same gates as the SIREN network."""
+    import torch
+    nif = ptm.Nif(fr_blob, kind=ptm.NIF_FOURIER_RELU)
+    uv = _uv_cases(n, seed=n + 5)
+    got = ptm.nif_infer(nif, torch.from_numpy(uv).cuda()).cpu().numpy().astype(np.float64)
+    y = orc.fr_eval(fr_blob, uv.astype(np.float64))
+    assert np.isfinite(got).all() and (got > 0).all()
+    assert np.abs(np.log(got) - y).max() <= NIF_LOG_GATE
+    assert (np.abs(got - np.exp(y)) / np.exp(y)).max() <= NIF_REL_GATE
+
+
+def test_fr_nif_layer_accumulators(ptm, fr_blob):
+    """Debug view of the paper's NIF: each layer's fp32 accumulator against float64 products of the
+    fp16 activations the kernel fed forward (layout check for the 88-wide layer and the concat skip)."""
+    import torch
+    uv = _uv_cases(640, 11)
+    nif = ptm.Nif(fr_blob, kind=ptm.NIF_FOURIER_RELU)
+    out, dbg = ptm.nif_debug_layers(nif, torch.from_numpy(uv).cuda())
+    dbg = dbg.cpu().numpy().astype(np.float64)
+    B, L = scenes.fourier_relu_from_blob(fr_blob)
+    g = _fr_features(uv, B)
+    # layer 0: features rounded to fp16 (|err| <= 2^-12 on [-1, 1]) + __sincosf of a reduced argument
+    feat_err = 2.0 ** -12 + 2e-6
+    pre = g @ L[0][0].T + L[0][1]
+    assert np.abs(dbg[0] - pre).max() < feat_err * np.abs(L[0][0]).sum(1).max() + 1e-4
+    h = np.maximum(dbg[0], 0).astype(np.float16).astype(np.float64)
+    acc = lambda W, a: 1e-5 * (np.abs(a) @ np.abs(W).T).max() + 1e-5      # fp32 accumulation
+    pre = h @ L[1][0].T + L[1][1]
+    assert np.abs(dbg[1][:, :88] - pre).max() < acc(L[1][0], h)
+    h1 = np.maximum(dbg[1][:, :88], 0).astype(np.float16).astype(np.float64)
+    a = np.concatenate([h1, g], 1)
+    pre = a @ L[2][0].T + L[2][1]
+    tol = acc(L[2][0], a) + feat_err * np.abs(L[2][0][:, 88:]).sum(1).max()
+    assert np.abs(dbg[2] - pre).max() < tol
+    h = np.maximum(dbg[2], 0).astype(np.float16).astype(np.float64)
+    pre = h @ L[3][0].T + L[3][1]
+    assert np.abs(dbg[3] - pre).max() < acc(L[3][0], h)
+    h = np.maximum(dbg[3], 0).astype(np.float16).astype(np.float64)
+    yuv = h @ L[4][0].T + L[4][1]
+    assert np.abs(dbg[4][:, :3] - yuv).max() < acc(L[4][0], h)
+    M = np.array(scenes.YUV_TO_RGB)
+    y_gpu = np.log(out.cpu().numpy().astype(np.float64))
+    assert np.abs(y_gpu - dbg[4][:, :3] @ M.T).max() < 1e-5 * (1 + np.abs(y_gpu).max())
+
+
+def test_fr_nif_rejects_wrong_size(ptm, fr_blob, blob):
+    with pytest.raises(RuntimeError):
+        ptm.Nif(blob, kind=ptm.NIF_FOURIER_RELU)
+    with pytest.raises(RuntimeError):
+        ptm.Nif(fr_blob, kind=ptm.NIF_SIREN)
+    with pytest.raises(RuntimeError):
+        ptm.Nif(fr_blob, kind=7)
+
+
 def _primary_check(ptm, orc, sc, W, H, pix, seed=0, sample=0):
     prim_g, t_g = ptm.trace_primary(ptm.Scene(sc), W, H, seed, sample)
     prim_g = prim_g.cpu().numpy()[pix]

@@ -20,10 +20,11 @@ ap.add_argument("--n", type=int, default=1 << 24)
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--check", action="store_true")
 ap.add_argument("--tag", default="")
+ap.add_argument("--kind", type=int, default=0, help="0 SIREN, 1 the paper's Fourier/ReLU NIF")
 a = ap.parse_args()
 peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-blob = scenes.siren_blob(0)
-nif = pt.Nif(blob)
+blob = scenes.siren_blob(0) if a.kind == 0 else scenes.fourier_relu_blob(0)
+nif = pt.Nif(blob, kind=a.kind)
 uv = torch.from_numpy(scenes.query_uv(a.n, 3)).cuda()
 out = torch.empty((a.n, 3), device="cuda")
 for _ in range(3):
@@ -37,14 +38,17 @@ e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / a.iters
 rate = a.n / (ms / 1e3)
+# dense flops per inference: SIREN 3 hidden 128x128 layers; paper NIF 40x128 + 128x88 + 2 x 128x128
+# (both 98,304; the tiny input/output layers are not counted)
 tf = rate * 98304 / 1e12
-res = {"tag": a.tag, "n": a.n, "ms": ms, "inferences_per_s": rate, "tflops_hidden": tf,
+res = {"tag": a.tag, "kind": a.kind, "n": a.n, "ms": ms, "inferences_per_s": rate, "tflops_hidden": tf,
        "frac_burst": tf / peaks["bf16_tflops"], "frac_sustained": tf / peaks["bf16_tflops_sustained"],
        "note": "includes the tiny query-pack kernel of pt_nif_infer"}
 if a.check:
     import oracle
     k = 4096
-    y = oracle.nif_eval(blob, scenes.query_uv(a.n, 3)[:k].astype(np.float64))
+    q = scenes.query_uv(a.n, 3)[:k].astype(np.float64)
+    y = oracle.nif_eval(blob, q) if a.kind == 0 else oracle.fr_eval(blob, q)
     got = out[:k].cpu().numpy().astype(np.float64)
     res["max_abs_dy"] = float(np.abs(np.log(got) - y).max())
     res["max_rel"] = float((np.abs(got - np.exp(y)) / np.exp(y)).max())
