@@ -259,7 +259,7 @@ int build_wide_bvh(const pt_triangle* tris, int64_t n_tris, const pt_sphere* sph
         for (int32_t c : ch) units += B.nodes[c].count == 0 ? kNodeUnits : (int64_t)kPrimUnits * B.nodes[c].count;
         units = (units + 3) & ~int64_t(3);
         int64_t base = alloc(units);
-        if (base > 0xFFFFFFFFll) { *msg = "BVH pool exceeds 2^32 units"; return PT_ERR_DOMAIN; }
+        if (base + units > (1ll << 28)) { *msg = "BVH pool exceeds 2^28 units (4 GiB)"; return PT_ERR_DOMAIN; }
         // node header
         Box nb;
         nb.empty();

@@ -15,6 +15,7 @@
 // to the other's accumulator.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
+#include <math_constants.h>
 #include <stdint.h>
 
 #include <cmath>
@@ -53,8 +54,16 @@ constexpr int kFrOffOnes = kFrOffB4 + 16 * 144 * 2;
 constexpr int kFrOffFreq = kFrOffOnes + kOnesBytes;
 constexpr int kFrImageBytes = kFrOffFreq + 20 * 2 * 4;   // 126,624
 constexpr int kImageMax = kFrImageBytes > kImageBytes ? kFrImageBytes : kImageBytes;
-constexpr int kBarBytes = 80;
-constexpr int kSmemBytes = kImageMax + kBarBytes + 128;
+// barriers: [0] weights, [1..4] a_ready[slot][half], [5..8] d_full[slot][half], [9..10] a0_full[slot],
+// [11..12] a0_empty[slot]; TMEM base address at byte 120
+constexpr int kBarBytes = 128;
+// SIREN layer-1 A tiles staged in shared memory by the producer warps (one 128x16 fp16 K-major tile per
+// slot: row m = (x_hi, y_hi, x_lo, y_lo, 1, 0, 0, 0) at 16 m, k = 8..15 zero at 2048 + 16 m)
+constexpr int kA0Bytes = 128 * 16 * 2;
+constexpr int kOffA0 = ((kImageMax + kBarBytes + 1023) / 1024) * 1024;
+constexpr int kSmemBytes = kOffA0 + 2 * kA0Bytes + 128;
+constexpr int kProducerWarp0 = 2;                  // warps 2-3 stage the layer-1 inputs (SIREN)
+constexpr int kProducerThreads = 64;
 
 constexpr int kNumEpiWarps = 16;                   // 4 per TMEM lane quarter, 32 columns each
 constexpr int kEpiArrivals = kNumEpiWarps;         // arrivals per a_ready phase
@@ -359,6 +368,22 @@ __device__ unsigned long long g_nif_trace[3 * 4096 * 2];
     } while (0)
 #endif
 
+// Equirect map of an escaped direction (S4 -> S5; moved here from the trace kernel so the divergent
+// atan2/acos run once per queued ray in the NIF prologue instead of in the traversal warps)
+__device__ __forceinline__ void equirect_f32(float3 d, float& u, float& v) {
+    // SPEC.md:438 convention (reading R14): u = 0.5 + atan2(d.x, -d.z)/2pi wrapped to [0,1); v = acos(d.y)/pi
+    const float len = sqrtf(d.x * d.x + d.y * d.y + d.z * d.z);
+    float uu;
+    if (d.x == 0.0f && d.z == 0.0f) uu = 0.5f;
+    else {
+        uu = 0.5f + atan2f(d.x, -d.z) * (0.5f / CUDART_PI_F);
+        if (uu >= 1.0f) uu -= 1.0f;
+    }
+    const float y = fminf(1.0f, fmaxf(-1.0f, d.y / len));
+    u = uu;
+    v = acosf(y) * (1.0f / CUDART_PI_F);
+}
+
 // ReLU epilogue of the paper's NIF: relu + fp16x2 pack in one cvt per pair
 __device__ __forceinline__ uint32_t relu_pack(float lo, float hi) {
     uint32_t r;
@@ -390,7 +415,7 @@ template <int kKind, bool kDebug>
 __global__ void __launch_bounds__(nif::kThreads, 1)
     nif_fused_kernel(const uint8_t* __restrict__ g_image, const float4* __restrict__ esc,
                      const float4* __restrict__ esc_beta, const uint32_t* __restrict__ count, float* __restrict__ out,
-                     float* __restrict__ dbg) {
+                     float* __restrict__ dbg, int dir_input) {
     using namespace nif;
     constexpr int kImg = kKind == 0 ? kImageBytes : kFrImageBytes;
     constexpr uint32_t kOnesOff = kKind == 0 ? kOffOnes : kFrOffOnes;
@@ -398,7 +423,7 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
     uint8_t* image = smem;
     // [0] weights, [1..4] a_ready[slot][column half], [5..8] d_full[slot][column half]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kImageMax);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kImageMax + 72);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kImageMax + 120);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -410,6 +435,8 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
         mbar_init(bar_w, 1);
         for (int b = 1; b < 5; ++b) mbar_init(smem_u32(&bars[b]), kEpiArrivals / 2);
         for (int b = 5; b < 9; ++b) mbar_init(smem_u32(&bars[b]), 1);
+        for (int b = 9; b < 11; ++b) mbar_init(smem_u32(&bars[b]), kProducerThreads);
+        for (int b = 11; b < 13; ++b) mbar_init(smem_u32(&bars[b]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
@@ -446,6 +473,7 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
             const uint32_t img = smem_u32(image);
             const uint64_t ones = smem_desc(img + kOnesOff, 2048, 128);
             uint32_t a_phase[2] = {0, 0};
+            uint32_t a0_phase[2] = {0, 0};
             for (uint32_t i = 0;; i += 2) {
                 const uint32_t t0 = blockIdx.x + i * gridDim.x;
                 if (t0 >= n_tiles) break;
@@ -462,13 +490,20 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
                         if (layer == 0) {
                             mbar_wait(bar_ahi, a_phase[s]);
                             tc_fence_after();
+                            if (kKind == 0) {
+                                mbar_wait(smem_u32(&bars[9 + s]), a0_phase[s]);   // staged by the producers
+                                a0_phase[s] ^= 1;
+                                tc_fence_after();
+                            }
                             if (elect_one()) {
                                 if (kKind == 0) {
-                                    // x0 hi/lo + constant-1 bias column in one K=16 step
-                                    mma_ts(dt, at, smem_desc(img + kOffB1, 2048, 128), idesc(64), 0);
+                                    // x0 hi/lo + constant-1 bias column in one K=16 step, A from shared memory
+                                    const uint64_t a0 = smem_desc(smem_u32(smem + kOffA0 + s * kA0Bytes), 2048, 128);
+                                    mma_ss(dt, a0, smem_desc(img + kOffB1, 2048, 128), idesc(64), 0);
                                     mma_commit(bar_lo);
-                                    mma_ts(dt + 64, at, smem_desc(img + kOffB1 + 1024, 2048, 128), idesc(64), 0);
+                                    mma_ss(dt + 64, a0, smem_desc(img + kOffB1 + 1024, 2048, 128), idesc(64), 0);
                                     mma_commit(bar_hi);
+                                    mma_commit(smem_u32(&bars[11 + s]));             // staging buffer free
                                 } else {
                                     // Fourier features in A columns 40..63 (K' 0..47) + bias step
 #pragma unroll
@@ -519,6 +554,48 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
                 }
             }
         }
+    } else if (kKind == 0 && (warp == kProducerWarp0 || warp == kProducerWarp0 + 1)) {
+        // ===== producers: layer-1 inputs of every tile, staged one tile ahead per slot =====
+        // queue entry -> (u, v) (equirect of the escape direction for the render queue, reading R14)
+        // -> x0 = (2u-1, 2v-1) split into fp16 hi + lo (reading R15), constant-1 bias column.
+        const int p = threadIdx.x - 32 * kProducerWarp0;
+        uint8_t* a0s = smem + kOffA0;
+        for (int i = p; i < 2 * kA0Bytes / 16; i += kProducerThreads)
+            *reinterpret_cast<uint4*>(a0s + 16 * i) = make_uint4(0, 0, 0, 0);
+        uint32_t e_phase[2] = {0, 0};
+        uint32_t fills[2] = {0, 0};
+        for (uint32_t i = 0;; i += 2) {
+            const uint32_t t0 = blockIdx.x + i * gridDim.x;
+            if (t0 >= n_tiles) break;
+            const int nslots = (t0 + gridDim.x < n_tiles) ? 2 : 1;
+            for (int s = 0; s < nslots; ++s) {
+                const uint32_t tile = t0 + s * gridDim.x;
+                if (fills[s]++ > 0) {
+                    mbar_wait(smem_u32(&bars[11 + s]), e_phase[s]);
+                    e_phase[s] ^= 1;
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int m = p + 64 * h;
+                    const uint32_t row = tile * kTileM + m;
+                    float u = 0.5f, v = 0.5f;
+                    if (row < n_rows) {
+                        const float4 en = __ldg(esc + row);
+                        u = en.x;
+                        v = en.y;
+                        if (dir_input) equirect_f32(make_float3(en.x, en.y, en.z), u, v);
+                    }
+                    const float x = 2.0f * u - 1.0f, y = 2.0f * v - 1.0f;
+                    const __half xh = __float2half_rn(x), yh = __float2half_rn(y);
+                    const __half xl = __float2half_rn(x - __half2float(xh)), yl = __float2half_rn(y - __half2float(yh));
+                    *reinterpret_cast<uint4*>(a0s + s * kA0Bytes + 16 * m) = make_uint4(
+                        (uint32_t)__half_as_ushort(xh) | ((uint32_t)__half_as_ushort(yh) << 16),
+                        (uint32_t)__half_as_ushort(xl) | ((uint32_t)__half_as_ushort(yl) << 16), 0x00003C00u, 0u);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic -> async proxy
+                mbar_arrive(smem_u32(&bars[9 + s]));
+            }
+        }
     } else if (warp >= kFirstEpiWarp) {
         // ===== epilogue warps =====
         // All 16 epilogue warps work on one (slot, layer) at a time, in the MMA's issue order, so the
@@ -536,17 +613,7 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
         auto write_a0 = [&](int s, float4 en) {
             const uint32_t a0 = tmem + a_col(s, 0) + lane_addr;
             if (kKind == 0) {
-                if (cb != 0) return;
-                // layer-1 A tile: (x_hi, y_hi, x_lo, y_lo, 1, 0 ...), x0 = (2u-1, 2v-1) (reading R15)
-                const float x = 2.0f * en.x - 1.0f, y = 2.0f * en.y - 1.0f;
-                const __half xh = __float2half_rn(x), yh = __float2half_rn(y);
-                const __half xl = __float2half_rn(x - __half2float(xh)), yl = __float2half_rn(y - __half2float(yh));
-                uint32_t v[8];
-                v[0] = (uint32_t)__half_as_ushort(xh) | ((uint32_t)__half_as_ushort(yh) << 16);
-                v[1] = (uint32_t)__half_as_ushort(xl) | ((uint32_t)__half_as_ushort(yl) << 16);
-                v[2] = 0x00003C00u;
-                v[3] = v[4] = v[5] = v[6] = v[7] = 0;
-                tmem_st8(a0, v);
+                return;   // SIREN: the layer-1 tile is staged in shared memory by the producer warps
             } else {
                 // Fourier features (sin_j, cos_j) of 2 pi B_j.(u, v) into A column 44 + j; the four warps
                 // of a lane quarter split the 20 frequencies (4 / 8 / 8) and zero columns 40..43
@@ -575,9 +642,14 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
                 }
             }
         };
+        // queue entry -> (u, v, -, slot): the render queues escape directions (d.xyz, slot) and the
+        // query hook (u, v, 0, slot)
         auto load_ent = [&](uint32_t tile) {
             const uint32_t row = row_of(tile);
-            return (tile < n_tiles && row < n_rows) ? __ldg(esc + row) : make_float4(0.5f, 0.5f, 0.0f, 0.0f);
+            float4 en = (tile < n_tiles && row < n_rows) ? __ldg(esc + row) : make_float4(0.5f, 0.5f, 0.0f, 0.0f);
+            if (kKind == 1 && dir_input && tile < n_tiles && row < n_rows)
+                equirect_f32(make_float3(en.x, en.y, en.z), en.x, en.y);
+            return en;
         };
         // prologue: layer-1 inputs of the first tile pair (weights must be resident for kind 1)
         if (kKind == 1 && blockIdx.x < n_tiles) mbar_wait(bar_w, 0);
@@ -664,7 +736,7 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
                             tmem_ld4(dt, v);
                             tmem_wait_ld_dep4(v);
                             if (valid) {
-                                const uint32_t slot = __float_as_uint(ent[s].z);
+                                const uint32_t slot = __float_as_uint(ent[s].w);
                                 float y0 = __uint_as_float(v[0]), y1 = __uint_as_float(v[1]), y2 = __uint_as_float(v[2]);
                                 if (kDebug) {
                                     dbg[((size_t)4 * n_rows + row) * kHid + 0] = y0;
@@ -719,7 +791,7 @@ int num_sms() {
 
 template <int kKind, bool kDebug>
 static cudaError_t nif_launch_t(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,
-                                int grid, float* out, float* dbg, cudaStream_t st) {
+                                int grid, float* out, float* dbg, int dir_input, cudaStream_t st) {
     using namespace nif;
     static bool configured = false;
     if (!configured) {
@@ -729,31 +801,31 @@ static cudaError_t nif_launch_t(const pt_nif* nif, const float4* esc, const floa
         configured = true;
     }
     nif_fused_kernel<kKind, kDebug><<<grid, kThreads, kSmemBytes, st>>>((const uint8_t*)nif->d_smem_image, esc,
-                                                                        esc_beta, count, out, dbg);
+                                                                        esc_beta, count, out, dbg, dir_input);
     return cudaGetLastError();
 }
 
 static cudaError_t nif_launch_impl(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,
-                                   int64_t max_rows, float* out, float* dbg, cudaStream_t st) {
+                                   int64_t max_rows, float* out, float* dbg, int dir_input, cudaStream_t st) {
     using namespace nif;
     int64_t tiles = (max_rows + kTileM - 1) / kTileM;
     int grid = num_sms();
     if (tiles < grid) grid = (int)(tiles > 0 ? tiles : 1);
     if (nif->kind == PT_NIF_FOURIER_RELU)
-        return dbg ? nif_launch_t<1, true>(nif, esc, esc_beta, count, grid, out, dbg, st)
-                   : nif_launch_t<1, false>(nif, esc, esc_beta, count, grid, out, dbg, st);
-    return dbg ? nif_launch_t<0, true>(nif, esc, esc_beta, count, grid, out, dbg, st)
-               : nif_launch_t<0, false>(nif, esc, esc_beta, count, grid, out, dbg, st);
+        return dbg ? nif_launch_t<1, true>(nif, esc, esc_beta, count, grid, out, dbg, dir_input, st)
+                   : nif_launch_t<1, false>(nif, esc, esc_beta, count, grid, out, dbg, dir_input, st);
+    return dbg ? nif_launch_t<0, true>(nif, esc, esc_beta, count, grid, out, dbg, dir_input, st)
+               : nif_launch_t<0, false>(nif, esc, esc_beta, count, grid, out, dbg, dir_input, st);
 }
 
 cudaError_t launch_nif(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,
-                       int64_t max_rows, float* out, cudaStream_t st) {
-    return nif_launch_impl(nif, esc, esc_beta, count, max_rows, out, nullptr, st);
+                       int64_t max_rows, float* out, int dir_input, cudaStream_t st) {
+    return nif_launch_impl(nif, esc, esc_beta, count, max_rows, out, nullptr, dir_input, st);
 }
 
 cudaError_t launch_nif_debug(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,
                              int64_t rows, float* out, float* dbg, cudaStream_t st) {
-    return nif_launch_impl(nif, esc, esc_beta, count, rows, out, dbg, st);
+    return nif_launch_impl(nif, esc, esc_beta, count, rows, out, dbg, 0, st);
 }
 
 }  // namespace pt

@@ -229,7 +229,7 @@ int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, i
         }
         if (use_nif) {
             tm.begin(T_NIF, &e0);
-            cudaError_t e = pt::launch_nif(nif, ws.esc, ws.esc_beta, ws.counters + pt::kCounterEsc, slots, ws.wave_buf, st);
+            cudaError_t e = pt::launch_nif(nif, ws.esc, ws.esc_beta, ws.counters + pt::kCounterEsc, slots, ws.wave_buf, 1, st);
             tm.end(T_NIF, e0);
             if (e != cudaSuccess) return fail(PT_ERR_CUDA, std::string("nif launch: ") + cudaGetErrorString(e));
             stats.launches += 1;
@@ -509,7 +509,7 @@ static int nif_infer_impl(const pt_nif* nif, const float* d_uv, int64_t n, float
     if (!cnt) CU(cudaMalloc(&cnt, sizeof(uint32_t)));
     pt::launch_pack_queries(d_uv, n, esc, esc_beta, cnt, st);
     cudaError_t e = d_dbg ? pt::launch_nif_debug(nif, esc, esc_beta, cnt, n, d_rgb, d_dbg, st)
-                          : pt::launch_nif(nif, esc, esc_beta, cnt, n, d_rgb, st);
+                          : pt::launch_nif(nif, esc, esc_beta, cnt, n, d_rgb, 0, st);
     if (e != cudaSuccess) return fail(PT_ERR_CUDA, std::string("nif launch: ") + cudaGetErrorString(e));
     return PT_OK;
 }

@@ -59,7 +59,7 @@ struct Workspace {
     float4* rayA[2] = {nullptr, nullptr};   // (o.xyz, slot bits)
     float4* rayB[2] = {nullptr, nullptr};   // (d.xyz, beta.x)
     float2* rayC[2] = {nullptr, nullptr};   // (beta.y, beta.z)
-    float4* esc = nullptr;     // [cap] escaped-ray queue: (u, v, slot bits, 0)
+    float4* esc = nullptr;     // [cap] escaped-ray queue: (d.xyz, slot bits); the NIF maps d to (u, v)
     float4* esc_beta = nullptr;// [cap] escaped-ray throughput
     float* wave_buf = nullptr; // [cap][3] radiance per slot, written exactly once per path
     uint32_t* counters = nullptr;  // [kCounters]
@@ -145,7 +145,7 @@ int64_t nif_smem_image_bytes();
 void nif_build_smem_image(const uint16_t* blob, std::vector<uint8_t>* image);
 void nif_build_smem_image_fr(const uint16_t* blob, std::vector<uint8_t>* image);
 cudaError_t launch_nif(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,
-                       int64_t max_rows, float* out, cudaStream_t st);
+                       int64_t max_rows, float* out, int dir_input, cudaStream_t st);
 int num_sms();
 
 }  // namespace pt

@@ -338,94 +338,130 @@ __device__ __forceinline__ void cswap(float& ta, uint32_t& oa, float& tb, uint32
     }
 }
 
+// Traversal entries (stack, current node, postponed leaf): one word per child,
+//   interior node: its unit index (< 2^28);  leaf: unit index of its first primitive | kLeafBit |
+//   (count - 1) << 28;  kNoEntry: nothing.
+constexpr uint32_t kLeafBit = 0x80000000u;
+constexpr uint32_t kNoEntry = 0x7FFFFFFFu;
+__device__ __forceinline__ bool is_node(uint32_t e) { return e < (1u << 28); }
+__device__ __forceinline__ bool is_leaf(uint32_t e) { return (e & kLeafBit) != 0; }
+
 __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
     Hit best{CUDART_INF, CUDART_INF_F, CUDART_INF_F, -1, 0u, true};
     if (tp.empty) return best;
     RayT r;
     ray_prepare(o, d, r);
     constexpr float kGrow = 1.0f + 2.0f * (3.0f * 0x1p-24f) / (1.0f - 3.0f * 0x1p-24f);   // 1 + 2 gamma_3
+    // per-axis fp16x2 half swap so that t.x is always the near slab plane and t.y the far one
+    uint32_t swz[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) swz[a] = ((r.negmask >> a) & 1u) ? 0x1032u : 0x3210u;
     uint2 stack[kStackSize];
     int sp = 0;
-    uint32_t cur = 0;
     const uint4* __restrict__ pool = tp.pool;
     TCOUNT(4, 1);
-    for (;;) {
-        TCOUNT(0, 1);
-        const uint4 h = __ldg(pool + cur);
-        const uint4 q0 = __ldg(pool + cur + 1), q1 = __ldg(pool + cur + 2), q2 = __ldg(pool + cur + 3);
-        const uint32_t w[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
-        const float O[3] = {__uint_as_float(h.x), __uint_as_float(h.y), __uint_as_float(h.z)};
-        uint32_t off = h.w;
-        // per-child results in registers (static indices only: no local-memory arrays)
-        float ctn[4];
-        uint32_t coff[4];
-        uint32_t lu[4];
-        uint32_t leafmask = 0, cntpack = 0;
-        const float tcull0 = cull_bound(best);
-#pragma unroll
-        for (int ci = 0; ci < 4; ++ci) {
-            ctn[ci] = CUDART_INF_F;
-            coff[ci] = 0;
-            lu[ci] = off;
-            const uint32_t w0 = w[3 * ci], w1 = w[3 * ci + 1], w2 = w[3 * ci + 2];
-            const bool valid = (w0 & 0x8000u) != 0;
-            const bool leaf = (w1 & 0x8000u) != 0;
-            const uint32_t cnt = (((w2 >> 15) & 1u) | ((w0 >> 30) & 2u)) + 1u;
-            const uint32_t wa[3] = {w0 & 0x7FFF7FFFu, w1 & 0x7FFF7FFFu, w2 & 0x7FFF7FFFu};
-            float tn = 0.0f, tf = CUDART_INF_F;
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                // (lo, hi) of this axis: exact fp16 -> fp32, then the same rn ops as the builder's check
-                const float2 lh = __half22float2(*reinterpret_cast<const __half2*>(&wa[a]));
-                const float2 b = __fadd2_rn(make_float2(O[a], O[a]), lh);
-                const float2 t = __fmul2_rn(__fadd2_rn(b, make_float2(-r.o[a], -r.o[a])),
-                                            make_float2(r.inv[a], r.inv[a]));
-                const bool ng = (r.negmask >> a) & 1u;
-                tn = fmaxf(tn, ng ? t.y : t.x);
-                tf = fminf(tf, ng ? t.x : t.y);
-            }
-            tf = tf * kGrow;
-            const bool hit = valid && tn <= tf && tn <= tcull0;
-            if (hit && leaf) {
-                leafmask |= 1u << ci;
-                cntpack |= cnt << (4 * ci);
-            }
-            if (hit && !leaf) {
-                ctn[ci] = tn;
-                coff[ci] = off;
-            }
-            off += valid ? (leaf ? kPrimUnits * cnt : (uint32_t)kNodeUnits) : 0u;
-        }
-        // primitives of the hit leaves (one instantiation of test_prim)
-        while (leafmask) {
-            const int ci = __ffs(leafmask) - 1;
-            leafmask &= leafmask - 1;
-            uint32_t unit = ci == 0 ? lu[0] : ci == 1 ? lu[1] : ci == 2 ? lu[2] : lu[3];
-            const uint32_t cnt = (cntpack >> (4 * ci)) & 15u;
-            for (uint32_t k = 0; k < cnt; ++k, unit += kPrimUnits) test_prim(pool, unit, r, best);
-        }
-        const float tcull = cull_bound(best);
-        // sort the interior children by entry distance (network of 5 compare-swaps), cull, descend
-        cswap(ctn[0], coff[0], ctn[1], coff[1]);
-        cswap(ctn[2], coff[2], ctn[3], coff[3]);
-        cswap(ctn[0], coff[0], ctn[2], coff[2]);
-        cswap(ctn[1], coff[1], ctn[3], coff[3]);
-        cswap(ctn[1], coff[1], ctn[2], coff[2]);
-        // (non-hit children carry +inf, which is never <= a finite bound; with no hit yet the bound is
-        // +inf, so test finiteness explicitly)
-#pragma unroll
-        for (int ci = 3; ci >= 1; --ci)
-            if (ctn[ci] < CUDART_INF_F && ctn[ci] <= tcull) stack[sp++] = make_uint2(coff[ci], __float_as_uint(ctn[ci]));
-        if (ctn[0] < CUDART_INF_F && ctn[0] <= tcull) {
-            cur = coff[0];
-            continue;
-        }
-        bool found = false;
+    // While-while traversal with postponed leaves (Aila & Laine 2009): interior nodes are visited until
+    // every lane of the warp holds a leaf (or has finished), then the lanes test their leaves'
+    // primitives together, so the primitive test runs warp-convergent. Box culling uses the best hit
+    // at the time an entry is popped or visited; it only drops boxes entered strictly beyond a
+    // conservative bound of the best t (reading R11), so the visiting order never changes the result.
+    uint32_t cur = 0;
+    float cur_t = -CUDART_INF_F;
+    uint32_t leaf = kNoEntry;
+    float leaf_t = 0.0f;
+    auto pop = [&](float tcull) -> uint32_t {
         while (sp > 0) {
             const uint2 e = stack[--sp];
-            if (__uint_as_float(e.y) <= tcull) { cur = e.x; found = true; break; }
+            if (__uint_as_float(e.y) <= tcull) {
+                cur_t = __uint_as_float(e.y);
+                return e.x;
+            }
         }
-        if (!found) break;
+        return kNoEntry;
+    };
+    for (;;) {
+        // ---- phase 1: interior nodes --------------------------------------------------------------
+        while (is_node(cur)) {
+            const float tcull0 = cull_bound(best);
+            if (cur_t > tcull0) {          // entered beyond the best hit found since it was pushed
+                cur = pop(tcull0);
+            } else {
+                TCOUNT(0, 1);
+                const uint4 h = __ldg(pool + cur);
+                const uint4 q0 = __ldg(pool + cur + 1), q1 = __ldg(pool + cur + 2), q2 = __ldg(pool + cur + 3);
+                const uint32_t w[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
+                const float O[3] = {__uint_as_float(h.x), __uint_as_float(h.y), __uint_as_float(h.z)};
+                uint32_t off = h.w;
+                // per-child results in registers (static indices only: no local-memory arrays)
+                float ctn[4];
+                uint32_t cent[4];
+#pragma unroll
+                for (int ci = 0; ci < 4; ++ci) {
+                    const uint32_t w0 = w[3 * ci], w1 = w[3 * ci + 1], w2 = w[3 * ci + 2];
+                    const bool valid = (w0 & 0x8000u) != 0;
+                    const bool lf = (w1 & 0x8000u) != 0;
+                    const uint32_t cm1 = ((w2 >> 15) & 1u) | ((w0 >> 30) & 2u);
+                    const uint32_t wa[3] = {w0 & 0x7FFF7FFFu, w1 & 0x7FFF7FFFu, w2 & 0x7FFF7FFFu};
+                    float tn = 0.0f, tf = CUDART_INF_F;
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        // (near, far) bounds of this axis: exact fp16 -> fp32, then the same rn ops as the
+                        // builder's check (the half swap only reorders the two lanes)
+                        const uint32_t ws = __byte_perm(wa[a], 0u, swz[a]);
+                        const float2 lh = __half22float2(*reinterpret_cast<const __half2*>(&ws));
+                        const float2 b = __fadd2_rn(make_float2(O[a], O[a]), lh);
+                        const float2 t = __fmul2_rn(__fadd2_rn(b, make_float2(-r.o[a], -r.o[a])),
+                                                    make_float2(r.inv[a], r.inv[a]));
+                        tn = fmaxf(tn, t.x);
+                        tf = fminf(tf, t.y);
+                    }
+                    tf = tf * kGrow;
+                    const bool hit = valid && tn <= tf && tn <= tcull0;
+                    ctn[ci] = hit ? tn : CUDART_INF_F;
+                    cent[ci] = lf ? (off | kLeafBit | (cm1 << 28)) : off;
+                    off += valid ? (lf ? kPrimUnits * (cm1 + 1u) : (uint32_t)kNodeUnits) : 0u;
+                }
+                // sort the children by entry distance (network of 5 compare-swaps), push all but the
+                // nearest (farthest first), descend into the nearest
+                cswap(ctn[0], cent[0], ctn[1], cent[1]);
+                cswap(ctn[2], cent[2], ctn[3], cent[3]);
+                cswap(ctn[0], cent[0], ctn[2], cent[2]);
+                cswap(ctn[1], cent[1], ctn[3], cent[3]);
+                cswap(ctn[1], cent[1], ctn[2], cent[2]);
+                // (non-hit children carry +inf; the bound may be +inf, so test finiteness explicitly)
+#pragma unroll
+                for (int ci = 3; ci >= 1; --ci)
+                    if (ctn[ci] < CUDART_INF_F) stack[sp++] = make_uint2(cent[ci], __float_as_uint(ctn[ci]));
+                if (ctn[0] < CUDART_INF_F) {
+                    cur = cent[0];
+                    cur_t = ctn[0];
+                } else {
+                    cur = pop(tcull0);
+                }
+            }
+            // postpone the first leaf reached and keep traversing until the whole warp holds one
+            if (is_leaf(cur) && leaf == kNoEntry) {
+                leaf = cur;
+                leaf_t = cur_t;
+                cur = pop(cull_bound(best));
+            }
+            if (!__any_sync(__activemask(), leaf == kNoEntry)) break;
+        }
+        // ---- phase 2: primitives of the postponed leaf (and of leaves met next) ---------------------
+        while (leaf != kNoEntry) {
+            if (leaf_t <= cull_bound(best)) {
+                const uint32_t cnt = ((leaf >> 28) & 3u) + 1u;
+                uint32_t unit = leaf & 0x0FFFFFFFu;
+                for (uint32_t k = 0; k < cnt; ++k, unit += kPrimUnits) test_prim(pool, unit, r, best);
+            }
+            leaf = kNoEntry;
+            if (is_leaf(cur)) {
+                leaf = cur;
+                leaf_t = cur_t;
+                cur = pop(cull_bound(best));
+            }
+        }
+        if (cur == kNoEntry) break;
     }
     // the fp32 sphere t can lose ~1e-5 (disc cancellation): refine the winner's t in fp64 so the
     // spawn point stays well inside the 1e-4 self-intersection offset (reading R10)
@@ -454,20 +490,6 @@ __global__ void __launch_bounds__(256) raygen_kernel(Cam32 cam, int W, int H, in
         B[slot] = make_float4(d.x, d.y, d.z, 1.0f);
         C[slot] = make_float2(1.0f, 1.0f);
     }
-}
-
-__device__ __forceinline__ void equirect_f32(float3 d, float& u, float& v) {
-    // SPEC.md:438 convention (reading R14): u = 0.5 + atan2(d.x, -d.z)/2pi wrapped to [0,1); v = acos(d.y)/pi
-    const float len = sqrtf(d.x * d.x + d.y * d.y + d.z * d.z);
-    float uu;
-    if (d.x == 0.0f && d.z == 0.0f) uu = 0.5f;
-    else {
-        uu = 0.5f + atan2f(d.x, -d.z) * (0.5f / CUDART_PI_F);
-        if (uu >= 1.0f) uu -= 1.0f;
-    }
-    const float y = fminf(1.0f, fmaxf(-1.0f, d.y / len));
-    u = uu;
-    v = acosf(y) * (1.0f / CUDART_PI_F);
 }
 
 // warp-aggregated append: one atomic per warp (Guideline 12), returns this lane's slot
@@ -519,7 +541,6 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) trace_shade_kernel(ShadeArgs 
         bool alive = false, escaped = false;
         uint32_t slot = 0;
         float3 o3 = make_float3(0, 0, 0), wi = make_float3(0, 0, 0), bt = make_float3(0, 0, 0);
-        float eu = 0.0f, ev = 0.0f;
         if (active) {
             const float4 o = __ldg(a.A_in + i), d4 = __ldg(a.B_in + i);
             const float2 c2 = __ldg(a.C_in + i);
@@ -532,7 +553,8 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) trace_shade_kernel(ShadeArgs 
             bool done = true;
             if (prim < 0) {                                   // escaped: environment light
                 if (a.use_nif) {
-                    equirect_f32(d, eu, ev);
+                    // queued by direction; the NIF kernel maps it to equirect (u, v) (S4 -> S5)
+                    wi = d;
                     escaped = true;
                     done = false;
                 } else {
@@ -645,7 +667,7 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) trace_shade_kernel(ShadeArgs 
             a.C_out[pos_a] = make_float2(bt.y, bt.z);
         }
         if (escaped) {
-            a.esc[pos_e] = make_float4(eu, ev, __uint_as_float(slot), 0.0f);
+            a.esc[pos_e] = make_float4(wi.x, wi.y, wi.z, __uint_as_float(slot));
             a.esc_beta[pos_e] = make_float4(bt.x, bt.y, bt.z, 0.0f);
         }
     }
@@ -687,7 +709,7 @@ __global__ void scale_kernel(float* fb, int64_t n, float s) {
 
 __global__ void pack_queries_kernel(const float* uv, int64_t n, float4* esc, float4* esc_beta, uint32_t* count) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        esc[i] = make_float4(uv[2 * i], uv[2 * i + 1], __uint_as_float((uint32_t)i), 0.0f);
+        esc[i] = make_float4(uv[2 * i], uv[2 * i + 1], 0.0f, __uint_as_float((uint32_t)i));
         esc_beta[i] = make_float4(1.0f, 1.0f, 1.0f, 0.0f);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) *count = (uint32_t)n;
