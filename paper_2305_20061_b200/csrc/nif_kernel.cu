@@ -1,18 +1,17 @@
-// nif_kernel.cu -- fused HDR-NIF inference on sm_100a tensor cores (tcgen05 + TMEM).
+// nif_kernel.cu -- the paper's own HDR-NIF (PT_NIF_FOURIER_RELU) fused on sm_100a tensor cores
+// (tcgen05 + TMEM); the SIREN NIF of the hot path is siren_kernel.cu.
 //
-// What it computes (BASELINE.json SIREN; readings R1-R3, R15):
-//   for every escaped ray with equirect (u, v) and throughput beta:
-//     x0 = (2u-1, 2v-1); h1 = sin(W1' x0 + b1'); h_{k+1} = sin(W'_{k+1} h_k + b'_{k+1}) (k = 1..3);
-//     y = W5 h4 + b5; radiance += beta * exp(y)        (written to the path's own wave slot)
-// The paper runs the batched MLP with Poplibs matmuls spread over the chip; here
-// one persistent CTA per SM keeps the whole fp16 weight set resident in shared memory (loaded once by
-// a bulk TMA copy), and runs each layer of a 128-ray tile as tcgen05.mma kind::f16 (M=128, N=128,
-// K=16 steps) with fp32 accumulators in TMEM and the fp16 activations written back to TMEM as the A
-// operand of the next layer (A-from-TMEM), so activations never touch shared memory or registers
-// beyond one 32-column chunk. Biases ride in the MMA as an extra K=16 step against a constant-1
-// column, the layer-1 input is a K=16 step with an fp16 hi/lo split of x0 (reading R15). Two tiles
-// are in flight per CTA: the tensor core runs one tile's layer while 8 epilogue warps apply the sine
-// to the other's accumulator.
+// What it computes (reading R4): for every escaped ray with equirect (u, v)
+// and throughput beta: Fourier features (sin, cos)(2 pi B (u, v)) (F = 20 frequencies) -> 4 ReLU layers
+// of width 128 with the features concatenated again after the second (layer 1 has 88 units) -> linear
+// (Y, U, V) -> fixed BT.601 YUV -> RGB -> exp; radiance = beta * exp(rgb).
+// One persistent CTA per SM keeps the fp16 weight set resident in shared memory (one bulk TMA copy);
+// each layer of a 128-ray tile is a chain of tcgen05.mma kind::f16 (M = 128, K = 16 steps) with fp32
+// accumulators in TMEM and the fp16 activations written back to TMEM as the next layer's A operand.
+// Biases ride in the MMA as an extra K step against a constant-1 column in shared memory. Two tiles are
+// in flight per CTA; each layer is issued as two column halves with their own commit barriers so the
+// low-half epilogue overlaps the high-half MMAs. The feature columns stay in A buffer 0 (columns
+// 44..63) for the concat skip, so A is double-buffered per slot.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
@@ -23,6 +22,7 @@
 #include <vector>
 
 #include "pt_internal.h"
+#include "tc_ptx.cuh"
 
 namespace pt {
 
@@ -30,17 +30,7 @@ namespace nif {
 
 constexpr int kHid = 128;
 constexpr int kTileM = 128;
-// shared-memory image: K-major operand tiles, SWIZZLE_NONE canonical layout
-//   core matrix (nb, kb) = rows 8nb..8nb+7 x k 8kb..8kb+7, 128 B, at ((kb * N/8) + nb) * 128
-constexpr int kB1Bytes = 128 * 16 * 2;        // layer 1: N=128, K=16
-constexpr int kBHBytes = 128 * 144 * 2;       // layers 2-4: N=128, K=128 + 16 (bias step)
-constexpr int kB5Bytes = 16 * 144 * 2;        // layer 5: N=16 (3 used), K=144
-constexpr int kOffB1 = 0;
-constexpr int kOffB2 = kOffB1 + kB1Bytes;
-constexpr int kOffB5 = kOffB2 + 3 * kBHBytes;
-constexpr int kOffOnes = kOffB5 + kB5Bytes;      // A operand of the bias K step: [128][16], row = (1, 0, ...)
 constexpr int kOnesBytes = 128 * 16 * 2;
-constexpr int kImageBytes = kOffOnes + kOnesBytes;   // 123,392
 // The paper's own NIF (kind 1: Fourier features + ReLU + concat skip + YUV->RGB, reading R4):
 //   B0: N=128, K=48 (+16 bias) -- K' 0..7 zero, K' 8+2j / 9+2j = weights of sin_j / cos_j
 //   B1: N=96 (88 used), K=128 (+16); B2: N=128, K = [h1 (88), (sin_j, cos_j) interleaved (40)] (+16)
@@ -53,17 +43,8 @@ constexpr int kFrOffB4 = kFrOffB3 + 128 * 144 * 2;
 constexpr int kFrOffOnes = kFrOffB4 + 16 * 144 * 2;
 constexpr int kFrOffFreq = kFrOffOnes + kOnesBytes;
 constexpr int kFrImageBytes = kFrOffFreq + 20 * 2 * 4;   // 126,624
-constexpr int kImageMax = kFrImageBytes > kImageBytes ? kFrImageBytes : kImageBytes;
-// barriers: [0] weights, [1..4] a_ready[slot][half], [5..8] d_full[slot][half], [9..10] a0_full[slot],
-// [11..12] a0_empty[slot]; TMEM base address at byte 120
-constexpr int kBarBytes = 128;
-// SIREN layer-1 A tiles staged in shared memory by the producer warps (one 128x16 fp16 K-major tile per
-// slot: row m = (x_hi, y_hi, x_lo, y_lo, 1, 0, 0, 0) at 16 m, k = 8..15 zero at 2048 + 16 m)
-constexpr int kA0Bytes = 128 * 16 * 2;
-constexpr int kOffA0 = ((kImageMax + kBarBytes + 1023) / 1024) * 1024;
-constexpr int kSmemBytes = kOffA0 + 2 * kA0Bytes + 128;
-constexpr int kProducerWarp0 = 2;                  // warps 2-3 stage the layer-1 inputs (SIREN)
-constexpr int kProducerThreads = 64;
+constexpr int kBarBytes = 80;   // [0] weights, [1..4] a_ready[slot][half], [5..8] d_full[slot][half]; TMEM at +72
+constexpr int kSmemBytes = kFrImageBytes + kBarBytes + 128;
 
 constexpr int kNumEpiWarps = 16;                   // 4 per TMEM lane quarter, 32 columns each
 constexpr int kEpiArrivals = kNumEpiWarps;         // arrivals per a_ready phase
@@ -90,47 +71,6 @@ inline void put_core(std::vector<uint8_t>& img, int base, int N, int n, int k, u
 }
 
 }  // namespace nif
-
-int64_t nif_smem_image_bytes() { return nif::kImageBytes; }
-
-// Re-lay the fp16 blob (layer l: W_l[out][in] then b_l[out]) into the kernel's shared-memory image.
-void nif_build_smem_image(const uint16_t* blob, std::vector<uint8_t>* image) {
-    using namespace nif;
-    std::vector<uint8_t>& img = *image;
-    img.assign(kImageBytes, 0);
-    const uint16_t one = 0x3C00;
-    (void)one;
-    size_t off = 0;
-    // layer 1: W1 [128][2], b1 [128]  -> B1 row n = (W n0, W n1, W n0, W n1, b n, 0...)
-    const uint16_t* W1 = blob + off; off += 128 * 2;
-    const uint16_t* b1 = blob + off; off += 128;
-    for (int n = 0; n < 128; ++n) {
-        put_core(img, kOffB1, 128, n, 0, W1[2 * n + 0]);
-        put_core(img, kOffB1, 128, n, 1, W1[2 * n + 1]);
-        put_core(img, kOffB1, 128, n, 2, W1[2 * n + 0]);
-        put_core(img, kOffB1, 128, n, 3, W1[2 * n + 1]);
-        put_core(img, kOffB1, 128, n, 4, b1[n]);
-    }
-    // layers 2-4: W [128][128] + bias at k = 128
-    for (int l = 0; l < 3; ++l) {
-        const uint16_t* W = blob + off; off += 128 * 128;
-        const uint16_t* b = blob + off; off += 128;
-        const int base = kOffB2 + l * kBHBytes;
-        for (int n = 0; n < 128; ++n) {
-            for (int k = 0; k < 128; ++k) put_core(img, base, 128, n, k, W[n * 128 + k]);
-            put_core(img, base, 128, n, 128, b[n]);
-        }
-    }
-    // layer 5: W5 [3][128], b5 [3]  -> N padded to 16
-    const uint16_t* W5 = blob + off; off += 3 * 128;
-    const uint16_t* b5 = blob + off; off += 3;
-    for (int n = 0; n < 3; ++n) {
-        for (int k = 0; k < 128; ++k) put_core(img, kOffB5, 16, n, k, W5[n * 128 + k]);
-        put_core(img, kOffB5, 16, n, 128, b5[n]);
-    }
-    // constant-1 A tile of the bias step (M = 128 rows, K = 16)
-    for (int m = 0; m < 128; ++m) put_core(img, kOffOnes, 128, m, 0, 0x3C00);
-}
 
 // The paper's NIF (blob: B[20][2], then W[out][in], b[out] of the 5 layers) -> kind-1 smem image.
 void nif_build_smem_image_fr(const uint16_t* blob, std::vector<uint8_t>* image) {
@@ -192,238 +132,35 @@ void nif_build_smem_image_fr(const uint16_t* blob, std::vector<uint8_t>* image) 
 }
 
 // ---------------------------------------------------------------------------------------------
-// PTX wrappers
-// ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t phase) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(bar), "r"(phase)
-        : "memory");
-    return ok != 0;
-}
-// bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
-    if (mbar_try(bar, phase)) return;
-    const long long t0 = clock64();
-    while (!mbar_try(bar, phase)) {
-        if (clock64() - t0 > 4000000000ll) __trap();
-    }
-}
-
-__device__ __forceinline__ bool elect_one() {
-    uint32_t pred = 0;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "elect.sync _|p, 0xffffffff;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(pred));
-    return pred != 0;
-}
-
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
-    // SWIZZLE_NONE K-major canonical layout; version bits [46,48) = 1 (sm_100)
-    uint64_t d = 0;
-    d |= (uint64_t)((addr >> 4) & 0x3FFFu);
-    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
-    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
-    d |= (uint64_t)1 << 46;
-    return d;
-}
-
-__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t id, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
-        ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(id), "r"(acc)
-        : "memory");
-}
-__device__ __forceinline__ void mma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t id, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
-        ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(id), "r"(acc)
-        : "memory");
-}
-__device__ __forceinline__ void mma_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
-}
-
-#define TMEM_LD32(taddr, v)                                                                                        \
-    asm volatile(                                                                                                  \
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18," \
-        "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                              \
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),          \
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),    \
-          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),  \
-          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])   \
-        : "r"(taddr))
-
-#define TMEM_ST16(taddr, v)                                                                                        \
-    asm volatile(                                                                                                  \
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"   \
-        ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),      \
-        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])              \
-        : "memory")
-
-__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
-                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
-                 : "memory");
-}
-__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t* v) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
-                 : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-
-__device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
-    const __half2 h = __floats2half2_rn(lo, hi);
-    return *reinterpret_cast<const uint32_t*>(&h);
-}
-
-// wait for all prior tcgen05.ld of this thread; the register operands pin later uses of v after it
-__device__ __forceinline__ void tmem_wait_ld_dep(uint32_t* v) {
-    asm volatile("tcgen05.wait::ld.sync.aligned;"
-                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
-                   "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]),
-                   "+r"(v[15]), "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]),
-                   "+r"(v[22]), "+r"(v[23]), "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]),
-                   "+r"(v[29]), "+r"(v[30]), "+r"(v[31])
-                 :
-                 : "memory");
-}
-
-__device__ __forceinline__ void tmem_wait_ld_dep4(uint32_t* v) {
-    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]) : : "memory");
-}
-
-// Sine epilogue, split between two pipes: the SFU (MUFU.SIN, 16 lanes/clk/SM) and
-// the FMA pipe, where sin runs as an fp16x2 odd polynomial after an fp32 quarter-period reduction
-// w = |frac(x/2pi + 1/4)| - 1/4, sin(x) = sin(2 pi w), |w| <= 1/4 (max abs error 1.1e-3 in fp16).
-#ifndef PT_NIF_MUFU_PAIRS
-#define PT_NIF_MUFU_PAIRS 9   // of the 16 column pairs of a 32-column chunk, on the SFU
-#endif
-__device__ __forceinline__ uint32_t sin2_poly(float a, float b) {
-    // packed fp32x2 range reduction (FFMA2/FADD2, sm_100), then an fp16x2 odd polynomial
-    constexpr float kInv2Pi = 0.15915494309189535f;
-    constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23: x + magic - magic = rint(x)
-    const float2 sv = __ffma2_rn(make_float2(a, b), make_float2(kInv2Pi, kInv2Pi), make_float2(0.25f, 0.25f));
-    const float2 tv = __fadd2_rn(sv, make_float2(kMagic, kMagic));
-    const float2 kv = __fadd2_rn(tv, make_float2(-kMagic, -kMagic));
-    const float2 uv = __fadd2_rn(sv, make_float2(-kv.x, -kv.y));
-    const float2 wv = __fadd2_rn(make_float2(fabsf(uv.x), fabsf(uv.y)), make_float2(-0.25f, -0.25f));
-    const __half2 w = __floats2half2_rn(wv.x, wv.y);
-    const __half2 w2 = __hmul2(w, w);
-    const __half2 c1 = __halves2half2(__ushort_as_half(0x4648), __ushort_as_half(0x4648));   //  6.28125
-    const __half2 c3 = __halves2half2(__ushort_as_half(0xD123), __ushort_as_half(0xD123));   // -41.09375
-    const __half2 c5 = __halves2half2(__ushort_as_half(0x5499), __ushort_as_half(0x5499));   //  73.5625
-    __half2 p = __hfma2(w2, c5, c3);
-    p = __hfma2(p, w2, c1);
-    const __half2 r = __hmul2(p, w);
-    return *reinterpret_cast<const uint32_t*>(&r);
-}
-__device__ __forceinline__ void sine_chunk(const uint32_t* v, uint32_t* p) {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        const float a = __uint_as_float(v[2 * j]), b = __uint_as_float(v[2 * j + 1]);
-        p[j] = j < PT_NIF_MUFU_PAIRS ? pack_half2(__sinf(a), __sinf(b)) : sin2_poly(a, b);
-    }
-}
-
-// ---------------------------------------------------------------------------------------------
 // The fused kernel
 // ---------------------------------------------------------------------------------------------
-#ifdef PT_NIF_TRACE
-// timing trace of CTA 0 (variant builds only): [role][record][2] clock64 stamps
-__device__ unsigned long long g_nif_trace[3 * 4096 * 2];
-#define NIF_TRACE(role, rec, k)                                                                  \
-    do {                                                                                         \
-        if (blockIdx.x == 0 && (rec) < 4096) g_nif_trace[((role) * 4096 + (rec)) * 2 + (k)] = clock64(); \
-    } while (0)
-#else
-#define NIF_TRACE(role, rec, k) \
-    do {                        \
-    } while (0)
-#endif
-
-// Equirect map of an escaped direction (S4 -> S5; moved here from the trace kernel so the divergent
-// atan2/acos run once per queued ray in the NIF prologue instead of in the traversal warps)
-__device__ __forceinline__ void equirect_f32(float3 d, float& u, float& v) {
-    // SPEC.md:438 convention (reading R14): u = 0.5 + atan2(d.x, -d.z)/2pi wrapped to [0,1); v = acos(d.y)/pi
-    const float len = sqrtf(d.x * d.x + d.y * d.y + d.z * d.z);
-    float uu;
-    if (d.x == 0.0f && d.z == 0.0f) uu = 0.5f;
-    else {
-        uu = 0.5f + atan2f(d.x, -d.z) * (0.5f / CUDART_PI_F);
-        if (uu >= 1.0f) uu -= 1.0f;
-    }
-    const float y = fminf(1.0f, fmaxf(-1.0f, d.y / len));
-    u = uu;
-    v = acosf(y) * (1.0f / CUDART_PI_F);
-}
-
-// ReLU epilogue of the paper's NIF: relu + fp16x2 pack in one cvt per pair
-__device__ __forceinline__ uint32_t relu_pack(float lo, float hi) {
-    uint32_t r;
-    asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
-    return r;
-}
-
-// Per-layer MMA layout of a kind (SIREN 0 / paper NIF 1): B tile base, K-direction core-matrix stride
-// (LBO = N/8 * 128 B), N of the low and high column halves.
+// Per-layer MMA layout: B tile base, K-direction core-matrix stride (LBO = N/8 * 128 B), N of the low and
+// high column halves.
 struct LayerDesc {
     uint32_t base, lbo;
     int n_lo, n_hi;
 };
-template <int kKind>
 __device__ __forceinline__ LayerDesc layer_desc(int layer) {
     using namespace nif;
-    if (kKind == 0) {
-        if (layer == 4) return {(uint32_t)kOffB5, 256u, 16, 0};
-        return {(uint32_t)(kOffB2 + (layer - 1) * kBHBytes), 2048u, 64, 64};
-    } else {
-        if (layer == 1) return {(uint32_t)kFrOffB1, 1536u, 64, 32};
-        if (layer == 2) return {(uint32_t)kFrOffB2, 2048u, 64, 64};
-        if (layer == 3) return {(uint32_t)kFrOffB3, 2048u, 64, 64};
-        return {(uint32_t)kFrOffB4, 256u, 16, 0};
-    }
+    if (layer == 1) return {(uint32_t)kFrOffB1, 1536u, 64, 32};
+    if (layer == 2) return {(uint32_t)kFrOffB2, 2048u, 64, 64};
+    if (layer == 3) return {(uint32_t)kFrOffB3, 2048u, 64, 64};
+    return {(uint32_t)kFrOffB4, 256u, 16, 0};
 }
 
-template <int kKind, bool kDebug>
+template <bool kDebug>
 __global__ void __launch_bounds__(nif::kThreads, 1)
-    nif_fused_kernel(const uint8_t* __restrict__ g_image, const float4* __restrict__ esc,
+    nif_fr_kernel(const uint8_t* __restrict__ g_image, const float4* __restrict__ esc,
                      const float4* __restrict__ esc_beta, const uint32_t* __restrict__ count, float* __restrict__ out,
                      float* __restrict__ dbg, int dir_input) {
     using namespace nif;
-    constexpr int kImg = kKind == 0 ? kImageBytes : kFrImageBytes;
-    constexpr uint32_t kOnesOff = kKind == 0 ? kOffOnes : kFrOffOnes;
+    constexpr int kImg = kFrImageBytes;
+    constexpr uint32_t kOnesOff = kFrOffOnes;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* image = smem;
     // [0] weights, [1..4] a_ready[slot][column half], [5..8] d_full[slot][column half]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kImageMax);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kImageMax + 120);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kFrImageBytes);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kFrImageBytes + 72);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -435,8 +172,6 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
         mbar_init(bar_w, 1);
         for (int b = 1; b < 5; ++b) mbar_init(smem_u32(&bars[b]), kEpiArrivals / 2);
         for (int b = 5; b < 9; ++b) mbar_init(smem_u32(&bars[b]), 1);
-        for (int b = 9; b < 11; ++b) mbar_init(smem_u32(&bars[b]), kProducerThreads);
-        for (int b = 11; b < 13; ++b) mbar_init(smem_u32(&bars[b]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
@@ -473,7 +208,6 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
             const uint32_t img = smem_u32(image);
             const uint64_t ones = smem_desc(img + kOnesOff, 2048, 128);
             uint32_t a_phase[2] = {0, 0};
-            uint32_t a0_phase[2] = {0, 0};
             for (uint32_t i = 0;; i += 2) {
                 const uint32_t t0 = blockIdx.x + i * gridDim.x;
                 if (t0 >= n_tiles) break;
@@ -485,41 +219,25 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
                         const uint32_t dt = tmem + d_col(s);
                         const uint32_t at = tmem + a_col(s, layer & 1);
                         mbar_wait(bar_alo, a_phase[s]);
-                        if (lane == 0) NIF_TRACE(0, ((i / 2) * 5 + layer) * 2 + s, 0);
                         tc_fence_after();
                         if (layer == 0) {
                             mbar_wait(bar_ahi, a_phase[s]);
                             tc_fence_after();
-                            if (kKind == 0) {
-                                mbar_wait(smem_u32(&bars[9 + s]), a0_phase[s]);   // staged by the producers
-                                a0_phase[s] ^= 1;
-                                tc_fence_after();
-                            }
                             if (elect_one()) {
-                                if (kKind == 0) {
-                                    // x0 hi/lo + constant-1 bias column in one K=16 step, A from shared memory
-                                    const uint64_t a0 = smem_desc(smem_u32(smem + kOffA0 + s * kA0Bytes), 2048, 128);
-                                    mma_ss(dt, a0, smem_desc(img + kOffB1, 2048, 128), idesc(64), 0);
-                                    mma_commit(bar_lo);
-                                    mma_ss(dt + 64, a0, smem_desc(img + kOffB1 + 1024, 2048, 128), idesc(64), 0);
-                                    mma_commit(bar_hi);
-                                    mma_commit(smem_u32(&bars[11 + s]));             // staging buffer free
-                                } else {
-                                    // Fourier features in A columns 40..63 (K' 0..47) + bias step
+                                // Fourier features in A columns 40..63 (K' 0..47) + bias step
 #pragma unroll
-                                    for (int half = 0; half < 2; ++half) {
-                                        const uint32_t b0 = img + kFrOffB0 + 1024 * half;
+                                for (int half = 0; half < 2; ++half) {
+                                    const uint32_t b0 = img + kFrOffB0 + 1024 * half;
 #pragma unroll
-                                        for (int k = 0; k < 3; ++k)
-                                            mma_ts(dt + 64 * half, at + 40 + 8 * k, smem_desc(b0 + k * 2 * 2048, 2048, 128),
-                                                   idesc(64), k > 0);
-                                        mma_ss(dt + 64 * half, ones, smem_desc(b0 + 6 * 2048, 2048, 128), idesc(64), 1);
-                                        mma_commit(half ? bar_hi : bar_lo);
-                                    }
+                                    for (int k = 0; k < 3; ++k)
+                                        mma_ts(dt + 64 * half, at + 40 + 8 * k, smem_desc(b0 + k * 2 * 2048, 2048, 128),
+                                               idesc(64), k > 0);
+                                    mma_ss(dt + 64 * half, ones, smem_desc(b0 + 6 * 2048, 2048, 128), idesc(64), 1);
+                                    mma_commit(half ? bar_hi : bar_lo);
                                 }
                             }
                         } else {
-                            const LayerDesc L = layer_desc<kKind>(layer);
+                            const LayerDesc L = layer_desc(layer);
                             const uint32_t base = img + L.base, lbo = L.lbo;
                             const uint32_t id_lo = idesc(L.n_lo);
                             if (elect_one()) {
@@ -549,51 +267,8 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
                         }
                         a_phase[s] ^= 1;
                         __syncwarp();
-                        if (lane == 0) NIF_TRACE(0, ((i / 2) * 5 + layer) * 2 + s, 1);
                     }
                 }
-            }
-        }
-    } else if (kKind == 0 && (warp == kProducerWarp0 || warp == kProducerWarp0 + 1)) {
-        // ===== producers: layer-1 inputs of every tile, staged one tile ahead per slot =====
-        // queue entry -> (u, v) (equirect of the escape direction for the render queue, reading R14)
-        // -> x0 = (2u-1, 2v-1) split into fp16 hi + lo (reading R15), constant-1 bias column.
-        const int p = threadIdx.x - 32 * kProducerWarp0;
-        uint8_t* a0s = smem + kOffA0;
-        for (int i = p; i < 2 * kA0Bytes / 16; i += kProducerThreads)
-            *reinterpret_cast<uint4*>(a0s + 16 * i) = make_uint4(0, 0, 0, 0);
-        uint32_t e_phase[2] = {0, 0};
-        uint32_t fills[2] = {0, 0};
-        for (uint32_t i = 0;; i += 2) {
-            const uint32_t t0 = blockIdx.x + i * gridDim.x;
-            if (t0 >= n_tiles) break;
-            const int nslots = (t0 + gridDim.x < n_tiles) ? 2 : 1;
-            for (int s = 0; s < nslots; ++s) {
-                const uint32_t tile = t0 + s * gridDim.x;
-                if (fills[s]++ > 0) {
-                    mbar_wait(smem_u32(&bars[11 + s]), e_phase[s]);
-                    e_phase[s] ^= 1;
-                }
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int m = p + 64 * h;
-                    const uint32_t row = tile * kTileM + m;
-                    float u = 0.5f, v = 0.5f;
-                    if (row < n_rows) {
-                        const float4 en = __ldg(esc + row);
-                        u = en.x;
-                        v = en.y;
-                        if (dir_input) equirect_f32(make_float3(en.x, en.y, en.z), u, v);
-                    }
-                    const float x = 2.0f * u - 1.0f, y = 2.0f * v - 1.0f;
-                    const __half xh = __float2half_rn(x), yh = __float2half_rn(y);
-                    const __half xl = __float2half_rn(x - __half2float(xh)), yl = __float2half_rn(y - __half2float(yh));
-                    *reinterpret_cast<uint4*>(a0s + s * kA0Bytes + 16 * m) = make_uint4(
-                        (uint32_t)__half_as_ushort(xh) | ((uint32_t)__half_as_ushort(yh) << 16),
-                        (uint32_t)__half_as_ushort(xl) | ((uint32_t)__half_as_ushort(yl) << 16), 0x00003C00u, 0u);
-                }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic -> async proxy
-                mbar_arrive(smem_u32(&bars[9 + s]));
             }
         }
     } else if (warp >= kFirstEpiWarp) {
@@ -605,16 +280,13 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
         const int cb = e >> 2;                        // column block 0..3
         const int q = warp & 3;                       // TMEM lane quarter
         const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
-        const bool row_warp = kKind == 1 || cb == 0;  // warps that need the queue entry of their rows
         const float* freq = reinterpret_cast<const float*>(image + kFrOffFreq);
         uint32_t d_phase[2] = {0, 0};
         float4 ent[2] = {make_float4(0.5f, 0.5f, 0.0f, 0.0f), make_float4(0.5f, 0.5f, 0.0f, 0.0f)};
         auto row_of = [&](uint32_t tile) { return tile * kTileM + 32 * q + lane; };
         auto write_a0 = [&](int s, float4 en) {
             const uint32_t a0 = tmem + a_col(s, 0) + lane_addr;
-            if (kKind == 0) {
-                return;   // SIREN: the layer-1 tile is staged in shared memory by the producer warps
-            } else {
+            {
                 // Fourier features (sin_j, cos_j) of 2 pi B_j.(u, v) into A column 44 + j; the four warps
                 // of a lane quarter split the 20 frequencies (4 / 8 / 8) and zero columns 40..43
                 auto feat = [&](int j) {
@@ -647,18 +319,16 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
         auto load_ent = [&](uint32_t tile) {
             const uint32_t row = row_of(tile);
             float4 en = (tile < n_tiles && row < n_rows) ? __ldg(esc + row) : make_float4(0.5f, 0.5f, 0.0f, 0.0f);
-            if (kKind == 1 && dir_input && tile < n_tiles && row < n_rows)
+            if (dir_input && tile < n_tiles && row < n_rows)
                 equirect_f32(make_float3(en.x, en.y, en.z), en.x, en.y);
             return en;
         };
-        // prologue: layer-1 inputs of the first tile pair (weights must be resident for kind 1)
-        if (kKind == 1 && blockIdx.x < n_tiles) mbar_wait(bar_w, 0);
+        // prologue: layer-1 inputs of the first tile pair (the frequencies are part of the weight image)
+        if (blockIdx.x < n_tiles) mbar_wait(bar_w, 0);
         for (int s = 0; s < 2; ++s) {
             const uint32_t tile = blockIdx.x + s * gridDim.x;
-            if (row_warp) {
-                ent[s] = load_ent(tile);
-                if (tile < n_tiles) write_a0(s, ent[s]);
-            }
+            ent[s] = load_ent(tile);
+            if (tile < n_tiles) write_a0(s, ent[s]);
         }
         tmem_wait_st();
         tc_fence_before();
@@ -674,13 +344,11 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
             // prefetch: this pair's throughputs (cb == 0) and the next pair's queue entries
             float4 beta[2] = {make_float4(0, 0, 0, 0), make_float4(0, 0, 0, 0)};
             float4 ent_next[2] = {ent[0], ent[1]};
-            if (row_warp) {
-                for (int s = 0; s < nslots; ++s) {
-                    const uint32_t tile = t0 + s * gridDim.x;
-                    const uint32_t row = row_of(tile);
-                    if (cb == 0 && row < n_rows) beta[s] = __ldg(esc_beta + row);
-                    ent_next[s] = load_ent(tile + 2 * gridDim.x);
-                }
+            for (int s = 0; s < nslots; ++s) {
+                const uint32_t tile = t0 + s * gridDim.x;
+                const uint32_t row = row_of(tile);
+                if (cb == 0 && row < n_rows) beta[s] = __ldg(esc_beta + row);
+                ent_next[s] = load_ent(tile + 2 * gridDim.x);
             }
             for (int layer = 0; layer < 5; ++layer) {
                 for (int s = 0; s < nslots; ++s) {
@@ -692,16 +360,14 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
                     const uint32_t dph = d_phase[s];
                     d_phase[s] ^= 1;
                     mbar_wait(smem_u32(&bars[5 + 2 * s + (cb >> 1)]), dph);
-                    const int trole = (warp == kFirstEpiWarp) ? 1 : (warp == kFirstEpiWarp + kNumEpiWarps - 1 ? 2 : -1);
-                    if (trole > 0 && lane == 0) NIF_TRACE(trole, ((i / 2) * 5 + layer) * 2 + s, 0);
                     tc_fence_after();
                     bool arrive = true;
                     if (layer < 4) {
-                        // hidden layer: D (fp32) -> activation -> fp16 -> A (this warp's 32 columns).
-                        // Paper NIF layer 1: only D columns 0..87 are units (A columns 0..43); A columns
-                        // 44..63 keep the Fourier features for the concat skip.
+                        // hidden layer: D (fp32) -> ReLU -> fp16 -> A (this warp's 32 columns). Layer 1:
+                        // only D columns 0..87 are units (A columns 0..43); A columns 44..63 keep the
+                        // Fourier features for the concat skip.
                         const int col = 32 * cb;
-                        const bool skip = kKind == 1 && layer == 1 && cb == 3;
+                        const bool skip = layer == 1 && cb == 3;
                         if (!skip) {
                             uint32_t v[32];
                             TMEM_LD32(dt + col, v);
@@ -711,14 +377,10 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
                                     dbg[((size_t)layer * n_rows + row) * kHid + col + j] = __uint_as_float(v[j]);
                             }
                             uint32_t p[16];
-                            if (kKind == 0) {
-                                sine_chunk(v, p);
-                            } else {
 #pragma unroll
-                                for (int j = 0; j < 16; ++j)
-                                    p[j] = relu_pack(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
-                            }
-                            if (kKind == 1 && layer == 1 && cb == 2) {
+                            for (int j = 0; j < 16; ++j)
+                                p[j] = relu_pack(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+                            if (layer == 1 && cb == 2) {
                                 tmem_st8(at + 32, p);        // units 64..79
                                 asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(at + 40),
                                              "r"(p[8]), "r"(p[9]), "r"(p[10]), "r"(p[11])
@@ -743,7 +405,7 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
                                     dbg[((size_t)4 * n_rows + row) * kHid + 1] = y1;
                                     dbg[((size_t)4 * n_rows + row) * kHid + 2] = y2;
                                 }
-                                if (kKind == 1) {
+                                {
                                     // fixed BT.601 YUV -> RGB colour layer, log space
                                     const float Y = y0, U = y1, V = y2;
                                     y0 = fmaf(1.13983f, V, Y);
@@ -755,16 +417,13 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
                                 out[3 * (size_t)slot + 2] = beta[s].z * __expf(y2);
                             }
                         }
-                        if (row_warp) {
-                            ent[s] = ent_next[s];
-                            if (next < n_tiles) write_a0(s, ent[s]);
-                        }
+                        ent[s] = ent_next[s];
+                        if (next < n_tiles) write_a0(s, ent[s]);
                         arrive = next < n_tiles;
                     }
                     tmem_wait_st();
                     tc_fence_before();
                     __syncwarp();
-                    if (trole > 0 && lane == 0) NIF_TRACE(trole, ((i / 2) * 5 + layer) * 2 + s, 1);
                     if (lane == 0 && arrive) mbar_arrive(smem_u32(&bars[1 + 2 * s + (cb >> 1)]));
                 }
             }
@@ -789,33 +448,35 @@ int num_sms() {
     return n;
 }
 
-template <int kKind, bool kDebug>
-static cudaError_t nif_launch_t(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,
-                                int grid, float* out, float* dbg, int dir_input, cudaStream_t st) {
+template <bool kDebug>
+static cudaError_t nif_fr_launch_t(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,
+                                   int grid, float* out, float* dbg, int dir_input, cudaStream_t st) {
     using namespace nif;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(nif_fused_kernel<kKind, kDebug>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaError_t e = cudaFuncSetAttribute(nif_fr_kernel<kDebug>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kSmemBytes);
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    nif_fused_kernel<kKind, kDebug><<<grid, kThreads, kSmemBytes, st>>>((const uint8_t*)nif->d_smem_image, esc,
-                                                                        esc_beta, count, out, dbg, dir_input);
+    nif_fr_kernel<kDebug><<<grid, kThreads, kSmemBytes, st>>>((const uint8_t*)nif->d_smem_image, esc, esc_beta, count,
+                                                               out, dbg, dir_input);
     return cudaGetLastError();
 }
 
+cudaError_t launch_siren(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count, int grid,
+                         float* out, float* dbg, int dir_input, cudaStream_t st);
+
+// one persistent CTA per SM (or per tile when there are fewer tiles); the row count is read on device
 static cudaError_t nif_launch_impl(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,
                                    int64_t max_rows, float* out, float* dbg, int dir_input, cudaStream_t st) {
-    using namespace nif;
-    int64_t tiles = (max_rows + kTileM - 1) / kTileM;
+    int64_t tiles = (max_rows + 127) / 128;
     int grid = num_sms();
     if (tiles < grid) grid = (int)(tiles > 0 ? tiles : 1);
     if (nif->kind == PT_NIF_FOURIER_RELU)
-        return dbg ? nif_launch_t<1, true>(nif, esc, esc_beta, count, grid, out, dbg, dir_input, st)
-                   : nif_launch_t<1, false>(nif, esc, esc_beta, count, grid, out, dbg, dir_input, st);
-    return dbg ? nif_launch_t<0, true>(nif, esc, esc_beta, count, grid, out, dbg, dir_input, st)
-               : nif_launch_t<0, false>(nif, esc, esc_beta, count, grid, out, dbg, dir_input, st);
+        return dbg ? nif_fr_launch_t<true>(nif, esc, esc_beta, count, grid, out, dbg, dir_input, st)
+                   : nif_fr_launch_t<false>(nif, esc, esc_beta, count, grid, out, dbg, dir_input, st);
+    return launch_siren(nif, esc, esc_beta, count, grid, out, dbg, dir_input, st);
 }
 
 cudaError_t launch_nif(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,
@@ -829,9 +490,3 @@ cudaError_t launch_nif_debug(const pt_nif* nif, const float4* esc, const float4*
 }
 
 }  // namespace pt
-
-#ifdef PT_NIF_TRACE
-extern "C" __attribute__((visibility("default"))) int pt_debug_nif_trace(unsigned long long* host_out) {
-    return (int)cudaMemcpyFromSymbol(host_out, pt::g_nif_trace, sizeof(pt::g_nif_trace));
-}
-#endif

@@ -1,6 +1,6 @@
 #!/usr/bin/env python
-"""Run the trace build of the NIF kernel (PT_NIF_TRACE) and print the per-step timeline of CTA 0:
-MMA wait/issue stamps and epilogue wake/done stamps (cycles)."""
+"""Run the trace build of the SIREN NIF kernel (PT_NIF_TRACE) and print the per-step timeline of CTA 0:
+MMA wait/issue stamps and epilogue wake/done stamps (cycles); 5 MMA stages per tile (the epilogue columns are empty for layer 5), 2 slots."""
 import ctypes as C
 import os
 import sys
@@ -24,7 +24,7 @@ pt.lib().pt_debug_nif_trace(C.c_void_p(buf.ctypes.data))
 tr = buf.reshape(3, 4096, 2).astype(np.int64)
 nrec = int((tr[0, :, 1] > 0).sum())
 t0 = tr[0, 0, 0]
-print("rec  layer slot | mma_wait_done  mma_issued | epiA_wake epiA_done | epiB_wake epiB_done")
+print("rec  stage slot | mma_wait_done  mma_issued | epiA_wake epiA_done | epiB_wake epiB_done")
 for r in range(min(nrec, 60)):
     layer, s = (r // 2) % 5, r % 2
     row = [tr[0, r, 0] - t0, tr[0, r, 1] - t0, tr[1, r, 0] - t0, tr[1, r, 1] - t0, tr[2, r, 0] - t0, tr[2, r, 1] - t0]
