@@ -34,9 +34,27 @@ HIDDEN_FLOP_PER_INF = 3 * 2 * 128 * 128          # tensor-counted FLOPs per NIF 
 TOTAL_FLOP_PER_INF = 2 * (2 * 128 + 3 * 128 * 128 + 128 * 3)
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 L2_READ_GBS = 16409.6                       # tools/l2_bench.cu on this pool's B200 (profiles/round1/l2_bench.json)
-# algorithmic traversal bytes per traced segment, per config (counting build: 64 B x node visits +
-# 48 B x primitive tests + 80 B path state; profiles/round1/trace_count.json)
-TRACE_BYTES_PER_SEGMENT = {1: 300.0}
+PROFILES = os.path.join(ROOT, "profiles", "round1")
+
+
+def trace_bytes_per_segment(cfg_index: int):
+    """Algorithmic traversal bytes per traced segment of a config's render (counting build of the same
+    kernel, tools/trace_count.py: 64 B x node visits + 48 B x primitive tests + 80 B path state)."""
+    try:
+        with open(os.path.join(PROFILES, "trace_count.json")) as f:
+            return float(json.load(f)[f"render_c{cfg_index}"]["alg_bytes_per_segment"])
+    except Exception:
+        return None
+
+
+def ncu_traffic(kernel: str, cfg_index: int):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu capture of one bench step
+    (tools/ncu_traffic.py), or None."""
+    try:
+        with open(os.path.join(PROFILES, f"ncu_traffic_c{cfg_index}.json")) as f:
+            return float(json.load(f)[kernel]["dram_bytes_per_launch"])
+    except Exception:
+        return None
 
 
 def load_peaks():
@@ -306,8 +324,10 @@ def main():
     dominant = max(kernels, key=lambda n: kernels[n]["ms_per_step"])
     nif_tflops = (HIDDEN_FLOP_PER_INF * infers) / (nif_ms / 1e3) / 1e12 if nif_ms > 0 else 0.0
     nif_roof = {"bound": "tensor", "achieved": nif_tflops, "peak": peaks["bf16_tflops_sustained"],
-                "unit": "TFLOP/s", "frac": nif_tflops / peaks["bf16_tflops_sustained"], "traffic": None,
-                "kernel": "nif_fused_kernel", "flop_per_inference": HIDDEN_FLOP_PER_INF,
+                "unit": "TFLOP/s", "frac": nif_tflops / peaks["bf16_tflops_sustained"],
+                "frac_burst": nif_tflops / peaks["bf16_tflops"],
+                "traffic": ncu_traffic("siren_kernel", cfg.index),
+                "kernel": "siren_kernel", "flop_per_inference": HIDDEN_FLOP_PER_INF,
                 "inferences_per_launch": infers / max(1, nif_launches),
                 "peak_source": peaks["source"] + " bf16 sustained (fp16 same rate)"}
     if dominant == "trace_shade":
@@ -315,11 +335,12 @@ def main():
         # profiles/round1/trace_count.json): node visits x 64 B + primitive tests x 48 B + 80 B of path
         # state, against the measured L2 read bandwidth (tools/l2_bench.cu, profiles/round1/l2_bench.json)
         ms_k = kt["traverse"]
-        byts = TRACE_BYTES_PER_SEGMENT.get(cfg.index, 300.0) * segments
+        bps = trace_bytes_per_segment(cfg.index)
+        byts = (bps or 0.0) * segments
         gbs = byts / (ms_k / 1e3) / 1e9 if ms_k > 0 else 0.0
         roof = {"bound": "l2", "achieved": gbs, "peak": L2_READ_GBS, "unit": "GB/s", "frac": gbs / L2_READ_GBS,
-                "traffic": None, "kernel": "trace_shade_kernel",
-                "bytes_per_segment": TRACE_BYTES_PER_SEGMENT.get(cfg.index, 300.0),
+                "traffic": ncu_traffic("trace_shade_kernel", cfg.index), "kernel": "trace_shade_kernel",
+                "bytes_per_segment": bps,
                 "segments_per_launch": segments / max(1, trav_launches),
                 "peak_source": "measured L2 read bandwidth, tools/l2_bench.cu (MEASURED_PEAKS.json has none)",
                 "hbm_frac": (80.0 * segments / (ms_k / 1e3) / 1e9) / peaks["hbm_gbs"] if ms_k > 0 else 0.0}

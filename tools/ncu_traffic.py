@@ -1,0 +1,36 @@
+#!/usr/bin/env python
+"""DRAM traffic per launch of the hot-path kernels from an ncu metrics capture of one bench step:
+
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \\
+      -k regex:"trace_shade|siren|raygen|accumulate" --csv --log-file X.csv python bench.py --steps 1 --warmup 0 ...
+  python tools/ncu_traffic.py X.csv > profiles/round1/ncu_traffic_c1.json
+
+The bench's warm-up and timed step both appear; per-kernel averages are over every captured launch."""
+import collections
+import csv
+import json
+import sys
+
+rows = list(csv.reader(open(sys.argv[1])))
+hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+h = rows[hi]
+ki, ni, vi, ui = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("Metric Unit")
+scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3, "msecond": 1e6}
+per = collections.defaultdict(lambda: collections.defaultdict(list))
+idi = h.index("ID")
+launch = {}
+for r in rows[hi + 1:]:
+    if len(r) <= vi:
+        continue
+    name = r[ki].split("(")[0].replace("void ", "").replace("pt::", "").split("<")[0].strip()
+    v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1)
+    launch.setdefault((name, r[idi]), {})[r[ni]] = v
+for (name, _), m in launch.items():
+    per[name]["bytes"].append(m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0))
+    per[name]["ns"].append(m.get("gpu__time_duration.sum", 0))
+out = {}
+for name, d in per.items():
+    n = len(d["bytes"])
+    out[name] = {"launches": n, "dram_bytes_per_launch": sum(d["bytes"]) / n,
+                 "dram_bytes_total": sum(d["bytes"]), "ns_per_launch": sum(d["ns"]) / n}
+print(json.dumps(out, indent=1))

@@ -1,6 +1,6 @@
 #!/usr/bin/env python
-"""Counting build (PT_COUNT): node visits and primitive tests per traced segment for the bench
-workload and the primary rays of configs 1-3, i.e. the algorithmic traversal bytes of SURVEY 8d:
+"""Counting build (PT_COUNT): node visits and primitive tests per traced segment for the render
+workloads of configs 1-4 and the primary rays of configs 1-3, i.e. the algorithmic traversal bytes of SURVEY 8d:
 bytes/segment = visits * 64 B + prim tests * 48 B + 40 B state in + ~40 B state out."""
 import ctypes as C
 import json
@@ -40,16 +40,22 @@ for cfg in (1, 2, 3):
     k["per_ray"] = {"visits": k["node_visits"] / k["rays"], "prims": k["prim_tests"] / k["rays"],
                     "fp64": k["fp64_tests"] / k["rays"]}
     out[f"primary_c{cfg}"] = k
-# bench workload (config 1 render), all bounces
-c = scenes.CONFIGS[1]
-S = pt.Scene(scenes.scene_for_config(1))
-N = pt.Nif(scenes.siren_blob(0))
-acc = torch.zeros(c.width * c.height * 3, device="cuda")
-counts()
-pt.render_samples(S, N, c.width, c.height, 0, c.spp, c.max_depth, 0, acc, wave_samples=c.wave_samples)
-k = counts()
-k["per_segment"] = {"visits": k["node_visits"] / k["rays"], "prims": k["prim_tests"] / k["rays"],
-                    "fp64": k["fp64_tests"] / k["rays"]}
-k["alg_bytes_per_segment"] = 64 * k["per_segment"]["visits"] + 48 * k["per_segment"]["prims"] + 80
-out["render_c1"] = k
+# render workloads (all bounces): config 1 in full, configs 2-4 at min(spp, 4) samples per pixel (the
+# per-segment averages do not depend on the sample count)
+for cfg in (1, 2, 3, 4):
+    c = scenes.CONFIGS[cfg]
+    S = pt.Scene(scenes.scene_for_config(cfg))
+    N = pt.Nif(scenes.siren_blob(0)) if c.use_nif else None
+    spp = c.spp if cfg == 1 else min(c.spp, 4)
+    acc = torch.zeros(c.width * c.height * 3, device="cuda")
+    counts()
+    pt.render_samples(S, N, c.width, c.height, 0, spp, c.max_depth, 0, acc, env_rgb=None if c.use_nif else c.env_rgb,
+                      wave_samples=min(c.wave_samples, spp))
+    k = counts()
+    k["spp"] = spp
+    k["per_segment"] = {"visits": k["node_visits"] / k["rays"], "prims": k["prim_tests"] / k["rays"],
+                        "fp64": k["fp64_tests"] / k["rays"]}
+    k["alg_bytes_per_segment"] = 64 * k["per_segment"]["visits"] + 48 * k["per_segment"]["prims"] + 80
+    out[f"render_c{cfg}"] = k
+    del S, N
 print(json.dumps(out, indent=1))
