@@ -109,8 +109,12 @@ __device__ __forceinline__ void ensure64(RayT& r) {
 // misses, 1 if it certainly hits with t in [t - dt, t + dt], t - dt > 0, and 2 if undecided (near an
 // edge or t ~ 0): then the fp64 test decides. Error bounds: with eps = 2^-24,
 // mX = max|A[kx]| + |Sx| max|A[kz]| (over the 3 vertices) and likewise mY, the sheared coordinates
-// carry |dAx| <= 4 eps mX, the edge functions |dU| <= 19 eps mX mY (we use 24), and
-// |dT| <= 3 eU mZ + 18 eps maxE mZ, |ddet| <= 3 eU + 6 eps maxE with mZ = |Sz| max|A[kz]|.
+// carry |dAx| <= eX = 4 eps mX, |dAy| <= eY = 4 eps mY. First a uniform bound on the edge functions,
+// |dU| <= 19 eps mX mY (we use 24); if that leaves the signs undecided (ray origins far from small
+// triangles: mX mY >> |U|), per-edge bounds that scale with the sheared coordinates themselves,
+//   |dU| <= eX (|By| + |Cy|) + eY (|Bx| + |Cx|) + eps (|U| + |Cy Bx|) + 32 eps^2 mX mY
+// (U = Cx By - Cy Bx; likewise V, W), plus 2^-44 mX mY for the fp64 oracle's own rounding, times 1.125.
+// Then |dT| <= (eU + eV + eW) mZ + 18 eps maxE mZ, |ddet| <= eU + eV + eW + 6 eps maxE, mZ = |Sz| max|A[kz]|.
 __device__ __forceinline__ int tri_test32(const RayT& r, float3 v0, float3 v1, float3 v2, float& t, float& dt) {
     constexpr float eps = 0x1p-24f;
     const float A0 = self3(v0, r.kx) - r.ok[0], A1 = self3(v0, r.ky) - r.ok[1], A2 = self3(v0, r.kz) - r.ok[2];
@@ -119,24 +123,38 @@ __device__ __forceinline__ int tri_test32(const RayT& r, float3 v0, float3 v1, f
     const float Ax = fmaf(-r.Sx, A2, A0), Ay = fmaf(-r.Sy, A2, A1);
     const float Bx = fmaf(-r.Sx, B2, B0), By = fmaf(-r.Sy, B2, B1);
     const float Cx = fmaf(-r.Sx, C2, C0), Cy = fmaf(-r.Sy, C2, C1);
-    const float U = fmaf(Cx, By, -Cy * Bx);
-    const float V = fmaf(Ax, Cy, -Ay * Cx);
-    const float W = fmaf(Bx, Ay, -By * Ax);
+    const float CyBx = Cy * Bx, AyCx = Ay * Cx, ByAx = By * Ax;
+    const float U = fmaf(Cx, By, -CyBx);
+    const float V = fmaf(Ax, Cy, -AyCx);
+    const float W = fmaf(Bx, Ay, -ByAx);
     const float mz2 = fmaxf(fabsf(A2), fmaxf(fabsf(B2), fabsf(C2)));
     const float mX = fmaf(fabsf(r.Sx), mz2, fmaxf(fabsf(A0), fmaxf(fabsf(B0), fabsf(C0))));
     const float mY = fmaf(fabsf(r.Sy), mz2, fmaxf(fabsf(A1), fmaxf(fabsf(B1), fabsf(C1))));
-    const float eU = (24.0f * eps) * mX * mY;
-    const bool neg = U < -eU || V < -eU || W < -eU;
-    const bool pos = U > eU || V > eU || W > eU;
+    float eU = (24.0f * eps) * mX * mY, eV = eU, eW = eU;
+    bool neg = U < -eU || V < -eV || W < -eW;
+    bool pos = U > eU || V > eV || W > eW;
     if (neg && pos) return 0;
-    const bool certain = (U > eU && V > eU && W > eU) || (U < -eU && V < -eU && W < -eU);
-    if (!certain) return 2;
+    bool certain = (U > eU && V > eV && W > eW) || (U < -eU && V < -eV && W < -eW);
+    if (!certain) {
+        const float eX = (4.0f * eps) * mX, eY = (4.0f * eps) * mY;
+        const float tail = (32.0f * eps * eps + 0x1p-44f) * mX * mY;
+        const float aAx = fabsf(Ax), aAy = fabsf(Ay), aBx = fabsf(Bx), aBy = fabsf(By), aCx = fabsf(Cx), aCy = fabsf(Cy);
+        eU = 1.125f * (eX * (aBy + aCy) + eY * (aBx + aCx) + eps * (fabsf(U) + fabsf(CyBx)) + tail);
+        eV = 1.125f * (eX * (aCy + aAy) + eY * (aCx + aAx) + eps * (fabsf(V) + fabsf(AyCx)) + tail);
+        eW = 1.125f * (eX * (aAy + aBy) + eY * (aAx + aBx) + eps * (fabsf(W) + fabsf(ByAx)) + tail);
+        neg = U < -eU || V < -eV || W < -eW;
+        pos = U > eU || V > eV || W > eW;
+        if (neg && pos) return 0;
+        certain = (U > eU && V > eV && W > eW) || (U < -eU && V < -eV && W < -eW);
+        if (!certain) return 2;
+    }
     const float det = U + V + W;
     const float T = fmaf(W, r.Sz * C2, fmaf(V, r.Sz * B2, U * (r.Sz * A2)));
     const float mZ = fabsf(r.Sz) * mz2;
     const float maxE = fmaxf(fabsf(U), fmaxf(fabsf(V), fabsf(W)));
-    const float dT = 3.0f * eU * mZ + (18.0f * eps) * maxE * mZ;
-    const float dDet = 3.0f * eU + (6.0f * eps) * maxE;
+    const float eSum = eU + eV + eW;
+    const float dT = eSum * mZ + (18.0f * eps) * maxE * mZ;
+    const float dDet = eSum + (6.0f * eps) * maxE;
     const float adet = fabsf(det);
     if (adet <= 2.0f * dDet) return 2;
     t = __fdiv_rn(T, det);
@@ -528,7 +546,7 @@ struct ShadeArgs {
 // BSDF sampling, Russian roulette (S3) and warp-aggregated compaction into the next live queue or
 // the escaped-ray queue of the NIF (S4). Fused so the path state is read once and written once.
 #ifndef PT_TS_MINB
-#define PT_TS_MINB 8   // min resident blocks per SM for trace_shade: 64-register cap; tools/ts_tune.sh on B200
+#define PT_TS_MINB 7   // min resident blocks per SM for trace_shade: 72-register cap; tools/ts_tune.sh on B200
 #endif
 __global__ void __launch_bounds__(128, PT_TS_MINB) trace_shade_kernel(ShadeArgs a) {
     const uint32_t n = *a.cnt_in;
