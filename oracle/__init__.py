@@ -65,6 +65,9 @@ def lib():
             L.orc_roulette.argtypes = [P, I32, D]
             L.orc_nif_eval.argtypes = [P, P, I64, P]
             L.orc_fr_eval.argtypes = [P, P, I64, P]
+            L.orc_fr_eval_hl.argtypes = [I32, I32, P, P, I64, P]
+            L.orc_fr_concat_layer.restype = C.c_int
+            L.orc_fr_concat_layer.argtypes = [I32]
             L.orc_scatter.argtypes = [C.c_int, P, P, D, P, P, P, P]
             L.orc_render.restype = C.c_int
             L.orc_render.argtypes = [P, P, P, I32, I32, I32, U64, P, I64, I32, I32, I32, P, P]
@@ -197,6 +200,20 @@ def fr_eval(blob, uv):
     y = np.empty((uv.shape[0], 3), np.float64)
     lib().orc_fr_eval(_p(blob), _p(uv), uv.shape[0], _p(y))
     return y
+
+
+def fr_eval_hl(hidden, layers, blob, uv):
+    """The paper's NIF family of the size sweep (hidden size H, L dense-ReLU layers; reading R23) in
+    fp64: RGB log radiance [n][3]."""
+    blob = np.ascontiguousarray(blob, dtype=np.uint16)
+    uv = np.ascontiguousarray(uv, dtype=np.float64).reshape(-1, 2)
+    y = np.empty((uv.shape[0], 3), np.float64)
+    lib().orc_fr_eval_hl(int(hidden), int(layers), _p(blob), _p(uv), uv.shape[0], _p(y))
+    return y
+
+
+def fr_concat_layer(layers):
+    return int(lib().orc_fr_concat_layer(int(layers)))
 
 
 def scatter(kind, d, ng, xi, ior=1.5):

@@ -623,6 +623,79 @@ EXPORT void orc_fr_eval(const uint16_t* blob, const double* uv, int64_t n, doubl
     for (int l = 0; l < 5; ++l) { free(W[l]); free(b[l]); }
 }
 
+/* The paper's NIF family of the size sweep ("hidden size H (128) and number of dense-relu
+   layers L (4) can be varied"; Fig. nrf-vs-blender H64 L2 / H256 L4 / H1024 L8, PAPER.md:225-227;
+   DESIGN.md reading R23): 40 Fourier features -> L dense ReLU layers of width H, where layer c =
+   the largest odd index below L/2 (c = 0 when there is none, L <= 2) outputs H - 40 units and is
+   concatenated with the 40 features ("always concatenated with the last odd layer before the middle
+   of the network, which has a reduced dense layer output size to compensate") -> linear H -> 3 (YUV,
+   log) -> fixed BT.601 YUV -> RGB. Blob: B [20][2], then W_l [out][in], b_l [out] for the L + 1
+   layers. (H, L) = (128, 4) is the network of orc_fr_eval. */
+EXPORT int orc_fr_concat_layer(int32_t L) {
+    int c = 0;
+    for (int l = 1; 2 * l < L; l += 2) c = l;
+    return c;
+}
+
+EXPORT void orc_fr_dims(int32_t H, int32_t L, int32_t* fin, int32_t* fout) {
+    const int c = orc_fr_concat_layer(L);
+    for (int l = 0; l <= L; ++l) {
+        fin[l] = l == 0 ? 40 : H;
+        fout[l] = l == L ? 3 : (l == c ? H - 40 : H);
+    }
+}
+
+EXPORT void orc_fr_eval_hl(int32_t H, int32_t L, const uint16_t* blob, const double* uv, int64_t n, double* y_out) {
+    const double PI = 3.14159265358979323846;
+    int32_t fin[64], fout[64];
+    orc_fr_dims(H, L, fin, fout);
+    const int c = orc_fr_concat_layer(L);
+    double B[40];
+    double** W = (double**)malloc(sizeof(double*) * (L + 1));
+    double** b = (double**)malloc(sizeof(double*) * (L + 1));
+    int64_t off = 0;
+    for (int i = 0; i < 40; ++i) B[i] = half_to_double(blob[off++]);
+    for (int l = 0; l <= L; ++l) {
+        W[l] = (double*)malloc(sizeof(double) * fin[l] * fout[l]);
+        b[l] = (double*)malloc(sizeof(double) * fout[l]);
+        for (int64_t i = 0; i < (int64_t)fin[l] * fout[l]; ++i) W[l][i] = half_to_double(blob[off++]);
+        for (int i = 0; i < fout[l]; ++i) b[l][i] = half_to_double(blob[off++]);
+    }
+    double* a = (double*)malloc(sizeof(double) * (H > 40 ? H : 40));
+    double* h = (double*)malloc(sizeof(double) * (H > 40 ? H : 40));
+    for (int64_t q = 0; q < n; ++q) {
+        double g[40];
+        for (int j = 0; j < 20; ++j) {
+            const double p = 2.0 * PI * (B[2 * j] * uv[2 * q] + B[2 * j + 1] * uv[2 * q + 1]);
+            g[j] = sin(p);
+            g[20 + j] = cos(p);
+        }
+        memcpy(a, g, sizeof(double) * 40);
+        for (int l = 0; l < L; ++l) {
+            for (int o = 0; o < fout[l]; ++o) {
+                double s = 0.0;
+                for (int i = 0; i < fin[l]; ++i) s += W[l][(int64_t)o * fin[l] + i] * a[i];
+                s += b[l][o];
+                h[o] = s > 0.0 ? s : 0.0;
+            }
+            memcpy(a, h, sizeof(double) * fout[l]);
+            if (l == c) memcpy(a + (H - 40), g, sizeof(double) * 40);   /* concat skip: [h_c, gamma] */
+        }
+        double yuv[3];
+        for (int o = 0; o < 3; ++o) {
+            double s = 0.0;
+            for (int i = 0; i < H; ++i) s += W[L][(int64_t)o * H + i] * a[i];
+            yuv[o] = s + b[L][o];
+        }
+        double* y = y_out + 3 * q;
+        y[0] = yuv[0] + 1.13983 * yuv[2];
+        y[1] = yuv[0] - 0.39465 * yuv[1] - 0.58060 * yuv[2];
+        y[2] = yuv[0] + 2.03211 * yuv[1];
+    }
+    for (int l = 0; l <= L; ++l) { free(W[l]); free(b[l]); }
+    free(W); free(b); free(a); free(h);
+}
+
 /* ---------------------------------------------------------------------------------------------- */
 /* Scattering (readings R9, R10)                                        */
 /* ---------------------------------------------------------------------------------------------- */

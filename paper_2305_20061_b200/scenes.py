@@ -419,6 +419,56 @@ def fourier_relu_blob(seed: int = 0, sigma: float = 6.0) -> np.ndarray:
     return flat.view(np.uint16).copy()
 
 
+# The NIF family of the size sweep (SURVEY 8f #3; PAPER.md:117, 225-227; DESIGN.md reading R23): hidden
+# size H, L dense-ReLU layers; the concat layer c is the largest odd index below L / 2 (0 if none) and
+# outputs H - 40 units. (H, L) = (128, 4) is FR_LAYERS.
+NIF_SWEEP = [(64, 2), (128, 4), (256, 4), (1024, 8)]
+
+
+def fr_concat_layer(layers: int) -> int:
+    c = 0
+    for l in range(1, layers):
+        if 2 * l < layers and l % 2 == 1:
+            c = l
+    return c
+
+
+def fr_family_layers(hidden: int, layers: int):
+    """[(fan_in, fan_out)] of the L dense-ReLU layers and the linear output layer."""
+    c = fr_concat_layer(layers)
+    dims = []
+    for l in range(layers + 1):
+        fin = FR_FEATURES if l == 0 else hidden
+        fout = 3 if l == layers else (hidden - FR_FEATURES if l == c else hidden)
+        dims.append((fin, fout))
+    return dims
+
+
+def fr_family_halves(hidden: int, layers: int) -> int:
+    return 2 * FR_FREQS + sum(o * i + o for i, o in fr_family_layers(hidden, layers))
+
+
+def fourier_relu_family_blob(hidden: int, layers: int, seed: int = 0, sigma: float = 6.0) -> np.ndarray:
+    """fp16 blob of a sweep member: B[20][2] then W_l[out][in], b_l[out] for the L + 1 layers; the same
+    untrained seeded init as fourier_relu_blob (He-uniform ReLU layers, output scaled by 0.1, b_out =
+    (0.5, 0, 0)). (128, 4) reproduces fourier_relu_blob's layer shapes (not its values)."""
+    rng = np.random.default_rng([seed, 11, hidden, layers])
+    dims = fr_family_layers(hidden, layers)
+    parts = [rng.normal(0.0, sigma, size=(FR_FREQS, 2)).reshape(-1)]
+    for li, (fin, fout) in enumerate(dims):
+        bound = math.sqrt(6.0 / fin)
+        W = rng.uniform(-bound, bound, size=(fout, fin))
+        b = rng.uniform(-0.05, 0.05, size=fout)
+        if li == len(dims) - 1:
+            W = 0.1 * W
+            b = np.array([0.5, 0.0, 0.0])
+        parts.append(W.reshape(-1))
+        parts.append(b)
+    flat = np.concatenate(parts).astype(np.float16)
+    assert flat.size == fr_family_halves(hidden, layers)
+    return flat.view(np.uint16).copy()
+
+
 def fourier_relu_from_blob(blob: np.ndarray):
     """(B [20][2], [(W, b)] x 5) as float64 arrays (exact widening)."""
     h = np.asarray(blob, dtype=np.uint16).view(np.float16).astype(np.float64)
