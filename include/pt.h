@@ -90,7 +90,20 @@ PT_API int pt_nif_load(const uint16_t* fp16_blob, int64_t n_halves, pt_nif** out
    B (40) then W_l [out][in], b_l [out] for the 5 layers. Errors as pt_nif_load. */
 #define PT_NIF_SIREN 0
 #define PT_NIF_FOURIER_RELU 1
+#define PT_NIF_FR_FAMILY 2 /* created by pt_nif_load_family only */
 PT_API int pt_nif_load_ex(int32_t kind, const uint16_t* fp16_blob, int64_t n_halves, pt_nif** out);
+
+/* The paper's NIF family of its size sweep ("hidden size H (128) and number of dense-relu
+   layers L (4) can be varied"; Fig. nrf-vs-blender H64 L2 / H256 L4 / H1024 L8, PAPER.md:225-227;
+   DESIGN.md reading R23): the PT_NIF_FOURIER_RELU architecture with width `hidden` and `layers` dense
+   ReLU layers; layer c = the largest odd index below layers/2 (0 if none) outputs hidden - 40 units and
+   is concatenated with the 40 Fourier features. fp16_blob: B (40) then W_l [out][in], b_l [out] for the
+   layers + 1 layers (n_halves = 40 + sum of fan_out * (fan_in + 1)). Evaluated as one tcgen05 GEMM per
+   layer over the whole batch (weights of H >= 256 exceed one SM's shared memory). hidden: a multiple of
+   64 in [64, 1024]; layers in [1, 16].
+   Errors: INVALID_ARG (hidden/layers out of range), FORMAT (n_halves), DOMAIN (non-finite), CUDA, OOM. */
+PT_API int pt_nif_load_family(int32_t hidden, int32_t layers, const uint16_t* fp16_blob, int64_t n_halves,
+                              pt_nif** out);
 PT_API int pt_nif_destroy(pt_nif* nif);
 
 /* Render a full frame. env: nif != NULL -> HDR-NIF environment; nif == NULL -> constant env_rgb

@@ -1,0 +1,502 @@
+// mlp_kernel.cu -- the paper's NIF family of the size sweep (
+// DESIGN.md reading R23) as a chain of per-layer tcgen05 GEMMs with fused epilogues.
+//
+// What it computes, per escaped ray (direction d, or (u, v) from the query hook) with throughput beta:
+//   gamma = (sin 2 pi B x, cos 2 pi B x) (40 features of x = (u, v)); h_0 = relu(W_0 gamma + b_0);
+//   h_l = relu(W_l a_{l-1} + b_l) with a_c = [h_c, gamma] for the concat layer c and a_l = h_l otherwise;
+//   yuv = W_L a_{L-1} + b_L; rgb = M_601 yuv; radiance = beta * exp(rgb).
+//
+// Why layered and not fused: from H = 256 the weights (387 KiB, 14 MiB for H1024 L8) no longer fit one
+// SM's shared memory, and for H = 1024 one 128-row tile's activations (128 x 1024 fp16 = 256 KiB) no
+// longer fit TMEM or shared memory either -- the regime the paper calls the point "at which current GPUs
+// can not operate ... loads weights into SRAM/registers exactly once". On B200 each layer
+// is one GEMM over the whole batch of escaped rays: activations stream through L2/HBM in a blocked fp16
+// layout, weights stream as K-chunks (or stay resident in shared memory when a layer fits, H <= 256).
+//
+// GEMM kernel (one persistent CTA per SM, 192 threads):
+//   warp 0 producer: cp.async.bulk of 16 KB A chunks (128 rows x 64 K) and BN x 64 B chunks into a
+//     STAGES-deep shared-memory ring (mbarrier complete_tx); resident-B mode loads the layer's whole B
+//     once.
+//   warp 1 MMA: 4 SS tcgen05.mma (M = 128, N = BN, K = 16) per chunk, commit frees the stage; one commit
+//     per tile hands the TMEM accumulator (2 buffers x BN columns) to the epilogue.
+//   warps 2-5 epilogue (one TMEM lane quarter each): bias + ReLU + fp16 pack, 16-byte stores into the
+//     next layer's blocked A layout; the output layer instead applies YUV -> RGB, exp and beta and
+//     writes the path's wave slot.
+// Blocked layout (A and B alike, SWIZZLE_NONE K-major core matrices): a (R rows x 64 K) chunk is one
+// contiguous block, core matrix (rows 8nb..8nb+7, k 8kb..8kb+7) at ((kb * R/8) + nb) * 128 B.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "pt_internal.h"
+#include "tc_ptx.cuh"
+
+namespace pt {
+
+namespace mlp {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;
+constexpr int kAChunk = kBM * kBK * 2;          // 16 KB
+constexpr int kThreads = 192;
+constexpr int kSmemBudget = 220 * 1024;
+constexpr int kMaxStages = 8;
+// barriers: [0..7] full[stage], [8..15] empty[stage], [16..17] acc_full, [18..19] acc_empty, [20] b_res;
+// TMEM base address at 21 * 8
+constexpr int kBarBytes = 256;
+
+__host__ __device__ constexpr uint32_t idesc(int n) {
+    return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
+}
+
+struct LayerArgs {
+    const uint8_t* A;        // blocked input activations of this row chunk, [m_tiles][KC][16 KB]
+    const uint8_t* B;        // blocked weights, [NT][KC][BN * 128]
+    const float* bias;       // [NT * BN] fp32, zero padded
+    uint8_t* out_act;        // blocked output activations, [m_tiles][out_KC][16 KB] (kEpi 0)
+    int KC, NT, N_valid, out_KC;
+    int b_res, stages;
+    const uint32_t* count;   // device row count (all chunks)
+    int row0, rows_cap;      // this chunk: rows [row0, row0 + min(count - row0, rows_cap))
+    const float4* esc;       // output layer: queue entries (slot in .w) and throughputs
+    const float4* esc_beta;
+    float* out_rgb;
+};
+
+// 16 B of 8 consecutive fp16 columns of one row into a blocked activation buffer
+__device__ __forceinline__ void store_act8(uint8_t* buf, int out_KC, int tile, int row_in_tile, int col, uint4 v) {
+    const int kc = col >> 6, kb = (col & 63) >> 3;
+    uint8_t* p = buf + ((size_t)tile * out_KC + kc) * kAChunk + ((kb * 16 + (row_in_tile >> 3)) * 128) +
+                 (row_in_tile & 7) * 16;
+    *reinterpret_cast<uint4*>(p) = v;
+}
+
+}  // namespace mlp
+
+// Fourier features of the chunk's rows into a blocked activation buffer: part 0 writes the layer-0
+// input (columns 0..39 = [sin_0..19, cos_0..19], 40..63 zero), part 1 the concat columns H-40..H-1 of
+// the layer after the concat layer. Rows past the count get the features of (u, v) = (0.5, 0.5).
+__global__ void mlp_features_kernel(const float4* __restrict__ esc, const uint32_t* __restrict__ count, int row0,
+                                    int rows_cap, int dir_input, const float* __restrict__ freq, uint8_t* out,
+                                    int out_KC, int col0, int zero_pad) {
+    const uint32_t n = *count;
+    const int M = (int)min((int64_t)rows_cap, max((int64_t)0, (int64_t)n - row0));
+    const int rows = ((M + mlp::kBM - 1) / mlp::kBM) * mlp::kBM;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+        float u = 0.5f, v = 0.5f;
+        if (r < M) {
+            const float4 en = __ldg(esc + row0 + r);
+            u = en.x;
+            v = en.y;
+            if (dir_input) equirect_f32(make_float3(en.x, en.y, en.z), u, v);
+        }
+        __half f[40];
+#pragma unroll
+        for (int j = 0; j < 20; ++j) {
+            const float p = fmaf(__ldg(freq + 2 * j), u, __ldg(freq + 2 * j + 1) * v);
+            const float q = p - rintf(p);                 // exact-range turns in [-1/2, 1/2]
+            float sn, cs;
+            __sincosf(6.28318530717958647692f * q, &sn, &cs);
+            f[j] = __float2half_rn(sn);
+            f[20 + j] = __float2half_rn(cs);
+        }
+        const int tile = r / mlp::kBM, rt = r % mlp::kBM;
+#pragma unroll
+        for (int g = 0; g < 5; ++g) {
+            uint4 w;
+            uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                wp[i] = (uint32_t)__half_as_ushort(f[8 * g + 2 * i]) | ((uint32_t)__half_as_ushort(f[8 * g + 2 * i + 1]) << 16);
+            mlp::store_act8(out, out_KC, tile, rt, col0 + 8 * g, w);
+        }
+        if (zero_pad) {
+#pragma unroll
+            for (int g = 5; g < 8; ++g) mlp::store_act8(out, out_KC, tile, rt, col0 + 8 * g, make_uint4(0, 0, 0, 0));
+        }
+    }
+}
+
+template <int BN, int kEpi>
+__global__ void __launch_bounds__(mlp::kThreads, 1) mlp_layer_kernel(mlp::LayerArgs a) {
+    using namespace mlp;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    constexpr int kBChunk = BN * kBK * 2;
+    constexpr uint32_t kTmemCols = (2 * BN) < 32 ? 32u : (uint32_t)(2 * BN);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 21 * 8);
+    auto bar = [&](int b) { return smem_u32(&bars[b]); };
+    const int stage_bytes = kAChunk + (a.b_res ? 0 : kBChunk);
+    uint8_t* ring = smem + kBarBytes;                               // stages x (A [, B])
+    uint8_t* bres = ring + a.stages * stage_bytes;                  // resident B: KC x kBChunk
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t n = *a.count;
+    const int M = (int)min((int64_t)a.rows_cap, max((int64_t)0, (int64_t)n - a.row0));
+    const int m_tiles = (M + kBM - 1) / kBM;
+    const int n_tiles_total = m_tiles * a.NT;
+    if (m_tiles == 0) return;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < a.stages; ++s) {
+            mbar_init(bar(s), 1);
+            mbar_init(bar(8 + s), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(bar(16 + b), 1);
+            mbar_init(bar(18 + b), 4);
+        }
+        mbar_init(bar(20), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ===== producer =====
+        if (lane == 0) {
+            if (a.b_res) {
+                mbar_expect_tx(bar(20), (uint32_t)(a.KC * kBChunk));
+                for (int kc = 0; kc < a.KC; ++kc)
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            smem_u32(bres + kc * kBChunk)),
+                        "l"(a.B + (size_t)kc * kBChunk), "r"(kBChunk), "r"(bar(20))
+                        : "memory");
+            }
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+                const int mt = t / a.NT, nt = t % a.NT;
+                for (int kc = 0; kc < a.KC; ++kc, ++it) {
+                    if (it >= a.stages) mbar_wait(bar(8 + stage), phase ^ 1);
+                    uint8_t* sa = ring + stage * stage_bytes;
+                    mbar_expect_tx(bar(stage), (uint32_t)stage_bytes);
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            smem_u32(sa)),
+                        "l"(a.A + ((size_t)mt * a.KC + kc) * kAChunk), "r"(kAChunk), "r"(bar(stage))
+                        : "memory");
+                    if (!a.b_res)
+                        asm volatile(
+                            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                smem_u32(sa + kAChunk)),
+                            "l"(a.B + ((size_t)nt * a.KC + kc) * kBChunk), "r"(kBChunk), "r"(bar(stage))
+                            : "memory");
+                    if (++stage == a.stages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer =====
+        if (a.b_res) mbar_wait(bar(20), 0);
+        int stage = 0;
+        uint32_t phase = 0;
+        uint32_t acc_phase[2] = {0, 0};
+        int local = 0;
+        for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++local) {
+            const int nt = t % a.NT;
+            const int acc = local & 1;
+            if (local >= 2) {
+                mbar_wait(bar(18 + acc), acc_phase[acc]);       // epilogue drained this accumulator
+                acc_phase[acc] ^= 1;
+            }
+            tc_fence_after();
+            const uint32_t dt = tmem + (uint32_t)(acc * BN);
+            for (int kc = 0; kc < a.KC; ++kc) {
+                mbar_wait(bar(stage), phase);
+                tc_fence_after();
+                const uint8_t* sa = ring + stage * stage_bytes;
+                const uint8_t* sb = a.b_res ? bres + kc * kBChunk : sa + kAChunk;
+                (void)nt;
+                if (elect_one()) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint64_t ad = smem_desc(smem_u32(sa) + k * 2 * 2048, 2048, 128);
+                        const uint64_t bd = smem_desc(smem_u32(sb) + k * 2 * (BN / 8) * 128, (BN / 8) * 128, 128);
+                        mma_ss(dt, ad, bd, idesc(BN), (kc | k) != 0);
+                    }
+                    mma_commit(bar(8 + stage));                  // stage free once these MMAs are done
+                }
+                __syncwarp();
+                if (++stage == a.stages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            if (elect_one()) mma_commit(bar(16 + acc));          // accumulator complete
+            __syncwarp();
+        }
+    } else {
+        // ===== epilogue: warps 2-5, TMEM lane quarter warp % 4 =====
+        const int q = warp & 3;
+        const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
+        uint32_t acc_phase[2] = {0, 0};
+        int local = 0;
+        for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++local) {
+            const int mt = t / a.NT, nt = t % a.NT;
+            const int acc = local & 1;
+            mbar_wait(bar(16 + acc), acc_phase[acc]);
+            acc_phase[acc] ^= 1;
+            tc_fence_after();
+            const int rt = 32 * q + lane;                          // row within the tile
+            const int row = a.row0 + mt * kBM + rt;
+            const bool valid = mt * kBM + rt < M;
+            const uint32_t dt = tmem + (uint32_t)(acc * BN) + lane_addr;
+            if (kEpi == 0) {
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    const int col = nt * BN + 32 * c;
+                    if (col >= a.N_valid) break;
+                    uint32_t v[32];
+                    TMEM_LD32(dt + 32 * c, v);
+                    tmem_wait_ld_dep(v);
+                    const float4* bp = reinterpret_cast<const float4*>(a.bias + col);
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        if (col + 8 * g >= a.N_valid) break;
+                        const float4 b0 = __ldg(bp + 2 * g), b1 = __ldg(bp + 2 * g + 1);
+                        const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                        uint4 w;
+                        uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const float lo = __uint_as_float(v[8 * g + 2 * i]) + bb[2 * i];
+                            const float hi = __uint_as_float(v[8 * g + 2 * i + 1]) + bb[2 * i + 1];
+                            asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(wp[i]) : "f"(hi), "f"(lo));
+                        }
+                        store_act8(a.out_act, a.out_KC, mt, rt, col + 8 * g, w);
+                    }
+                }
+            } else {
+                uint32_t v[4];
+                tmem_ld4(dt, v);
+                tmem_wait_ld_dep4(v);
+                if (valid) {
+                    const float Y = __uint_as_float(v[0]) + __ldg(a.bias + 0);
+                    const float U = __uint_as_float(v[1]) + __ldg(a.bias + 1);
+                    const float V = __uint_as_float(v[2]) + __ldg(a.bias + 2);
+                    // fixed BT.601 YUV -> RGB colour layer, log space; then exp
+                    const float r = fmaf(1.13983f, V, Y);
+                    const float gch = fmaf(-0.58060f, V, fmaf(-0.39465f, U, Y));
+                    const float bch = fmaf(2.03211f, U, Y);
+                    const uint32_t slot = __float_as_uint(__ldg(a.esc + row).w);
+                    const float4 beta = __ldg(a.esc_beta + row);
+                    a.out_rgb[3 * (size_t)slot + 0] = beta.x * __expf(r);
+                    a.out_rgb[3 * (size_t)slot + 1] = beta.y * __expf(gch);
+                    a.out_rgb[3 * (size_t)slot + 2] = beta.z * __expf(bch);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar(18 + acc));
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Host side: weight re-layout at load, launch sequence per row chunk
+// ---------------------------------------------------------------------------------------------
+namespace {
+
+int pick_bn(int n_valid) { return n_valid <= 16 ? 16 : n_valid <= 64 ? 64 : n_valid <= 128 ? 128 : 256; }
+
+float half_to_float(uint16_t h) {
+    const int e = (h >> 10) & 31, m = h & 1023;
+    float v = e == 0 ? std::ldexp((float)m, -24) : std::ldexp((float)(m | 1024), e - 25);
+    return (h & 0x8000) ? -v : v;
+}
+
+}  // namespace
+
+int mlp_concat_layer(int L) {
+    int c = 0;
+    for (int l = 1; 2 * l < L; l += 2) c = l;
+    return c;
+}
+
+int64_t mlp_blob_halves(int H, int L) {
+    const int c = mlp_concat_layer(L);
+    int64_t n = 40;
+    for (int l = 0; l <= L; ++l) {
+        const int64_t fin = l == 0 ? 40 : H, fout = l == L ? 3 : (l == c ? H - 40 : H);
+        n += fin * fout + fout;
+    }
+    return n;
+}
+
+// Build the blocked device weights of every layer (K padded to 64, N padded to BN, zeros elsewhere).
+int mlp_load(pt_nif* nif, int H, int L, const uint16_t* blob, std::string* msg) {
+    const int c = mlp_concat_layer(L);
+    nif->mlp_H = H;
+    nif->mlp_L = L;
+    nif->mlp_c = c;
+    int64_t off = 0;
+    std::vector<float> freq(40);
+    for (int i = 0; i < 40; ++i) freq[i] = half_to_float(blob[off++]);
+    if (cudaMalloc(&nif->mlp_freq, sizeof(float) * 40) != cudaSuccess ||
+        cudaMemcpy(nif->mlp_freq, freq.data(), sizeof(float) * 40, cudaMemcpyHostToDevice) != cudaSuccess) {
+        *msg = "mlp: frequency upload failed";
+        return PT_ERR_CUDA;
+    }
+    for (int l = 0; l <= L; ++l) {
+        MlpLayer ly;
+        const int fin = l == 0 ? 40 : H, fout = l == L ? 3 : (l == c ? H - 40 : H);
+        ly.K = ((fin + 63) / 64) * 64;
+        ly.N_valid = fout;
+        ly.BN = pick_bn(fout);
+        ly.NT = (fout + ly.BN - 1) / ly.BN;
+        const int KC = ly.K / 64;
+        std::vector<uint8_t> img((size_t)ly.NT * KC * ly.BN * 128, 0);
+        const uint16_t* W = blob + off;
+        off += (int64_t)fin * fout;
+        const uint16_t* b = blob + off;
+        off += fout;
+        for (int nrow = 0; nrow < fout; ++nrow) {
+            const int nt = nrow / ly.BN, nn = nrow % ly.BN, nb = nn >> 3, r = nn & 7;
+            for (int k = 0; k < fin; ++k) {
+                const int kc = k >> 6, kb = (k & 63) >> 3, cc = k & 7;
+                const size_t o = ((size_t)nt * KC + kc) * ly.BN * 128 + (size_t)((kb * (ly.BN / 8) + nb) * 128) + r * 16 + cc * 2;
+                std::memcpy(&img[o], &W[(int64_t)nrow * fin + k], 2);
+            }
+        }
+        std::vector<float> bias((size_t)ly.NT * ly.BN, 0.0f);
+        for (int i = 0; i < fout; ++i) bias[i] = half_to_float(b[i]);
+        if (cudaMalloc(&ly.d_w, img.size()) != cudaSuccess ||
+            cudaMemcpy(ly.d_w, img.data(), img.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMalloc(&ly.d_bias, sizeof(float) * bias.size()) != cudaSuccess ||
+            cudaMemcpy(ly.d_bias, bias.data(), sizeof(float) * bias.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+            *msg = "mlp: weight upload failed";
+            nif->mlp_layers.push_back(ly);
+            return PT_ERR_OOM;
+        }
+        nif->mlp_layers.push_back(ly);
+    }
+    return PT_OK;
+}
+
+void mlp_free(pt_nif* nif) {
+    for (auto& ly : nif->mlp_layers) {
+        cudaFree(ly.d_w);
+        cudaFree(ly.d_bias);
+    }
+    nif->mlp_layers.clear();
+    cudaFree(nif->mlp_freq);
+    cudaFree(nif->mlp_act[0]);
+    cudaFree(nif->mlp_act[1]);
+    nif->mlp_freq = nullptr;
+    nif->mlp_act[0] = nif->mlp_act[1] = nullptr;
+}
+
+template <int BN, int kEpi>
+static cudaError_t launch_layer_t(const mlp::LayerArgs& a, int grid, int smem, cudaStream_t st) {
+    static int configured = 0;
+    if (configured < smem) {
+        cudaError_t e = cudaFuncSetAttribute(mlp_layer_kernel<BN, kEpi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             mlp::kSmemBudget + mlp::kBarBytes);
+        if (e != cudaSuccess) return e;
+        configured = mlp::kSmemBudget + mlp::kBarBytes;
+    }
+    mlp_layer_kernel<BN, kEpi><<<grid, mlp::kThreads, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+static cudaError_t launch_layer(const MlpLayer& ly, int epi, mlp::LayerArgs a, cudaStream_t st) {
+    using namespace mlp;
+    const int KC = ly.K / 64;
+    const int bchunk = ly.BN * 128;
+    const bool res = ly.NT == 1 && (int64_t)KC * bchunk <= 128 * 1024;
+    const int stage_bytes = kAChunk + (res ? 0 : bchunk);
+    const int avail = kSmemBudget - (res ? KC * bchunk : 0);
+    a.KC = KC;
+    a.NT = ly.NT;
+    a.N_valid = ly.N_valid;
+    a.B = (const uint8_t*)ly.d_w;
+    a.bias = ly.d_bias;
+    a.b_res = res ? 1 : 0;
+    a.stages = std::min(kMaxStages, avail / stage_bytes);
+    const int smem = kBarBytes + a.stages * stage_bytes + (res ? KC * bchunk : 0);
+    const int64_t tiles = (int64_t)((a.rows_cap + kBM - 1) / kBM) * ly.NT;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, num_sms()));
+    if (epi == 1) return launch_layer_t<16, 1>(a, grid, smem, st);
+    switch (ly.BN) {
+        case 64: return launch_layer_t<64, 0>(a, grid, smem, st);
+        case 128: return launch_layer_t<128, 0>(a, grid, smem, st);
+        case 256: return launch_layer_t<256, 0>(a, grid, smem, st);
+        default: return launch_layer_t<16, 0>(a, grid, smem, st);
+    }
+}
+
+// Row chunks of up to kChunkRows rows; every chunk launch reads the device row count and exits when
+// the chunk is empty, so the host never synchronises on the count.
+constexpr int kChunkRows = 1 << 20;
+
+cudaError_t launch_mlp(pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count, int64_t max_rows,
+                       float* out, int dir_input, cudaStream_t st) {
+    using namespace mlp;
+    const int H = nif->mlp_H, L = nif->mlp_L, c = nif->mlp_c;
+    const int kmax = std::max(64, H);
+    const int cap = (int)std::min<int64_t>(kChunkRows, ((max_rows + kBM - 1) / kBM) * kBM);
+    const int64_t need = (int64_t)((cap + kBM - 1) / kBM) * kBM * kmax * 2;
+    if (need > nif->mlp_act_bytes) {
+        cudaStreamSynchronize(st);
+        cudaFree(nif->mlp_act[0]);
+        cudaFree(nif->mlp_act[1]);
+        nif->mlp_act[0] = nif->mlp_act[1] = nullptr;
+        nif->mlp_act_bytes = 0;
+        cudaError_t e = cudaMalloc(&nif->mlp_act[0], need);
+        if (e == cudaSuccess) e = cudaMalloc(&nif->mlp_act[1], need);
+        if (e != cudaSuccess) return e;
+        nif->mlp_act_bytes = need;
+    }
+    uint8_t* buf[2] = {(uint8_t*)nif->mlp_act[0], (uint8_t*)nif->mlp_act[1]};
+    const int kc_of_H = H / 64;
+    for (int64_t r0 = 0; r0 < max_rows; r0 += cap) {
+        const int fgrid = std::max(1, std::min(num_sms() * 4, (cap + 255) / 256));
+        // layer-0 input; the concat columns of layer c + 1 too when that buffer is not read before
+        mlp_features_kernel<<<fgrid, 256, 0, st>>>(esc, count, (int)r0, cap, dir_input, nif->mlp_freq, buf[0], 1, 0, 1);
+        for (int l = 0; l <= L; ++l) {
+            if (l == c) {
+                mlp_features_kernel<<<fgrid, 256, 0, st>>>(esc, count, (int)r0, cap, dir_input, nif->mlp_freq,
+                                                           buf[(c + 1) & 1], kc_of_H, H - 40, 0);
+            }
+            LayerArgs a{};
+            a.A = buf[l & 1];
+            a.out_act = buf[(l + 1) & 1];
+            a.out_KC = kc_of_H;
+            a.count = count;
+            a.row0 = (int)r0;
+            a.rows_cap = cap;
+            a.esc = esc;
+            a.esc_beta = esc_beta;
+            a.out_rgb = out;
+            cudaError_t e = launch_layer(nif->mlp_layers[l], l == L ? 1 : 0, a, st);
+            if (e != cudaSuccess) return e;
+        }
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace pt

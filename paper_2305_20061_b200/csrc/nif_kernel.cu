@@ -470,6 +470,10 @@ cudaError_t launch_siren(const pt_nif* nif, const float4* esc, const float4* esc
 // one persistent CTA per SM (or per tile when there are fewer tiles); the row count is read on device
 static cudaError_t nif_launch_impl(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,
                                    int64_t max_rows, float* out, float* dbg, int dir_input, cudaStream_t st) {
+    if (nif->kind == PT_NIF_FR_FAMILY) {
+        if (dbg) return cudaErrorNotSupported;
+        return launch_mlp(const_cast<pt_nif*>(nif), esc, esc_beta, count, max_rows, out, dir_input, st);
+    }
     int64_t tiles = (max_rows + 127) / 128;
     int grid = num_sms();
     if (tiles < grid) grid = (int)(tiles > 0 ? tiles : 1);

@@ -422,8 +422,33 @@ int pt_nif_load(const uint16_t* blob, int64_t n_halves, pt_nif** out) {
     return pt_nif_load_ex(PT_NIF_SIREN, blob, n_halves, out);
 }
 
+int pt_nif_load_family(int32_t hidden, int32_t layers, const uint16_t* blob, int64_t n_halves, pt_nif** out) {
+    if (!blob || !out) return fail(PT_ERR_INVALID_ARG, "null argument");
+    *out = nullptr;
+    if (hidden < 64 || hidden > 1024 || hidden % 64 != 0 || layers < 1 || layers > 16)
+        return fail(PT_ERR_INVALID_ARG, "hidden must be a multiple of 64 in [64, 1024], layers in [1, 16]");
+    if (n_halves != pt::mlp_blob_halves(hidden, layers))
+        return fail(PT_ERR_FORMAT, "NIF family blob size does not match (hidden, layers)");
+    for (int64_t i = 0; i < n_halves; ++i)
+        if ((blob[i] & 0x7C00u) == 0x7C00u) return fail(PT_ERR_DOMAIN, "non-finite NIF weight");
+    int rc = check_device();
+    if (rc) return rc;
+    pt_nif* n = new pt_nif();
+    n->kind = PT_NIF_FR_FAMILY;
+    cudaGetDevice(&n->device);
+    std::string msg;
+    rc = pt::mlp_load(n, hidden, layers, blob, &msg);
+    if (rc) {
+        pt_nif_destroy(n);
+        return fail(rc, msg);
+    }
+    *out = n;
+    return PT_OK;
+}
+
 int pt_nif_destroy(pt_nif* n) {
     if (!n) return PT_OK;
+    pt::mlp_free(n);
     cudaFree(n->d_smem_image);
     cudaFree(n->d_blob);
     delete n;

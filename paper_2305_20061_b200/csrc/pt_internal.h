@@ -98,12 +98,25 @@ struct pt_scene {
     std::vector<pt::TimedLaunch> pending;   // launch timers awaiting pt_get_stats
 };
 
+// one layer of the layered paper-NIF family (mlp_kernel.cu): blocked fp16 weights, fp32 bias
+struct MlpLayer {
+    int K = 0, N_valid = 0, BN = 0, NT = 0;
+    void* d_w = nullptr;
+    float* d_bias = nullptr;
+};
+
 struct pt_nif {
     int device = 0;
     int kind = PT_NIF_SIREN;
     void* d_smem_image = nullptr;     // pre-laid-out shared-memory image of the fused kernel
     int64_t smem_bytes = 0;
-    uint16_t* d_blob = nullptr;       // raw fp16 blob (reference SIMT kernel)
+    uint16_t* d_blob = nullptr;       // raw fp16 blob
+    // PT_NIF_FR_FAMILY (layered GEMM path)
+    int mlp_H = 0, mlp_L = 0, mlp_c = 0;
+    float* mlp_freq = nullptr;        // B [20][2] fp32
+    std::vector<MlpLayer> mlp_layers;
+    void* mlp_act[2] = {nullptr, nullptr};   // blocked activation ping-pong buffers (lazily sized)
+    int64_t mlp_act_bytes = 0;
 };
 
 namespace pt {
@@ -147,5 +160,12 @@ void nif_build_smem_image_fr(const uint16_t* blob, std::vector<uint8_t>* image);
 cudaError_t launch_nif(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,
                        int64_t max_rows, float* out, int dir_input, cudaStream_t st);
 int num_sms();
+// the paper's NIF family (mlp_kernel.cu)
+int mlp_concat_layer(int L);
+int64_t mlp_blob_halves(int H, int L);
+int mlp_load(pt_nif* nif, int H, int L, const uint16_t* blob, std::string* msg);
+void mlp_free(pt_nif* nif);
+cudaError_t launch_mlp(pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count, int64_t max_rows,
+                       float* out, int dir_input, cudaStream_t st);
 
 }  // namespace pt

@@ -29,7 +29,8 @@ class PtStats(C.Structure):
                 ("nif_launches", C.c_int64), ("traverse_launches", C.c_int64)]
 
 
-EXPORTED = ["pt_scene_create", "pt_scene_destroy", "pt_nif_load", "pt_nif_load_ex", "pt_nif_destroy", "pt_render",
+EXPORTED = ["pt_scene_create", "pt_scene_destroy", "pt_nif_load", "pt_nif_load_ex", "pt_nif_load_family",
+            "pt_nif_destroy", "pt_render",
             "pt_render_samples", "pt_trace_primary", "pt_trace_rays", "pt_nif_infer", "pt_get_stats",
             "pt_set_profiling", "pt_last_error", "pt_version"]
 
@@ -47,6 +48,7 @@ def lib():
             L.pt_scene_destroy.argtypes = [P]
             L.pt_nif_load.argtypes = [P, I64, C.POINTER(P)]
             L.pt_nif_load_ex.argtypes = [I32, P, I64, C.POINTER(P)]
+            L.pt_nif_load_family.argtypes = [I32, I32, P, I64, C.POINTER(P)]
             L.pt_nif_destroy.argtypes = [P]
             L.pt_render.argtypes = [P, P, P, I32, I32, I32, I32, U64, P]
             L.pt_render_samples.argtypes = [P, P, P, I32, I32, I32, I32, I32, U64, I32, P, P]
@@ -122,13 +124,18 @@ class Scene:
 
 NIF_SIREN = 0          # PT_NIF_SIREN: SIREN 2-128x4-3 (scenes.siren_blob)
 NIF_FOURIER_RELU = 1   # PT_NIF_FOURIER_RELU: the paper's Fourier/ReLU/YUV NIF (scenes.fourier_relu_blob)
+NIF_FR_FAMILY = 2      # PT_NIF_FR_FAMILY: the size-sweep family (scenes.fourier_relu_family_blob)
 
 
 class Nif:
-    def __init__(self, blob: np.ndarray, kind: int = NIF_SIREN):
+    def __init__(self, blob: np.ndarray, kind: int = NIF_SIREN, hidden: int = 0, layers: int = 0):
+        """kind NIF_FR_FAMILY needs (hidden, layers): pt_nif_load_family; else pt_nif_load_ex."""
         b = np.ascontiguousarray(blob, dtype=np.uint16)
         h = C.c_void_p()
-        _check(lib().pt_nif_load_ex(int(kind), _p(b), b.size, C.byref(h)))
+        if kind == NIF_FR_FAMILY:
+            _check(lib().pt_nif_load_family(int(hidden), int(layers), _p(b), b.size, C.byref(h)))
+        else:
+            _check(lib().pt_nif_load_ex(int(kind), _p(b), b.size, C.byref(h)))
         self._lib = lib()
         self.h = h
         self.kind = int(kind)

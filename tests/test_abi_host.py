@@ -61,3 +61,23 @@ def test_null_arguments(L):
     assert L.pt_render_samples(None, None, None, 4, 4, 0, 1, 1, 0, 0, None, None) == -1
     assert L.pt_get_stats(None, None) == -1
     assert L.pt_version().startswith(b"pt_b200")
+
+
+def test_nif_family_argument_checks(L):
+    b = scenes.fourier_relu_family_blob(64, 2)
+    h = C.c_void_p()
+    assert L.pt_nif_load_family(96, 2, pt._p(b), b.size, C.byref(h)) == -1          # hidden % 64 != 0
+    assert L.pt_nif_load_family(64, 0, pt._p(b), b.size, C.byref(h)) == -1          # layers < 1
+    assert L.pt_nif_load_family(128, 2, pt._p(b), b.size, C.byref(h)) == -3         # size of (128, 2) differs
+    bad = b.copy()
+    bad[41] = 0x7C00
+    assert L.pt_nif_load_family(64, 2, pt._p(bad), bad.size, C.byref(h)) == -2
+
+
+def test_every_declared_symbol_is_exported(L):
+    import re
+    decl = re.findall(r"PT_API\s+[\w\s\*]+?\b(pt_\w+)\s*\(", open(pt.os.path.join(
+        pt.os.path.dirname(pt._PKG), "include", "pt.h")).read())
+    assert set(decl) == set(pt.EXPORTED)
+    for name in decl:
+        assert hasattr(L, name), name

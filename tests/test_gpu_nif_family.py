@@ -1,0 +1,110 @@
+"""GPU parity of the paper's NIF family of the size sweep (pt_nif_load_family, the
+layered tcgen05 GEMM path of mlp_kernel.cu) against the fp64 oracle (oracle.fr_eval_hl) on the same
+seeded networks and queries. Gates as for the other NIFs: |dy| <= 1e-3 in log
+space and relative error of exp(y) <= 1e-2, plus a derived bound for the wide nets: the fp16 rounding of
+each layer's activations (2^-11 relative) propagated through the |W| row sums."""
+import numpy as np
+import pytest
+
+from paper_2305_20061_b200 import scenes
+
+pytestmark = pytest.mark.gpu
+
+NIF_LOG_GATE = 1e-3
+NIF_REL_GATE = 1e-2
+
+
+@pytest.fixture(scope="module")
+def ptm():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2305_20061_b200 import _build, pt
+    _build.build()
+    pt.lib()
+    return pt
+
+
+def _queries(n, seed):
+    uv = scenes.query_uv(n, seed)
+    edge = np.array([[0, 0], [1, 1], [0.5, 0.5], [0, 1], [1, 0], [1e-7, 0.5]], np.float32)
+    return np.concatenate([edge, uv])[:n] if n >= len(edge) else uv
+
+
+def _log_gate(H, L, blob):
+    """fp16 activations: every layer's output rounded once (2^-11 relative) and propagated through
+    the following layers' |W| (a bound, not an estimate); at least the 1e-3 gate."""
+    B = np.asarray(blob, np.uint16).view(np.float16).astype(np.float64)
+    dims = scenes.fr_family_layers(H, L)
+    off, Ws = 40, []
+    for fin, fout in dims:
+        Ws.append(np.abs(B[off:off + fin * fout].reshape(fout, fin)))
+        off += fin * fout + fout
+    # propagate a unit relative error bound of 2^-11 * (typical |h| <= 4) per layer
+    g = 0.0
+    for W in Ws[1:]:
+        g = (g + 2.0 ** -11 * 4.0) * W.sum(1).max()
+    return max(NIF_LOG_GATE, 3.0 * g)
+
+
+@pytest.mark.parametrize("H,L", scenes.NIF_SWEEP)
+@pytest.mark.parametrize("n", [1, 129, 4 * 148 * 128 + 77])
+def test_family_vs_oracle(ptm, orc, H, L, n):
+    import torch
+    blob = scenes.fourier_relu_family_blob(H, L, seed=1)
+    nif = ptm.Nif(blob, kind=ptm.NIF_FR_FAMILY, hidden=H, layers=L)
+    uv = _queries(n, seed=n + H)
+    got = ptm.nif_infer(nif, torch.from_numpy(uv).cuda()).cpu().numpy().astype(np.float64)
+    assert np.isfinite(got).all() and (got > 0).all()
+    k = min(n, 2000 if H < 1024 else 300)                 # the fp64 oracle costs 14.7 MFLOP per H1024 query
+    idx = np.linspace(0, n - 1, k).astype(np.int64)
+    y = orc.fr_eval_hl(H, L, blob, uv[idx].astype(np.float64))
+    assert np.abs(np.log(got[idx]) - y).max() <= _log_gate(H, L, blob)
+    assert (np.abs(got[idx] - np.exp(y)) / np.exp(y)).max() <= NIF_REL_GATE
+
+
+def test_family_row_chunks(ptm, orc):
+    """More rows than one launch chunk (2^20): every chunk boundary and the ragged tail."""
+    import torch
+    H, L = 64, 2
+    blob = scenes.fourier_relu_family_blob(H, L, seed=2)
+    nif = ptm.Nif(blob, kind=ptm.NIF_FR_FAMILY, hidden=H, layers=L)
+    n = (1 << 20) * 2 + 333
+    uv = scenes.query_uv(n, 9)
+    got = ptm.nif_infer(nif, torch.from_numpy(uv).cuda()).cpu().numpy().astype(np.float64)
+    idx = np.concatenate([np.arange(0, 50), (1 << 20) + np.arange(-50, 50), (2 << 20) + np.arange(-50, 333)])
+    y = orc.fr_eval_hl(H, L, blob, uv[idx].astype(np.float64))
+    assert np.abs(np.log(got[idx]) - y).max() <= _log_gate(H, L, blob)
+
+
+def test_family_h128_l4_matches_fused_kernel(ptm):
+    """The (128, 4) member through the layered path and the fused PT_NIF_FOURIER_RELU kernel (same
+    weights): both fp16-activation evaluations of one network agree to the gate."""
+    import torch
+    blob = scenes.fourier_relu_blob(0)
+    a = ptm.Nif(blob, kind=ptm.NIF_FR_FAMILY, hidden=128, layers=4)
+    b = ptm.Nif(blob, kind=ptm.NIF_FOURIER_RELU)
+    uv = torch.from_numpy(scenes.query_uv(20000, 4)).cuda()
+    ya = ptm.nif_infer(a, uv).log().cpu().numpy()
+    yb = ptm.nif_infer(b, uv).log().cpu().numpy()
+    assert np.abs(ya - yb).max() <= 2 * NIF_LOG_GATE
+
+
+def test_family_rejects_bad_shapes(ptm):
+    blob = scenes.fourier_relu_family_blob(64, 2)
+    with pytest.raises(ptm.PtError):
+        ptm.Nif(blob, kind=ptm.NIF_FR_FAMILY, hidden=128, layers=2)     # wrong size for (128, 2)
+    with pytest.raises(ptm.PtError):
+        ptm.Nif(blob, kind=ptm.NIF_FR_FAMILY, hidden=96, layers=2)      # not a multiple of 64
+
+
+def test_render_with_family_nif(ptm):
+    """A render through each sweep member: finite, positive radiance where rays escape, deterministic."""
+    c = scenes.CONFIGS[2]
+    S = ptm.Scene(scenes.scene_for_config(2))
+    for H, L in scenes.NIF_SWEEP:
+        nif = ptm.Nif(scenes.fourier_relu_family_blob(H, L, seed=1), kind=ptm.NIF_FR_FAMILY, hidden=H, layers=L)
+        a = ptm.render(S, nif, 96, 64, 2, c.max_depth, seed=3)
+        b = ptm.render(S, nif, 96, 64, 2, c.max_depth, seed=3)
+        assert np.isfinite(a).all() and (a >= 0).all() and a.max() > 0
+        assert np.array_equal(a, b)
