@@ -72,9 +72,11 @@ struct TimedLaunch {
     int cls;
     cudaEvent_t a, b;
 };
-constexpr int kCounters = 64;   // [d] = alive count produced at depth d (d = 0 raygen), [62] = escaped, [63] = error flags
+constexpr int kCounters = 128;  // [d] = alive count produced at depth d (d = 0 raygen), [62] = escaped, [63] = error
+                                // flags, [64 + d] = work-fetch counter of bounce d
 constexpr int kCounterEsc = 62;
 constexpr int kCounterErr = 63;
+constexpr int kCounterWork = 64;
 
 }  // namespace pt
 

@@ -528,6 +528,7 @@ struct ShadeArgs {
     uint2 key;
     const uint32_t* cnt_in;
     uint32_t* cnt_out;
+    uint32_t* work;
     uint32_t* cnt_esc;
     int use_nif;
     float3 env;
@@ -551,10 +552,15 @@ struct ShadeArgs {
 __global__ void __launch_bounds__(128, PT_TS_MINB) trace_shade_kernel(ShadeArgs a) {
     const uint32_t n = *a.cnt_in;
     const int np = a.W * a.H;
-    const uint32_t stride = gridDim.x * blockDim.x;
-    // warp-uniform trip count so every lane reaches the ballots
-    const uint32_t n_round = (n + 31u) & ~31u;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += stride) {
+    const int lane_id = threadIdx.x & 31;
+    // dynamic work fetching, 32 paths per warp and fetch (one atomic): no static partition, so the SMs
+    // finish a bounce together instead of waiting for the slowest grid-stride share
+    for (;;) {
+        uint32_t base = 0;
+        if (lane_id == 0) base = atomicAdd(a.work, 32u);
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        if (base >= n) break;
+        const uint32_t i = base + (uint32_t)lane_id;
         const bool active = i < n;
         bool alive = false, escaped = false;
         uint32_t slot = 0;
@@ -767,6 +773,7 @@ void launch_trace_shade(const TraceParams& tp, int W, int H, int first_sample, i
     a.W = W; a.H = H; a.first_sample = first_sample; a.depth = depth; a.max_depth = max_depth;
     a.key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
     a.cnt_in = count_in; a.cnt_out = count_out; a.cnt_esc = ws.counters + kCounterEsc;
+    a.work = ws.counters + kCounterWork + depth;
     a.use_nif = use_nif; a.env = env;
     a.A_in = ws.rayA[buf]; a.B_in = ws.rayB[buf]; a.C_in = ws.rayC[buf];
     a.A_out = ws.rayA[buf ^ 1]; a.B_out = ws.rayB[buf ^ 1]; a.C_out = ws.rayC[buf ^ 1];
