@@ -161,7 +161,7 @@ void collect_timers(pt_scene* sc) {
 
 __global__ void stats_kernel(const uint32_t* counters, int max_depth, unsigned long long* acc) {
     unsigned long long seg = 0;
-    for (int d = 0; d < max_depth; ++d) seg += counters[d];
+    for (int d = 0; d < max_depth; ++d) seg += counters[2 * d];
     acc[0] += counters[0];
     acc[1] += seg;
     acc[2] += counters[pt::kCounterEsc];
@@ -169,12 +169,19 @@ __global__ void stats_kernel(const uint32_t* counters, int max_depth, unsigned l
 
 __global__ void set_count_kernel(uint32_t* c, uint32_t v) { *c = v; }
 
+// total escaped paths of the wave (the NIF's row count) from the bounces' packed queue counters
+__global__ void escaped_total_kernel(uint32_t* counters, int max_depth) {
+    uint32_t e = 0;
+    for (int d = 1; d <= max_depth; ++d) e += counters[2 * d + 1];
+    counters[pt::kCounterEsc] = e;
+}
+
 int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, int W, int H, int first_sample,
                         int n_samples, int max_depth, uint64_t seed, int wave_samples, float* d_accum,
                         cudaStream_t st) {
     if (W < 1 || H < 1 || n_samples < 1 || max_depth < 1 || first_sample < 0)
         return fail(PT_ERR_INVALID_ARG, "width, height, n_samples, max_depth must be >= 1");
-    if (max_depth >= pt::kCounterEsc - 1) return fail(PT_ERR_INVALID_ARG, "max_depth too large (<= 60)");
+    if (max_depth > 60) return fail(PT_ERR_INVALID_ARG, "max_depth too large (<= 60)");
     if (!nif && !env_rgb) return fail(PT_ERR_INVALID_ARG, "env_rgb must be given when nif is NULL");
     if (!d_accum) return fail(PT_ERR_INVALID_ARG, "d_accum is NULL");
     const int64_t np = (int64_t)W * H;
@@ -221,12 +228,13 @@ int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, i
         for (int d = 1; d <= max_depth; ++d) {
             const int buf = (d - 1) & 1;       // bounce d reads state buffer buf, shade writes buf ^ 1
             tm.begin(T_TRAVERSE, &e0);
-            pt::launch_trace_shade(tp, W, H, (int)w0, d, max_depth, seed, buf, ws.counters + (d - 1),
-                                   ws.counters + d, use_nif, env, ws, st);
+            pt::launch_trace_shade(tp, W, H, (int)w0, d, max_depth, seed, buf, use_nif, env, ws, st);
             tm.end(T_TRAVERSE, e0);
             stats.launches += 1;
             stats.traverse_launches += 1;
         }
+        escaped_total_kernel<<<1, 1, 0, st>>>(ws.counters, max_depth);
+        stats.launches += 1;
         if (use_nif) {
             tm.begin(T_NIF, &e0);
             cudaError_t e = pt::launch_nif(nif, ws.esc, ws.esc_beta, ws.counters + pt::kCounterEsc, slots, ws.wave_buf, 1, st);

@@ -72,11 +72,14 @@ struct TimedLaunch {
     int cls;
     cudaEvent_t a, b;
 };
-constexpr int kCounters = 128;  // [d] = alive count produced at depth d (d = 0 raygen), [62] = escaped, [63] = error
-                                // flags, [64 + d] = work-fetch counter of bounce d
-constexpr int kCounterEsc = 62;
-constexpr int kCounterErr = 63;
-constexpr int kCounterWork = 64;
+// device counters of one wave (uint32 words): [2d, 2d+1] = the packed 64-bit queue counter of bounce d
+// (low: alive paths appended by bounce d, d = 0 raygen; high: escaped paths appended by bounce d), one
+// 64-bit atomic per warp appends to both queues; [128] = total escaped, [129] = error flags, [130 + d] =
+// work-fetch counter of bounce d
+constexpr int kCounters = 192;
+constexpr int kCounterEsc = 128;
+constexpr int kCounterErr = 129;
+constexpr int kCounterWork = 130;
 
 }  // namespace pt
 
@@ -144,8 +147,7 @@ struct TraceParams {
 void launch_raygen(const Cam32& cam, int W, int H, int first_sample, int n_slots, uint64_t seed, Workspace& ws,
                    cudaStream_t st);
 void launch_trace_shade(const TraceParams& tp, int W, int H, int first_sample, int depth, int max_depth, uint64_t seed,
-                  int buf, const uint32_t* count_in, uint32_t* count_out, int use_nif, float3 env, Workspace& ws,
-                  cudaStream_t st);
+                        int buf, int use_nif, float3 env, Workspace& ws, cudaStream_t st);
 void launch_accumulate(const float* wave_buf, int n_pix, int k, float* fb, cudaStream_t st);
 void launch_primary(const TraceParams& tp, const Cam32& cam, int W, int H, int sample, uint64_t seed,
                     int32_t* prim, float* t, cudaStream_t st);

@@ -63,10 +63,8 @@ struct RayT {
     float o[3], d[3], inv[3];   // slab test, sphere test
     float ok[3];          // origin permuted to (kx, ky, kz)
     float Sx, Sy, Sz;     // fp32 shear (pre-test only)
-    double Sx64, Sy64, Sz64;
     int kx, ky, kz;
     unsigned negmask;     // bit a: d[a] has its sign bit set
-    bool have64;
 };
 
 __device__ __forceinline__ float self3(float3 v, int k) { return k == 0 ? v.x : (k == 1 ? v.y : v.z); }
@@ -81,12 +79,12 @@ __device__ __forceinline__ void ray_prepare(float3 o, float3 d, RayT& r) {
     if (dkz < 0.0f) { int t = kx; kx = ky; ky = t; }
     r.kx = kx; r.ky = ky; r.kz = kz;
     // fp32 shear for the pre-test only (its error bound tolerates the reciprocal-multiply form);
-    // the fp64 shear of the exact test is computed on first use (ensure64)
+    // the fp64 shear of the exact test is recomputed by each (rare) fp64 test: caching it would keep
+    // six more registers live through the whole traversal
     const float rz = __frcp_rn(dkz);
     r.Sx = self3(d, kx) * rz;
     r.Sy = self3(d, ky) * rz;
     r.Sz = rz;
-    r.have64 = false;
     r.o[0] = o.x; r.o[1] = o.y; r.o[2] = o.z;
     r.d[0] = d.x; r.d[1] = d.y; r.d[2] = d.z;
     r.ok[0] = self3(o, kx); r.ok[1] = self3(o, ky); r.ok[2] = self3(o, kz);
@@ -95,14 +93,13 @@ __device__ __forceinline__ void ray_prepare(float3 o, float3 d, RayT& r) {
 }
 
 // fp64 shear constants, exactly the oracle's divisions
-__device__ __forceinline__ void ensure64(RayT& r) {
-    if (r.have64) return;
+struct Shear64 {
+    double Sx, Sy, Sz;
+};
+__device__ __forceinline__ Shear64 shear64(const RayT& r) {
     const float3 d = make_float3(r.d[0], r.d[1], r.d[2]);
     const double dkz64 = (double)self3(d, r.kz);
-    r.Sx64 = __ddiv_rn((double)self3(d, r.kx), dkz64);
-    r.Sy64 = __ddiv_rn((double)self3(d, r.ky), dkz64);
-    r.Sz64 = __ddiv_rn(1.0, dkz64);
-    r.have64 = true;
+    return {__ddiv_rn((double)self3(d, r.kx), dkz64), __ddiv_rn((double)self3(d, r.ky), dkz64), __ddiv_rn(1.0, dkz64)};
 }
 
 // Certified fp32 watertight test. Returns 0 if the exact (hence the fp64 oracle's) test certainly
@@ -166,7 +163,7 @@ __device__ __forceinline__ int tri_test32(const RayT& r, float3 v0, float3 v1, f
 
 // fp64 watertight test in the oracle's operation order; true and t if hit with t > 0
 __device__ __forceinline__ bool tri_test64(RayT& r, float3 v0, float3 v1, float3 v2, double& t_out) {
-    ensure64(r);
+    const Shear64 sh = shear64(r);
     const double ox = r.ok[0], oy = r.ok[1], oz = r.ok[2];
     const double A0 = __dsub_rn((double)self3(v0, r.kx), ox);
     const double A1 = __dsub_rn((double)self3(v0, r.ky), oy);
@@ -177,21 +174,21 @@ __device__ __forceinline__ bool tri_test64(RayT& r, float3 v0, float3 v1, float3
     const double C0 = __dsub_rn((double)self3(v2, r.kx), ox);
     const double C1 = __dsub_rn((double)self3(v2, r.ky), oy);
     const double C2 = __dsub_rn((double)self3(v2, r.kz), oz);
-    const double Ax = __dsub_rn(A0, __dmul_rn(r.Sx64, A2));
-    const double Ay = __dsub_rn(A1, __dmul_rn(r.Sy64, A2));
-    const double Bx = __dsub_rn(B0, __dmul_rn(r.Sx64, B2));
-    const double By = __dsub_rn(B1, __dmul_rn(r.Sy64, B2));
-    const double Cx = __dsub_rn(C0, __dmul_rn(r.Sx64, C2));
-    const double Cy = __dsub_rn(C1, __dmul_rn(r.Sy64, C2));
+    const double Ax = __dsub_rn(A0, __dmul_rn(sh.Sx, A2));
+    const double Ay = __dsub_rn(A1, __dmul_rn(sh.Sy, A2));
+    const double Bx = __dsub_rn(B0, __dmul_rn(sh.Sx, B2));
+    const double By = __dsub_rn(B1, __dmul_rn(sh.Sy, B2));
+    const double Cx = __dsub_rn(C0, __dmul_rn(sh.Sx, C2));
+    const double Cy = __dsub_rn(C1, __dmul_rn(sh.Sy, C2));
     const double U = __dsub_rn(__dmul_rn(Cx, By), __dmul_rn(Cy, Bx));
     const double V = __dsub_rn(__dmul_rn(Ax, Cy), __dmul_rn(Ay, Cx));
     const double Wt = __dsub_rn(__dmul_rn(Bx, Ay), __dmul_rn(By, Ax));
     if ((U < 0.0 || V < 0.0 || Wt < 0.0) && (U > 0.0 || V > 0.0 || Wt > 0.0)) return false;
     const double det = __dadd_rn(__dadd_rn(U, V), Wt);
     if (det == 0.0) return false;
-    const double Az = __dmul_rn(r.Sz64, A2);
-    const double Bz = __dmul_rn(r.Sz64, B2);
-    const double Cz = __dmul_rn(r.Sz64, C2);
+    const double Az = __dmul_rn(sh.Sz, A2);
+    const double Bz = __dmul_rn(sh.Sz, B2);
+    const double Cz = __dmul_rn(sh.Sz, C2);
     const double T = __dadd_rn(__dadd_rn(__dmul_rn(U, Az), __dmul_rn(V, Bz)), __dmul_rn(Wt, Cz));
     if (det < 0.0 && T >= 0.0) return false;
     if (det > 0.0 && T <= 0.0) return false;
@@ -510,26 +507,30 @@ __global__ void __launch_bounds__(256) raygen_kernel(Cam32 cam, int W, int H, in
     }
 }
 
-// warp-aggregated append: one atomic per warp (Guideline 12), returns this lane's slot
-__device__ __forceinline__ uint32_t warp_append(bool pred, uint32_t* counter) {
-    const uint32_t mask = __ballot_sync(0xFFFFFFFFu, pred);
-    if (mask == 0) return 0;
+// warp-aggregated append to the alive and the escaped queue at once: one 64-bit atomic per warp on the
+// bounce's packed counter (low: alive, high: escaped); returns this lane's positions in both queues
+__device__ __forceinline__ void warp_append2(bool alive, bool escaped, unsigned long long* counter, uint32_t& pos_a,
+                                             uint32_t& pos_e) {
+    const uint32_t ma = __ballot_sync(0xFFFFFFFFu, alive), me = __ballot_sync(0xFFFFFFFFu, escaped);
+    if ((ma | me) == 0) return;
     const int lane = threadIdx.x & 31;
-    const int leader = __ffs(mask) - 1;
-    uint32_t base = 0;
-    if (lane == leader) base = atomicAdd(counter, (uint32_t)__popc(mask));
+    const int leader = __ffs(ma | me) - 1;
+    unsigned long long base = 0;
+    if (lane == leader)
+        base = atomicAdd(counter, ((unsigned long long)__popc(me) << 32) | (unsigned long long)__popc(ma));
     base = __shfl_sync(0xFFFFFFFFu, base, leader);
-    return base + (uint32_t)__popc(mask & ((1u << lane) - 1u));
+    const uint32_t lt = (1u << lane) - 1u;
+    pos_a = (uint32_t)base + (uint32_t)__popc(ma & lt);
+    pos_e = (uint32_t)(base >> 32) + (uint32_t)__popc(me & lt);
 }
 
 struct ShadeArgs {
     TraceParams tp;
     int W, H, first_sample, depth, max_depth;
     uint2 key;
-    const uint32_t* cnt_in;
-    uint32_t* cnt_out;
+    const uint32_t* counters;   // the wave's counters (pt_internal.h kCounters layout)
+    unsigned long long* q_out;  // packed queue counter of this bounce
     uint32_t* work;
-    uint32_t* cnt_esc;
     int use_nif;
     float3 env;
     const float4* A_in;
@@ -550,7 +551,10 @@ struct ShadeArgs {
 #define PT_TS_MINB 7   // min resident blocks per SM for trace_shade: 72-register cap; tools/ts_tune.sh on B200
 #endif
 __global__ void __launch_bounds__(128, PT_TS_MINB) trace_shade_kernel(ShadeArgs a) {
-    const uint32_t n = *a.cnt_in;
+    const uint32_t n = a.counters[2 * (a.depth - 1)];          // alive paths of the previous bounce
+    // this bounce's escaped paths follow those of the earlier bounces in the escaped queue
+    uint32_t esc_base = 0;
+    for (int d = 1; d < a.depth; ++d) esc_base += a.counters[2 * d + 1];
     const int np = a.W * a.H;
     const int lane_id = threadIdx.x & 31;
     // dynamic work fetching, 32 paths per warp and fetch (one atomic): no static partition, so the SMs
@@ -683,8 +687,9 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) trace_shade_kernel(ShadeArgs 
                 a.wave_buf[3 * (size_t)slot + 2] = L.z;
             }
         }
-        const uint32_t pos_a = warp_append(alive, a.cnt_out);
-        const uint32_t pos_e = warp_append(escaped, a.cnt_esc);
+        uint32_t pos_a = 0, pos_e = 0;
+        warp_append2(alive, escaped, a.q_out, pos_a, pos_e);
+        pos_e += esc_base;
         if (alive) {
             a.A_out[pos_a] = make_float4(o3.x, o3.y, o3.z, __uint_as_float(slot));
             a.B_out[pos_a] = make_float4(wi.x, wi.y, wi.z, bt.x);
@@ -766,13 +771,13 @@ static int resident_grid(K kernel, int block) {
 }
 
 void launch_trace_shade(const TraceParams& tp, int W, int H, int first_sample, int depth, int max_depth, uint64_t seed,
-                  int buf, const uint32_t* count_in, uint32_t* count_out, int use_nif, float3 env, Workspace& ws,
-                  cudaStream_t st) {
+                        int buf, int use_nif, float3 env, Workspace& ws, cudaStream_t st) {
     ShadeArgs a;
     a.tp = tp;
     a.W = W; a.H = H; a.first_sample = first_sample; a.depth = depth; a.max_depth = max_depth;
     a.key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
-    a.cnt_in = count_in; a.cnt_out = count_out; a.cnt_esc = ws.counters + kCounterEsc;
+    a.counters = ws.counters;
+    a.q_out = reinterpret_cast<unsigned long long*>(ws.counters + 2 * depth);
     a.work = ws.counters + kCounterWork + depth;
     a.use_nif = use_nif; a.env = env;
     a.A_in = ws.rayA[buf]; a.B_in = ws.rayB[buf]; a.C_in = ws.rayC[buf];
