@@ -61,8 +61,12 @@ __device__ __forceinline__ float3 cam_dir(const Cam32& k, int W, int H, int x, i
 // ---------------------------------------------------------------------------------------------
 struct RayT {
     float o[3], d[3], inv[3];   // slab test, sphere test
-    float ok[3];          // origin permuted to (kx, ky, kz)
-    float Sx, Sy, Sz;     // fp32 shear (pre-test only)
+    // fp32 shear of the certified pre-test as a matrix over the world axes a, so a vertex is sheared with
+    // packed FFMA2s instead of permutation selects: (Ax, Ay) = sum_a mxy[a] (v - o)_a with mxy[a] =
+    // ((e_kx - Sx e_kz)_a, (e_ky - Sy e_kz)_a), Az = sum_a mz[a] (v - o)_a with mz = Sz e_kz
+    float2 mxy[3];
+    float mz[3];
+    float aSx, aSy, adkz;       // |Sx|, |Sy|, |d[kz]| for the error bounds
     int kx, ky, kz;
     unsigned negmask;     // bit a: d[a] has its sign bit set
 };
@@ -82,12 +86,17 @@ __device__ __forceinline__ void ray_prepare(float3 o, float3 d, RayT& r) {
     // the fp64 shear of the exact test is recomputed by each (rare) fp64 test: caching it would keep
     // six more registers live through the whole traversal
     const float rz = __frcp_rn(dkz);
-    r.Sx = self3(d, kx) * rz;
-    r.Sy = self3(d, ky) * rz;
-    r.Sz = rz;
+    const float Sx = self3(d, kx) * rz, Sy = self3(d, ky) * rz;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        r.mxy[a] = make_float2(a == kx ? 1.0f : (a == kz ? -Sx : 0.0f), a == ky ? 1.0f : (a == kz ? -Sy : 0.0f));
+        r.mz[a] = a == kz ? rz : 0.0f;
+    }
+    r.aSx = fabsf(Sx);
+    r.aSy = fabsf(Sy);
+    r.adkz = fabsf(dkz);
     r.o[0] = o.x; r.o[1] = o.y; r.o[2] = o.z;
     r.d[0] = d.x; r.d[1] = d.y; r.d[2] = d.z;
-    r.ok[0] = self3(o, kx); r.ok[1] = self3(o, ky); r.ok[2] = self3(o, kz);
     r.inv[0] = __frcp_rn(d.x); r.inv[1] = __frcp_rn(d.y); r.inv[2] = __frcp_rn(d.z);
     r.negmask = (signbit(d.x) ? 1u : 0u) | (signbit(d.y) ? 2u : 0u) | (signbit(d.z) ? 4u : 0u);
 }
@@ -102,39 +111,53 @@ __device__ __forceinline__ Shear64 shear64(const RayT& r) {
     return {__ddiv_rn((double)self3(d, r.kx), dkz64), __ddiv_rn((double)self3(d, r.ky), dkz64), __ddiv_rn(1.0, dkz64)};
 }
 
+// Shear one vertex into the ray's frame: D = v - o (world axes, one rounding each), then the products
+// with the 0/1/-S entries of the shear rows; at most two roundings per sheared coordinate (the -S
+// product and the sum), the same single-rounding Sz D[kz] for Az as the permuted form.
+__device__ __forceinline__ void shear_vertex(const RayT& r, float3 v, float& x, float& y, float& z) {
+    const float2 dxy = __fadd2_rn(make_float2(v.x, v.y), make_float2(-r.o[0], -r.o[1]));
+    const float dz = v.z - r.o[2];
+    float2 a = __fmul2_rn(r.mxy[0], make_float2(dxy.x, dxy.x));
+    a = __ffma2_rn(r.mxy[1], make_float2(dxy.y, dxy.y), a);
+    a = __ffma2_rn(r.mxy[2], make_float2(dz, dz), a);
+    x = a.x;
+    y = a.y;
+    z = fmaf(r.mz[2], dz, fmaf(r.mz[1], dxy.y, r.mz[0] * dxy.x));
+}
+
 // Certified fp32 watertight test. Returns 0 if the exact (hence the fp64 oracle's) test certainly
 // misses, 1 if it certainly hits with t in [t - dt, t + dt], t - dt > 0, and 2 if undecided (near an
 // edge or t ~ 0): then the fp64 test decides. Error bounds: with eps = 2^-24,
-// mX = max|A[kx]| + |Sx| max|A[kz]| (over the 3 vertices) and likewise mY, the sheared coordinates
-// carry |dAx| <= eX = 4 eps mX, |dAy| <= eY = 4 eps mY. First a uniform bound on the edge functions,
-// |dU| <= 19 eps mX mY (we use 24); if that leaves the signs undecided (ray origins far from small
+// mX >= max|A[kx]| + |Sx| max|A[kz]| (over the 3 vertices; computed as max|Ax| + 2|Sx| max|A[kz]|) and
+// likewise mY, the sheared coordinates carry |dAx| <= eX = 5 eps mX, |dAy| <= eY = 5 eps mY (two
+// roundings, the D = v - o rounding and the fp32 S). First a uniform bound on the edge functions,
+// |dU| <= 23 eps mX mY (we use 26); if that leaves the signs undecided (ray origins far from small
 // triangles: mX mY >> |U|), per-edge bounds that scale with the sheared coordinates themselves,
-//   |dU| <= eX (|By| + |Cy|) + eY (|Bx| + |Cx|) + eps (|U| + |Cy Bx|) + 32 eps^2 mX mY
+//   |dU| <= eX (|By| + |Cy|) + eY (|Bx| + |Cx|) + eps (|U| + |Cy Bx|) + 50 eps^2 mX mY
 // (U = Cx By - Cy Bx; likewise V, W), plus 2^-44 mX mY for the fp64 oracle's own rounding, times 1.125.
-// Then |dT| <= (eU + eV + eW) mZ + 18 eps maxE mZ, |ddet| <= eU + eV + eW + 6 eps maxE, mZ = |Sz| max|A[kz]|.
+// Then |dT| <= (eU + eV + eW) mZ + 18 eps maxE mZ, |ddet| <= eU + eV + eW + 6 eps maxE, mZ >= max|Az|.
 __device__ __forceinline__ int tri_test32(const RayT& r, float3 v0, float3 v1, float3 v2, float& t, float& dt) {
     constexpr float eps = 0x1p-24f;
-    const float A0 = self3(v0, r.kx) - r.ok[0], A1 = self3(v0, r.ky) - r.ok[1], A2 = self3(v0, r.kz) - r.ok[2];
-    const float B0 = self3(v1, r.kx) - r.ok[0], B1 = self3(v1, r.ky) - r.ok[1], B2 = self3(v1, r.kz) - r.ok[2];
-    const float C0 = self3(v2, r.kx) - r.ok[0], C1 = self3(v2, r.ky) - r.ok[1], C2 = self3(v2, r.kz) - r.ok[2];
-    const float Ax = fmaf(-r.Sx, A2, A0), Ay = fmaf(-r.Sy, A2, A1);
-    const float Bx = fmaf(-r.Sx, B2, B0), By = fmaf(-r.Sy, B2, B1);
-    const float Cx = fmaf(-r.Sx, C2, C0), Cy = fmaf(-r.Sy, C2, C1);
+    float Ax, Ay, Az, Bx, By, Bz, Cx, Cy, Cz;
+    shear_vertex(r, v0, Ax, Ay, Az);
+    shear_vertex(r, v1, Bx, By, Bz);
+    shear_vertex(r, v2, Cx, Cy, Cz);
     const float CyBx = Cy * Bx, AyCx = Ay * Cx, ByAx = By * Ax;
     const float U = fmaf(Cx, By, -CyBx);
     const float V = fmaf(Ax, Cy, -AyCx);
     const float W = fmaf(Bx, Ay, -ByAx);
-    const float mz2 = fmaxf(fabsf(A2), fmaxf(fabsf(B2), fabsf(C2)));
-    const float mX = fmaf(fabsf(r.Sx), mz2, fmaxf(fabsf(A0), fmaxf(fabsf(B0), fabsf(C0))));
-    const float mY = fmaf(fabsf(r.Sy), mz2, fmaxf(fabsf(A1), fmaxf(fabsf(B1), fabsf(C1))));
-    float eU = (24.0f * eps) * mX * mY, eV = eU, eW = eU;
+    const float mZ = (1.0f + 2.0f * eps) * fmaxf(fabsf(Az), fmaxf(fabsf(Bz), fabsf(Cz)));   // >= max|Sz A[kz]|
+    const float mz2 = (1.0f + 4.0f * eps) * mZ * r.adkz;                                      // >= max|A[kz]|
+    const float mX = fmaf(2.0f * r.aSx, mz2, fmaxf(fabsf(Ax), fmaxf(fabsf(Bx), fabsf(Cx))));
+    const float mY = fmaf(2.0f * r.aSy, mz2, fmaxf(fabsf(Ay), fmaxf(fabsf(By), fabsf(Cy))));
+    float eU = (26.0f * eps) * mX * mY, eV = eU, eW = eU;
     bool neg = U < -eU || V < -eV || W < -eW;
     bool pos = U > eU || V > eV || W > eW;
     if (neg && pos) return 0;
     bool certain = (U > eU && V > eV && W > eW) || (U < -eU && V < -eV && W < -eW);
     if (!certain) {
-        const float eX = (4.0f * eps) * mX, eY = (4.0f * eps) * mY;
-        const float tail = (32.0f * eps * eps + 0x1p-44f) * mX * mY;
+        const float eX = (5.0f * eps) * mX, eY = (5.0f * eps) * mY;
+        const float tail = (50.0f * eps * eps + 0x1p-44f) * mX * mY;
         const float aAx = fabsf(Ax), aAy = fabsf(Ay), aBx = fabsf(Bx), aBy = fabsf(By), aCx = fabsf(Cx), aCy = fabsf(Cy);
         eU = 1.125f * (eX * (aBy + aCy) + eY * (aBx + aCx) + eps * (fabsf(U) + fabsf(CyBx)) + tail);
         eV = 1.125f * (eX * (aCy + aAy) + eY * (aCx + aAx) + eps * (fabsf(V) + fabsf(AyCx)) + tail);
@@ -146,8 +169,7 @@ __device__ __forceinline__ int tri_test32(const RayT& r, float3 v0, float3 v1, f
         if (!certain) return 2;
     }
     const float det = U + V + W;
-    const float T = fmaf(W, r.Sz * C2, fmaf(V, r.Sz * B2, U * (r.Sz * A2)));
-    const float mZ = fabsf(r.Sz) * mz2;
+    const float T = fmaf(W, Cz, fmaf(V, Bz, U * Az));
     const float maxE = fmaxf(fabsf(U), fmaxf(fabsf(V), fabsf(W)));
     const float eSum = eU + eV + eW;
     const float dT = eSum * mZ + (18.0f * eps) * maxE * mZ;
@@ -164,7 +186,8 @@ __device__ __forceinline__ int tri_test32(const RayT& r, float3 v0, float3 v1, f
 // fp64 watertight test in the oracle's operation order; true and t if hit with t > 0
 __device__ __forceinline__ bool tri_test64(RayT& r, float3 v0, float3 v1, float3 v2, double& t_out) {
     const Shear64 sh = shear64(r);
-    const double ox = r.ok[0], oy = r.ok[1], oz = r.ok[2];
+    const float3 o32 = make_float3(r.o[0], r.o[1], r.o[2]);
+    const double ox = self3(o32, r.kx), oy = self3(o32, r.ky), oz = self3(o32, r.kz);
     const double A0 = __dsub_rn((double)self3(v0, r.kx), ox);
     const double A1 = __dsub_rn((double)self3(v0, r.ky), oy);
     const double A2 = __dsub_rn((double)self3(v0, r.kz), oz);
