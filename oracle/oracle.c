@@ -645,55 +645,68 @@ EXPORT void orc_fr_dims(int32_t H, int32_t L, int32_t* fin, int32_t* fout) {
     }
 }
 
-EXPORT void orc_fr_eval_hl(int32_t H, int32_t L, const uint16_t* blob, const double* uv, int64_t n, double* y_out) {
-    const double PI = 3.14159265358979323846;
-    int32_t fin[64], fout[64];
-    orc_fr_dims(H, L, fin, fout);
-    const int c = orc_fr_concat_layer(L);
+typedef struct {
+    int H, L, c;
+    int32_t fin[17], fout[17];
     double B[40];
-    double** W = (double**)malloc(sizeof(double*) * (L + 1));
-    double** b = (double**)malloc(sizeof(double*) * (L + 1));
+    double* W[17];
+    double* b[17];
+} fr_net;
+
+static void fr_unpack(int32_t H, int32_t L, const uint16_t* blob, fr_net* n) {
+    n->H = H; n->L = L; n->c = orc_fr_concat_layer(L);
+    orc_fr_dims(H, L, n->fin, n->fout);
     int64_t off = 0;
-    for (int i = 0; i < 40; ++i) B[i] = half_to_double(blob[off++]);
+    for (int i = 0; i < 40; ++i) n->B[i] = half_to_double(blob[off++]);
     for (int l = 0; l <= L; ++l) {
-        W[l] = (double*)malloc(sizeof(double) * fin[l] * fout[l]);
-        b[l] = (double*)malloc(sizeof(double) * fout[l]);
-        for (int64_t i = 0; i < (int64_t)fin[l] * fout[l]; ++i) W[l][i] = half_to_double(blob[off++]);
-        for (int i = 0; i < fout[l]; ++i) b[l][i] = half_to_double(blob[off++]);
+        n->W[l] = (double*)malloc(sizeof(double) * n->fin[l] * n->fout[l]);
+        n->b[l] = (double*)malloc(sizeof(double) * n->fout[l]);
+        for (int64_t i = 0; i < (int64_t)n->fin[l] * n->fout[l]; ++i) n->W[l][i] = half_to_double(blob[off++]);
+        for (int i = 0; i < n->fout[l]; ++i) n->b[l][i] = half_to_double(blob[off++]);
     }
-    double* a = (double*)malloc(sizeof(double) * (H > 40 ? H : 40));
-    double* h = (double*)malloc(sizeof(double) * (H > 40 ? H : 40));
-    for (int64_t q = 0; q < n; ++q) {
-        double g[40];
-        for (int j = 0; j < 20; ++j) {
-            const double p = 2.0 * PI * (B[2 * j] * uv[2 * q] + B[2 * j + 1] * uv[2 * q + 1]);
-            g[j] = sin(p);
-            g[20 + j] = cos(p);
-        }
-        memcpy(a, g, sizeof(double) * 40);
-        for (int l = 0; l < L; ++l) {
-            for (int o = 0; o < fout[l]; ++o) {
-                double s = 0.0;
-                for (int i = 0; i < fin[l]; ++i) s += W[l][(int64_t)o * fin[l] + i] * a[i];
-                s += b[l][o];
-                h[o] = s > 0.0 ? s : 0.0;
-            }
-            memcpy(a, h, sizeof(double) * fout[l]);
-            if (l == c) memcpy(a + (H - 40), g, sizeof(double) * 40);   /* concat skip: [h_c, gamma] */
-        }
-        double yuv[3];
-        for (int o = 0; o < 3; ++o) {
+}
+
+static void fr_net_free(fr_net* n) {
+    for (int l = 0; l <= n->L; ++l) { free(n->W[l]); free(n->b[l]); }
+}
+
+/* RGB log radiance of (u, v), the steps in the order of the comment above */
+static void fr_net_eval(const fr_net* n, double u, double v, double y[3]) {
+    const double PI = 3.14159265358979323846;
+    const int H = n->H, L = n->L;
+    double g[40], a[1024], h[1024];
+    for (int j = 0; j < 20; ++j) {
+        const double p = 2.0 * PI * (n->B[2 * j] * u + n->B[2 * j + 1] * v);
+        g[j] = sin(p);
+        g[20 + j] = cos(p);
+    }
+    memcpy(a, g, sizeof(double) * 40);
+    for (int l = 0; l < L; ++l) {
+        for (int o = 0; o < n->fout[l]; ++o) {
             double s = 0.0;
-            for (int i = 0; i < H; ++i) s += W[L][(int64_t)o * H + i] * a[i];
-            yuv[o] = s + b[L][o];
+            for (int i = 0; i < n->fin[l]; ++i) s += n->W[l][(int64_t)o * n->fin[l] + i] * a[i];
+            s += n->b[l][o];
+            h[o] = s > 0.0 ? s : 0.0;
         }
-        double* y = y_out + 3 * q;
-        y[0] = yuv[0] + 1.13983 * yuv[2];
-        y[1] = yuv[0] - 0.39465 * yuv[1] - 0.58060 * yuv[2];
-        y[2] = yuv[0] + 2.03211 * yuv[1];
+        memcpy(a, h, sizeof(double) * n->fout[l]);
+        if (l == n->c) memcpy(a + (H - 40), g, sizeof(double) * 40);   /* concat skip: [h_c, gamma] */
     }
-    for (int l = 0; l <= L; ++l) { free(W[l]); free(b[l]); }
-    free(W); free(b); free(a); free(h);
+    double yuv[3];
+    for (int o = 0; o < 3; ++o) {
+        double s = 0.0;
+        for (int i = 0; i < H; ++i) s += n->W[L][(int64_t)o * H + i] * a[i];
+        yuv[o] = s + n->b[L][o];
+    }
+    y[0] = yuv[0] + 1.13983 * yuv[2];
+    y[1] = yuv[0] - 0.39465 * yuv[1] - 0.58060 * yuv[2];
+    y[2] = yuv[0] + 2.03211 * yuv[1];
+}
+
+EXPORT void orc_fr_eval_hl(int32_t H, int32_t L, const uint16_t* blob, const double* uv, int64_t n, double* y_out) {
+    fr_net net;
+    fr_unpack(H, L, blob, &net);
+    for (int64_t q = 0; q < n; ++q) fr_net_eval(&net, uv[2 * q], uv[2 * q + 1], y_out + 3 * q);
+    fr_net_free(&net);
 }
 
 /* ---------------------------------------------------------------------------------------------- */
@@ -770,7 +783,8 @@ EXPORT void orc_scatter(int kind, const double* d, const double* ng, double ior,
 /* ---------------------------------------------------------------------------------------------- */
 typedef struct {
     const orc_scene* sc;
-    const nif64* nif;        /* NULL -> constant env */
+    const nif64* nif;        /* SIREN HDR-NIF, or NULL */
+    const fr_net* fr;        /* the paper's NIF family, or NULL; both NULL -> constant env */
     double env[3];
     int32_t W, H, max_depth;
     uint64_t seed;
@@ -822,10 +836,11 @@ static void trace_path(const render_ctx* c, int64_t p, int32_t s, double L[3], p
         if (trace_prims && depth <= MAX_TRACE) { trace_prims[depth - 1] = h.prim; *trace_len = depth; }
         if (h.prim < 0) {                                   /* escaped: environment light */
             double env[3];
-            if (c->nif) {
+            if (c->nif || c->fr) {
                 double u, v, y[3];
                 equirect(d, &u, &v);
-                nif_eval(c->nif, u, v, y);
+                if (c->nif) nif_eval(c->nif, u, v, y);
+                else fr_net_eval(c->fr, u, v, y);
                 for (int k = 0; k < 3; ++k) env[k] = exp(y[k]);
             } else {
                 for (int k = 0; k < 3; ++k) env[k] = c->env[k];
@@ -912,16 +927,9 @@ static void* worker(void* vp) {
 
 /* Sum over samples [s0, s1) of the radiance of each listed pixel (out[3*i..] = sum, not mean).
    stats[0..4] = segments, escaped, emitted, capped, rr_killed. */
-EXPORT int orc_render(const orc_scene* sc, const uint16_t* nif_blob, const double* env_rgb, int32_t W, int32_t H,
-                      int32_t max_depth, uint64_t seed, const int64_t* pix, int64_t n_pix, int32_t s0, int32_t s1,
-                      int32_t nthreads, double* out, int64_t* stats) {
-    render_ctx c;
-    c.sc = sc; c.W = W; c.H = H; c.max_depth = max_depth; c.seed = seed;
-    cam_setup(&sc->cam, W, H, &c.cam);
-    nif64 net;
-    if (nif_blob) { nif_unpack(nif_blob, &net); c.nif = &net; }
-    else c.nif = NULL;
-    for (int k = 0; k < 3; ++k) c.env[k] = env_rgb ? env_rgb[k] : 1.0;
+static void render_pixels(render_ctx* cp, const int64_t* pix, int64_t n_pix, int32_t s0, int32_t s1,
+                          int32_t nthreads, double* out, int64_t* stats) {
+    render_ctx c = *cp;
     if (nthreads < 1) nthreads = 1;
     pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * nthreads);
     worker_arg* args = (worker_arg*)malloc(sizeof(worker_arg) * nthreads);
@@ -937,7 +945,39 @@ EXPORT int orc_render(const orc_scene* sc, const uint16_t* nif_blob, const doubl
     }
     if (stats) { stats[0] = tot.segments; stats[1] = tot.escaped; stats[2] = tot.emitted; stats[3] = tot.capped; stats[4] = tot.rr_killed; }
     free(th); free(args);
+}
+
+EXPORT int orc_render(const orc_scene* sc, const uint16_t* nif_blob, const double* env_rgb, int32_t W, int32_t H,
+                      int32_t max_depth, uint64_t seed, const int64_t* pix, int64_t n_pix, int32_t s0, int32_t s1,
+                      int32_t nthreads, double* out, int64_t* stats) {
+    render_ctx c;
+    c.sc = sc; c.W = W; c.H = H; c.max_depth = max_depth; c.seed = seed;
+    cam_setup(&sc->cam, W, H, &c.cam);
+    nif64 net;
+    if (nif_blob) { nif_unpack(nif_blob, &net); c.nif = &net; }
+    else c.nif = NULL;
+    c.fr = NULL;
+    for (int k = 0; k < 3; ++k) c.env[k] = env_rgb ? env_rgb[k] : 1.0;
+    render_pixels(&c, pix, n_pix, s0, s1, nthreads, out, stats);
     if (nif_blob) nif_free(&net);
+    return 0;
+}
+
+/* As orc_render, with the environment given by the paper's NIF family (fr_H, fr_L; (128, 4) is the
+   PT_NIF_FOURIER_RELU network). */
+EXPORT int orc_render_fr(const orc_scene* sc, int32_t fr_H, int32_t fr_L, const uint16_t* fr_blob, int32_t W,
+                         int32_t H, int32_t max_depth, uint64_t seed, const int64_t* pix, int64_t n_pix, int32_t s0,
+                         int32_t s1, int32_t nthreads, double* out, int64_t* stats) {
+    render_ctx c;
+    c.sc = sc; c.W = W; c.H = H; c.max_depth = max_depth; c.seed = seed;
+    cam_setup(&sc->cam, W, H, &c.cam);
+    fr_net net;
+    fr_unpack(fr_H, fr_L, fr_blob, &net);
+    c.nif = NULL;
+    c.fr = &net;
+    for (int k = 0; k < 3; ++k) c.env[k] = 1.0;
+    render_pixels(&c, pix, n_pix, s0, s1, nthreads, out, stats);
+    fr_net_free(&net);
     return 0;
 }
 
@@ -949,6 +989,7 @@ EXPORT int32_t orc_trace_one(const orc_scene* sc, const uint16_t* nif_blob, cons
     cam_setup(&sc->cam, W, H, &c.cam);
     nif64 net;
     if (nif_blob) { nif_unpack(nif_blob, &net); c.nif = &net; } else c.nif = NULL;
+    c.fr = NULL;
     for (int k = 0; k < 3; ++k) c.env[k] = env_rgb ? env_rgb[k] : 1.0;
     path_stats st = {0, 0, 0, 0, 0};
     int32_t len = 0;

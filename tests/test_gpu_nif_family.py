@@ -108,3 +108,26 @@ def test_render_with_family_nif(ptm):
         b = ptm.render(S, nif, 96, 64, 2, c.max_depth, seed=3)
         assert np.isfinite(a).all() and (a >= 0).all() and a.max() > 0
         assert np.array_equal(a, b)
+
+
+REL_RMSE_GATE = 2e-3
+
+
+@pytest.mark.parametrize("kind,H,L", [(1, 128, 4), (2, 64, 2), (2, 256, 4)])
+def test_render_paper_nif_vs_oracle(ptm, orc, kind, H, L):
+    """Frames lit by the paper's NIF (fused kind 1, layered family members) against the oracle's path
+    tracer with the same fp64 NIF (oracle render_fr): config 0's box at full size and the Spheres scene
+    (the paper's sweep scene) on sampled rows; rel-RMSE gate as for the SIREN frames."""
+    blob = scenes.fourier_relu_blob(0) if kind == 1 else scenes.fourier_relu_family_blob(H, L, seed=1)
+    nif = ptm.Nif(blob, kind=kind, hidden=H, layers=L)
+    for cfg, W, Hh, spp, rows in ((0, 64, 64, 4, None), (2, 128, 96, 4, slice(0, 96, 6))):
+        c = scenes.CONFIGS[cfg]
+        src = scenes.scene_for_config(cfg)
+        img = ptm.render(ptm.Scene(src), nif, W, Hh, spp, c.max_depth, seed=2)
+        ys = np.arange(Hh)[rows] if rows is not None else np.arange(Hh)
+        pix = (ys[:, None] * W + np.arange(W)[None, :]).reshape(-1)
+        ref, _ = orc.OracleScene(src).render_fr(H, L, blob, W, Hh, c.max_depth, 2, pix=pix, s0=0, s1=spp)
+        got = img.reshape(-1, 3)[pix].astype(np.float64)
+        ref = ref / spp
+        rel = float(np.sqrt(((got - ref) ** 2).sum() / (ref ** 2).sum()))
+        assert rel <= REL_RMSE_GATE, (cfg, rel)

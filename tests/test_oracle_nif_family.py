@@ -96,3 +96,20 @@ def test_family_blob_generator_is_seeded():
     assert np.array_equal(a, b) and not np.array_equal(a, c)
     h = a.view(np.float16).astype(np.float64)
     assert np.isfinite(h).all()
+
+
+@pytest.mark.parametrize("H,L", [(64, 2), (128, 4)])
+def test_render_fr_empty_scene_is_the_nif_of_the_camera_rays(orc, H, L):
+    """Empty scene: every sample escapes at its camera ray, so the render is exactly exp of the NIF at
+    equirect(d) for the oracle's fp32 camera ray d (one NIF evaluation per sample, no other term)."""
+    blob = scenes.fourier_relu_family_blob(H, L, seed=4)
+    sc = orc.OracleScene(scenes.empty_scene())
+    W, Hh, seed = 12, 8, 5
+    pix = np.arange(W * Hh)
+    out, st = sc.render_fr(H, L, blob, W, Hh, 4, seed, pix=pix, s0=0, s1=2)
+    want = np.zeros((W * Hh, 3))
+    for s in range(2):
+        d = orc.camera_rays(sc.scene.camera, W, Hh, seed, s, pix).astype(np.float64)
+        want += np.exp(orc.fr_eval_hl(H, L, blob, orc.equirect(d)))
+    assert st["escaped"] == W * Hh * 2
+    assert np.abs(out - want).max() <= 1e-12 * np.abs(want).max()
