@@ -35,11 +35,25 @@ __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t phase) {
         : "memory");
     return ok != 0;
 }
+// try_wait with a suspend-time hint: the waiting warp is parked by the hardware until the phase
+// completes (or ~1 ms passes) instead of spinning, so waiting warps (the MMA issuer, producers, idle
+// epilogue warps) do not steal issue slots from the epilogue warps sharing their SM sub-partition
+__device__ __forceinline__ bool mbar_try_sleep(uint32_t bar, uint32_t phase) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(phase), "r"(1000000u)
+        : "memory");
+    return ok != 0;
+}
 // bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
     if (mbar_try(bar, phase)) return;
     const long long t0 = clock64();
-    while (!mbar_try(bar, phase)) {
+    while (!mbar_try_sleep(bar, phase)) {
         if (clock64() - t0 > 4000000000ll) __trap();
     }
 }
