@@ -73,6 +73,12 @@ struct RayT {
 
 __device__ __forceinline__ float self3(float3 v, int k) { return k == 0 ? v.x : (k == 1 ? v.y : v.z); }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ void ray_prepare(float3 o, float3 d, RayT& r) {
     int kz = 0;
     if (fabsf(d.y) > fabsf(d.x)) kz = 1;
@@ -97,7 +103,8 @@ __device__ __forceinline__ void ray_prepare(float3 o, float3 d, RayT& r) {
     r.adkz = fabsf(dkz);
     r.o[0] = o.x; r.o[1] = o.y; r.o[2] = o.z;
     r.d[0] = d.x; r.d[1] = d.y; r.d[2] = d.z;
-    r.inv[0] = __frcp_rn(d.x); r.inv[1] = __frcp_rn(d.y); r.inv[2] = __frcp_rn(d.z);
+    // slab reciprocals: the SFU approximation (<= 1 ulp); the slab bound below allows for its rounding
+    r.inv[0] = rcp_approx(d.x); r.inv[1] = rcp_approx(d.y); r.inv[2] = rcp_approx(d.z);
     r.negmask = (signbit(d.x) ? 1u : 0u) | (signbit(d.y) ? 2u : 0u) | (signbit(d.z) ? 4u : 0u);
 }
 
@@ -389,7 +396,9 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
     if (tp.empty) return best;
     RayT r;
     ray_prepare(o, d, r);
-    constexpr float kGrow = 1.0f + 2.0f * (3.0f * 0x1p-24f) / (1.0f - 3.0f * 0x1p-24f);   // 1 + 2 gamma_3
+    // PBRT-v3's robust t_far * (1 + 2 gamma_3), with gamma_5: the approximate reciprocal adds up to
+    // two more roundings' worth of relative error to each slab distance
+    constexpr float kGrow = 1.0f + 2.0f * (5.0f * 0x1p-24f) / (1.0f - 5.0f * 0x1p-24f);   // 1 + 2 gamma_5
     // per-axis fp16x2 half swap so that t.x is always the near slab plane and t.y the far one
     uint32_t swz[3];
 #pragma unroll
