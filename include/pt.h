@@ -104,6 +104,17 @@ PT_API int pt_nif_load_ex(int32_t kind, const uint16_t* fp16_blob, int64_t n_hal
    Errors: INVALID_ARG (hidden/layers out of range), FORMAT (n_halves), DOMAIN (non-finite), CUDA, OOM. */
 PT_API int pt_nif_load_family(int32_t hidden, int32_t layers, const uint16_t* fp16_blob, int64_t n_halves,
                               pt_nif** out);
+
+/* As pt_nif_load_family with a storage/compute precision: PT_NIF_FP16 (as above) or PT_NIF_FP8 (SURVEY
+   8f #4; "float8 ... would halve the memory required for weights and increase performance"):
+   weights are rounded once from the fp16 blob to OCP e4m3 (round to nearest even, saturating at 448),
+   the Fourier features and every hidden activation are rounded to e4m3 before the next layer, products
+   accumulate in fp32 (tcgen05 kind::f8f6f4), biases and the output stay fp32.
+   Errors: as pt_nif_load_family; INVALID_ARG for an unknown precision. */
+#define PT_NIF_FP16 0
+#define PT_NIF_FP8 1
+PT_API int pt_nif_load_family_ex(int32_t hidden, int32_t layers, int32_t precision, const uint16_t* fp16_blob,
+                                 int64_t n_halves, pt_nif** out);
 PT_API int pt_nif_destroy(pt_nif* nif);
 
 /* Render a full frame. env: nif != NULL -> HDR-NIF environment; nif == NULL -> constant env_rgb

@@ -66,6 +66,9 @@ def lib():
             L.orc_nif_eval.argtypes = [P, P, I64, P]
             L.orc_fr_eval.argtypes = [P, P, I64, P]
             L.orc_fr_eval_hl.argtypes = [I32, I32, P, P, I64, P]
+            L.orc_fr_eval_hl_fp8.argtypes = [I32, I32, P, P, I64, P]
+            L.orc_e4m3_round.restype = D
+            L.orc_e4m3_round.argtypes = [D]
             L.orc_render_fr.restype = C.c_int
             L.orc_render_fr.argtypes = [P, I32, I32, P, I32, I32, I32, U64, P, I64, I32, I32, I32, P, P]
             L.orc_fr_concat_layer.restype = C.c_int
@@ -226,6 +229,19 @@ def fr_eval_hl(hidden, layers, blob, uv):
     y = np.empty((uv.shape[0], 3), np.float64)
     lib().orc_fr_eval_hl(int(hidden), int(layers), _p(blob), _p(uv), uv.shape[0], _p(y))
     return y
+
+
+def fr_eval_hl_fp8(hidden, layers, blob, uv):
+    """The fp8 (e4m3) variant of the family (weights, features and hidden activations rounded to e4m3)."""
+    blob = np.ascontiguousarray(blob, dtype=np.uint16)
+    uv = np.ascontiguousarray(uv, dtype=np.float64).reshape(-1, 2)
+    y = np.empty((uv.shape[0], 3), np.float64)
+    lib().orc_fr_eval_hl_fp8(int(hidden), int(layers), _p(blob), _p(uv), uv.shape[0], _p(y))
+    return y
+
+
+def e4m3_round(x):
+    return float(lib().orc_e4m3_round(float(x)))
 
 
 def fr_concat_layer(layers):

@@ -702,6 +702,70 @@ static void fr_net_eval(const fr_net* n, double u, double v, double y[3]) {
     y[2] = yuv[0] + 2.03211 * yuv[1];
 }
 
+/* OCP e4m3 (1 sign, 4 exponent bits with bias 7, 3 mantissa bits, no infinities, largest finite 448):
+   round to nearest, ties to the even code, saturating -- written as a search over the decoded table of
+   the 127 non-negative finite codes, independent of the CUDA path's arithmetic conversion. */
+static double e4m3_value(int code) {          /* 0 <= code <= 0x7E */
+    const int e = code >> 3, m = code & 7;
+    return e == 0 ? ldexp((double)m, -9) : ldexp((double)(8 + m), e - 10);
+}
+static double e4m3_round(double x) {
+    double a = fabs(x);
+    if (a >= 448.0) a = 448.0;
+    int lo = 0, hi = 0x7E;                     /* largest code with value <= a */
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) / 2;
+        if (e4m3_value(mid) <= a) lo = mid; else hi = mid - 1;
+    }
+    double r = e4m3_value(lo);
+    if (lo < 0x7E && r < a) {
+        const double up = e4m3_value(lo + 1);
+        if (up - a < a - r || (up - a == a - r && ((lo + 1) & 1) == 0)) r = up;
+    }
+    return x < 0 ? -r : r;
+}
+EXPORT double orc_e4m3_round(double x) { return e4m3_round(x); }
+
+/* The fp8 variant (PT_NIF_FP8): weights rounded to e4m3 once, the features and every hidden activation
+   rounded to e4m3 before they feed the next layer; biases, sums and the output in fp64. */
+EXPORT void orc_fr_eval_hl_fp8(int32_t H, int32_t L, const uint16_t* blob, const double* uv, int64_t n, double* y_out) {
+    const double PI = 3.14159265358979323846;
+    fr_net net;
+    fr_unpack(H, L, blob, &net);
+    for (int l = 0; l <= L; ++l)
+        for (int64_t i = 0; i < (int64_t)net.fin[l] * net.fout[l]; ++i) net.W[l][i] = e4m3_round(net.W[l][i]);
+    double g[40], a[1024], h[1024];
+    for (int64_t q = 0; q < n; ++q) {
+        for (int j = 0; j < 20; ++j) {
+            const double p = 2.0 * PI * (net.B[2 * j] * uv[2 * q] + net.B[2 * j + 1] * uv[2 * q + 1]);
+            g[j] = e4m3_round(sin(p));
+            g[20 + j] = e4m3_round(cos(p));
+        }
+        memcpy(a, g, sizeof(double) * 40);
+        for (int l = 0; l < L; ++l) {
+            for (int o = 0; o < net.fout[l]; ++o) {
+                double s = 0.0;
+                for (int i = 0; i < net.fin[l]; ++i) s += net.W[l][(int64_t)o * net.fin[l] + i] * a[i];
+                s += net.b[l][o];
+                h[o] = e4m3_round(s > 0.0 ? s : 0.0);
+            }
+            memcpy(a, h, sizeof(double) * net.fout[l]);
+            if (l == net.c) memcpy(a + (H - 40), g, sizeof(double) * 40);
+        }
+        double yuv[3];
+        for (int o = 0; o < 3; ++o) {
+            double s = 0.0;
+            for (int i = 0; i < H; ++i) s += net.W[L][(int64_t)o * H + i] * a[i];
+            yuv[o] = s + net.b[L][o];
+        }
+        double* y = y_out + 3 * q;
+        y[0] = yuv[0] + 1.13983 * yuv[2];
+        y[1] = yuv[0] - 0.39465 * yuv[1] - 0.58060 * yuv[2];
+        y[2] = yuv[0] + 2.03211 * yuv[1];
+    }
+    fr_net_free(&net);
+}
+
 EXPORT void orc_fr_eval_hl(int32_t H, int32_t L, const uint16_t* blob, const double* uv, int64_t n, double* y_out) {
     fr_net net;
     fr_unpack(H, L, blob, &net);

@@ -22,8 +22,12 @@
 //   warps 2-5 epilogue (one TMEM lane quarter each): bias + ReLU + fp16 pack, 16-byte stores into the
 //     next layer's blocked A layout; the output layer instead applies YUV -> RGB, exp and beta and
 //     writes the path's wave slot.
-// Blocked layout (A and B alike, SWIZZLE_NONE K-major core matrices): a (R rows x 64 K) chunk is one
-// contiguous block, core matrix (rows 8nb..8nb+7, k 8kb..8kb+7) at ((kb * R/8) + nb) * 128 B.
+// Blocked layout (A and B alike, SWIZZLE_NONE K-major core matrices): a (R rows x 128 bytes of K) chunk
+// is one contiguous block, core matrix (rows 8nb..8nb+7, K bytes 16kb..16kb+15) at ((kb * R/8) + nb) * 128.
+// fp16 networks hold 64 K elements per chunk; the fp8 variant ("float8 ... would halve the
+// memory ... and increase performance") stores weights and activations as e4m3, 128 K
+// elements per chunk, and runs tcgen05.mma kind::f8f6f4 (K = 32 per instruction, the same bytes and
+// cycles as an fp16 K = 16 step, i.e. twice the FLOP rate).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -41,8 +45,8 @@ namespace pt {
 namespace mlp {
 
 constexpr int kBM = 128;
-constexpr int kBK = 64;
-constexpr int kAChunk = kBM * kBK * 2;          // 16 KB
+constexpr int kChunkBytesK = 128;               // bytes of K per chunk row (64 fp16 or 128 fp8 elements)
+constexpr int kAChunk = kBM * kChunkBytesK;     // 16 KB
 constexpr int kThreads = 192;
 constexpr int kSmemBudget = 220 * 1024;
 constexpr int kMaxStages = 8;
@@ -68,12 +72,25 @@ struct LayerArgs {
     float* out_rgb;
 };
 
-// 16 B of 8 consecutive fp16 columns of one row into a blocked activation buffer
+// address of element column `col` (a multiple of 8) of one row in a blocked activation buffer
+__device__ __forceinline__ uint8_t* act_ptr(uint8_t* buf, int out_KC, int tile, int row_in_tile, int col, int esize) {
+    const int bc = col * esize;
+    const int kc = bc >> 7, kb = (bc & 127) >> 4;
+    return buf + ((size_t)tile * out_KC + kc) * kAChunk + ((kb * 16 + (row_in_tile >> 3)) * 128) + (row_in_tile & 7) * 16 +
+           (bc & 15);
+}
+// 8 consecutive columns: 16 B of fp16 or 8 B of e4m3
 __device__ __forceinline__ void store_act8(uint8_t* buf, int out_KC, int tile, int row_in_tile, int col, uint4 v) {
-    const int kc = col >> 6, kb = (col & 63) >> 3;
-    uint8_t* p = buf + ((size_t)tile * out_KC + kc) * kAChunk + ((kb * 16 + (row_in_tile >> 3)) * 128) +
-                 (row_in_tile & 7) * 16;
-    *reinterpret_cast<uint4*>(p) = v;
+    *reinterpret_cast<uint4*>(act_ptr(buf, out_KC, tile, row_in_tile, col, 2)) = v;
+}
+__device__ __forceinline__ void store_act8_f8(uint8_t* buf, int out_KC, int tile, int row_in_tile, int col, uint2 v) {
+    *reinterpret_cast<uint2*>(act_ptr(buf, out_KC, tile, row_in_tile, col, 1)) = v;
+}
+// two floats -> e4m3x2 (RN, saturating), `lo` in the low byte (the lower column)
+__device__ __forceinline__ uint32_t e4m3x2(float lo, float hi) {
+    uint16_t r;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+    return r;
 }
 
 }  // namespace mlp
@@ -83,7 +100,7 @@ __device__ __forceinline__ void store_act8(uint8_t* buf, int out_KC, int tile, i
 // the layer after the concat layer. Rows past the count get the features of (u, v) = (0.5, 0.5).
 __global__ void mlp_features_kernel(const float4* __restrict__ esc, const uint32_t* __restrict__ count, int row0,
                                     int rows_cap, int dir_input, const float* __restrict__ freq, uint8_t* out,
-                                    int out_KC, int col0, int zero_pad) {
+                                    int out_KC, int col0, int zero_pad, int fp8) {
     const uint32_t n = *count;
     const int M = (int)min((int64_t)rows_cap, max((int64_t)0, (int64_t)n - row0));
     const int rows = ((M + mlp::kBM - 1) / mlp::kBM) * mlp::kBM;
@@ -95,38 +112,47 @@ __global__ void mlp_features_kernel(const float4* __restrict__ esc, const uint32
             v = en.y;
             if (dir_input) equirect_f32(make_float3(en.x, en.y, en.z), u, v);
         }
-        __half f[40];
+        float f[40];
 #pragma unroll
         for (int j = 0; j < 20; ++j) {
             const float p = fmaf(__ldg(freq + 2 * j), u, __ldg(freq + 2 * j + 1) * v);
             const float q = p - rintf(p);                 // exact-range turns in [-1/2, 1/2]
-            float sn, cs;
-            __sincosf(6.28318530717958647692f * q, &sn, &cs);
-            f[j] = __float2half_rn(sn);
-            f[20 + j] = __float2half_rn(cs);
+            __sincosf(6.28318530717958647692f * q, &f[j], &f[20 + j]);
         }
         const int tile = r / mlp::kBM, rt = r % mlp::kBM;
+        if (!fp8) {
 #pragma unroll
-        for (int g = 0; g < 5; ++g) {
-            uint4 w;
-            uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+            for (int g = 0; g < 5; ++g) {
+                uint4 w;
+                uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-                wp[i] = (uint32_t)__half_as_ushort(f[8 * g + 2 * i]) | ((uint32_t)__half_as_ushort(f[8 * g + 2 * i + 1]) << 16);
-            mlp::store_act8(out, out_KC, tile, rt, col0 + 8 * g, w);
-        }
-        if (zero_pad) {
+                for (int i = 0; i < 4; ++i) wp[i] = pack_half2(f[8 * g + 2 * i], f[8 * g + 2 * i + 1]);
+                mlp::store_act8(out, out_KC, tile, rt, col0 + 8 * g, w);
+            }
+            if (zero_pad) {
 #pragma unroll
-            for (int g = 5; g < 8; ++g) mlp::store_act8(out, out_KC, tile, rt, col0 + 8 * g, make_uint4(0, 0, 0, 0));
+                for (int g = 5; g < 8; ++g) mlp::store_act8(out, out_KC, tile, rt, col0 + 8 * g, make_uint4(0, 0, 0, 0));
+            }
+        } else {
+#pragma unroll
+            for (int g = 0; g < 5; ++g) {
+                const uint32_t lo = mlp::e4m3x2(f[8 * g], f[8 * g + 1]) | (mlp::e4m3x2(f[8 * g + 2], f[8 * g + 3]) << 16);
+                const uint32_t hi = mlp::e4m3x2(f[8 * g + 4], f[8 * g + 5]) | (mlp::e4m3x2(f[8 * g + 6], f[8 * g + 7]) << 16);
+                mlp::store_act8_f8(out, out_KC, tile, rt, col0 + 8 * g, make_uint2(lo, hi));
+            }
+            if (zero_pad) {
+#pragma unroll
+                for (int g = 5; g < 16; ++g) mlp::store_act8_f8(out, out_KC, tile, rt, col0 + 8 * g, make_uint2(0, 0));
+            }
         }
     }
 }
 
-template <int BN, int kEpi>
+template <int BN, int kEpi, bool kFp8>
 __global__ void __launch_bounds__(mlp::kThreads, 1) mlp_layer_kernel(mlp::LayerArgs a) {
     using namespace mlp;
     extern __shared__ __align__(1024) uint8_t smem[];
-    constexpr int kBChunk = BN * kBK * 2;
+    constexpr int kBChunk = BN * kChunkBytesK;
     constexpr uint32_t kTmemCols = (2 * BN) < 32 ? 32u : (uint32_t)(2 * BN);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 21 * 8);
@@ -230,7 +256,8 @@ __global__ void __launch_bounds__(mlp::kThreads, 1) mlp_layer_kernel(mlp::LayerA
                     for (int k = 0; k < 4; ++k) {
                         const uint64_t ad = smem_desc(smem_u32(sa) + k * 2 * 2048, 2048, 128);
                         const uint64_t bd = smem_desc(smem_u32(sb) + k * 2 * (BN / 8) * 128, (BN / 8) * 128, 128);
-                        mma_ss(dt, ad, bd, idesc(BN), (kc | k) != 0);
+                        if (kFp8) mma_ss_f8(dt, ad, bd, idesc(BN), (kc | k) != 0);
+                        else mma_ss(dt, ad, bd, idesc(BN), (kc | k) != 0);
                     }
                     mma_commit(bar(8 + stage));                  // stage free once these MMAs are done
                 }
@@ -273,15 +300,23 @@ __global__ void __launch_bounds__(mlp::kThreads, 1) mlp_layer_kernel(mlp::LayerA
                         if (col + 8 * g >= a.N_valid) break;
                         const float4 b0 = __ldg(bp + 2 * g), b1 = __ldg(bp + 2 * g + 1);
                         const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-                        uint4 w;
-                        uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+                        float h[8];
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            const float lo = __uint_as_float(v[8 * g + 2 * i]) + bb[2 * i];
-                            const float hi = __uint_as_float(v[8 * g + 2 * i + 1]) + bb[2 * i + 1];
-                            asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(wp[i]) : "f"(hi), "f"(lo));
+                        for (int i = 0; i < 8; ++i) h[i] = __uint_as_float(v[8 * g + i]) + bb[i];
+                        if (!kFp8) {
+                            uint4 w;
+                            uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+                            for (int i = 0; i < 4; ++i)
+                                asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(wp[i]) : "f"(h[2 * i + 1]), "f"(h[2 * i]));
+                            store_act8(a.out_act, a.out_KC, mt, rt, col + 8 * g, w);
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) h[i] = fmaxf(h[i], 0.0f);
+                            const uint32_t lo = e4m3x2(h[0], h[1]) | (e4m3x2(h[2], h[3]) << 16);
+                            const uint32_t hi = e4m3x2(h[4], h[5]) | (e4m3x2(h[6], h[7]) << 16);
+                            store_act8_f8(a.out_act, a.out_KC, mt, rt, col + 8 * g, make_uint2(lo, hi));
                         }
-                        store_act8(a.out_act, a.out_KC, mt, rt, col + 8 * g, w);
                     }
                 }
             } else {
@@ -329,6 +364,25 @@ float half_to_float(uint16_t h) {
     return (h & 0x8000) ? -v : v;
 }
 
+// fp32 -> OCP e4m3 (1-4-3, bias 7, no infinities, max 448), round to nearest even, saturating: the
+// conversion cvt.rn.satfinite.e4m3x2.f32 does on the device
+uint8_t float_to_e4m3(float x) {
+    const uint8_t sign = std::signbit(x) ? 0x80 : 0;
+    double a = std::fabs((double)x);
+    if (!(a > 0.0)) return sign;
+    if (a >= 448.0) return sign | 0x7E;                   // 448 = 1.75 * 2^8
+    int e;
+    std::frexp(a, &e);                                     // a = f * 2^e, f in [0.5, 1)
+    int ex = std::max(e - 1, -6);                          // subnormals share the exponent of 2^-6
+    const double q = std::ldexp(1.0, ex - 3);              // quantum
+    double m = a / q;                                      // in [0, 16)
+    double r = std::nearbyint(m);                          // ties to even (default rounding mode)
+    if (r >= 16.0) { r = 8.0; ex += 1; }
+    if (ex > 8 || (ex == 8 && r > 14.0)) return sign | 0x7E;
+    if (r < 8.0) return sign | (uint8_t)r;                 // subnormal (ex == -6)
+    return sign | (uint8_t)(((ex + 7) << 3) | ((int)r - 8));
+}
+
 }  // namespace
 
 int mlp_concat_layer(int L) {
@@ -348,11 +402,13 @@ int64_t mlp_blob_halves(int H, int L) {
 }
 
 // Build the blocked device weights of every layer (K padded to 64, N padded to BN, zeros elsewhere).
-int mlp_load(pt_nif* nif, int H, int L, const uint16_t* blob, std::string* msg) {
+int mlp_load(pt_nif* nif, int H, int L, const uint16_t* blob, int fp8, std::string* msg) {
     const int c = mlp_concat_layer(L);
     nif->mlp_H = H;
     nif->mlp_L = L;
     nif->mlp_c = c;
+    nif->mlp_fp8 = fp8 ? 1 : 0;
+    const int esize = fp8 ? 1 : 2, chunk_k = 128 / esize;
     int64_t off = 0;
     std::vector<float> freq(40);
     for (int i = 0; i < 40; ++i) freq[i] = half_to_float(blob[off++]);
@@ -364,11 +420,11 @@ int mlp_load(pt_nif* nif, int H, int L, const uint16_t* blob, std::string* msg) 
     for (int l = 0; l <= L; ++l) {
         MlpLayer ly;
         const int fin = l == 0 ? 40 : H, fout = l == L ? 3 : (l == c ? H - 40 : H);
-        ly.K = ((fin + 63) / 64) * 64;
+        ly.K = ((fin + chunk_k - 1) / chunk_k) * chunk_k;
         ly.N_valid = fout;
         ly.BN = pick_bn(fout);
         ly.NT = (fout + ly.BN - 1) / ly.BN;
-        const int KC = ly.K / 64;
+        const int KC = ly.K / chunk_k;
         std::vector<uint8_t> img((size_t)ly.NT * KC * ly.BN * 128, 0);
         const uint16_t* W = blob + off;
         off += (int64_t)fin * fout;
@@ -377,9 +433,11 @@ int mlp_load(pt_nif* nif, int H, int L, const uint16_t* blob, std::string* msg) 
         for (int nrow = 0; nrow < fout; ++nrow) {
             const int nt = nrow / ly.BN, nn = nrow % ly.BN, nb = nn >> 3, r = nn & 7;
             for (int k = 0; k < fin; ++k) {
-                const int kc = k >> 6, kb = (k & 63) >> 3, cc = k & 7;
-                const size_t o = ((size_t)nt * KC + kc) * ly.BN * 128 + (size_t)((kb * (ly.BN / 8) + nb) * 128) + r * 16 + cc * 2;
-                std::memcpy(&img[o], &W[(int64_t)nrow * fin + k], 2);
+                const int bc = k * esize, kc = bc >> 7, kb = (bc & 127) >> 4, cc = bc & 15;
+                const size_t o = ((size_t)nt * KC + kc) * ly.BN * 128 + (size_t)((kb * (ly.BN / 8) + nb) * 128) + r * 16 + cc;
+                const uint16_t w = W[(int64_t)nrow * fin + k];
+                if (fp8) img[o] = float_to_e4m3(half_to_float(w));
+                else std::memcpy(&img[o], &w, 2);
             }
         }
         std::vector<float> bias((size_t)ly.NT * ly.BN, 0.0f);
@@ -410,22 +468,33 @@ void mlp_free(pt_nif* nif) {
     nif->mlp_act[0] = nif->mlp_act[1] = nullptr;
 }
 
-template <int BN, int kEpi>
+template <int BN, int kEpi, bool kFp8>
 static cudaError_t launch_layer_t(const mlp::LayerArgs& a, int grid, int smem, cudaStream_t st) {
     static int configured = 0;
     if (configured < smem) {
-        cudaError_t e = cudaFuncSetAttribute(mlp_layer_kernel<BN, kEpi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             mlp::kSmemBudget + mlp::kBarBytes);
+        cudaError_t e = cudaFuncSetAttribute(mlp_layer_kernel<BN, kEpi, kFp8>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, mlp::kSmemBudget + mlp::kBarBytes);
         if (e != cudaSuccess) return e;
         configured = mlp::kSmemBudget + mlp::kBarBytes;
     }
-    mlp_layer_kernel<BN, kEpi><<<grid, mlp::kThreads, smem, st>>>(a);
+    mlp_layer_kernel<BN, kEpi, kFp8><<<grid, mlp::kThreads, smem, st>>>(a);
     return cudaGetLastError();
 }
 
-static cudaError_t launch_layer(const MlpLayer& ly, int epi, mlp::LayerArgs a, cudaStream_t st) {
+template <bool kFp8>
+static cudaError_t launch_layer_bn(int bn, int epi, const mlp::LayerArgs& a, int grid, int smem, cudaStream_t st) {
+    if (epi == 1) return launch_layer_t<16, 1, kFp8>(a, grid, smem, st);
+    switch (bn) {
+        case 64: return launch_layer_t<64, 0, kFp8>(a, grid, smem, st);
+        case 128: return launch_layer_t<128, 0, kFp8>(a, grid, smem, st);
+        case 256: return launch_layer_t<256, 0, kFp8>(a, grid, smem, st);
+        default: return launch_layer_t<16, 0, kFp8>(a, grid, smem, st);
+    }
+}
+
+static cudaError_t launch_layer(const MlpLayer& ly, int epi, int fp8, mlp::LayerArgs a, cudaStream_t st) {
     using namespace mlp;
-    const int KC = ly.K / 64;
+    const int KC = ly.K / (fp8 ? 128 : 64);
     const int bchunk = ly.BN * 128;
     const bool res = ly.NT == 1 && (int64_t)KC * bchunk <= 128 * 1024;
     const int stage_bytes = kAChunk + (res ? 0 : bchunk);
@@ -440,13 +509,7 @@ static cudaError_t launch_layer(const MlpLayer& ly, int epi, mlp::LayerArgs a, c
     const int smem = kBarBytes + a.stages * stage_bytes + (res ? KC * bchunk : 0);
     const int64_t tiles = (int64_t)((a.rows_cap + kBM - 1) / kBM) * ly.NT;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, num_sms()));
-    if (epi == 1) return launch_layer_t<16, 1>(a, grid, smem, st);
-    switch (ly.BN) {
-        case 64: return launch_layer_t<64, 0>(a, grid, smem, st);
-        case 128: return launch_layer_t<128, 0>(a, grid, smem, st);
-        case 256: return launch_layer_t<256, 0>(a, grid, smem, st);
-        default: return launch_layer_t<16, 0>(a, grid, smem, st);
-    }
+    return fp8 ? launch_layer_bn<true>(ly.BN, epi, a, grid, smem, st) : launch_layer_bn<false>(ly.BN, epi, a, grid, smem, st);
 }
 
 // Row chunks of up to kChunkRows rows; every chunk launch reads the device row count and exits when
@@ -456,10 +519,10 @@ constexpr int kChunkRows = 1 << 20;
 cudaError_t launch_mlp(pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count, int64_t max_rows,
                        float* out, int dir_input, cudaStream_t st) {
     using namespace mlp;
-    const int H = nif->mlp_H, L = nif->mlp_L, c = nif->mlp_c;
-    const int kmax = std::max(64, H);
+    const int H = nif->mlp_H, L = nif->mlp_L, c = nif->mlp_c, fp8 = nif->mlp_fp8;
+    const int kc_of_H = (H * (fp8 ? 1 : 2) + 127) / 128;          // K chunks of an H-wide activation row
     const int cap = (int)std::min<int64_t>(kChunkRows, ((max_rows + kBM - 1) / kBM) * kBM);
-    const int64_t need = (int64_t)((cap + kBM - 1) / kBM) * kBM * kmax * 2;
+    const int64_t need = (int64_t)((cap + kBM - 1) / kBM) * kAChunk * kc_of_H;
     if (need > nif->mlp_act_bytes) {
         cudaStreamSynchronize(st);
         cudaFree(nif->mlp_act[0]);
@@ -468,19 +531,22 @@ cudaError_t launch_mlp(pt_nif* nif, const float4* esc, const float4* esc_beta, c
         nif->mlp_act_bytes = 0;
         cudaError_t e = cudaMalloc(&nif->mlp_act[0], need);
         if (e == cudaSuccess) e = cudaMalloc(&nif->mlp_act[1], need);
+        // K padding columns (fp8 H = 64: 64..127) are never written and must read as zeros
+        if (e == cudaSuccess) e = cudaMemsetAsync(nif->mlp_act[0], 0, need, st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(nif->mlp_act[1], 0, need, st);
         if (e != cudaSuccess) return e;
         nif->mlp_act_bytes = need;
     }
     uint8_t* buf[2] = {(uint8_t*)nif->mlp_act[0], (uint8_t*)nif->mlp_act[1]};
-    const int kc_of_H = H / 64;
     for (int64_t r0 = 0; r0 < max_rows; r0 += cap) {
         const int fgrid = std::max(1, std::min(num_sms() * 4, (cap + 255) / 256));
         // layer-0 input; the concat columns of layer c + 1 too when that buffer is not read before
-        mlp_features_kernel<<<fgrid, 256, 0, st>>>(esc, count, (int)r0, cap, dir_input, nif->mlp_freq, buf[0], 1, 0, 1);
+        mlp_features_kernel<<<fgrid, 256, 0, st>>>(esc, count, (int)r0, cap, dir_input, nif->mlp_freq, buf[0], 1, 0, 1,
+                                                   fp8);
         for (int l = 0; l <= L; ++l) {
             if (l == c) {
                 mlp_features_kernel<<<fgrid, 256, 0, st>>>(esc, count, (int)r0, cap, dir_input, nif->mlp_freq,
-                                                           buf[(c + 1) & 1], kc_of_H, H - 40, 0);
+                                                           buf[(c + 1) & 1], kc_of_H, H - 40, 0, fp8);
             }
             LayerArgs a{};
             a.A = buf[l & 1];
@@ -492,7 +558,7 @@ cudaError_t launch_mlp(pt_nif* nif, const float4* esc, const float4* esc_beta, c
             a.esc = esc;
             a.esc_beta = esc_beta;
             a.out_rgb = out;
-            cudaError_t e = launch_layer(nif->mlp_layers[l], l == L ? 1 : 0, a, st);
+            cudaError_t e = launch_layer(nif->mlp_layers[l], l == L ? 1 : 0, fp8, a, st);
             if (e != cudaSuccess) return e;
         }
     }

@@ -430,11 +430,14 @@ int pt_nif_load(const uint16_t* blob, int64_t n_halves, pt_nif** out) {
     return pt_nif_load_ex(PT_NIF_SIREN, blob, n_halves, out);
 }
 
-int pt_nif_load_family(int32_t hidden, int32_t layers, const uint16_t* blob, int64_t n_halves, pt_nif** out) {
+int pt_nif_load_family_ex(int32_t hidden, int32_t layers, int32_t precision, const uint16_t* blob, int64_t n_halves,
+                          pt_nif** out) {
     if (!blob || !out) return fail(PT_ERR_INVALID_ARG, "null argument");
     *out = nullptr;
     if (hidden < 64 || hidden > 1024 || hidden % 64 != 0 || layers < 1 || layers > 16)
         return fail(PT_ERR_INVALID_ARG, "hidden must be a multiple of 64 in [64, 1024], layers in [1, 16]");
+    if (precision != PT_NIF_FP16 && precision != PT_NIF_FP8)
+        return fail(PT_ERR_INVALID_ARG, "precision must be PT_NIF_FP16 or PT_NIF_FP8");
     if (n_halves != pt::mlp_blob_halves(hidden, layers))
         return fail(PT_ERR_FORMAT, "NIF family blob size does not match (hidden, layers)");
     for (int64_t i = 0; i < n_halves; ++i)
@@ -445,13 +448,17 @@ int pt_nif_load_family(int32_t hidden, int32_t layers, const uint16_t* blob, int
     n->kind = PT_NIF_FR_FAMILY;
     cudaGetDevice(&n->device);
     std::string msg;
-    rc = pt::mlp_load(n, hidden, layers, blob, &msg);
+    rc = pt::mlp_load(n, hidden, layers, blob, precision == PT_NIF_FP8, &msg);
     if (rc) {
         pt_nif_destroy(n);
         return fail(rc, msg);
     }
     *out = n;
     return PT_OK;
+}
+
+int pt_nif_load_family(int32_t hidden, int32_t layers, const uint16_t* blob, int64_t n_halves, pt_nif** out) {
+    return pt_nif_load_family_ex(hidden, layers, PT_NIF_FP16, blob, n_halves, out);
 }
 
 int pt_nif_destroy(pt_nif* n) {

@@ -117,7 +117,7 @@ struct pt_nif {
     int64_t smem_bytes = 0;
     uint16_t* d_blob = nullptr;       // raw fp16 blob
     // PT_NIF_FR_FAMILY (layered GEMM path)
-    int mlp_H = 0, mlp_L = 0, mlp_c = 0;
+    int mlp_H = 0, mlp_L = 0, mlp_c = 0, mlp_fp8 = 0;
     float* mlp_freq = nullptr;        // B [20][2] fp32
     std::vector<MlpLayer> mlp_layers;
     void* mlp_act[2] = {nullptr, nullptr};   // blocked activation ping-pong buffers (lazily sized)
@@ -167,7 +167,7 @@ int num_sms();
 // the paper's NIF family (mlp_kernel.cu)
 int mlp_concat_layer(int L);
 int64_t mlp_blob_halves(int H, int L);
-int mlp_load(pt_nif* nif, int H, int L, const uint16_t* blob, std::string* msg);
+int mlp_load(pt_nif* nif, int H, int L, const uint16_t* blob, int fp8, std::string* msg);
 void mlp_free(pt_nif* nif);
 cudaError_t launch_mlp(pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count, int64_t max_rows,
                        float* out, int dir_input, cudaStream_t st);

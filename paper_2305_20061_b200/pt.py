@@ -30,7 +30,7 @@ class PtStats(C.Structure):
 
 
 EXPORTED = ["pt_scene_create", "pt_scene_destroy", "pt_nif_load", "pt_nif_load_ex", "pt_nif_load_family",
-            "pt_nif_destroy", "pt_render",
+            "pt_nif_load_family_ex", "pt_nif_destroy", "pt_render",
             "pt_render_samples", "pt_trace_primary", "pt_trace_rays", "pt_nif_infer", "pt_get_stats",
             "pt_set_profiling", "pt_last_error", "pt_version"]
 
@@ -49,6 +49,7 @@ def lib():
             L.pt_nif_load.argtypes = [P, I64, C.POINTER(P)]
             L.pt_nif_load_ex.argtypes = [I32, P, I64, C.POINTER(P)]
             L.pt_nif_load_family.argtypes = [I32, I32, P, I64, C.POINTER(P)]
+            L.pt_nif_load_family_ex.argtypes = [I32, I32, I32, P, I64, C.POINTER(P)]
             L.pt_nif_destroy.argtypes = [P]
             L.pt_render.argtypes = [P, P, P, I32, I32, I32, I32, U64, P]
             L.pt_render_samples.argtypes = [P, P, P, I32, I32, I32, I32, I32, U64, I32, P, P]
@@ -128,12 +129,13 @@ NIF_FR_FAMILY = 2      # PT_NIF_FR_FAMILY: the size-sweep family (scenes.fourier
 
 
 class Nif:
-    def __init__(self, blob: np.ndarray, kind: int = NIF_SIREN, hidden: int = 0, layers: int = 0):
-        """kind NIF_FR_FAMILY needs (hidden, layers): pt_nif_load_family; else pt_nif_load_ex."""
+    def __init__(self, blob: np.ndarray, kind: int = NIF_SIREN, hidden: int = 0, layers: int = 0, fp8: bool = False):
+        """kind NIF_FR_FAMILY needs (hidden, layers) (+ fp8: e4m3 weights/activations):
+        pt_nif_load_family_ex; else pt_nif_load_ex."""
         b = np.ascontiguousarray(blob, dtype=np.uint16)
         h = C.c_void_p()
         if kind == NIF_FR_FAMILY:
-            _check(lib().pt_nif_load_family(int(hidden), int(layers), _p(b), b.size, C.byref(h)))
+            _check(lib().pt_nif_load_family_ex(int(hidden), int(layers), int(bool(fp8)), _p(b), b.size, C.byref(h)))
         else:
             _check(lib().pt_nif_load_ex(int(kind), _p(b), b.size, C.byref(h)))
         self._lib = lib()

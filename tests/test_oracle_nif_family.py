@@ -30,7 +30,7 @@ def test_family_sizes():
     assert abs(kib[(1024, 8)] / 1024 - 14.02) < 0.01          # 14.0 MiB
 
 
-def _chain_blob(H, L):
+def _chain_blob(H, L, w=None, bias=None, cos_w=3.0):
     """Single active path: sin feature 5 -> unit 3 of layer 0 -> ... ; the layer after the concat
     also reads cos feature 5 from its concat column. Returns (blob, closed-form function of (u, v))."""
     c = scenes.fr_concat_layer(L)
@@ -42,14 +42,14 @@ def _chain_blob(H, L):
     units = [3 + 2 * l for l in range(L)]               # active unit of layer l (always < H - 40)
     Ws[0][units[0], 5] = 2.0                             # sin feature 5
     bs[0][units[0]] = 0.25
-    wl = [None] + [(-1.5 if l % 2 else 0.75) for l in range(1, L)]
-    bl = [None] + [(1.0 if l % 2 else 0.125) for l in range(1, L)]
+    wl = [None] + [(w if w is not None else (-1.5 if l % 2 else 0.75)) for l in range(1, L)]
+    bl = [None] + [(bias if bias is not None else (1.0 if l % 2 else 0.125)) for l in range(1, L)]
     cos_col = (H - 40) + 20 + 5                          # cos feature 5 in the concat input
     for l in range(1, L):
         Ws[l][units[l], units[l - 1]] = wl[l]
         bs[l][units[l]] = bl[l]
         if l == c + 1:
-            Ws[l][units[l], cos_col] = 3.0
+            Ws[l][units[l], cos_col] = cos_w
     Ws[L][0, units[L - 1]] = 1.0                         # Y
     Ws[L][2, units[L - 1]] = 0.5                         # V
     bs[L][:] = (0.125, 0.25, 0.0)
@@ -65,7 +65,7 @@ def _chain_blob(H, L):
         for l in range(1, L):
             z = wl[l] * x + bl[l]
             if l == c + 1:
-                z += 3.0 * math.cos(p)
+                z += cos_w * math.cos(p)
             x = relu(z)
         Y, U, V = 0.125 + x, 0.25, 0.5 * x
         return np.array([Y + 1.13983 * V, Y - 0.39465 * U - 0.58060 * V, Y + 2.03211 * U])
@@ -113,3 +113,51 @@ def test_render_fr_empty_scene_is_the_nif_of_the_camera_rays(orc, H, L):
         want += np.exp(orc.fr_eval_hl(H, L, blob, orc.equirect(d)))
     assert st["escaped"] == W * Hh * 2
     assert np.abs(out - want).max() <= 1e-12 * np.abs(want).max()
+
+
+def test_e4m3_rounding(orc):
+    """OCP e4m3, round to nearest even, saturating at 448: hand-computed cases (ties go to the even
+    code), and agreement with torch's float8_e4m3fn conversion (a library routine) inside the range."""
+    import torch
+    cases = {0.0: 0.0, 1.0: 1.0, 1.0625: 1.0, 1.1875: 1.25, 1.125: 1.125, 448.0: 448.0, 500.0: 448.0,
+             2.0 ** -9: 2.0 ** -9, 2.0 ** -10: 0.0, 3 * 2.0 ** -11: 2.0 ** -9, 232.0: 224.0, 248.0: 256.0,
+             -0.3: -0.3125}
+    for x, want in cases.items():
+        assert orc.e4m3_round(x) == want, x
+    xs = np.random.default_rng(1).uniform(-440, 440, 5000) * np.random.default_rng(2).choice([1e-3, 1e-1, 1], 5000)
+    ref = torch.from_numpy(xs).float().to(torch.float8_e4m3fn).double().numpy()
+    assert np.array_equal(np.array([orc.e4m3_round(float(np.float32(x))) for x in xs]), ref)
+
+
+def test_fp8_oracle_on_representable_chain_equals_fp16(orc):
+    """With B = 0 (features sin 0 = 0, cos 0 = 1) and weights/biases whose every partial result is an
+    e4m3 value, the fp8 evaluation performs no rounding at all and equals the fp16 one exactly."""
+    for H, L in [(64, 2), (256, 4)]:
+        blob, _ = _chain_blob(H, L, w=1.0, bias=0.25, cos_w=0.5)   # activations 0.25, 0.5, 1.25, 1.5 ...
+        h = blob.view(np.float16).copy()
+        h[:40] = 0                                         # B = 0
+        blob0 = h.view(np.uint16)
+        uv = np.random.default_rng(3).random((8, 2))
+        a = orc.fr_eval_hl_fp8(H, L, blob0, uv)
+        b = orc.fr_eval_hl(H, L, blob0, uv)
+        assert np.array_equal(a, b), (H, L)
+
+
+def test_fp8_oracle_rounds_hidden_activations(orc):
+    """One unit whose pre-activation is 1.0625 (a tie between e4m3 1.0 and 1.125): the fp8 model feeds
+    1.0 forward, the fp16 model 1.0625 (closed form through the output Y)."""
+    H, L = 64, 2
+    dims = scenes.fr_family_layers(H, L)
+    Ws = [np.zeros((o, i)) for i, o in dims]
+    bs = [np.zeros(o) for i, o in dims]
+    bs[0][3] = 1.0625                                      # h0[3] = relu(1.0625), exact in fp16
+    Ws[1][5, 3] = 1.0
+    Ws[2][0, 5] = 1.0                                      # Y = h1[5]
+    parts = [np.zeros(40)]
+    for W, b in zip(Ws, bs):
+        parts += [W.reshape(-1), b]
+    blob = np.concatenate(parts).astype(np.float16).view(np.uint16)
+    uv = np.array([[0.3, 0.6]])
+    y8 = orc.fr_eval_hl_fp8(H, L, blob, uv)[0]
+    y16 = orc.fr_eval_hl(H, L, blob, uv)[0]
+    assert y16[0] == 1.0625 and y8[0] == 1.0 and y8[1] == 1.0 and y8[2] == 1.0

@@ -36,10 +36,12 @@ def flops_of(dims):
 nets = [("siren", pt.Nif(scenes.siren_blob(0)), 3 * 2 * 128 * 128 + 2 * (2 * 128 + 128 * 3)),
         ("paper_fused_H128L4", pt.Nif(scenes.fourier_relu_blob(0), kind=pt.NIF_FOURIER_RELU),
          flops_of(scenes.FR_LAYERS))]
-for H, L in scenes.NIF_SWEEP:
-    nets.append((f"paper_layered_H{H}L{L}",
-                 pt.Nif(scenes.fourier_relu_family_blob(H, L, seed=1), kind=pt.NIF_FR_FAMILY, hidden=H, layers=L),
-                 flops_of(scenes.fr_family_layers(H, L))))
+for fp8 in (False, True):
+    for H, L in scenes.NIF_SWEEP:
+        nets.append((f"paper_layered_H{H}L{L}" + ("_fp8" if fp8 else ""),
+                     pt.Nif(scenes.fourier_relu_family_blob(H, L, seed=1), kind=pt.NIF_FR_FAMILY, hidden=H, layers=L,
+                            fp8=fp8),
+                     flops_of(scenes.fr_family_layers(H, L))))
 
 c = scenes.CONFIGS[2]
 S = pt.Scene(scenes.scene_for_config(2)) if a.render else None
@@ -59,8 +61,11 @@ for name, nif, flop in nets:
     ms = e0.elapsed_time(e1) / a.iters
     rate = n / (ms / 1e3)
     tf = rate * flop / 1e12
+    # the peak of the arithmetic type: fp8 dense = 2 x the measured bf16 peak (the guide's nominal ratio)
+    pk = 2.0 if name.endswith("_fp8") else 1.0
     res = {"net": name, "queries": n, "ms": ms, "inferences_per_s": rate, "flop_per_inference": flop,
-           "tflops": tf, "frac_burst": tf / peaks["bf16_tflops"], "frac_sustained": tf / peaks["bf16_tflops_sustained"]}
+           "tflops": tf, "frac_burst": tf / (pk * peaks["bf16_tflops"]),
+           "frac_sustained": tf / (pk * peaks["bf16_tflops_sustained"])}
     if a.render:
         acc = torch.zeros(c.width * c.height * 3, device="cuda")
         pt.render_samples(S, nif, c.width, c.height, 0, a.spp, c.max_depth, 0, acc, wave_samples=a.spp)
