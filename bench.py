@@ -318,7 +318,6 @@ def main():
                         "bytes_alg": 80 * segments},
         "nif": {"ms_per_step": nif_ms / K, "launches_per_step": nif_launches / K,
                 "flops_alg": HIDDEN_FLOP_PER_INF * infers},
-        "raygen": {"ms_per_step": kt["raygen"] / K, "bytes_alg": 40 * paths},
         "accumulate": {"ms_per_step": kt["accum"] / K},
     }
     dominant = max(kernels, key=lambda n: kernels[n]["ms_per_step"])
@@ -344,11 +343,6 @@ def main():
                 "segments_per_launch": segments / max(1, trav_launches),
                 "peak_source": "measured L2 read bandwidth, tools/l2_bench.cu (MEASURED_PEAKS.json has none)",
                 "hbm_frac": (80.0 * segments / (ms_k / 1e3) / 1e9) / peaks["hbm_gbs"] if ms_k > 0 else 0.0}
-    elif dominant == "raygen":
-        ms_k = kt["raygen"]
-        gbs = 40 * paths / (ms_k / 1e3) / 1e9
-        roof = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": gbs / peaks["hbm_gbs"], "traffic": None, "kernel": "raygen_kernel"}
     else:
         roof = nif_roof
     clocks = clk.summary()

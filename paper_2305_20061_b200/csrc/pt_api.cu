@@ -222,13 +222,10 @@ int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, i
         CU(cudaMemsetAsync(ws.counters, 0, sizeof(uint32_t) * pt::kCounters, st));
         set_count_kernel<<<1, 1, 0, st>>>(ws.counters + 0, (uint32_t)slots);
         cudaEvent_t e0;
-        tm.begin(T_RAYGEN, &e0);
-        pt::launch_raygen(cam, W, H, (int)w0, (int)slots, seed, ws, st);
-        tm.end(T_RAYGEN, e0);
         for (int d = 1; d <= max_depth; ++d) {
             const int buf = (d - 1) & 1;       // bounce d reads state buffer buf, shade writes buf ^ 1
             tm.begin(T_TRAVERSE, &e0);
-            pt::launch_trace_shade(tp, W, H, (int)w0, d, max_depth, seed, buf, use_nif, env, ws, st);
+            pt::launch_trace_shade(tp, cam, W, H, (int)w0, d, max_depth, seed, buf, use_nif, env, ws, st);
             tm.end(T_TRAVERSE, e0);
             stats.launches += 1;
             stats.traverse_launches += 1;
@@ -247,7 +244,7 @@ int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, i
         pt::launch_accumulate(ws.wave_buf, (int)np, (int)kk, d_accum, st);
         tm.end(T_ACCUM, e0);
         stats_kernel<<<1, 1, 0, st>>>(ws.counters, max_depth, d_stats);
-        stats.launches += 4;   // set_count, raygen, accumulate, stats
+        stats.launches += 3;   // set_count, accumulate, stats
         stats.waves += 1;
     }
     CU(cudaGetLastError());

@@ -144,10 +144,8 @@ struct TraceParams {
 };
 
 // kernel launchers (trace_kernels.cu)
-void launch_raygen(const Cam32& cam, int W, int H, int first_sample, int n_slots, uint64_t seed, Workspace& ws,
-                   cudaStream_t st);
-void launch_trace_shade(const TraceParams& tp, int W, int H, int first_sample, int depth, int max_depth, uint64_t seed,
-                        int buf, int use_nif, float3 env, Workspace& ws, cudaStream_t st);
+void launch_trace_shade(const TraceParams& tp, const Cam32& cam, int W, int H, int first_sample, int depth, int max_depth,
+                        uint64_t seed, int buf, int use_nif, float3 env, Workspace& ws, cudaStream_t st);
 void launch_accumulate(const float* wave_buf, int n_pix, int k, float* fb, cudaStream_t st);
 void launch_primary(const TraceParams& tp, const Cam32& cam, int W, int H, int sample, uint64_t seed,
                     int32_t* prim, float* t, cudaStream_t st);

@@ -524,20 +524,7 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
 // ---------------------------------------------------------------------------------------------
 // Ray state is kept in queue order (compacted every bounce) so every kernel reads and writes it
 // coalesced: A = (o.xyz, slot), B = (d.xyz, beta.x), C = (beta.y, beta.z)  -- 40 B per live path.
-__global__ void __launch_bounds__(256) raygen_kernel(Cam32 cam, int W, int H, int first_sample, int n_slots, uint2 key,
-                                                     float4* __restrict__ A, float4* __restrict__ B,
-                                                     float2* __restrict__ C) {
-    const int np = W * H;
-    for (int slot = blockIdx.x * blockDim.x + threadIdx.x; slot < n_slots; slot += gridDim.x * blockDim.x) {
-        const int p = slot % np;
-        const int s = first_sample + slot / np;
-        const uint4 r = philox10(make_uint4((uint32_t)p, (uint32_t)s, 0u, 0u), key);
-        const float3 d = cam_dir(cam, W, H, p % W, p / W, u01f(r.x), u01f(r.y));
-        A[slot] = make_float4(cam.eye[0], cam.eye[1], cam.eye[2], __uint_as_float((uint32_t)slot));
-        B[slot] = make_float4(d.x, d.y, d.z, 1.0f);
-        C[slot] = make_float2(1.0f, 1.0f);
-    }
-}
+// (The first bounce computes its camera rays itself: S1 raygen is fused into trace_shade_kernel.)
 
 // warp-aggregated append to the alive and the escaped queue at once: one 64-bit atomic per warp on the
 // bounce's packed counter (low: alive, high: escaped); returns this lane's positions in both queues
@@ -558,6 +545,7 @@ __device__ __forceinline__ void warp_append2(bool alive, bool escaped, unsigned 
 
 struct ShadeArgs {
     TraceParams tp;
+    Cam32 cam;
     int W, H, first_sample, depth, max_depth;
     uint2 key;
     const uint32_t* counters;   // the wave's counters (pt_internal.h kCounters layout)
@@ -602,8 +590,24 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) trace_shade_kernel(ShadeArgs 
         uint32_t slot = 0;
         float3 o3 = make_float3(0, 0, 0), wi = make_float3(0, 0, 0), bt = make_float3(0, 0, 0);
         if (active) {
-            const float4 o = __ldg(a.A_in + i), d4 = __ldg(a.B_in + i);
-            const float2 c2 = __ldg(a.C_in + i);
+            float4 o, d4;
+            float2 c2;
+            if (a.depth == 1) {
+                // S1 raygen fused into the first bounce: the wave's slot i is (pixel i % np, sample
+                // first + i / np); the camera ray is recomputed here instead of round-tripping 40 B per
+                // path through HBM
+                const int p = (int)(i % (uint32_t)np);
+                const int sm = a.first_sample + (int)(i / (uint32_t)np);
+                const uint4 r = philox10(make_uint4((uint32_t)p, (uint32_t)sm, 0u, 0u), a.key);
+                const float3 dc = cam_dir(a.cam, a.W, a.H, p % a.W, p / a.W, u01f(r.x), u01f(r.y));
+                o = make_float4(a.cam.eye[0], a.cam.eye[1], a.cam.eye[2], __uint_as_float(i));
+                d4 = make_float4(dc.x, dc.y, dc.z, 1.0f);
+                c2 = make_float2(1.0f, 1.0f);
+            } else {
+                o = __ldg(a.A_in + i);
+                d4 = __ldg(a.B_in + i);
+                c2 = __ldg(a.C_in + i);
+            }
             const Hit hh = closest_hit(a.tp, make_float3(o.x, o.y, o.z), make_float3(d4.x, d4.y, d4.z));
             const int32_t prim = hh.prim;
             slot = __float_as_uint(o.w);
@@ -787,13 +791,6 @@ static int grid_for(int64_t n, int block, int per_sm) {
     return (int)g;
 }
 
-void launch_raygen(const Cam32& cam, int W, int H, int first_sample, int n_slots, uint64_t seed, Workspace& ws,
-                   cudaStream_t st) {
-    const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
-    raygen_kernel<<<grid_for(n_slots, 256, 8), 256, 0, st>>>(cam, W, H, first_sample, n_slots, key, ws.rayA[0],
-                                                             ws.rayB[0], ws.rayC[0]);
-}
-
 // persistent grids: exactly the resident block count (one wave), so no SM idles behind a partial wave
 template <typename K>
 static int resident_grid(K kernel, int block) {
@@ -802,10 +799,11 @@ static int resident_grid(K kernel, int block) {
     return num_sms() * (per_sm > 0 ? per_sm : 1);
 }
 
-void launch_trace_shade(const TraceParams& tp, int W, int H, int first_sample, int depth, int max_depth, uint64_t seed,
-                        int buf, int use_nif, float3 env, Workspace& ws, cudaStream_t st) {
+void launch_trace_shade(const TraceParams& tp, const Cam32& cam, int W, int H, int first_sample, int depth, int max_depth,
+                        uint64_t seed, int buf, int use_nif, float3 env, Workspace& ws, cudaStream_t st) {
     ShadeArgs a;
     a.tp = tp;
+    a.cam = cam;
     a.W = W; a.H = H; a.first_sample = first_sample; a.depth = depth; a.max_depth = max_depth;
     a.key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
     a.counters = ws.counters;
