@@ -278,13 +278,16 @@ def main():
 
     # ---- end-to-end through the public API: host arrays in, host framebuffer out ----
     e2e_steps = max(3, min(args.steps, 20))
+    e2e_warmup = max(1, min(args.warmup, 3))
     host_fb = torch.empty(W * H * 3, dtype=torch.float32, pin_memory=True)
     h2d = src.tris.nbytes + src.spheres.nbytes + src.materials.nbytes + src.camera.nbytes + (blob.nbytes if blob is not None else 0)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    te0 = time.perf_counter()
-    for _ in range(e2e_steps):
+    te0 = None
+    for it in range(e2e_warmup + e2e_steps):
+        if it == e2e_warmup:            # untimed warm-up iterations first (allocator, first-launch setup)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            te0 = time.perf_counter()
         S2 = pt.Scene(src)
         N2 = pt.Nif(blob) if cfg.use_nif else None
         acc2 = torch.zeros(W * H * 3, dtype=torch.float32, device="cuda")
