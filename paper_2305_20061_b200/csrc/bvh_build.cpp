@@ -151,6 +151,17 @@ inline float f32_next_up(double x) {
     return f;
 }
 
+// The node origin with 4 metadata bits embedded in its lowest mantissa bits: a float <= lo (so every
+// child offset stays >= 0) whose low 4 bits are `nib` -- 16 ulps below lo, then the bits replaced
+// (positive: the value rises by at most 15 ulps; negative: the magnitude falls by at most 15 ulps).
+inline float embed_nibble(float lo, uint32_t nib) {
+    float x = lo;
+    for (int i = 0; i < 16; ++i) x = std::nextafter(x, -std::numeric_limits<float>::infinity());
+    uint32_t b = __builtin_bit_cast(uint32_t, x);
+    b = (b & ~15u) | (nib & 15u);
+    return __builtin_bit_cast(float, b);
+}
+
 inline float decode(float O, uint16_t h) {
     volatile float hv = (float)f16_value(h);   // exact widening
     volatile float s = O + hv;                 // the single fp32 round-to-nearest add the kernel does
@@ -260,22 +271,32 @@ int build_wide_bvh(const pt_triangle* tris, int64_t n_tris, const pt_sphere* sph
         units = (units + 3) & ~int64_t(3);
         int64_t base = alloc(units);
         if (base + units > (1ll << 28)) { *msg = "BVH pool exceeds 2^28 units (4 GiB)"; return PT_ERR_DOMAIN; }
-        // node header
+        // node header. Child metadata: one nibble per child = its size in pool units (0: no child,
+        // 4: interior node, 3 * count: leaf of count primitives), so the kernel gets validity, kind,
+        // count and the running child offset from one 16-bit field: nibbles 0-2 ride in the low
+        // mantissa bits of the origin's x, y, z (embed_nibble), nibble 3 in the top bits of the base.
+        uint32_t nib[4] = {0, 0, 0, 0};
+        for (int ci = 0; ci < (int)ch.size(); ++ci) {
+            const Node2& c = B.nodes[ch[ci]];
+            nib[ci] = c.count > 0 ? (uint32_t)(kPrimUnits * c.count) : (uint32_t)kNodeUnits;
+        }
         Box nb;
         nb.empty();
         for (int32_t c : ch) nb.grow(B.nodes[c].b);
+        float Oq[3];
+        for (int a = 0; a < 3; ++a) Oq[a] = embed_nibble(nb.lo[a], nib[a]);
         uint4& h0 = pool[pnd.unit];
-        h0.x = __builtin_bit_cast(uint32_t, nb.lo[0]);
-        h0.y = __builtin_bit_cast(uint32_t, nb.lo[1]);
-        h0.z = __builtin_bit_cast(uint32_t, nb.lo[2]);
-        h0.w = (uint32_t)base;
+        h0.x = __builtin_bit_cast(uint32_t, Oq[0]);
+        h0.y = __builtin_bit_cast(uint32_t, Oq[1]);
+        h0.z = __builtin_bit_cast(uint32_t, Oq[2]);
+        h0.w = (uint32_t)base | (nib[3] << 28);
         uint16_t q[4][6];
         std::memset(q, 0, sizeof(q));
         int64_t off = base;
         for (int ci = 0; ci < (int)ch.size(); ++ci) {
             const Node2& c = B.nodes[ch[ci]];
             for (int a = 0; a < 3; ++a) {
-                const float O = nb.lo[a];
+                const float O = Oq[a];
                 double dlo = (double)c.b.lo[a] - (double)O, dhi = (double)c.b.hi[a] - (double)O;
                 if (!(dhi <= 65504.0) || !(dlo >= 0.0)) {
                     *msg = "child box offset outside the fp16 range (scene extent too large for one node)";
@@ -292,12 +313,7 @@ int build_wide_bvh(const pt_triangle* tris, int64_t n_tris, const pt_sphere* sph
                 q[ci][3 + a] = hh;
             }
             const bool leaf = c.count > 0;
-            q[ci][0] |= 0x8000;                         // valid
             if (leaf) {
-                q[ci][1] |= 0x8000;
-                int cm1 = c.count - 1;
-                if (cm1 & 1) q[ci][2] |= 0x8000;
-                if (cm1 & 2) q[ci][3] |= 0x8000;
                 ++n_leaves;
                 for (int k = 0; k < c.count; ++k) {
                     int64_t id = B.order[c.first + k];

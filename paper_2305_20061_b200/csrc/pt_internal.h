@@ -14,13 +14,13 @@ namespace pt {
 
 // ---------------------------------------------------------------------------------------------
 // Wide BVH, device layout:
-//   a pool of 16-byte units. An interior node is 4 units (64 B, 64-B aligned):
-//     unit 0: float O.x, O.y, O.z (node origin = box min, fp32), uint32 base (unit index of the child block)
+//   a pool of 16-byte units (< 2^28 of them). An interior node is 4 units (64 B, 64-B aligned):
+//     unit 0: float O.x, O.y, O.z (node origin, <= the box min, fp32), uint32 base | nib3 << 28
 //     units 1-3: 4 child boxes x 12 B: words (lo.x|hi.x) (lo.y|hi.y) (lo.z|hi.z), f16 offsets from O,
 //                lo rounded down / hi rounded up so fp32(O + lo) <= exact lo, fp32(O + hi) >= exact hi
 //                (the paper's "round-to-nearest-not-lower", made exact for the decode).
-//                The offsets are >= 0, so their sign bits carry the child meta:
-//                lo.x sign = valid, lo.y sign = leaf, {lo.z, hi.x} signs = prim count - 1.
+//   Child metadata: nibble c = child c's size in units (0 none, 4 interior, 3 * count leaf); nibbles 0-2
+//   are the low 4 mantissa bits of O.x, O.y, O.z (the origin is chosen so), nibble 3 the top of word 3.
 //   A child block holds the node's children contiguously (first child implicit at `base`, like the
 //   paper's "first child is implicitly stored next"): interior children first (4 units
 //   each), then the leaves' primitives inline, 3 units (48 B) per primitive:

@@ -438,23 +438,24 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
                 const uint4 q0 = __ldg(pool + cur + 1), q1 = __ldg(pool + cur + 2), q2 = __ldg(pool + cur + 3);
                 const uint32_t w[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
                 const float O[3] = {__uint_as_float(h.x), __uint_as_float(h.y), __uint_as_float(h.z)};
-                uint32_t off = h.w;
+                // child sizes in units (nibbles: 0 none, 4 interior, 3 * count leaf), see pt_internal.h
+                const uint32_t meta = (h.x & 15u) | ((h.y & 15u) << 4) | ((h.z & 15u) << 8) | ((h.w >> 28) << 12);
+                uint32_t off = h.w & 0x0FFFFFFFu;
                 // per-child results in registers (static indices only: no local-memory arrays)
                 float ctn[4];
                 uint32_t cent[4];
 #pragma unroll
                 for (int ci = 0; ci < 4; ++ci) {
-                    const uint32_t w0 = w[3 * ci], w1 = w[3 * ci + 1], w2 = w[3 * ci + 2];
-                    const bool valid = (w0 & 0x8000u) != 0;
-                    const bool lf = (w1 & 0x8000u) != 0;
-                    const uint32_t cm1 = ((w2 >> 15) & 1u) | ((w0 >> 30) & 2u);
-                    const uint32_t wa[3] = {w0 & 0x7FFF7FFFu, w1 & 0x7FFF7FFFu, w2 & 0x7FFF7FFFu};
+                    const uint32_t nib = (meta >> (4 * ci)) & 15u;
+                    const bool valid = nib != 0u;
+                    const bool lf = nib != (uint32_t)kNodeUnits;
+                    const uint32_t cm1 = ((nib * 86u) >> 8) - 1u;       // count - 1 = nib / 3 - 1 for leaves
                     float tn = 0.0f, tf = CUDART_INF_F;
 #pragma unroll
                     for (int a = 0; a < 3; ++a) {
                         // (near, far) bounds of this axis: exact fp16 -> fp32, then the same rn ops as the
                         // builder's check (the half swap only reorders the two lanes)
-                        const uint32_t ws = __byte_perm(wa[a], 0u, swz[a]);
+                        const uint32_t ws = __byte_perm(w[3 * ci + a], 0u, swz[a]);
                         const float2 lh = __half22float2(*reinterpret_cast<const __half2*>(&ws));
                         const float2 b = __fadd2_rn(make_float2(O[a], O[a]), lh);
                         const float2 t = __fmul2_rn(__fadd2_rn(b, make_float2(-r.o[a], -r.o[a])),
@@ -466,7 +467,7 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
                     const bool hit = valid && tn <= tf && tn <= tcull0;
                     ctn[ci] = hit ? tn : CUDART_INF_F;
                     cent[ci] = lf ? (off | kLeafBit | (cm1 << 28)) : off;
-                    off += valid ? (lf ? kPrimUnits * (cm1 + 1u) : (uint32_t)kNodeUnits) : 0u;
+                    off += nib;
                 }
                 // sort the children by entry distance (network of 5 compare-swaps), push all but the
                 // nearest (farthest first), descend into the nearest

@@ -30,7 +30,7 @@ def test_f16_not_lower_worked_values(built):
 
 
 def _f16(bits):
-    return np.array([bits & 0x7FFF], np.uint16).view(np.float16).astype(np.float32)[0]
+    return np.array([bits & 0xFFFF], np.uint16).view(np.float16).astype(np.float32)[0]
 
 
 def _check_pool(sc, pool):
@@ -53,16 +53,21 @@ def _check_pool(sc, pool):
 
     def walk(unit):
         O = f32[unit, :3]
-        off = int(u32[unit, 3])
+        hw = int(u32[unit, 3])
+        off = hw & 0x0FFFFFFF
+        # child sizes in units: nibbles in the low mantissa bits of O.x, O.y, O.z and the top of word 3
+        nibs = [int(u32[unit, 0]) & 15, int(u32[unit, 1]) & 15, int(u32[unit, 2]) & 15, hw >> 28]
         words = u32[unit + 1: unit + 4].reshape(-1)
         lo_all = np.full(3, np.inf)
         hi_all = np.full(3, -np.inf)
         for ci in range(4):
-            w0, w1, w2 = int(words[3 * ci]), int(words[3 * ci + 1]), int(words[3 * ci + 2])
-            if not (w0 & 0x8000):
+            nib = nibs[ci]
+            if nib == 0:
                 continue
-            leaf = bool(w1 & 0x8000)
-            cnt = (((w2 >> 15) & 1) | ((w0 >> 30) & 2)) + 1
+            assert nib == 4 or nib in (3, 6, 9, 12), nib
+            leaf = nib != 4
+            cnt = nib // 3
+            w0, w1, w2 = int(words[3 * ci]), int(words[3 * ci + 1]), int(words[3 * ci + 2])
             qs = [w0, w1, w2, w0 >> 16, w1 >> 16, w2 >> 16]      # lo.x lo.y lo.z hi.x hi.y hi.z
             dlo = np.array([np.float32(O[a] + _f16(qs[a])) for a in range(3)], np.float64)
             dhi = np.array([np.float32(O[a] + _f16(qs[3 + a])) for a in range(3)], np.float64)
@@ -72,10 +77,9 @@ def _check_pool(sc, pool):
                     pid, plo, phi = prim_bounds(off + 3 * k)
                     seen[pid] += 1
                     blo, bhi = np.minimum(blo, plo), np.maximum(bhi, phi)
-                off += 3 * cnt
             else:
                 blo, bhi = walk(off)
-                off += 4
+            off += nib
             assert (dlo <= blo).all() and (dhi >= bhi).all(), (dlo, blo, dhi, bhi)
             lo_all, hi_all = np.minimum(lo_all, blo), np.maximum(hi_all, bhi)
         return lo_all, hi_all
