@@ -58,6 +58,7 @@ struct PathPool {
     float4* esc_beta = nullptr;
     float* wave_buf = nullptr;
     cudaEvent_t last_use = nullptr;
+    cudaStream_t host_stream = nullptr;   // stream of the host-buffer entry point pt_render (all scenes)
 };
 
 PathPool& path_pool(int dev) {
@@ -91,20 +92,18 @@ int ensure_pool(PathPool& pp, int64_t cap) {
 }
 
 void free_ws(pt::Workspace& ws) {
-    cudaFree(ws.counters);
     cudaFree(ws.fb);
-    cudaFree(ws.d_stats);
-    if (ws.own_stream) cudaStreamDestroy(ws.own_stream);
     ws = pt::Workspace();
 }
 
-// per-scene small state: counters, stats, scratch framebuffer stream
-int ensure_ws(pt::Workspace& ws) {
-    if (!ws.counters) {
-        CU(cudaMalloc(&ws.counters, sizeof(uint32_t) * pt::kCounters));
-        CU(cudaMalloc(&ws.d_stats, sizeof(unsigned long long) * 4));
-        CU(cudaMemset(ws.d_stats, 0, sizeof(unsigned long long) * 4));
-        CU(cudaStreamCreateWithFlags(&ws.own_stream, cudaStreamNonBlocking));
+// the scene's counters and stats live in its single device allocation (pt_scene_create); the
+// host-path stream is per device, created once
+int ensure_ws(pt_scene* sc) {
+    if (!sc->ws.own_stream) {
+        PathPool& pp = path_pool(sc->device);
+        std::lock_guard<std::mutex> lk(pp.mu);
+        if (!pp.host_stream) CU(cudaStreamCreateWithFlags(&pp.host_stream, cudaStreamNonBlocking));
+        sc->ws.own_stream = pp.host_stream;
     }
     return PT_OK;
 }
@@ -190,7 +189,7 @@ int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, i
     if (k <= 0) k = std::max<int64_t>(1, std::min<int64_t>(n_samples, (int64_t)(8 << 20) / np));
     k = std::min<int64_t>(k, n_samples);
     while (k > 1 && k * np > (1ll << 31)) --k;
-    int rc = ensure_ws(sc->ws);
+    int rc = ensure_ws(sc);
     if (rc) return rc;
     PathPool& pp = path_pool(sc->device);
     std::lock_guard<std::mutex> pool_lock(pp.mu);
@@ -340,41 +339,52 @@ int pt_scene_create(const pt_triangle* tris, int64_t n_tris, const pt_sphere* sp
         if (_e != cudaSuccess)                                                                           \
             return cleanup(_e == cudaErrorMemoryAllocation ? PT_ERR_OOM : PT_ERR_CUDA, cudaGetErrorString(_e)); \
     } while (0)
+    // one device allocation and one copy for everything the scene owns: BVH pool, shading vertices,
+    // spheres, materials, and the wave's counters and stats (256-B aligned sub-buffers)
     sc->pool_units = (int64_t)bvh.pool.size();
-    if (sc->pool_units > 0) {
-        CUS(cudaMalloc(&sc->d_pool, sizeof(uint4) * sc->pool_units));
-        CUS(cudaMemcpy(sc->d_pool, bvh.pool.data(), sizeof(uint4) * sc->pool_units, cudaMemcpyHostToDevice));
+    static_assert(sizeof(pt::DevMaterial) == sizeof(pt_material), "material layout");
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    const size_t b_pool = al(sizeof(uint4) * sc->pool_units), b_tri = al(sizeof(float4) * 3 * n_tris),
+                 b_sph = al(sizeof(float4) * n_spheres), b_smat = al(sizeof(uint32_t) * n_spheres),
+                 b_mat = al(sizeof(pt_material) * n_mats), b_cnt = al(sizeof(uint32_t) * pt::kCounters),
+                 b_st = al(sizeof(unsigned long long) * 4);
+    const size_t total = b_pool + b_tri + b_sph + b_smat + b_mat + b_cnt + b_st;
+    std::vector<uint8_t> host(total, 0);
+    size_t o = 0;
+    const size_t o_pool = o; o += b_pool;
+    const size_t o_tri = o; o += b_tri;
+    const size_t o_sph = o; o += b_sph;
+    const size_t o_smat = o; o += b_smat;
+    const size_t o_mat = o; o += b_mat;
+    const size_t o_cnt = o; o += b_cnt;
+    const size_t o_st = o;
+    if (sc->pool_units > 0) std::memcpy(&host[o_pool], bvh.pool.data(), sizeof(uint4) * sc->pool_units);
+    float4* tv = reinterpret_cast<float4*>(&host[o_tri]);
+    for (int64_t i = 0; i < n_tris; ++i) {
+        uint32_t mb = tris[i].material;
+        float mf;
+        std::memcpy(&mf, &mb, 4);
+        tv[3 * i + 0] = make_float4(tris[i].v0[0], tris[i].v0[1], tris[i].v0[2], mf);
+        tv[3 * i + 1] = make_float4(tris[i].v1[0], tris[i].v1[1], tris[i].v1[2], 0.0f);
+        tv[3 * i + 2] = make_float4(tris[i].v2[0], tris[i].v2[1], tris[i].v2[2], 0.0f);
     }
-    if (n_tris > 0) {
-        std::vector<float4> tv(3 * n_tris);
-        for (int64_t i = 0; i < n_tris; ++i) {
-            uint32_t mb = tris[i].material;
-            float mf;
-            std::memcpy(&mf, &mb, 4);
-            tv[3 * i + 0] = make_float4(tris[i].v0[0], tris[i].v0[1], tris[i].v0[2], mf);
-            tv[3 * i + 1] = make_float4(tris[i].v1[0], tris[i].v1[1], tris[i].v1[2], 0.0f);
-            tv[3 * i + 2] = make_float4(tris[i].v2[0], tris[i].v2[1], tris[i].v2[2], 0.0f);
-        }
-        CUS(cudaMalloc(&sc->d_tri_v, sizeof(float4) * tv.size()));
-        CUS(cudaMemcpy(sc->d_tri_v, tv.data(), sizeof(float4) * tv.size(), cudaMemcpyHostToDevice));
+    float4* sv = reinterpret_cast<float4*>(&host[o_sph]);
+    uint32_t* sm = reinterpret_cast<uint32_t*>(&host[o_smat]);
+    for (int64_t i = 0; i < n_spheres; ++i) {
+        sv[i] = make_float4(spheres[i].center[0], spheres[i].center[1], spheres[i].center[2], spheres[i].radius);
+        sm[i] = spheres[i].material;
     }
-    if (n_spheres > 0) {
-        std::vector<float4> sv(n_spheres);
-        std::vector<uint32_t> sm(n_spheres);
-        for (int64_t i = 0; i < n_spheres; ++i) {
-            sv[i] = make_float4(spheres[i].center[0], spheres[i].center[1], spheres[i].center[2], spheres[i].radius);
-            sm[i] = spheres[i].material;
-        }
-        CUS(cudaMalloc(&sc->d_sph, sizeof(float4) * n_spheres));
-        CUS(cudaMemcpy(sc->d_sph, sv.data(), sizeof(float4) * n_spheres, cudaMemcpyHostToDevice));
-        CUS(cudaMalloc(&sc->d_sph_mat, sizeof(uint32_t) * n_spheres));
-        CUS(cudaMemcpy(sc->d_sph_mat, sm.data(), sizeof(uint32_t) * n_spheres, cudaMemcpyHostToDevice));
-    }
-    if (n_mats > 0) {
-        static_assert(sizeof(pt::DevMaterial) == sizeof(pt_material), "material layout");
-        CUS(cudaMalloc(&sc->d_mats, sizeof(pt_material) * n_mats));
-        CUS(cudaMemcpy(sc->d_mats, mats, sizeof(pt_material) * n_mats, cudaMemcpyHostToDevice));
-    }
+    if (n_mats > 0) std::memcpy(&host[o_mat], mats, sizeof(pt_material) * n_mats);
+    CUS(cudaMalloc(&sc->d_alloc, total));
+    CUS(cudaMemcpy(sc->d_alloc, host.data(), total, cudaMemcpyHostToDevice));
+    uint8_t* base = static_cast<uint8_t*>(sc->d_alloc);
+    sc->d_pool = sc->pool_units > 0 ? reinterpret_cast<uint4*>(base + o_pool) : nullptr;
+    sc->d_tri_v = n_tris > 0 ? reinterpret_cast<float4*>(base + o_tri) : nullptr;
+    sc->d_sph = n_spheres > 0 ? reinterpret_cast<float4*>(base + o_sph) : nullptr;
+    sc->d_sph_mat = n_spheres > 0 ? reinterpret_cast<uint32_t*>(base + o_smat) : nullptr;
+    sc->d_mats = n_mats > 0 ? reinterpret_cast<pt::DevMaterial*>(base + o_mat) : nullptr;
+    sc->ws.counters = reinterpret_cast<uint32_t*>(base + o_cnt);
+    sc->ws.d_stats = reinterpret_cast<unsigned long long*>(base + o_st);
 #undef CUS
     *out = sc;
     return PT_OK;
@@ -385,7 +395,7 @@ int pt_scene_destroy(pt_scene* sc) {
     {
         std::lock_guard<std::mutex> lk(sc->mu);
         collect_timers(sc);
-        cudaFree(sc->d_pool); cudaFree(sc->d_tri_v); cudaFree(sc->d_sph); cudaFree(sc->d_sph_mat); cudaFree(sc->d_mats);
+        cudaFree(sc->d_alloc);
         free_ws(sc->ws);
     }
     delete sc;
@@ -411,10 +421,13 @@ int pt_nif_load_ex(int32_t kind, const uint16_t* blob, int64_t n_halves, pt_nif*
     n->kind = kind;
     cudaGetDevice(&n->device);
     n->smem_bytes = (int64_t)img.size();
+    // one allocation and one copy: the kernel's shared-memory image, then the raw blob
+    const size_t b_img = (img.size() + 255) & ~size_t(255);
+    img.resize(b_img + sizeof(uint16_t) * n_halves, 0);
+    std::memcpy(&img[b_img], blob, sizeof(uint16_t) * n_halves);
     cudaError_t e = cudaMalloc(&n->d_smem_image, img.size());
     if (e == cudaSuccess) e = cudaMemcpy(n->d_smem_image, img.data(), img.size(), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMalloc(&n->d_blob, sizeof(uint16_t) * n_halves);
-    if (e == cudaSuccess) e = cudaMemcpy(n->d_blob, blob, sizeof(uint16_t) * n_halves, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) n->d_blob = reinterpret_cast<uint16_t*>(static_cast<uint8_t*>(n->d_smem_image) + b_img);
     if (e != cudaSuccess) {
         pt_nif_destroy(n);
         return fail(e == cudaErrorMemoryAllocation ? PT_ERR_OOM : PT_ERR_CUDA, cudaGetErrorString(e));
@@ -462,7 +475,7 @@ int pt_nif_destroy(pt_nif* n) {
     if (!n) return PT_OK;
     pt::mlp_free(n);
     cudaFree(n->d_smem_image);
-    cudaFree(n->d_blob);
+    // (d_blob lives inside the d_smem_image allocation)
     delete n;
     return PT_OK;
 }
@@ -483,7 +496,7 @@ int pt_render(const pt_scene* scene, const pt_nif* nif, const float env_rgb[3], 
     if (width < 1 || height < 1 || spp < 1 || max_depth < 1) return fail(PT_ERR_INVALID_ARG, "W, H, spp, max_depth >= 1");
     pt_scene* sc = const_cast<pt_scene*>(scene);
     std::lock_guard<std::mutex> lk(sc->mu);
-    int rc = ensure_ws(sc->ws);
+    int rc = ensure_ws(sc);
     if (rc) return rc;
     const int64_t n = (int64_t)width * height * 3;
     if (sc->ws.fb_capacity < n) {

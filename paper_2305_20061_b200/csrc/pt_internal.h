@@ -65,7 +65,7 @@ struct Workspace {
     uint32_t* counters = nullptr;  // [kCounters]
     int64_t fb_capacity = 0;
     float* fb = nullptr;       // scratch framebuffer for pt_render (host-output path)
-    cudaStream_t own_stream = nullptr;
+    cudaStream_t own_stream = nullptr;      // the device's host-path stream (not owned)
     unsigned long long* d_stats = nullptr;  // [paths, segments, escaped, -] accumulated per call
 };
 struct TimedLaunch {
@@ -88,6 +88,7 @@ struct pt_scene {
     int64_t n_tris = 0, n_sph = 0;
     int32_t n_mats = 0;
     pt_camera cam{};
+    void* d_alloc = nullptr;          // the scene's single device allocation (all arrays below)
     uint4* d_pool = nullptr;          // wide BVH + inline primitives
     int64_t pool_units = 0;
     bool empty = true;
