@@ -79,11 +79,9 @@ int ensure_pool(PathPool& pp, int64_t cap) {
     pp.esc = pp.esc_beta = nullptr;
     pp.wave_buf = nullptr;
     pp.capacity = 0;
-    for (int b = 0; b < 2; ++b) {
-        CU(cudaMalloc(&pp.rayA[b], sizeof(float4) * cap));
-        CU(cudaMalloc(&pp.rayB[b], sizeof(float4) * cap));
-        CU(cudaMalloc(&pp.rayC[b], sizeof(float2) * cap));
-    }
+    CU(cudaMalloc(&pp.rayA[0], sizeof(float4) * cap));
+    CU(cudaMalloc(&pp.rayB[0], sizeof(float4) * cap));
+    CU(cudaMalloc(&pp.rayC[0], sizeof(float2) * cap));
     CU(cudaMalloc(&pp.esc, sizeof(float4) * cap));
     CU(cudaMalloc(&pp.esc_beta, sizeof(float4) * cap));
     CU(cudaMalloc(&pp.wave_buf, sizeof(float) * 3 * cap));
@@ -158,22 +156,14 @@ void collect_timers(pt_scene* sc) {
     sc->pending.clear();
 }
 
-__global__ void stats_kernel(const uint32_t* counters, int max_depth, unsigned long long* acc) {
-    unsigned long long seg = 0;
-    for (int d = 0; d < max_depth; ++d) seg += counters[2 * d];
+__global__ void stats_kernel(const uint32_t* counters, unsigned long long* acc) {
     acc[0] += counters[0];
-    acc[1] += seg;
+    acc[1] += counters[pt::kCounterSeg];
     acc[2] += counters[pt::kCounterEsc];
 }
 
 __global__ void set_count_kernel(uint32_t* c, uint32_t v) { *c = v; }
 
-// total escaped paths of the wave (the NIF's row count) from the bounces' packed queue counters
-__global__ void escaped_total_kernel(uint32_t* counters, int max_depth) {
-    uint32_t e = 0;
-    for (int d = 1; d <= max_depth; ++d) e += counters[2 * d + 1];
-    counters[pt::kCounterEsc] = e;
-}
 
 int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, int W, int H, int first_sample,
                         int n_samples, int max_depth, uint64_t seed, int wave_samples, float* d_accum,
@@ -221,16 +211,11 @@ int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, i
         CU(cudaMemsetAsync(ws.counters, 0, sizeof(uint32_t) * pt::kCounters, st));
         set_count_kernel<<<1, 1, 0, st>>>(ws.counters + 0, (uint32_t)slots);
         cudaEvent_t e0;
-        for (int d = 1; d <= max_depth; ++d) {
-            const int buf = (d - 1) & 1;       // bounce d reads state buffer buf, shade writes buf ^ 1
-            tm.begin(T_TRAVERSE, &e0);
-            pt::launch_trace_shade(tp, cam, W, H, (int)w0, d, max_depth, seed, buf, use_nif, env, ws, st);
-            tm.end(T_TRAVERSE, e0);
-            stats.launches += 1;
-            stats.traverse_launches += 1;
-        }
-        escaped_total_kernel<<<1, 1, 0, st>>>(ws.counters, max_depth);
-        stats.launches += 1;
+        tm.begin(T_TRAVERSE, &e0);
+        pt::launch_paths(tp, cam, W, H, (int)w0, max_depth, seed, use_nif, env, ws, st);
+        tm.end(T_TRAVERSE, e0);
+        stats.launches += max_depth > 1 ? 2 : 1;
+        stats.traverse_launches += max_depth > 1 ? 2 : 1;
         if (use_nif) {
             tm.begin(T_NIF, &e0);
             cudaError_t e = pt::launch_nif(nif, ws.esc, ws.esc_beta, ws.counters + pt::kCounterEsc, slots, ws.wave_buf, 1, st);
@@ -242,7 +227,7 @@ int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, i
         tm.begin(T_ACCUM, &e0);
         pt::launch_accumulate(ws.wave_buf, (int)np, (int)kk, d_accum, st);
         tm.end(T_ACCUM, e0);
-        stats_kernel<<<1, 1, 0, st>>>(ws.counters, max_depth, d_stats);
+        stats_kernel<<<1, 1, 0, st>>>(ws.counters, d_stats);
         stats.launches += 3;   // set_count, accumulate, stats
         stats.waves += 1;
     }

@@ -56,7 +56,7 @@ double f16_value(uint16_t h);
 struct Workspace {
     int64_t capacity = 0;      // path slots
     // live-path state in queue order, double buffered (in/out of each bounce):
-    float4* rayA[2] = {nullptr, nullptr};   // (o.xyz, slot bits)
+    float4* rayA[2] = {nullptr, nullptr};   // (o.xyz, slot bits) -- [0]: the first bounce's survivors
     float4* rayB[2] = {nullptr, nullptr};   // (d.xyz, beta.x)
     float2* rayC[2] = {nullptr, nullptr};   // (beta.y, beta.z)
     float4* esc = nullptr;     // [cap] escaped-ray queue: (d.xyz, slot bits); the NIF maps d to (u, v)
@@ -80,6 +80,8 @@ constexpr int kCounters = 192;
 constexpr int kCounterEsc = 128;
 constexpr int kCounterErr = 129;
 constexpr int kCounterWork = 130;
+constexpr int kCounterSeg = 132;   // traced segments of the wave
+constexpr int kCounterAlive = 133; // paths alive after the first bounce
 
 }  // namespace pt
 
@@ -145,8 +147,8 @@ struct TraceParams {
 };
 
 // kernel launchers (trace_kernels.cu)
-void launch_trace_shade(const TraceParams& tp, const Cam32& cam, int W, int H, int first_sample, int depth, int max_depth,
-                        uint64_t seed, int buf, int use_nif, float3 env, Workspace& ws, cudaStream_t st);
+void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int first_sample, int max_depth, uint64_t seed,
+                  int use_nif, float3 env, Workspace& ws, cudaStream_t st);
 void launch_accumulate(const float* wave_buf, int n_pix, int k, float* fb, cudaStream_t st);
 void launch_primary(const TraceParams& tp, const Cam32& cam, int W, int H, int sample, uint64_t seed,
                     int32_t* prim, float* t, cudaStream_t st);

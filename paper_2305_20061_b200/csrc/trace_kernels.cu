@@ -523,26 +523,6 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
 // ---------------------------------------------------------------------------------------------
 // Kernels
 // ---------------------------------------------------------------------------------------------
-// Ray state is kept in queue order (compacted every bounce) so every kernel reads and writes it
-// coalesced: A = (o.xyz, slot), B = (d.xyz, beta.x), C = (beta.y, beta.z)  -- 40 B per live path.
-// (The first bounce computes its camera rays itself: S1 raygen is fused into trace_shade_kernel.)
-
-// warp-aggregated append to the alive and the escaped queue at once: one 64-bit atomic per warp on the
-// bounce's packed counter (low: alive, high: escaped); returns this lane's positions in both queues
-__device__ __forceinline__ void warp_append2(bool alive, bool escaped, unsigned long long* counter, uint32_t& pos_a,
-                                             uint32_t& pos_e) {
-    const uint32_t ma = __ballot_sync(0xFFFFFFFFu, alive), me = __ballot_sync(0xFFFFFFFFu, escaped);
-    if ((ma | me) == 0) return;
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(ma | me) - 1;
-    unsigned long long base = 0;
-    if (lane == leader)
-        base = atomicAdd(counter, ((unsigned long long)__popc(me) << 32) | (unsigned long long)__popc(ma));
-    base = __shfl_sync(0xFFFFFFFFu, base, leader);
-    const uint32_t lt = (1u << lane) - 1u;
-    pos_a = (uint32_t)base + (uint32_t)__popc(ma & lt);
-    pos_e = (uint32_t)(base >> 32) + (uint32_t)__popc(me & lt);
-}
 
 struct ShadeArgs {
     TraceParams tp;
@@ -550,193 +530,280 @@ struct ShadeArgs {
     int W, H, first_sample, depth, max_depth;
     uint2 key;
     const uint32_t* counters;   // the wave's counters (pt_internal.h kCounters layout)
-    unsigned long long* q_out;  // packed queue counter of this bounce
-    uint32_t* work;
+    uint32_t* work;             // fetch counter of the kernel
+    uint32_t* alive_count;      // paths alive after the first bounce (its output queue length)
+    uint32_t* esc_count;        // escaped-queue length
+    uint32_t* seg_count;        // traced segments
     int use_nif;
     float3 env;
-    const float4* A_in;
-    const float4* B_in;
-    const float2* C_in;
-    float4* A_out;
-    float4* B_out;
-    float2* C_out;
+    // path state after the first bounce, in queue order: (o.xyz, slot), (d.xyz, beta.x), (beta.y, beta.z)
+    float4* qA;
+    float4* qB;
+    float2* qC;
     float4* esc;
     float4* esc_beta;
     float* wave_buf;
 };
 
-// One bounce of the wavefront for every live path: closest hit over the wide BVH (S2), then emission,
-// BSDF sampling, Russian roulette (S3) and warp-aggregated compaction into the next live queue or
-// the escaped-ray queue of the NIF (S4). Fused so the path state is read once and written once.
-#ifndef PT_TS_MINB
-#define PT_TS_MINB 7   // min resident blocks per SM for trace_shade: 72-register cap; tools/ts_tune.sh on B200
-#endif
-__global__ void __launch_bounds__(128, PT_TS_MINB) trace_shade_kernel(ShadeArgs a) {
-    const uint32_t n = a.counters[2 * (a.depth - 1)];          // alive paths of the previous bounce
-    // this bounce's escaped paths follow those of the earlier bounces in the escaped queue
-    uint32_t esc_base = 0;
-    for (int d = 1; d < a.depth; ++d) esc_base += a.counters[2 * d + 1];
+// One segment of one path: closest hit over the wide BVH (S2), then emission, BSDF sampling and
+// Russian roulette (S3). `depth` counts this segment (reading R7).
+struct SegOut {
+    bool alive, escaped, done;
+    float3 o, d, beta, L;
+};
+
+__device__ __forceinline__ void shade_segment(const ShadeArgs& a, int depth, uint32_t slot, float3 o, float3 d,
+                                              float3 bt, SegOut& r) {
     const int np = a.W * a.H;
-    const int lane_id = threadIdx.x & 31;
-    // dynamic work fetching, 32 paths per warp and fetch (one atomic): no static partition, so the SMs
-    // finish a bounce together instead of waiting for the slowest grid-stride share
-    for (;;) {
-        uint32_t base = 0;
-        if (lane_id == 0) base = atomicAdd(a.work, 32u);
-        base = __shfl_sync(0xFFFFFFFFu, base, 0);
-        if (base >= n) break;
-        const uint32_t i = base + (uint32_t)lane_id;
-        const bool active = i < n;
-        bool alive = false, escaped = false;
-        uint32_t slot = 0;
-        float3 o3 = make_float3(0, 0, 0), wi = make_float3(0, 0, 0), bt = make_float3(0, 0, 0);
-        if (active) {
-            float4 o, d4;
-            float2 c2;
-            if (a.depth == 1) {
-                // S1 raygen fused into the first bounce: the wave's slot i is (pixel i % np, sample
-                // first + i / np); the camera ray is recomputed here instead of round-tripping 40 B per
-                // path through HBM
-                const int p = (int)(i % (uint32_t)np);
-                const int sm = a.first_sample + (int)(i / (uint32_t)np);
-                const uint4 r = philox10(make_uint4((uint32_t)p, (uint32_t)sm, 0u, 0u), a.key);
-                const float3 dc = cam_dir(a.cam, a.W, a.H, p % a.W, p / a.W, u01f(r.x), u01f(r.y));
-                o = make_float4(a.cam.eye[0], a.cam.eye[1], a.cam.eye[2], __uint_as_float(i));
-                d4 = make_float4(dc.x, dc.y, dc.z, 1.0f);
-                c2 = make_float2(1.0f, 1.0f);
-            } else {
-                o = __ldg(a.A_in + i);
-                d4 = __ldg(a.B_in + i);
-                c2 = __ldg(a.C_in + i);
-            }
-            const Hit hh = closest_hit(a.tp, make_float3(o.x, o.y, o.z), make_float3(d4.x, d4.y, d4.z));
-            const int32_t prim = hh.prim;
-            slot = __float_as_uint(o.w);
-            const float3 d = make_float3(d4.x, d4.y, d4.z);
-            bt = make_float3(d4.w, c2.x, c2.y);
-            float3 L = make_float3(0, 0, 0);
-            bool done = true;
-            if (prim < 0) {                                   // escaped: environment light
-                if (a.use_nif) {
-                    // queued by direction; the NIF kernel maps it to equirect (u, v) (S4 -> S5)
-                    wi = d;
-                    escaped = true;
-                    done = false;
-                } else {
-                    L = make_float3(bt.x * a.env.x, bt.y * a.env.y, bt.z * a.env.z);
-                }
-            } else {
-                const float t = (float)hh.t;
-                const float3 P = make_float3(fmaf(t, d.x, o.x), fmaf(t, d.y, o.y), fmaf(t, d.z, o.z));
-                float3 ng;
-                uint32_t mi;
-                if (prim < a.tp.n_tris) {
-                    const float4 v0 = __ldg(a.tp.tri_v + 3 * prim), v1 = __ldg(a.tp.tri_v + 3 * prim + 1),
-                                 v2 = __ldg(a.tp.tri_v + 3 * prim + 2);
-                    const float3 e1 = make_float3(v1.x - v0.x, v1.y - v0.y, v1.z - v0.z);
-                    const float3 e2 = make_float3(v2.x - v0.x, v2.y - v0.y, v2.z - v0.z);
-                    ng = make_float3(e1.y * e2.z - e1.z * e2.y, e1.z * e2.x - e1.x * e2.z, e1.x * e2.y - e1.y * e2.x);
-                    const float il = rsqrtf(ng.x * ng.x + ng.y * ng.y + ng.z * ng.z);
-                    ng = make_float3(ng.x * il, ng.y * il, ng.z * il);
-                    mi = __float_as_uint(v0.w);
-                } else {
-                    const int si = prim - (int)a.tp.n_tris;
-                    const float4 s = __ldg(a.tp.sph + si);
-                    const float ir = 1.0f / s.w;
-                    ng = make_float3((P.x - s.x) * ir, (P.y - s.y) * ir, (P.z - s.z) * ir);
-                    mi = __ldg(a.tp.sph_mat + si);
-                }
-                const DevMaterial m = a.tp.mats[mi];
-                const float cosd = d.x * ng.x + d.y * ng.y + d.z * ng.z;
-                if (m.kind == PT_EMISSIVE) {
-                    if (cosd < 0.0f) L = make_float3(bt.x * m.emission[0], bt.y * m.emission[1], bt.z * m.emission[2]);
-                } else if (a.depth < a.max_depth) {
-                    const int p = (int)(slot % (uint32_t)np);
-                    const int s = a.first_sample + (int)(slot / (uint32_t)np);
-                    const uint4 rr = philox10(make_uint4((uint32_t)p, (uint32_t)s, (uint32_t)a.depth, 0u), a.key);
-                    const float xi0 = u01f(rr.x), xi1 = u01f(rr.y), xi2 = u01f(rr.z), xi3 = u01f(rr.w);
-                    const bool entering = cosd < 0.0f;
-                    const float3 n = entering ? ng : make_float3(-ng.x, -ng.y, -ng.z);
-                    float side = 1.0f;
-                    if (m.kind == PT_LAMBERT) {
-                        // cosine-weighted hemisphere, ONB of Duff et al. 2017 (reading R9)
-                        const float sg = copysignf(1.0f, n.z);
-                        const float aa = -1.0f / (sg + n.z);
-                        const float bb = n.x * n.y * aa;
-                        const float3 t1 = make_float3(1.0f + sg * n.x * n.x * aa, sg * bb, -sg * n.x);
-                        const float3 t2 = make_float3(bb, sg + n.y * n.y * aa, -n.y);
-                        float sphi, cphi;
-                        sincospif(2.0f * xi1, &sphi, &cphi);   // sin/cos(2 pi xi1), cheap exact-argument reduction
-                        const float rho = sqrtf(xi0), c3 = sqrtf(1.0f - xi0);
-                        const float c1 = rho * cphi, c2 = rho * sphi;
-                        wi = make_float3(c1 * t1.x + c2 * t2.x + c3 * n.x, c1 * t1.y + c2 * t2.y + c3 * n.y,
-                                         c1 * t1.z + c2 * t2.z + c3 * n.z);
-                        bt = make_float3(bt.x * m.albedo[0], bt.y * m.albedo[1], bt.z * m.albedo[2]);
-                    } else if (m.kind == PT_MIRROR) {
-                        const float dn = d.x * n.x + d.y * n.y + d.z * n.z;
-                        wi = make_float3(d.x - 2.0f * dn * n.x, d.y - 2.0f * dn * n.y, d.z - 2.0f * dn * n.z);
-                        bt = make_float3(bt.x * m.albedo[0], bt.y * m.albedo[1], bt.z * m.albedo[2]);
-                    } else {
-                        // dielectric, Schlick Fresnel, TIR -> F = 1 (reading R9)
-                        const float eta = entering ? 1.0f / m.ior : m.ior;
-                        const float cosi = -(d.x * n.x + d.y * n.y + d.z * n.z);
-                        const float sin2t = eta * eta * (1.0f - cosi * cosi);
-                        float F = 1.0f, cost = 0.0f;
-                        if (sin2t <= 1.0f) {
-                            cost = sqrtf(1.0f - sin2t);
-                            const float c = entering ? cosi : cost;
-                            float r0 = (1.0f - m.ior) / (1.0f + m.ior);
-                            r0 = r0 * r0;
-                            const float mm = 1.0f - c;
-                            F = r0 + (1.0f - r0) * (mm * mm * mm * mm * mm);
-                        }
-                        if (xi2 < F) {
-                            wi = make_float3(d.x + 2.0f * cosi * n.x, d.y + 2.0f * cosi * n.y, d.z + 2.0f * cosi * n.z);
-                        } else {
-                            const float k = eta * cosi - cost;
-                            wi = make_float3(eta * d.x + k * n.x, eta * d.y + k * n.y, eta * d.z + k * n.z);
-                            side = -1.0f;
-                        }
-                    }
-                    const float il = rsqrtf(wi.x * wi.x + wi.y * wi.y + wi.z * wi.z);
-                    wi = make_float3(wi.x * il, wi.y * il, wi.z * il);
-                    // spawn with normal offset on the side wi leaves to (reading R10)
-                    const float pm = fmaxf(1.0f, fmaxf(fabsf(P.x), fmaxf(fabsf(P.y), fabsf(P.z))));
-                    const float eps = 1e-4f * pm * side;
-                    o3 = make_float3(P.x + eps * n.x, P.y + eps * n.y, P.z + eps * n.z);
-                    alive = true;
-                    done = false;
-                    // Russian roulette from depth 3, q = min(1, max beta) (reading R8)
-                    if (a.depth >= 3) {
-                        const float q = fminf(1.0f, fmaxf(bt.x, fmaxf(bt.y, bt.z)));
-                        if (xi3 >= q) {
-                            alive = false;
-                            done = true;
-                        } else {
-                            bt = make_float3(bt.x / q, bt.y / q, bt.z / q);
-                        }
-                    }
-                }
-            }
-            if (done) {
-                a.wave_buf[3 * (size_t)slot + 0] = L.x;
-                a.wave_buf[3 * (size_t)slot + 1] = L.y;
-                a.wave_buf[3 * (size_t)slot + 2] = L.z;
-            }
+    r.alive = false;
+    r.escaped = false;
+    r.done = true;
+    r.L = make_float3(0, 0, 0);
+    r.beta = bt;
+    r.d = d;
+    r.o = o;
+    const Hit hh = closest_hit(a.tp, o, d);
+    const int32_t prim = hh.prim;
+    if (prim < 0) {                                   // escaped: environment light
+        if (a.use_nif) {
+            // queued by direction; the NIF kernel maps it to equirect (u, v) (S4 -> S5)
+            r.escaped = true;
+            r.done = false;
+        } else {
+            r.L = make_float3(bt.x * a.env.x, bt.y * a.env.y, bt.z * a.env.z);
         }
-        uint32_t pos_a = 0, pos_e = 0;
-        warp_append2(alive, escaped, a.q_out, pos_a, pos_e);
-        pos_e += esc_base;
-        if (alive) {
-            a.A_out[pos_a] = make_float4(o3.x, o3.y, o3.z, __uint_as_float(slot));
-            a.B_out[pos_a] = make_float4(wi.x, wi.y, wi.z, bt.x);
-            a.C_out[pos_a] = make_float2(bt.y, bt.z);
+        return;
+    }
+    const float t = (float)hh.t;
+    const float3 P = make_float3(fmaf(t, d.x, o.x), fmaf(t, d.y, o.y), fmaf(t, d.z, o.z));
+    float3 ng;
+    uint32_t mi;
+    if (prim < a.tp.n_tris) {
+        const float4 v0 = __ldg(a.tp.tri_v + 3 * prim), v1 = __ldg(a.tp.tri_v + 3 * prim + 1),
+                     v2 = __ldg(a.tp.tri_v + 3 * prim + 2);
+        const float3 e1 = make_float3(v1.x - v0.x, v1.y - v0.y, v1.z - v0.z);
+        const float3 e2 = make_float3(v2.x - v0.x, v2.y - v0.y, v2.z - v0.z);
+        ng = make_float3(e1.y * e2.z - e1.z * e2.y, e1.z * e2.x - e1.x * e2.z, e1.x * e2.y - e1.y * e2.x);
+        const float il = rsqrtf(ng.x * ng.x + ng.y * ng.y + ng.z * ng.z);
+        ng = make_float3(ng.x * il, ng.y * il, ng.z * il);
+        mi = __float_as_uint(v0.w);
+    } else {
+        const int si = prim - (int)a.tp.n_tris;
+        const float4 s = __ldg(a.tp.sph + si);
+        const float ir = 1.0f / s.w;
+        ng = make_float3((P.x - s.x) * ir, (P.y - s.y) * ir, (P.z - s.z) * ir);
+        mi = __ldg(a.tp.sph_mat + si);
+    }
+    const DevMaterial m = a.tp.mats[mi];
+    const float cosd = d.x * ng.x + d.y * ng.y + d.z * ng.z;
+    if (m.kind == PT_EMISSIVE) {
+        if (cosd < 0.0f) r.L = make_float3(bt.x * m.emission[0], bt.y * m.emission[1], bt.z * m.emission[2]);
+        return;
+    }
+    if (depth >= a.max_depth) return;                 // capped: no further segment, no env (reading R7)
+    const int p = (int)(slot % (uint32_t)np);
+    const int s = a.first_sample + (int)(slot / (uint32_t)np);
+    const uint4 rr = philox10(make_uint4((uint32_t)p, (uint32_t)s, (uint32_t)depth, 0u), a.key);
+    const float xi0 = u01f(rr.x), xi1 = u01f(rr.y), xi2 = u01f(rr.z), xi3 = u01f(rr.w);
+    const bool entering = cosd < 0.0f;
+    const float3 n = entering ? ng : make_float3(-ng.x, -ng.y, -ng.z);
+    float side = 1.0f;
+    float3 wi;
+    if (m.kind == PT_LAMBERT) {
+        // cosine-weighted hemisphere, ONB of Duff et al. 2017 (reading R9)
+        const float sg = copysignf(1.0f, n.z);
+        const float aa = -1.0f / (sg + n.z);
+        const float bb = n.x * n.y * aa;
+        const float3 t1 = make_float3(1.0f + sg * n.x * n.x * aa, sg * bb, -sg * n.x);
+        const float3 t2 = make_float3(bb, sg + n.y * n.y * aa, -n.y);
+        float sphi, cphi;
+        sincospif(2.0f * xi1, &sphi, &cphi);   // sin/cos(2 pi xi1), cheap exact-argument reduction
+        const float rho = sqrtf(xi0), c3 = sqrtf(1.0f - xi0);
+        const float c1 = rho * cphi, c2 = rho * sphi;
+        wi = make_float3(c1 * t1.x + c2 * t2.x + c3 * n.x, c1 * t1.y + c2 * t2.y + c3 * n.y,
+                         c1 * t1.z + c2 * t2.z + c3 * n.z);
+        bt = make_float3(bt.x * m.albedo[0], bt.y * m.albedo[1], bt.z * m.albedo[2]);
+    } else if (m.kind == PT_MIRROR) {
+        const float dn = d.x * n.x + d.y * n.y + d.z * n.z;
+        wi = make_float3(d.x - 2.0f * dn * n.x, d.y - 2.0f * dn * n.y, d.z - 2.0f * dn * n.z);
+        bt = make_float3(bt.x * m.albedo[0], bt.y * m.albedo[1], bt.z * m.albedo[2]);
+    } else {
+        // dielectric, Schlick Fresnel, TIR -> F = 1 (reading R9)
+        const float eta = entering ? 1.0f / m.ior : m.ior;
+        const float cosi = -(d.x * n.x + d.y * n.y + d.z * n.z);
+        const float sin2t = eta * eta * (1.0f - cosi * cosi);
+        float F = 1.0f, cost = 0.0f;
+        if (sin2t <= 1.0f) {
+            cost = sqrtf(1.0f - sin2t);
+            const float c = entering ? cosi : cost;
+            float r0 = (1.0f - m.ior) / (1.0f + m.ior);
+            r0 = r0 * r0;
+            const float mm = 1.0f - c;
+            F = r0 + (1.0f - r0) * (mm * mm * mm * mm * mm);
         }
-        if (escaped) {
-            a.esc[pos_e] = make_float4(wi.x, wi.y, wi.z, __uint_as_float(slot));
-            a.esc_beta[pos_e] = make_float4(bt.x, bt.y, bt.z, 0.0f);
+        if (xi2 < F) {
+            wi = make_float3(d.x + 2.0f * cosi * n.x, d.y + 2.0f * cosi * n.y, d.z + 2.0f * cosi * n.z);
+        } else {
+            const float k = eta * cosi - cost;
+            wi = make_float3(eta * d.x + k * n.x, eta * d.y + k * n.y, eta * d.z + k * n.z);
+            side = -1.0f;
         }
     }
+    const float il = rsqrtf(wi.x * wi.x + wi.y * wi.y + wi.z * wi.z);
+    wi = make_float3(wi.x * il, wi.y * il, wi.z * il);
+    // spawn with normal offset on the side wi leaves to (reading R10)
+    const float pm = fmaxf(1.0f, fmaxf(fabsf(P.x), fmaxf(fabsf(P.y), fabsf(P.z))));
+    const float eps = 1e-4f * pm * side;
+    r.o = make_float3(P.x + eps * n.x, P.y + eps * n.y, P.z + eps * n.z);
+    r.d = wi;
+    r.alive = true;
+    r.done = false;
+    // Russian roulette from depth 3, q = min(1, max beta) (reading R8)
+    if (depth >= 3) {
+        const float q = fminf(1.0f, fmaxf(bt.x, fmaxf(bt.y, bt.z)));
+        if (xi3 >= q) {
+            r.alive = false;
+            r.done = true;
+            return;
+        }
+        bt = make_float3(bt.x / q, bt.y / q, bt.z / q);
+    }
+    r.beta = bt;
+}
+
+// The camera ray of wave slot i = (pixel i % np, sample first + i / np) (S1, reading R22)
+__device__ __forceinline__ float3 camera_ray(const ShadeArgs& a, uint32_t i) {
+    const int np = a.W * a.H;
+    const int p = (int)(i % (uint32_t)np);
+    const int sm = a.first_sample + (int)(i / (uint32_t)np);
+    const uint4 r = philox10(make_uint4((uint32_t)p, (uint32_t)sm, 0u, 0u), a.key);
+    return cam_dir(a.cam, a.W, a.H, p % a.W, p / a.W, u01f(r.x), u01f(r.y));
+}
+
+#ifndef PT_TS_MINB
+#define PT_TS_MINB 7   // min resident blocks per SM for the path kernels: 72-register cap; tools/ts_tune.sh
+#endif
+
+// Warp-aggregated append (one atomic per warp), returns this lane's position
+__device__ __forceinline__ uint32_t warp_append(bool pred, uint32_t* counter) {
+    const uint32_t mask = __ballot_sync(0xFFFFFFFFu, pred);
+    if (mask == 0) return 0;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(mask) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(counter, (uint32_t)__popc(mask));
+    base = __shfl_sync(0xFFFFFFFFu, base, leader);
+    return base + (uint32_t)__popc(mask & ((1u << lane) - 1u));
+}
+
+__device__ __forceinline__ void append_escaped(const ShadeArgs& a, const SegOut& r, uint32_t slot) {
+    const uint32_t pos = warp_append(r.escaped, a.esc_count);
+    if (r.escaped) {
+        a.esc[pos] = make_float4(r.d.x, r.d.y, r.d.z, __uint_as_float(slot));
+        a.esc_beta[pos] = make_float4(r.beta.x, r.beta.y, r.beta.z, 0.0f);
+    }
+}
+
+__device__ __forceinline__ void write_radiance(const ShadeArgs& a, const SegOut& r, uint32_t slot) {
+    if (r.done) {
+        a.wave_buf[3 * (size_t)slot + 0] = r.L.x;
+        a.wave_buf[3 * (size_t)slot + 1] = r.L.y;
+        a.wave_buf[3 * (size_t)slot + 2] = r.L.z;
+    }
+}
+
+// Bounce 1 (S1 raygen + S2-S4): whole warps of 32 consecutive slots, so the primary rays stay coherent;
+// the camera rays are computed here (no raygen pass), survivors are compacted into the path queue
+// with warp-aggregated appends, escapes into the NIF queue.
+__global__ void __launch_bounds__(128, PT_TS_MINB) first_bounce_kernel(ShadeArgs a) {
+    const uint32_t n = a.counters[0];
+    const int lane = threadIdx.x & 31;
+    uint32_t segs = 0;
+    for (;;) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(a.work, 32u);
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        if (base >= n) break;
+        const uint32_t i = base + (uint32_t)lane;
+        SegOut r;
+        r.alive = r.escaped = false;
+        if (i < n) {
+            ++segs;
+            const float3 eye = make_float3(a.cam.eye[0], a.cam.eye[1], a.cam.eye[2]);
+            shade_segment(a, 1, i, eye, camera_ray(a, i), make_float3(1.0f, 1.0f, 1.0f), r);
+            write_radiance(a, r, i);
+        }
+        const uint32_t pos = warp_append(r.alive, a.alive_count);
+        if (r.alive) {
+            a.qA[pos] = make_float4(r.o.x, r.o.y, r.o.z, __uint_as_float(i));
+            a.qB[pos] = make_float4(r.d.x, r.d.y, r.d.z, r.beta.x);
+            a.qC[pos] = make_float2(r.beta.y, r.beta.z);
+        }
+        append_escaped(a, r, i);
+    }
+#pragma unroll
+    for (int k = 16; k > 0; k >>= 1) segs += __shfl_xor_sync(0xFFFFFFFFu, segs, k);
+    if (lane == 0) atomicAdd(a.seg_count, segs);
+}
+
+// Bounces 2.. (persistent): every lane carries one path from the first bounce's queue to its end,
+// and a lane whose path ends refills from the queue (one warp-aggregated atomic for all of the warp's
+// free lanes), so the warps stay full without a launch, a barrier or a state round trip through HBM
+// per bounce. Per-path results do not depend on the schedule: the RNG is keyed by (pixel, sample,
+// depth) and every path writes only its own slot.
+__global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
+    const uint32_t n = *a.alive_count;
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    bool have = false;
+    uint32_t slot = 0;
+    int depth = 0;
+    float3 o = make_float3(0, 0, 0), d = make_float3(0, 0, 1), bt = make_float3(1, 1, 1);
+    uint32_t segs = 0;
+    for (;;) {
+        const uint32_t mneed = __ballot_sync(0xFFFFFFFFu, !have);
+        if (mneed) {
+            const int leader = __ffs(mneed) - 1;
+            uint32_t base = 0;
+            if (lane == leader) base = atomicAdd(a.work, (uint32_t)__popc(mneed));
+            base = __shfl_sync(0xFFFFFFFFu, base, leader);
+            if (!have) {
+                const uint32_t idx = base + (uint32_t)__popc(mneed & lt);
+                if (idx < n) {
+                    const float4 qa = __ldg(a.qA + idx), qb = __ldg(a.qB + idx);
+                    const float2 qc = __ldg(a.qC + idx);
+                    o = make_float3(qa.x, qa.y, qa.z);
+                    slot = __float_as_uint(qa.w);
+                    d = make_float3(qb.x, qb.y, qb.z);
+                    bt = make_float3(qb.w, qc.x, qc.y);
+                    depth = 2;
+                    have = true;
+                }
+            }
+        }
+        if (!__any_sync(0xFFFFFFFFu, have)) break;
+        SegOut r;
+        r.escaped = false;
+        if (have) {
+            ++segs;
+            shade_segment(a, depth, slot, o, d, bt, r);
+            write_radiance(a, r, slot);
+        }
+        append_escaped(a, r, slot);
+        if (have) {
+            if (r.alive) {
+                o = r.o;
+                d = r.d;
+                bt = r.beta;
+                ++depth;
+            } else {
+                have = false;
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 16; k > 0; k >>= 1) segs += __shfl_xor_sync(0xFFFFFFFFu, segs, k);
+    if (lane == 0) atomicAdd(a.seg_count, segs);
 }
 
 __global__ void accumulate_kernel(const float* __restrict__ wave_buf, int n_elems, int k, float* __restrict__ fb) {
@@ -800,22 +867,28 @@ static int resident_grid(K kernel, int block) {
     return num_sms() * (per_sm > 0 ? per_sm : 1);
 }
 
-void launch_trace_shade(const TraceParams& tp, const Cam32& cam, int W, int H, int first_sample, int depth, int max_depth,
-                        uint64_t seed, int buf, int use_nif, float3 env, Workspace& ws, cudaStream_t st) {
+void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int first_sample, int max_depth, uint64_t seed,
+                  int use_nif, float3 env, Workspace& ws, cudaStream_t st) {
     ShadeArgs a;
     a.tp = tp;
     a.cam = cam;
-    a.W = W; a.H = H; a.first_sample = first_sample; a.depth = depth; a.max_depth = max_depth;
+    a.W = W; a.H = H; a.first_sample = first_sample; a.depth = 1; a.max_depth = max_depth;
     a.key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
     a.counters = ws.counters;
-    a.q_out = reinterpret_cast<unsigned long long*>(ws.counters + 2 * depth);
-    a.work = ws.counters + kCounterWork + depth;
+    a.alive_count = ws.counters + kCounterAlive;
+    a.esc_count = ws.counters + kCounterEsc;
+    a.seg_count = ws.counters + kCounterSeg;
     a.use_nif = use_nif; a.env = env;
-    a.A_in = ws.rayA[buf]; a.B_in = ws.rayB[buf]; a.C_in = ws.rayC[buf];
-    a.A_out = ws.rayA[buf ^ 1]; a.B_out = ws.rayB[buf ^ 1]; a.C_out = ws.rayC[buf ^ 1];
+    a.qA = ws.rayA[0]; a.qB = ws.rayB[0]; a.qC = ws.rayC[0];
     a.esc = ws.esc; a.esc_beta = ws.esc_beta; a.wave_buf = ws.wave_buf;
-    static const int grid = resident_grid(trace_shade_kernel, 128);
-    trace_shade_kernel<<<grid, 128, 0, st>>>(a);
+    static const int grid1 = resident_grid(first_bounce_kernel, 128);
+    static const int grid2 = resident_grid(path_kernel, 128);
+    a.work = ws.counters + kCounterWork;
+    first_bounce_kernel<<<grid1, 128, 0, st>>>(a);
+    if (max_depth > 1) {
+        a.work = ws.counters + kCounterWork + 1;
+        path_kernel<<<grid2, 128, 0, st>>>(a);
+    }
 }
 
 void launch_accumulate(const float* wave_buf, int n_pix, int k, float* fb, cudaStream_t st) {
