@@ -47,12 +47,13 @@ def trace_bytes_per_segment(cfg_index: int):
         return None
 
 
-def ncu_traffic(kernel: str, cfg_index: int):
-    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu capture of one bench step
-    (tools/ncu_traffic.py), or None."""
+def ncu_traffic(kernels, cfg_index: int):
+    """DRAM bytes (read + write) per wave of the named kernels (each launched once per wave) from the
+    committed ncu capture of one bench step (tools/ncu_traffic.py), or None."""
     try:
         with open(os.path.join(PROFILES, f"ncu_traffic_c{cfg_index}.json")) as f:
-            return float(json.load(f)[kernel]["dram_bytes_per_launch"])
+            d = json.load(f)
+        return float(sum(d[k]["dram_bytes_per_launch"] for k in kernels))
     except Exception:
         return None
 
@@ -317,7 +318,7 @@ def main():
     nif_ms = kt["nif"]
     infers = escaped
     kernels = {
-        "trace_shade": {"ms_per_step": kt["traverse"] / K, "launches_per_step": trav_launches / K,
+        "trace_paths": {"ms_per_step": kt["traverse"] / K, "launches_per_step": trav_launches / K,
                         "bytes_alg": 80 * segments},
         "nif": {"ms_per_step": nif_ms / K, "launches_per_step": nif_launches / K,
                 "flops_alg": HIDDEN_FLOP_PER_INF * infers},
@@ -328,22 +329,25 @@ def main():
     nif_roof = {"bound": "tensor", "achieved": nif_tflops, "peak": peaks["bf16_tflops_sustained"],
                 "unit": "TFLOP/s", "frac": nif_tflops / peaks["bf16_tflops_sustained"],
                 "frac_burst": nif_tflops / peaks["bf16_tflops"],
-                "traffic": ncu_traffic("siren_kernel", cfg.index),
+                "traffic": ncu_traffic(["siren_kernel"], cfg.index),
                 "kernel": "siren_kernel", "flop_per_inference": HIDDEN_FLOP_PER_INF,
                 "inferences_per_launch": infers / max(1, nif_launches),
                 "peak_source": peaks["source"] + " bf16 sustained (fp16 same rate)"}
-    if dominant == "trace_shade":
-        # traversal + shading: algorithmic L2 bytes per segment (counting build, tools/trace_count.py,
-        # profiles/round1/trace_count.json): node visits x 64 B + primitive tests x 48 B + 80 B of path
-        # state, against the measured L2 read bandwidth (tools/l2_bench.cu, profiles/round1/l2_bench.json)
+    if dominant == "trace_paths":
+        # traversal + shading (first_bounce_kernel + path_kernel, timed together per wave): algorithmic
+        # L2 bytes per segment (counting build, tools/trace_count.py, profiles/round1/trace_count.json):
+        # node visits x 64 B + primitive tests x 48 B + 80 B of path state, against the measured L2 read
+        # bandwidth (tools/l2_bench.cu, profiles/round1/l2_bench.json); traffic = DRAM bytes of both
+        # kernels per wave
         ms_k = kt["traverse"]
         bps = trace_bytes_per_segment(cfg.index)
         byts = (bps or 0.0) * segments
         gbs = byts / (ms_k / 1e3) / 1e9 if ms_k > 0 else 0.0
         roof = {"bound": "l2", "achieved": gbs, "peak": L2_READ_GBS, "unit": "GB/s", "frac": gbs / L2_READ_GBS,
-                "traffic": ncu_traffic("trace_shade_kernel", cfg.index), "kernel": "trace_shade_kernel",
+                "traffic": ncu_traffic(["first_bounce_kernel", "path_kernel"], cfg.index),
+                "kernel": "first_bounce_kernel + path_kernel",
                 "bytes_per_segment": bps,
-                "segments_per_launch": segments / max(1, trav_launches),
+                "segments_per_wave": segments / max(1, trav_launches / 2),
                 "peak_source": "measured L2 read bandwidth, tools/l2_bench.cu (MEASURED_PEAKS.json has none)",
                 "hbm_frac": (80.0 * segments / (ms_k / 1e3) / 1e9) / peaks["hbm_gbs"] if ms_k > 0 else 0.0}
     else:

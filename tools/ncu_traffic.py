@@ -2,7 +2,7 @@
 """DRAM traffic per launch of the hot-path kernels from an ncu metrics capture of one bench step:
 
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \\
-      -k regex:"trace_shade|siren|raygen|accumulate" --csv --log-file X.csv python bench.py --steps 1 --warmup 0 ...
+      -k regex:"first_bounce|path_kernel|siren|accumulate" --csv --log-file X.csv python bench.py --steps 1 --warmup 0 ...
   python tools/ncu_traffic.py X.csv > profiles/round1/ncu_traffic_c1.json
 
 The bench's warm-up and timed step both appear; per-kernel averages are over every captured launch."""

@@ -1,4 +1,4 @@
-# trace_shade register-cap variants: frame time of the bench workload
+# path-kernel register-cap variants (PT_TS_MINB): frame time of the bench workload
 mkdir -p gpurun_out build/variants
 for m in ${TS_MINB:-1 5 6 7 8}; do
   python -c "from paper_2305_20061_b200 import _build; _build.build(out='build/variants/libpt_ts$m.so', defines=['PT_TS_MINB=$m'])" > /dev/null 2>&1 || { echo "build $m failed"; continue; }
