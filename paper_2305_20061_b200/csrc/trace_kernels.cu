@@ -666,7 +666,8 @@ __device__ __forceinline__ void shade_segment(const ShadeArgs& a, int depth, uin
             r.done = true;
             return;
         }
-        bt = make_float3(bt.x / q, bt.y / q, bt.z / q);
+        const float iq = __frcp_rn(q);            // beta / q as one reciprocal and three products
+        bt = make_float3(bt.x * iq, bt.y * iq, bt.z * iq);
     }
     r.beta = bt;
 }
