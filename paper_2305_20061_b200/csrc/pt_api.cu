@@ -61,6 +61,59 @@ struct PathPool {
     cudaStream_t host_stream = nullptr;   // stream of the host-buffer entry point pt_render (all scenes)
 };
 
+// Device blocks of destroyed scene / NIF handles are kept per device and size class (powers of two)
+// and handed to the next handle: creating and destroying a handle per frame (the end-to-end path)
+// then costs a host-to-device copy, not a cudaMalloc / cudaFree pair. A block returns to the cache
+// only after the device is idle (the same guarantee cudaFree gives).
+struct BlockCache {
+    std::mutex mu;
+    std::vector<std::pair<size_t, void*>> free_blocks;   // (class bytes, pointer)
+    size_t cached = 0;
+};
+constexpr size_t kBlockCacheMax = 512ull << 20;
+
+BlockCache& block_cache(int dev) {
+    static BlockCache caches[64];
+    return caches[dev & 63];
+}
+
+size_t block_class(size_t bytes) {
+    size_t c = 256;
+    while (c < bytes) c <<= 1;
+    return c;
+}
+
+cudaError_t cache_alloc(int dev, size_t bytes, void** out) {
+    const size_t c = block_class(bytes);
+    BlockCache& bc = block_cache(dev);
+    {
+        std::lock_guard<std::mutex> lk(bc.mu);
+        for (size_t i = 0; i < bc.free_blocks.size(); ++i) {
+            if (bc.free_blocks[i].first == c) {
+                *out = bc.free_blocks[i].second;
+                bc.free_blocks.erase(bc.free_blocks.begin() + i);
+                bc.cached -= c;
+                return cudaSuccess;
+            }
+        }
+    }
+    return cudaMalloc(out, c);
+}
+
+void cache_free(int dev, void* p, size_t bytes) {
+    if (!p) return;
+    const size_t c = block_class(bytes);
+    cudaDeviceSynchronize();   // no stream may still read the block
+    BlockCache& bc = block_cache(dev);
+    std::lock_guard<std::mutex> lk(bc.mu);
+    if (bc.cached + c > kBlockCacheMax) {
+        cudaFree(p);
+        return;
+    }
+    bc.free_blocks.emplace_back(c, p);
+    bc.cached += c;
+}
+
 PathPool& path_pool(int dev) {
     static PathPool pools[64];
     return pools[dev & 63];
@@ -360,7 +413,8 @@ int pt_scene_create(const pt_triangle* tris, int64_t n_tris, const pt_sphere* sp
         sm[i] = spheres[i].material;
     }
     if (n_mats > 0) std::memcpy(&host[o_mat], mats, sizeof(pt_material) * n_mats);
-    CUS(cudaMalloc(&sc->d_alloc, total));
+    sc->d_alloc_bytes = total;
+    CUS(cache_alloc(sc->device, total, &sc->d_alloc));
     CUS(cudaMemcpy(sc->d_alloc, host.data(), total, cudaMemcpyHostToDevice));
     uint8_t* base = static_cast<uint8_t*>(sc->d_alloc);
     sc->d_pool = sc->pool_units > 0 ? reinterpret_cast<uint4*>(base + o_pool) : nullptr;
@@ -380,7 +434,9 @@ int pt_scene_destroy(pt_scene* sc) {
     {
         std::lock_guard<std::mutex> lk(sc->mu);
         collect_timers(sc);
-        cudaFree(sc->d_alloc);
+        cache_free(sc->device, sc->d_alloc, sc->d_alloc_bytes);
+        cache_free(sc->device, sc->ws.fb, sizeof(float) * sc->ws.fb_capacity);
+        sc->ws.fb = nullptr;
         free_ws(sc->ws);
     }
     delete sc;
@@ -410,7 +466,8 @@ int pt_nif_load_ex(int32_t kind, const uint16_t* blob, int64_t n_halves, pt_nif*
     const size_t b_img = (img.size() + 255) & ~size_t(255);
     img.resize(b_img + sizeof(uint16_t) * n_halves, 0);
     std::memcpy(&img[b_img], blob, sizeof(uint16_t) * n_halves);
-    cudaError_t e = cudaMalloc(&n->d_smem_image, img.size());
+    n->d_alloc_bytes = img.size();
+    cudaError_t e = cache_alloc(n->device, img.size(), &n->d_smem_image);
     if (e == cudaSuccess) e = cudaMemcpy(n->d_smem_image, img.data(), img.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) n->d_blob = reinterpret_cast<uint16_t*>(static_cast<uint8_t*>(n->d_smem_image) + b_img);
     if (e != cudaSuccess) {
@@ -459,7 +516,7 @@ int pt_nif_load_family(int32_t hidden, int32_t layers, const uint16_t* blob, int
 int pt_nif_destroy(pt_nif* n) {
     if (!n) return PT_OK;
     pt::mlp_free(n);
-    cudaFree(n->d_smem_image);
+    cache_free(n->device, n->d_smem_image, n->d_alloc_bytes);
     // (d_blob lives inside the d_smem_image allocation)
     delete n;
     return PT_OK;
@@ -485,10 +542,10 @@ int pt_render(const pt_scene* scene, const pt_nif* nif, const float env_rgb[3], 
     if (rc) return rc;
     const int64_t n = (int64_t)width * height * 3;
     if (sc->ws.fb_capacity < n) {
-        cudaFree(sc->ws.fb);
+        cache_free(sc->device, sc->ws.fb, sizeof(float) * sc->ws.fb_capacity);
         sc->ws.fb = nullptr;
         sc->ws.fb_capacity = 0;
-        CU(cudaMalloc(&sc->ws.fb, sizeof(float) * n));
+        CU(cache_alloc(sc->device, sizeof(float) * n, reinterpret_cast<void**>(&sc->ws.fb)));
         sc->ws.fb_capacity = n;
     }
     cudaStream_t st = sc->ws.own_stream;

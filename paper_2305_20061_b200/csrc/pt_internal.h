@@ -91,6 +91,7 @@ struct pt_scene {
     int32_t n_mats = 0;
     pt_camera cam{};
     void* d_alloc = nullptr;          // the scene's single device allocation (all arrays below)
+    size_t d_alloc_bytes = 0;
     uint4* d_pool = nullptr;          // wide BVH + inline primitives
     int64_t pool_units = 0;
     bool empty = true;
@@ -116,7 +117,8 @@ struct MlpLayer {
 struct pt_nif {
     int device = 0;
     int kind = PT_NIF_SIREN;
-    void* d_smem_image = nullptr;     // pre-laid-out shared-memory image of the fused kernel
+    void* d_smem_image = nullptr;     // pre-laid-out shared-memory image of the fused kernel (+ raw blob)
+    size_t d_alloc_bytes = 0;
     int64_t smem_bytes = 0;
     uint16_t* d_blob = nullptr;       // raw fp16 blob
     // PT_NIF_FR_FAMILY (layered GEMM path)

@@ -104,7 +104,9 @@ void nif_build_smem_image(const uint16_t* blob, std::vector<uint8_t>* image) {
         const uint16_t* b = blob + off; off += 128;
         const int base = kOffBH + l * kBHBytes;
         for (int n = 0; n < 128; ++n) {
-            for (int k = 0; k < 128; ++k) put_core(img, base, 128, n, k, W[n * 128 + k]);
+            // 8 consecutive k of one row are one 16-byte core-matrix row
+            for (int kb = 0; kb < 16; ++kb)
+                std::memcpy(&img[base + ((kb * 16) + (n >> 3)) * 128 + (n & 7) * 16], &W[n * 128 + 8 * kb], 16);
             put_core(img, base, 128, n, 128, b[n]);
         }
     }
