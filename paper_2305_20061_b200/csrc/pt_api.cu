@@ -209,13 +209,6 @@ void collect_timers(pt_scene* sc) {
     sc->pending.clear();
 }
 
-__global__ void stats_kernel(const uint32_t* counters, unsigned long long* acc) {
-    acc[0] += counters[0];
-    acc[1] += counters[pt::kCounterSeg];
-    acc[2] += counters[pt::kCounterEsc];
-}
-
-__global__ void set_count_kernel(uint32_t* c, uint32_t v) { *c = v; }
 
 
 int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, int W, int H, int first_sample,
@@ -262,10 +255,9 @@ int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, i
         const int64_t kk = std::min<int64_t>(k, (int64_t)first_sample + n_samples - w0);
         const int64_t slots = kk * np;
         CU(cudaMemsetAsync(ws.counters, 0, sizeof(uint32_t) * pt::kCounters, st));
-        set_count_kernel<<<1, 1, 0, st>>>(ws.counters + 0, (uint32_t)slots);
         cudaEvent_t e0;
         tm.begin(T_TRAVERSE, &e0);
-        pt::launch_paths(tp, cam, W, H, (int)w0, max_depth, seed, use_nif, env, ws, st);
+        pt::launch_paths(tp, cam, W, H, (int)w0, (int)slots, max_depth, seed, use_nif, env, ws, st);
         tm.end(T_TRAVERSE, e0);
         stats.launches += max_depth > 1 ? 2 : 1;
         stats.traverse_launches += max_depth > 1 ? 2 : 1;
@@ -278,10 +270,9 @@ int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, i
             stats.nif_launches += 1;
         }
         tm.begin(T_ACCUM, &e0);
-        pt::launch_accumulate(ws.wave_buf, (int)np, (int)kk, d_accum, st);
+        pt::launch_accumulate(ws.wave_buf, (int)np, (int)kk, d_accum, ws.counters, d_stats, (uint32_t)slots, st);
         tm.end(T_ACCUM, e0);
-        stats_kernel<<<1, 1, 0, st>>>(ws.counters, d_stats);
-        stats.launches += 3;   // set_count, accumulate, stats
+        stats.launches += 1;   // accumulate (with the wave statistics)
         stats.waves += 1;
     }
     CU(cudaGetLastError());

@@ -72,10 +72,9 @@ struct TimedLaunch {
     int cls;
     cudaEvent_t a, b;
 };
-// device counters of one wave (uint32 words): [2d, 2d+1] = the packed 64-bit queue counter of bounce d
-// (low: alive paths appended by bounce d, d = 0 raygen; high: escaped paths appended by bounce d), one
-// 64-bit atomic per warp appends to both queues; [128] = total escaped, [129] = error flags, [130 + d] =
-// work-fetch counter of bounce d
+// device counters of one wave (uint32 words): [128] = escaped paths (the NIF's row count), [129] = error
+// flags, [130] / [131] = work-fetch counters of the first-bounce and path kernels, [132] = traced
+// segments, [133] = paths alive after the first bounce
 constexpr int kCounters = 192;
 constexpr int kCounterEsc = 128;
 constexpr int kCounterErr = 129;
@@ -149,9 +148,10 @@ struct TraceParams {
 };
 
 // kernel launchers (trace_kernels.cu)
-void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int first_sample, int max_depth, uint64_t seed,
-                  int use_nif, float3 env, Workspace& ws, cudaStream_t st);
-void launch_accumulate(const float* wave_buf, int n_pix, int k, float* fb, cudaStream_t st);
+void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int first_sample, int n_slots, int max_depth,
+                  uint64_t seed, int use_nif, float3 env, Workspace& ws, cudaStream_t st);
+void launch_accumulate(const float* wave_buf, int n_pix, int k, float* fb, const uint32_t* counters,
+                       unsigned long long* stats, uint32_t paths, cudaStream_t st);
 void launch_primary(const TraceParams& tp, const Cam32& cam, int W, int H, int sample, uint64_t seed,
                     int32_t* prim, float* t, cudaStream_t st);
 void launch_trace_rays(const TraceParams& tp, const float* o, const float* d, int64_t n, int32_t* prim, float* t,

@@ -530,6 +530,7 @@ struct ShadeArgs {
     int W, H, first_sample, depth, max_depth;
     uint2 key;
     const uint32_t* counters;   // the wave's counters (pt_internal.h kCounters layout)
+    uint32_t n_slots;           // paths of the wave
     uint32_t* work;             // fetch counter of the kernel
     uint32_t* alive_count;      // paths alive after the first bounce (its output queue length)
     uint32_t* esc_count;        // escaped-queue length
@@ -716,8 +717,11 @@ __device__ __forceinline__ void write_radiance(const ShadeArgs& a, const SegOut&
 // Bounce 1 (S1 raygen + S2-S4): whole warps of 32 consecutive slots, so the primary rays stay coherent;
 // the camera rays are computed here (no raygen pass), survivors are compacted into the path queue
 // with warp-aggregated appends, escapes into the NIF queue.
-__global__ void __launch_bounds__(128, PT_TS_MINB) first_bounce_kernel(ShadeArgs a) {
-    const uint32_t n = a.counters[0];
+#ifndef PT_FB_MINB
+#define PT_FB_MINB PT_TS_MINB   // the first bounce's own register cap (tools/ts_tune.sh)
+#endif
+__global__ void __launch_bounds__(128, PT_FB_MINB) first_bounce_kernel(ShadeArgs a) {
+    const uint32_t n = a.n_slots;
     const int lane = threadIdx.x & 31;
     uint32_t segs = 0;
     for (;;) {
@@ -807,7 +811,16 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
     if (lane == 0) atomicAdd(a.seg_count, segs);
 }
 
-__global__ void accumulate_kernel(const float* __restrict__ wave_buf, int n_elems, int k, float* __restrict__ fb) {
+// S6: fb += the wave's per-slot radiance, summed over its k samples in sample order (deterministic); one
+// thread also folds the wave's counters into the scene's statistics (paths, segments, escaped)
+__global__ void accumulate_kernel(const float* __restrict__ wave_buf, int n_elems, int k, float* __restrict__ fb,
+                                  const uint32_t* __restrict__ counters, unsigned long long* __restrict__ stats,
+                                  uint32_t paths) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && stats) {
+        stats[0] += paths;
+        stats[1] += counters[kCounterSeg];
+        stats[2] += counters[kCounterEsc];
+    }
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n_elems; e += gridDim.x * blockDim.x) {
         float s = fb[e];
         for (int j = 0; j < k; ++j) s += __ldg(wave_buf + (size_t)j * n_elems + e);   // fixed sample order
@@ -868,9 +881,10 @@ static int resident_grid(K kernel, int block) {
     return num_sms() * (per_sm > 0 ? per_sm : 1);
 }
 
-void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int first_sample, int max_depth, uint64_t seed,
-                  int use_nif, float3 env, Workspace& ws, cudaStream_t st) {
+void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int first_sample, int n_slots, int max_depth,
+                  uint64_t seed, int use_nif, float3 env, Workspace& ws, cudaStream_t st) {
     ShadeArgs a;
+    a.n_slots = (uint32_t)n_slots;
     a.tp = tp;
     a.cam = cam;
     a.W = W; a.H = H; a.first_sample = first_sample; a.depth = 1; a.max_depth = max_depth;
@@ -892,9 +906,10 @@ void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int fir
     }
 }
 
-void launch_accumulate(const float* wave_buf, int n_pix, int k, float* fb, cudaStream_t st) {
+void launch_accumulate(const float* wave_buf, int n_pix, int k, float* fb, const uint32_t* counters,
+                       unsigned long long* stats, uint32_t paths, cudaStream_t st) {
     const int n = 3 * n_pix;
-    accumulate_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(wave_buf, n, k, fb);
+    accumulate_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(wave_buf, n, k, fb, counters, stats, paths);
 }
 
 void launch_primary(const TraceParams& tp, const Cam32& cam, int W, int H, int sample, uint64_t seed, int32_t* prim,
