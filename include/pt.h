@@ -70,7 +70,8 @@ typedef struct pt_nif pt_nif;
    Sec. 3.1.4). Host arrays: tris[n_tris], spheres[n_spheres], mats[n_mats], *cam. n_tris and
    n_spheres may be 0 (an empty scene is legal: the furnace case). Every decoded child box is
    verified at build time to contain its subtree's exact fp32 bounds.
-   Errors: INVALID_ARG, DOMAIN, CUDA, OOM. */
+   Errors: INVALID_ARG, DOMAIN (non-finite input, a child box beyond the fp16 offset range, or a BVH
+   larger than 2^28 16-byte units = 4 GiB), CUDA, OOM. */
 PT_API int pt_scene_create(const pt_triangle* tris, int64_t n_tris, const pt_sphere* spheres, int64_t n_spheres,
                     const pt_material* mats, int32_t n_mats, const pt_camera* cam, pt_scene** out);
 PT_API int pt_scene_destroy(pt_scene* scene);
