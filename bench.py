@@ -47,6 +47,17 @@ def trace_bytes_per_segment(cfg_index: int):
         return None
 
 
+def ncu_inst(kernels, cfg_index: int):
+    """Warp instructions issued per wave by the named kernels (same ncu capture as ncu_traffic), or None."""
+    try:
+        with open(os.path.join(PROFILES, f"ncu_traffic_c{cfg_index}.json")) as f:
+            d = json.load(f)
+        v = float(sum(d[k]["warp_inst_per_launch"] for k in kernels))
+        return v if v > 0 else None
+    except Exception:
+        return None
+
+
 def ncu_traffic(kernels, cfg_index: int):
     """DRAM bytes (read + write) per wave of the named kernels (each launched once per wave) from the
     committed ncu capture of one bench step (tools/ncu_traffic.py), or None."""
@@ -56,6 +67,9 @@ def ncu_traffic(kernels, cfg_index: int):
         return float(sum(d[k]["dram_bytes_per_launch"] for k in kernels))
     except Exception:
         return None
+
+
+ClockSampler_last = {}
 
 
 def load_peaks():
@@ -314,6 +328,8 @@ def main():
         return
 
     peaks = load_peaks()
+    global ClockSampler_last
+    ClockSampler_last = clk.summary()
     K = args.steps
     nif_ms = kt["nif"]
     infers = escaped
@@ -350,9 +366,20 @@ def main():
                 "segments_per_wave": segments / max(1, trav_launches / 2),
                 "peak_source": "measured L2 read bandwidth, tools/l2_bench.cu (MEASURED_PEAKS.json has none)",
                 "hbm_frac": (80.0 * segments / (ms_k / 1e3) / 1e9) / peaks["hbm_gbs"] if ms_k > 0 else 0.0}
+        # the bound in practice: instruction issue. Warp instructions per wave (ncu capture of the same
+        # kernels) / the live kernel time, against 4 issue slots per SM per clock at the sampled clock
+        inst = ncu_inst(["first_bounce_kernel", "path_kernel"], cfg.index)
+        waves = max(1, trav_launches / 2)
+        if inst and ms_k > 0:
+            f_clk = (ClockSampler_last.get("sm_mhz") or 1965.0) * 1e6
+            peak_issue = 4 * torch.cuda.get_device_properties(local).multi_processor_count * f_clk
+            ach = inst * waves / (ms_k / 1e3)
+            roof["issue"] = {"bound": "alu", "achieved": ach, "peak": peak_issue, "unit": "warp-inst/s",
+                             "frac": ach / peak_issue, "warp_inst_per_wave": inst,
+                             "peak_source": "4 warp-instructions per clock per SM (B200_PROFILING.md) x SMs x sampled SM clock"}
     else:
         roof = nif_roof
-    clocks = clk.summary()
+    clocks = ClockSampler_last
     line = {
         "metric": "samples/sec", "value": value, "unit": "samples/s", "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak",

@@ -4,7 +4,7 @@ mkdir -p gpurun_out
 timeout 1200 python -m pytest tests -m gpu -x -q --timeout=400 -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo "pytest rc $?" >> gpurun_out/gpu_tests.log
 python tools/trace_count.py > gpurun_out/trace_count.json 2> gpurun_out/trace_count.err
 mkdir -p profiles/round1 && cp gpurun_out/trace_count.json profiles/round1/trace_count.json
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"first_bounce|path_kernel|siren|accumulate" --csv --log-file gpurun_out/traffic_c1.csv python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_traffic.log 2>&1
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum --clock-control none -k regex:"first_bounce|path_kernel|siren|accumulate" --csv --log-file gpurun_out/traffic_c1.csv python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_traffic.log 2>&1
 python tools/ncu_traffic.py gpurun_out/traffic_c1.csv > gpurun_out/ncu_traffic_c1.json && cp gpurun_out/ncu_traffic_c1.json profiles/round1/
 python bench.py --steps 50 --warmup 5 > gpurun_out/bench.log 2> gpurun_out/bench.err; echo "bench rc $?" >> gpurun_out/bench.err
 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1

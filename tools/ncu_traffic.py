@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """DRAM traffic per launch of the hot-path kernels from an ncu metrics capture of one bench step:
 
-  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \\
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum \\
+      --clock-control none \\
       -k regex:"first_bounce|path_kernel|siren|accumulate" --csv --log-file X.csv python bench.py --steps 1 --warmup 0 ...
   python tools/ncu_traffic.py X.csv > profiles/round1/ncu_traffic_c1.json
 
@@ -28,9 +29,11 @@ for r in rows[hi + 1:]:
 for (name, _), m in launch.items():
     per[name]["bytes"].append(m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0))
     per[name]["ns"].append(m.get("gpu__time_duration.sum", 0))
+    per[name]["inst"].append(m.get("smsp__inst_executed.sum", 0))
 out = {}
 for name, d in per.items():
     n = len(d["bytes"])
     out[name] = {"launches": n, "dram_bytes_per_launch": sum(d["bytes"]) / n,
-                 "dram_bytes_total": sum(d["bytes"]), "ns_per_launch": sum(d["ns"]) / n}
+                 "dram_bytes_total": sum(d["bytes"]), "ns_per_launch": sum(d["ns"]) / n,
+                 "warp_inst_per_launch": sum(d["inst"]) / n}
 print(json.dumps(out, indent=1))
