@@ -34,6 +34,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -352,6 +353,247 @@ __global__ void __launch_bounds__(mlp::kThreads, 1) mlp_layer_kernel(mlp::LayerA
 }
 
 // ---------------------------------------------------------------------------------------------
+// Fused variant for H <= 256: one 128-row tile runs through all layers with its activations resident
+// in TMEM (A: H/2 columns of fp16 pairs, D: H fp32 columns) and the layers' weights streamed from L2 as
+// the same blocked K-chunks through a shared-memory ring -- no activation traffic to HBM at all (the
+// layered path moves 4 H bytes per ray per layer). 320 threads: warp 0 producer (bulk copies of weight
+// chunks in the order the MMA consumes them), warp 1 MMA issuer (TS MMAs, A from TMEM), warps 2-9 the
+// epilogue (bias + ReLU + fp16 into A, the Fourier features into A for layer 0 and the concat columns,
+// the YUV -> RGB / exp / beta output).
+// ---------------------------------------------------------------------------------------------
+namespace mlpf {
+constexpr int kMaxLayers = 17;
+constexpr int kRing = 6;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 32 * (2 + kEpiWarps);
+struct FusedArgs {
+    const uint8_t* W[kMaxLayers];      // blocked weights of layer l, one N tile: [KC][BN * 128 B]
+    const float* bias[kMaxLayers];
+    int KC[kMaxLayers], BN[kMaxLayers], N[kMaxLayers];
+    int L, c;
+    const float* freq;
+    const float4* esc;
+    const float4* esc_beta;
+    const uint32_t* count;
+    float* out;
+    int dir_input;
+};
+}  // namespace mlpf
+
+template <int kH>
+constexpr int fused_ctas_per_sm() { return kH == 64 ? 3 : kH == 128 ? 2 : 1; }
+
+template <int kH>
+__global__ void __launch_bounds__(mlpf::kThreads, fused_ctas_per_sm<kH>()) mlp_fused_kernel(mlpf::FusedArgs a) {
+    using namespace mlpf;
+    constexpr int kStage = kH * 128;                         // bytes of the widest weight chunk
+    constexpr uint32_t kTmemCols = kH == 256 ? 512u : (kH == 128 ? 256u : 128u);
+    constexpr uint32_t kDCol = 0, kACol = kH;                // D: kH fp32 columns; A: kH / 2 columns
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);     // [0..5] full, [6..11] empty, [12] d_full, [13] a_ready
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 120);
+    uint8_t* ring = smem + 1024;
+    auto bar = [&](int b) { return smem_u32(&bars[b]); };
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t n_rows = *a.count;
+    const uint32_t n_tiles = (n_rows + mlp::kBM - 1) / mlp::kBM;
+    if (blockIdx.x >= n_tiles) return;
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < kRing; ++s) {
+            mbar_init(bar(s), 1);
+            mbar_init(bar(kRing + s), 1);
+        }
+        mbar_init(bar(12), 1);
+        mbar_init(bar(13), kEpiWarps);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0, it = 0;
+            uint32_t phase = 0;
+            for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+                for (int l = 0; l <= a.L; ++l) {
+                    const uint32_t bytes = (uint32_t)a.BN[l] * 128u;
+                    for (int kc = 0; kc < a.KC[l]; ++kc, ++it) {
+                        if (it >= kRing) mbar_wait(bar(kRing + stage), phase ^ 1);
+                        mbar_expect_tx(bar(stage), bytes);
+                        asm volatile(
+                            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                smem_u32(ring + stage * kStage)),
+                            "l"(a.W[l] + (size_t)kc * bytes), "r"(bytes), "r"(bar(stage))
+                            : "memory");
+                        if (++stage == kRing) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        int stage = 0;
+        uint32_t phase = 0, a_phase = 0;
+        for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+            for (int l = 0; l <= a.L; ++l) {
+                mbar_wait(bar(13), a_phase);                  // this layer's A written (and D read out)
+                a_phase ^= 1;
+                tc_fence_after();
+                const int bn = a.BN[l];
+                const uint32_t id = mlp::idesc(bn);
+                const uint32_t lbo = (uint32_t)(bn / 8) * 128u;
+                for (int kc = 0; kc < a.KC[l]; ++kc) {
+                    mbar_wait(bar(stage), phase);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t sb = smem_u32(ring + stage * kStage);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            mma_ts(tmem + kDCol, tmem + kACol + (uint32_t)(32 * kc + 8 * k),
+                                   smem_desc(sb + k * 2 * lbo, lbo, 128), id, (kc | k) != 0);
+                        mma_commit(bar(kRing + stage));
+                    }
+                    __syncwarp();
+                    if (++stage == kRing) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                if (elect_one()) mma_commit(bar(12));
+                __syncwarp();
+            }
+        }
+    } else {
+        // ===== epilogue: warps 2-9; two per TMEM lane quarter (half 0 / 1 split the column work) =====
+        const int e = warp - 2;
+        const int half = e >> 2;
+        const int q = warp & 3;
+        const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
+        const uint32_t A = tmem + kACol + lane_addr, D = tmem + kDCol + lane_addr;
+        uint32_t d_phase = 0;
+        // Fourier features of this row into A element columns col0 .. col0 + 39: half 0 the 20 sines,
+        // half 1 the 20 cosines; `pad` also zeroes element columns 40..63 (layer-0 input)
+        auto write_features = [&](float u, float v, int col0, bool pad) {
+            uint32_t w[10];
+#pragma unroll
+            for (int j = 0; j < 10; ++j) {
+                float f[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int fj = 2 * j + h;
+                    const float p = fmaf(__ldg(a.freq + 2 * fj), u, __ldg(a.freq + 2 * fj + 1) * v);
+                    const float r = p - rintf(p);
+                    f[h] = half == 0 ? __sinf(6.28318530717958647692f * r) : __cosf(6.28318530717958647692f * r);
+                }
+                w[j] = pack_half2(f[0], f[1]);
+            }
+            const uint32_t c0 = A + (uint32_t)(col0 / 2 + 10 * half);
+            tmem_st8(c0, w);
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(c0 + 8), "r"(w[8]), "r"(w[9])
+                         : "memory");
+            if (pad && half == 1) {
+                const uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                tmem_st8(A + 20, z);
+                asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%1,%1,%1};" ::"r"(A + 28), "r"(0u)
+                             : "memory");
+            }
+        };
+        for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+            const uint32_t row = t * mlp::kBM + 32 * q + lane;
+            const bool valid = row < n_rows;
+            float u = 0.5f, v = 0.5f;
+            float4 en = make_float4(0.5f, 0.5f, 0.0f, 0.0f);
+            if (valid) {
+                en = __ldg(a.esc + row);
+                u = en.x;
+                v = en.y;
+                if (a.dir_input) equirect_f32(make_float3(en.x, en.y, en.z), u, v);
+            }
+            write_features(u, v, 0, true);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar(13));
+            for (int l = 0; l <= a.L; ++l) {
+                mbar_wait(bar(12), d_phase);
+                d_phase ^= 1;
+                tc_fence_after();
+                if (l < a.L) {
+                    const int N = a.N[l];
+                    const float* bias = a.bias[l];
+                    for (int j = half; 32 * j < N; j += 2) {
+                        uint32_t vv[32];
+                        TMEM_LD32(D + 32 * j, vv);
+                        tmem_wait_ld_dep(vv);
+                        uint32_t pk[16];
+                        const float4* bp = reinterpret_cast<const float4*>(bias + 32 * j);
+#pragma unroll
+                        for (int g = 0; g < 8; ++g) {
+                            const float4 b4 = __ldg(bp + g);
+                            const float x0 = __uint_as_float(vv[4 * g]) + b4.x, x1 = __uint_as_float(vv[4 * g + 1]) + b4.y;
+                            const float x2 = __uint_as_float(vv[4 * g + 2]) + b4.z, x3 = __uint_as_float(vv[4 * g + 3]) + b4.w;
+                            asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(pk[2 * g]) : "f"(x1), "f"(x0));
+                            asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(pk[2 * g + 1]) : "f"(x3), "f"(x2));
+                        }
+                        if (32 * j + 32 <= N) {
+                            TMEM_ST16(A + 16 * j, pk);
+                        } else {
+                            // the concat layer's last chunk: 24 valid columns (H - 40 = 24 mod 32)
+                            tmem_st8(A + 16 * j, pk);
+                            asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(A + 16 * j + 8),
+                                         "r"(pk[8]), "r"(pk[9]), "r"(pk[10]), "r"(pk[11])
+                                         : "memory");
+                        }
+                    }
+                    if (l == a.c) write_features(u, v, kH - 40, false);   // the concat skip
+                    tmem_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(bar(13));
+                } else {
+                    // output layer: YUV (D columns 0..2) + bias -> fixed BT.601 -> RGB -> exp -> beta
+                    if (half == 0) {
+                        uint32_t y[4];
+                        tmem_ld4(D, y);
+                        tmem_wait_ld_dep4(y);
+                        if (valid) {
+                            const float Y = __uint_as_float(y[0]) + __ldg(a.bias[l] + 0);
+                            const float U = __uint_as_float(y[1]) + __ldg(a.bias[l] + 1);
+                            const float V = __uint_as_float(y[2]) + __ldg(a.bias[l] + 2);
+                            const float r = fmaf(1.13983f, V, Y);
+                            const float gch = fmaf(-0.58060f, V, fmaf(-0.39465f, U, Y));
+                            const float bch = fmaf(2.03211f, U, Y);
+                            const uint32_t slot = __float_as_uint(en.w);
+                            const float4 beta = __ldg(a.esc_beta + row);
+                            a.out[3 * (size_t)slot + 0] = beta.x * __expf(r);
+                            a.out[3 * (size_t)slot + 1] = beta.y * __expf(gch);
+                            a.out[3 * (size_t)slot + 2] = beta.z * __expf(bch);
+                        }
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
 // Host side: weight re-layout at load, launch sequence per row chunk
 // ---------------------------------------------------------------------------------------------
 namespace {
@@ -516,10 +758,54 @@ static cudaError_t launch_layer(const MlpLayer& ly, int epi, int fp8, mlp::Layer
 // the chunk is empty, so the host never synchronises on the count.
 constexpr int kChunkRows = 1 << 20;
 
+template <int kH>
+static cudaError_t launch_fused_t(const mlpf::FusedArgs& fa, int grid, cudaStream_t st) {
+    const int smem = 1024 + mlpf::kRing * kH * 128;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(mlp_fused_kernel<kH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    mlp_fused_kernel<kH><<<grid * fused_ctas_per_sm<kH>(), mlpf::kThreads, smem, st>>>(fa);
+    return cudaGetLastError();
+}
+
+// The fused path serves H = 64, 128, 256 in fp16 (PT_MLP_LAYERED=1 forces the layered path, for tests)
+static bool use_fused(const pt_nif* nif) {
+    const char* env = std::getenv("PT_MLP_LAYERED");
+    const bool layered = env && env[0] == '1';
+    return !layered && !nif->mlp_fp8 && (nif->mlp_H == 64 || nif->mlp_H == 128 || nif->mlp_H == 256) &&
+           nif->mlp_L + 1 <= mlpf::kMaxLayers;
+}
+
 cudaError_t launch_mlp(pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count, int64_t max_rows,
                        float* out, int dir_input, cudaStream_t st) {
     using namespace mlp;
     const int H = nif->mlp_H, L = nif->mlp_L, c = nif->mlp_c, fp8 = nif->mlp_fp8;
+    if (use_fused(nif)) {
+        mlpf::FusedArgs fa{};
+        for (int l = 0; l <= L; ++l) {
+            const MlpLayer& ly = nif->mlp_layers[l];
+            fa.W[l] = (const uint8_t*)ly.d_w;
+            fa.bias[l] = ly.d_bias;
+            fa.KC[l] = ly.K / 64;
+            fa.BN[l] = ly.BN;
+            fa.N[l] = ly.N_valid;
+        }
+        fa.L = L;
+        fa.c = c;
+        fa.freq = nif->mlp_freq;
+        fa.esc = esc;
+        fa.esc_beta = esc_beta;
+        fa.count = count;
+        fa.out = out;
+        fa.dir_input = dir_input;
+        const int64_t tiles = (max_rows + kBM - 1) / kBM;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, num_sms()));   // x CTAs per SM
+        return H == 256 ? launch_fused_t<256>(fa, grid, st) : H == 128 ? launch_fused_t<128>(fa, grid, st)
+                                                                         : launch_fused_t<64>(fa, grid, st);
+    }
     const int kc_of_H = (H * (fp8 ? 1 : 2) + 127) / 128;          // K chunks of an H-wide activation row
     const int cap = (int)std::min<int64_t>(kChunkRows, ((max_rows + kBM - 1) / kBM) * kBM);
     const int64_t need = (int64_t)((cap + kBM - 1) / kBM) * kAChunk * kc_of_H;

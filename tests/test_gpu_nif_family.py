@@ -1,5 +1,6 @@
-"""GPU parity of the paper's NIF family of the size sweep (pt_nif_load_family, the
-layered tcgen05 GEMM path of mlp_kernel.cu) against the fp64 oracle (oracle.fr_eval_hl) on the same
+"""GPU parity of the paper's NIF family of the size sweep (pt_nif_load_family: the fused
+streamed-weight kernel for H <= 256 fp16, the layered tcgen05 GEMM path otherwise or with
+PT_MLP_LAYERED=1, both in mlp_kernel.cu) against the fp64 oracle (oracle.fr_eval_hl) on the same
 seeded networks and queries. Gates as for the other NIFs: |dy| <= 1e-3 in log
 space and relative error of exp(y) <= 1e-2, plus a derived bound for the wide nets: the fp16 rounding of
 each layer's activations (2^-11 relative) propagated through the |W| row sums."""
@@ -47,10 +48,23 @@ def _log_gate(H, L, blob):
     return max(NIF_LOG_GATE, 3.0 * g)
 
 
-@pytest.mark.parametrize("H,L", scenes.NIF_SWEEP)
+@pytest.fixture(params=["fused", "layered"])
+def mlp_path(request, monkeypatch):
+    if request.param == "layered":
+        monkeypatch.setenv("PT_MLP_LAYERED", "1")
+    else:
+        monkeypatch.delenv("PT_MLP_LAYERED", raising=False)
+    return request.param
+
+
+@pytest.mark.parametrize("H,L", scenes.NIF_SWEEP + [(128, 6), (64, 3), (256, 16)])
 @pytest.mark.parametrize("n", [1, 129, 4 * 148 * 128 + 77])
-def test_family_vs_oracle(ptm, orc, H, L, n):
+def test_family_vs_oracle(ptm, orc, mlp_path, H, L, n):
     import torch
+    if H == 1024 and mlp_path == "fused":
+        pytest.skip("H1024 always runs the layered path")
+    if L > 8 and n > 129:
+        pytest.skip("deep member: small sizes only")
     blob = scenes.fourier_relu_family_blob(H, L, seed=1)
     nif = ptm.Nif(blob, kind=ptm.NIF_FR_FAMILY, hidden=H, layers=L)
     uv = _queries(n, seed=n + H)
@@ -63,7 +77,22 @@ def test_family_vs_oracle(ptm, orc, H, L, n):
     assert (np.abs(got[idx] - np.exp(y)) / np.exp(y)).max() <= NIF_REL_GATE
 
 
-def test_family_row_chunks(ptm, orc):
+def test_family_fused_equals_layered(ptm, monkeypatch):
+    """Same network, same fp16 activation roundings: the fused kernel and the layered GEMMs differ only
+    in fp32 accumulation order (both accumulate in tensor-core fp32)."""
+    import torch
+    for H, L in [(64, 2), (128, 4), (256, 4)]:
+        nif = ptm.Nif(scenes.fourier_relu_family_blob(H, L, seed=6), kind=ptm.NIF_FR_FAMILY, hidden=H, layers=L)
+        uv = torch.from_numpy(scenes.query_uv(50000, 8)).cuda()
+        monkeypatch.delenv("PT_MLP_LAYERED", raising=False)
+        a = ptm.nif_infer(nif, uv).log().cpu().numpy()
+        monkeypatch.setenv("PT_MLP_LAYERED", "1")
+        b = ptm.nif_infer(nif, uv).log().cpu().numpy()
+        monkeypatch.delenv("PT_MLP_LAYERED")
+        assert np.abs(a - b).max() <= 2e-3, (H, L)
+
+
+def test_family_row_chunks(ptm, orc, mlp_path):
     """More rows than one launch chunk (2^20): every chunk boundary and the ragged tail."""
     import torch
     H, L = 64, 2
