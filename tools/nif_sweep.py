@@ -40,7 +40,7 @@ nets = [("siren", pt.Nif(scenes.siren_blob(0)), 3 * 2 * 128 * 128 + 2 * (2 * 128
 for fp8 in (False, True):
     for H, L in scenes.NIF_SWEEP:
         path = "fused" if (not fp8 and H <= 256) else "layered"      # mlp_kernel.cu use_fused()
-        nets.append((f"paper_{path}_H{H}L{L}" + ("_fp8" if fp8 else ""),
+        nets.append((f"paper_family_{path}_H{H}L{L}" + ("_fp8" if fp8 else ""),
                      pt.Nif(scenes.fourier_relu_family_blob(H, L, seed=1), kind=pt.NIF_FR_FAMILY, hidden=H, layers=L,
                             fp8=fp8),
                      flops_of(scenes.fr_family_layers(H, L))))
