@@ -79,6 +79,22 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return y;
 }
 
+// n / d for n < 2^31, quotient < 2^20, with inv = fl(1 / d): the fp32 estimate is within one of the
+// quotient (relative error < 2^-22), then one exact correction each way; r = n - q d
+__device__ __forceinline__ uint32_t udiv_exact(uint32_t n, uint32_t d, float inv, uint32_t& r) {
+    uint32_t q = __float2uint_rz(__uint2float_rn(n) * inv);
+    int32_t rr = (int32_t)(n - q * d);
+    if (rr < 0) {
+        --q;
+        rr += (int32_t)d;
+    } else if (rr >= (int32_t)d) {
+        ++q;
+        rr -= (int32_t)d;
+    }
+    r = (uint32_t)rr;
+    return q;
+}
+
 __device__ __forceinline__ void ray_prepare(float3 o, float3 d, RayT& r) {
     int kz = 0;
     if (fabsf(d.y) > fabsf(d.x)) kz = 1;
@@ -183,8 +199,11 @@ __device__ __forceinline__ int tri_test32(const RayT& r, float3 v0, float3 v1, f
     const float dDet = eSum + (6.0f * eps) * maxE;
     const float adet = fabsf(det);
     if (adet <= 2.0f * dDet) return 2;
-    t = __fdiv_rn(T, det);
-    dt = 1.25f * ((dT + fabsf(t) * dDet) / (adet - dDet) + (2.0f * eps) * fabsf(t));
+    // t = T / det via rcp.approx (max error 1 ulp) and one rounded product: |t - T/det| <= 3 eps |t|
+    // (bounded with 6 eps); the bound's own quotient carries the same relative error, inside the 1.25
+    t = T * rcp_approx(det);
+    dt = 1.25f * ((dT + fabsf(t) * dDet) * rcp_approx(adet - dDet) + (6.0f * eps) * fabsf(t));
+    if (!(dt < CUDART_INF_F)) return 2;          // subnormal det (flushed by rcp.approx.ftz) or overflow
     if (t + dt <= 0.0f) return 0;
     if (t - dt <= 0.0f) return 2;
     return 1;
@@ -528,6 +547,7 @@ struct ShadeArgs {
     TraceParams tp;
     Cam32 cam;
     int W, H, first_sample, depth, max_depth;
+    float inv_np, inv_w;        // 1 / (W H), 1 / W for udiv_exact
     uint2 key;
     const uint32_t* counters;   // the wave's counters (pt_internal.h kCounters layout)
     uint32_t n_slots;           // paths of the wave
@@ -602,8 +622,9 @@ __device__ __forceinline__ void shade_segment(const ShadeArgs& a, int depth, uin
         return;
     }
     if (depth >= a.max_depth) return;                 // capped: no further segment, no env (reading R7)
-    const int p = (int)(slot % (uint32_t)np);
-    const int s = a.first_sample + (int)(slot / (uint32_t)np);
+    uint32_t pu;
+    const int s = a.first_sample + (int)udiv_exact(slot, (uint32_t)np, a.inv_np, pu);
+    const int p = (int)pu;
     const uint4 rr = philox10(make_uint4((uint32_t)p, (uint32_t)s, (uint32_t)depth, 0u), a.key);
     const float xi0 = u01f(rr.x), xi1 = u01f(rr.y), xi2 = u01f(rr.z), xi3 = u01f(rr.w);
     const bool entering = cosd < 0.0f;
@@ -613,7 +634,7 @@ __device__ __forceinline__ void shade_segment(const ShadeArgs& a, int depth, uin
     if (m.kind == PT_LAMBERT) {
         // cosine-weighted hemisphere, ONB of Duff et al. 2017 (reading R9)
         const float sg = copysignf(1.0f, n.z);
-        const float aa = -1.0f / (sg + n.z);
+        const float aa = -rcp_approx(sg + n.z);           // |sg + n.z| in [1, 2]
         const float bb = n.x * n.y * aa;
         const float3 t1 = make_float3(1.0f + sg * n.x * n.x * aa, sg * bb, -sg * n.x);
         const float3 t2 = make_float3(bb, sg + n.y * n.y * aa, -n.y);
@@ -676,10 +697,12 @@ __device__ __forceinline__ void shade_segment(const ShadeArgs& a, int depth, uin
 // The camera ray of wave slot i = (pixel i % np, sample first + i / np) (S1, reading R22)
 __device__ __forceinline__ float3 camera_ray(const ShadeArgs& a, uint32_t i) {
     const int np = a.W * a.H;
-    const int p = (int)(i % (uint32_t)np);
-    const int sm = a.first_sample + (int)(i / (uint32_t)np);
+    uint32_t pu, px;
+    const int sm = a.first_sample + (int)udiv_exact(i, (uint32_t)np, a.inv_np, pu);
+    const int p = (int)pu;
+    const uint32_t py = udiv_exact(pu, (uint32_t)a.W, a.inv_w, px);
     const uint4 r = philox10(make_uint4((uint32_t)p, (uint32_t)sm, 0u, 0u), a.key);
-    return cam_dir(a.cam, a.W, a.H, p % a.W, p / a.W, u01f(r.x), u01f(r.y));
+    return cam_dir(a.cam, a.W, a.H, (int)px, (int)py, u01f(r.x), u01f(r.y));
 }
 
 #ifndef PT_TS_MINB
@@ -888,6 +911,8 @@ void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int fir
     a.tp = tp;
     a.cam = cam;
     a.W = W; a.H = H; a.first_sample = first_sample; a.depth = 1; a.max_depth = max_depth;
+    a.inv_np = 1.0f / (float)((int64_t)W * H);
+    a.inv_w = 1.0f / (float)W;
     a.key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
     a.counters = ws.counters;
     a.alive_count = ws.counters + kCounterAlive;
