@@ -175,4 +175,30 @@ void mlp_free(pt_nif* nif);
 cudaError_t launch_mlp(pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count, int64_t max_rows,
                        float* out, int dir_input, cudaStream_t st);
 
+// Programmatic dependent launch along the wave's kernel chain (first_bounce -> path -> siren ->
+// accumulate): a kernel launched with launch_pdl may be scheduled while its predecessor drains (the
+// predecessor calls pdl_trigger() once all its CTAs are resident); it runs its input-independent prologue
+// (barrier init, TMEM alloc, weight copies) and calls pdl_wait() before touching the predecessor's
+// outputs (griddepcontrol.wait: the predecessor has completed and its memory is visible). Both are
+// no-ops for a normal launch. PT_NO_PDL=1 launches normally (A/B measurement).
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#endif
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 }  // namespace pt

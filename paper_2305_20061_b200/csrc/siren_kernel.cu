@@ -145,8 +145,7 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const uint32_t n_rows = *count;
-    const uint32_t n_tiles = (n_rows + kTileM - 1) / kTileM;
+    pdl_trigger();
 
     if (warp == 1 && lane == 0) {
         mbar_init(bar(kBarW), 1);
@@ -170,8 +169,9 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 1 && lane == 0 && blockIdx.x < n_tiles) {
-        // stage the whole weight image once (bulk TMA copies, complete_tx on the weight barrier)
+    if (warp == 1 && lane == 0) {
+        // stage the whole weight image once (bulk TMA copies, complete_tx on the weight barrier); the
+        // image is the NIF's own, so this runs before the wait on the previous kernel of the wave
         mbar_expect_tx(bar(kBarW), (uint32_t)kImageBytes);
         constexpr int kChunk = 16384;
         for (int off = 0; off < kImageBytes; off += kChunk) {
@@ -183,6 +183,10 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
                 : "memory");
         }
     }
+
+    pdl_wait();                       // the escaped queue and its count are complete and visible
+    const uint32_t n_rows = *count;
+    const uint32_t n_tiles = (n_rows + kTileM - 1) / kTileM;
 
     if (warp == 0) {
         // ===== MMA issuer: warp 0 walks the schedule, one elected lane issues =====
@@ -374,6 +378,8 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
             }
         }
     }
+    // a CTA without tiles still owns the weight copies in flight into its shared memory
+    if (warp == 1 && lane == 0 && blockIdx.x >= n_tiles) mbar_wait(bar(kBarW), 0);
     tc_fence_before();
     __syncthreads();
     if (warp == 0) {
@@ -392,9 +398,8 @@ static cudaError_t siren_launch_t(const pt_nif* nif, const float4* esc, const fl
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    siren_kernel<kDebug><<<grid, siren::kThreads, siren::kSmemBytes, st>>>((const uint8_t*)nif->d_smem_image, esc,
-                                                                           esc_beta, count, out, dbg, dir_input);
-    return cudaGetLastError();
+    return launch_pdl(siren_kernel<kDebug>, dim3(grid), dim3(siren::kThreads), siren::kSmemBytes, st,
+                      (const uint8_t*)nif->d_smem_image, esc, esc_beta, count, out, dbg, dir_input);
 }
 
 cudaError_t launch_siren(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count, int grid,

@@ -15,6 +15,8 @@
 #include <math_constants.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #include "pt_internal.h"
 
 namespace pt {
@@ -744,6 +746,7 @@ __device__ __forceinline__ void write_radiance(const ShadeArgs& a, const SegOut&
 #define PT_FB_MINB PT_TS_MINB   // the first bounce's own register cap (tools/ts_tune.sh)
 #endif
 __global__ void __launch_bounds__(128, PT_FB_MINB) first_bounce_kernel(ShadeArgs a) {
+    pdl_trigger();                    // all CTAs resident (grid = resident capacity): let path_kernel queue
     const uint32_t n = a.n_slots;
     const int lane = threadIdx.x & 31;
     uint32_t segs = 0;
@@ -780,6 +783,8 @@ __global__ void __launch_bounds__(128, PT_FB_MINB) first_bounce_kernel(ShadeArgs
 // per bounce. Per-path results do not depend on the schedule: the RNG is keyed by (pixel, sample,
 // depth) and every path writes only its own slot.
 __global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
+    pdl_wait();                       // first_bounce complete: its queue and counters are visible
+    pdl_trigger();
     const uint32_t n = *a.alive_count;
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
@@ -839,6 +844,7 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
 __global__ void accumulate_kernel(const float* __restrict__ wave_buf, int n_elems, int k, float* __restrict__ fb,
                                   const uint32_t* __restrict__ counters, unsigned long long* __restrict__ stats,
                                   uint32_t paths) {
+    pdl_wait();
     if (blockIdx.x == 0 && threadIdx.x == 0 && stats) {
         stats[0] += paths;
         stats[1] += counters[kCounterSeg];
@@ -897,6 +903,14 @@ static int grid_for(int64_t n, int block, int per_sm) {
 }
 
 // persistent grids: exactly the resident block count (one wave), so no SM idles behind a partial wave
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("PT_NO_PDL");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+
 template <typename K>
 static int resident_grid(K kernel, int block) {
     int per_sm = 0;
@@ -927,14 +941,15 @@ void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int fir
     first_bounce_kernel<<<grid1, 128, 0, st>>>(a);
     if (max_depth > 1) {
         a.work = ws.counters + kCounterWork + 1;
-        path_kernel<<<grid2, 128, 0, st>>>(a);
+        launch_pdl(path_kernel, dim3(grid2), dim3(128), 0, st, a);
     }
 }
 
 void launch_accumulate(const float* wave_buf, int n_pix, int k, float* fb, const uint32_t* counters,
                        unsigned long long* stats, uint32_t paths, cudaStream_t st) {
     const int n = 3 * n_pix;
-    accumulate_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(wave_buf, n, k, fb, counters, stats, paths);
+    launch_pdl(accumulate_kernel, dim3(grid_for(n, 256, 8)), dim3(256), 0, st, wave_buf, n, k, fb, counters, stats,
+               paths);
 }
 
 void launch_primary(const TraceParams& tp, const Cam32& cam, int W, int H, int sample, uint64_t seed, int32_t* prim,
