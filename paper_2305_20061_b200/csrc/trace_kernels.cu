@@ -857,7 +857,7 @@ __global__ void accumulate_kernel(const float* __restrict__ wave_buf, int n_elem
     }
 }
 
-__global__ void primary_kernel(TraceParams tp, Cam32 cam, int W, int H, int sample, uint2 key, int32_t* prim,
+__global__ void __launch_bounds__(128, PT_TS_MINB) primary_kernel(TraceParams tp, Cam32 cam, int W, int H, int sample, uint2 key, int32_t* prim,
                                float* tout) {
     const int np = W * H;
     for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < np; p += gridDim.x * blockDim.x) {
@@ -869,7 +869,7 @@ __global__ void primary_kernel(TraceParams tp, Cam32 cam, int W, int H, int samp
     }
 }
 
-__global__ void trace_rays_kernel(TraceParams tp, const float* o, const float* d, int64_t n, int32_t* prim, float* tout) {
+__global__ void __launch_bounds__(128, PT_TS_MINB) trace_rays_kernel(TraceParams tp, const float* o, const float* d, int64_t n, int32_t* prim, float* tout) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const Hit h = closest_hit(tp, make_float3(o[3 * i], o[3 * i + 1], o[3 * i + 2]),
                                   make_float3(d[3 * i], d[3 * i + 1], d[3 * i + 2]));
@@ -955,12 +955,12 @@ void launch_accumulate(const float* wave_buf, int n_pix, int k, float* fb, const
 void launch_primary(const TraceParams& tp, const Cam32& cam, int W, int H, int sample, uint64_t seed, int32_t* prim,
                     float* t, cudaStream_t st) {
     const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
-    primary_kernel<<<grid_for((int64_t)W * H, 128, 8), 128, 0, st>>>(tp, cam, W, H, sample, key, prim, t);
+    primary_kernel<<<grid_for((int64_t)W * H, 128, PT_TS_MINB), 128, 0, st>>>(tp, cam, W, H, sample, key, prim, t);
 }
 
 void launch_trace_rays(const TraceParams& tp, const float* o, const float* d, int64_t n, int32_t* prim, float* t,
                        cudaStream_t st) {
-    trace_rays_kernel<<<grid_for(n, 128, 8), 128, 0, st>>>(tp, o, d, n, prim, t);
+    trace_rays_kernel<<<grid_for(n, 128, PT_TS_MINB), 128, 0, st>>>(tp, o, d, n, prim, t);
 }
 
 void launch_scale(float* fb, int64_t n, float s, cudaStream_t st) {
