@@ -303,3 +303,27 @@ def test_invalid_arguments_raise(ptm, blob):
         ptm.render(s, ptm.Nif(blob), 4, 4, 1, 0)
     with pytest.raises(ptm.PtError):
         ptm.Nif(blob[:-1])
+
+
+def test_render_closed_box_no_escapes(ptm, orc, blob):
+    """Camera inside a closed box: no path escapes, so the NIF queue is empty in every wave (the NIF
+    kernels launch with a zero row count and must only drain their prologue). The frame equals the
+    oracle's (emitter light only), and is bit-identical whichever NIF is attached."""
+    sc = scenes.box_scene()
+    h = 0.5
+    front = scenes._quad((-h, -h, h), (-h, h, h), (h, h, h), (h, -h, h), 0)      # -z, closes the box
+    sc.tris = np.concatenate([sc.tris, front])
+    sc.camera = scenes._camera((0.0, 0.0, 0.4), (0.0, 0.0, -0.5), (0.0, 1.0, 0.0), 60.0)
+    W, H, spp, depth = 24, 16, 4, 6
+    S = ptm.Scene(sc)
+    img = ptm.render(S, ptm.Nif(blob), W, H, spp, depth, seed=3)
+    assert S.stats()["escaped"] == 0
+    ref, st = orc.OracleScene(sc).render(W, H, depth, 3, s0=0, s1=spp, nif_blob=blob)
+    assert st["escaped"] == 0
+    assert _rel_rmse(img, ref.reshape(H, W, 3) / spp) <= REL_RMSE_GATE
+    others = [ptm.Nif(scenes.fourier_relu_blob(0), kind=ptm.NIF_FOURIER_RELU),
+              ptm.Nif(scenes.fourier_relu_family_blob(64, 2, seed=1), kind=ptm.NIF_FR_FAMILY, hidden=64, layers=2),
+              ptm.Nif(scenes.fourier_relu_family_blob(1024, 8, seed=1), kind=ptm.NIF_FR_FAMILY, hidden=1024,
+                      layers=8)]
+    for nif in others:
+        assert np.array_equal(ptm.render(ptm.Scene(sc), nif, W, H, spp, depth, seed=3), img)
