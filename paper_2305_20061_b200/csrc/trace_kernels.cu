@@ -61,17 +61,35 @@ __device__ __forceinline__ float3 cam_dir(const Cam32& k, int W, int H, int x, i
 // mixed signs by more than a proven fp32 error bound; every remaining candidate is decided in fp64
 // with explicitly rounded intrinsics in the oracle's operation order (R22).
 // ---------------------------------------------------------------------------------------------
+// Kept compact (14 registers) because it is live through the whole traversal under the path kernels'
+// 72-register cap; the shear matrix of the certified pre-test is rebuilt inside each triangle test.
 struct RayT {
     float o[3], d[3], inv[3];   // slab test, sphere test
-    // fp32 shear of the certified pre-test as a matrix over the world axes a, so a vertex is sheared with
-    // packed FFMA2s instead of permutation selects: (Ax, Ay) = sum_a mxy[a] (v - o)_a with mxy[a] =
-    // ((e_kx - Sx e_kz)_a, (e_ky - Sy e_kz)_a), Az = sum_a mz[a] (v - o)_a with mz = Sz e_kz
+    float Sx, Sy, rz, adkz;     // fp32 shear constants, |d[kz]| for the error bounds
+    uint32_t kbits;             // kx | ky << 2 | kz << 4 | negmask << 8 (bit a: d[a] has its sign bit set)
+};
+__device__ __forceinline__ int ray_kx(const RayT& r) { return (int)(r.kbits & 3u); }
+__device__ __forceinline__ int ray_ky(const RayT& r) { return (int)((r.kbits >> 2) & 3u); }
+__device__ __forceinline__ int ray_kz(const RayT& r) { return (int)((r.kbits >> 4) & 3u); }
+// fp32 shear as a matrix over the world axes a, so a vertex is sheared with packed FFMA2s instead of
+// permutation selects: (Ax, Ay) = sum_a mxy[a] (v - o)_a with mxy[a] = ((e_kx - Sx e_kz)_a,
+// (e_ky - Sy e_kz)_a), Az = sum_a mz[a] (v - o)_a with mz = Sz e_kz
+struct Shear32 {
     float2 mxy[3];
     float mz[3];
-    float aSx, aSy, adkz;       // |Sx|, |Sy|, |d[kz]| for the error bounds
-    int kx, ky, kz;
-    unsigned negmask;     // bit a: d[a] has its sign bit set
 };
+__device__ __forceinline__ Shear32 shear_matrix(const RayT& r) {
+    uint32_t kb = r.kbits;
+    asm volatile("" : "+r"(kb));   // rebuilt per test: keep the compiler from hoisting it into registers
+    const int kx = (int)(kb & 3u), ky = (int)((kb >> 2) & 3u), kz = (int)((kb >> 4) & 3u);
+    Shear32 m;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        m.mxy[a] = make_float2(a == kx ? 1.0f : (a == kz ? -r.Sx : 0.0f), a == ky ? 1.0f : (a == kz ? -r.Sy : 0.0f));
+        m.mz[a] = a == kz ? r.rz : 0.0f;
+    }
+    return m;
+}
 
 __device__ __forceinline__ float self3(float3 v, int k) { return k == 0 ? v.x : (k == 1 ? v.y : v.z); }
 
@@ -105,25 +123,20 @@ __device__ __forceinline__ void ray_prepare(float3 o, float3 d, RayT& r) {
     int ky = kx + 1; if (ky == 3) ky = 0;
     const float dkz = self3(d, kz);
     if (dkz < 0.0f) { int t = kx; kx = ky; ky = t; }
-    r.kx = kx; r.ky = ky; r.kz = kz;
     // fp32 shear for the pre-test only (its error bound tolerates the reciprocal-multiply form);
     // the fp64 shear of the exact test is recomputed by each (rare) fp64 test: caching it would keep
     // six more registers live through the whole traversal
     const float rz = __frcp_rn(dkz);
-    const float Sx = self3(d, kx) * rz, Sy = self3(d, ky) * rz;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        r.mxy[a] = make_float2(a == kx ? 1.0f : (a == kz ? -Sx : 0.0f), a == ky ? 1.0f : (a == kz ? -Sy : 0.0f));
-        r.mz[a] = a == kz ? rz : 0.0f;
-    }
-    r.aSx = fabsf(Sx);
-    r.aSy = fabsf(Sy);
+    r.Sx = self3(d, kx) * rz;
+    r.Sy = self3(d, ky) * rz;
+    r.rz = rz;
     r.adkz = fabsf(dkz);
     r.o[0] = o.x; r.o[1] = o.y; r.o[2] = o.z;
     r.d[0] = d.x; r.d[1] = d.y; r.d[2] = d.z;
     // slab reciprocals: the SFU approximation (<= 1 ulp); the slab bound below allows for its rounding
     r.inv[0] = rcp_approx(d.x); r.inv[1] = rcp_approx(d.y); r.inv[2] = rcp_approx(d.z);
-    r.negmask = (signbit(d.x) ? 1u : 0u) | (signbit(d.y) ? 2u : 0u) | (signbit(d.z) ? 4u : 0u);
+    const uint32_t negmask = (signbit(d.x) ? 1u : 0u) | (signbit(d.y) ? 2u : 0u) | (signbit(d.z) ? 4u : 0u);
+    r.kbits = (uint32_t)kx | ((uint32_t)ky << 2) | ((uint32_t)kz << 4) | (negmask << 8);
 }
 
 // fp64 shear constants, exactly the oracle's divisions
@@ -132,22 +145,22 @@ struct Shear64 {
 };
 __device__ __forceinline__ Shear64 shear64(const RayT& r) {
     const float3 d = make_float3(r.d[0], r.d[1], r.d[2]);
-    const double dkz64 = (double)self3(d, r.kz);
-    return {__ddiv_rn((double)self3(d, r.kx), dkz64), __ddiv_rn((double)self3(d, r.ky), dkz64), __ddiv_rn(1.0, dkz64)};
+    const double dkz64 = (double)self3(d, ray_kz(r));
+    return {__ddiv_rn((double)self3(d, ray_kx(r)), dkz64), __ddiv_rn((double)self3(d, ray_ky(r)), dkz64), __ddiv_rn(1.0, dkz64)};
 }
 
 // Shear one vertex into the ray's frame: D = v - o (world axes, one rounding each), then the products
 // with the 0/1/-S entries of the shear rows; at most two roundings per sheared coordinate (the -S
 // product and the sum), the same single-rounding Sz D[kz] for Az as the permuted form.
-__device__ __forceinline__ void shear_vertex(const RayT& r, float3 v, float& x, float& y, float& z) {
+__device__ __forceinline__ void shear_vertex(const RayT& r, const Shear32& m, float3 v, float& x, float& y, float& z) {
     const float2 dxy = __fadd2_rn(make_float2(v.x, v.y), make_float2(-r.o[0], -r.o[1]));
     const float dz = v.z - r.o[2];
-    float2 a = __fmul2_rn(r.mxy[0], make_float2(dxy.x, dxy.x));
-    a = __ffma2_rn(r.mxy[1], make_float2(dxy.y, dxy.y), a);
-    a = __ffma2_rn(r.mxy[2], make_float2(dz, dz), a);
+    float2 a = __fmul2_rn(m.mxy[0], make_float2(dxy.x, dxy.x));
+    a = __ffma2_rn(m.mxy[1], make_float2(dxy.y, dxy.y), a);
+    a = __ffma2_rn(m.mxy[2], make_float2(dz, dz), a);
     x = a.x;
     y = a.y;
-    z = fmaf(r.mz[2], dz, fmaf(r.mz[1], dxy.y, r.mz[0] * dxy.x));
+    z = fmaf(m.mz[2], dz, fmaf(m.mz[1], dxy.y, m.mz[0] * dxy.x));
 }
 
 // Certified fp32 watertight test. Returns 0 if the exact (hence the fp64 oracle's) test certainly
@@ -164,17 +177,18 @@ __device__ __forceinline__ void shear_vertex(const RayT& r, float3 v, float& x, 
 __device__ __forceinline__ int tri_test32(const RayT& r, float3 v0, float3 v1, float3 v2, float& t, float& dt) {
     constexpr float eps = 0x1p-24f;
     float Ax, Ay, Az, Bx, By, Bz, Cx, Cy, Cz;
-    shear_vertex(r, v0, Ax, Ay, Az);
-    shear_vertex(r, v1, Bx, By, Bz);
-    shear_vertex(r, v2, Cx, Cy, Cz);
+    const Shear32 m = shear_matrix(r);
+    shear_vertex(r, m, v0, Ax, Ay, Az);
+    shear_vertex(r, m, v1, Bx, By, Bz);
+    shear_vertex(r, m, v2, Cx, Cy, Cz);
     const float CyBx = Cy * Bx, AyCx = Ay * Cx, ByAx = By * Ax;
     const float U = fmaf(Cx, By, -CyBx);
     const float V = fmaf(Ax, Cy, -AyCx);
     const float W = fmaf(Bx, Ay, -ByAx);
     const float mZ = (1.0f + 2.0f * eps) * fmaxf(fabsf(Az), fmaxf(fabsf(Bz), fabsf(Cz)));   // >= max|Sz A[kz]|
     const float mz2 = (1.0f + 4.0f * eps) * mZ * r.adkz;                                      // >= max|A[kz]|
-    const float mX = fmaf(2.0f * r.aSx, mz2, fmaxf(fabsf(Ax), fmaxf(fabsf(Bx), fabsf(Cx))));
-    const float mY = fmaf(2.0f * r.aSy, mz2, fmaxf(fabsf(Ay), fmaxf(fabsf(By), fabsf(Cy))));
+    const float mX = fmaf(2.0f * fabsf(r.Sx), mz2, fmaxf(fabsf(Ax), fmaxf(fabsf(Bx), fabsf(Cx))));
+    const float mY = fmaf(2.0f * fabsf(r.Sy), mz2, fmaxf(fabsf(Ay), fmaxf(fabsf(By), fabsf(Cy))));
     float eU = (26.0f * eps) * mX * mY, eV = eU, eW = eU;
     bool neg = U < -eU || V < -eV || W < -eW;
     bool pos = U > eU || V > eV || W > eW;
@@ -215,16 +229,17 @@ __device__ __forceinline__ int tri_test32(const RayT& r, float3 v0, float3 v1, f
 __device__ __forceinline__ bool tri_test64(RayT& r, float3 v0, float3 v1, float3 v2, double& t_out) {
     const Shear64 sh = shear64(r);
     const float3 o32 = make_float3(r.o[0], r.o[1], r.o[2]);
-    const double ox = self3(o32, r.kx), oy = self3(o32, r.ky), oz = self3(o32, r.kz);
-    const double A0 = __dsub_rn((double)self3(v0, r.kx), ox);
-    const double A1 = __dsub_rn((double)self3(v0, r.ky), oy);
-    const double A2 = __dsub_rn((double)self3(v0, r.kz), oz);
-    const double B0 = __dsub_rn((double)self3(v1, r.kx), ox);
-    const double B1 = __dsub_rn((double)self3(v1, r.ky), oy);
-    const double B2 = __dsub_rn((double)self3(v1, r.kz), oz);
-    const double C0 = __dsub_rn((double)self3(v2, r.kx), ox);
-    const double C1 = __dsub_rn((double)self3(v2, r.ky), oy);
-    const double C2 = __dsub_rn((double)self3(v2, r.kz), oz);
+    const int kx = ray_kx(r), ky = ray_ky(r), kz = ray_kz(r);
+    const double ox = self3(o32, kx), oy = self3(o32, ky), oz = self3(o32, kz);
+    const double A0 = __dsub_rn((double)self3(v0, kx), ox);
+    const double A1 = __dsub_rn((double)self3(v0, ky), oy);
+    const double A2 = __dsub_rn((double)self3(v0, kz), oz);
+    const double B0 = __dsub_rn((double)self3(v1, kx), ox);
+    const double B1 = __dsub_rn((double)self3(v1, ky), oy);
+    const double B2 = __dsub_rn((double)self3(v1, kz), oz);
+    const double C0 = __dsub_rn((double)self3(v2, kx), ox);
+    const double C1 = __dsub_rn((double)self3(v2, ky), oy);
+    const double C2 = __dsub_rn((double)self3(v2, kz), oz);
     const double Ax = __dsub_rn(A0, __dmul_rn(sh.Sx, A2));
     const double Ay = __dsub_rn(A1, __dmul_rn(sh.Sy, A2));
     const double Bx = __dsub_rn(B0, __dmul_rn(sh.Sx, B2));
@@ -423,7 +438,7 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
     // per-axis fp16x2 half swap so that t.x is always the near slab plane and t.y the far one
     uint32_t swz[3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) swz[a] = ((r.negmask >> a) & 1u) ? 0x1032u : 0x3210u;
+    for (int a = 0; a < 3; ++a) swz[a] = ((r.kbits >> (8 + a)) & 1u) ? 0x1032u : 0x3210u;
     uint2 stack[kStackSize];
     int sp = 0;
     const uint4* __restrict__ pool = tp.pool;
