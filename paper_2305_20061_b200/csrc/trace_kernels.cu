@@ -420,12 +420,11 @@ __device__ __forceinline__ void cswap(float& ta, uint32_t& oa, float& tb, uint32
 }
 
 // Traversal entries (stack, current node, postponed leaf): one word per child,
-//   interior node: its unit index (< 2^28);  leaf: unit index of its first primitive | kLeafBit |
-//   (count - 1) << 28;  kNoEntry: nothing.
-constexpr uint32_t kLeafBit = 0x80000000u;
-constexpr uint32_t kNoEntry = 0x7FFFFFFFu;
+//   interior node: its unit index (< 2^28);  leaf: unit index of its first primitive | (3 count) << 28,
+//   i.e. the child's size nibble itself (one IMAD to form);  kNoEntry: nothing.
+constexpr uint32_t kNoEntry = 0xFFFFFFFFu;
 __device__ __forceinline__ bool is_node(uint32_t e) { return e < (1u << 28); }
-__device__ __forceinline__ bool is_leaf(uint32_t e) { return (e & kLeafBit) != 0; }
+__device__ __forceinline__ bool is_leaf(uint32_t e) { return e - (1u << 28) < 0xE0000000u; }   // nibble 1..14
 
 __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
     Hit best{CUDART_INF, CUDART_INF_F, CUDART_INF_F, -1, 0u, true};
@@ -485,7 +484,6 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
                     const uint32_t nib = (meta >> (4 * ci)) & 15u;
                     const bool valid = nib != 0u;
                     const bool lf = nib != (uint32_t)kNodeUnits;
-                    const uint32_t cm1 = ((nib * 86u) >> 8) - 1u;       // count - 1 = nib / 3 - 1 for leaves
                     float tn = 0.0f, tf = CUDART_INF_F;
 #pragma unroll
                     for (int a = 0; a < 3; ++a) {
@@ -502,7 +500,7 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
                     tf = tf * kGrow;
                     const bool hit = valid && tn <= tf && tn <= tcull0;
                     ctn[ci] = hit ? tn : CUDART_INF_F;
-                    cent[ci] = lf ? (off | kLeafBit | (cm1 << 28)) : off;
+                    cent[ci] = off + ((lf ? nib : 0u) << 28);
                     off += nib;
                 }
                 // sort the children by entry distance (network of 5 compare-swaps), push all but the
@@ -534,7 +532,7 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
         // ---- phase 2: primitives of the postponed leaf (and of leaves met next) ---------------------
         while (leaf != kNoEntry) {
             if (leaf_t <= cull_bound(best)) {
-                const uint32_t cnt = ((leaf >> 28) & 3u) + 1u;
+                const uint32_t cnt = ((leaf >> 28) * 86u) >> 8;   // nibble / 3
                 uint32_t unit = leaf & 0x0FFFFFFFu;
                 for (uint32_t k = 0; k < cnt; ++k, unit += kPrimUnits) test_prim(pool, unit, r, best);
             }
