@@ -64,10 +64,24 @@ __device__ __forceinline__ float3 cam_dir(const Cam32& k, int W, int H, int x, i
 // Kept compact (14 registers) because it is live through the whole traversal under the path kernels'
 // 72-register cap; the shear matrix of the certified pre-test is rebuilt inside each triangle test.
 struct RayT {
-    float o[3], d[3], inv[3];   // slab test, sphere test
-    float Sx, Sy, rz, adkz;     // fp32 shear constants, |d[kz]| for the error bounds
+    float o[3], inv[3];         // slab test
     uint32_t kbits;             // kx | ky << 2 | kz << 4 | negmask << 8 (bit a: d[a] has its sign bit set)
+    uint32_t cold;              // local-memory address of (Sx, Sy, rz, |d[kz]|) (d.x, d.y, d.z, 0): only
+                                // primitive tests read them, so they are spilled by hand, not by ptxas
 };
+__device__ __forceinline__ float4 ldl4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.local.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void stl4(uint32_t a, float4 v) {
+    asm volatile("st.local.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+__device__ __forceinline__ float4 ray_shear_consts(const RayT& r) { return ldl4(r.cold); }   // Sx, Sy, rz, |d[kz]|
+__device__ __forceinline__ float3 ray_dir(const RayT& r) {
+    const float4 v = ldl4(r.cold + 16);
+    return make_float3(v.x, v.y, v.z);
+}
 __device__ __forceinline__ int ray_kx(const RayT& r) { return (int)(r.kbits & 3u); }
 __device__ __forceinline__ int ray_ky(const RayT& r) { return (int)((r.kbits >> 2) & 3u); }
 __device__ __forceinline__ int ray_kz(const RayT& r) { return (int)((r.kbits >> 4) & 3u); }
@@ -78,15 +92,15 @@ struct Shear32 {
     float2 mxy[3];
     float mz[3];
 };
-__device__ __forceinline__ Shear32 shear_matrix(const RayT& r) {
+__device__ __forceinline__ Shear32 shear_matrix(const RayT& r, float4 sc) {
     uint32_t kb = r.kbits;
     asm volatile("" : "+r"(kb));   // rebuilt per test: keep the compiler from hoisting it into registers
     const int kx = (int)(kb & 3u), ky = (int)((kb >> 2) & 3u), kz = (int)((kb >> 4) & 3u);
     Shear32 m;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        m.mxy[a] = make_float2(a == kx ? 1.0f : (a == kz ? -r.Sx : 0.0f), a == ky ? 1.0f : (a == kz ? -r.Sy : 0.0f));
-        m.mz[a] = a == kz ? r.rz : 0.0f;
+        m.mxy[a] = make_float2(a == kx ? 1.0f : (a == kz ? -sc.x : 0.0f), a == ky ? 1.0f : (a == kz ? -sc.y : 0.0f));
+        m.mz[a] = a == kz ? sc.z : 0.0f;
     }
     return m;
 }
@@ -115,7 +129,7 @@ __device__ __forceinline__ uint32_t udiv_exact(uint32_t n, uint32_t d, float inv
     return q;
 }
 
-__device__ __forceinline__ void ray_prepare(float3 o, float3 d, RayT& r) {
+__device__ __forceinline__ void ray_prepare(float3 o, float3 d, RayT& r, uint32_t cold) {
     int kz = 0;
     if (fabsf(d.y) > fabsf(d.x)) kz = 1;
     if (fabsf(d.z) > fabsf(self3(d, kz))) kz = 2;
@@ -127,12 +141,10 @@ __device__ __forceinline__ void ray_prepare(float3 o, float3 d, RayT& r) {
     // the fp64 shear of the exact test is recomputed by each (rare) fp64 test: caching it would keep
     // six more registers live through the whole traversal
     const float rz = __frcp_rn(dkz);
-    r.Sx = self3(d, kx) * rz;
-    r.Sy = self3(d, ky) * rz;
-    r.rz = rz;
-    r.adkz = fabsf(dkz);
+    r.cold = cold;
+    stl4(cold, make_float4(self3(d, kx) * rz, self3(d, ky) * rz, rz, fabsf(dkz)));
+    stl4(cold + 16, make_float4(d.x, d.y, d.z, 0.0f));
     r.o[0] = o.x; r.o[1] = o.y; r.o[2] = o.z;
-    r.d[0] = d.x; r.d[1] = d.y; r.d[2] = d.z;
     // slab reciprocals: the SFU approximation (<= 1 ulp); the slab bound below allows for its rounding
     r.inv[0] = rcp_approx(d.x); r.inv[1] = rcp_approx(d.y); r.inv[2] = rcp_approx(d.z);
     const uint32_t negmask = (signbit(d.x) ? 1u : 0u) | (signbit(d.y) ? 2u : 0u) | (signbit(d.z) ? 4u : 0u);
@@ -144,7 +156,7 @@ struct Shear64 {
     double Sx, Sy, Sz;
 };
 __device__ __forceinline__ Shear64 shear64(const RayT& r) {
-    const float3 d = make_float3(r.d[0], r.d[1], r.d[2]);
+    const float3 d = ray_dir(r);
     const double dkz64 = (double)self3(d, ray_kz(r));
     return {__ddiv_rn((double)self3(d, ray_kx(r)), dkz64), __ddiv_rn((double)self3(d, ray_ky(r)), dkz64), __ddiv_rn(1.0, dkz64)};
 }
@@ -177,7 +189,8 @@ __device__ __forceinline__ void shear_vertex(const RayT& r, const Shear32& m, fl
 __device__ __forceinline__ int tri_test32(const RayT& r, float3 v0, float3 v1, float3 v2, float& t, float& dt) {
     constexpr float eps = 0x1p-24f;
     float Ax, Ay, Az, Bx, By, Bz, Cx, Cy, Cz;
-    const Shear32 m = shear_matrix(r);
+    const float4 sc = ray_shear_consts(r);
+    const Shear32 m = shear_matrix(r, sc);
     shear_vertex(r, m, v0, Ax, Ay, Az);
     shear_vertex(r, m, v1, Bx, By, Bz);
     shear_vertex(r, m, v2, Cx, Cy, Cz);
@@ -186,9 +199,9 @@ __device__ __forceinline__ int tri_test32(const RayT& r, float3 v0, float3 v1, f
     const float V = fmaf(Ax, Cy, -AyCx);
     const float W = fmaf(Bx, Ay, -ByAx);
     const float mZ = (1.0f + 2.0f * eps) * fmaxf(fabsf(Az), fmaxf(fabsf(Bz), fabsf(Cz)));   // >= max|Sz A[kz]|
-    const float mz2 = (1.0f + 4.0f * eps) * mZ * r.adkz;                                      // >= max|A[kz]|
-    const float mX = fmaf(2.0f * fabsf(r.Sx), mz2, fmaxf(fabsf(Ax), fmaxf(fabsf(Bx), fabsf(Cx))));
-    const float mY = fmaf(2.0f * fabsf(r.Sy), mz2, fmaxf(fabsf(Ay), fmaxf(fabsf(By), fabsf(Cy))));
+    const float mz2 = (1.0f + 4.0f * eps) * mZ * sc.w;                                        // >= max|A[kz]|
+    const float mX = fmaf(2.0f * fabsf(sc.x), mz2, fmaxf(fabsf(Ax), fmaxf(fabsf(Bx), fabsf(Cx))));
+    const float mY = fmaf(2.0f * fabsf(sc.y), mz2, fmaxf(fabsf(Ay), fmaxf(fabsf(By), fabsf(Cy))));
     float eU = (26.0f * eps) * mX * mY, eV = eU, eW = eU;
     bool neg = U < -eU || V < -eV || W < -eW;
     bool pos = U > eU || V > eV || W > eW;
@@ -263,7 +276,8 @@ __device__ __forceinline__ bool tri_test64(RayT& r, float3 v0, float3 v1, float3
 }
 
 __device__ __forceinline__ bool sph_test64(RayT& r, float3 c, float rad, double& t_out) {
-    const double d0 = r.d[0], d1 = r.d[1], d2 = r.d[2];
+    const float3 dd = ray_dir(r);
+    const double d0 = dd.x, d1 = dd.y, d2 = dd.z;
     const double oc0 = __dsub_rn((double)r.o[0], (double)c.x);
     const double oc1 = __dsub_rn((double)r.o[1], (double)c.y);
     const double oc2 = __dsub_rn((double)r.o[2], (double)c.z);
@@ -287,8 +301,9 @@ __device__ __forceinline__ bool sph_test64(RayT& r, float3 c, float rad, double&
 __device__ __forceinline__ int sph_test32(const RayT& r, float3 c, float rad, float& t, float& dt) {
     constexpr float eps = 0x1p-24f;
     const float ox = r.o[0] - c.x, oy = r.o[1] - c.y, oz = r.o[2] - c.z;
-    const float a = fmaf(r.d[0], r.d[0], fmaf(r.d[1], r.d[1], r.d[2] * r.d[2]));
-    const float b = fmaf(ox, r.d[0], fmaf(oy, r.d[1], oz * r.d[2]));
+    const float3 dd = ray_dir(r);
+    const float a = fmaf(dd.x, dd.x, fmaf(dd.y, dd.y, dd.z * dd.z));
+    const float b = fmaf(ox, dd.x, fmaf(oy, dd.y, oz * dd.z));
     const float oc2 = fmaf(ox, ox, fmaf(oy, oy, oz * oz));
     const float cc = oc2 - rad * rad;
     const float disc = fmaf(b, b, -a * cc);
@@ -429,8 +444,9 @@ __device__ __forceinline__ bool is_leaf(uint32_t e) { return e - (1u << 28) < 0x
 __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
     Hit best{CUDART_INF, CUDART_INF_F, CUDART_INF_F, -1, 0u, true};
     if (tp.empty) return best;
+    float4 cold[2];                   // local memory: written and read only through ld/st.local asm
     RayT r;
-    ray_prepare(o, d, r);
+    ray_prepare(o, d, r, (uint32_t)__cvta_generic_to_local(cold));
     // PBRT-v3's robust t_far * (1 + 2 gamma_3), with gamma_5: the approximate reciprocal adds up to
     // two more roundings' worth of relative error to each slab distance
     constexpr float kGrow = 1.0f + 2.0f * (5.0f * 0x1p-24f) / (1.0f - 5.0f * 0x1p-24f);   // 1 + 2 gamma_5
