@@ -393,11 +393,14 @@ __global__ void __launch_bounds__(mlpf::kThreads, fused_ctas_per_sm<kH>()) mlp_f
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);     // [0..5] full, [6..11] empty, [12] d_full, [13] a_ready
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 120);
     uint8_t* ring = smem + 1024;
+    float* sbias = reinterpret_cast<float*>(ring + kRing * kStage);   // [layer][kH]: the epilogue's biases
     auto bar = [&](int b) { return smem_u32(&bars[b]); };
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t n_rows = *a.count;
     const uint32_t n_tiles = (n_rows + mlp::kBM - 1) / mlp::kBM;
     if (blockIdx.x >= n_tiles) return;
+    for (int l = 0; l <= a.L; ++l)
+        for (int i = threadIdx.x; i < a.BN[l]; i += blockDim.x) sbias[l * kH + i] = __ldg(a.bias[l] + i);
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < kRing; ++s) {
             mbar_init(bar(s), 1);
@@ -507,13 +510,28 @@ __global__ void __launch_bounds__(mlpf::kThreads, fused_ctas_per_sm<kH>()) mlp_f
                              : "memory");
             }
         };
+        float4 en_next = make_float4(0.5f, 0.5f, 0.0f, 0.0f), beta_next = en_next;
+        {
+            const uint32_t r0 = blockIdx.x * mlp::kBM + 32 * q + lane;
+            if (r0 < n_rows) {
+                en_next = __ldg(a.esc + r0);
+                beta_next = __ldg(a.esc_beta + r0);
+            }
+        }
         for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
             const uint32_t row = t * mlp::kBM + 32 * q + lane;
             const bool valid = row < n_rows;
+            // this tile's queue entry was loaded one tile ahead (off the tile's critical path)
+            const float4 en = en_next, beta = beta_next;
+            {
+                const uint32_t tn = t + gridDim.x, rn = tn * mlp::kBM + 32 * q + lane;
+                if (tn < n_tiles && rn < n_rows) {
+                    en_next = __ldg(a.esc + rn);
+                    beta_next = __ldg(a.esc_beta + rn);
+                }
+            }
             float u = 0.5f, v = 0.5f;
-            float4 en = make_float4(0.5f, 0.5f, 0.0f, 0.0f);
             if (valid) {
-                en = __ldg(a.esc + row);
                 u = en.x;
                 v = en.y;
                 if (a.dir_input) equirect_f32(make_float3(en.x, en.y, en.z), u, v);
@@ -529,16 +547,16 @@ __global__ void __launch_bounds__(mlpf::kThreads, fused_ctas_per_sm<kH>()) mlp_f
                 tc_fence_after();
                 if (l < a.L) {
                     const int N = a.N[l];
-                    const float* bias = a.bias[l];
+                    const float* bias = sbias + l * kH;
                     for (int j = half; 32 * j < N; j += 2) {
                         uint32_t vv[32];
                         TMEM_LD32(D + 32 * j, vv);
                         tmem_wait_ld_dep(vv);
                         uint32_t pk[16];
-                        const float4* bp = reinterpret_cast<const float4*>(bias + 32 * j);
+                        const float4* bp = reinterpret_cast<const float4*>(bias + 32 * j);   // shared memory
 #pragma unroll
                         for (int g = 0; g < 8; ++g) {
-                            const float4 b4 = __ldg(bp + g);
+                            const float4 b4 = bp[g];
                             const float x0 = __uint_as_float(vv[4 * g]) + b4.x, x1 = __uint_as_float(vv[4 * g + 1]) + b4.y;
                             const float x2 = __uint_as_float(vv[4 * g + 2]) + b4.z, x3 = __uint_as_float(vv[4 * g + 3]) + b4.w;
                             asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(pk[2 * g]) : "f"(x1), "f"(x0));
@@ -566,14 +584,13 @@ __global__ void __launch_bounds__(mlpf::kThreads, fused_ctas_per_sm<kH>()) mlp_f
                         tmem_ld4(D, y);
                         tmem_wait_ld_dep4(y);
                         if (valid) {
-                            const float Y = __uint_as_float(y[0]) + __ldg(a.bias[l] + 0);
-                            const float U = __uint_as_float(y[1]) + __ldg(a.bias[l] + 1);
-                            const float V = __uint_as_float(y[2]) + __ldg(a.bias[l] + 2);
+                            const float Y = __uint_as_float(y[0]) + sbias[l * kH + 0];
+                            const float U = __uint_as_float(y[1]) + sbias[l * kH + 1];
+                            const float V = __uint_as_float(y[2]) + sbias[l * kH + 2];
                             const float r = fmaf(1.13983f, V, Y);
                             const float gch = fmaf(-0.58060f, V, fmaf(-0.39465f, U, Y));
                             const float bch = fmaf(2.03211f, U, Y);
                             const uint32_t slot = __float_as_uint(en.w);
-                            const float4 beta = __ldg(a.esc_beta + row);
                             a.out[3 * (size_t)slot + 0] = beta.x * __expf(r);
                             a.out[3 * (size_t)slot + 1] = beta.y * __expf(gch);
                             a.out[3 * (size_t)slot + 2] = beta.z * __expf(bch);
@@ -760,7 +777,7 @@ constexpr int kChunkRows = 1 << 20;
 
 template <int kH>
 static cudaError_t launch_fused_t(const mlpf::FusedArgs& fa, int grid, cudaStream_t st) {
-    const int smem = 1024 + mlpf::kRing * kH * 128;
+    const int smem = 1024 + mlpf::kRing * kH * 128 + mlpf::kMaxLayers * kH * 4;   // + the bias table
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(mlp_fused_kernel<kH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
