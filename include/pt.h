@@ -100,7 +100,7 @@ PT_API int pt_nif_load_ex(int32_t kind, const uint16_t* fp16_blob, int64_t n_hal
    ReLU layers; layer c = the largest odd index below layers/2 (0 if none) outputs hidden - 40 units and
    is concatenated with the 40 Fourier features. fp16_blob: B (40) then W_l [out][in], b_l [out] for the
    layers + 1 layers (n_halves = 40 + sum of fan_out * (fan_in + 1)). Evaluated, for hidden in {64, 128, 256}
-   at fp16, by one fused kernel (activations resident in TMEM, weights streamed from L2 chunk by chunk),
+   (fp16 or fp8), by one fused kernel (activations resident in TMEM, weights streamed from L2 chunk by chunk),
    otherwise as one tcgen05 GEMM per layer over the whole batch; the environment variable
    PT_MLP_LAYERED=1, read at each inference, forces the per-layer path (for tests). hidden: a multiple of
    64 in [64, 1024]; layers in [1, 16].

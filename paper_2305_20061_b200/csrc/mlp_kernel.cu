@@ -383,12 +383,15 @@ struct FusedArgs {
 template <int kH>
 constexpr int fused_ctas_per_sm() { return kH == 64 ? 3 : kH == 128 ? 2 : 1; }
 
-template <int kH>
+// kFp8: e4m3 weights, features and activations (reading R24), tcgen05 kind::f8f6f4 with A in TMEM:
+// a 128-B K-chunk is 128 elements and 4 MMAs of K = 32, so the MMA schedule and A column offsets are
+// those of fp16 (whose 128-B chunk is 64 elements, 4 MMAs of K = 16); A holds 4 activations per column.
+template <int kH, bool kFp8>
 __global__ void __launch_bounds__(mlpf::kThreads, fused_ctas_per_sm<kH>()) mlp_fused_kernel(mlpf::FusedArgs a) {
     using namespace mlpf;
     constexpr int kStage = kH * 128;                         // bytes of the widest weight chunk
     constexpr uint32_t kTmemCols = kH == 256 ? 512u : (kH == 128 ? 256u : 128u);
-    constexpr uint32_t kDCol = 0, kACol = kH;                // D: kH fp32 columns; A: kH / 2 columns
+    constexpr uint32_t kDCol = 0, kACol = kH;                // D: kH fp32 columns; A: kH / 2 (fp8: kH / 4) columns
     extern __shared__ __align__(1024) uint8_t smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);     // [0..5] full, [6..11] empty, [12] d_full, [13] a_ready
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 120);
@@ -461,8 +464,12 @@ __global__ void __launch_bounds__(mlpf::kThreads, fused_ctas_per_sm<kH>()) mlp_f
                         const uint32_t sb = smem_u32(ring + stage * kStage);
 #pragma unroll
                         for (int k = 0; k < 4; ++k)
-                            mma_ts(tmem + kDCol, tmem + kACol + (uint32_t)(32 * kc + 8 * k),
-                                   smem_desc(sb + k * 2 * lbo, lbo, 128), id, (kc | k) != 0);
+                        {
+                            const uint32_t at = tmem + kACol + (uint32_t)(32 * kc + 8 * k);
+                            const uint64_t bd = smem_desc(sb + k * 2 * lbo, lbo, 128);
+                            if (kFp8) mma_ts_f8(tmem + kDCol, at, bd, id, (kc | k) != 0);
+                            else mma_ts(tmem + kDCol, at, bd, id, (kc | k) != 0);
+                        }
                         mma_commit(bar(kRing + stage));
                     }
                     __syncwarp();
@@ -486,30 +493,51 @@ __global__ void __launch_bounds__(mlpf::kThreads, fused_ctas_per_sm<kH>()) mlp_f
         // Fourier features of this row into A element columns col0 .. col0 + 39: half 0 the 20 sines,
         // half 1 the 20 cosines; `pad` also zeroes element columns 40..63 (layer-0 input)
         auto write_features = [&](float u, float v, int col0, bool pad) {
-            uint32_t w[10];
+            float f[20];
 #pragma unroll
-            for (int j = 0; j < 10; ++j) {
-                float f[2];
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int fj = 2 * j + h;
-                    const float p = fmaf(__ldg(a.freq + 2 * fj), u, __ldg(a.freq + 2 * fj + 1) * v);
-                    const float r = p - rintf(p);
-                    f[h] = half == 0 ? __sinf(6.28318530717958647692f * r) : __cosf(6.28318530717958647692f * r);
-                }
-                w[j] = pack_half2(f[0], f[1]);
+            for (int fj = 0; fj < 20; ++fj) {
+                const float p = fmaf(__ldg(a.freq + 2 * fj), u, __ldg(a.freq + 2 * fj + 1) * v);
+                const float r = p - rintf(p);
+                f[fj] = half == 0 ? __sinf(6.28318530717958647692f * r) : __cosf(6.28318530717958647692f * r);
             }
-            const uint32_t c0 = A + (uint32_t)(col0 / 2 + 10 * half);
-            tmem_st8(c0, w);
-            asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(c0 + 8), "r"(w[8]), "r"(w[9])
-                         : "memory");
-            if (pad && half == 1) {
-                const uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                tmem_st8(A + 20, z);
-                asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%1,%1,%1};" ::"r"(A + 28), "r"(0u)
+            if (!kFp8) {
+                uint32_t w[10];
+#pragma unroll
+                for (int j = 0; j < 10; ++j) w[j] = pack_half2(f[2 * j], f[2 * j + 1]);
+                const uint32_t c0 = A + (uint32_t)(col0 / 2 + 10 * half);
+                tmem_st8(c0, w);
+                asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(c0 + 8), "r"(w[8]), "r"(w[9])
                              : "memory");
+                if (pad && half == 1) {
+                    const uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                    tmem_st8(A + 20, z);
+                    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%1,%1,%1};" ::"r"(A + 28), "r"(0u)
+                                 : "memory");
+                }
+            } else {
+                uint32_t w[5];
+#pragma unroll
+                for (int j = 0; j < 5; ++j)
+                    w[j] = mlp::e4m3x2(f[4 * j], f[4 * j + 1]) | (mlp::e4m3x2(f[4 * j + 2], f[4 * j + 3]) << 16);
+                const uint32_t c0 = A + (uint32_t)(col0 / 4 + 5 * half);
+                asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(c0), "r"(w[0]), "r"(w[1]),
+                             "r"(w[2]), "r"(w[3])
+                             : "memory");
+                asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(c0 + 4), "r"(w[4]) : "memory");
+                if (pad && half == 1) {                     // elements 40..127 (K = 128) = A columns 10..31
+                    const uint32_t z[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+                    TMEM_ST16(A + 10, z);
+                    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%1,%1,%1};" ::"r"(A + 26), "r"(0u)
+                                 : "memory");
+                    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%1};" ::"r"(A + 30), "r"(0u) : "memory");
+                }
             }
         };
+        if (kFp8 && kH == 64 && half == 0) {
+            // e4m3 K-chunks are 128 wide: A columns 16..31 (elements 64..127, zero weights) stay 0, not NaN
+            const uint32_t z[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+            TMEM_ST16(A + 16, z);
+        }
         float4 en_next = make_float4(0.5f, 0.5f, 0.0f, 0.0f), beta_next = en_next;
         {
             const uint32_t r0 = blockIdx.x * mlp::kBM + 32 * q + lane;
@@ -559,17 +587,36 @@ __global__ void __launch_bounds__(mlpf::kThreads, fused_ctas_per_sm<kH>()) mlp_f
                             const float4 b4 = bp[g];
                             const float x0 = __uint_as_float(vv[4 * g]) + b4.x, x1 = __uint_as_float(vv[4 * g + 1]) + b4.y;
                             const float x2 = __uint_as_float(vv[4 * g + 2]) + b4.z, x3 = __uint_as_float(vv[4 * g + 3]) + b4.w;
-                            asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(pk[2 * g]) : "f"(x1), "f"(x0));
-                            asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(pk[2 * g + 1]) : "f"(x3), "f"(x2));
+                            if (!kFp8) {
+                                asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(pk[2 * g]) : "f"(x1), "f"(x0));
+                                asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(pk[2 * g + 1]) : "f"(x3), "f"(x2));
+                            } else {
+                                pk[g] = mlp::e4m3x2(fmaxf(x0, 0.0f), fmaxf(x1, 0.0f)) |
+                                        (mlp::e4m3x2(fmaxf(x2, 0.0f), fmaxf(x3, 0.0f)) << 16);
+                            }
                         }
-                        if (32 * j + 32 <= N) {
-                            TMEM_ST16(A + 16 * j, pk);
+                        if (!kFp8) {
+                            if (32 * j + 32 <= N) {
+                                TMEM_ST16(A + 16 * j, pk);
+                            } else {
+                                // the concat layer's last chunk: 24 valid columns (H - 40 = 24 mod 32)
+                                tmem_st8(A + 16 * j, pk);
+                                asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(A + 16 * j + 8),
+                                             "r"(pk[8]), "r"(pk[9]), "r"(pk[10]), "r"(pk[11])
+                                             : "memory");
+                            }
                         } else {
-                            // the concat layer's last chunk: 24 valid columns (H - 40 = 24 mod 32)
-                            tmem_st8(A + 16 * j, pk);
-                            asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(A + 16 * j + 8),
-                                         "r"(pk[8]), "r"(pk[9]), "r"(pk[10]), "r"(pk[11])
-                                         : "memory");
+                            if (32 * j + 32 <= N) {
+                                tmem_st8(A + 8 * j, pk);
+                            } else {
+                                // 24 valid columns = 6 A columns of 4 e4m3
+                                asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(A + 8 * j),
+                                             "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3])
+                                             : "memory");
+                                asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(A + 8 * j + 4),
+                                             "r"(pk[4]), "r"(pk[5])
+                                             : "memory");
+                            }
                         }
                     }
                     if (l == a.c) write_features(u, v, kH - 40, false);   // the concat skip
@@ -775,24 +822,24 @@ static cudaError_t launch_layer(const MlpLayer& ly, int epi, int fp8, mlp::Layer
 // the chunk is empty, so the host never synchronises on the count.
 constexpr int kChunkRows = 1 << 20;
 
-template <int kH>
+template <int kH, bool kFp8>
 static cudaError_t launch_fused_t(const mlpf::FusedArgs& fa, int grid, cudaStream_t st) {
     const int smem = 1024 + mlpf::kRing * kH * 128 + mlpf::kMaxLayers * kH * 4;   // + the bias table
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(mlp_fused_kernel<kH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(mlp_fused_kernel<kH, kFp8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    mlp_fused_kernel<kH><<<grid * fused_ctas_per_sm<kH>(), mlpf::kThreads, smem, st>>>(fa);
+    mlp_fused_kernel<kH, kFp8><<<grid * fused_ctas_per_sm<kH>(), mlpf::kThreads, smem, st>>>(fa);
     return cudaGetLastError();
 }
 
-// The fused path serves H = 64, 128, 256 in fp16 (PT_MLP_LAYERED=1 forces the layered path, for tests)
+// The fused path serves H = 64, 128, 256 in fp16 and fp8 (PT_MLP_LAYERED=1 forces the layered path, for tests)
 static bool use_fused(const pt_nif* nif) {
     const char* env = std::getenv("PT_MLP_LAYERED");
     const bool layered = env && env[0] == '1';
-    return !layered && !nif->mlp_fp8 && (nif->mlp_H == 64 || nif->mlp_H == 128 || nif->mlp_H == 256) &&
+    return !layered && (nif->mlp_H == 64 || nif->mlp_H == 128 || nif->mlp_H == 256) &&
            nif->mlp_L + 1 <= mlpf::kMaxLayers;
 }
 
@@ -806,7 +853,7 @@ cudaError_t launch_mlp(pt_nif* nif, const float4* esc, const float4* esc_beta, c
             const MlpLayer& ly = nif->mlp_layers[l];
             fa.W[l] = (const uint8_t*)ly.d_w;
             fa.bias[l] = ly.d_bias;
-            fa.KC[l] = ly.K / 64;
+            fa.KC[l] = ly.K / (fp8 ? 128 : 64);
             fa.BN[l] = ly.BN;
             fa.N[l] = ly.N_valid;
         }
@@ -820,8 +867,11 @@ cudaError_t launch_mlp(pt_nif* nif, const float4* esc, const float4* esc_beta, c
         fa.dir_input = dir_input;
         const int64_t tiles = (max_rows + kBM - 1) / kBM;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, num_sms()));   // x CTAs per SM
-        return H == 256 ? launch_fused_t<256>(fa, grid, st) : H == 128 ? launch_fused_t<128>(fa, grid, st)
-                                                                         : launch_fused_t<64>(fa, grid, st);
+        if (fp8)
+            return H == 256 ? launch_fused_t<256, true>(fa, grid, st)
+                            : H == 128 ? launch_fused_t<128, true>(fa, grid, st) : launch_fused_t<64, true>(fa, grid, st);
+        return H == 256 ? launch_fused_t<256, false>(fa, grid, st)
+                        : H == 128 ? launch_fused_t<128, false>(fa, grid, st) : launch_fused_t<64, false>(fa, grid, st);
     }
     const int kc_of_H = (H * (fp8 ? 1 : 2) + 127) / 128;          // K chunks of an H-wide activation row
     const int cap = (int)std::min<int64_t>(kChunkRows, ((max_rows + kBM - 1) / kBM) * kBM);

@@ -2,8 +2,8 @@
 """NIF size sweep (Fig. nrf-vs-blender: H64 L2 311.8 M, H256 L4 149.1 M,
 H1024 L8 9.3 M paths/s on one GC200 with the Spheres scene).
 
-For each member of the paper's NIF family (pt_nif_load_family: the fused streamed-weight kernel for fp16
-H <= 256, the layered tcgen05 GEMM path for H1024 and fp8), the fused
+For each member of the paper's NIF family (pt_nif_load_family: the fused streamed-weight kernel for
+H <= 256, the layered tcgen05 GEMM path for H1024; fp16 and fp8 each), the fused
 paper NIF (H128 L4, PT_NIF_FOURIER_RELU) and the SIREN of the hot path:
   * inference microbenchmark: N uniform (u, v) queries, CUDA events, inferences/s and dense tensor
     TFLOP/s (2 x sum of fan_in x fan_out over the layers) against the measured bf16 peak;
@@ -39,7 +39,7 @@ nets = [("siren", pt.Nif(scenes.siren_blob(0)), 3 * 2 * 128 * 128 + 2 * (2 * 128
          flops_of(scenes.FR_LAYERS))]
 for fp8 in (False, True):
     for H, L in scenes.NIF_SWEEP:
-        path = "fused" if (not fp8 and H <= 256) else "layered"      # mlp_kernel.cu use_fused()
+        path = "fused" if H <= 256 else "layered"      # mlp_kernel.cu use_fused()
         nets.append((f"paper_family_{path}_H{H}L{L}" + ("_fp8" if fp8 else ""),
                      pt.Nif(scenes.fourier_relu_family_blob(H, L, seed=1), kind=pt.NIF_FR_FAMILY, hidden=H, layers=L,
                             fp8=fp8),
