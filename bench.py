@@ -281,7 +281,8 @@ def main():
     if world > 1:
         dist.barrier()
     t_wall = time.perf_counter() - t_wall0
-    ms = sum(a.elapsed_time(b) for a, b in evs)
+    step_ms = sorted(a.elapsed_time(b) for a, b in evs)
+    ms = sum(step_ms)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -404,6 +405,8 @@ def main():
         "kernels_ms_per_step": {k: v["ms_per_step"] for k, v in kernels.items()},
         "paths_per_step": paths / K, "segments_per_step": segments / K,
         "wall_s_timed_region": t_wall,
+        "step_ms": {"median": step_ms[len(step_ms) // 2], "best": step_ms[0], "worst": step_ms[-1],
+                    "note": "this rank's per-step device times (SURVEY 8d: median and best)"},
         "clocks": clocks,
     }
     if world == 1 and not args.no_cpu_baseline:
