@@ -195,8 +195,12 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--oracle-rows-every", type=int, default=8)
+    ap.add_argument("--wave-samples", type=int, default=0, help="samples per wave (default: the config's)")
     args = ap.parse_args()
     cfg = scenes.CONFIGS[args.config]
+    if args.wave_samples > 0:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, wave_samples=args.wave_samples)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))

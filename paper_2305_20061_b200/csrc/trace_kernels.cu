@@ -330,6 +330,19 @@ __device__ __forceinline__ int sph_test32(const RayT& r, float3 c, float rad, fl
 // ---------------------------------------------------------------------------------------------
 // Best hit so far. Decided exactly like the fp64 oracle, but carried as a certified fp32 interval
 // [tlo, thi] until a near-tie forces the exact fp64 t (exact == true).
+#ifdef PT_TAIL_TRACE
+// tail-analysis build (tools/tail_trace.py): globaltimer at each warp's exit, [kernel][warp]
+__device__ unsigned long long g_tail[2][1 << 14];
+__device__ __forceinline__ void tail_stamp(int k) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if ((threadIdx.x & 31) == 0 && w < (1 << 14)) g_tail[k][w] = t;
+}
+#define TAIL_STAMP(k) tail_stamp(k)
+#else
+#define TAIL_STAMP(k) do { } while (0)
+#endif
 #ifdef PT_COUNT
 // counting build (tools/trace_count.py): node visits, box tests, primitive tests, fp64 tests, rays
 __device__ unsigned long long g_trav_count[8];
@@ -804,6 +817,7 @@ __global__ void __launch_bounds__(128, PT_FB_MINB) first_bounce_kernel(ShadeArgs
 #pragma unroll
     for (int k = 16; k > 0; k >>= 1) segs += __shfl_xor_sync(0xFFFFFFFFu, segs, k);
     if (lane == 0) atomicAdd(a.seg_count, segs);
+    TAIL_STAMP(0);
 }
 
 // Bounces 2.. (persistent): every lane carries one path from the first bounce's queue to its end,
@@ -866,6 +880,7 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
 #pragma unroll
     for (int k = 16; k > 0; k >>= 1) segs += __shfl_xor_sync(0xFFFFFFFFu, segs, k);
     if (lane == 0) atomicAdd(a.seg_count, segs);
+    TAIL_STAMP(1);
 }
 
 // S6: fb += the wave's per-slot radiance, summed over its k samples in sample order (deterministic); one
@@ -1010,5 +1025,11 @@ extern "C" __attribute__((visibility("default"))) int pt_debug_trav_counts(unsig
         cudaMemcpyToSymbol(pt::g_trav_count, z, sizeof(z));
     }
     return 0;
+}
+#endif
+
+#ifdef PT_TAIL_TRACE
+extern "C" __attribute__((visibility("default"))) int pt_debug_tail(unsigned long long* host) {
+    return cudaMemcpyFromSymbol(host, pt::g_tail, sizeof(pt::g_tail)) == cudaSuccess ? 0 : -1;
 }
 #endif
