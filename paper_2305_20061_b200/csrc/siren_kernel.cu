@@ -329,16 +329,26 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
                         oslot[s] = __float_as_uint(__ldg(esc + row).w);
                     }
                     uint32_t v[32];
-                    TMEM_LD32(tmem + d_col(s) + lane_addr + 32 * cb, v);
-                    tmem_wait_ld_dep(v);
-                    if (kDebug && valid) {
-                        for (int j = 0; j < 32; ++j)
-                            dbg[((size_t)stage * n_rows + row) * 128 + 32 * cb + j] = __uint_as_float(v[j]);
+                    uint32_t pk[16];
+                    if (kDebug) {
+                        TMEM_LD32(tmem + d_col(s) + lane_addr + 32 * cb, v);
+                        tmem_wait_ld_dep(v);
+                        if (valid)
+                            for (int j = 0; j < 32; ++j)
+                                dbg[((size_t)stage * n_rows + row) * 128 + 32 * cb + j] = __uint_as_float(v[j]);
+                        sine_half(v, 0, pk);
+                        sine_half(v + 16, 1, pk + 8);
+                    } else {
+                        // D (fp32) -> sin -> fp16: the second 16 columns load while the first are computed
+                        TMEM_LD16(tmem + d_col(s) + lane_addr + 32 * cb, v);
+                        tmem_wait_ld_dep16(v);
+                        TMEM_LD16(tmem + d_col(s) + lane_addr + 32 * cb + 16, v + 16);
+                        sine_half(v, 0, pk);
+                        tmem_wait_ld_dep16(v + 16);
+                        sine_half(v + 16, 1, pk + 8);
                     }
                     {
-                        // D (fp32) -> sin -> fp16 -> A of the next layer (this warp's 32 columns)
-                        uint32_t pk[16];
-                        sine_chunk(v, pk);
+                        // -> A of the next layer (this warp's 32 columns)
                         TMEM_ST16(tmem + a_col(s) + lane_addr + 16 * cb, pk);
                         tmem_wait_st();
                         tc_fence_before();

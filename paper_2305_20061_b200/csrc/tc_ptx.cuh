@@ -137,6 +137,21 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
         "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])              \
         : "memory")
 
+#define TMEM_LD16(taddr, v)                                                                                    \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+                 : "=r"((v)[0]), "=r"((v)[1]), "=r"((v)[2]), "=r"((v)[3]), "=r"((v)[4]), "=r"((v)[5]),         \
+                   "=r"((v)[6]), "=r"((v)[7]), "=r"((v)[8]), "=r"((v)[9]), "=r"((v)[10]), "=r"((v)[11]),        \
+                   "=r"((v)[12]), "=r"((v)[13]), "=r"((v)[14]), "=r"((v)[15])                                   \
+                 : "r"(taddr))
+// wait for all prior tcgen05.ld of this thread, pinning the 16 registers of one of them
+__device__ __forceinline__ void tmem_wait_ld_dep16(uint32_t* v) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                   "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]),
+                   "+r"(v[15])
+                 :
+                 : "memory");
+}
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
                  "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
@@ -195,6 +210,19 @@ __device__ __forceinline__ uint32_t sin2_poly(float a, float b) {
     p = __hfma2(p, w2, c1);
     const __half2 r = __hmul2(p, w);
     return *reinterpret_cast<const uint32_t*>(&r);
+}
+// half of a 32-column chunk (pairs 8 h .. 8 h + 7), loaded while the other half is computed; the SFU
+// pairs are the even ones plus pair 1 (9 of 16 at the default), so both halves carry a similar SFU share
+__device__ __forceinline__ bool sfu_pair(int j) {
+    return PT_NIF_MUFU_PAIRS >= 16 || (j % 2 == 0 ? j / 2 < PT_NIF_MUFU_PAIRS : (j - 1) / 2 + 8 < PT_NIF_MUFU_PAIRS);
+}
+__device__ __forceinline__ void sine_half(const uint32_t* v, int h, uint32_t* p) {
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+        const int j = 8 * h + jj;
+        const float a = __uint_as_float(v[2 * jj]), b = __uint_as_float(v[2 * jj + 1]);
+        p[jj] = sfu_pair(j) ? pack_half2(__sinf(a), __sinf(b)) : sin2_poly(a, b);
+    }
 }
 __device__ __forceinline__ void sine_chunk(const uint32_t* v, uint32_t* p) {
 #pragma unroll
