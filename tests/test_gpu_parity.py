@@ -327,3 +327,23 @@ def test_render_closed_box_no_escapes(ptm, orc, blob):
                       layers=8)]
     for nif in others:
         assert np.array_equal(ptm.render(ptm.Scene(sc), nif, W, H, spp, depth, seed=3), img)
+
+
+def test_render_identical_without_programmatic_dependent_launch(ptm, blob, tmp_path):
+    """The wave's kernels chained with programmatic dependent launch (griddepcontrol) produce exactly the
+    frame of plain stream-ordered launches (PT_NO_PDL=1, read once per process: a child process)."""
+    import os
+    import subprocess
+    import sys
+    c = scenes.CONFIGS[0]
+    img = ptm.render(ptm.Scene(scenes.scene_for_config(0)), ptm.Nif(blob), c.width, c.height, c.spp, c.max_depth,
+                     seed=c.seed)
+    out = tmp_path / "nopdl.npy"
+    code = ("import numpy as np; from paper_2305_20061_b200 import pt, scenes; c = scenes.CONFIGS[0]; "
+            "img = pt.render(pt.Scene(scenes.scene_for_config(0)), pt.Nif(scenes.siren_blob(0)), c.width, c.height, "
+            f"c.spp, c.max_depth, seed=c.seed); np.save(r'{out}', img)")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, PT_NO_PDL="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    assert np.array_equal(np.load(out), img)
