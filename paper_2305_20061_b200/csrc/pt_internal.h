@@ -76,11 +76,12 @@ struct TimedLaunch {
 // flags, [130] / [131] = work-fetch counters of the first-bounce and path kernels, [132] = traced
 // segments, [133] = paths alive after the first bounce
 constexpr int kCounters = 192;
-constexpr int kCounterEsc = 128;
-constexpr int kCounterErr = 129;
+// alive (low) and escaped (high) share one 8-byte word: the first bounce reserves both queues with one
+// 64-bit atomic per warp
+constexpr int kCounterAlive = 128; // paths alive after the first bounce
+constexpr int kCounterEsc = 129;
 constexpr int kCounterWork = 130;
 constexpr int kCounterSeg = 132;   // traced segments of the wave
-constexpr int kCounterAlive = 133; // paths alive after the first bounce
 
 }  // namespace pt
 

@@ -806,13 +806,27 @@ __global__ void __launch_bounds__(128, PT_FB_MINB) first_bounce_kernel(ShadeArgs
             shade_segment(a, 1, i, eye, camera_ray(a, i), make_float3(1.0f, 1.0f, 1.0f), r);
             write_radiance(a, r, i);
         }
-        const uint32_t pos = warp_append(r.alive, a.alive_count);
+        // both queues reserved with one 64-bit atomic (alive in the low word, escaped in the high word)
+        const uint32_t ma = __ballot_sync(0xFFFFFFFFu, r.alive), me = __ballot_sync(0xFFFFFFFFu, r.escaped);
+        unsigned long long qb = 0;
+        if ((ma | me) != 0u) {
+            if (lane == 0)
+                qb = atomicAdd(reinterpret_cast<unsigned long long*>(a.alive_count),
+                               (unsigned long long)__popc(ma) | ((unsigned long long)__popc(me) << 32));
+            qb = __shfl_sync(0xFFFFFFFFu, qb, 0);
+        }
+        const uint32_t lt = (1u << lane) - 1u;
         if (r.alive) {
+            const uint32_t pos = (uint32_t)qb + (uint32_t)__popc(ma & lt);
             a.qA[pos] = make_float4(r.o.x, r.o.y, r.o.z, __uint_as_float(i));
             a.qB[pos] = make_float4(r.d.x, r.d.y, r.d.z, r.beta.x);
             a.qC[pos] = make_float2(r.beta.y, r.beta.z);
         }
-        append_escaped(a, r, i);
+        if (r.escaped) {
+            const uint32_t pos = (uint32_t)(qb >> 32) + (uint32_t)__popc(me & lt);
+            a.esc[pos] = make_float4(r.d.x, r.d.y, r.d.z, __uint_as_float(i));
+            a.esc_beta[pos] = make_float4(r.beta.x, r.beta.y, r.beta.z, 0.0f);
+        }
     }
 #pragma unroll
     for (int k = 16; k > 0; k >>= 1) segs += __shfl_xor_sync(0xFFFFFFFFu, segs, k);
