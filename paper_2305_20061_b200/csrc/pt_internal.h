@@ -76,10 +76,12 @@ struct TimedLaunch {
 // flags, [130] / [131] = work-fetch counters of the first-bounce and path kernels, [132] = traced
 // segments, [133] = paths alive after the first bounce
 constexpr int kCounters = 192;
-// alive (low) and escaped (high) share one 8-byte word: the first bounce reserves both queues with one
-// 64-bit atomic per warp
-constexpr int kCounterAlive = 128; // paths alive after the first bounce
-constexpr int kCounterEsc = 129;
+// escaped (low) and alive (high) share one 8-byte word: the first bounce reserves both of its output
+// queues with one 64-bit atomic per warp; the path kernel then takes paths from the top of the alive
+// queue (decrementing the high word) and appends escapes (low word) with one 64-bit atomic per warp
+// iteration
+constexpr int kCounterEsc = 128;
+constexpr int kCounterAlive = 129; // paths alive after the first bounce, then the path queue's remainder
 constexpr int kCounterWork = 130;
 constexpr int kCounterSeg = 132;   // traced segments of the wave
 

@@ -765,14 +765,6 @@ __device__ __forceinline__ uint32_t warp_append(bool pred, uint32_t* counter) {
     return base + (uint32_t)__popc(mask & ((1u << lane) - 1u));
 }
 
-__device__ __forceinline__ void append_escaped(const ShadeArgs& a, const SegOut& r, uint32_t slot) {
-    const uint32_t pos = warp_append(r.escaped, a.esc_count);
-    if (r.escaped) {
-        a.esc[pos] = make_float4(r.d.x, r.d.y, r.d.z, __uint_as_float(slot));
-        a.esc_beta[pos] = make_float4(r.beta.x, r.beta.y, r.beta.z, 0.0f);
-    }
-}
-
 __device__ __forceinline__ void write_radiance(const ShadeArgs& a, const SegOut& r, uint32_t slot) {
     if (r.done) {
         a.wave_buf[3 * (size_t)slot + 0] = r.L.x;
@@ -806,24 +798,24 @@ __global__ void __launch_bounds__(128, PT_FB_MINB) first_bounce_kernel(ShadeArgs
             shade_segment(a, 1, i, eye, camera_ray(a, i), make_float3(1.0f, 1.0f, 1.0f), r);
             write_radiance(a, r, i);
         }
-        // both queues reserved with one 64-bit atomic (alive in the low word, escaped in the high word)
+        // both queues reserved with one 64-bit atomic (escaped in the low word, alive in the high word)
         const uint32_t ma = __ballot_sync(0xFFFFFFFFu, r.alive), me = __ballot_sync(0xFFFFFFFFu, r.escaped);
         unsigned long long qb = 0;
         if ((ma | me) != 0u) {
             if (lane == 0)
-                qb = atomicAdd(reinterpret_cast<unsigned long long*>(a.alive_count),
-                               (unsigned long long)__popc(ma) | ((unsigned long long)__popc(me) << 32));
+                qb = atomicAdd(reinterpret_cast<unsigned long long*>(a.esc_count),
+                               ((unsigned long long)__popc(ma) << 32) | (unsigned long long)__popc(me));
             qb = __shfl_sync(0xFFFFFFFFu, qb, 0);
         }
         const uint32_t lt = (1u << lane) - 1u;
         if (r.alive) {
-            const uint32_t pos = (uint32_t)qb + (uint32_t)__popc(ma & lt);
+            const uint32_t pos = (uint32_t)(qb >> 32) + (uint32_t)__popc(ma & lt);
             a.qA[pos] = make_float4(r.o.x, r.o.y, r.o.z, __uint_as_float(i));
             a.qB[pos] = make_float4(r.d.x, r.d.y, r.d.z, r.beta.x);
             a.qC[pos] = make_float2(r.beta.y, r.beta.z);
         }
         if (r.escaped) {
-            const uint32_t pos = (uint32_t)(qb >> 32) + (uint32_t)__popc(me & lt);
+            const uint32_t pos = (uint32_t)qb + (uint32_t)__popc(me & lt);
             a.esc[pos] = make_float4(r.d.x, r.d.y, r.d.z, __uint_as_float(i));
             a.esc_beta[pos] = make_float4(r.beta.x, r.beta.y, r.beta.z, 0.0f);
         }
@@ -842,35 +834,37 @@ __global__ void __launch_bounds__(128, PT_FB_MINB) first_bounce_kernel(ShadeArgs
 __global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
     pdl_wait();                       // first_bounce complete: its queue and counters are visible
     pdl_trigger();
-    const uint32_t n = *a.alive_count;
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
+    // (escaped count, alive remainder) word: paths are taken from the top of the first bounce's queue
+    unsigned long long* const qw = reinterpret_cast<unsigned long long*>(a.esc_count);
     bool have = false;
     uint32_t slot = 0;
     int depth = 0;
     float3 o = make_float3(0, 0, 0), d = make_float3(0, 0, 1), bt = make_float3(1, 1, 1);
     uint32_t segs = 0;
-    for (;;) {
-        const uint32_t mneed = __ballot_sync(0xFFFFFFFFu, !have);
-        if (mneed) {
-            const int leader = __ffs(mneed) - 1;
-            uint32_t base = 0;
-            if (lane == leader) base = atomicAdd(a.work, (uint32_t)__popc(mneed));
-            base = __shfl_sync(0xFFFFFFFFu, base, leader);
-            if (!have) {
-                const uint32_t idx = base + (uint32_t)__popc(mneed & lt);
-                if (idx < n) {
-                    const float4 qa = __ldg(a.qA + idx), qb = __ldg(a.qB + idx);
-                    const float2 qc = __ldg(a.qC + idx);
-                    o = make_float3(qa.x, qa.y, qa.z);
-                    slot = __float_as_uint(qa.w);
-                    d = make_float3(qb.x, qb.y, qb.z);
-                    bt = make_float3(qb.w, qc.x, qc.y);
-                    depth = 2;
-                    have = true;
-                }
+    // lanes without a path take queue entries r0 - 1 - (rank among them) while those are >= 0
+    auto refill = [&](unsigned long long old, uint32_t mneed) {
+        if (!have) {
+            const int idx = (int)(uint32_t)(old >> 32) - 1 - __popc(mneed & lt);
+            if (idx >= 0) {
+                const float4 qa = __ldg(a.qA + idx), qb = __ldg(a.qB + idx);
+                const float2 qc = __ldg(a.qC + idx);
+                o = make_float3(qa.x, qa.y, qa.z);
+                slot = __float_as_uint(qa.w);
+                d = make_float3(qb.x, qb.y, qb.z);
+                bt = make_float3(qb.w, qc.x, qc.y);
+                depth = 2;
+                have = true;
             }
         }
+    };
+    {
+        unsigned long long old = 0;
+        if (lane == 0) old = atomicAdd(qw, (unsigned long long)(0u - 32u) << 32);
+        refill(__shfl_sync(0xFFFFFFFFu, old, 0), 0xFFFFFFFFu);
+    }
+    for (;;) {
         if (!__any_sync(0xFFFFFFFFu, have)) break;
         SegOut r;
         r.escaped = false;
@@ -878,9 +872,6 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
             ++segs;
             shade_segment(a, depth, slot, o, d, bt, r);
             write_radiance(a, r, slot);
-        }
-        append_escaped(a, r, slot);
-        if (have) {
             if (r.alive) {
                 o = r.o;
                 d = r.d;
@@ -889,6 +880,24 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
             } else {
                 have = false;
             }
+        }
+        // one 64-bit atomic per warp iteration: append this iteration's escapes (low word) and take
+        // new paths for the free lanes (high word)
+        const uint32_t me = __ballot_sync(0xFFFFFFFFu, r.escaped);
+        const uint32_t mneed = __ballot_sync(0xFFFFFFFFu, !have);
+        if ((me | mneed) != 0u) {
+            const int leader = __ffs(me | mneed) - 1;
+            unsigned long long old = 0;
+            if (lane == leader)
+                old = atomicAdd(qw, ((unsigned long long)(0u - (uint32_t)__popc(mneed)) << 32) +
+                                        (unsigned long long)__popc(me));
+            old = __shfl_sync(0xFFFFFFFFu, old, leader);
+            if (r.escaped) {
+                const uint32_t pos = (uint32_t)old + (uint32_t)__popc(me & lt);
+                a.esc[pos] = make_float4(r.d.x, r.d.y, r.d.z, __uint_as_float(slot));
+                a.esc_beta[pos] = make_float4(r.beta.x, r.beta.y, r.beta.z, 0.0f);
+            }
+            refill(old, mneed);
         }
     }
 #pragma unroll
