@@ -76,13 +76,13 @@ struct TimedLaunch {
 // flags, [130] / [131] = work-fetch counters of the first-bounce and path kernels, [132] = traced
 // segments, [133] = paths alive after the first bounce
 constexpr int kCounters = 192;
-// escaped (low) and alive (high) share one 8-byte word: the first bounce reserves both of its output
-// queues with one 64-bit atomic per warp; the path kernel then takes paths from the top of the alive
-// queue (decrementing the high word) and appends escapes (low word) with one 64-bit atomic per warp
-// iteration
+// Two 8-byte words, each advanced by one 64-bit atomic per warp iteration:
+//   [128] escaped-queue length | [129] paths taken from the alive queue by the path kernel
+//   [130] first-bounce work (slots fetched) | [131] alive-queue length (paths alive after bounce 1)
 constexpr int kCounterEsc = 128;
-constexpr int kCounterAlive = 129; // paths alive after the first bounce, then the path queue's remainder
+constexpr int kCounterTaken = 129;
 constexpr int kCounterWork = 130;
+constexpr int kCounterAlive = 131;
 constexpr int kCounterSeg = 132;   // traced segments of the wave
 
 }  // namespace pt

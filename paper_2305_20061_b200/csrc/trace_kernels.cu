@@ -784,11 +784,14 @@ __global__ void __launch_bounds__(128, PT_FB_MINB) first_bounce_kernel(ShadeArgs
     const uint32_t n = a.n_slots;
     const int lane = threadIdx.x & 31;
     uint32_t segs = 0;
-    for (;;) {
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(a.work, 32u);
-        base = __shfl_sync(0xFFFFFFFFu, base, 0);
-        if (base >= n) break;
+    const uint32_t lt = (1u << lane) - 1u;
+    // (work, alive) word: one 64-bit atomic per iteration reserves this chunk's survivors in the path
+    // queue and fetches the next chunk of 32 slots
+    unsigned long long* const ww = reinterpret_cast<unsigned long long*>(a.work);
+    unsigned long long wo = 0;
+    if (lane == 0) wo = atomicAdd(ww, 32ull);
+    uint32_t base = (uint32_t)__shfl_sync(0xFFFFFFFFu, wo, 0);
+    while (base < n) {
         const uint32_t i = base + (uint32_t)lane;
         SegOut r;
         r.alive = r.escaped = false;
@@ -798,27 +801,26 @@ __global__ void __launch_bounds__(128, PT_FB_MINB) first_bounce_kernel(ShadeArgs
             shade_segment(a, 1, i, eye, camera_ray(a, i), make_float3(1.0f, 1.0f, 1.0f), r);
             write_radiance(a, r, i);
         }
-        // both queues reserved with one 64-bit atomic (escaped in the low word, alive in the high word)
         const uint32_t ma = __ballot_sync(0xFFFFFFFFu, r.alive), me = __ballot_sync(0xFFFFFFFFu, r.escaped);
-        unsigned long long qb = 0;
-        if ((ma | me) != 0u) {
-            if (lane == 0)
-                qb = atomicAdd(reinterpret_cast<unsigned long long*>(a.esc_count),
-                               ((unsigned long long)__popc(ma) << 32) | (unsigned long long)__popc(me));
-            qb = __shfl_sync(0xFFFFFFFFu, qb, 0);
-        }
-        const uint32_t lt = (1u << lane) - 1u;
+        if (lane == 0) wo = atomicAdd(ww, 32ull | ((unsigned long long)__popc(ma) << 32));
+        wo = __shfl_sync(0xFFFFFFFFu, wo, 0);
         if (r.alive) {
-            const uint32_t pos = (uint32_t)(qb >> 32) + (uint32_t)__popc(ma & lt);
+            const uint32_t pos = (uint32_t)(wo >> 32) + (uint32_t)__popc(ma & lt);
             a.qA[pos] = make_float4(r.o.x, r.o.y, r.o.z, __uint_as_float(i));
             a.qB[pos] = make_float4(r.d.x, r.d.y, r.d.z, r.beta.x);
             a.qC[pos] = make_float2(r.beta.y, r.beta.z);
         }
-        if (r.escaped) {
-            const uint32_t pos = (uint32_t)qb + (uint32_t)__popc(me & lt);
-            a.esc[pos] = make_float4(r.d.x, r.d.y, r.d.z, __uint_as_float(i));
-            a.esc_beta[pos] = make_float4(r.beta.x, r.beta.y, r.beta.z, 0.0f);
+        if (me != 0u) {                   // camera rays that miss everything: rare inside a scene
+            uint32_t eb = 0;
+            if (lane == 0) eb = atomicAdd(a.esc_count, (uint32_t)__popc(me));
+            eb = __shfl_sync(0xFFFFFFFFu, eb, 0);
+            if (r.escaped) {
+                const uint32_t pos = eb + (uint32_t)__popc(me & lt);
+                a.esc[pos] = make_float4(r.d.x, r.d.y, r.d.z, __uint_as_float(i));
+                a.esc_beta[pos] = make_float4(r.beta.x, r.beta.y, r.beta.z, 0.0f);
+            }
         }
+        base = (uint32_t)wo;
     }
 #pragma unroll
     for (int k = 16; k > 0; k >>= 1) segs += __shfl_xor_sync(0xFFFFFFFFu, segs, k);
@@ -836,8 +838,9 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
     pdl_trigger();
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
-    // (escaped count, alive remainder) word: paths are taken from the top of the first bounce's queue
+    // (escaped count, paths taken) word; the alive queue's length is final once first_bounce is done
     unsigned long long* const qw = reinterpret_cast<unsigned long long*>(a.esc_count);
+    const int n_alive = (int)*a.alive_count;
     bool have = false;
     uint32_t slot = 0;
     int depth = 0;
@@ -846,7 +849,7 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
     // lanes without a path take queue entries r0 - 1 - (rank among them) while those are >= 0
     auto refill = [&](unsigned long long old, uint32_t mneed) {
         if (!have) {
-            const int idx = (int)(uint32_t)(old >> 32) - 1 - __popc(mneed & lt);
+            const int idx = n_alive - 1 - (int)(uint32_t)(old >> 32) - __popc(mneed & lt);
             if (idx >= 0) {
                 const float4 qa = __ldg(a.qA + idx), qb = __ldg(a.qB + idx);
                 const float2 qc = __ldg(a.qC + idx);
@@ -861,7 +864,7 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
     };
     {
         unsigned long long old = 0;
-        if (lane == 0) old = atomicAdd(qw, (unsigned long long)(0u - 32u) << 32);
+        if (lane == 0) old = atomicAdd(qw, 32ull << 32);
         refill(__shfl_sync(0xFFFFFFFFu, old, 0), 0xFFFFFFFFu);
     }
     for (;;) {
@@ -889,8 +892,7 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
             const int leader = __ffs(me | mneed) - 1;
             unsigned long long old = 0;
             if (lane == leader)
-                old = atomicAdd(qw, ((unsigned long long)(0u - (uint32_t)__popc(mneed)) << 32) +
-                                        (unsigned long long)__popc(me));
+                old = atomicAdd(qw, ((unsigned long long)__popc(mneed) << 32) + (unsigned long long)__popc(me));
             old = __shfl_sync(0xFFFFFFFFu, old, leader);
             if (r.escaped) {
                 const uint32_t pos = (uint32_t)old + (uint32_t)__popc(me & lt);
@@ -1006,10 +1008,7 @@ void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int fir
     static const int grid2 = resident_grid(path_kernel, 128);
     a.work = ws.counters + kCounterWork;
     first_bounce_kernel<<<grid1, 128, 0, st>>>(a);
-    if (max_depth > 1) {
-        a.work = ws.counters + kCounterWork + 1;
-        launch_pdl(path_kernel, dim3(grid2), dim3(128), 0, st, a);
-    }
+    if (max_depth > 1) launch_pdl(path_kernel, dim3(grid2), dim3(128), 0, st, a);
 }
 
 void launch_accumulate(const float* wave_buf, int n_pix, int k, float* fb, const uint32_t* counters,
