@@ -754,17 +754,6 @@ __device__ __forceinline__ float3 camera_ray(const ShadeArgs& a, uint32_t i) {
 #endif
 
 // Warp-aggregated append (one atomic per warp), returns this lane's position
-__device__ __forceinline__ uint32_t warp_append(bool pred, uint32_t* counter) {
-    const uint32_t mask = __ballot_sync(0xFFFFFFFFu, pred);
-    if (mask == 0) return 0;
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(mask) - 1;
-    uint32_t base = 0;
-    if (lane == leader) base = atomicAdd(counter, (uint32_t)__popc(mask));
-    base = __shfl_sync(0xFFFFFFFFu, base, leader);
-    return base + (uint32_t)__popc(mask & ((1u << lane) - 1u));
-}
-
 __device__ __forceinline__ void write_radiance(const ShadeArgs& a, const SegOut& r, uint32_t slot) {
     if (r.done) {
         a.wave_buf[3 * (size_t)slot + 0] = r.L.x;
@@ -829,7 +818,7 @@ __global__ void __launch_bounds__(128, PT_FB_MINB) first_bounce_kernel(ShadeArgs
 }
 
 // Bounces 2.. (persistent): every lane carries one path from the first bounce's queue to its end,
-// and a lane whose path ends refills from the queue (one warp-aggregated atomic for all of the warp's
+// and a lane whose path ends refills from the queue (one 64-bit atomic per warp iteration for all of the warp's
 // free lanes), so the warps stay full without a launch, a barrier or a state round trip through HBM
 // per bounce. Per-path results do not depend on the schedule: the RNG is keyed by (pixel, sample,
 // depth) and every path writes only its own slot.
