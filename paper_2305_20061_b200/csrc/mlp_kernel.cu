@@ -93,6 +93,12 @@ __device__ __forceinline__ uint32_t e4m3x2(float lo, float hi) {
     asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
     return r;
 }
+// relu fused into the conversion (F2FP.SATFINITE.RELU.E4M3)
+__device__ __forceinline__ uint32_t e4m3x2_relu(float lo, float hi) {
+    uint16_t r;
+    asm("cvt.rn.satfinite.relu.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+    return r;
+}
 
 }  // namespace mlp
 
@@ -312,10 +318,8 @@ __global__ void __launch_bounds__(mlp::kThreads, 1) mlp_layer_kernel(mlp::LayerA
                                 asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(wp[i]) : "f"(h[2 * i + 1]), "f"(h[2 * i]));
                             store_act8(a.out_act, a.out_KC, mt, rt, col + 8 * g, w);
                         } else {
-#pragma unroll
-                            for (int i = 0; i < 8; ++i) h[i] = fmaxf(h[i], 0.0f);
-                            const uint32_t lo = e4m3x2(h[0], h[1]) | (e4m3x2(h[2], h[3]) << 16);
-                            const uint32_t hi = e4m3x2(h[4], h[5]) | (e4m3x2(h[6], h[7]) << 16);
+                            const uint32_t lo = e4m3x2_relu(h[0], h[1]) | (e4m3x2_relu(h[2], h[3]) << 16);
+                            const uint32_t hi = e4m3x2_relu(h[4], h[5]) | (e4m3x2_relu(h[6], h[7]) << 16);
                             store_act8_f8(a.out_act, a.out_KC, mt, rt, col + 8 * g, make_uint2(lo, hi));
                         }
                     }
@@ -591,8 +595,7 @@ __global__ void __launch_bounds__(mlpf::kThreads, fused_ctas_per_sm<kH>()) mlp_f
                                 asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(pk[2 * g]) : "f"(x1), "f"(x0));
                                 asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(pk[2 * g + 1]) : "f"(x3), "f"(x2));
                             } else {
-                                pk[g] = mlp::e4m3x2(fmaxf(x0, 0.0f), fmaxf(x1, 0.0f)) |
-                                        (mlp::e4m3x2(fmaxf(x2, 0.0f), fmaxf(x3, 0.0f)) << 16);
+                                pk[g] = mlp::e4m3x2_relu(x0, x1) | (mlp::e4m3x2_relu(x2, x3) << 16);
                             }
                         }
                         if (!kFp8) {
