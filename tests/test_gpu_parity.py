@@ -59,6 +59,20 @@ def test_nif_vs_oracle(ptm, orc, n, scale):
     assert (np.abs(got - ref) / ref).max() <= NIF_REL_GATE
 
 
+def test_nif_bench_size_sampled(ptm, orc, blob):
+    """The escaped-queue size of the bench's config-1 frame (about 2.2 M queries; here 2^21 + 333, so the
+    last tile is ragged and every CTA runs > 100 tiles in both slots), checked on 4000 sampled rows."""
+    import torch
+    n = (1 << 21) + 333
+    uv = scenes.query_uv(n, 11)
+    got = ptm.nif_infer(ptm.Nif(blob), torch.from_numpy(uv).cuda()).cpu().numpy().astype(np.float64)
+    assert np.isfinite(got).all() and (got > 0).all()
+    idx = np.concatenate([np.linspace(0, n - 1, 3600).astype(np.int64), np.arange(n - 400, n)])
+    y = orc.nif_eval(blob, uv[idx].astype(np.float64))
+    assert np.abs(np.log(got[idx]) - y).max() <= NIF_LOG_GATE
+    assert (np.abs(got[idx] - np.exp(y)) / np.exp(y)).max() <= NIF_REL_GATE
+
+
 def test_nif_layer_accumulators(ptm, blob):
     """Debug view: every layer's fp32 accumulator against an independent float64 evaluation of the
     same fp16 activations (isolates MMA layout bugs from the sine epilogue)."""
