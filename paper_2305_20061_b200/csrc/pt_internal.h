@@ -122,7 +122,6 @@ struct pt_nif {
     void* d_smem_image = nullptr;     // pre-laid-out shared-memory image of the fused kernel (+ raw blob)
     size_t d_alloc_bytes = 0;
     int64_t smem_bytes = 0;
-    uint16_t* d_blob = nullptr;       // raw fp16 blob
     // PT_NIF_FR_FAMILY (layered GEMM path)
     int mlp_H = 0, mlp_L = 0, mlp_c = 0, mlp_fp8 = 0;
     float* mlp_freq = nullptr;        // B [20][2] fp32
