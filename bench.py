@@ -300,6 +300,9 @@ def main():
     e2e_steps = max(3, min(args.steps, 20))
     e2e_warmup = max(1, min(args.warmup, 3))
     host_fb = torch.empty(W * H * 3, dtype=torch.float32, pin_memory=True)
+    host_np = host_fb.numpy()
+    auto_k = max(1, min(spp, (8 << 20) // (W * H)))       # pt_render's wave size (pt_api.cu)
+    host_render = world == 1 and auto_k == cfg.wave_samples
     h2d = src.tris.nbytes + src.spheres.nbytes + src.materials.nbytes + src.camera.nbytes + (blob.nbytes if blob is not None else 0)
     te0 = None
     for it in range(e2e_warmup + e2e_steps):
@@ -310,14 +313,20 @@ def main():
             te0 = time.perf_counter()
         S2 = pt.Scene(src)
         N2 = pt.Nif(blob) if cfg.use_nif else None
-        acc2 = torch.zeros(W * H * 3, dtype=torch.float32, device="cuda")
+        if host_render:
+            # one GPU: pt_render, the C-ABI's host-buffer call (device accumulator, scale, read-back into
+            # the caller's pinned buffer); its automatic wave size equals the config's here
+            pt.render(S2, N2, W, H, spp, depth, cfg.seed, env_rgb=env, out=host_np)
+        else:
+            acc2 = torch.zeros(W * H * 3, dtype=torch.float32, device="cuda")
 
-        def block2(f, c, acc, S2=S2, N2=N2):
-            pt.render_samples(S2, N2, W, H, f, c, depth, cfg.seed, acc, env_rgb=env, wave_samples=cfg.wave_samples)
+            def block2(f, c, acc, S2=S2, N2=N2):
+                pt.render_samples(S2, N2, W, H, f, c, depth, cfg.seed, acc, env_rgb=env,
+                                  wave_samples=cfg.wave_samples)
 
-        render_partitioned(block2, n_total, acc2, rank, world)
-        if rank == 0:
-            host_fb.copy_(acc2.mul_(1.0 / n_total), non_blocking=False)
+            render_partitioned(block2, n_total, acc2, rank, world)
+            if rank == 0:
+                host_fb.copy_(acc2.mul_(1.0 / n_total), non_blocking=False)
         torch.cuda.synchronize()
         S2.close()
         if N2:
@@ -401,7 +410,9 @@ def main():
         "config": workload_config(cfg, world),
         "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(host_fb.numel() * 4),
-                "what": "pt_scene_create + pt_nif_load from host arrays, render, reduce, framebuffer to pinned host"},
+                "what": ("pt_scene_create + pt_nif_load from host arrays, pt_render into a pinned host buffer"
+                         if host_render else
+                         "pt_scene_create + pt_nif_load from host arrays, render, reduce, framebuffer to pinned host")},
         "gpu_launches": int(launches),
         "roofline": roof,
         "nif": {"inferences_per_s": infers / (nif_ms / 1e3) if nif_ms > 0 else None,

@@ -155,9 +155,13 @@ def _env(env_rgb):
     return None if env_rgb is None else np.ascontiguousarray(env_rgb, dtype=np.float32)
 
 
-def render(scene: Scene, nif: Nif | None, width, height, spp, max_depth, seed=0, env_rgb=None) -> np.ndarray:
-    """pt_render: full frame, mean over spp, host float32 [H][W][3]."""
-    out = np.empty((height, width, 3), np.float32)
+def render(scene: Scene, nif: Nif | None, width, height, spp, max_depth, seed=0, env_rgb=None, out=None) -> np.ndarray:
+    """pt_render: full frame, mean over spp, host float32 [H][W][3]. `out` (optional): a C-contiguous
+    float32 host array of H*W*3 elements to write into (e.g. a view of pinned memory)."""
+    if out is None:
+        out = np.empty((height, width, 3), np.float32)
+    elif out.dtype != np.float32 or not out.flags["C_CONTIGUOUS"] or out.size != height * width * 3:
+        raise PtError(-1, "out must be a C-contiguous float32 array of height * width * 3 elements")
     env = _env(env_rgb if env_rgb is not None else ((1.0, 1.0, 1.0) if nif is None else None))
     _check(lib().pt_render(scene.h, nif.h if nif else None, _p(env), width, height, spp, max_depth, seed, _p(out)))
     return out
