@@ -28,7 +28,8 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
-    """Compile every source for sm_100a and link libpt_b200.so (or `out`, with extra -D defines)."""
+    """Compile every source for sm_100a and link libpt_b200.so (or `out`, with extra -D defines; the
+    environment variable PT_NVCC_EXTRA adds nvcc flags, for experiments)."""
     lib = os.path.abspath(out) if out else LIB
     os.makedirs(os.path.dirname(lib), exist_ok=True)
     if not force and out is None and not _stale():
@@ -37,7 +38,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     os.makedirs(objdir, exist_ok=True)
     objs = []
     common = ["-O3", "-std=c++17", "-lineinfo", "-I", INCLUDE, "-I", CSRC,
-              "-Xcompiler", "-fPIC,-ffp-contract=off,-fvisibility=hidden"]
+              "-Xcompiler", "-fPIC,-ffp-contract=off,-fvisibility=hidden"] + os.environ.get("PT_NVCC_EXTRA", "").split()
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         cmd = [NVCC, *ARCH, *common, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
