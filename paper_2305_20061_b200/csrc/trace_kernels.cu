@@ -105,6 +105,13 @@ __device__ __forceinline__ Shear32 shear_matrix(const RayT& r, float4 sc) {
     return m;
 }
 
+// 32-B read-only global load (LDG.E.ENL2.256), p 32-B aligned
+__device__ __forceinline__ void ldg256(const uint4* p, uint4& a, uint4& b) {
+    asm("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+        : "l"(p));
+}
+
 __device__ __forceinline__ float self3(float3 v, int k) { return k == 0 ? v.x : (k == 1 ? v.y : v.z); }
 
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -498,8 +505,9 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
                 cur = pop(tcull0);
             } else {
                 TCOUNT(0, 1);
-                const uint4 h = __ldg(pool + cur);
-                const uint4 q0 = __ldg(pool + cur + 1), q1 = __ldg(pool + cur + 2), q2 = __ldg(pool + cur + 3);
+                uint4 h, q0, q1, q2;
+                ldg256(pool + cur, h, q0);               // a node is 64 B, 64-B aligned: two 32-B loads
+                ldg256(pool + cur + 2, q1, q2);
                 const uint32_t w[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
                 const float O[3] = {__uint_as_float(h.x), __uint_as_float(h.y), __uint_as_float(h.z)};
                 // child sizes in units (nibbles: 0 none, 4 interior, 3 * count leaf), see pt_internal.h
