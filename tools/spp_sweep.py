@@ -2,7 +2,8 @@
 """spp sweep (the paper's Fig. roofline: ray I/O is hidden above 256 spp
 on the IPU). On B200 the per-frame fixed costs are kernel launches, the shrinking tail bounces and the
 accumulate pass; this measures samples/s of config 1's scene (512 x 512, depth 8, SIREN NIF) as spp grows
-(waves of up to 16 samples), one JSON line per spp."""
+(waves of up to 16 samples; from 32 spp also waves of 32 samples = 8.4 M paths), one JSON line per
+(spp, wave size)."""
 import json
 import os
 import sys
@@ -17,8 +18,8 @@ c = scenes.CONFIGS[1]
 S = pt.Scene(scenes.scene_for_config(1))
 N = pt.Nif(scenes.siren_blob(0))
 acc = torch.zeros(c.width * c.height * 3, device="cuda")
-for spp in (1, 2, 4, 8, 16, 32, 64, 128, 256):
-    k = min(spp, 16)
+for spp, kmax in [(s_, 16) for s_ in (1, 2, 4, 8, 16, 32, 64, 128, 256)] + [(s_, 32) for s_ in (32, 64, 128, 256)]:
+    k = min(spp, kmax)
     reps = max(2, 64 // spp)
     for _ in range(2):
         pt.render_samples(S, N, c.width, c.height, 0, spp, c.max_depth, 0, acc, wave_samples=k)
