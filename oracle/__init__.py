@@ -71,6 +71,8 @@ def lib():
             L.orc_e4m3_round.argtypes = [D]
             L.orc_render_fr.restype = C.c_int
             L.orc_render_fr.argtypes = [P, I32, I32, P, I32, I32, I32, U64, P, I64, I32, I32, I32, P, P]
+            L.orc_render_fr_ex.restype = C.c_int
+            L.orc_render_fr_ex.argtypes = [P, I32, I32, P, I32, I32, I32, I32, U64, P, I64, I32, I32, I32, P, P]
             L.orc_fr_concat_layer.restype = C.c_int
             L.orc_fr_concat_layer.argtypes = [I32]
             L.orc_scatter.argtypes = [C.c_int, P, P, D, P, P, P, P]
@@ -142,8 +144,10 @@ class OracleScene:
         stats = dict(zip(["segments", "escaped", "emitted", "capped", "rr_killed"], st.tolist()))
         return out, stats
 
-    def render_fr(self, hidden, layers, blob, width, height, max_depth, seed, pix=None, s0=0, s1=1, nthreads=None):
-        """As render, with the environment of the paper's NIF family (hidden, layers)."""
+    def render_fr(self, hidden, layers, blob, width, height, max_depth, seed, pix=None, s0=0, s1=1, nthreads=None,
+                  fp8=False):
+        """As render, with the environment of the paper's NIF family (hidden, layers); fp8: its e4m3 model
+        (reading R24, as fr_eval_hl_fp8)."""
         if pix is None:
             pix = np.arange(width * height, dtype=np.int64)
         pix = np.ascontiguousarray(pix, dtype=np.int64)
@@ -151,8 +155,8 @@ class OracleScene:
         st = np.zeros(5, np.int64)
         blob = np.ascontiguousarray(blob, dtype=np.uint16)
         nthreads = nthreads or os.cpu_count() or 1
-        lib().orc_render_fr(self.h, int(hidden), int(layers), _p(blob), width, height, max_depth, seed, _p(pix),
-                            pix.shape[0], s0, s1, nthreads, _p(out), _p(st))
+        lib().orc_render_fr_ex(self.h, int(hidden), int(layers), _p(blob), int(bool(fp8)), width, height, max_depth,
+                               seed, _p(pix), pix.shape[0], s0, s1, nthreads, _p(out), _p(st))
         stats = dict(zip(["segments", "escaped", "emitted", "capped", "rr_killed"], st.tolist()))
         return out, stats
 

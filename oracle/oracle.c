@@ -726,43 +726,48 @@ static double e4m3_round(double x) {
 }
 EXPORT double orc_e4m3_round(double x) { return e4m3_round(x); }
 
-/* The fp8 variant (PT_NIF_FP8): weights rounded to e4m3 once, the features and every hidden activation
-   rounded to e4m3 before they feed the next layer; biases, sums and the output in fp64. */
-EXPORT void orc_fr_eval_hl_fp8(int32_t H, int32_t L, const uint16_t* blob, const double* uv, int64_t n, double* y_out) {
+/* The fp8 variant (PT_NIF_FP8, reading R24): weights rounded to e4m3 once (fr_quantize_fp8),
+   the features and every hidden activation rounded to e4m3 before they feed the next layer; biases,
+   sums and the output in fp64. */
+static void fr_quantize_fp8(fr_net* net) {
+    for (int l = 0; l <= net->L; ++l)
+        for (int64_t i = 0; i < (int64_t)net->fin[l] * net->fout[l]; ++i) net->W[l][i] = e4m3_round(net->W[l][i]);
+}
+static void fr_net_eval_fp8(const fr_net* net, double u, double v, double y[3]) {
     const double PI = 3.14159265358979323846;
+    const int H = net->H, L = net->L;
+    double g[40], a[1024], h[1024];
+    for (int j = 0; j < 20; ++j) {
+        const double p = 2.0 * PI * (net->B[2 * j] * u + net->B[2 * j + 1] * v);
+        g[j] = e4m3_round(sin(p));
+        g[20 + j] = e4m3_round(cos(p));
+    }
+    memcpy(a, g, sizeof(double) * 40);
+    for (int l = 0; l < L; ++l) {
+        for (int o = 0; o < net->fout[l]; ++o) {
+            double s = 0.0;
+            for (int i = 0; i < net->fin[l]; ++i) s += net->W[l][(int64_t)o * net->fin[l] + i] * a[i];
+            s += net->b[l][o];
+            h[o] = e4m3_round(s > 0.0 ? s : 0.0);
+        }
+        memcpy(a, h, sizeof(double) * net->fout[l]);
+        if (l == net->c) memcpy(a + (H - 40), g, sizeof(double) * 40);
+    }
+    double yuv[3];
+    for (int o = 0; o < 3; ++o) {
+        double s = 0.0;
+        for (int i = 0; i < H; ++i) s += net->W[L][(int64_t)o * H + i] * a[i];
+        yuv[o] = s + net->b[L][o];
+    }
+    y[0] = yuv[0] + 1.13983 * yuv[2];
+    y[1] = yuv[0] - 0.39465 * yuv[1] - 0.58060 * yuv[2];
+    y[2] = yuv[0] + 2.03211 * yuv[1];
+}
+EXPORT void orc_fr_eval_hl_fp8(int32_t H, int32_t L, const uint16_t* blob, const double* uv, int64_t n, double* y_out) {
     fr_net net;
     fr_unpack(H, L, blob, &net);
-    for (int l = 0; l <= L; ++l)
-        for (int64_t i = 0; i < (int64_t)net.fin[l] * net.fout[l]; ++i) net.W[l][i] = e4m3_round(net.W[l][i]);
-    double g[40], a[1024], h[1024];
-    for (int64_t q = 0; q < n; ++q) {
-        for (int j = 0; j < 20; ++j) {
-            const double p = 2.0 * PI * (net.B[2 * j] * uv[2 * q] + net.B[2 * j + 1] * uv[2 * q + 1]);
-            g[j] = e4m3_round(sin(p));
-            g[20 + j] = e4m3_round(cos(p));
-        }
-        memcpy(a, g, sizeof(double) * 40);
-        for (int l = 0; l < L; ++l) {
-            for (int o = 0; o < net.fout[l]; ++o) {
-                double s = 0.0;
-                for (int i = 0; i < net.fin[l]; ++i) s += net.W[l][(int64_t)o * net.fin[l] + i] * a[i];
-                s += net.b[l][o];
-                h[o] = e4m3_round(s > 0.0 ? s : 0.0);
-            }
-            memcpy(a, h, sizeof(double) * net.fout[l]);
-            if (l == net.c) memcpy(a + (H - 40), g, sizeof(double) * 40);
-        }
-        double yuv[3];
-        for (int o = 0; o < 3; ++o) {
-            double s = 0.0;
-            for (int i = 0; i < H; ++i) s += net.W[L][(int64_t)o * H + i] * a[i];
-            yuv[o] = s + net.b[L][o];
-        }
-        double* y = y_out + 3 * q;
-        y[0] = yuv[0] + 1.13983 * yuv[2];
-        y[1] = yuv[0] - 0.39465 * yuv[1] - 0.58060 * yuv[2];
-        y[2] = yuv[0] + 2.03211 * yuv[1];
-    }
+    fr_quantize_fp8(&net);
+    for (int64_t q = 0; q < n; ++q) fr_net_eval_fp8(&net, uv[2 * q], uv[2 * q + 1], y_out + 3 * q);
     fr_net_free(&net);
 }
 
@@ -849,6 +854,7 @@ typedef struct {
     const orc_scene* sc;
     const nif64* nif;        /* SIREN HDR-NIF, or NULL */
     const fr_net* fr;        /* the paper's NIF family, or NULL; both NULL -> constant env */
+    int fr_fp8;              /* fr evaluated in the fp8 model (reading R24; weights already rounded) */
     double env[3];
     int32_t W, H, max_depth;
     uint64_t seed;
@@ -904,6 +910,7 @@ static void trace_path(const render_ctx* c, int64_t p, int32_t s, double L[3], p
                 double u, v, y[3];
                 equirect(d, &u, &v);
                 if (c->nif) nif_eval(c->nif, u, v, y);
+                else if (c->fr_fp8) fr_net_eval_fp8(c->fr, u, v, y);
                 else fr_net_eval(c->fr, u, v, y);
                 for (int k = 0; k < 3; ++k) env[k] = exp(y[k]);
             } else {
@@ -1021,6 +1028,7 @@ EXPORT int orc_render(const orc_scene* sc, const uint16_t* nif_blob, const doubl
     if (nif_blob) { nif_unpack(nif_blob, &net); c.nif = &net; }
     else c.nif = NULL;
     c.fr = NULL;
+    c.fr_fp8 = 0;
     for (int k = 0; k < 3; ++k) c.env[k] = env_rgb ? env_rgb[k] : 1.0;
     render_pixels(&c, pix, n_pix, s0, s1, nthreads, out, stats);
     if (nif_blob) nif_free(&net);
@@ -1028,21 +1036,29 @@ EXPORT int orc_render(const orc_scene* sc, const uint16_t* nif_blob, const doubl
 }
 
 /* As orc_render, with the environment given by the paper's NIF family (fr_H, fr_L; (128, 4) is the
-   PT_NIF_FOURIER_RELU network). */
-EXPORT int orc_render_fr(const orc_scene* sc, int32_t fr_H, int32_t fr_L, const uint16_t* fr_blob, int32_t W,
-                         int32_t H, int32_t max_depth, uint64_t seed, const int64_t* pix, int64_t n_pix, int32_t s0,
-                         int32_t s1, int32_t nthreads, double* out, int64_t* stats) {
+   PT_NIF_FOURIER_RELU network); fp8 != 0 evaluates it in the fp8 model (reading R24). */
+EXPORT int orc_render_fr_ex(const orc_scene* sc, int32_t fr_H, int32_t fr_L, const uint16_t* fr_blob, int32_t fp8,
+                            int32_t W, int32_t H, int32_t max_depth, uint64_t seed, const int64_t* pix, int64_t n_pix,
+                            int32_t s0, int32_t s1, int32_t nthreads, double* out, int64_t* stats) {
     render_ctx c;
     c.sc = sc; c.W = W; c.H = H; c.max_depth = max_depth; c.seed = seed;
     cam_setup(&sc->cam, W, H, &c.cam);
     fr_net net;
     fr_unpack(fr_H, fr_L, fr_blob, &net);
+    if (fp8) fr_quantize_fp8(&net);
     c.nif = NULL;
     c.fr = &net;
+    c.fr_fp8 = fp8 != 0;
     for (int k = 0; k < 3; ++k) c.env[k] = 1.0;
     render_pixels(&c, pix, n_pix, s0, s1, nthreads, out, stats);
     fr_net_free(&net);
     return 0;
+}
+EXPORT int orc_render_fr(const orc_scene* sc, int32_t fr_H, int32_t fr_L, const uint16_t* fr_blob, int32_t W,
+                         int32_t H, int32_t max_depth, uint64_t seed, const int64_t* pix, int64_t n_pix, int32_t s0,
+                         int32_t s1, int32_t nthreads, double* out, int64_t* stats) {
+    return orc_render_fr_ex(sc, fr_H, fr_L, fr_blob, 0, W, H, max_depth, seed, pix, n_pix, s0, s1, nthreads, out,
+                            stats);
 }
 
 /* Single path with its per-segment primitive ids (first-divergence classifier, tests only). */
@@ -1054,6 +1070,7 @@ EXPORT int32_t orc_trace_one(const orc_scene* sc, const uint16_t* nif_blob, cons
     nif64 net;
     if (nif_blob) { nif_unpack(nif_blob, &net); c.nif = &net; } else c.nif = NULL;
     c.fr = NULL;
+    c.fr_fp8 = 0;
     for (int k = 0; k < 3; ++k) c.env[k] = env_rgb ? env_rgb[k] : 1.0;
     path_stats st = {0, 0, 0, 0, 0};
     int32_t len = 0;

@@ -162,6 +162,26 @@ def test_render_paper_nif_vs_oracle(ptm, orc, kind, H, L):
         assert rel <= REL_RMSE_GATE, (cfg, rel)
 
 
+@pytest.mark.parametrize("H,L", [(64, 2), (256, 4)])
+def test_render_fp8_family_vs_oracle(ptm, orc, H, L):
+    """Frames lit by fp8 family members (the fused kernel) against the oracle path tracer with the same
+    e4m3 NIF model (render_fr(fp8=True), reading R24): config 0's box at full size and the Spheres scene on
+    sampled rows, the same rel-RMSE gate."""
+    blob = scenes.fourier_relu_family_blob(H, L, seed=1)
+    nif = ptm.Nif(blob, kind=ptm.NIF_FR_FAMILY, hidden=H, layers=L, fp8=True)
+    for cfg, W, Hh, spp, rows in ((0, 64, 64, 4, None), (2, 128, 96, 4, slice(0, 96, 6))):
+        c = scenes.CONFIGS[cfg]
+        src = scenes.scene_for_config(cfg)
+        img = ptm.render(ptm.Scene(src), nif, W, Hh, spp, c.max_depth, seed=2)
+        ys = np.arange(Hh)[rows] if rows is not None else np.arange(Hh)
+        pix = (ys[:, None] * W + np.arange(W)[None, :]).reshape(-1)
+        ref, _ = orc.OracleScene(src).render_fr(H, L, blob, W, Hh, c.max_depth, 2, pix=pix, s0=0, s1=spp, fp8=True)
+        got = img.reshape(-1, 3)[pix].astype(np.float64)
+        ref = ref / spp
+        rel = float(np.sqrt(((got - ref) ** 2).sum() / (ref ** 2).sum()))
+        assert rel <= REL_RMSE_GATE, (cfg, rel)
+
+
 @pytest.mark.parametrize("H,L", scenes.NIF_SWEEP + [(64, 3)])
 def test_family_fp8_vs_oracle(ptm, orc, mlp_path, H, L):
     """PT_NIF_FP8 against the oracle's e4m3 model (oracle.fr_eval_hl_fp8: weights, features and hidden

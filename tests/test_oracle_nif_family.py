@@ -161,3 +161,22 @@ def test_fp8_oracle_rounds_hidden_activations(orc):
     y8 = orc.fr_eval_hl_fp8(H, L, blob, uv)[0]
     y16 = orc.fr_eval_hl(H, L, blob, uv)[0]
     assert y16[0] == 1.0625 and y8[0] == 1.0 and y8[1] == 1.0 and y8[2] == 1.0
+
+
+@pytest.mark.parametrize("H,L", [(64, 2), (128, 4)])
+def test_render_fr_fp8_empty_scene_is_the_fp8_nif(orc, H, L):
+    """As the fp16 case: with the fp8 model (reading R24) the empty-scene render is exactly exp of
+    fr_eval_hl_fp8 at each camera ray's equirect coordinates."""
+    blob = scenes.fourier_relu_family_blob(H, L, seed=4)
+    sc = orc.OracleScene(scenes.empty_scene())
+    W, Hh, seed = 12, 8, 5
+    pix = np.arange(W * Hh)
+    out, st = sc.render_fr(H, L, blob, W, Hh, 4, seed, pix=pix, s0=0, s1=2, fp8=True)
+    want = np.zeros((W * Hh, 3))
+    for s in range(2):
+        d = orc.camera_rays(sc.scene.camera, W, Hh, seed, s, pix).astype(np.float64)
+        want += np.exp(orc.fr_eval_hl_fp8(H, L, blob, orc.equirect(d)))
+    assert st["escaped"] == W * Hh * 2
+    assert np.abs(out - want).max() <= 1e-12 * np.abs(want).max()
+    out16, _ = sc.render_fr(H, L, blob, W, Hh, 4, seed, pix=pix, s0=0, s1=2)
+    assert not np.array_equal(out, out16)                     # the flag reaches the evaluation
