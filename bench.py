@@ -297,8 +297,8 @@ def main():
     value = samples_per_step * args.steps / (ms_max / 1e3)
 
     # ---- end-to-end through the public API: host arrays in, host framebuffer out ----
-    e2e_steps = max(3, min(args.steps, 20))
-    e2e_warmup = max(1, min(args.warmup, 3))
+    e2e_steps = max(3, min(2 * args.steps, 100))      # host-side timing: more steps than the device loop
+    e2e_warmup = max(1, min(args.warmup, 5))
     host_fb = torch.empty(W * H * 3, dtype=torch.float32, pin_memory=True)
     host_np = host_fb.numpy()
     auto_k = max(1, min(spp, (8 << 20) // (W * H)))       # pt_render's wave size (pt_api.cu)
