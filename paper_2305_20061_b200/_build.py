@@ -19,12 +19,30 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
 
 
+STAMP = LIB + ".flags"
+
+
+def _deps():
+    """Every file the library's objects depend on: sources, private headers (.h and .cuh), the C-ABI
+    header and this build script."""
+    return (sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))
+            + glob.glob(os.path.join(INCLUDE, "*.h")) + [os.path.abspath(__file__)])
+
+
+def _flags_key(defines=()) -> str:
+    return " ".join([*ARCH, os.environ.get("PT_NVCC_EXTRA", ""), *[f"-D{d}" for d in defines]])
+
+
 def _stale() -> bool:
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
+        return True
+    try:
+        if open(STAMP).read() != _flags_key():
+            return True                   # built with other flags (PT_NVCC_EXTRA, defines)
+    except OSError:
         return True
     t = os.path.getmtime(LIB)
-    deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(INCLUDE, "*.h"))
-    return any(os.path.getmtime(p) > t for p in deps)
+    return any(os.path.getmtime(p) > t for p in _deps())
 
 
 def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
@@ -53,6 +71,9 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     tmp = lib + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"])
     os.replace(tmp, lib)
+    if out is None:
+        with open(STAMP, "w") as f:
+            f.write(_flags_key(defines))
     return lib
 
 

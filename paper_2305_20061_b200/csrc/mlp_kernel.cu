@@ -773,19 +773,16 @@ void mlp_free(pt_nif* nif) {
     cudaFree(nif->mlp_freq);
     cudaFree(nif->mlp_act[0]);
     cudaFree(nif->mlp_act[1]);
+    if (nif->mlp_last_use) cudaEventDestroy(nif->mlp_last_use);
+    nif->mlp_last_use = nullptr;
     nif->mlp_freq = nullptr;
     nif->mlp_act[0] = nif->mlp_act[1] = nullptr;
 }
 
 template <int BN, int kEpi, bool kFp8>
 static cudaError_t launch_layer_t(const mlp::LayerArgs& a, int grid, int smem, cudaStream_t st) {
-    static int configured = 0;
-    if (configured < smem) {
-        cudaError_t e = cudaFuncSetAttribute(mlp_layer_kernel<BN, kEpi, kFp8>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, mlp::kSmemBudget + mlp::kBarBytes);
-        if (e != cudaSuccess) return e;
-        configured = mlp::kSmemBudget + mlp::kBarBytes;
-    }
+    cudaError_t e = ensure_dyn_smem((const void*)mlp_layer_kernel<BN, kEpi, kFp8>, std::max(smem, mlp::kSmemBudget + mlp::kBarBytes));
+    if (e != cudaSuccess) return e;
     mlp_layer_kernel<BN, kEpi, kFp8><<<grid, mlp::kThreads, smem, st>>>(a);
     return cudaGetLastError();
 }
@@ -828,12 +825,8 @@ constexpr int kChunkRows = 1 << 20;
 template <int kH, bool kFp8>
 static cudaError_t launch_fused_t(const mlpf::FusedArgs& fa, int grid, cudaStream_t st) {
     const int smem = 1024 + mlpf::kRing * kH * 128 + mlpf::kMaxLayers * kH * 4;   // + the bias table
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(mlp_fused_kernel<kH, kFp8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    cudaError_t e = ensure_dyn_smem((const void*)mlp_fused_kernel<kH, kFp8>, smem);
+    if (e != cudaSuccess) return e;
     mlp_fused_kernel<kH, kFp8><<<grid * fused_ctas_per_sm<kH>(), mlpf::kThreads, smem, st>>>(fa);
     return cudaGetLastError();
 }
@@ -879,7 +872,23 @@ cudaError_t launch_mlp(pt_nif* nif, const float4* esc, const float4* esc_beta, c
     const int kc_of_H = (H * (fp8 ? 1 : 2) + 127) / 128;          // K chunks of an H-wide activation row
     const int cap = (int)std::min<int64_t>(kChunkRows, ((max_rows + kBM - 1) / kBM) * kBM);
     const int64_t need = (int64_t)((cap + kBM - 1) / kBM) * kAChunk * kc_of_H;
+    // the activation buffers are per-handle scratch: serialise their (re)allocation and order this use
+    // after the previous one, which may run on another stream
+    std::lock_guard<std::mutex> lk(nif->mlp_mu);
+    if (!nif->mlp_last_use) {
+        cudaError_t e = cudaEventCreateWithFlags(&nif->mlp_last_use, cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+    } else {
+        cudaError_t e = cudaStreamWaitEvent(st, nif->mlp_last_use, 0);
+        if (e != cudaSuccess) return e;
+    }
+    struct RecordOnExit {
+        cudaEvent_t ev;
+        cudaStream_t st;
+        ~RecordOnExit() { cudaEventRecord(ev, st); }
+    } record_on_exit{nif->mlp_last_use, st};
     if (need > nif->mlp_act_bytes) {
+        cudaEventSynchronize(nif->mlp_last_use);   // no earlier use may still read the old buffers
         cudaStreamSynchronize(st);
         cudaFree(nif->mlp_act[0]);
         cudaFree(nif->mlp_act[1]);

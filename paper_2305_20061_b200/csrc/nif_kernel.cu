@@ -17,8 +17,11 @@
 #include <math_constants.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "pt_internal.h"
@@ -437,28 +440,42 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
     }
 }
 
+int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev & 63;
+}
+
 int num_sms() {
-    static int n = 0;
-    if (n == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
+    static std::atomic<int> n[64];
+    const int dev = current_device();
+    int v = n[dev].load(std::memory_order_relaxed);
+    if (v <= 0) {
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        if (v <= 0) v = 148;
+        n[dev].store(v, std::memory_order_relaxed);
     }
-    return n;
+    return v;
+}
+
+cudaError_t ensure_dyn_smem(const void* kernel, int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, int> done;   // (device, kernel) -> bytes configured
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(mu);
+    int& have = done[{dev, kernel}];
+    if (have >= bytes) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) have = bytes;
+    return e;
 }
 
 template <bool kDebug>
 static cudaError_t nif_fr_launch_t(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,
                                    int grid, float* out, float* dbg, int dir_input, cudaStream_t st) {
     using namespace nif;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(nif_fr_kernel<kDebug>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kSmemBytes);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    cudaError_t e = ensure_dyn_smem((const void*)nif_fr_kernel<kDebug>, kSmemBytes);
+    if (e != cudaSuccess) return e;
     nif_fr_kernel<kDebug><<<grid, kThreads, kSmemBytes, st>>>((const uint8_t*)nif->d_smem_image, esc, esc_beta, count,
                                                                out, dbg, dir_input);
     return cudaGetLastError();

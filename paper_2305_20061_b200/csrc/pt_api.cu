@@ -265,6 +265,13 @@ int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, i
     rc = ensure_pool(pp, k * np);
     if (rc) return rc;
     CU(cudaStreamWaitEvent(st, pp.last_use, 0));   // previous user of the pooled buffers is done
+    // from here on work may be enqueued on st: record the pool's last use on every exit path, so the
+    // next user waits for whatever this call enqueued even when it returns an error
+    struct RecordOnExit {
+        cudaEvent_t ev;
+        cudaStream_t st;
+        ~RecordOnExit() { cudaEventRecord(ev, st); }
+    } record_on_exit{pp.last_use, st};
     pt::Workspace& ws = sc->ws;
     for (int b = 0; b < 2; ++b) {
         ws.rayA[b] = pp.rayA[b];
@@ -309,7 +316,6 @@ int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, i
         stats.waves += 1;
     }
     CU(cudaGetLastError());
-    CU(cudaEventRecord(pp.last_use, st));
     sc->stats = stats;   // kernel times and paths/segments/escaped are resolved by pt_get_stats
     return PT_OK;
 }
@@ -596,31 +602,41 @@ int pt_trace_rays(const pt_scene* scene, const float* d_o, const float* d_d, int
     return PT_OK;
 }
 
+// Scratch query queue of the pt_nif_infer hook, per device. Every use waits for the previous one (which
+// may run on another stream) through `last_use`, and growth first waits for it on the host.
+struct InferScratch {
+    std::mutex mu;
+    float4* esc = nullptr;
+    float4* esc_beta = nullptr;
+    uint32_t* cnt = nullptr;
+    int64_t cap = 0;
+    cudaEvent_t last_use = nullptr;
+};
+
 static int nif_infer_impl(const pt_nif* nif, const float* d_uv, int64_t n, float* d_rgb, float* d_dbg, void* stream) {
     if (!nif || n < 0 || (n > 0 && (!d_uv || !d_rgb))) return fail(PT_ERR_INVALID_ARG, "bad argument");
     if (n == 0) return PT_OK;
     if (n > (1ll << 31)) return fail(PT_ERR_INVALID_ARG, "too many queries");
     cudaStream_t st = (cudaStream_t)stream;
-    // scratch queue (test/bench hook): cached per process, grown on demand
-    static float4* esc = nullptr;
-    static float4* esc_beta = nullptr;
-    static uint32_t* cnt = nullptr;
-    static int64_t cap = 0;
-    static std::mutex mu;
-    std::lock_guard<std::mutex> lk(mu);
-    if (n > cap) {
-        CU(cudaStreamSynchronize(st));
-        cudaFree(esc); cudaFree(esc_beta);
-        esc = esc_beta = nullptr;
-        cap = 0;
-        CU(cudaMalloc(&esc, sizeof(float4) * n));
-        CU(cudaMalloc(&esc_beta, sizeof(float4) * n));
-        cap = n;
+    static InferScratch scratch[64];
+    InferScratch& sc = scratch[pt::current_device()];
+    std::lock_guard<std::mutex> lk(sc.mu);
+    if (!sc.last_use) CU(cudaEventCreateWithFlags(&sc.last_use, cudaEventDisableTiming));
+    if (n > sc.cap) {
+        CU(cudaEventSynchronize(sc.last_use));     // no earlier call may still use the old queue
+        cudaFree(sc.esc); cudaFree(sc.esc_beta);
+        sc.esc = sc.esc_beta = nullptr;
+        sc.cap = 0;
+        CU(cudaMalloc(&sc.esc, sizeof(float4) * n));
+        CU(cudaMalloc(&sc.esc_beta, sizeof(float4) * n));
+        sc.cap = n;
     }
-    if (!cnt) CU(cudaMalloc(&cnt, sizeof(uint32_t)));
-    pt::launch_pack_queries(d_uv, n, esc, esc_beta, cnt, st);
-    cudaError_t e = d_dbg ? pt::launch_nif_debug(nif, esc, esc_beta, cnt, n, d_rgb, d_dbg, st)
-                          : pt::launch_nif(nif, esc, esc_beta, cnt, n, d_rgb, 0, st);
+    if (!sc.cnt) CU(cudaMalloc(&sc.cnt, sizeof(uint32_t)));
+    CU(cudaStreamWaitEvent(st, sc.last_use, 0));
+    pt::launch_pack_queries(d_uv, n, sc.esc, sc.esc_beta, sc.cnt, st);
+    cudaError_t e = d_dbg ? pt::launch_nif_debug(nif, sc.esc, sc.esc_beta, sc.cnt, n, d_rgb, d_dbg, st)
+                          : pt::launch_nif(nif, sc.esc, sc.esc_beta, sc.cnt, n, d_rgb, 0, st);
+    cudaEventRecord(sc.last_use, st);            // also on failure: the pack kernel was enqueued
     if (e != cudaSuccess) return fail(PT_ERR_CUDA, std::string("nif launch: ") + cudaGetErrorString(e));
     return PT_OK;
 }

@@ -128,6 +128,10 @@ struct pt_nif {
     std::vector<MlpLayer> mlp_layers;
     void* mlp_act[2] = {nullptr, nullptr};   // blocked activation ping-pong buffers (lazily sized)
     int64_t mlp_act_bytes = 0;
+    // the layered path's activation buffers are per-handle scratch: mlp_mu guards their (re)allocation
+    // and every use is ordered after the previous one by mlp_last_use (recorded on the using stream)
+    std::mutex mlp_mu;
+    cudaEvent_t mlp_last_use = nullptr;
 };
 
 namespace pt {
@@ -168,7 +172,10 @@ void nif_build_smem_image(const uint16_t* blob, std::vector<uint8_t>* image);
 void nif_build_smem_image_fr(const uint16_t* blob, std::vector<uint8_t>* image);
 cudaError_t launch_nif(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,
                        int64_t max_rows, float* out, int dir_input, cudaStream_t st);
-int num_sms();
+int num_sms();   // SM count of the current device (cached per device)
+int current_device();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel): the attribute is per device
+cudaError_t ensure_dyn_smem(const void* kernel, int bytes);
 // the paper's NIF family (mlp_kernel.cu)
 int mlp_concat_layer(int L);
 int64_t mlp_blob_halves(int H, int L);

@@ -401,13 +401,8 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
 template <bool kDebug>
 static cudaError_t siren_launch_t(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,
                                   int grid, float* out, float* dbg, int dir_input, cudaStream_t st) {
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(siren_kernel<kDebug>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             siren::kSmemBytes);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    cudaError_t e = ensure_dyn_smem((const void*)siren_kernel<kDebug>, siren::kSmemBytes);
+    if (e != cudaSuccess) return e;
     return launch_pdl(siren_kernel<kDebug>, dim3(grid), dim3(siren::kThreads), siren::kSmemBytes, st,
                       (const uint8_t*)nif->d_smem_image, esc, esc_beta, count, out, dbg, dir_input);
 }

@@ -15,6 +15,7 @@
 #include <math_constants.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <cstdlib>
 
 #include "pt_internal.h"
@@ -984,6 +985,20 @@ static int resident_grid(K kernel, int block) {
     return num_sms() * (per_sm > 0 ? per_sm : 1);
 }
 
+// resident grids of the two path kernels, per device (occupancy and SM count are per-device properties)
+static int2 path_grids() {
+    static std::atomic<int> g1[64], g2[64];
+    const int dev = current_device();
+    int a = g1[dev].load(std::memory_order_relaxed), b = g2[dev].load(std::memory_order_relaxed);
+    if (a <= 0 || b <= 0) {
+        a = resident_grid(first_bounce_kernel, 128);
+        b = resident_grid(path_kernel, 128);
+        g1[dev].store(a, std::memory_order_relaxed);
+        g2[dev].store(b, std::memory_order_relaxed);
+    }
+    return make_int2(a, b);
+}
+
 void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int first_sample, int n_slots, int max_depth,
                   uint64_t seed, int use_nif, float3 env, Workspace& ws, cudaStream_t st) {
     ShadeArgs a;
@@ -1001,11 +1016,10 @@ void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int fir
     a.use_nif = use_nif; a.env = env;
     a.qA = ws.rayA[0]; a.qB = ws.rayB[0]; a.qC = ws.rayC[0];
     a.esc = ws.esc; a.esc_beta = ws.esc_beta; a.wave_buf = ws.wave_buf;
-    static const int grid1 = resident_grid(first_bounce_kernel, 128);
-    static const int grid2 = resident_grid(path_kernel, 128);
+    const int2 grids = path_grids();
     a.work = ws.counters + kCounterWork;
-    first_bounce_kernel<<<grid1, 128, 0, st>>>(a);
-    if (max_depth > 1) launch_pdl(path_kernel, dim3(grid2), dim3(128), 0, st, a);
+    first_bounce_kernel<<<grids.x, 128, 0, st>>>(a);
+    if (max_depth > 1) launch_pdl(path_kernel, dim3(grids.y), dim3(128), 0, st, a);
 }
 
 void launch_accumulate(const float* wave_buf, int n_pix, int k, float* fb, const uint32_t* counters,

@@ -36,4 +36,10 @@ for name, d in per.items():
     out[name] = {"launches": n, "dram_bytes_per_launch": sum(d["bytes"]) / n,
                  "dram_bytes_total": sum(d["bytes"]), "ns_per_launch": sum(d["ns"]) / n,
                  "warp_inst_per_launch": sum(d["inst"]) / n}
+if len(sys.argv) > 2:     # kernel-sources hash of the capture (bench.py flags stale captures)
+    sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
+    import bench
+    out["sources_sha16"] = bench.sources_sha16(bench.TRACE_SOURCES if sys.argv[2] == "trace" else bench.NIF_SOURCES)
+    out["trace_sources_sha16"] = bench.sources_sha16(bench.TRACE_SOURCES)
+    out["nif_sources_sha16"] = bench.sources_sha16(bench.NIF_SOURCES)
 print(json.dumps(out, indent=1))

@@ -58,4 +58,6 @@ for cfg in (1, 2, 3, 4):
     k["alg_bytes_per_segment"] = 64 * k["per_segment"]["visits"] + 48 * k["per_segment"]["prims"] + 80
     out[f"render_c{cfg}"] = k
     del S, N
+import bench  # noqa: E402  (sources hash: bench.py flags a capture taken with other kernel sources)
+out["sources_sha16"] = bench.sources_sha16(bench.TRACE_SOURCES)
 print(json.dumps(out, indent=1))
