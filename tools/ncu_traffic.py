@@ -24,18 +24,28 @@ for r in rows[hi + 1:]:
     if len(r) <= vi:
         continue
     name = r[ki].split("(")[0].replace("void ", "").replace("pt::", "").split("<")[0].strip()
-    v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1)
+    u = r[ui]
+    f = scale.get(u)
+    if f is None:     # counts with an SI prefix ("Ksector", "Minst", ...)
+        f = {"K": 1e3, "M": 1e6, "G": 1e9}.get(u[:1], 1) if len(u) > 1 and u[1:2].islower() else 1
+    v = float(r[vi].replace(",", "")) * f
     launch.setdefault((name, r[idi]), {})[r[ni]] = v
 for (name, _), m in launch.items():
     per[name]["bytes"].append(m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0))
     per[name]["ns"].append(m.get("gpu__time_duration.sum", 0))
     per[name]["inst"].append(m.get("smsp__inst_executed.sum", 0))
+    per[name]["tinst"].append(m.get("smsp__thread_inst_executed.sum", 0))
+    per[name]["lld"].append(m.get("l1tex__t_sectors_pipe_lsu_mem_local_op_ld.sum", 0))
+    per[name]["lst"].append(m.get("l1tex__t_sectors_pipe_lsu_mem_local_op_st.sum", 0))
 out = {}
 for name, d in per.items():
     n = len(d["bytes"])
     out[name] = {"launches": n, "dram_bytes_per_launch": sum(d["bytes"]) / n,
                  "dram_bytes_total": sum(d["bytes"]), "ns_per_launch": sum(d["ns"]) / n,
-                 "warp_inst_per_launch": sum(d["inst"]) / n}
+                 "warp_inst_per_launch": sum(d["inst"]) / n,
+                 "thread_inst_per_launch": sum(d["tinst"]) / n,
+                 "simt_efficiency": (sum(d["tinst"]) / (32.0 * sum(d["inst"]))) if sum(d["inst"]) else None,
+                 "local_ld_sectors_per_launch": sum(d["lld"]) / n, "local_st_sectors_per_launch": sum(d["lst"]) / n}
 if len(sys.argv) > 2:     # kernel-sources hash of the capture (bench.py flags stale captures)
     sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
     import bench
