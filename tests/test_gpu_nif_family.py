@@ -183,12 +183,13 @@ def test_render_fp8_family_vs_oracle(ptm, orc, H, L):
 
 
 @pytest.mark.parametrize("H,L", scenes.NIF_SWEEP + [(64, 3)])
-def test_family_fp8_vs_oracle(ptm, orc, mlp_path, H, L):
+def test_family_fp8_vs_oracle(ptm, orc, parity_log, mlp_path, H, L):
     """PT_NIF_FP8 against the oracle's e4m3 model (oracle.fr_eval_hl_fp8: weights, features and hidden
     activations rounded to e4m3, everything else exact). The two differ by fp32 vs fp64 sums, which can
     flip an activation's e4m3 rounding (one code, <= 12.5 % of that activation) when its exact value lies
     within ~1e-6 of a rounding boundary: rare, and damped by the 0.1-scaled output layer. Gates: median
-    |dy| <= 1e-4, 99th percentile <= 1e-2, max <= 0.1 (log space). Both paths: the fused kernel
+    |dy| <= 1e-4, 99th percentile <= 1e-3, max <= 1e-2 (log space; the north_star NIF tolerance), and
+    the max relative error of exp(y) <= 1e-2. Both paths: the fused kernel
     (H <= 256) and the per-layer GEMMs."""
     import torch
     if H == 1024 and mlp_path == "fused":
@@ -204,6 +205,12 @@ def test_family_fp8_vs_oracle(ptm, orc, mlp_path, H, L):
     y = orc.fr_eval_hl_fp8(H, L, blob, uv[idx].astype(np.float64))
     dy = np.abs(np.log(got[idx]) - y).max(1)
     print(f"fp8 {mlp_path} H{H}L{L}: median {np.median(dy):.2e} p99 {np.quantile(dy, 0.99):.2e} max {dy.max():.2e}")
+    ref = np.exp(y)
+    rel = (np.abs(got[idx] - ref) / ref).max()
+    parity_log(f"nif_fp8_{mlp_path}_H{H}L{L}_max_abs_dy", dy.max(), 1e-2, median=float(np.median(dy)),
+               p99=float(np.quantile(dy, 0.99)))
+    parity_log(f"nif_fp8_{mlp_path}_H{H}L{L}_max_rel", rel, 1e-2)
     assert np.median(dy) <= 1e-4
-    assert np.quantile(dy, 0.99) <= 1e-2
-    assert dy.max() <= 0.1
+    assert np.quantile(dy, 0.99) <= 1e-3
+    assert dy.max() <= 1e-2
+    assert rel <= 1e-2

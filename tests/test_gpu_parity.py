@@ -42,7 +42,7 @@ def _uv_cases(n, seed):
 
 @pytest.mark.parametrize("n", [1, 127, 128, 129, 1000, 4 * 148 * 128 + 77])
 @pytest.mark.parametrize("scale", [1.0, 30.0])
-def test_nif_vs_oracle(ptm, orc, n, scale):
+def test_nif_vs_oracle(ptm, orc, parity_log, n, scale):
     import torch
     blob = scenes.siren_blob(0, out_scale=scale)
     nif = ptm.Nif(blob)
@@ -55,8 +55,12 @@ def test_nif_vs_oracle(ptm, orc, n, scale):
     # rounding of the last hidden activations, 2^-11 * max_j sum_k |W5_jk|, exceeds it
     W5 = scenes.nif_layers_from_blob(blob)[4][0]
     log_gate = max(NIF_LOG_GATE, 2.0 ** -11 * np.abs(W5).sum(1).max())
-    assert np.abs(np.log(got) - y).max() <= log_gate
-    assert (np.abs(got - ref) / ref).max() <= NIF_REL_GATE
+    dy = np.abs(np.log(got) - y).max()
+    rel = (np.abs(got - ref) / ref).max()
+    parity_log(f"nif_siren_x{scale:g}_n{n}_max_abs_dy", dy, log_gate)
+    parity_log(f"nif_siren_x{scale:g}_n{n}_max_rel", rel, NIF_REL_GATE)
+    assert dy <= log_gate
+    assert rel <= NIF_REL_GATE
 
 
 def test_nif_bench_size_sampled(ptm, orc, blob):
@@ -165,7 +169,7 @@ def test_fr_nif_rejects_wrong_size(ptm, fr_blob, blob):
         ptm.Nif(fr_blob, kind=7)
 
 
-def _primary_check(ptm, orc, sc, W, H, pix, seed=0, sample=0):
+def _primary_check(ptm, orc, sc, W, H, pix, seed=0, sample=0, log=None, name=None):
     prim_g, t_g = ptm.trace_primary(ptm.Scene(sc), W, H, seed, sample)
     prim_g = prim_g.cpu().numpy()[pix]
     t_g = t_g.cpu().numpy()[pix]
@@ -173,6 +177,8 @@ def _primary_check(ptm, orc, sc, W, H, pix, seed=0, sample=0):
     eq = prim_g == prim_o
     frac = eq.mean()
     mism = ~eq
+    if log is not None:
+        log(name, frac, 0.9999, pixels=int(len(pix)), mismatches=int(mism.sum()), higher_is_better=True)
     assert frac >= 0.9999, f"primary-hit agreement {frac}"
     assert (edge[mism] <= 1e-5).all(), f"mismatches off the edge band: {edge[mism]}"
     hit = prim_o >= 0
@@ -182,19 +188,39 @@ def _primary_check(ptm, orc, sc, W, H, pix, seed=0, sample=0):
 
 
 @pytest.mark.parametrize("cfg", [0, 1, 2])
-def test_primary_hits_full_frame(ptm, orc, cfg):
+def test_primary_hits_full_frame(ptm, orc, parity_log, cfg):
     c = scenes.CONFIGS[cfg]
     sc = scenes.scene_for_config(cfg)
     pix = np.arange(c.n_pix, dtype=np.int64)
-    assert _primary_check(ptm, orc, sc, c.width, c.height, pix) == 1.0
+    assert _primary_check(ptm, orc, sc, c.width, c.height, pix, log=parity_log,
+                          name=f"primary_hits_c{cfg}_full_s0") == 1.0
 
 
-def test_primary_hits_small_bvh_sampled(ptm, orc):
+def test_primary_hits_small_bvh_sampled(ptm, orc, parity_log):
     c = scenes.CONFIGS[3]
     sc = scenes.scene_for_config(3)
     rows = np.arange(0, c.height, 8)
     pix = (rows[:, None] * c.width + np.arange(c.width)[None, :]).reshape(-1).astype(np.int64)
-    assert _primary_check(ptm, orc, sc, c.width, c.height, pix, sample=3) == 1.0
+    assert _primary_check(ptm, orc, sc, c.width, c.height, pix, sample=3, log=parity_log,
+                          name="primary_hits_c3_rows8_s3") == 1.0
+
+
+@pytest.fixture(scope="module")
+def large_bvh():
+    return scenes.scene_for_config(4)
+
+
+@pytest.mark.parametrize("sample", [0, 3])
+def test_primary_hits_large_bvh_sampled(ptm, orc, parity_log, large_bvh, sample):
+    """Config 4 (5.08 M triangles of 64 overlapping displaced icospheres seen from 8-15 units: the
+    geometry where SURVEY 8c predicts fp32 barycentric error above the 1e-5 band), every 16th pixel of
+    samples 0 and 3: the north_star gate (>= 99.99 % equal, any remainder inside the edge band); the
+    certified test with its fp64 fallback makes it 100 %."""
+    c = scenes.CONFIGS[4]
+    pix = np.arange(0, c.n_pix, 16, dtype=np.int64)
+    frac = _primary_check(ptm, orc, large_bvh, c.width, c.height, pix, sample=sample, log=parity_log,
+                          name=f"primary_hits_c4_every16_s{sample}")
+    assert frac == 1.0
 
 
 @pytest.mark.parametrize("seed", [0, 1])
@@ -235,16 +261,18 @@ def _rel_rmse(a, b):
     return float(np.sqrt(((a - b) ** 2).sum() / (b ** 2).sum()))
 
 
-def test_render_config0_full_vs_oracle(ptm, orc, blob):
+def test_render_config0_full_vs_oracle(ptm, orc, blob, parity_log):
     c = scenes.CONFIGS[0]
     sc = scenes.scene_for_config(0)
     img = ptm.render(ptm.Scene(sc), ptm.Nif(blob), c.width, c.height, c.spp, c.max_depth, seed=c.seed)
     ref, _ = orc.OracleScene(sc).render(c.width, c.height, c.max_depth, c.seed, s0=0, s1=c.spp, nif_blob=blob)
     ref = ref.reshape(c.height, c.width, 3) / c.spp
-    assert _rel_rmse(img, ref) <= REL_RMSE_GATE
+    rel = _rel_rmse(img, ref)
+    parity_log("frame_rel_rmse_c0_full", rel, REL_RMSE_GATE)
+    assert rel <= REL_RMSE_GATE
 
 
-def test_render_config1_rows_vs_oracle(ptm, orc, blob):
+def test_render_config1_rows_vs_oracle(ptm, orc, blob, parity_log):
     """Config 1 at full size in the bench launch configuration; oracle on every 16th row."""
     c = scenes.CONFIGS[1]
     sc = scenes.scene_for_config(1)
@@ -254,7 +282,9 @@ def test_render_config1_rows_vs_oracle(ptm, orc, blob):
     ref, _ = orc.OracleScene(sc).render(c.width, c.height, c.max_depth, c.seed, pix=pix, s0=0, s1=c.spp,
                                         nif_blob=blob)
     got = img.reshape(-1, 3)[pix]
-    assert _rel_rmse(got, ref / c.spp) <= REL_RMSE_GATE
+    rel = _rel_rmse(got, ref / c.spp)
+    parity_log("frame_rel_rmse_c1_rows16", rel, REL_RMSE_GATE)
+    assert rel <= REL_RMSE_GATE
 
 
 def test_render_deterministic_and_wave_invariant(ptm, blob):
@@ -279,7 +309,7 @@ def _rows_pix(c, n_rows):
 
 
 @pytest.mark.parametrize("cfg,n_rows", [(2, 12), (3, 6), (4, 4)])
-def test_render_full_size_rows_vs_oracle(ptm, orc, blob, cfg, n_rows):
+def test_render_full_size_rows_vs_oracle(ptm, orc, blob, parity_log, cfg, n_rows):
     """Configs 2-4 at full resolution and full spp (config 4: 5.08 M triangles, constant env);
     the oracle evaluates evenly spaced full rows of the same frame."""
     c = scenes.CONFIGS[cfg]
@@ -292,6 +322,7 @@ def test_render_full_size_rows_vs_oracle(ptm, orc, blob, cfg, n_rows):
                                         nif_blob=blob if c.use_nif else None, env_rgb=c.env_rgb)
     got = img.reshape(-1, 3)[pix].astype(np.float64)
     rel = _rel_rmse(got, ref / c.spp)
+    parity_log(f"frame_rel_rmse_c{cfg}_{n_rows}rows", rel, REL_RMSE_GATE)
     assert rel <= REL_RMSE_GATE, rel
 
 
