@@ -7,10 +7,30 @@
 // behind one base index, leaf primitives are stored inline, and each child box is quantised to fp16
 // offsets from the node origin -- lo rounded down, hi rounded up, then corrected until the exact fp32
 // decode the traversal kernel performs (O + f16) contains the exact box. Every node is re-verified.
+//
+// Parallel build (std::thread workers per call):
+//   1.+2. binned-SAH splits over a reference array partitioned in place (32-B records, so every pass
+//      streams memory), collapsed to 4-wide nodes as they are made (no binary tree is stored); each split
+//      passes its children's bounds and centroid bounds down (one pass per node); wide subtrees above a
+//      grain size are handed to idle workers through a shared queue;
+//   3. subtree sizes and the pool layout: a node's child block is followed by the regions of its
+//      interior children in order (depth-first, the first child's block right behind its parent's);
+//   4. every wide node's record, inline primitives and block padding are written in parallel (disjoint
+//      ranges; the pool is never zero-filled).
+// The tree depends only on the input (the splits are deterministic), so the pool is identical for any
+// thread count and run.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <atomic>
 #include <cmath>
+#include <condition_variable>
 #include <cstring>
+#include <deque>
 #include <limits>
+#include <mutex>
+#include <thread>
 
 #include "pt_internal.h"
 
@@ -18,13 +38,18 @@ namespace pt {
 
 namespace {
 
+constexpr float kInf = std::numeric_limits<float>::infinity();
+
 struct Box {
     float lo[3], hi[3];
     void empty() {
-        for (int a = 0; a < 3; ++a) { lo[a] = std::numeric_limits<float>::infinity(); hi[a] = -lo[a]; }
+        for (int a = 0; a < 3; ++a) { lo[a] = kInf; hi[a] = -kInf; }
     }
     void grow(const Box& b) {
         for (int a = 0; a < 3; ++a) { lo[a] = std::min(lo[a], b.lo[a]); hi[a] = std::max(hi[a], b.hi[a]); }
+    }
+    void grow_pt(const float* p) {
+        for (int a = 0; a < 3; ++a) { lo[a] = std::min(lo[a], p[a]); hi[a] = std::max(hi[a], p[a]); }
     }
     double area() const {
         double dx = (double)hi[0] - lo[0], dy = (double)hi[1] - lo[1], dz = (double)hi[2] - lo[2];
@@ -33,121 +58,306 @@ struct Box {
     }
 };
 
-struct Node2 {
+// primitive reference: its exact fp32 box and id (32 B); the centroid is 0.5 (lo + hi)
+struct Ref {
     Box b;
-    int32_t left = -1, right = -1;
-    int32_t first = 0, count = 0;  // leaf iff count > 0
+    uint32_t id;
+    uint32_t pad;
+    void centroid(float* c) const {
+        for (int a = 0; a < 3; ++a) c[a] = 0.5f * (b.lo[a] + b.hi[a]);
+    }
+};
+static_assert(sizeof(Ref) == 32, "Ref layout");
+
+
+int n_workers(int64_t n) {
+    unsigned hc = std::thread::hardware_concurrency();
+    if (const char* e = std::getenv("PT_BVH_THREADS")) hc = (unsigned)std::max(1, std::atoi(e));
+    if (hc == 0) hc = 1;
+    if (n < 20000) return 1;
+    return (int)std::min<unsigned>(hc, 64);
+}
+
+// ---- 1.+2. binned-SAH splits, collapsed to 4-wide nodes on the fly --------------------------------
+// A wide node is built from its binary node: split it, then repeatedly split the largest-area interior
+// child (the first one on equal areas) until it has 4 children or only leaves are left -- exactly the
+// collapse of the full binary tree, without storing it. Every child's own split is decided here too
+// (its leaf/interior kind and size go into the parent's record); an interior child carries its two
+// binary children into its own task.
+struct Item {
+    int64_t first, count;
+    Box bb, cb;   // bounds of the primitives and of their centroids
+};
+
+struct WChild {
+    Box b;
+    int32_t ref;     // leaf: first reference; interior: wide-node id
+    int32_t count;   // leaf: primitive count; interior: 0
+};
+static_assert(sizeof(WChild) == 32, "WChild layout");
+
+struct Wide {
+    WChild c[4];
+    int32_t nch = 0;
+    int32_t depth = 1;
+    int64_t block = 0;    // units of the child block (multiple of 4)
+    int64_t region = 0;   // units of the child block plus the regions of all interior children
+    int64_t rec = 0;      // unit of this node's 64-B record
+    int64_t base = 0;     // unit of its child block
+};
+
+struct WideTask {
+    int32_t id, depth;
+    Item it, l, r;   // the node and its (already decided) binary split
 };
 
 struct Builder {
-    std::vector<Box> pbox;
-    std::vector<float> cen;  // [n][3]
-    std::vector<int64_t> order;
-    std::vector<Node2> nodes;
+    std::vector<Ref> refs;
+    std::vector<Wide> wide;          // preallocated (at most one wide node per primitive)
+    std::atomic<int32_t> next_wide{1};
+    std::atomic<int64_t> n_leaves{0};
+    std::atomic<int32_t> max_depth{1};
+    std::mutex mu;
+    std::condition_variable cv;
+    std::deque<WideTask> queue;
+    int busy = 0;
+    bool done = false;
+    static constexpr int64_t kGrain = 2048;   // subtrees larger than this may move to another worker
+    static constexpr int NB = 16;
 
-    void build(int64_t n) {
-        order.resize(n);
-        for (int64_t i = 0; i < n; ++i) order[i] = i;
-        nodes.reserve(2 * n + 1);
-        nodes.emplace_back();
-        struct Item { int64_t node, first, count; };
-        std::vector<Item> stack;
-        stack.push_back({0, 0, n});
-        constexpr int NB = 16;
-        while (!stack.empty()) {
-            Item it = stack.back();
-            stack.pop_back();
-            Box bb, cb;
-            bb.empty();
-            cb.empty();
-            for (int64_t i = it.first; i < it.first + it.count; ++i) {
-                int64_t id = order[i];
-                bb.grow(pbox[id]);
-                for (int a = 0; a < 3; ++a) {
-                    cb.lo[a] = std::min(cb.lo[a], cen[3 * id + a]);
-                    cb.hi[a] = std::max(cb.hi[a], cen[3 * id + a]);
-                }
+    void build(int threads) {
+        const int64_t n = (int64_t)refs.size();
+        wide.resize((size_t)std::max<int64_t>(1, n));
+        Item root{0, n, {}, {}};
+        root.bb.empty();
+        root.cb.empty();
+        for (const Ref& r : refs) {
+            float c[3];
+            r.centroid(c);
+            root.bb.grow(r.b);
+            root.cb.grow_pt(c);
+        }
+        WideTask t0{0, 1, root, {}, {}};
+        if (!split(root, t0.l, t0.r)) {     // one leaf: a root node with a single leaf child
+            Wide& w = wide[0];
+            w.nch = 1;
+            w.c[0] = WChild{root.bb, 0, (int32_t)n};
+            n_leaves = 1;
+            next_wide = 1;
+            return;
+        }
+        if (threads <= 1) {
+            run_local(t0, false);
+            return;
+        }
+        queue.push_back(t0);
+        std::vector<std::thread> ws;
+        for (int t = 0; t < threads; ++t) ws.emplace_back([this] { worker(); });
+        for (auto& w : ws) w.join();
+    }
+
+    void worker() {
+        for (;;) {
+            WideTask t;
+            {
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait(lk, [&] { return done || !queue.empty(); });
+                if (queue.empty()) return;   // done
+                t = queue.front();
+                queue.pop_front();
+                ++busy;
             }
-            nodes[it.node].b = bb;
-            int axis = 0;
-            float ext = cb.hi[0] - cb.lo[0];
-            for (int a = 1; a < 3; ++a)
-                if (cb.hi[a] - cb.lo[a] > ext) { ext = cb.hi[a] - cb.lo[a]; axis = a; }
-            int64_t split = -1;
-            if (it.count > 1 && ext > 0.0f) {
-                int64_t cnt[NB] = {0};
-                Box bins[NB];
-                for (auto& b : bins) b.empty();
-                const double scale = NB / (double)ext;
-                auto bin_of = [&](int64_t id) {
-                    int k = (int)(((double)cen[3 * id + axis] - cb.lo[axis]) * scale);
-                    return std::min(NB - 1, std::max(0, k));
-                };
-                for (int64_t i = it.first; i < it.first + it.count; ++i) {
-                    int64_t id = order[i];
-                    int k = bin_of(id);
-                    cnt[k]++;
-                    bins[k].grow(pbox[id]);
+            run_local(t, true);
+            {
+                std::lock_guard<std::mutex> lk(mu);
+                --busy;
+                if (busy == 0 && queue.empty()) {
+                    done = true;
+                    cv.notify_all();
                 }
-                // prefix/suffix sweeps
-                double rarea[NB];
-                int64_t rcnt[NB];
-                Box acc;
-                acc.empty();
-                int64_t c = 0;
-                for (int k = NB - 1; k >= 1; --k) {
-                    acc.grow(bins[k]);
-                    c += cnt[k];
-                    rarea[k] = acc.area();
-                    rcnt[k] = c;
-                }
-                double best = std::numeric_limits<double>::infinity();
-                int best_k = -1;
-                acc.empty();
-                c = 0;
-                for (int k = 0; k < NB - 1; ++k) {
-                    acc.grow(bins[k]);
-                    c += cnt[k];
-                    if (c == 0 || rcnt[k + 1] == 0) continue;
-                    double cost = acc.area() * (double)c + rarea[k + 1] * (double)rcnt[k + 1];
-                    if (cost < best) { best = cost; best_k = k; }
-                }
-                // SAH with a node-traversal cost of kTraversalCost primitive tests (per unit area)
-                constexpr double kTraversalCost = 1.5;
-                double leaf_cost = bb.area() * (double)it.count;
-                best += kTraversalCost * bb.area();
-                if (best_k >= 0 && (best < leaf_cost || it.count > kMaxLeafPrims)) {
-                    auto mid = std::partition(order.begin() + it.first, order.begin() + it.first + it.count,
-                                              [&](int64_t id) { return bin_of(id) <= best_k; });
-                    split = mid - order.begin();
-                }
-            } else if (it.count > kMaxLeafPrims) {
-                split = it.first + it.count / 2;  // coincident centroids
-            }
-            if (split > it.first && split < it.first + it.count) {
-                int64_t l = (int64_t)nodes.size();
-                nodes.emplace_back();
-                nodes.emplace_back();
-                nodes[it.node].left = (int32_t)l;
-                nodes[it.node].right = (int32_t)(l + 1);
-                stack.push_back({l + 1, split, it.first + it.count - split});
-                stack.push_back({l, it.first, split - it.first});
-            } else {
-                nodes[it.node].first = (int32_t)it.first;
-                nodes[it.node].count = (int32_t)it.count;
             }
         }
+    }
+
+    void run_local(const WideTask& top, bool share) {
+        std::vector<WideTask> stack;
+        stack.push_back(top);
+        WideTask kids[4];
+        while (!stack.empty()) {
+            const WideTask t = stack.back();
+            stack.pop_back();
+            const int nk = make_wide(t, kids);
+            for (int k = nk - 1; k >= 0; --k) {
+                if (share && k > 0 && kids[k].it.count > kGrain) {
+                    std::lock_guard<std::mutex> lk(mu);
+                    if (queue.size() < 1024) {
+                        queue.push_back(kids[k]);
+                        cv.notify_one();
+                        continue;
+                    }
+                }
+                stack.push_back(kids[k]);
+            }
+        }
+    }
+
+    // Build wide node t.id from its split; returns its interior children's tasks.
+    int make_wide(const WideTask& t, WideTask* kids) {
+        struct Cand {
+            Item it, l, r;
+            int state;   // 0 undecided, 1 leaf, 2 interior (l, r valid)
+        };
+        Cand c[4];
+        int nc = 2;
+        c[0] = Cand{t.l, {}, {}, 0};
+        c[1] = Cand{t.r, {}, {}, 0};
+        auto decide = [&](Cand& x) {
+            if (x.state == 0) x.state = split(x.it, x.l, x.r) ? 2 : 1;
+        };
+        while (nc < 4) {
+            // the largest-area interior candidate (first on ties), deciding candidates as needed
+            int best = -1;
+            double ba = -1.0;
+            bool retry = true;
+            while (retry) {
+                retry = false;
+                best = -1;
+                ba = -1.0;
+                for (int i = 0; i < nc; ++i) {
+                    if (c[i].state == 1) continue;
+                    const double a = c[i].it.bb.area();
+                    if (a > ba) { ba = a; best = i; }
+                }
+                if (best >= 0 && c[best].state == 0) {
+                    decide(c[best]);
+                    if (c[best].state == 1) retry = true;
+                }
+            }
+            if (best < 0) break;
+            const Cand e = c[best];
+            for (int i = best; i + 1 < nc; ++i) c[i] = c[i + 1];
+            --nc;
+            c[nc++] = Cand{e.l, {}, {}, 0};
+            c[nc++] = Cand{e.r, {}, {}, 0};
+        }
+        for (int i = 0; i < nc; ++i) decide(c[i]);
+        Wide& w = wide[t.id];
+        w.depth = t.depth;
+        int nk = 0, o = 0;
+        for (int pass = 0; pass < 2; ++pass) {          // interior children first, then leaves
+            for (int i = 0; i < nc; ++i) {
+                const bool interior = c[i].state == 2;
+                if (interior != (pass == 0)) continue;
+                if (interior) {
+                    const int32_t id = next_wide.fetch_add(1);
+                    w.c[o++] = WChild{c[i].it.bb, id, 0};
+                    kids[nk++] = WideTask{id, t.depth + 1, c[i].it, c[i].l, c[i].r};
+                } else {
+                    w.c[o++] = WChild{c[i].it.bb, (int32_t)c[i].it.first, (int32_t)c[i].it.count};
+                    n_leaves.fetch_add(1, std::memory_order_relaxed);
+                }
+            }
+        }
+        w.nch = o;
+        int32_t md = max_depth.load(std::memory_order_relaxed);
+        while (t.depth > md && !max_depth.compare_exchange_weak(md, t.depth)) {
+        }
+        return nk;
+    }
+
+    // Split one node (binned SAH over the widest centroid axis, node-traversal cost 1.5 primitive tests
+    // per unit area), or decide it is a leaf. Returns true and the two children if it was split; the
+    // references of the node are partitioned in place.
+    bool split(const Item& it, Item& L, Item& R) {
+        int axis = 0;
+        float ext = it.cb.hi[0] - it.cb.lo[0];
+        for (int a = 1; a < 3; ++a)
+            if (it.cb.hi[a] - it.cb.lo[a] > ext) { ext = it.cb.hi[a] - it.cb.lo[a]; axis = a; }
+        Ref* const r0 = refs.data() + it.first;
+        const int64_t cnt_all = it.count;
+        int64_t split = -1;
+        Box lb, lcb, rb, rcb;
+        if (cnt_all > 1 && ext > 0.0f) {
+            int64_t cnt[NB] = {0};
+            Box bins[NB], cbins[NB];
+            for (int k = 0; k < NB; ++k) { bins[k].empty(); cbins[k].empty(); }
+            const float scale = (float)(NB / (double)ext);
+            const float c0 = it.cb.lo[axis];
+            auto bin_of = [&](const Ref& r) {
+                const float c = 0.5f * (r.b.lo[axis] + r.b.hi[axis]);
+                const int k = (int)((c - c0) * scale);
+                return std::min(NB - 1, std::max(0, k));
+            };
+            for (int64_t i = 0; i < cnt_all; ++i) {
+                const Ref& r = r0[i];
+                const int k = bin_of(r);
+                cnt[k]++;
+                bins[k].grow(r.b);
+                float c[3];
+                r.centroid(c);
+                cbins[k].grow_pt(c);
+            }
+            double rarea[NB];
+            int64_t rcnt[NB];
+            Box acc;
+            acc.empty();
+            int64_t c = 0;
+            for (int k = NB - 1; k >= 1; --k) {
+                acc.grow(bins[k]);
+                c += cnt[k];
+                rarea[k] = acc.area();
+                rcnt[k] = c;
+            }
+            double best = std::numeric_limits<double>::infinity();
+            int best_k = -1;
+            acc.empty();
+            c = 0;
+            for (int k = 0; k < NB - 1; ++k) {
+                acc.grow(bins[k]);
+                c += cnt[k];
+                if (c == 0 || rcnt[k + 1] == 0) continue;
+                const double cost = acc.area() * (double)c + rarea[k + 1] * (double)rcnt[k + 1];
+                if (cost < best) { best = cost; best_k = k; }
+            }
+            constexpr double kTraversalCost = 1.5;
+            const double leaf_cost = it.bb.area() * (double)cnt_all;
+            best += kTraversalCost * it.bb.area();
+            if (best_k >= 0 && (best < leaf_cost || cnt_all > kMaxLeafPrims)) {
+                Ref* mid = std::partition(r0, r0 + cnt_all, [&](const Ref& r) { return bin_of(r) <= best_k; });
+                split = it.first + (mid - r0);
+                lb.empty(); lcb.empty(); rb.empty(); rcb.empty();
+                for (int k = 0; k < NB; ++k) {
+                    if (k <= best_k) { lb.grow(bins[k]); lcb.grow(cbins[k]); }
+                    else { rb.grow(bins[k]); rcb.grow(cbins[k]); }
+                }
+            }
+        } else if (cnt_all > kMaxLeafPrims) {
+            split = it.first + cnt_all / 2;   // coincident centroids
+            lb.empty(); lcb.empty(); rb.empty(); rcb.empty();
+            for (int64_t i = 0; i < cnt_all; ++i) {
+                float c[3];
+                r0[i].centroid(c);
+                if (it.first + i < split) { lb.grow(r0[i].b); lcb.grow_pt(c); }
+                else { rb.grow(r0[i].b); rcb.grow_pt(c); }
+            }
+        }
+        if (split > it.first && split < it.first + cnt_all) {
+            L = Item{it.first, split - it.first, lb, lcb};
+            R = Item{split, it.first + cnt_all - split, rb, rcb};
+            return true;
+        }
+        return false;
     }
 };
 
 inline float f32_next_down(double x) {
     float f = (float)x;
-    if ((double)f > x) f = std::nextafter(f, -std::numeric_limits<float>::infinity());
+    if ((double)f > x) f = std::nextafter(f, -kInf);
     return f;
 }
 inline float f32_next_up(double x) {
     float f = (float)x;
-    if ((double)f < x) f = std::nextafter(f, std::numeric_limits<float>::infinity());
+    if ((double)f < x) f = std::nextafter(f, kInf);
     return f;
 }
 
@@ -156,7 +366,7 @@ inline float f32_next_up(double x) {
 // (positive: the value rises by at most 15 ulps; negative: the magnitude falls by at most 15 ulps).
 inline float embed_nibble(float lo, uint32_t nib) {
     float x = lo;
-    for (int i = 0; i < 16; ++i) x = std::nextafter(x, -std::numeric_limits<float>::infinity());
+    for (int i = 0; i < 16; ++i) x = std::nextafter(x, -kInf);
     uint32_t b = __builtin_bit_cast(uint32_t, x);
     b = (b & ~15u) | (nib & 15u);
     return __builtin_bit_cast(float, b);
@@ -166,6 +376,27 @@ inline float decode(float O, uint16_t h) {
     volatile float hv = (float)f16_value(h);   // exact widening
     volatile float s = O + hv;                 // the single fp32 round-to-nearest add the kernel does
     return s;
+}
+
+template <typename F>
+void parallel_for(int threads, int64_t n, F f) {
+    if (threads <= 1 || n < 1024) {
+        for (int64_t i = 0; i < n; ++i) f(i);
+        return;
+    }
+    std::atomic<int64_t> next{0};
+    constexpr int64_t kChunk = 512;
+    std::vector<std::thread> ws;
+    for (int t = 0; t < threads; ++t)
+        ws.emplace_back([&] {
+            for (;;) {
+                const int64_t s = next.fetch_add(kChunk);
+                if (s >= n) return;
+                const int64_t e = std::min(n, s + kChunk);
+                for (int64_t i = s; i < e; ++i) f(i);
+            }
+        });
+    for (auto& w : ws) w.join();
 }
 
 }  // namespace
@@ -204,155 +435,186 @@ uint16_t f16_round_up(double x) {
 int build_wide_bvh(const pt_triangle* tris, int64_t n_tris, const pt_sphere* sph, int64_t n_sph, HostBvh* out,
                    std::string* msg) {
     const int64_t n = n_tris + n_sph;
-    out->pool.clear();
+    out->pool.reset();
+    out->units = 0;
     out->empty = (n == 0);
     out->n_nodes = out->n_leaves = out->max_depth = 0;
     if (n == 0) return PT_OK;
+    const int threads = n_workers(n);
+    static const bool timing = std::getenv("PT_BVH_TIMING") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto t0 = now();
+    auto lap = [&](const char* what) {
+        if (!timing) return;
+        auto t1 = now();
+        std::fprintf(stderr, "bvh %-10s %8.2f ms (%d threads)\n", what,
+                     std::chrono::duration<double, std::milli>(t1 - t0).count(), threads);
+        t0 = t1;
+    };
+    if (n >= (1ll << 30)) { *msg = "too many primitives for the BVH builder (< 2^30)"; return PT_ERR_INVALID_ARG; }
     Builder B;
-    B.pbox.resize(n);
-    B.cen.resize(3 * n);
-    for (int64_t i = 0; i < n; ++i) {
-        Box& b = B.pbox[i];
+    B.refs.resize(n);
+    parallel_for(threads, n, [&](int64_t i) {
+        Ref& r = B.refs[i];
+        r.id = (uint32_t)i;
+        r.pad = 0;
         if (i < n_tris) {
             const pt_triangle& t = tris[i];
             for (int a = 0; a < 3; ++a) {
-                b.lo[a] = std::min(t.v0[a], std::min(t.v1[a], t.v2[a]));
-                b.hi[a] = std::max(t.v0[a], std::max(t.v1[a], t.v2[a]));
+                r.b.lo[a] = std::min(t.v0[a], std::min(t.v1[a], t.v2[a]));
+                r.b.hi[a] = std::max(t.v0[a], std::max(t.v1[a], t.v2[a]));
             }
         } else {
             const pt_sphere& s = sph[i - n_tris];
             for (int a = 0; a < 3; ++a) {
-                b.lo[a] = f32_next_down((double)s.center[a] - (double)s.radius);
-                b.hi[a] = f32_next_up((double)s.center[a] + (double)s.radius);
+                r.b.lo[a] = f32_next_down((double)s.center[a] - (double)s.radius);
+                r.b.hi[a] = f32_next_up((double)s.center[a] + (double)s.radius);
             }
         }
-        for (int a = 0; a < 3; ++a) B.cen[3 * i + a] = 0.5f * (b.lo[a] + b.hi[a]);
+    });
+    lap("refs");
+    B.build(threads);
+    lap("wide");
+    const int64_t n_wide = B.next_wide.load();
+    std::vector<Wide>& W = B.wide;
+    // ---- 3. layout: block sizes, regions (children have larger ids than parents: reverse order), then
+    // bases in id order (a node's base depends only on its parent's base and its earlier siblings) ----
+    for (int64_t wi = n_wide - 1; wi >= 0; --wi) {
+        Wide& w = W[wi];
+        int64_t units = 0, region = 0;
+        for (int i = 0; i < w.nch; ++i) {
+            if (w.c[i].count == 0) {
+                units += kNodeUnits;
+                region += W[w.c[i].ref].region;
+            } else {
+                units += (int64_t)kPrimUnits * w.c[i].count;
+            }
+        }
+        w.block = (units + 3) & ~int64_t(3);
+        w.region = w.block + region;
     }
-    B.build(n);
+    const int64_t total = (int64_t)kNodeUnits + W[0].region;
+    if (total > (1ll << 28)) { *msg = "BVH pool exceeds 2^28 units (4 GiB)"; return PT_ERR_DOMAIN; }
+    W[0].rec = 0;
+    W[0].base = kNodeUnits;
+    for (int64_t wi = 0; wi < n_wide; ++wi) {
+        const Wide& w = W[wi];
+        int64_t next = w.base + w.block;
+        for (int i = 0; i < w.nch; ++i) {
+            if (w.c[i].count != 0) continue;
+            Wide& c = W[w.c[i].ref];
+            c.rec = w.base + (int64_t)kNodeUnits * i;   // interior children lead the block
+            c.base = next;
+            next += c.region;
+        }
+    }
+    lap("layout");
+    // every unit is written below (records, inline primitives, block padding): no zero fill
+    out->pool.reset(new uint4[(size_t)total]);
+    out->units = total;
+    uint4* pool = out->pool.get();
+    const Ref* refs = B.refs.data();
+    lap("alloc");
 
-    // ---- collapse to 4-wide + layout ----------------------------------------------------------
-    std::vector<uint4>& pool = out->pool;
-    auto alloc = [&](int64_t units) {
-        int64_t at = (int64_t)pool.size();
-        pool.resize(at + units, make_uint4(0, 0, 0, 0));
-        return at;
-    };
-    struct Pending { int32_t n2; int64_t unit; int64_t depth; };
-    std::vector<Pending> work;
-    alloc(kNodeUnits);
-    work.push_back({0, 0, 1});
-    int64_t n_nodes = 0, n_leaves = 0, maxd = 0;
-    while (!work.empty()) {
-        Pending pnd = work.back();
-        work.pop_back();
-        ++n_nodes;
-        maxd = std::max(maxd, pnd.depth);
-        std::vector<int32_t> ch;
-        const Node2& root2 = B.nodes[pnd.n2];
-        if (root2.count > 0) ch.push_back(pnd.n2);   // whole scene is one leaf
-        else { ch.push_back(root2.left); ch.push_back(root2.right); }
-        while ((int)ch.size() < 4) {
-            int best = -1;
-            double ba = -1.0;
-            for (int i = 0; i < (int)ch.size(); ++i) {
-                const Node2& c = B.nodes[ch[i]];
-                if (c.count == 0 && c.b.area() > ba) { ba = c.b.area(); best = i; }
-            }
-            if (best < 0) break;
-            int32_t e = ch[best];
-            ch.erase(ch.begin() + best);
-            ch.push_back(B.nodes[e].left);
-            ch.push_back(B.nodes[e].right);
-        }
-        // interior children first, then leaves
-        std::stable_partition(ch.begin(), ch.end(), [&](int32_t c) { return B.nodes[c].count == 0; });
-        int64_t units = 0;
-        for (int32_t c : ch) units += B.nodes[c].count == 0 ? kNodeUnits : (int64_t)kPrimUnits * B.nodes[c].count;
-        units = (units + 3) & ~int64_t(3);
-        int64_t base = alloc(units);
-        if (base + units > (1ll << 28)) { *msg = "BVH pool exceeds 2^28 units (4 GiB)"; return PT_ERR_DOMAIN; }
-        // node header. Child metadata: one nibble per child = its size in pool units (0: no child,
-        // 4: interior node, 3 * count: leaf of count primitives), so the kernel gets validity, kind,
-        // count and the running child offset from one 16-bit field: nibbles 0-2 ride in the low
-        // mantissa bits of the origin's x, y, z (embed_nibble), nibble 3 in the top bits of the base.
+    // ---- 4. records and inline primitives, in parallel ----
+    std::atomic<int> err{0};
+    std::mutex err_mu;
+    parallel_for(threads, n_wide, [&](int64_t wi) {
+        const Wide& w = W[wi];
+        // Child metadata: one nibble per child = its size in pool units (0: no child, 4: interior node,
+        // 3 * count: leaf of count primitives), so the kernel gets validity, kind, count and the running
+        // child offset from one 16-bit field: nibbles 0-2 ride in the low mantissa bits of the origin's
+        // x, y, z (embed_nibble), nibble 3 in the top bits of the base.
         uint32_t nib[4] = {0, 0, 0, 0};
-        for (int ci = 0; ci < (int)ch.size(); ++ci) {
-            const Node2& c = B.nodes[ch[ci]];
-            nib[ci] = c.count > 0 ? (uint32_t)(kPrimUnits * c.count) : (uint32_t)kNodeUnits;
-        }
         Box nb;
         nb.empty();
-        for (int32_t c : ch) nb.grow(B.nodes[c].b);
+        for (int ci = 0; ci < w.nch; ++ci) {
+            const WChild& c = w.c[ci];
+            nib[ci] = c.count > 0 ? (uint32_t)(kPrimUnits * c.count) : (uint32_t)kNodeUnits;
+            nb.grow(c.b);
+        }
         float Oq[3];
         for (int a = 0; a < 3; ++a) Oq[a] = embed_nibble(nb.lo[a], nib[a]);
-        uint4& h0 = pool[pnd.unit];
+        uint4& h0 = pool[w.rec];
         h0.x = __builtin_bit_cast(uint32_t, Oq[0]);
         h0.y = __builtin_bit_cast(uint32_t, Oq[1]);
         h0.z = __builtin_bit_cast(uint32_t, Oq[2]);
-        h0.w = (uint32_t)base | (nib[3] << 28);
+        h0.w = (uint32_t)w.base | (nib[3] << 28);
         uint16_t q[4][6];
         std::memset(q, 0, sizeof(q));
-        int64_t off = base;
-        for (int ci = 0; ci < (int)ch.size(); ++ci) {
-            const Node2& c = B.nodes[ch[ci]];
+        int64_t off = w.base;
+        for (int ci = 0; ci < w.nch; ++ci) {
+            const WChild& c = w.c[ci];
             for (int a = 0; a < 3; ++a) {
                 const float O = Oq[a];
-                double dlo = (double)c.b.lo[a] - (double)O, dhi = (double)c.b.hi[a] - (double)O;
+                const double dlo = (double)c.b.lo[a] - (double)O, dhi = (double)c.b.hi[a] - (double)O;
                 if (!(dhi <= 65504.0) || !(dlo >= 0.0)) {
-                    *msg = "child box offset outside the fp16 range (scene extent too large for one node)";
-                    return PT_ERR_DOMAIN;
+                    std::lock_guard<std::mutex> lk(err_mu);
+                    if (!err.exchange(1))
+                        *msg = "child box offset outside the fp16 range (scene extent too large for one node)";
+                    return;
                 }
                 uint16_t hl = f16_round_down(dlo);
                 while (hl > 0 && decode(O, hl) > c.b.lo[a]) --hl;
                 uint16_t hh = f16_round_up(dhi);
                 while (decode(O, hh) < c.b.hi[a]) {
-                    if (hh >= 0x7BFF) { *msg = "child box hi beyond fp16 range"; return PT_ERR_DOMAIN; }
+                    if (hh >= 0x7BFF) {
+                        std::lock_guard<std::mutex> lk(err_mu);
+                        if (!err.exchange(1)) *msg = "child box hi beyond fp16 range";
+                        return;
+                    }
                     ++hh;
                 }
                 q[ci][a] = hl;
                 q[ci][3 + a] = hh;
             }
-            const bool leaf = c.count > 0;
-            if (leaf) {
-                ++n_leaves;
-                for (int k = 0; k < c.count; ++k) {
-                    int64_t id = B.order[c.first + k];
+            if (c.count > 0) {
+                for (int64_t k = 0; k < c.count; ++k) {
+                    const uint32_t id = refs[c.ref + k].id;
                     uint4* u = &pool[off + kPrimUnits * k];
-                    if (id < n_tris) {
+                    // material bits ride in the spare words, so shading reads the hit primitive from here
+                    if ((int64_t)id < n_tris) {
                         const pt_triangle& t = tris[id];
                         u[0] = make_uint4(__builtin_bit_cast(uint32_t, t.v0[0]), __builtin_bit_cast(uint32_t, t.v0[1]),
-                                          __builtin_bit_cast(uint32_t, t.v0[2]), (uint32_t)id);
+                                          __builtin_bit_cast(uint32_t, t.v0[2]), id);
                         u[1] = make_uint4(__builtin_bit_cast(uint32_t, t.v1[0]), __builtin_bit_cast(uint32_t, t.v1[1]),
-                                          __builtin_bit_cast(uint32_t, t.v1[2]), 0u);
+                                          __builtin_bit_cast(uint32_t, t.v1[2]), t.material);
                         u[2] = make_uint4(__builtin_bit_cast(uint32_t, t.v2[0]), __builtin_bit_cast(uint32_t, t.v2[1]),
                                           __builtin_bit_cast(uint32_t, t.v2[2]), 0u);
                     } else {
                         const pt_sphere& s = sph[id - n_tris];
                         u[0] = make_uint4(__builtin_bit_cast(uint32_t, s.center[0]),
                                           __builtin_bit_cast(uint32_t, s.center[1]),
-                                          __builtin_bit_cast(uint32_t, s.center[2]), (uint32_t)id | kSphereFlag);
-                        u[1] = make_uint4(__builtin_bit_cast(uint32_t, s.radius), 0u, 0u, 0u);
+                                          __builtin_bit_cast(uint32_t, s.center[2]), id | kSphereFlag);
+                        u[1] = make_uint4(__builtin_bit_cast(uint32_t, s.radius), s.material, 0u, 0u);
                         u[2] = make_uint4(0u, 0u, 0u, 0u);
                     }
                 }
                 off += (int64_t)kPrimUnits * c.count;
             } else {
-                work.push_back({ch[ci], off, pnd.depth + 1});
                 off += kNodeUnits;
             }
         }
+        for (int64_t u = off; u < w.base + w.block; ++u) pool[u] = make_uint4(0, 0, 0, 0);   // block padding
         // pack the 4 x 12-B child records into units 1..3: one word per axis, (lo | hi << 16), so the
         // kernel decodes both bounds of an axis with one packed fp16x2 -> fp32x2 conversion
         uint32_t words[12];
         for (int ci = 0; ci < 4; ++ci)
             for (int a = 0; a < 3; ++a) words[3 * ci + a] = (uint32_t)q[ci][a] | ((uint32_t)q[ci][3 + a] << 16);
-        pool[pnd.unit + 1] = make_uint4(words[0], words[1], words[2], words[3]);
-        pool[pnd.unit + 2] = make_uint4(words[4], words[5], words[6], words[7]);
-        pool[pnd.unit + 3] = make_uint4(words[8], words[9], words[10], words[11]);
+        pool[w.rec + 1] = make_uint4(words[0], words[1], words[2], words[3]);
+        pool[w.rec + 2] = make_uint4(words[4], words[5], words[6], words[7]);
+        pool[w.rec + 3] = make_uint4(words[8], words[9], words[10], words[11]);
+    });
+    lap("fill");
+    if (err.load()) {
+        out->pool.reset();
+        out->units = 0;
+        return PT_ERR_DOMAIN;
     }
-    out->n_nodes = n_nodes;
-    out->n_leaves = n_leaves;
-    out->max_depth = maxd;
+    out->n_nodes = n_wide;
+    out->n_leaves = B.n_leaves.load();
+    out->max_depth = B.max_depth.load();
+    const int64_t maxd = out->max_depth;
     if (3 * maxd + 4 > kStackSize) { *msg = "BVH too deep for the traversal stack"; return PT_ERR_DOMAIN; }
     return PT_OK;
 }

@@ -196,9 +196,6 @@ pt::TraceParams trace_params(const pt_scene* sc) {
     pt::TraceParams tp;
     tp.pool = sc->d_pool;
     tp.empty = sc->empty ? 1 : 0;
-    tp.tri_v = sc->d_tri_v;
-    tp.sph = sc->d_sph;
-    tp.sph_mat = sc->d_sph_mat;
     tp.mats = sc->d_mats;
     tp.n_tris = sc->n_tris;
     return tp;
@@ -407,50 +404,26 @@ int pt_scene_create(const pt_triangle* tris, int64_t n_tris, const pt_sphere* sp
         if (_e != cudaSuccess)                                                                           \
             return cleanup(_e == cudaErrorMemoryAllocation ? PT_ERR_OOM : PT_ERR_CUDA, cudaGetErrorString(_e)); \
     } while (0)
-    // one device allocation and one copy for everything the scene owns: BVH pool, shading vertices,
-    // spheres, materials, and the wave's counters and stats (256-B aligned sub-buffers)
-    sc->pool_units = (int64_t)bvh.pool.size();
+    // one device allocation for everything the scene owns: materials, the wave's counters and stats
+    // (256-B aligned, uploaded from one small zeroed host block), then the BVH pool with its inline
+    // primitives (uploaded straight from the builder's buffer; shading reads the hit primitive there)
+    sc->pool_units = bvh.units;
     static_assert(sizeof(pt::DevMaterial) == sizeof(pt_material), "material layout");
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-    const size_t b_pool = al(sizeof(uint4) * sc->pool_units), b_tri = al(sizeof(float4) * 3 * n_tris),
-                 b_sph = al(sizeof(float4) * n_spheres), b_smat = al(sizeof(uint32_t) * n_spheres),
-                 b_mat = al(sizeof(pt_material) * n_mats), b_cnt = al(sizeof(uint32_t) * pt::kCounters),
+    const size_t b_mat = al(sizeof(pt_material) * n_mats), b_cnt = al(sizeof(uint32_t) * pt::kCounters),
                  b_st = al(sizeof(unsigned long long) * 4);
-    const size_t total = b_pool + b_tri + b_sph + b_smat + b_mat + b_cnt + b_st;
-    std::vector<uint8_t> host(total, 0);
-    size_t o = 0;
-    const size_t o_pool = o; o += b_pool;
-    const size_t o_tri = o; o += b_tri;
-    const size_t o_sph = o; o += b_sph;
-    const size_t o_smat = o; o += b_smat;
-    const size_t o_mat = o; o += b_mat;
-    const size_t o_cnt = o; o += b_cnt;
-    const size_t o_st = o;
-    if (sc->pool_units > 0) std::memcpy(&host[o_pool], bvh.pool.data(), sizeof(uint4) * sc->pool_units);
-    float4* tv = reinterpret_cast<float4*>(&host[o_tri]);
-    for (int64_t i = 0; i < n_tris; ++i) {
-        uint32_t mb = tris[i].material;
-        float mf;
-        std::memcpy(&mf, &mb, 4);
-        tv[3 * i + 0] = make_float4(tris[i].v0[0], tris[i].v0[1], tris[i].v0[2], mf);
-        tv[3 * i + 1] = make_float4(tris[i].v1[0], tris[i].v1[1], tris[i].v1[2], 0.0f);
-        tv[3 * i + 2] = make_float4(tris[i].v2[0], tris[i].v2[1], tris[i].v2[2], 0.0f);
-    }
-    float4* sv = reinterpret_cast<float4*>(&host[o_sph]);
-    uint32_t* sm = reinterpret_cast<uint32_t*>(&host[o_smat]);
-    for (int64_t i = 0; i < n_spheres; ++i) {
-        sv[i] = make_float4(spheres[i].center[0], spheres[i].center[1], spheres[i].center[2], spheres[i].radius);
-        sm[i] = spheres[i].material;
-    }
+    const size_t b_small = b_mat + b_cnt + b_st;
+    const size_t b_pool = sizeof(uint4) * (size_t)sc->pool_units;
+    const size_t total = b_small + b_pool;
+    std::vector<uint8_t> host(b_small, 0);
+    const size_t o_mat = 0, o_cnt = b_mat, o_st = b_mat + b_cnt;
     if (n_mats > 0) std::memcpy(&host[o_mat], mats, sizeof(pt_material) * n_mats);
     sc->d_alloc_bytes = total;
     CUS(cache_alloc(sc->device, total, &sc->d_alloc));
-    CUS(upload(sc->device, sc->d_alloc, host.data(), total));
     uint8_t* base = static_cast<uint8_t*>(sc->d_alloc);
-    sc->d_pool = sc->pool_units > 0 ? reinterpret_cast<uint4*>(base + o_pool) : nullptr;
-    sc->d_tri_v = n_tris > 0 ? reinterpret_cast<float4*>(base + o_tri) : nullptr;
-    sc->d_sph = n_spheres > 0 ? reinterpret_cast<float4*>(base + o_sph) : nullptr;
-    sc->d_sph_mat = n_spheres > 0 ? reinterpret_cast<uint32_t*>(base + o_smat) : nullptr;
+    CUS(upload(sc->device, base, host.data(), b_small));
+    if (b_pool > 0) CUS(upload(sc->device, base + b_small, bvh.pool.get(), b_pool));
+    sc->d_pool = sc->pool_units > 0 ? reinterpret_cast<uint4*>(base + b_small) : nullptr;
     sc->d_mats = n_mats > 0 ? reinterpret_cast<pt::DevMaterial*>(base + o_mat) : nullptr;
     sc->ws.counters = reinterpret_cast<uint32_t*>(base + o_cnt);
     sc->ws.d_stats = reinterpret_cast<unsigned long long*>(base + o_st);
@@ -687,10 +660,10 @@ PT_API int pt_debug_build_bvh(const pt_triangle* tris, int64_t n_tris, const pt_
         stats[0] = bvh.n_nodes;
         stats[1] = bvh.n_leaves;
         stats[2] = bvh.max_depth;
-        stats[3] = (int64_t)bvh.pool.size();
+        stats[3] = bvh.units;
     }
-    if (pool_out && pool_cap_units >= (int64_t)bvh.pool.size())
-        std::memcpy(pool_out, bvh.pool.data(), sizeof(uint4) * bvh.pool.size());
+    if (pool_out && pool_cap_units >= bvh.units && bvh.units > 0)
+        std::memcpy(pool_out, bvh.pool.get(), sizeof(uint4) * bvh.units);
     return PT_OK;
 }
 

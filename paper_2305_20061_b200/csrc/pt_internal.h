@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -24,7 +25,8 @@ namespace pt {
 //   A child block holds the node's children contiguously (first child implicit at `base`, like the
 //   paper's "first child is implicitly stored next"): interior children first (4 units
 //   each), then the leaves' primitives inline, 3 units (48 B) per primitive:
-//     triangle: (v0.xyz, id) (v1.xyz, 0) (v2.xyz, 0); sphere: (c.xyz, id | SPHERE_FLAG) (r, 0, 0, 0) (0)
+//     triangle: (v0.xyz, id) (v1.xyz, material) (v2.xyz, 0); sphere: (c.xyz, id | SPHERE_FLAG) (r, material, 0, 0) (0)
+//   (shading reads the hit primitive's vertices and material from here: no separate vertex arrays)
 // ---------------------------------------------------------------------------------------------
 constexpr uint32_t kSphereFlag = 0x80000000u;
 constexpr int kNodeUnits = 4;
@@ -40,7 +42,8 @@ struct DevMaterial {        // 32 B, same field order as pt_material
 };
 
 struct HostBvh {
-    std::vector<uint4> pool;  // 16-B units
+    std::unique_ptr<uint4[]> pool;  // 16-B units
+    int64_t units = 0;
     int64_t n_nodes = 0, n_leaves = 0, max_depth = 0;
     bool empty = true;
 };
@@ -97,9 +100,6 @@ struct pt_scene {
     uint4* d_pool = nullptr;          // wide BVH + inline primitives
     int64_t pool_units = 0;
     bool empty = true;
-    float4* d_tri_v = nullptr;        // [n_tris*3] vertices (shading), .w of vertex 0 = material bits
-    float4* d_sph = nullptr;          // [n_sph] (c, r)
-    uint32_t* d_sph_mat = nullptr;    // [n_sph]
     pt::DevMaterial* d_mats = nullptr;
     int64_t bvh_nodes = 0, bvh_leaves = 0, bvh_depth = 0;
     std::mutex mu;                    // guards ws + stats
@@ -146,9 +146,6 @@ Cam32 make_cam32(const pt_camera& c, int W, int H);
 struct TraceParams {
     const uint4* pool;
     int empty;
-    const float4* tri_v;
-    const float4* sph;
-    const uint32_t* sph_mat;
     const DevMaterial* mats;
     int64_t n_tris;
 };

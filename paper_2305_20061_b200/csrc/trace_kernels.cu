@@ -462,9 +462,22 @@ constexpr uint32_t kNoEntry = 0xFFFFFFFFu;
 __device__ __forceinline__ bool is_node(uint32_t e) { return e < (1u << 28); }
 __device__ __forceinline__ bool is_leaf(uint32_t e) { return e - (1u << 28) < 0xE0000000u; }   // nibble 1..14
 
+// Traversal stack: the bottom kShortStack entries of every thread live in shared memory, laid out
+// [depth][thread] so that a warp's accesses are bank-conflict free whatever depth each lane is at; deeper
+// entries spill to a local-memory array (rare: 3 pushes per level at most, 9-14 levels on configs 3-4).
+// All kernels that trace run 128-thread blocks.
+#ifndef PT_SSTACK
+#define PT_SSTACK 16
+#endif
+constexpr int kShortStack = PT_SSTACK;
+constexpr int kTraceBlock = 128;
+
 __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
     Hit best{CUDART_INF, CUDART_INF_F, CUDART_INF_F, -1, 0u, true};
     if (tp.empty) return best;
+    __shared__ uint32_t s_ent[kShortStack][kTraceBlock];
+    __shared__ float s_tn[kShortStack][kTraceBlock];
+    const int tid = threadIdx.x;
     float4 cold[2];                   // local memory: written and read only through ld/st.local asm
     RayT r;
     ray_prepare(o, d, r, (uint32_t)__cvta_generic_to_local(cold));
@@ -475,8 +488,17 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
     uint32_t swz[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) swz[a] = ((r.kbits >> (8 + a)) & 1u) ? 0x1032u : 0x3210u;
-    uint2 stack[kStackSize];
+    uint2 lstack[kStackSize - kShortStack];   // overflow (local memory)
     int sp = 0;
+    auto push = [&](uint32_t e, float t) {
+        if (sp < kShortStack) {
+            s_ent[sp][tid] = e;
+            s_tn[sp][tid] = t;
+        } else {
+            lstack[sp - kShortStack] = make_uint2(e, __float_as_uint(t));
+        }
+        ++sp;
+    };
     const uint4* __restrict__ pool = tp.pool;
     TCOUNT(4, 1);
     // While-while traversal with postponed leaves (Aila & Laine 2009): interior nodes are visited until
@@ -490,10 +512,20 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
     float leaf_t = 0.0f;
     auto pop = [&](float tcull) -> uint32_t {
         while (sp > 0) {
-            const uint2 e = stack[--sp];
-            if (__uint_as_float(e.y) <= tcull) {
-                cur_t = __uint_as_float(e.y);
-                return e.x;
+            --sp;
+            uint32_t e;
+            float t;
+            if (sp < kShortStack) {
+                e = s_ent[sp][tid];
+                t = s_tn[sp][tid];
+            } else {
+                const uint2 v = lstack[sp - kShortStack];
+                e = v.x;
+                t = __uint_as_float(v.y);
+            }
+            if (t <= tcull) {
+                cur_t = t;
+                return e;
             }
         }
         return kNoEntry;
@@ -551,7 +583,7 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
                 // (non-hit children carry +inf; the bound may be +inf, so test finiteness explicitly)
 #pragma unroll
                 for (int ci = 3; ci >= 1; --ci)
-                    if (ctn[ci] < CUDART_INF_F) stack[sp++] = make_uint2(cent[ci], __float_as_uint(ctn[ci]));
+                    if (ctn[ci] < CUDART_INF_F) push(cent[ci], ctn[ci]);
                 if (ctn[0] < CUDART_INF_F) {
                     cur = cent[0];
                     cur_t = ctn[0];
@@ -650,23 +682,26 @@ __device__ __forceinline__ void shade_segment(const ShadeArgs& a, int depth, uin
     }
     const float t = (float)hh.t;
     const float3 P = make_float3(fmaf(t, d.x, o.x), fmaf(t, d.y, o.y), fmaf(t, d.z, o.z));
+    // the hit primitive's record in the BVH pool (just read by the traversal): vertices / sphere + material
     float3 ng;
     uint32_t mi;
-    if (prim < a.tp.n_tris) {
-        const float4 v0 = __ldg(a.tp.tri_v + 3 * prim), v1 = __ldg(a.tp.tri_v + 3 * prim + 1),
-                     v2 = __ldg(a.tp.tri_v + 3 * prim + 2);
-        const float3 e1 = make_float3(v1.x - v0.x, v1.y - v0.y, v1.z - v0.z);
-        const float3 e2 = make_float3(v2.x - v0.x, v2.y - v0.y, v2.z - v0.z);
+    const uint4 u0 = __ldg(a.tp.pool + hh.unit), u1 = __ldg(a.tp.pool + hh.unit + 1);
+    if (!(u0.w & kSphereFlag)) {
+        const uint4 u2 = __ldg(a.tp.pool + hh.unit + 2);
+        const float3 v0 = make_float3(__uint_as_float(u0.x), __uint_as_float(u0.y), __uint_as_float(u0.z));
+        const float3 e1 = make_float3(__uint_as_float(u1.x) - v0.x, __uint_as_float(u1.y) - v0.y,
+                                      __uint_as_float(u1.z) - v0.z);
+        const float3 e2 = make_float3(__uint_as_float(u2.x) - v0.x, __uint_as_float(u2.y) - v0.y,
+                                      __uint_as_float(u2.z) - v0.z);
         ng = make_float3(e1.y * e2.z - e1.z * e2.y, e1.z * e2.x - e1.x * e2.z, e1.x * e2.y - e1.y * e2.x);
         const float il = rsqrtf(ng.x * ng.x + ng.y * ng.y + ng.z * ng.z);
         ng = make_float3(ng.x * il, ng.y * il, ng.z * il);
-        mi = __float_as_uint(v0.w);
+        mi = u1.w;
     } else {
-        const int si = prim - (int)a.tp.n_tris;
-        const float4 s = __ldg(a.tp.sph + si);
-        const float ir = 1.0f / s.w;
-        ng = make_float3((P.x - s.x) * ir, (P.y - s.y) * ir, (P.z - s.z) * ir);
-        mi = __ldg(a.tp.sph_mat + si);
+        const float ir = 1.0f / __uint_as_float(u1.x);
+        ng = make_float3((P.x - __uint_as_float(u0.x)) * ir, (P.y - __uint_as_float(u0.y)) * ir,
+                         (P.z - __uint_as_float(u0.z)) * ir);
+        mi = u1.y;
     }
     const DevMaterial m = a.tp.mats[mi];
     const float cosd = d.x * ng.x + d.y * ng.y + d.z * ng.z;
