@@ -397,8 +397,12 @@ static void closest_bvh(const orc_scene* sc, const ray_pre* r, hit_rec* h) {
     while (sp > 0) {
         int32_t ni = stack[--sp];
         const bvh_node* nd = &sc->nodes[ni];
-        double tb = h->prim < 0 ? INFINITY : h->t;
-        /* cull only boxes entered strictly beyond the best hit: ties are kept (reading R11) */
+        /* cull only boxes entered beyond the best hit: ties are kept (reading R11). The entry distance
+           carries its own rounding (and the primitive's t its own), so a box whose computed entry lies a
+           few ulps beyond a tied hit at its face can still hold an equal-t, smaller-id primitive (rays
+           through a shared vertex): the bound is widened by 2^-32 relative, far above the fp64 rounding of
+           both, so the BVH returns exactly the brute-force (t, id) minimum. */
+        double tb = h->prim < 0 ? INFINITY : h->t * (1.0 + 0x1p-32);
         double te = slab(r, &nd->b, INFINITY);
         if (te == INFINITY || te > tb) continue;
         if (nd->count > 0) {

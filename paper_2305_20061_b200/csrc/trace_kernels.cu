@@ -469,15 +469,17 @@ __device__ __forceinline__ bool is_leaf(uint32_t e) { return e - (1u << 28) < 0x
 #ifndef PT_SSTACK
 #define PT_SSTACK 16
 #endif
-constexpr int kShortStack = PT_SSTACK;
+constexpr int kShortStack = PT_SSTACK;   // 0: the whole stack in local memory
 constexpr int kTraceBlock = 128;
 
 __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
     Hit best{CUDART_INF, CUDART_INF_F, CUDART_INF_F, -1, 0u, true};
     if (tp.empty) return best;
+#if PT_SSTACK > 0
     __shared__ uint32_t s_ent[kShortStack][kTraceBlock];
     __shared__ float s_tn[kShortStack][kTraceBlock];
     const int tid = threadIdx.x;
+#endif
     float4 cold[2];                   // local memory: written and read only through ld/st.local asm
     RayT r;
     ray_prepare(o, d, r, (uint32_t)__cvta_generic_to_local(cold));
@@ -491,10 +493,13 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
     uint2 lstack[kStackSize - kShortStack];   // overflow (local memory)
     int sp = 0;
     auto push = [&](uint32_t e, float t) {
+#if PT_SSTACK > 0
         if (sp < kShortStack) {
             s_ent[sp][tid] = e;
             s_tn[sp][tid] = t;
-        } else {
+        } else
+#endif
+        {
             lstack[sp - kShortStack] = make_uint2(e, __float_as_uint(t));
         }
         ++sp;
@@ -515,10 +520,13 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
             --sp;
             uint32_t e;
             float t;
+#if PT_SSTACK > 0
             if (sp < kShortStack) {
                 e = s_ent[sp][tid];
                 t = s_tn[sp][tid];
-            } else {
+            } else
+#endif
+            {
                 const uint2 v = lstack[sp - kShortStack];
                 e = v.x;
                 t = __uint_as_float(v.y);
@@ -1020,12 +1028,22 @@ static int resident_grid(K kernel, int block) {
     return num_sms() * (per_sm > 0 ? per_sm : 1);
 }
 
-// resident grids of the two path kernels, per device (occupancy and SM count are per-device properties)
+// resident grids of the two path kernels, per device (occupancy and SM count are per-device properties).
+// PT_TRACE_CARVEOUT (percent of the maximum shared memory, or -1 = driver default): the shared/L1 split of
+// the traversal kernels -- the short stack needs kShortStack * 1 KiB per block, the rest stays L1 for
+// BVH nodes.
+#ifndef PT_TRACE_CARVEOUT
+#define PT_TRACE_CARVEOUT -1
+#endif
 static int2 path_grids() {
     static std::atomic<int> g1[64], g2[64];
     const int dev = current_device();
     int a = g1[dev].load(std::memory_order_relaxed), b = g2[dev].load(std::memory_order_relaxed);
     if (a <= 0 || b <= 0) {
+        if (PT_TRACE_CARVEOUT >= 0) {
+            cudaFuncSetAttribute(first_bounce_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, PT_TRACE_CARVEOUT);
+            cudaFuncSetAttribute(path_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, PT_TRACE_CARVEOUT);
+        }
         a = resident_grid(first_bounce_kernel, 128);
         b = resident_grid(path_kernel, 128);
         g1[dev].store(a, std::memory_order_relaxed);

@@ -114,3 +114,31 @@ def test_empty_scene_misses(orc):
     o_sc = orc.OracleScene(scenes.empty_scene())
     prim, t, _, _ = o_sc.closest_hit([[0, 0, 0.0]], [[0, 0, 1.0]])
     assert prim[0] == -1 and np.isinf(t[0])
+
+
+@pytest.mark.parametrize("freq,n_rays", [(17, None), (71, 1500)])
+def test_bvh_equals_brute_at_shared_vertices_and_edges(orc, freq, n_rays):
+    """The oracle's BVH returns exactly the brute-force (t, id) minimum (reading R11) also where hits tie:
+    rays from inside a closed geodesic mesh at its shared vertices (3-6 triangles at one t), edge midpoints
+    and centroids, from three origins. (A cull of boxes entered strictly beyond the best t without a
+    rounding margin returned a larger id on ~1 % of these rays.)"""
+    P, F = scenes.geodesic_sphere(freq)
+    Q = P.astype(np.float32)
+    t = np.zeros(F.shape[0], dtype=scenes.TRI_DTYPE)
+    t["v0"], t["v1"], t["v2"] = Q[F[:, 0]], Q[F[:, 1]], Q[F[:, 2]]
+    sc = scenes.Scene("g", t, np.zeros(0, dtype=scenes.SPHERE_DTYPE), scenes.empty_scene().materials,
+                      scenes.empty_scene().camera)
+    o_sc = orc.OracleScene(sc)
+    e = np.unique(np.sort(np.concatenate([F[:, [0, 1]], F[:, [1, 2]], F[:, [2, 0]]]), 1), axis=0)
+    Q64 = Q.astype(np.float64)
+    tg = np.concatenate([Q, (0.5 * (Q64[e[:, 0]] + Q64[e[:, 1]])).astype(np.float32),
+                         Q64[F].mean(1).astype(np.float32)])
+    if n_rays is not None:
+        tg = tg[np.linspace(0, len(tg) - 1, n_rays).astype(np.int64)]
+    for origin in ([0, 0, 0], [0.1, -0.2, 0.05], [0.37, 0.41, -0.29]):
+        o = np.broadcast_to(np.asarray(origin, np.float32), tg.shape).astype(np.float64)
+        d = (tg - o.astype(np.float32)).astype(np.float32).astype(np.float64)
+        pb, tb, _, _ = o_sc.closest_hit(o, d, brute=False)
+        pf, tf, _, _ = o_sc.closest_hit(o, d, brute=True)
+        assert np.array_equal(pb, pf) and np.array_equal(tb, tf)
+        assert (pf >= 0).all()
