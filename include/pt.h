@@ -139,11 +139,33 @@ PT_API int pt_render_samples(const pt_scene* scene, const pt_nif* nif, const flo
                       int32_t height, int32_t first_sample, int32_t n_samples, int32_t max_depth, uint64_t seed,
                       int32_t wave_samples, float* d_accum, void* stream);
 
+/* As pt_render_samples for the rows [row0, row1) of the frame only (0 <= row0 < row1 <= height): ADD the
+   per-pixel sums over samples [first_sample, first_sample + n_samples) of those rows into d_accum (the
+   FULL-frame buffer, [height][width][3]; other rows are not touched). Every path uses the same Philox
+   counters (pixel index in the full frame, sample, depth) as a full-frame render, so any partition of the
+   (sample, row) range sums to the full-frame result up to fp32 summation order: the multi-GPU split for
+   more GPUs than samples (reading R19). Asynchronous. Errors: INVALID_ARG, CUDA, OOM. */
+PT_API int pt_render_rows(const pt_scene* scene, const pt_nif* nif, const float env_rgb[3], int32_t width,
+                          int32_t height, int32_t row0, int32_t row1, int32_t first_sample, int32_t n_samples,
+                          int32_t max_depth, uint64_t seed, int32_t wave_samples, float* d_accum, void* stream);
+
 /* Test/bench hook: closest hits of the camera rays of one sample (raygen + traversal only).
    d_prim[width*height] int32 (-1 = miss), d_t[width*height] float (t of the hit, +inf on miss).
    Asynchronous. Errors: INVALID_ARG, CUDA, OOM. */
 PT_API int pt_trace_primary(const pt_scene* scene, int32_t width, int32_t height, uint64_t seed, int32_t sample,
                      int32_t* d_prim, float* d_t, void* stream);
+
+/* Test/report hook: the precision AOVs of PAPER.md:169-188 (Sec. 4.2, Table 3 "normals and primary
+   hit-points") for the camera rays of one sample, as the render kernels compute them: d_prim, d_t as
+   pt_trace_primary; d_pos[width*height][3] the hit point P = o + t d (fp32, the shading's formula);
+   d_normal[width*height][3] the geometric normal the shading uses (triangle: normalize((v1 - v0) x
+   (v2 - v0)); sphere: (P - c) / r); d_bary2[width*height][2] the barycentrics (b1, b2) of a triangle
+   hit (P = (1 - b1 - b2) v0 + b1 v1 + b2 v2, fp32 watertight edge functions; 0 for spheres). Misses
+   write prim -1 and zeros. All buffers are caller-owned device memory. Asynchronous.
+   Errors: INVALID_ARG, CUDA. */
+PT_API int pt_trace_primary_aov(const pt_scene* scene, int32_t width, int32_t height, uint64_t seed, int32_t sample,
+                                int32_t* d_prim, float* d_t, float* d_pos, float* d_normal, float* d_bary2,
+                                void* stream);
 
 /* Test/bench hook: closest hits of arbitrary rays. d_o, d_d: [n][3] float device arrays; writes
    d_prim[n] (-1 = miss) and d_t[n]. Asynchronous. */

@@ -81,6 +81,7 @@ def lib():
             L.orc_trace_one.restype = I32
             L.orc_trace_one.argtypes = [P, P, P, I32, I32, I32, U64, I64, I32, P, P]
             L.orc_primary.argtypes = [P, I32, I32, U64, I32, P, I64, P, P, P]
+            L.orc_primary_aov.argtypes = [P, I32, I32, U64, I32, P, I64, P, P, P, P, P]
             _lib = L
     return _lib
 
@@ -127,6 +128,20 @@ class OracleScene:
         edge = np.empty(n, np.float64)
         lib().orc_primary(self.h, width, height, seed, sample, _p(pix), n, _p(prim), _p(t), _p(edge))
         return prim, t, edge
+
+    def primary_aov(self, width, height, seed, sample, pix):
+        """Table-3 AOVs of the primary hits (orc_primary_aov): prim, t, hit point [n][3], geometric
+        normal [n][3], (b1, b2) [n][2]."""
+        pix = np.ascontiguousarray(pix, dtype=np.int64)
+        n = pix.shape[0]
+        prim = np.empty(n, np.int64)
+        t = np.empty(n, np.float64)
+        pos = np.empty((n, 3), np.float64)
+        nrm = np.empty((n, 3), np.float64)
+        bary2 = np.empty((n, 2), np.float64)
+        lib().orc_primary_aov(self.h, width, height, seed, sample, _p(pix), n, _p(prim), _p(t), _p(pos), _p(nrm),
+                              _p(bary2))
+        return prim, t, pos, nrm, bary2
 
     def render(self, width, height, max_depth, seed, pix=None, s0=0, s1=1, nif_blob=None, env_rgb=(1, 1, 1),
                nthreads=None):

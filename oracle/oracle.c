@@ -1105,3 +1105,51 @@ EXPORT void orc_primary(const orc_scene* sc, int32_t W, int32_t H, uint64_t seed
         edge[i] = h.prim >= 0 ? h.edge : 0.0;
     }
 }
+
+/* Table-3 AOVs of the primary hits (Sec. 4.2: normals and primary hit points): for
+   listed pixels of sample `sample`, the fp64 closest hit of the fp32 camera ray (widened), the hit point
+   P = o + t d, the geometric normal n_g (triangle: normalize((v1 - v0) x (v2 - v0)); sphere: (P - c) / r,
+   SURVEY 8c step 6) and the barycentrics (b1, b2) = (V, W) / det of the watertight test (0 for spheres
+   and misses). pos/nrm: [n][3], bary2: [n][2]; misses give prim -1 and zeros. */
+EXPORT void orc_primary_aov(const orc_scene* sc, int32_t W, int32_t H, uint64_t seed, int32_t sample,
+                            const int64_t* pix, int64_t n, int64_t* prim, double* t, double* pos, double* nrm,
+                            double* bary2) {
+    cam32 k;
+    cam_setup(&sc->cam, W, H, &k);
+    for (int64_t i = 0; i < n; ++i) {
+        double xi[4];
+        int64_t p = pix[i];
+        draw4(seed, (uint32_t)p, (uint32_t)sample, 0u, xi);
+        float d32[3];
+        cam_dir32(&k, W, H, (int32_t)(p % W), (int32_t)(p / W), (float)xi[0], (float)xi[1], d32);
+        double o[3] = {k.eye[0], k.eye[1], k.eye[2]}, d[3] = {d32[0], d32[1], d32[2]};
+        ray_pre r;
+        ray_prepare(o, d, &r);
+        hit_rec h;
+        closest_bvh(sc, &r, &h);
+        prim[i] = h.prim;
+        t[i] = h.prim >= 0 ? h.t : INFINITY;
+        for (int a = 0; a < 3; ++a) { pos[3 * i + a] = 0.0; nrm[3 * i + a] = 0.0; }
+        bary2[2 * i] = bary2[2 * i + 1] = 0.0;
+        if (h.prim < 0) continue;
+        double P[3];
+        for (int a = 0; a < 3; ++a) P[a] = o[a] + h.t * d[a];
+        double ng[3];
+        if (h.prim < sc->n_tris) {
+            const double* v = sc->tv + 9 * h.prim;
+            double e1[3], e2[3];
+            for (int a = 0; a < 3; ++a) { e1[a] = v[3 + a] - v[a]; e2[a] = v[6 + a] - v[a]; }
+            ng[0] = e1[1] * e2[2] - e1[2] * e2[1];
+            ng[1] = e1[2] * e2[0] - e1[0] * e2[2];
+            ng[2] = e1[0] * e2[1] - e1[1] * e2[0];
+            double l = sqrt(ng[0] * ng[0] + ng[1] * ng[1] + ng[2] * ng[2]);
+            for (int a = 0; a < 3; ++a) ng[a] /= l;
+            bary2[2 * i] = h.bary[1];
+            bary2[2 * i + 1] = h.bary[2];
+        } else {
+            const double* s = sc->sp + 4 * (h.prim - sc->n_tris);
+            for (int a = 0; a < 3; ++a) ng[a] = (P[a] - s[a]) / s[3];
+        }
+        for (int a = 0; a < 3; ++a) { pos[3 * i + a] = P[a]; nrm[3 * i + a] = ng[a]; }
+    }
+}

@@ -241,16 +241,18 @@ void collect_timers(pt_scene* sc) {
 
 
 
-int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, int W, int H, int first_sample,
-                        int n_samples, int max_depth, uint64_t seed, int wave_samples, float* d_accum,
+int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, int W, int H, int row0, int row1,
+                        int first_sample, int n_samples, int max_depth, uint64_t seed, int wave_samples, float* d_accum,
                         cudaStream_t st) {
     if (W < 1 || H < 1 || n_samples < 1 || max_depth < 1 || first_sample < 0)
         return fail(PT_ERR_INVALID_ARG, "width, height, n_samples, max_depth must be >= 1");
+    if (row0 < 0 || row1 > H || row0 >= row1) return fail(PT_ERR_INVALID_ARG, "rows must satisfy 0 <= row0 < row1 <= height");
     if (max_depth > 60) return fail(PT_ERR_INVALID_ARG, "max_depth too large (<= 60)");
     if (!nif && !env_rgb) return fail(PT_ERR_INVALID_ARG, "env_rgb must be given when nif is NULL");
     if (!d_accum) return fail(PT_ERR_INVALID_ARG, "d_accum is NULL");
-    const int64_t np = (int64_t)W * H;
-    if (np > (1ll << 31) / 2) return fail(PT_ERR_INVALID_ARG, "frame too large");
+    if ((int64_t)W * H > (1ll << 31) / 2) return fail(PT_ERR_INVALID_ARG, "frame too large");
+    const int64_t np = (int64_t)W * (row1 - row0);   // pixels rendered
+    const int64_t p0 = (int64_t)W * row0;
     int64_t k = wave_samples;
     if (k <= 0) k = std::max<int64_t>(1, std::min<int64_t>(n_samples, (int64_t)(8 << 20) / np));
     k = std::min<int64_t>(k, n_samples);
@@ -294,7 +296,7 @@ int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, i
         CU(cudaMemsetAsync(ws.counters, 0, sizeof(uint32_t) * pt::kCounters, st));
         cudaEvent_t e0;
         tm.begin(T_TRAVERSE, &e0);
-        pt::launch_paths(tp, cam, W, H, (int)w0, (int)slots, max_depth, seed, use_nif, env, ws, st);
+        pt::launch_paths(tp, cam, W, H, (int)p0, (int)np, (int)w0, (int)slots, max_depth, seed, use_nif, env, ws, st);
         tm.end(T_TRAVERSE, e0);
         stats.launches += max_depth > 1 ? 2 : 1;
         stats.traverse_launches += max_depth > 1 ? 2 : 1;
@@ -307,7 +309,7 @@ int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, i
             stats.nif_launches += 1;
         }
         tm.begin(T_ACCUM, &e0);
-        pt::launch_accumulate(ws.wave_buf, (int)np, (int)kk, d_accum, ws.counters, d_stats, (uint32_t)slots, st);
+        pt::launch_accumulate(ws.wave_buf, (int)np, (int)kk, d_accum + 3 * p0, ws.counters, d_stats, (uint32_t)slots, st);
         tm.end(T_ACCUM, e0);
         stats.launches += 1;   // accumulate (with the wave statistics)
         stats.waves += 1;
@@ -526,7 +528,17 @@ int pt_render_samples(const pt_scene* scene, const pt_nif* nif, const float env_
     if (!scene) return fail(PT_ERR_INVALID_ARG, "scene is NULL");
     pt_scene* sc = const_cast<pt_scene*>(scene);
     std::lock_guard<std::mutex> lk(sc->mu);
-    return render_samples_impl(sc, nif, env_rgb, width, height, first_sample, n_samples, max_depth, seed,
+    return render_samples_impl(sc, nif, env_rgb, width, height, 0, height, first_sample, n_samples, max_depth, seed,
+                               wave_samples, d_accum, (cudaStream_t)stream);
+}
+
+int pt_render_rows(const pt_scene* scene, const pt_nif* nif, const float env_rgb[3], int32_t width, int32_t height,
+                   int32_t row0, int32_t row1, int32_t first_sample, int32_t n_samples, int32_t max_depth, uint64_t seed,
+                   int32_t wave_samples, float* d_accum, void* stream) {
+    if (!scene) return fail(PT_ERR_INVALID_ARG, "scene is NULL");
+    pt_scene* sc = const_cast<pt_scene*>(scene);
+    std::lock_guard<std::mutex> lk(sc->mu);
+    return render_samples_impl(sc, nif, env_rgb, width, height, row0, row1, first_sample, n_samples, max_depth, seed,
                                wave_samples, d_accum, (cudaStream_t)stream);
 }
 
@@ -548,7 +560,7 @@ int pt_render(const pt_scene* scene, const pt_nif* nif, const float env_rgb[3], 
     }
     cudaStream_t st = sc->ws.own_stream;
     CU(cudaMemsetAsync(sc->ws.fb, 0, sizeof(float) * n, st));
-    rc = render_samples_impl(sc, nif, env_rgb, width, height, 0, spp, max_depth, seed, 0, sc->ws.fb, st);
+    rc = render_samples_impl(sc, nif, env_rgb, width, height, 0, height, 0, spp, max_depth, seed, 0, sc->ws.fb, st);
     if (rc) return rc;
     pt::launch_scale(sc->ws.fb, n, 1.0f / (float)spp, st);
     CU(cudaMemcpyAsync(out_rgb, sc->ws.fb, sizeof(float) * n, cudaMemcpyDeviceToHost, st));
@@ -562,6 +574,18 @@ int pt_trace_primary(const pt_scene* scene, int32_t width, int32_t height, uint6
         return fail(PT_ERR_INVALID_ARG, "bad argument");
     const pt::Cam32 cam = pt::make_cam32(scene->cam, width, height);
     pt::launch_primary(trace_params(scene), cam, width, height, sample, seed, d_prim, d_t, (cudaStream_t)stream);
+    CU(cudaGetLastError());
+    return PT_OK;
+}
+
+int pt_trace_primary_aov(const pt_scene* scene, int32_t width, int32_t height, uint64_t seed, int32_t sample,
+                         int32_t* d_prim, float* d_t, float* d_pos, float* d_normal, float* d_bary2, void* stream) {
+    if (!scene || !d_prim || !d_t || !d_pos || !d_normal || !d_bary2 || width < 1 || height < 1 || sample < 0)
+        return fail(PT_ERR_INVALID_ARG, "bad argument");
+    if ((int64_t)width * height > (1ll << 30)) return fail(PT_ERR_INVALID_ARG, "frame too large");
+    const pt::Cam32 cam = pt::make_cam32(scene->cam, width, height);
+    pt::launch_primary_aov(trace_params(scene), cam, width, height, sample, seed, d_prim, d_t, d_pos, d_normal, d_bary2,
+                           (cudaStream_t)stream);
     CU(cudaGetLastError());
     return PT_OK;
 }

@@ -151,12 +151,16 @@ struct TraceParams {
 };
 
 // kernel launchers (trace_kernels.cu)
-void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int first_sample, int n_slots, int max_depth,
-                  uint64_t seed, int use_nif, float3 env, Workspace& ws, cudaStream_t st);
+// one wave: slots i in [0, n_slots) = (pixel p0 + i % np, sample first_sample + i / np); np = the pixels of
+// the rendered row range (p0 = row0 W)
+void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int p0, int np, int first_sample, int n_slots,
+                  int max_depth, uint64_t seed, int use_nif, float3 env, Workspace& ws, cudaStream_t st);
 void launch_accumulate(const float* wave_buf, int n_pix, int k, float* fb, const uint32_t* counters,
                        unsigned long long* stats, uint32_t paths, cudaStream_t st);
 void launch_primary(const TraceParams& tp, const Cam32& cam, int W, int H, int sample, uint64_t seed,
                     int32_t* prim, float* t, cudaStream_t st);
+void launch_primary_aov(const TraceParams& tp, const Cam32& cam, int W, int H, int sample, uint64_t seed, int32_t* prim,
+                        float* t, float* pos, float* nrm, float* bary2, cudaStream_t st);
 void launch_trace_rays(const TraceParams& tp, const float* o, const float* d, int64_t n, int32_t* prim, float* t,
                        cudaStream_t st);
 void launch_scale(float* fb, int64_t n, float s, cudaStream_t st);

@@ -63,7 +63,6 @@ constexpr int kThreads = 32 * (kFirstEpiWarp + kNumEpiWarps);   // 640
 // the output warps read it before they arrive on a_ready(s) for the next tile's layer 4, which the
 // issuer waits for before it issues that tile's layer 5.)
 enum { kBarW = 0, kBarAReady = 1, kBarDFull = 3, kBarA0Full = 5, kBarA0Empty = 7, kBarOFull = 9 };
-constexpr int kOutWarps = 4;                    // epilogue warps with cb == 0 (one per lane quarter)
 
 constexpr uint32_t kTmemCols = 512;
 __host__ __device__ constexpr uint32_t d_col(int s) { return 256u * s; }
@@ -314,11 +313,15 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        // b5 (fp16 in the image's bias step of B5: row n, k = 128), added by the output warps
-        float b5[3];
+        // b5 (fp16 in the image's bias step of B5: row n, k = 128), added by the output warps once the
+        // weight image has landed (the bulk copies complete on kBarW)
+        float b5[3] = {0.0f, 0.0f, 0.0f};
+        if (cb == 0) {
+            mbar_wait(bar(kBarW), 0);
 #pragma unroll
-        for (int n = 0; n < 3; ++n)
-            b5[n] = __half2float(*reinterpret_cast<const __half*>(smem + kOffB5 + (16 * 2) * 128 + n * 16));
+            for (int n = 0; n < 3; ++n)
+                b5[n] = __half2float(*reinterpret_cast<const __half*>(smem + kOffB5 + (16 * 2) * 128 + n * 16));
+        }
         uint32_t d_phase[2] = {0, 0}, o_phase[2] = {0, 0};
         // the output rows of each slot's previous tile (cb == 0 warps): slot id, throughput, validity
         float4 beta[2] = {make_float4(0, 0, 0, 0), make_float4(0, 0, 0, 0)};

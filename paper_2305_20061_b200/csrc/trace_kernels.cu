@@ -467,7 +467,7 @@ __device__ __forceinline__ bool is_leaf(uint32_t e) { return e - (1u << 28) < 0x
 // entries spill to a local-memory array (rare: 3 pushes per level at most, 9-14 levels on configs 3-4).
 // All kernels that trace run 128-thread blocks.
 #ifndef PT_SSTACK
-#define PT_SSTACK 16
+#define PT_SSTACK 0   // measured slower at every depth 8-24 and carveout (profiles/round2/variants_s3.log)
 #endif
 constexpr int kShortStack = PT_SSTACK;   // 0: the whole stack in local memory
 constexpr int kTraceBlock = 128;
@@ -636,11 +636,61 @@ __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
 // Kernels
 // ---------------------------------------------------------------------------------------------
 
+// Geometric normal and material of the hit primitive, from its record in the BVH pool (just read by the
+// traversal): triangle n_g = normalize((v1 - v0) x (v2 - v0)), sphere n_g = (P - c) / r.
+// The shading path and the Table-3 AOV hook (pt_trace_primary_aov) share this code.
+__device__ __forceinline__ void hit_normal(const uint4* __restrict__ pool, uint32_t unit, float3 P, float3& ng,
+                                           uint32_t& mi) {
+    const uint4 u0 = __ldg(pool + unit), u1 = __ldg(pool + unit + 1);
+    if (!(u0.w & kSphereFlag)) {
+        const uint4 u2 = __ldg(pool + unit + 2);
+        const float3 v0 = make_float3(__uint_as_float(u0.x), __uint_as_float(u0.y), __uint_as_float(u0.z));
+        const float3 e1 = make_float3(__uint_as_float(u1.x) - v0.x, __uint_as_float(u1.y) - v0.y,
+                                      __uint_as_float(u1.z) - v0.z);
+        const float3 e2 = make_float3(__uint_as_float(u2.x) - v0.x, __uint_as_float(u2.y) - v0.y,
+                                      __uint_as_float(u2.z) - v0.z);
+        ng = make_float3(e1.y * e2.z - e1.z * e2.y, e1.z * e2.x - e1.x * e2.z, e1.x * e2.y - e1.y * e2.x);
+        const float il = rsqrtf(ng.x * ng.x + ng.y * ng.y + ng.z * ng.z);
+        ng = make_float3(ng.x * il, ng.y * il, ng.z * il);
+        mi = u1.w;
+    } else {
+        const float ir = 1.0f / __uint_as_float(u1.x);
+        ng = make_float3((P.x - __uint_as_float(u0.x)) * ir, (P.y - __uint_as_float(u0.y)) * ir,
+                         (P.z - __uint_as_float(u0.z)) * ir);
+        mi = u1.y;
+    }
+}
+
+// fp32 barycentrics (b1, b2) = (V, W) / det of the watertight test's sheared edge functions (the AOV hook)
+__device__ __forceinline__ float2 tri_bary32(float3 o, float3 d, float3 v0, float3 v1, float3 v2) {
+    int kz = 0;
+    if (fabsf(d.y) > fabsf(d.x)) kz = 1;
+    if (fabsf(d.z) > fabsf(self3(d, kz))) kz = 2;
+    int kx = kz + 1; if (kx == 3) kx = 0;
+    int ky = kx + 1; if (ky == 3) ky = 0;
+    if (self3(d, kz) < 0.0f) { const int t = kx; kx = ky; ky = t; }
+    const float Sx = self3(d, kx) / self3(d, kz), Sy = self3(d, ky) / self3(d, kz);
+    auto sh = [&](float3 v, float& x, float& y) {
+        const float3 q = make_float3(v.x - o.x, v.y - o.y, v.z - o.z);
+        x = self3(q, kx) - Sx * self3(q, kz);
+        y = self3(q, ky) - Sy * self3(q, kz);
+    };
+    float Ax, Ay, Bx, By, Cx, Cy;
+    sh(v0, Ax, Ay);
+    sh(v1, Bx, By);
+    sh(v2, Cx, Cy);
+    const float U = Cx * By - Cy * Bx, V = Ax * Cy - Ay * Cx, W = Bx * Ay - By * Ax;
+    const float det = U + V + W;
+    return det != 0.0f ? make_float2(V / det, W / det) : make_float2(0.0f, 0.0f);
+}
+
 struct ShadeArgs {
     TraceParams tp;
     Cam32 cam;
     int W, H, first_sample, depth, max_depth;
-    float inv_np, inv_w;        // 1 / (W H), 1 / W for udiv_exact
+    float inv_np, inv_w;        // 1 / np, 1 / W for udiv_exact
+    int np;                     // pixels of the rendered row range (W x rows)
+    uint32_t p0;                // its first pixel (row0 W): slot i = (pixel p0 + i % np, sample first + i / np)
     uint2 key;
     const uint32_t* counters;   // the wave's counters (pt_internal.h kCounters layout)
     uint32_t n_slots;           // paths of the wave
@@ -668,7 +718,7 @@ struct SegOut {
 
 __device__ __forceinline__ void shade_segment(const ShadeArgs& a, int depth, uint32_t slot, float3 o, float3 d,
                                               float3 bt, SegOut& r) {
-    const int np = a.W * a.H;
+    const int np = a.np;
     r.alive = false;
     r.escaped = false;
     r.done = true;
@@ -690,27 +740,9 @@ __device__ __forceinline__ void shade_segment(const ShadeArgs& a, int depth, uin
     }
     const float t = (float)hh.t;
     const float3 P = make_float3(fmaf(t, d.x, o.x), fmaf(t, d.y, o.y), fmaf(t, d.z, o.z));
-    // the hit primitive's record in the BVH pool (just read by the traversal): vertices / sphere + material
     float3 ng;
     uint32_t mi;
-    const uint4 u0 = __ldg(a.tp.pool + hh.unit), u1 = __ldg(a.tp.pool + hh.unit + 1);
-    if (!(u0.w & kSphereFlag)) {
-        const uint4 u2 = __ldg(a.tp.pool + hh.unit + 2);
-        const float3 v0 = make_float3(__uint_as_float(u0.x), __uint_as_float(u0.y), __uint_as_float(u0.z));
-        const float3 e1 = make_float3(__uint_as_float(u1.x) - v0.x, __uint_as_float(u1.y) - v0.y,
-                                      __uint_as_float(u1.z) - v0.z);
-        const float3 e2 = make_float3(__uint_as_float(u2.x) - v0.x, __uint_as_float(u2.y) - v0.y,
-                                      __uint_as_float(u2.z) - v0.z);
-        ng = make_float3(e1.y * e2.z - e1.z * e2.y, e1.z * e2.x - e1.x * e2.z, e1.x * e2.y - e1.y * e2.x);
-        const float il = rsqrtf(ng.x * ng.x + ng.y * ng.y + ng.z * ng.z);
-        ng = make_float3(ng.x * il, ng.y * il, ng.z * il);
-        mi = u1.w;
-    } else {
-        const float ir = 1.0f / __uint_as_float(u1.x);
-        ng = make_float3((P.x - __uint_as_float(u0.x)) * ir, (P.y - __uint_as_float(u0.y)) * ir,
-                         (P.z - __uint_as_float(u0.z)) * ir);
-        mi = u1.y;
-    }
+    hit_normal(a.tp.pool, hh.unit, P, ng, mi);
     const DevMaterial m = a.tp.mats[mi];
     const float cosd = d.x * ng.x + d.y * ng.y + d.z * ng.z;
     if (m.kind == PT_EMISSIVE) {
@@ -720,7 +752,7 @@ __device__ __forceinline__ void shade_segment(const ShadeArgs& a, int depth, uin
     if (depth >= a.max_depth) return;                 // capped: no further segment, no env (reading R7)
     uint32_t pu;
     const int s = a.first_sample + (int)udiv_exact(slot, (uint32_t)np, a.inv_np, pu);
-    const int p = (int)pu;
+    const int p = (int)(a.p0 + pu);
     const uint4 rr = philox10(make_uint4((uint32_t)p, (uint32_t)s, (uint32_t)depth, 0u), a.key);
     const float xi0 = u01f(rr.x), xi1 = u01f(rr.y), xi2 = u01f(rr.z), xi3 = u01f(rr.w);
     const bool entering = cosd < 0.0f;
@@ -790,13 +822,12 @@ __device__ __forceinline__ void shade_segment(const ShadeArgs& a, int depth, uin
     r.beta = bt;
 }
 
-// The camera ray of wave slot i = (pixel i % np, sample first + i / np) (S1, reading R22)
+// The camera ray of wave slot i = (pixel p0 + i % np, sample first + i / np) (S1, reading R22)
 __device__ __forceinline__ float3 camera_ray(const ShadeArgs& a, uint32_t i) {
-    const int np = a.W * a.H;
     uint32_t pu, px;
-    const int sm = a.first_sample + (int)udiv_exact(i, (uint32_t)np, a.inv_np, pu);
-    const int p = (int)pu;
-    const uint32_t py = udiv_exact(pu, (uint32_t)a.W, a.inv_w, px);
+    const int sm = a.first_sample + (int)udiv_exact(i, (uint32_t)a.np, a.inv_np, pu);
+    const int p = (int)(a.p0 + pu);
+    const uint32_t py = udiv_exact((uint32_t)p, (uint32_t)a.W, a.inv_w, px);
     const uint4 r = philox10(make_uint4((uint32_t)p, (uint32_t)sm, 0u, 0u), a.key);
     return cam_dir(a.cam, a.W, a.H, (int)px, (int)py, u01f(r.x), u01f(r.y));
 }
@@ -979,6 +1010,40 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) primary_kernel(TraceParams tp
     }
 }
 
+// Table-3 AOVs of the primary hits: the kernel's own hit point (P = o + t d as the
+// shading computes it), geometric normal (hit_normal, the shading code) and fp32 barycentrics
+__global__ void __launch_bounds__(128, PT_TS_MINB) primary_aov_kernel(TraceParams tp, Cam32 cam, int W, int H, int sample,
+                                                                      uint2 key, int32_t* prim, float* tout, float* pos,
+                                                                      float* nrm, float* bary2) {
+    const int np = W * H;
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < np; p += gridDim.x * blockDim.x) {
+        const uint4 r = philox10(make_uint4((uint32_t)p, (uint32_t)sample, 0u, 0u), key);
+        const float3 d = cam_dir(cam, W, H, p % W, p / W, u01f(r.x), u01f(r.y));
+        const float3 o = make_float3(cam.eye[0], cam.eye[1], cam.eye[2]);
+        const Hit h = closest_hit(tp, o, d);
+        prim[p] = h.prim;
+        tout[p] = (float)h.t;
+        float3 P = make_float3(0, 0, 0), ng = make_float3(0, 0, 0);
+        float2 b = make_float2(0, 0);
+        if (h.prim >= 0) {
+            const float t = (float)h.t;
+            P = make_float3(fmaf(t, d.x, o.x), fmaf(t, d.y, o.y), fmaf(t, d.z, o.z));
+            uint32_t mi;
+            hit_normal(tp.pool, h.unit, P, ng, mi);
+            const uint4 u0 = __ldg(tp.pool + h.unit);
+            if (!(u0.w & kSphereFlag)) {
+                const uint4 u1 = __ldg(tp.pool + h.unit + 1), u2 = __ldg(tp.pool + h.unit + 2);
+                b = tri_bary32(o, d, make_float3(__uint_as_float(u0.x), __uint_as_float(u0.y), __uint_as_float(u0.z)),
+                               make_float3(__uint_as_float(u1.x), __uint_as_float(u1.y), __uint_as_float(u1.z)),
+                               make_float3(__uint_as_float(u2.x), __uint_as_float(u2.y), __uint_as_float(u2.z)));
+            }
+        }
+        pos[3 * p + 0] = P.x; pos[3 * p + 1] = P.y; pos[3 * p + 2] = P.z;
+        nrm[3 * p + 0] = ng.x; nrm[3 * p + 1] = ng.y; nrm[3 * p + 2] = ng.z;
+        bary2[2 * p + 0] = b.x; bary2[2 * p + 1] = b.y;
+    }
+}
+
 __global__ void __launch_bounds__(128, PT_TS_MINB) trace_rays_kernel(TraceParams tp, const float* o, const float* d, int64_t n, int32_t* prim, float* tout) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const Hit h = closest_hit(tp, make_float3(o[3 * i], o[3 * i + 1], o[3 * i + 2]),
@@ -1052,14 +1117,16 @@ static int2 path_grids() {
     return make_int2(a, b);
 }
 
-void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int first_sample, int n_slots, int max_depth,
-                  uint64_t seed, int use_nif, float3 env, Workspace& ws, cudaStream_t st) {
+void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int p0, int np, int first_sample, int n_slots,
+                  int max_depth, uint64_t seed, int use_nif, float3 env, Workspace& ws, cudaStream_t st) {
     ShadeArgs a;
     a.n_slots = (uint32_t)n_slots;
     a.tp = tp;
     a.cam = cam;
     a.W = W; a.H = H; a.first_sample = first_sample; a.depth = 1; a.max_depth = max_depth;
-    a.inv_np = 1.0f / (float)((int64_t)W * H);
+    a.np = np;
+    a.p0 = (uint32_t)p0;
+    a.inv_np = 1.0f / (float)np;
     a.inv_w = 1.0f / (float)W;
     a.key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
     a.counters = ws.counters;
@@ -1086,6 +1153,13 @@ void launch_primary(const TraceParams& tp, const Cam32& cam, int W, int H, int s
                     float* t, cudaStream_t st) {
     const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
     primary_kernel<<<grid_for((int64_t)W * H, 128, PT_TS_MINB), 128, 0, st>>>(tp, cam, W, H, sample, key, prim, t);
+}
+
+void launch_primary_aov(const TraceParams& tp, const Cam32& cam, int W, int H, int sample, uint64_t seed, int32_t* prim,
+                        float* t, float* pos, float* nrm, float* bary2, cudaStream_t st) {
+    const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+    primary_aov_kernel<<<grid_for((int64_t)W * H, 128, PT_TS_MINB), 128, 0, st>>>(tp, cam, W, H, sample, key, prim, t,
+                                                                                   pos, nrm, bary2);
 }
 
 void launch_trace_rays(const TraceParams& tp, const float* o, const float* d, int64_t n, int32_t* prim, float* t,

@@ -31,7 +31,7 @@ class PtStats(C.Structure):
 
 EXPORTED = ["pt_scene_create", "pt_scene_destroy", "pt_nif_load", "pt_nif_load_ex", "pt_nif_load_family",
             "pt_nif_load_family_ex", "pt_nif_destroy", "pt_render",
-            "pt_render_samples", "pt_trace_primary", "pt_trace_rays", "pt_nif_infer", "pt_get_stats",
+            "pt_render_samples", "pt_render_rows", "pt_trace_primary", "pt_trace_primary_aov", "pt_trace_rays", "pt_nif_infer", "pt_get_stats",
             "pt_set_profiling", "pt_last_error", "pt_version"]
 
 
@@ -53,7 +53,9 @@ def lib():
             L.pt_nif_destroy.argtypes = [P]
             L.pt_render.argtypes = [P, P, P, I32, I32, I32, I32, U64, P]
             L.pt_render_samples.argtypes = [P, P, P, I32, I32, I32, I32, I32, U64, I32, P, P]
+            L.pt_render_rows.argtypes = [P, P, P, I32, I32, I32, I32, I32, I32, I32, U64, I32, P, P]
             L.pt_trace_primary.argtypes = [P, I32, I32, U64, I32, P, P, P]
+            L.pt_trace_primary_aov.argtypes = [P, I32, I32, U64, I32, P, P, P, P, P, P]
             L.pt_trace_rays.argtypes = [P, P, P, I64, P, P, P]
             L.pt_nif_infer.argtypes = [P, P, I64, P, P]
             L.pt_debug_nif_layers.argtypes = [P, P, I64, P, P, P]
@@ -175,12 +177,34 @@ def render_samples(scene: Scene, nif: Nif | None, width, height, first_sample, n
                                    max_depth, seed, wave_samples, _dp(accum), _stream(stream)))
 
 
+def render_rows(scene: Scene, nif: Nif | None, width, height, row0, row1, first_sample, n_samples, max_depth, seed,
+                accum, env_rgb=None, wave_samples=0, stream=None):
+    """pt_render_rows: accum (full-frame CUDA float32 [H*W*3]) rows [row0, row1) += per-pixel sample sums."""
+    env = _env(env_rgb if env_rgb is not None else ((1.0, 1.0, 1.0) if nif is None else None))
+    _check(lib().pt_render_rows(scene.h, nif.h if nif else None, _p(env), width, height, row0, row1, first_sample,
+                                n_samples, max_depth, seed, wave_samples, _dp(accum), _stream(stream)))
+
+
 def trace_primary(scene: Scene, width, height, seed, sample, stream=None):
     import torch
     prim = torch.empty(width * height, dtype=torch.int32, device="cuda")
     t = torch.empty(width * height, dtype=torch.float32, device="cuda")
     _check(lib().pt_trace_primary(scene.h, width, height, seed, sample, _dp(prim), _dp(t), _stream(stream)))
     return prim, t
+
+
+def trace_primary_aov(scene: Scene, width, height, seed, sample, stream=None):
+    """pt_trace_primary_aov: (prim, t, hit point [n][3], normal [n][3], (b1, b2) [n][2]) CUDA tensors."""
+    import torch
+    n = width * height
+    prim = torch.empty(n, dtype=torch.int32, device="cuda")
+    t = torch.empty(n, dtype=torch.float32, device="cuda")
+    pos = torch.empty((n, 3), dtype=torch.float32, device="cuda")
+    nrm = torch.empty((n, 3), dtype=torch.float32, device="cuda")
+    bary2 = torch.empty((n, 2), dtype=torch.float32, device="cuda")
+    _check(lib().pt_trace_primary_aov(scene.h, width, height, seed, sample, _dp(prim), _dp(t), _dp(pos), _dp(nrm),
+                                      _dp(bary2), _stream(stream)))
+    return prim, t, pos, nrm, bary2
 
 
 def trace_rays(scene: Scene, o, d, stream=None):

@@ -142,3 +142,43 @@ def test_bvh_equals_brute_at_shared_vertices_and_edges(orc, freq, n_rays):
         pf, tf, _, _ = o_sc.closest_hit(o, d, brute=True)
         assert np.array_equal(pb, pf) and np.array_equal(tb, tf)
         assert (pf >= 0).all()
+
+
+@pytest.mark.parametrize("cfg", [0, 2])
+def test_primary_aov_invariants(orc, cfg):
+    """oracle.primary_aov (the Table-3 AOVs) against identities it does not compute
+    with: a triangle hit point equals the barycentric combination of the vertices, (1 - b1 - b2) v0 +
+    b1 v1 + b2 v2, its normal is unit and orthogonal to both edges; a sphere hit point lies on the sphere
+    and its normal is the unit radial direction; prim and t equal oracle.primary."""
+    c = scenes.CONFIGS[cfg]
+    sc = scenes.scene_for_config(cfg)
+    o_sc = orc.OracleScene(sc)
+    W, H = 64, 48
+    pix = np.arange(W * H, dtype=np.int64)
+    prim, t, pos, nrm, b2 = o_sc.primary_aov(W, H, 3, 1, pix)
+    p2, t2, _ = o_sc.primary(W, H, 3, 1, pix)
+    assert np.array_equal(prim, p2) and np.array_equal(t, t2)
+    nt = sc.n_tris
+    tri = (prim >= 0) & (prim < nt)
+    sph = prim >= nt
+    assert tri.sum() > 100 and (cfg != 2 or sph.sum() > 100)
+    v0 = sc.tris["v0"][prim[tri]].astype(np.float64)
+    v1 = sc.tris["v1"][prim[tri]].astype(np.float64)
+    v2 = sc.tris["v2"][prim[tri]].astype(np.float64)
+    b1, bb2 = b2[tri, 0], b2[tri, 1]
+    comb = (1 - b1 - bb2)[:, None] * v0 + b1[:, None] * v1 + bb2[:, None] * v2
+    scale = 1 + np.abs(pos[tri]).max(1)
+    assert (np.abs(comb - pos[tri]).max(1) <= 1e-12 * scale).all()
+    assert np.allclose(np.linalg.norm(nrm[tri], axis=1), 1, atol=1e-14)
+    assert np.abs((nrm[tri] * (v1 - v0)).sum(1)).max() <= 1e-13
+    assert np.abs((nrm[tri] * (v2 - v0)).sum(1)).max() <= 1e-13
+    if sph.any():
+        s = sc.spheres[prim[sph] - nt]
+        cen = s["center"].astype(np.float64)
+        r = s["radius"].astype(np.float64)
+        # (the quadratic's cancellation at |oc| ~ 7 >> r leaves ~1e-12 relative in t)
+        assert np.allclose(np.linalg.norm(pos[sph] - cen, axis=1), r, rtol=1e-9, atol=0)
+        assert np.allclose(nrm[sph], (pos[sph] - cen) / r[:, None], rtol=0, atol=1e-14)
+        assert np.allclose(np.linalg.norm(nrm[sph], axis=1), 1, atol=1e-9)
+    miss = prim < 0
+    assert (pos[miss] == 0).all() and (nrm[miss] == 0).all()
