@@ -238,15 +238,19 @@ class Renderer:
 
     def step(self):
         from paper_2305_20061_b200 import pt
-        from paper_2305_20061_b200.dist import render_partitioned
+        from paper_2305_20061_b200.dist import render_partitioned_rows
         c = self.cfg
 
-        def block(f, n, acc):
-            pt.render_samples(self.S, self.N, c.width, c.height, f, n, c.max_depth, c.seed, acc, env_rgb=self.env,
-                              wave_samples=c.wave_samples, stream=self.stream)
+        def rows(f, n, r0, r1, acc):
+            if r0 == 0 and r1 == c.height:
+                pt.render_samples(self.S, self.N, c.width, c.height, f, n, c.max_depth, c.seed, acc, env_rgb=self.env,
+                                  wave_samples=c.wave_samples, stream=self.stream)
+            else:    # (sample, row block) split when the GPU count does not divide the samples (reading R19)
+                pt.render_rows(self.S, self.N, c.width, c.height, r0, r1, f, n, c.max_depth, c.seed, acc,
+                               env_rgb=self.env, wave_samples=c.wave_samples, stream=self.stream)
 
         self.accum.zero_()
-        render_partitioned(block, self.n_total, self.accum, self.rank, self.world)
+        render_partitioned_rows(rows, self.n_total, c.height, self.accum, self.rank, self.world)
 
 
 def timed_steps(R, steps, flush, stream, world):
@@ -344,7 +348,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2305_20061_b200 import _build, pt
-    from paper_2305_20061_b200.dist import render_partitioned
+    from paper_2305_20061_b200.dist import render_partitioned_rows
 
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -401,11 +405,11 @@ def main():
         else:
             acc2 = torch.zeros(W * H * 3, dtype=torch.float32, device="cuda")
 
-            def block2(f, c, acc, S2=S2, N2=N2):
-                pt.render_samples(S2, N2, W, H, f, c, depth, cfg.seed, acc, env_rgb=env,
-                                  wave_samples=cfg.wave_samples)
+            def rows2(f, c, r0, r1, acc, S2=S2, N2=N2):
+                pt.render_rows(S2, N2, W, H, r0, r1, f, c, depth, cfg.seed, acc, env_rgb=env,
+                               wave_samples=cfg.wave_samples)
 
-            render_partitioned(block2, R.n_total, acc2, rank, world)
+            render_partitioned_rows(rows2, R.n_total, H, acc2, rank, world)
             if rank == 0:
                 host_fb.copy_(acc2.mul_(1.0 / R.n_total), non_blocking=False)
         torch.cuda.synchronize()

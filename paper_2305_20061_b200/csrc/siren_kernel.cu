@@ -62,6 +62,9 @@ constexpr int kThreads = 32 * (kFirstEpiWarp + kNumEpiWarps);   // 640
 // [9..10] o_full[slot] (commit of layer 5); TMEM base address at +120. (O(s) needs no "free" barrier:
 // the output warps read it before they arrive on a_ready(s) for the next tile's layer 4, which the
 // issuer waits for before it issues that tile's layer 5.)
+#ifndef PT_NIF_OUT_EARLY
+#define PT_NIF_OUT_EARLY 0
+#endif
 enum { kBarW = 0, kBarAReady = 1, kBarDFull = 3, kBarA0Full = 5, kBarA0Empty = 7, kBarOFull = 9 };
 
 constexpr uint32_t kTmemCols = 512;
@@ -383,7 +386,9 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
                         tmem_wait_ld_dep16(v + 16);
                         sine_half(v + 16, 1, pk + 8);
                     }
+#if PT_NIF_OUT_EARLY
                     if (cb == 0 && stage == 0 && pend[s]) output(s, prow[s]);   // O(prev) committed with layer 1
+#endif
                     {
                         // -> A of the next layer (this warp's 32 columns)
                         TMEM_ST16(tmem + a_col(s) + lane_addr + 16 * cb, pk);
@@ -393,6 +398,11 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
                     }
                     if (trole > 0 && lane == 0) NIF_TRACE(trole, rec, 1);
                     if (lane == 0) mbar_arrive(bar(kBarAReady + s));
+#if !PT_NIF_OUT_EARLY
+                    // O(prev) was committed with this layer 1: read it once this warp's share of the next
+                    // layer's A is handed over, off the MMA's critical path
+                    if (cb == 0 && stage == 0 && pend[s]) output(s, prow[s]);
+#endif
                     if (cb == 0 && stage == 1) {
                         // this tile's output rows (after the previous tile's output was written)
                         ovalid[s] = valid;
