@@ -49,11 +49,15 @@ __device__ __forceinline__ bool mbar_try_sleep(uint32_t bar, uint32_t phase) {
         : "memory");
     return ok != 0;
 }
-// bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU
+// bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU. PT_MBAR_SPIN=1 polls
+// without the suspend hint (A/B measurement of the wake-up latency)
+#ifndef PT_MBAR_SPIN
+#define PT_MBAR_SPIN 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
     if (mbar_try(bar, phase)) return;
     const long long t0 = clock64();
-    while (!mbar_try_sleep(bar, phase)) {
+    while (!(PT_MBAR_SPIN ? mbar_try(bar, phase) : mbar_try_sleep(bar, phase))) {
         if (clock64() - t0 > 4000000000ll) __trap();
     }
 }

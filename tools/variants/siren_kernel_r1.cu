@@ -14,15 +14,13 @@
 //     activations in TMEM, the 9th K step reads a constant-1 TMEM column against the bias row of B.
 //     Whole-N MMAs (tools/mma_shapes.cu: N = 64 from TMEM costs 57 of N = 128's 64 cycles) and no
 //     TMEM/SMEM A switch inside a layer (~50 cycles each).
-//   * Layer 5 (128 -> 3): 8 TS MMAs with N = 16 into the slot's own output columns O (b5 is added by the
-//     output warps). It is issued together with layer 1 of the slot's next tile (one commit group), so
-//     the tensor pipe never holds an output layer in front of the MMA the epilogue needs next; the 4
-//     warps owning TMEM lane quarters at column block 0 read O(prev tile) during the next tile's first
-//     sine stage (exp, beta, store). (On the FMA pipe inside the layer-4 epilogue it lengthened the
-//     epilogue, the bottleneck, by ~700 cycles per tile: tools/nif_trace.py.)
+//   * Layer 5 (128 -> 3): 9 TS MMAs with N = 16 (the 9th again the bias step); only the 4 warps owning
+//     D columns 0..31 read it (exp, beta, store), so the other 12 epilogue warps run ahead to the other
+//     slot. (On the FMA pipe inside the layer-4 epilogue it lengthened the epilogue, the bottleneck, by
+//     ~700 cycles per tile: tools/nif_trace.py.)
 // TMEM (512 columns): slot s: D at 256 s (128 fp32 columns), A at 256 s + 128 (64 columns of fp16
-// pairs + the constant K block 64..71), O at 256 s + 208 (16 columns). A is single-buffered: each
-// layer's epilogue starts after the layer's one commit, i.e. after the MMA finished reading A.
+// pairs + the constant K block 64..71). A is single-buffered: each layer's epilogue starts after the
+// layer's one commit, i.e. after the MMA finished reading A.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -59,21 +57,14 @@ constexpr int kProducerThreads = 64;
 constexpr int kThreads = 32 * (kFirstEpiWarp + kNumEpiWarps);   // 640
 // barriers: [0] weights, [1..2] a_ready[slot] (16 epilogue warps: next layer's A written), [3..4] d_full[slot]
 // (commit of layers 1-4), [5..6] a0_full[slot] (64 producer threads), [7..8] a0_empty[slot] (commit),
-// [9..10] o_full[slot] (commit of layer 5); TMEM base address at +120. (O(s) needs no "free" barrier:
-// the output warps read it before they arrive on a_ready(s) for the next tile's layer 4, which the
-// issuer waits for before it issues that tile's layer 5.)
-#ifndef PT_NIF_DIAG
-#define PT_NIF_DIAG 0   // diagnostic builds only (wrong results): 1 = no TMEM store of A, 2 = no sine
-#endif
-#ifndef PT_NIF_OUT_EARLY
-#define PT_NIF_OUT_EARLY 0
-#endif
-enum { kBarW = 0, kBarAReady = 1, kBarDFull = 3, kBarA0Full = 5, kBarA0Empty = 7, kBarOFull = 9 };
+// [9..10] o_full[slot] (commit of layer 5), [11..12] d_free[slot] (the 4 output warps: D read);
+// TMEM base address at +120
+enum { kBarW = 0, kBarAReady = 1, kBarDFull = 3, kBarA0Full = 5, kBarA0Empty = 7, kBarOFull = 9, kBarDFree = 11 };
+constexpr int kOutWarps = 4;                    // epilogue warps with cb == 0 (one per lane quarter)
 
 constexpr uint32_t kTmemCols = 512;
 __host__ __device__ constexpr uint32_t d_col(int s) { return 256u * s; }
 __host__ __device__ constexpr uint32_t a_col(int s) { return 256u * s + 128u; }
-__host__ __device__ constexpr uint32_t o_col(int s) { return 256u * s + 208u; }
 
 // instruction descriptor: D f32, A/B f16, K-major both, M = 128, N given
 __host__ __device__ constexpr uint32_t idesc(int n) {
@@ -164,6 +155,7 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
             mbar_init(bar(kBarA0Full + s), kProducerThreads);
             mbar_init(bar(kBarA0Empty + s), 1);
             mbar_init(bar(kBarOFull + s), 1);
+            mbar_init(bar(kBarDFree + s), kOutWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -201,32 +193,17 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
         if (blockIdx.x < n_tiles) {
             mbar_wait(bar(kBarW), 0);
             const uint32_t img = smem_u32(smem);
-            uint32_t a_phase[2] = {0, 0}, f_phase[2] = {0, 0};
-            bool pend[2] = {false, false};   // a tile of this slot still needs its output layer
+            uint32_t a_phase[2] = {0, 0}, f_phase[2] = {0, 0}, r_phase[2] = {0, 0};
             int rec = 0;
-            // layer 5 of the slot's previous tile: after its layer-4 epilogue (a_ready), into O(s)
-            auto issue_out = [&](int s) {
-                mbar_wait(bar(kBarAReady + s), a_phase[s]);
-                a_phase[s] ^= 1;
-                tc_fence_after();
-                if (elect_one()) {
-                    const uint32_t base = img + kOffB5;
-                    const uint32_t at = tmem + a_col(s);
-#pragma unroll
-                    for (int k = 0; k < 8; ++k)
-                        mma_ts(tmem + o_col(s), at + 8 * k, smem_desc(base + k * 2 * 256, 256, 128), idesc(16), k > 0);
-                    mma_commit(bar(kBarOFull + s));
-                }
-                __syncwarp();
-            };
             for (uint32_t i = 0;; i += 2) {
                 const uint32_t t0 = blockIdx.x + i * gridDim.x;
                 if (t0 >= n_tiles) break;
                 const int nslots = (t0 + gridDim.x < n_tiles) ? 2 : 1;
-                for (int stage = 0; stage < 4; ++stage) {
+                for (int stage = 0; stage < 5; ++stage) {
                     for (int s = 0; s < nslots; ++s, ++rec) {
                         if (stage == 0) {
-                            if (pend[s]) issue_out(s);                   // previous tile's output layer
+                            mbar_wait(bar(kBarDFree + s), r_phase[s]);   // previous tile's output read
+                            r_phase[s] ^= 1;
                             mbar_wait(bar(kBarA0Full + s), f_phase[s]);  // layer-1 inputs staged
                             f_phase[s] ^= 1;
                         } else {
@@ -242,23 +219,27 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
                                 mma_ss(dt, a0, smem_desc(img, 2048, 128), idesc(128), 0);
                                 mma_commit(bar(kBarDFull + s));
                                 mma_commit(bar(kBarA0Empty + s));   // staging tile free once layer 1 is done
-                            } else {
+                            } else if (stage < 4) {
                                 const uint32_t base = img + kOffBH + (stage - 1) * kBHBytes;
                                 const uint32_t at = tmem + a_col(s);
 #pragma unroll
                                 for (int k = 0; k < 9; ++k)
                                     mma_ts(dt, at + 8 * k, smem_desc(base + k * 2 * 2048, 2048, 128), idesc(128), k > 0);
                                 mma_commit(bar(kBarDFull + s));
+                            } else {
+                                const uint32_t base = img + kOffB5;
+                                const uint32_t at = tmem + a_col(s);
+#pragma unroll
+                                for (int k = 0; k < 9; ++k)
+                                    mma_ts(dt, at + 8 * k, smem_desc(base + k * 2 * 256, 256, 128), idesc(16), k > 0);
+                                mma_commit(bar(kBarOFull + s));
                             }
                         }
                         __syncwarp();
-                        if (stage == 0) pend[s] = true;
                         if (lane == 0) NIF_TRACE(0, rec, 1);
                     }
                 }
             }
-            for (int s = 0; s < 2; ++s)
-                if (pend[s]) issue_out(s);                           // the last tiles' output layers
         }
     } else if (warp == kProducerWarp0 || warp == kProducerWarp0 + 1) {
         // ===== producers: layer-1 inputs of every tile, staged one tile ahead per slot =====
@@ -319,47 +300,20 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        // b5 (fp16 in the image's bias step of B5: row n, k = 128), added by the output warps once the
-        // weight image has landed (the bulk copies complete on kBarW)
-        float b5[3] = {0.0f, 0.0f, 0.0f};
-        if (cb == 0) {
-            mbar_wait(bar(kBarW), 0);
-#pragma unroll
-            for (int n = 0; n < 3; ++n)
-                b5[n] = __half2float(*reinterpret_cast<const __half*>(smem + kOffB5 + (16 * 2) * 128 + n * 16));
+        if (cb == 0 && lane == 0) {
+            mbar_arrive(bar(kBarDFree + 0));      // D free for each slot's first tile
+            mbar_arrive(bar(kBarDFree + 1));
         }
         uint32_t d_phase[2] = {0, 0}, o_phase[2] = {0, 0};
-        // the output rows of each slot's previous tile (cb == 0 warps): slot id, throughput, validity
-        float4 beta[2] = {make_float4(0, 0, 0, 0), make_float4(0, 0, 0, 0)};
-        uint32_t oslot[2] = {0, 0};
-        bool ovalid[2] = {false, false}, pend[2] = {false, false};
-        // layer 5 of the slot's previous tile: y = O[:, 0:3] + b5; radiance = beta * exp(y)
-        auto output = [&](int s, uint32_t dbg_row) {
-            mbar_wait(bar(kBarOFull + s), o_phase[s]);
-            o_phase[s] ^= 1;
-            tc_fence_after();
-            uint32_t v[4];
-            tmem_ld4(tmem + o_col(s) + lane_addr, v);
-            tmem_wait_ld_dep4(v);
-            if (ovalid[s]) {
-                const float y0 = __uint_as_float(v[0]) + b5[0], y1 = __uint_as_float(v[1]) + b5[1],
-                            y2 = __uint_as_float(v[2]) + b5[2];
-                if (kDebug) {
-                    dbg[((size_t)4 * n_rows + dbg_row) * 128 + 0] = y0;
-                    dbg[((size_t)4 * n_rows + dbg_row) * 128 + 1] = y1;
-                    dbg[((size_t)4 * n_rows + dbg_row) * 128 + 2] = y2;
-                }
-                out[3 * (size_t)oslot[s] + 0] = beta[s].x * __expf(y0);
-                out[3 * (size_t)oslot[s] + 1] = beta[s].y * __expf(y1);
-                out[3 * (size_t)oslot[s] + 2] = beta[s].z * __expf(y2);
-            }
-        };
-        uint32_t prow[2] = {0, 0};
         int rec = 0;
         for (uint32_t i = 0;; i += 2) {
             const uint32_t t0 = blockIdx.x + i * gridDim.x;
             if (t0 >= n_tiles) break;
             const int nslots = (t0 + gridDim.x < n_tiles) ? 2 : 1;
+            // the output rows' slot ids and throughputs (cb == 0 warps write the radiance), loaded at
+            // layer 2 so their latency hides behind two layers
+            float4 beta[2] = {make_float4(0, 0, 0, 0), make_float4(0, 0, 0, 0)};
+            uint32_t oslot[2] = {0, 0};
             for (int stage = 0; stage < 4; ++stage) {
                 for (int s = 0; s < nslots; ++s, ++rec) {
                     const uint32_t tile = t0 + s * gridDim.x;
@@ -370,6 +324,10 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
                     const int trole = (warp == kFirstEpiWarp) ? 1 : (warp == kFirstEpiWarp + kNumEpiWarps - 1 ? 2 : -1);
                     if (trole > 0 && lane == 0) NIF_TRACE(trole, rec, 0);
                     tc_fence_after();
+                    if (cb == 0 && stage == 1 && valid) {
+                        beta[s] = __ldg(esc_beta + row);
+                        oslot[s] = __float_as_uint(__ldg(esc + row).w);
+                    }
                     uint32_t v[32];
                     uint32_t pk[16];
                     if (kDebug) {
@@ -380,12 +338,6 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
                                 dbg[((size_t)stage * n_rows + row) * 128 + 32 * cb + j] = __uint_as_float(v[j]);
                         sine_half(v, 0, pk);
                         sine_half(v + 16, 1, pk + 8);
-                    } else if (PT_NIF_DIAG == 2) {
-                        // diagnostic (wrong results): TMEM round trip without the sine
-                        TMEM_LD32(tmem + d_col(s) + lane_addr + 32 * cb, v);
-                        tmem_wait_ld_dep(v);
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) pk[j] = v[2 * j] ^ v[2 * j + 1];
                     } else {
                         // D (fp32) -> sin -> fp16: the second 16 columns load while the first are computed
                         TMEM_LD16(tmem + d_col(s) + lane_addr + 32 * cb, v);
@@ -395,44 +347,46 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
                         tmem_wait_ld_dep16(v + 16);
                         sine_half(v + 16, 1, pk + 8);
                     }
-#if PT_NIF_OUT_EARLY
-                    if (cb == 0 && stage == 0 && pend[s]) output(s, prow[s]);   // O(prev) committed with layer 1
-#endif
                     {
                         // -> A of the next layer (this warp's 32 columns)
-                        if (PT_NIF_DIAG != 1) {
-                            TMEM_ST16(tmem + a_col(s) + lane_addr + 16 * cb, pk);
-                        } else if (pk[0] == 0x7FFF7FFFu && pk[15] == 0x7FFF7FFFu) {   // diagnostic: keep pk live
-                            out[0] = 0.0f;
-                        }
+                        TMEM_ST16(tmem + a_col(s) + lane_addr + 16 * cb, pk);
                         tmem_wait_st();
                         tc_fence_before();
                         __syncwarp();
                     }
                     if (trole > 0 && lane == 0) NIF_TRACE(trole, rec, 1);
                     if (lane == 0) mbar_arrive(bar(kBarAReady + s));
-#if !PT_NIF_OUT_EARLY
-                    // O(prev) was committed with this layer 1: read it once this warp's share of the next
-                    // layer's A is handed over, off the MMA's critical path
-                    if (cb == 0 && stage == 0 && pend[s]) output(s, prow[s]);
-#endif
-                    if (cb == 0 && stage == 1) {
-                        // this tile's output rows (after the previous tile's output was written)
-                        ovalid[s] = valid;
-                        prow[s] = row;
-                        if (valid) {
-                            beta[s] = __ldg(esc_beta + row);
-                            oslot[s] = __float_as_uint(__ldg(esc + row).w);
-                        }
-                    }
-                    if (stage == 0) pend[s] = true;
                 }
             }
             rec += nslots;   // (trace records of the MMA's layer-5 steps)
+            // layer 5 (output): y = D[:, 0:3]; radiance = beta * exp(y) -- the cb == 0 warps only
+            if (cb == 0) {
+                for (int s = 0; s < nslots; ++s) {
+                    const uint32_t tile = t0 + s * gridDim.x;
+                    const uint32_t row = tile * kTileM + 32 * q + lane;
+                    mbar_wait(bar(kBarOFull + s), o_phase[s]);
+                    o_phase[s] ^= 1;
+                    tc_fence_after();
+                    uint32_t v[4];
+                    tmem_ld4(tmem + d_col(s) + lane_addr, v);
+                    tmem_wait_ld_dep4(v);
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(bar(kBarDFree + s));
+                    if (row < n_rows) {
+                        const float y0 = __uint_as_float(v[0]), y1 = __uint_as_float(v[1]), y2 = __uint_as_float(v[2]);
+                        if (kDebug) {
+                            dbg[((size_t)4 * n_rows + row) * 128 + 0] = y0;
+                            dbg[((size_t)4 * n_rows + row) * 128 + 1] = y1;
+                            dbg[((size_t)4 * n_rows + row) * 128 + 2] = y2;
+                        }
+                        out[3 * (size_t)oslot[s] + 0] = beta[s].x * __expf(y0);
+                        out[3 * (size_t)oslot[s] + 1] = beta[s].y * __expf(y1);
+                        out[3 * (size_t)oslot[s] + 2] = beta[s].z * __expf(y2);
+                    }
+                }
+            }
         }
-        if (cb == 0)
-            for (int s = 0; s < 2; ++s)
-                if (pend[s]) output(s, prow[s]);   // the last tiles' output layers
     }
     // a CTA without tiles still owns the weight copies in flight into its shared memory
     if (warp == 1 && lane == 0 && blockIdx.x >= n_tiles) mbar_wait(bar(kBarW), 0);
