@@ -215,6 +215,25 @@ __device__ __forceinline__ uint32_t sin2_poly(float a, float b) {
     const __half2 r = __hmul2(p, w);
     return *reinterpret_cast<const uint32_t*>(&r);
 }
+// as sin2_poly with the layer's bias folded into the reduction: q = 1/4 + b/(2 pi), sin(x + b) per lane
+__device__ __forceinline__ uint32_t sin2_poly_q(float a, float b, float q) {
+    constexpr float kInv2Pi = 0.15915494309189535f;
+    constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23: x + magic - magic = rint(x)
+    const float2 sv = __ffma2_rn(make_float2(a, b), make_float2(kInv2Pi, kInv2Pi), make_float2(q, q));
+    const float2 tv = __fadd2_rn(sv, make_float2(kMagic, kMagic));
+    const float2 kv = __fadd2_rn(tv, make_float2(-kMagic, -kMagic));
+    const float2 uv = __fadd2_rn(sv, make_float2(-kv.x, -kv.y));
+    const float2 wv = __fadd2_rn(make_float2(fabsf(uv.x), fabsf(uv.y)), make_float2(-0.25f, -0.25f));
+    const __half2 w = __floats2half2_rn(wv.x, wv.y);
+    const __half2 w2 = __hmul2(w, w);
+    const __half2 c1 = __halves2half2(__ushort_as_half(0x4648), __ushort_as_half(0x4648));   //  6.28125
+    const __half2 c3 = __halves2half2(__ushort_as_half(0xD123), __ushort_as_half(0xD123));   // -41.09375
+    const __half2 c5 = __halves2half2(__ushort_as_half(0x5499), __ushort_as_half(0x5499));   //  73.5625
+    __half2 p = __hfma2(w2, c5, c3);
+    p = __hfma2(p, w2, c1);
+    const __half2 r = __hmul2(p, w);
+    return *reinterpret_cast<const uint32_t*>(&r);
+}
 // half of a 32-column chunk (pairs 8 h .. 8 h + 7), loaded while the other half is computed; the SFU
 // pairs are the even ones plus pair 1 (9 of 16 at the default), so both halves carry a similar SFU share
 __device__ __forceinline__ bool sfu_pair(int j) {
