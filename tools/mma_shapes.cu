@@ -14,9 +14,13 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
     return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
            ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
 }
-__host__ __device__ constexpr uint32_t idesc(int n) { return (1u << 4) | ((uint32_t)(n >> 3) << 17) | (8u << 24); }
+__host__ __device__ constexpr uint32_t idesc(int n, uint32_t ta = 0, uint32_t tb = 0) {
+    return (1u << 4) | (ta << 15) | (tb << 16) | ((uint32_t)(n >> 3) << 17) | (8u << 24);
+}
 
-// mode: 0 TS single N, 1 SS single N, 2 TS N=64 halves alternating D regions, 3 TS N=128 + SS bias / 8
+// mode: 0 TS single N, 1 SS single N, 2 TS N=64 halves alternating D regions, 3 TS N=128 + SS bias / 8,
+// 4 TS with B MN-major (SWIZZLE_NONE, LBO = K stride 128 B, SBO = MN stride 2048 B; transpose-B bit),
+// 5 SS with A MN-major (same layout) and B K-major
 template <int mode, int n>
 __global__ void __launch_bounds__(128, 1) mma_rate(int iters, unsigned long long* out) {
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -44,7 +48,19 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int iters, unsigned long long
         const uint64_t ad = sdesc(a_s, 2048, 128);
         for (int it = 0; it < iters; ++it) {
             const uint32_t acc = (it & 7) != 0;
-            if (mode == 0 || mode == 2) {
+            if (mode == 4) {
+                const uint64_t bm = sdesc(b + (uint32_t)(it % 8) * 256, 128, 2048);
+                const uint32_t a = tmem + 384u + (uint32_t)(8 * (it % 8));
+                asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                             "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem), "r"(a),
+                             "l"(bm), "r"(idesc(n, 0, 1)), "r"(acc));
+            } else if (mode == 5) {
+                const uint64_t am = sdesc(b + (uint32_t)(it % 8) * 256, 128, 2048);
+                const uint64_t bk = sdesc(a_s, 256, 128);
+                asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                             "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem), "l"(am),
+                             "l"(bk), "r"(idesc(n, 1, 0)), "r"(acc));
+            } else if (mode == 0 || mode == 2) {
                 const uint32_t d = mode == 2 ? tmem + 64u * (it & 1) : tmem;
                 const uint32_t a = tmem + 384u + (uint32_t)(8 * ((it >> (mode == 2 ? 1 : 0)) % 8));
                 const uint32_t id = idesc(mode == 2 ? 64 : n);
@@ -78,11 +94,12 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int iters, unsigned long long
 int main() {
     unsigned long long* d_out;
     cudaMalloc(&d_out, 148 * 8);
-    const char* mname[4] = {"TS", "SS", "TS N64 halves", "TS + SS bias/8"};
+    const char* mname[6] = {"TS", "SS", "TS N64 halves", "TS + SS bias/8", "TS B MN-major", "SS A MN-major"};
     struct { int mode, n; void (*k)(int, unsigned long long*); } cases[] = {
         {0, 16, mma_rate<0, 16>}, {0, 32, mma_rate<0, 32>}, {0, 64, mma_rate<0, 64>}, {0, 128, mma_rate<0, 128>},
         {0, 256, mma_rate<0, 256>}, {1, 16, mma_rate<1, 16>}, {1, 64, mma_rate<1, 64>}, {1, 128, mma_rate<1, 128>},
-        {1, 256, mma_rate<1, 256>}, {2, 64, mma_rate<2, 64>}, {3, 128, mma_rate<3, 128>}};
+        {1, 256, mma_rate<1, 256>}, {2, 64, mma_rate<2, 64>}, {3, 128, mma_rate<3, 128>},
+        {4, 128, mma_rate<4, 128>}, {5, 16, mma_rate<5, 16>}};
     for (auto c : cases) {
         const int iters = 8192;
         cudaFuncSetAttribute(c.k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
