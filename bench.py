@@ -382,7 +382,7 @@ def main():
     e2e_warmup = 1
     host_fb = torch.empty(W * H * 3, dtype=torch.float32, pin_memory=True)
     host_np = host_fb.numpy()
-    auto_k = max(1, min(spp, (8 << 20) // (W * H)))       # pt_render's wave size (pt_api.cu)
+    auto_k = max(1, min(spp, (64 << 20) // (W * H)))      # pt_render's wave size (pt_api.cu)
     host_render = world == 1 and auto_k == cfg.wave_samples
     src, blob, env = R.src, R.blob, R.env
     h2d = src.tris.nbytes + src.spheres.nbytes + src.materials.nbytes + src.camera.nbytes + (blob.nbytes if blob is not None else 0)

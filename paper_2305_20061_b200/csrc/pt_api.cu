@@ -254,7 +254,9 @@ int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, i
     const int64_t np = (int64_t)W * (row1 - row0);   // pixels rendered
     const int64_t p0 = (int64_t)W * row0;
     int64_t k = wave_samples;
-    if (k <= 0) k = std::max<int64_t>(1, std::min<int64_t>(n_samples, (int64_t)(8 << 20) / np));
+    // automatic wave: ~64 M paths (one wave per frame up to that size): fewer wave tails and NIF launches
+    // (config 3: 2.19 -> 2.34 G samples/s from 8 to 66 M paths per wave, profiles/round2/wave_k_c3.log)
+    if (k <= 0) k = std::max<int64_t>(1, std::min<int64_t>(n_samples, (int64_t)(64 << 20) / np));
     k = std::min<int64_t>(k, n_samples);
     while (k > 1 && k * np > (1ll << 31)) --k;
     int rc = ensure_ws(sc);
