@@ -81,6 +81,7 @@ def lib():
             L.orc_trace_one.restype = I32
             L.orc_trace_one.argtypes = [P, P, P, I32, I32, I32, U64, I64, I32, P, P]
             L.orc_primary.argtypes = [P, I32, I32, U64, I32, P, I64, P, P, P]
+            L.orc_trace_paths.argtypes = [P, P, P, I32, I32, I32, U64, P, I64, I32, I32, P, P, P, P, P, P, P, P]
             L.orc_primary_aov.argtypes = [P, I32, I32, U64, I32, P, I64, P, P, P, P, P]
             _lib = L
     return _lib
@@ -174,6 +175,23 @@ class OracleScene:
                                seed, _p(pix), pix.shape[0], s0, s1, nthreads, _p(out), _p(st))
         stats = dict(zip(["segments", "escaped", "emitted", "capped", "rr_killed"], st.tolist()))
         return out, stats
+
+    def trace_paths(self, width, height, max_depth, seed, pix, s0, s1, nif_blob=None, env_rgb=(1, 1, 1)):
+        """Per-segment records of paths (pixel pix[i // ns], sample s0 + i % ns), orc_trace_paths: dict of prim
+        [n][D] (-2 past the end), edge, fres_delta (xi2 - F, < 0 reflect), rr_delta (xi3 - q, >= 0 kill) [n][D],
+        ray [n][D][7] (o, d, t), uv [n][2], L [n][3], len [n]."""
+        pix = np.ascontiguousarray(pix, dtype=np.int64)
+        n = pix.shape[0] * (s1 - s0)
+        D = max_depth
+        out = {"prim": np.empty((n, D), np.int64), "edge": np.empty((n, D)), "fres_delta": np.empty((n, D)),
+               "rr_delta": np.empty((n, D)), "ray": np.empty((n, D, 7)), "uv": np.empty((n, 2)),
+               "L": np.empty((n, 3)), "len": np.empty(n, np.int32)}
+        env = np.ascontiguousarray(env_rgb, dtype=np.float64)
+        blob = None if nif_blob is None else np.ascontiguousarray(nif_blob, dtype=np.uint16)
+        lib().orc_trace_paths(self.h, _p(blob), _p(env), width, height, max_depth, seed, _p(pix), pix.shape[0], s0,
+                              s1, _p(out["prim"]), _p(out["edge"]), _p(out["fres_delta"]), _p(out["rr_delta"]),
+                              _p(out["ray"]), _p(out["uv"]), _p(out["L"]), _p(out["len"]))
+        return out
 
     def trace_one(self, width, height, max_depth, seed, p, s, nif_blob=None, env_rgb=(1, 1, 1)):
         L = np.zeros(3, np.float64)

@@ -887,8 +887,23 @@ static int roulette(double beta[3], int depth, double xi3) {
 EXPORT int orc_roulette(double* beta, int32_t depth, double xi3) { return roulette(beta, depth, xi3); }
 
 /* trace record (optional): per segment prim id (-1 miss) */
+/* Optional per-segment record of one path (first-divergence classifier, tests only): segment k (0-based)
+   = the k+1-th traced ray: the ray (o, d) and its hit primitive (-1 = escape) and t, the hit's edge measure
+   (min barycentric, or the sphere graze measure), the signed decision deltas xi2 - F of a dielectric's
+   Fresnel choice (< 0: reflect) and xi3 - q of the roulette after it (>= 0: the path ends) (+inf where no
+   such decision), and the escape direction's equirect (u, v). */
+typedef struct {
+    int64_t* prim;      /* [max_depth] */
+    double* edge;       /* [max_depth] */
+    double* fres_delta;
+    double* rr_delta;
+    double* ray;        /* [max_depth][7]: o, d, t */
+    double* uv;         /* [2] of the escape segment (-1 if none) */
+    int32_t len;
+} path_rec;
+
 static void trace_path(const render_ctx* c, int64_t p, int32_t s, double L[3], path_stats* st,
-                       int64_t* trace_prims, int32_t* trace_len) {
+                       int64_t* trace_prims, int32_t* trace_len, path_rec* rec) {
     const orc_scene* sc = c->sc;
     double xi[4];
     draw4(c->seed, (uint32_t)p, (uint32_t)s, 0u, xi);
@@ -908,6 +923,16 @@ static void trace_path(const render_ctx* c, int64_t p, int32_t s, double L[3], p
         depth += 1;
         st->segments++;
         if (trace_prims && depth <= MAX_TRACE) { trace_prims[depth - 1] = h.prim; *trace_len = depth; }
+        if (rec) {
+            rec->prim[depth - 1] = h.prim;
+            rec->edge[depth - 1] = h.prim >= 0 ? h.edge : INFINITY;
+            rec->fres_delta[depth - 1] = INFINITY;
+            rec->rr_delta[depth - 1] = INFINITY;
+            double* ry = rec->ray + 7 * (depth - 1);
+            for (int k = 0; k < 3; ++k) { ry[k] = o[k]; ry[3 + k] = d[k]; }
+            ry[6] = h.prim >= 0 ? h.t : INFINITY;
+            rec->len = depth;
+        }
         if (h.prim < 0) {                                   /* escaped: environment light */
             double env[3];
             if (c->nif || c->fr) {
@@ -922,6 +947,7 @@ static void trace_path(const render_ctx* c, int64_t p, int32_t s, double L[3], p
             }
             for (int k = 0; k < 3; ++k) L[k] += beta[k] * env[k];
             st->escaped++;
+            if (rec) equirect(d, &rec->uv[0], &rec->uv[1]);
             return;
         }
         uint32_t mi;
@@ -964,6 +990,7 @@ static void trace_path(const render_ctx* c, int64_t p, int32_t s, double L[3], p
         } else {
             double F;
             side = scatter_dielectric(d, n, entering, (double)m->ior, xi[2], wi, &F);
+            if (rec) rec->fres_delta[depth - 1] = xi[2] - F;
         }
         normalize3(wi);
         /* spawn: offset along the side wi leaves to (reading R10) */
@@ -971,6 +998,13 @@ static void trace_path(const render_ctx* c, int64_t p, int32_t s, double L[3], p
         for (int k = 0; k < 3; ++k) if (fabs(P[k]) > pm) pm = fabs(P[k]);
         double eps = 1e-4 * pm;
         for (int k = 0; k < 3; ++k) { o[k] = P[k] + eps * (double)side * n[k]; d[k] = wi[k]; }
+        if (rec && depth >= RR_START) {
+            double q = beta[0];
+            if (beta[1] > q) q = beta[1];
+            if (beta[2] > q) q = beta[2];
+            if (q > 1.0) q = 1.0;
+            rec->rr_delta[depth - 1] = xi[3] - q;
+        }
         if (!roulette(beta, depth, xi[3])) { st->rr_killed++; return; }
     }
 }
@@ -992,7 +1026,7 @@ static void* worker(void* vp) {
         double acc[3] = {0, 0, 0};
         for (int32_t s = a->s0; s < a->s1; ++s) {
             double L[3];
-            trace_path(a->c, a->pix[i], s, L, &a->st, NULL, NULL);
+            trace_path(a->c, a->pix[i], s, L, &a->st, NULL, NULL, NULL);
             for (int k = 0; k < 3; ++k) acc[k] += L[k];
         }
         for (int k = 0; k < 3; ++k) a->out[3 * i + k] = acc[k];
@@ -1078,7 +1112,7 @@ EXPORT int32_t orc_trace_one(const orc_scene* sc, const uint16_t* nif_blob, cons
     for (int k = 0; k < 3; ++k) c.env[k] = env_rgb ? env_rgb[k] : 1.0;
     path_stats st = {0, 0, 0, 0, 0};
     int32_t len = 0;
-    trace_path(&c, p, s, L, &st, prims, &len);
+    trace_path(&c, p, s, L, &st, prims, &len, NULL);
     if (nif_blob) nif_free(&net);
     return len;
 }
@@ -1152,4 +1186,35 @@ EXPORT void orc_primary_aov(const orc_scene* sc, int32_t W, int32_t H, uint64_t 
         }
         for (int a = 0; a < 3; ++a) { pos[3 * i + a] = P[a]; nrm[3 * i + a] = ng[a]; }
     }
+}
+
+/* Per-segment records of the paths (listed pixels x samples [s0, s1)) for the first-divergence classifier
+   (tests only): path i = pixel pix[i / ns] sample s0 + i % ns, arrays [n_paths][max_depth] (prim -2 past
+   the end), ray [n_paths][max_depth][7], uv [n_paths][2] (-1 without escape), L [n_paths][3], len [n_paths]. */
+EXPORT void orc_trace_paths(const orc_scene* sc, const uint16_t* nif_blob, const double* env_rgb, int32_t W, int32_t H,
+                            int32_t max_depth, uint64_t seed, const int64_t* pix, int64_t n_pix, int32_t s0, int32_t s1,
+                            int64_t* prim, double* edge, double* fres_delta, double* rr_delta, double* ray, double* uv,
+                            double* L, int32_t* len) {
+    render_ctx c;
+    c.sc = sc; c.W = W; c.H = H; c.max_depth = max_depth; c.seed = seed;
+    cam_setup(&sc->cam, W, H, &c.cam);
+    nif64 net;
+    if (nif_blob) { nif_unpack(nif_blob, &net); c.nif = &net; } else c.nif = NULL;
+    c.fr = NULL;
+    c.fr_fp8 = 0;
+    for (int k = 0; k < 3; ++k) c.env[k] = env_rgb ? env_rgb[k] : 1.0;
+    const int32_t ns = s1 - s0;
+    path_stats st = {0, 0, 0, 0, 0};
+    for (int64_t i = 0; i < n_pix * ns; ++i) {
+        const int64_t o = i * max_depth;
+        for (int32_t k = 0; k < max_depth; ++k) {
+            prim[o + k] = -2; edge[o + k] = INFINITY; fres_delta[o + k] = INFINITY; rr_delta[o + k] = INFINITY;
+            for (int a = 0; a < 7; ++a) ray[7 * (o + k) + a] = 0.0;
+        }
+        path_rec r = {prim + o, edge + o, fres_delta + o, rr_delta + o, ray + 7 * o, uv + 2 * i, 0};
+        uv[2 * i] = uv[2 * i + 1] = -1.0;
+        trace_path(&c, pix[i / ns], s0 + (int32_t)(i % ns), L + 3 * i, &st, NULL, NULL, &r);
+        len[i] = r.len;
+    }
+    if (nif_blob) nif_free(&net);
 }

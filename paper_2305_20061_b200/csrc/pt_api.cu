@@ -674,6 +674,23 @@ int pt_set_profiling(pt_scene* scene, int32_t enabled) {
     return PT_OK;
 }
 
+// test hook (not in pt.h): per-segment records of single paths through the render kernels' shade_segment
+// (first-divergence classifier): paths i = (pixel d_pix[i / n_s], sample s0 + i % n_s)
+PT_API int pt_debug_path_records(const pt_scene* scene, int32_t use_nif, const float env_rgb[3], int32_t width,
+                                 int32_t height, int32_t max_depth, uint64_t seed, const int32_t* d_pix, int32_t n_pix,
+                                 int32_t s0, int32_t n_s, int32_t* d_prims, uint32_t* d_flags, float* d_esc_dir,
+                                 float* d_L, void* stream) {
+    if (!scene || !d_pix || !d_prims || !d_flags || !d_esc_dir || !d_L || n_pix < 0 || n_s < 1 || max_depth < 1 ||
+        (!use_nif && !env_rgb) || (int64_t)width * height * n_s >= (1ll << 31))
+        return fail(PT_ERR_INVALID_ARG, "bad argument");
+    const pt::Cam32 cam = pt::make_cam32(scene->cam, width, height);
+    const float3 env = env_rgb ? make_float3(env_rgb[0], env_rgb[1], env_rgb[2]) : make_float3(0, 0, 0);
+    pt::launch_path_record(trace_params(scene), cam, width, height, s0, n_s, max_depth, seed, use_nif ? 1 : 0, env, d_pix,
+                           n_pix, d_prims, d_flags, d_esc_dir, d_L, (cudaStream_t)stream);
+    CU(cudaGetLastError());
+    return PT_OK;
+}
+
 // host-only test hooks of the BVH builder (no GPU needed; not in pt.h)
 PT_API int pt_debug_build_bvh(const pt_triangle* tris, int64_t n_tris, const pt_sphere* spheres, int64_t n_spheres,
                        int64_t* stats /* [4]: nodes, leaves, depth, pool units */, uint32_t* pool_out,

@@ -164,6 +164,9 @@ void launch_primary_aov(const TraceParams& tp, const Cam32& cam, int W, int H, i
 void launch_trace_rays(const TraceParams& tp, const float* o, const float* d, int64_t n, int32_t* prim, float* t,
                        cudaStream_t st);
 void launch_scale(float* fb, int64_t n, float s, cudaStream_t st);
+void launch_path_record(const TraceParams& tp, const Cam32& cam, int W, int H, int s0, int n_s, int max_depth,
+                        uint64_t seed, int use_nif, float3 env, const int32_t* pix, int n_pix, int32_t* prims,
+                        uint32_t* flags, float* esc_dir, float* L, cudaStream_t st);
 void launch_pack_queries(const float* uv, int64_t n, float4* esc, float4* esc_beta, uint32_t* count,
                          cudaStream_t st);
 

@@ -66,7 +66,7 @@ constexpr int kThreads = 32 * (kFirstEpiWarp + kNumEpiWarps);   // 640
 #define PT_NIF_DIAG 0   // diagnostic builds only (wrong results): 1 = no TMEM store of A, 2 = no sine
 #endif
 #ifndef PT_NIF_DEFER_ST
-#define PT_NIF_DEFER_ST 1
+#define PT_NIF_DEFER_ST 0   // measured slower (5.96 vs 7.25 G inferences/s, profiles/round2/nif_defer.log)
 #endif
 #ifndef PT_NIF_OUT_EARLY
 #define PT_NIF_OUT_EARLY 0

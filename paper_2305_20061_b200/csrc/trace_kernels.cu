@@ -714,7 +714,10 @@ struct ShadeArgs {
 struct SegOut {
     bool alive, escaped, done;
     float3 o, d, beta, L;
+    int32_t prim;     // the segment's hit (-1 escape); read only by the path-record debug kernel
+    uint32_t flags;   // kSegReflect: dielectric chose reflection; kSegRRKill: roulette ended the path
 };
+constexpr uint32_t kSegReflect = 1u, kSegRRKill = 2u;
 
 __device__ __forceinline__ void shade_segment(const ShadeArgs& a, int depth, uint32_t slot, float3 o, float3 d,
                                               float3 bt, SegOut& r) {
@@ -728,6 +731,8 @@ __device__ __forceinline__ void shade_segment(const ShadeArgs& a, int depth, uin
     r.o = o;
     const Hit hh = closest_hit(a.tp, o, d);
     const int32_t prim = hh.prim;
+    r.prim = prim;
+    r.flags = 0u;
     if (prim < 0) {                                   // escaped: environment light
         if (a.use_nif) {
             // queued by direction; the NIF kernel maps it to equirect (u, v) (S4 -> S5)
@@ -792,6 +797,7 @@ __device__ __forceinline__ void shade_segment(const ShadeArgs& a, int depth, uin
             F = r0 + (1.0f - r0) * (mm * mm * mm * mm * mm);
         }
         if (xi2 < F) {
+            r.flags |= kSegReflect;
             wi = make_float3(d.x + 2.0f * cosi * n.x, d.y + 2.0f * cosi * n.y, d.z + 2.0f * cosi * n.z);
         } else {
             const float k = eta * cosi - cost;
@@ -812,6 +818,7 @@ __device__ __forceinline__ void shade_segment(const ShadeArgs& a, int depth, uin
     if (depth >= 3) {
         const float q = fminf(1.0f, fmaxf(bt.x, fmaxf(bt.y, bt.z)));
         if (xi3 >= q) {
+            r.flags |= kSegRRKill;
             r.alive = false;
             r.done = true;
             return;
@@ -1053,6 +1060,38 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) trace_rays_kernel(TraceParams
     }
 }
 
+// Debug (first-divergence classifier, tests only): one thread per path (listed pixel, sample), the render
+// kernels' own shade_segment per segment; records per segment the hit primitive and the decision flags,
+// the escape direction and the path radiance (constant environment; with a NIF only the direction).
+__global__ void __launch_bounds__(128) path_record_kernel(ShadeArgs a, const int32_t* pix, int n_pix, int n_s,
+                                                          int32_t* prims, uint32_t* flags, float* esc_dir, float* Lout) {
+    const int n = n_pix * n_s;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int p = pix[i / n_s], sj = i % n_s;
+        const uint32_t slot = (uint32_t)sj * (uint32_t)a.np + (uint32_t)p;   // first_sample = s0, p0 = 0
+        float3 o = make_float3(a.cam.eye[0], a.cam.eye[1], a.cam.eye[2]), d = camera_ray(a, slot);
+        float3 bt = make_float3(1.0f, 1.0f, 1.0f), L = make_float3(0, 0, 0), ed = make_float3(0, 0, 0);
+        for (int k = 0; k < a.max_depth; ++k) {
+            prims[(size_t)i * a.max_depth + k] = -2;
+            flags[(size_t)i * a.max_depth + k] = 0u;
+        }
+        for (int depth = 1; depth <= a.max_depth; ++depth) {
+            SegOut r;
+            shade_segment(a, depth, slot, o, d, bt, r);
+            prims[(size_t)i * a.max_depth + depth - 1] = r.prim;
+            flags[(size_t)i * a.max_depth + depth - 1] = r.flags;
+            L = make_float3(L.x + r.L.x, L.y + r.L.y, L.z + r.L.z);
+            if (r.escaped) ed = r.d;
+            if (!r.alive) break;
+            o = r.o;
+            d = r.d;
+            bt = r.beta;
+        }
+        esc_dir[3 * i + 0] = ed.x; esc_dir[3 * i + 1] = ed.y; esc_dir[3 * i + 2] = ed.z;
+        Lout[3 * i + 0] = L.x; Lout[3 * i + 1] = L.y; Lout[3 * i + 2] = L.z;
+    }
+}
+
 __global__ void scale_kernel(float* fb, int64_t n, float s) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         fb[i] *= s;
@@ -1165,6 +1204,23 @@ void launch_primary_aov(const TraceParams& tp, const Cam32& cam, int W, int H, i
 void launch_trace_rays(const TraceParams& tp, const float* o, const float* d, int64_t n, int32_t* prim, float* t,
                        cudaStream_t st) {
     trace_rays_kernel<<<grid_for(n, 128, PT_TS_MINB), 128, 0, st>>>(tp, o, d, n, prim, t);
+}
+
+void launch_path_record(const TraceParams& tp, const Cam32& cam, int W, int H, int s0, int n_s, int max_depth,
+                        uint64_t seed, int use_nif, float3 env, const int32_t* pix, int n_pix, int32_t* prims,
+                        uint32_t* flags, float* esc_dir, float* L, cudaStream_t st) {
+    ShadeArgs a = {};
+    a.tp = tp;
+    a.cam = cam;
+    a.W = W; a.H = H; a.first_sample = s0; a.depth = 1; a.max_depth = max_depth;
+    a.np = W * H;
+    a.p0 = 0;
+    a.inv_np = 1.0f / (float)((int64_t)W * H);
+    a.inv_w = 1.0f / (float)W;
+    a.key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+    a.use_nif = use_nif;
+    a.env = env;
+    path_record_kernel<<<grid_for((int64_t)n_pix * n_s, 128, 4), 128, 0, st>>>(a, pix, n_pix, n_s, prims, flags, esc_dir, L);
 }
 
 void launch_scale(float* fb, int64_t n, float s, cudaStream_t st) {

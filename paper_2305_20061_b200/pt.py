@@ -64,6 +64,7 @@ def lib():
             L.pt_last_error.restype = C.c_char_p
             L.pt_version.restype = C.c_char_p
             L.pt_debug_build_bvh.argtypes = [P, I64, P, I64, P, P, I64]
+            L.pt_debug_path_records.argtypes = [P, I32, P, I32, I32, I32, U64, P, I32, I32, I32, P, P, P, P, P]
             L.pt_debug_f16_round.restype = C.c_uint16
             L.pt_debug_f16_round.argtypes = [C.c_double, I32]
             if hasattr(L, "pt_debug_nif_trace"):
@@ -238,6 +239,26 @@ def nif_debug_layers(nif: Nif, uv, stream=None):
     dbg = torch.zeros((5, n, 128), dtype=torch.float32, device="cuda")
     _check(lib().pt_debug_nif_layers(nif.h, _dp(uv), n, _dp(out), _dp(dbg), _stream(stream)))
     return out, dbg
+
+
+def debug_path_records(scene: Scene, width, height, max_depth, seed, pix, s0, n_s, use_nif=True, env_rgb=None):
+    """Per-segment records of single paths through the render kernels (first-divergence classifier): dict of
+    prim [n][D] (-2 past the end), flags [n][D] (1 reflect, 2 roulette kill), esc_dir [n][3], L [n][3]
+    (numpy; path i = pixel pix[i // n_s], sample s0 + i % n_s)."""
+    import torch
+    pix_t = torch.as_tensor(np.ascontiguousarray(pix, dtype=np.int32)).cuda()
+    n = len(pix) * n_s
+    prims = torch.empty((n, max_depth), dtype=torch.int32, device="cuda")
+    flags = torch.empty((n, max_depth), dtype=torch.int32, device="cuda")
+    esc = torch.empty((n, 3), dtype=torch.float32, device="cuda")
+    L = torch.empty((n, 3), dtype=torch.float32, device="cuda")
+    env = _env(env_rgb if env_rgb is not None else (1.0, 1.0, 1.0))
+    _check(lib().pt_debug_path_records(scene.h, int(bool(use_nif)), _p(env), width, height, max_depth, seed,
+                                       _dp(pix_t), len(pix), s0, n_s, _dp(prims), _dp(flags), _dp(esc), _dp(L),
+                                       _stream(None)))
+    torch.cuda.synchronize()
+    return {"prim": prims.cpu().numpy(), "flags": flags.cpu().numpy(), "esc_dir": esc.cpu().numpy(),
+            "L": L.cpu().numpy()}
 
 
 def debug_build_bvh(sc: scenes.Scene, with_pool=False):

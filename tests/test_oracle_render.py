@@ -88,3 +88,43 @@ def test_depth_cap_and_thread_invariance(orc):
     d0, _ = sc.render(W, H, 4, 0, s0=0, s1=1, nif_blob=blob)
     d1, _ = sc.render(W, H, 4, 0, s0=1, s1=2, nif_blob=blob)
     assert np.allclose(d0 + d1, a, rtol=1e-15, atol=0)
+
+
+def test_divergence_classifier_on_synthetic_records(orc):
+    """tools/divergence.classify against hand-made differences of an oracle record set (no GPU): identical
+    records -> "same"; a roulette flip inside the xi band -> "roulette", outside -> "unexplained"; a
+    different primitive far from every edge -> "unexplained"; a near-edge hit -> "edge"."""
+    import os
+    import sys
+    import numpy as np
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import divergence
+    from paper_2305_20061_b200 import scenes
+    c = scenes.CONFIGS[0]
+    sc = scenes.scene_for_config(0)
+    pix = np.arange(64 * 20, 64 * 20 + 64)
+    o = orc.OracleScene(sc).trace_paths(c.width, c.height, 8, 0, pix, 0, 4, nif_blob=scenes.siren_blob(0))
+    # GPU-like records equal to the oracle's decisions
+    flags = np.where(np.isfinite(o["fres_delta"]) & (o["fres_delta"] < 0), 1, 0) | \
+        np.where(np.isfinite(o["rr_delta"]) & (o["rr_delta"] >= 0), 2, 0)
+    dirs = o["ray"][np.arange(len(o["len"])), o["len"] - 1, 3:6]
+    g = {"prim": o["prim"].copy(), "flags": flags, "esc_dir": dirs, "L": o["L"]}
+    cls, _ = divergence.classify(sc, g, o)
+    assert set(cls) == {"same"}
+    # a roulette decision flipped: inside / outside the band
+    i, j = next((i, j) for i in range(len(cls)) for j in range(8) if np.isfinite(o["rr_delta"][i, j]))
+    g2 = {k: v.copy() for k, v in g.items()}
+    g2["flags"][i, j] ^= 2
+    o2 = {k: v.copy() for k, v in o.items()}
+    o2["rr_delta"][i, j] = 5e-5 if o["rr_delta"][i, j] >= 0 else -5e-5
+    assert divergence.classify(sc, g2, o2)[0][i] == "roulette"
+    o2["rr_delta"][i, j] = 0.3 if o["rr_delta"][i, j] >= 0 else -0.3
+    assert divergence.classify(sc, g2, o2)[0][i] == "unexplained"
+    # a different triangle on a first-segment hit far from any edge -> unexplained; near the edge -> edge
+    i = next(i for i in range(len(cls)) if o["prim"][i, 0] >= 0 and o["edge"][i, 0] > 0.05)
+    g3 = {k: v.copy() for k, v in g.items()}
+    g3["prim"][i, 0] = (o["prim"][i, 0] + 6) % sc.n_tris
+    assert divergence.classify(sc, g3, o)[0][i] == "unexplained"
+    o3 = {k: v.copy() for k, v in o.items()}
+    o3["edge"][i, 0] = 1e-5
+    assert divergence.classify(sc, g3, o3)[0][i] == "edge"
