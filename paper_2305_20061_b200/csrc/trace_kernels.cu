@@ -462,174 +462,171 @@ constexpr uint32_t kNoEntry = 0xFFFFFFFFu;
 __device__ __forceinline__ bool is_node(uint32_t e) { return e < (1u << 28); }
 __device__ __forceinline__ bool is_leaf(uint32_t e) { return e - (1u << 28) < 0xE0000000u; }   // nibble 1..14
 
-// Traversal stack: the bottom kShortStack entries of every thread live in shared memory, laid out
-// [depth][thread] so that a warp's accesses are bank-conflict free whatever depth each lane is at; deeper
-// entries spill to a local-memory array (rare: 3 pushes per level at most, 9-14 levels on configs 3-4).
-// All kernels that trace run 128-thread blocks.
-#ifndef PT_SSTACK
-#define PT_SSTACK 0   // measured slower at every depth 8-24 and carveout (profiles/round2/variants_s3.log)
-#endif
-constexpr int kShortStack = PT_SSTACK;   // 0: the whole stack in local memory
-constexpr int kTraceBlock = 128;
-
-__device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
-    Hit best{CUDART_INF, CUDART_INF_F, CUDART_INF_F, -1, 0u, true};
-    if (tp.empty) return best;
-#if PT_SSTACK > 0
-    __shared__ uint32_t s_ent[kShortStack][kTraceBlock];
-    __shared__ float s_tn[kShortStack][kTraceBlock];
-    const int tid = threadIdx.x;
-#endif
-    float4 cold[2];                   // local memory: written and read only through ld/st.local asm
+// Closest-hit traversal, resumable: the state of one lane's traversal (the ray, the current entry, the
+// postponed leaf, the stack pointer and the best hit) lives in a Trav, its stack and cold ray data in
+// local memory the caller owns. closest_hit() runs it to completion; the path kernel interleaves it with
+// the shading of lanes whose traversal has finished (dynamic replacement, Aila & Laine 2009).
+struct Trav {
     RayT r;
-    ray_prepare(o, d, r, (uint32_t)__cvta_generic_to_local(cold));
+    uint32_t cur, leaf;
+    float cur_t, leaf_t;
+    int sp;
+    Hit best;
+    bool tracing;
+};
+
+__device__ __forceinline__ void stk_push(uint32_t stk, int& sp, uint32_t e, float t) {
+    asm volatile("st.local.v2.u32 [%0], {%1, %2};" ::"r"(stk + 8u * (uint32_t)sp), "r"(e), "r"(__float_as_uint(t))
+                 : "memory");
+    ++sp;
+}
+__device__ __forceinline__ uint2 stk_top(uint32_t stk, int sp) {
+    uint2 v;
+    asm volatile("ld.local.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(stk + 8u * (uint32_t)sp));
+    return v;
+}
+
+// cold: local address of 32 B (the ray's spilled constants); stk: local address of kStackSize 8-B entries
+__device__ __forceinline__ void trav_begin(Trav& t, const TraceParams& tp, float3 o, float3 d, uint32_t cold) {
+    t.best = Hit{CUDART_INF, CUDART_INF_F, CUDART_INF_F, -1, 0u, true};
+    ray_prepare(o, d, t.r, cold);
+    t.cur = 0;
+    t.cur_t = -CUDART_INF_F;
+    t.leaf = kNoEntry;
+    t.leaf_t = 0.0f;
+    t.sp = 0;
+    t.tracing = !tp.empty;
+    TCOUNT(4, 1);
+}
+
+// One round of the while-while loop with postponed leaves (Aila & Laine 2009): interior nodes are visited
+// until every tracing lane of the warp holds a leaf (or has finished), then the lanes test their leaves'
+// primitives together, so the primitive test runs warp-convergent. Box culling uses the best hit at the
+// time an entry is popped or visited; it only drops boxes entered strictly beyond a conservative bound of
+// the best t (reading R11), so the visiting order never changes the result. Clears t.tracing when the
+// traversal is complete.
+__device__ __forceinline__ void trav_round(const TraceParams& tp, Trav& t, uint32_t stk) {
     // PBRT-v3's robust t_far * (1 + 2 gamma_3), with gamma_5: the approximate reciprocal adds up to
     // two more roundings' worth of relative error to each slab distance
     constexpr float kGrow = 1.0f + 2.0f * (5.0f * 0x1p-24f) / (1.0f - 5.0f * 0x1p-24f);   // 1 + 2 gamma_5
+    const uint4* __restrict__ pool = tp.pool;
+    RayT& r = t.r;
     // per-axis fp16x2 half swap so that t.x is always the near slab plane and t.y the far one
     uint32_t swz[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) swz[a] = ((r.kbits >> (8 + a)) & 1u) ? 0x1032u : 0x3210u;
-    uint2 lstack[kStackSize - kShortStack];   // overflow (local memory)
-    int sp = 0;
-    auto push = [&](uint32_t e, float t) {
-#if PT_SSTACK > 0
-        if (sp < kShortStack) {
-            s_ent[sp][tid] = e;
-            s_tn[sp][tid] = t;
-        } else
-#endif
-        {
-            lstack[sp - kShortStack] = make_uint2(e, __float_as_uint(t));
-        }
-        ++sp;
-    };
-    const uint4* __restrict__ pool = tp.pool;
-    TCOUNT(4, 1);
-    // While-while traversal with postponed leaves (Aila & Laine 2009): interior nodes are visited until
-    // every lane of the warp holds a leaf (or has finished), then the lanes test their leaves'
-    // primitives together, so the primitive test runs warp-convergent. Box culling uses the best hit
-    // at the time an entry is popped or visited; it only drops boxes entered strictly beyond a
-    // conservative bound of the best t (reading R11), so the visiting order never changes the result.
-    uint32_t cur = 0;
-    float cur_t = -CUDART_INF_F;
-    uint32_t leaf = kNoEntry;
-    float leaf_t = 0.0f;
     auto pop = [&](float tcull) -> uint32_t {
-        while (sp > 0) {
-            --sp;
-            uint32_t e;
-            float t;
-#if PT_SSTACK > 0
-            if (sp < kShortStack) {
-                e = s_ent[sp][tid];
-                t = s_tn[sp][tid];
-            } else
-#endif
-            {
-                const uint2 v = lstack[sp - kShortStack];
-                e = v.x;
-                t = __uint_as_float(v.y);
-            }
-            if (t <= tcull) {
-                cur_t = t;
-                return e;
+        while (t.sp > 0) {
+            --t.sp;
+            const uint2 v = stk_top(stk, t.sp);
+            if (__uint_as_float(v.y) <= tcull) {
+                t.cur_t = __uint_as_float(v.y);
+                return v.x;
             }
         }
         return kNoEntry;
     };
-    for (;;) {
-        // ---- phase 1: interior nodes --------------------------------------------------------------
-        while (is_node(cur)) {
-            const float tcull0 = cull_bound(best);
-            if (cur_t > tcull0) {          // entered beyond the best hit found since it was pushed
-                cur = pop(tcull0);
+    // ---- phase 1: interior nodes --------------------------------------------------------------------
+    while (is_node(t.cur)) {
+        const float tcull0 = cull_bound(t.best);
+        if (t.cur_t > tcull0) {          // entered beyond the best hit found since it was pushed
+            t.cur = pop(tcull0);
+        } else {
+            TCOUNT(0, 1);
+            uint4 h, q0, q1, q2;
+            ldg256(pool + t.cur, h, q0);               // a node is 64 B, 64-B aligned: two 32-B loads
+            ldg256(pool + t.cur + 2, q1, q2);
+            const uint32_t w[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
+            const float O[3] = {__uint_as_float(h.x), __uint_as_float(h.y), __uint_as_float(h.z)};
+            // child sizes in units (nibbles: 0 none, 4 interior, 3 * count leaf), see pt_internal.h
+            const uint32_t meta = (h.x & 15u) | ((h.y & 15u) << 4) | ((h.z & 15u) << 8) | ((h.w >> 28) << 12);
+            uint32_t off = h.w & 0x0FFFFFFFu;
+            // per-child results in registers (static indices only: no local-memory arrays)
+            float ctn[4];
+            uint32_t cent[4];
+#pragma unroll
+            for (int ci = 0; ci < 4; ++ci) {
+                const uint32_t nib = (meta >> (4 * ci)) & 15u;
+                const bool valid = nib != 0u;
+                const bool lf = nib != (uint32_t)kNodeUnits;
+                float tn = 0.0f, tf = CUDART_INF_F;
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    // (near, far) bounds of this axis: exact fp16 -> fp32, then the same rn ops as the
+                    // builder's check (the half swap only reorders the two lanes)
+                    const uint32_t ws = __byte_perm(w[3 * ci + a], 0u, swz[a]);
+                    const float2 lh = __half22float2(*reinterpret_cast<const __half2*>(&ws));
+                    const float2 b = __fadd2_rn(make_float2(O[a], O[a]), lh);
+                    const float2 tt = __fmul2_rn(__fadd2_rn(b, make_float2(-r.o[a], -r.o[a])),
+                                                 make_float2(r.inv[a], r.inv[a]));
+                    tn = fmaxf(tn, tt.x);
+                    tf = fminf(tf, tt.y);
+                }
+                tf = tf * kGrow;
+                const bool hit = valid && tn <= tf && tn <= tcull0;
+                ctn[ci] = hit ? tn : CUDART_INF_F;
+                cent[ci] = off + ((lf ? nib : 0u) << 28);
+                off += nib;
+            }
+            // sort the children by entry distance (network of 5 compare-swaps), push all but the
+            // nearest (farthest first), descend into the nearest
+            cswap(ctn[0], cent[0], ctn[1], cent[1]);
+            cswap(ctn[2], cent[2], ctn[3], cent[3]);
+            cswap(ctn[0], cent[0], ctn[2], cent[2]);
+            cswap(ctn[1], cent[1], ctn[3], cent[3]);
+            cswap(ctn[1], cent[1], ctn[2], cent[2]);
+            // (non-hit children carry +inf; the bound may be +inf, so test finiteness explicitly)
+#pragma unroll
+            for (int ci = 3; ci >= 1; --ci)
+                if (ctn[ci] < CUDART_INF_F) stk_push(stk, t.sp, cent[ci], ctn[ci]);
+            if (ctn[0] < CUDART_INF_F) {
+                t.cur = cent[0];
+                t.cur_t = ctn[0];
             } else {
-                TCOUNT(0, 1);
-                uint4 h, q0, q1, q2;
-                ldg256(pool + cur, h, q0);               // a node is 64 B, 64-B aligned: two 32-B loads
-                ldg256(pool + cur + 2, q1, q2);
-                const uint32_t w[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
-                const float O[3] = {__uint_as_float(h.x), __uint_as_float(h.y), __uint_as_float(h.z)};
-                // child sizes in units (nibbles: 0 none, 4 interior, 3 * count leaf), see pt_internal.h
-                const uint32_t meta = (h.x & 15u) | ((h.y & 15u) << 4) | ((h.z & 15u) << 8) | ((h.w >> 28) << 12);
-                uint32_t off = h.w & 0x0FFFFFFFu;
-                // per-child results in registers (static indices only: no local-memory arrays)
-                float ctn[4];
-                uint32_t cent[4];
-#pragma unroll
-                for (int ci = 0; ci < 4; ++ci) {
-                    const uint32_t nib = (meta >> (4 * ci)) & 15u;
-                    const bool valid = nib != 0u;
-                    const bool lf = nib != (uint32_t)kNodeUnits;
-                    float tn = 0.0f, tf = CUDART_INF_F;
-#pragma unroll
-                    for (int a = 0; a < 3; ++a) {
-                        // (near, far) bounds of this axis: exact fp16 -> fp32, then the same rn ops as the
-                        // builder's check (the half swap only reorders the two lanes)
-                        const uint32_t ws = __byte_perm(w[3 * ci + a], 0u, swz[a]);
-                        const float2 lh = __half22float2(*reinterpret_cast<const __half2*>(&ws));
-                        const float2 b = __fadd2_rn(make_float2(O[a], O[a]), lh);
-                        const float2 t = __fmul2_rn(__fadd2_rn(b, make_float2(-r.o[a], -r.o[a])),
-                                                    make_float2(r.inv[a], r.inv[a]));
-                        tn = fmaxf(tn, t.x);
-                        tf = fminf(tf, t.y);
-                    }
-                    tf = tf * kGrow;
-                    const bool hit = valid && tn <= tf && tn <= tcull0;
-                    ctn[ci] = hit ? tn : CUDART_INF_F;
-                    cent[ci] = off + ((lf ? nib : 0u) << 28);
-                    off += nib;
-                }
-                // sort the children by entry distance (network of 5 compare-swaps), push all but the
-                // nearest (farthest first), descend into the nearest
-                cswap(ctn[0], cent[0], ctn[1], cent[1]);
-                cswap(ctn[2], cent[2], ctn[3], cent[3]);
-                cswap(ctn[0], cent[0], ctn[2], cent[2]);
-                cswap(ctn[1], cent[1], ctn[3], cent[3]);
-                cswap(ctn[1], cent[1], ctn[2], cent[2]);
-                // (non-hit children carry +inf; the bound may be +inf, so test finiteness explicitly)
-#pragma unroll
-                for (int ci = 3; ci >= 1; --ci)
-                    if (ctn[ci] < CUDART_INF_F) push(cent[ci], ctn[ci]);
-                if (ctn[0] < CUDART_INF_F) {
-                    cur = cent[0];
-                    cur_t = ctn[0];
-                } else {
-                    cur = pop(tcull0);
-                }
-            }
-            // postpone the first leaf reached and keep traversing until the whole warp holds one
-            if (is_leaf(cur) && leaf == kNoEntry) {
-                leaf = cur;
-                leaf_t = cur_t;
-                cur = pop(cull_bound(best));
-            }
-            if (!__any_sync(__activemask(), leaf == kNoEntry)) break;
-        }
-        // ---- phase 2: primitives of the postponed leaf (and of leaves met next) ---------------------
-        while (leaf != kNoEntry) {
-            if (leaf_t <= cull_bound(best)) {
-                const uint32_t cnt = ((leaf >> 28) * 86u) >> 8;   // nibble / 3
-                uint32_t unit = leaf & 0x0FFFFFFFu;
-                for (uint32_t k = 0; k < cnt; ++k, unit += kPrimUnits) test_prim(pool, unit, r, best);
-            }
-            leaf = kNoEntry;
-            if (is_leaf(cur)) {
-                leaf = cur;
-                leaf_t = cur_t;
-                cur = pop(cull_bound(best));
+                t.cur = pop(tcull0);
             }
         }
-        if (cur == kNoEntry) break;
+        // postpone the first leaf reached and keep traversing until the whole warp holds one
+        if (is_leaf(t.cur) && t.leaf == kNoEntry) {
+            t.leaf = t.cur;
+            t.leaf_t = t.cur_t;
+            t.cur = pop(cull_bound(t.best));
+        }
+        if (!__any_sync(__activemask(), t.leaf == kNoEntry)) break;
     }
-    // the fp32 sphere t can lose ~1e-5 (disc cancellation): refine the winner's t in fp64 so the
-    // spawn point stays well inside the 1e-4 self-intersection offset (reading R10)
-    if (best.prim >= 0 && !best.exact && best.prim >= (int32_t)tp.n_tris) {
-        double t64;
-        if (exact_test(pool, best.unit, r, t64)) best.t = t64;
+    // ---- phase 2: primitives of the postponed leaf (and of leaves met next) -------------------------
+    while (t.leaf != kNoEntry) {
+        if (t.leaf_t <= cull_bound(t.best)) {
+            const uint32_t cnt = ((t.leaf >> 28) * 86u) >> 8;   // nibble / 3
+            uint32_t unit = t.leaf & 0x0FFFFFFFu;
+            for (uint32_t k = 0; k < cnt; ++k, unit += kPrimUnits) test_prim(pool, unit, r, t.best);
+        }
+        t.leaf = kNoEntry;
+        if (is_leaf(t.cur)) {
+            t.leaf = t.cur;
+            t.leaf_t = t.cur_t;
+            t.cur = pop(cull_bound(t.best));
+        }
     }
-    return best;
+    if (t.cur == kNoEntry) {
+        t.tracing = false;
+        // the fp32 sphere t can lose ~1e-5 (disc cancellation): refine the winner's t in fp64 so the
+        // spawn point stays well inside the 1e-4 self-intersection offset (reading R10)
+        if (t.best.prim >= 0 && !t.best.exact && t.best.prim >= (int32_t)tp.n_tris) {
+            double t64;
+            if (exact_test(pool, t.best.unit, r, t64)) t.best.t = t64;
+        }
+    }
+}
+
+__device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
+    float4 cold[2];                   // local memory: written and read only through ld/st.local asm
+    uint2 stk[kStackSize];            // local memory: through ld/st.local asm
+    Trav t;
+    trav_begin(t, tp, o, d, (uint32_t)__cvta_generic_to_local(cold));
+    const uint32_t stk_a = (uint32_t)__cvta_generic_to_local(stk);
+    while (t.tracing) trav_round(tp, t, stk_a);
+    return t.best;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -719,8 +716,9 @@ struct SegOut {
 };
 constexpr uint32_t kSegReflect = 1u, kSegRRKill = 2u;
 
-__device__ __forceinline__ void shade_segment(const ShadeArgs& a, int depth, uint32_t slot, float3 o, float3 d,
-                                              float3 bt, SegOut& r) {
+// Emission, BSDF sampling and Russian roulette of one segment whose closest hit is hh (S3).
+__device__ __forceinline__ void shade_hit(const ShadeArgs& a, int depth, uint32_t slot, float3 o, float3 d,
+                                          float3 bt, const Hit& hh, SegOut& r) {
     const int np = a.np;
     r.alive = false;
     r.escaped = false;
@@ -729,7 +727,6 @@ __device__ __forceinline__ void shade_segment(const ShadeArgs& a, int depth, uin
     r.beta = bt;
     r.d = d;
     r.o = o;
-    const Hit hh = closest_hit(a.tp, o, d);
     const int32_t prim = hh.prim;
     r.prim = prim;
     r.flags = 0u;
@@ -829,6 +826,13 @@ __device__ __forceinline__ void shade_segment(const ShadeArgs& a, int depth, uin
     r.beta = bt;
 }
 
+// One segment of one path: closest hit over the wide BVH (S2), then shade_hit (S3).
+__device__ __forceinline__ void shade_segment(const ShadeArgs& a, int depth, uint32_t slot, float3 o, float3 d,
+                                              float3 bt, SegOut& r) {
+    const Hit hh = closest_hit(a.tp, o, d);
+    shade_hit(a, depth, slot, o, d, bt, hh, r);
+}
+
 // The camera ray of wave slot i = (pixel p0 + i % np, sample first + i / np) (S1, reading R22)
 __device__ __forceinline__ float3 camera_ray(const ShadeArgs& a, uint32_t i) {
     uint32_t pu, px;
@@ -908,10 +912,17 @@ __global__ void __launch_bounds__(128, PT_FB_MINB) first_bounce_kernel(ShadeArgs
 }
 
 // Bounces 2.. (persistent): every lane carries one path from the first bounce's queue to its end,
-// and a lane whose path ends refills from the queue (one 64-bit atomic per warp iteration for all of the warp's
-// free lanes), so the warps stay full without a launch, a barrier or a state round trip through HBM
-// per bounce. Per-path results do not depend on the schedule: the RNG is keyed by (pixel, sample,
-// depth) and every path writes only its own slot.
+// and a lane whose path ends refills from the queue (one 64-bit atomic per warp iteration for all of the
+// warp's free lanes), so the warps stay full without a launch, a barrier or a state round trip through
+// HBM per bounce. Traversal with dynamic replacement (Aila & Laine 2009): a lane's traversal state
+// survives across rounds, and the warp interrupts its traversal rounds as soon as PT_TRACE_WAKE lanes are
+// waiting (traversal finished, or no path while the queue still has some) to shade those segments and
+// start the next ones -- so lanes with short traversals do not idle behind the warp's longest one.
+// Per-path results do not depend on the schedule: the RNG is keyed by (pixel, sample, depth) and every
+// path writes only its own slot.
+#ifndef PT_TRACE_WAKE
+#define PT_TRACE_WAKE 12
+#endif
 __global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
     pdl_wait();                       // first_bounce complete: its queue and counters are visible
     pdl_trigger();
@@ -920,10 +931,16 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
     // (escaped count, paths taken) word; the alive queue's length is final once first_bounce is done
     unsigned long long* const qw = reinterpret_cast<unsigned long long*>(a.esc_count);
     const int n_alive = (int)*a.alive_count;
-    bool have = false;
+    float4 cold[2];                   // local memory (ld/st.local asm): the ray's spilled constants
+    uint2 stk[kStackSize];            // local memory: the traversal stack
+    const uint32_t cold_a = (uint32_t)__cvta_generic_to_local(cold);
+    const uint32_t stk_a = (uint32_t)__cvta_generic_to_local(stk);
+    bool have = false, dry = false;
     uint32_t slot = 0;
     int depth = 0;
-    float3 o = make_float3(0, 0, 0), d = make_float3(0, 0, 1), bt = make_float3(1, 1, 1);
+    float3 bt = make_float3(1, 1, 1);
+    Trav tv;
+    tv.tracing = false;
     uint32_t segs = 0;
     // lanes without a path take queue entries r0 - 1 - (rank among them) while those are >= 0
     auto refill = [&](unsigned long long old, uint32_t mneed) {
@@ -932,14 +949,14 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
             if (idx >= 0) {
                 const float4 qa = __ldg(a.qA + idx), qb = __ldg(a.qB + idx);
                 const float2 qc = __ldg(a.qC + idx);
-                o = make_float3(qa.x, qa.y, qa.z);
                 slot = __float_as_uint(qa.w);
-                d = make_float3(qb.x, qb.y, qb.z);
                 bt = make_float3(qb.w, qc.x, qc.y);
                 depth = 2;
                 have = true;
+                trav_begin(tv, a.tp, make_float3(qa.x, qa.y, qa.z), make_float3(qb.x, qb.y, qb.z), cold_a);
             }
         }
+        if (__any_sync(0xFFFFFFFFu, !have)) dry = true;   // the queue ran out (taken only grows)
     };
     {
         unsigned long long old = 0;
@@ -947,26 +964,31 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
         refill(__shfl_sync(0xFFFFFFFFu, old, 0), 0xFFFFFFFFu);
     }
     for (;;) {
-        if (!__any_sync(0xFFFFFFFFu, have)) break;
+        // traversal rounds until enough lanes wait (or none traces)
+        for (;;) {
+            const uint32_t tr = __ballot_sync(0xFFFFFFFFu, tv.tracing);
+            const uint32_t wake = __ballot_sync(0xFFFFFFFFu, have ? !tv.tracing : !dry);
+            if (tr == 0u || __popc(wake) >= PT_TRACE_WAKE) break;
+            if (tv.tracing) trav_round(a.tp, tv, stk_a);
+        }
         SegOut r;
         r.escaped = false;
-        if (have) {
+        if (have && !tv.tracing) {
             ++segs;
-            shade_segment(a, depth, slot, o, d, bt, r);
+            shade_hit(a, depth, slot, make_float3(tv.r.o[0], tv.r.o[1], tv.r.o[2]), ray_dir(tv.r), bt, tv.best, r);
             write_radiance(a, r, slot);
             if (r.alive) {
-                o = r.o;
-                d = r.d;
                 bt = r.beta;
                 ++depth;
+                trav_begin(tv, a.tp, r.o, r.d, cold_a);
             } else {
                 have = false;
             }
         }
         // one 64-bit atomic per warp iteration: append this iteration's escapes (low word) and take
-        // new paths for the free lanes (high word)
+        // new paths for the free lanes (high word) while the queue has some
         const uint32_t me = __ballot_sync(0xFFFFFFFFu, r.escaped);
-        const uint32_t mneed = __ballot_sync(0xFFFFFFFFu, !have);
+        const uint32_t mneed = dry ? 0u : __ballot_sync(0xFFFFFFFFu, !have);
         if ((me | mneed) != 0u) {
             const int leader = __ffs(me | mneed) - 1;
             unsigned long long old = 0;
@@ -978,8 +1000,9 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
                 a.esc[pos] = make_float4(r.d.x, r.d.y, r.d.z, __uint_as_float(slot));
                 a.esc_beta[pos] = make_float4(r.beta.x, r.beta.y, r.beta.z, 0.0f);
             }
-            refill(old, mneed);
+            if (mneed) refill(old, mneed);
         }
+        if (!__any_sync(0xFFFFFFFFu, have)) break;
     }
 #pragma unroll
     for (int k = 16; k > 0; k >>= 1) segs += __shfl_xor_sync(0xFFFFFFFFu, segs, k);
@@ -1132,22 +1155,12 @@ static int resident_grid(K kernel, int block) {
     return num_sms() * (per_sm > 0 ? per_sm : 1);
 }
 
-// resident grids of the two path kernels, per device (occupancy and SM count are per-device properties).
-// PT_TRACE_CARVEOUT (percent of the maximum shared memory, or -1 = driver default): the shared/L1 split of
-// the traversal kernels -- the short stack needs kShortStack * 1 KiB per block, the rest stays L1 for
-// BVH nodes.
-#ifndef PT_TRACE_CARVEOUT
-#define PT_TRACE_CARVEOUT -1
-#endif
+// resident grids of the two path kernels, per device (occupancy and SM count are per-device properties)
 static int2 path_grids() {
     static std::atomic<int> g1[64], g2[64];
     const int dev = current_device();
     int a = g1[dev].load(std::memory_order_relaxed), b = g2[dev].load(std::memory_order_relaxed);
     if (a <= 0 || b <= 0) {
-        if (PT_TRACE_CARVEOUT >= 0) {
-            cudaFuncSetAttribute(first_bounce_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, PT_TRACE_CARVEOUT);
-            cudaFuncSetAttribute(path_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, PT_TRACE_CARVEOUT);
-        }
         a = resident_grid(first_bounce_kernel, 128);
         b = resident_grid(path_kernel, 128);
         g1[dev].store(a, std::memory_order_relaxed);
