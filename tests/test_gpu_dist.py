@@ -66,7 +66,7 @@ def test_two_rank_cuda_render_reduce_equals_single_rank(spp):
     got = next(a for r, _, a in res if r == 0)
     blocks = {r: b for r, b, _ in res}
     if spp % world:
-        assert all(r0 > 0 or r1 < 64 for b in blocks.values() for _, _, r0, r1 in b)   # row-block split used
+        assert any(r0 > 0 or r1 < 64 for b in blocks.values() for _, _, r0, r1 in b)   # row-block split used
     c = scenes.CONFIGS[0]
     ref = torch.zeros(c.width * c.height * 3, dtype=torch.float32, device="cuda")
     pt.render_samples(pt.Scene(scenes.scene_for_config(0)), pt.Nif(scenes.siren_blob(0)), c.width, c.height, 0, spp,
