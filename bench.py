@@ -42,6 +42,7 @@ L2_READ_GBS = 16409.6                       # tools/l2_bench.cu on this pool's B
 PROFILE_DIRS = [os.path.join(ROOT, "profiles", "round2"), os.path.join(ROOT, "profiles", "round1")]
 TRACE_SOURCES = ["paper_2305_20061_b200/csrc/trace_kernels.cu", "paper_2305_20061_b200/csrc/bvh_build.cpp",
                  "paper_2305_20061_b200/csrc/pt_internal.h"]
+TRACE_KERNELS = ["path_kernel"]          # one fused path kernel per wave (first_bounce_kernel only if unfused)
 NIF_SOURCES = ["paper_2305_20061_b200/csrc/siren_kernel.cu", "paper_2305_20061_b200/csrc/tc_ptx.cuh"]
 
 
@@ -289,7 +290,8 @@ def profile_pass(R, steps):
     last step; a separate pass, so the timed loop above runs without the profiling events."""
     import torch
     kt = {"raygen": 0.0, "traverse": 0.0, "shade": 0.0, "nif": 0.0, "accum": 0.0}
-    tot = {"escaped": 0, "segments": 0, "paths": 0, "launches": 0, "nif_launches": 0, "traverse_launches": 0}
+    tot = {"escaped": 0, "segments": 0, "paths": 0, "launches": 0, "nif_launches": 0, "traverse_launches": 0,
+           "waves": 0}
     R.S.set_profiling(True)
     for _ in range(steps):
         R.step()
@@ -451,7 +453,7 @@ def main():
     K = args.steps
     infers = prof["escaped"]
     nif_ms = prof["nif"]
-    waves = max(1.0, prof["traverse_launches"] / 2)
+    waves = max(1.0, prof["waves"])
     nif_tflops = (HIDDEN_FLOP_PER_INF * infers) / (nif_ms / 1e3) / 1e12 if nif_ms > 0 else 0.0
     nif_traffic, nif_traffic_file, nif_traffic_cur = ncu_capture(["siren_kernel"], cfg.index, "dram_bytes_per_launch",
                                                                  NIF_SOURCES)
@@ -471,10 +473,8 @@ def main():
     segs = prof["segments"]
     bps = tc["bytes_per_segment"] if tc else None
     gbs = (bps or 0.0) * segs / (ms_k / 1e3) / 1e9 if ms_k > 0 else 0.0
-    tr_traffic, tr_file, tr_cur = ncu_capture(["first_bounce_kernel", "path_kernel"], cfg.index,
-                                              "dram_bytes_per_launch", TRACE_SOURCES)
-    inst, inst_file, inst_cur = ncu_capture(["first_bounce_kernel", "path_kernel"], cfg.index,
-                                            "warp_inst_per_launch", TRACE_SOURCES)
+    tr_traffic, tr_file, tr_cur = ncu_capture(TRACE_KERNELS, cfg.index, "dram_bytes_per_launch", TRACE_SOURCES)
+    inst, inst_file, inst_cur = ncu_capture(TRACE_KERNELS, cfg.index, "warp_inst_per_launch", TRACE_SOURCES)
     f_clk = (clocks.get("sm_mhz") or 1965.0) * 1e6
     peak_issue = 4 * torch.cuda.get_device_properties(local).multi_processor_count * f_clk
     issue = None
@@ -488,7 +488,7 @@ def main():
                                 "sampled during the timed region"}
     trace_roof = {"bound": "l2", "achieved": gbs, "peak": L2_READ_GBS, "unit": "GB/s", "frac": gbs / L2_READ_GBS,
                   "traffic": tr_traffic / 1.0 if tr_traffic else None, "traffic_file": tr_file,
-                  "traffic_current": tr_cur, "kernel": "first_bounce_kernel + path_kernel",
+                  "traffic_current": tr_cur, "kernel": " + ".join(TRACE_KERNELS),
                   "bytes_per_segment": bps, "per_segment": tc["per_segment"] if tc else None,
                   "counts_file": tc["file"] if tc else None, "counts_current": tc["current"] if tc else None,
                   "segments_per_wave": segs / waves, "launch_ms": ms_k / waves,

@@ -300,8 +300,8 @@ int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, i
         tm.begin(T_TRAVERSE, &e0);
         pt::launch_paths(tp, cam, W, H, (int)p0, (int)np, (int)w0, (int)slots, max_depth, seed, use_nif, env, ws, st);
         tm.end(T_TRAVERSE, e0);
-        stats.launches += max_depth > 1 ? 2 : 1;
-        stats.traverse_launches += max_depth > 1 ? 2 : 1;
+        stats.launches += pt::path_launches(max_depth);
+        stats.traverse_launches += pt::path_launches(max_depth);
         if (use_nif) {
             tm.begin(T_NIF, &e0);
             cudaError_t e = pt::launch_nif(nif, ws.esc, ws.esc_beta, ws.counters + pt::kCounterEsc, slots, ws.wave_buf, 1, st);

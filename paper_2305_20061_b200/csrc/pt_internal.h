@@ -155,6 +155,7 @@ struct TraceParams {
 // the rendered row range (p0 = row0 W)
 void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int p0, int np, int first_sample, int n_slots,
                   int max_depth, uint64_t seed, int use_nif, float3 env, Workspace& ws, cudaStream_t st);
+int path_launches(int max_depth);   // kernels launch_paths launches per wave
 void launch_accumulate(const float* wave_buf, int n_pix, int k, float* fb, const uint32_t* counters,
                        unsigned long long* stats, uint32_t paths, cudaStream_t st);
 void launch_primary(const TraceParams& tp, const Cam32& cam, int W, int H, int sample, uint64_t seed,

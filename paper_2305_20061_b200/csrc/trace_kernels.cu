@@ -923,14 +923,22 @@ __global__ void __launch_bounds__(128, PT_FB_MINB) first_bounce_kernel(ShadeArgs
 #ifndef PT_TRACE_WAKE
 #define PT_TRACE_WAKE 12
 #endif
+// PT_FUSED_PATHS=1: one kernel per wave -- lanes refill straight from the wave's camera slots (the S1
+// raygen of the refilled lanes only) and carry each path from its first segment to its end, so there is
+// no first-bounce pass and no alive queue (40 B written + 40 B read per surviving path)
+#ifndef PT_FUSED_PATHS
+#define PT_FUSED_PATHS 1
+#endif
+template <bool kFused>
 __global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
     pdl_wait();                       // first_bounce complete: its queue and counters are visible
     pdl_trigger();
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
-    // (escaped count, paths taken) word; the alive queue's length is final once first_bounce is done
+    // (escaped count, paths taken) word: taken counts alive-queue entries, or camera slots (fused); the
+    // alive queue's length is final once first_bounce is done
     unsigned long long* const qw = reinterpret_cast<unsigned long long*>(a.esc_count);
-    const int n_alive = (int)*a.alive_count;
+    const int n_alive = kFused ? 0 : (int)*a.alive_count;
     float4 cold[2];                   // local memory (ld/st.local asm): the ray's spilled constants
     uint2 stk[kStackSize];            // local memory: the traversal stack
     const uint32_t cold_a = (uint32_t)__cvta_generic_to_local(cold);
@@ -944,7 +952,17 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
     uint32_t segs = 0;
     // lanes without a path take queue entries r0 - 1 - (rank among them) while those are >= 0
     auto refill = [&](unsigned long long old, uint32_t mneed) {
-        if (!have) {
+        if (kFused && !have) {
+            // camera slots [taken, taken + popc(mneed)) for the free lanes, in lane order (coherent rays)
+            const uint32_t i = (uint32_t)(old >> 32) + (uint32_t)__popc(mneed & lt);
+            if (i < a.n_slots) {
+                slot = i;
+                bt = make_float3(1.0f, 1.0f, 1.0f);
+                depth = 1;
+                have = true;
+                trav_begin(tv, a.tp, make_float3(a.cam.eye[0], a.cam.eye[1], a.cam.eye[2]), camera_ray(a, i), cold_a);
+            }
+        } else if (!have) {
             const int idx = n_alive - 1 - (int)(uint32_t)(old >> 32) - __popc(mneed & lt);
             if (idx >= 0) {
                 const float4 qa = __ldg(a.qA + idx), qb = __ldg(a.qB + idx);
@@ -1162,7 +1180,7 @@ static int2 path_grids() {
     int a = g1[dev].load(std::memory_order_relaxed), b = g2[dev].load(std::memory_order_relaxed);
     if (a <= 0 || b <= 0) {
         a = resident_grid(first_bounce_kernel, 128);
-        b = resident_grid(path_kernel, 128);
+        b = resident_grid(path_kernel<PT_FUSED_PATHS != 0>, 128);
         g1[dev].store(a, std::memory_order_relaxed);
         g2[dev].store(b, std::memory_order_relaxed);
     }
@@ -1190,9 +1208,15 @@ void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int p0,
     a.esc = ws.esc; a.esc_beta = ws.esc_beta; a.wave_buf = ws.wave_buf;
     const int2 grids = path_grids();
     a.work = ws.counters + kCounterWork;
-    first_bounce_kernel<<<grids.x, 128, 0, st>>>(a);
-    if (max_depth > 1) launch_pdl(path_kernel, dim3(grids.y), dim3(128), 0, st, a);
+    if (PT_FUSED_PATHS) {
+        launch_pdl(path_kernel<true>, dim3(grids.y), dim3(128), 0, st, a);
+    } else {
+        first_bounce_kernel<<<grids.x, 128, 0, st>>>(a);
+        if (max_depth > 1) launch_pdl(path_kernel<false>, dim3(grids.y), dim3(128), 0, st, a);
+    }
 }
+
+int path_launches(int max_depth) { return PT_FUSED_PATHS ? 1 : (max_depth > 1 ? 2 : 1); }
 
 void launch_accumulate(const float* wave_buf, int n_pix, int k, float* fb, const uint32_t* counters,
                        unsigned long long* stats, uint32_t paths, cudaStream_t st) {
