@@ -42,7 +42,7 @@ L2_READ_GBS = 16409.6                       # tools/l2_bench.cu on this pool's B
 PROFILE_DIRS = [os.path.join(ROOT, "profiles", "round2"), os.path.join(ROOT, "profiles", "round1")]
 TRACE_SOURCES = ["paper_2305_20061_b200/csrc/trace_kernels.cu", "paper_2305_20061_b200/csrc/bvh_build.cpp",
                  "paper_2305_20061_b200/csrc/pt_internal.h"]
-TRACE_KERNELS = ["path_kernel"]          # one fused path kernel per wave (first_bounce_kernel only if unfused)
+TRACE_KERNELS = ["first_bounce_kernel", "path_kernel"]
 NIF_SOURCES = ["paper_2305_20061_b200/csrc/siren_kernel.cu", "paper_2305_20061_b200/csrc/tc_ptx.cuh"]
 
 

@@ -198,6 +198,7 @@ pt::TraceParams trace_params(const pt_scene* sc) {
     tp.empty = sc->empty ? 1 : 0;
     tp.mats = sc->d_mats;
     tp.n_tris = sc->n_tris;
+    tp.bvh_depth = (int)sc->bvh_depth;
     return tp;
 }
 

@@ -148,6 +148,7 @@ struct TraceParams {
     int empty;
     const DevMaterial* mats;
     int64_t n_tris;
+    int bvh_depth;       // 4-wide levels (chooses the path kernel variant)
 };
 
 // kernel launchers (trace_kernels.cu)

@@ -843,6 +843,15 @@ __device__ __forceinline__ float3 camera_ray(const ShadeArgs& a, uint32_t i) {
     return cam_dir(a.cam, a.W, a.H, (int)px, (int)py, u01f(r.x), u01f(r.y));
 }
 
+#ifndef PT_TRACE_WAKE
+#define PT_TRACE_WAKE 12
+#endif
+#ifndef PT_FB_REPLACE
+#define PT_FB_REPLACE 1          // the first bounce with dynamic replacement too (deep BVHs)
+#endif
+#ifndef PT_REPLACE_MIN_DEPTH
+#define PT_REPLACE_MIN_DEPTH 6   // BVH depth (4-wide levels) from which the replacement kernel runs
+#endif
 #ifndef PT_TS_MINB
 #define PT_TS_MINB 7   // min resident blocks per SM for the path kernels: 72-register cap; tools/ts_tune.sh
 #endif
@@ -862,6 +871,10 @@ __device__ __forceinline__ void write_radiance(const ShadeArgs& a, const SegOut&
 #ifndef PT_FB_MINB
 #define PT_FB_MINB PT_TS_MINB   // the first bounce's own register cap (tools/ts_tune.sh)
 #endif
+// kReplace (deep BVHs): the lanes' traversals are interrupted once PT_TRACE_WAKE lanes wait (as in
+// path_kernel); the waiting lanes shade, append and take the next camera slots (consecutive, so the
+// warp's rays stay coherent) while the others resume their traversal.
+template <bool kReplace>
 __global__ void __launch_bounds__(128, PT_FB_MINB) first_bounce_kernel(ShadeArgs a) {
     pdl_trigger();                    // all CTAs resident (grid = resident capacity): let path_kernel queue
     const uint32_t n = a.n_slots;
@@ -872,6 +885,78 @@ __global__ void __launch_bounds__(128, PT_FB_MINB) first_bounce_kernel(ShadeArgs
     // queue and fetches the next chunk of 32 slots
     unsigned long long* const ww = reinterpret_cast<unsigned long long*>(a.work);
     unsigned long long wo = 0;
+    if constexpr (kReplace) {
+        float4 cold[2];
+        uint2 stk[kStackSize];
+        const uint32_t cold_a = (uint32_t)__cvta_generic_to_local(cold);
+        const uint32_t stk_a = (uint32_t)__cvta_generic_to_local(stk);
+        const float3 eye = make_float3(a.cam.eye[0], a.cam.eye[1], a.cam.eye[2]);
+        Trav tv;
+        tv.tracing = false;
+        bool have = false, dry = false;
+        uint32_t i = 0;
+        // free lanes take slots base + (rank among them) while those are < n
+        auto refill = [&](uint32_t base, uint32_t mneed) {
+            if (!have) {
+                const uint32_t k = base + (uint32_t)__popc(mneed & lt);
+                if (k < n) {
+                    i = k;
+                    have = true;
+                    trav_begin(tv, a.tp, eye, camera_ray(a, i), cold_a);
+                }
+            }
+            if (__any_sync(0xFFFFFFFFu, !have)) dry = true;
+        };
+        if (lane == 0) wo = atomicAdd(ww, 32ull);
+        refill((uint32_t)__shfl_sync(0xFFFFFFFFu, wo, 0), 0xFFFFFFFFu);
+        for (;;) {
+            for (;;) {
+                const uint32_t tr = __ballot_sync(0xFFFFFFFFu, tv.tracing);
+                const uint32_t wake = __ballot_sync(0xFFFFFFFFu, have ? !tv.tracing : !dry);
+                if (tr == 0u || __popc(wake) >= PT_TRACE_WAKE) break;
+                if (tv.tracing) trav_round(a.tp, tv, stk_a);
+            }
+            SegOut r;
+            r.alive = r.escaped = false;
+            const bool ready = have && !tv.tracing;
+            if (ready) {
+                ++segs;
+                shade_hit(a, 1, i, eye, ray_dir(tv.r), make_float3(1.0f, 1.0f, 1.0f), tv.best, r);
+                write_radiance(a, r, i);
+                have = false;
+            }
+            const uint32_t ma = __ballot_sync(0xFFFFFFFFu, r.alive), me = __ballot_sync(0xFFFFFFFFu, r.escaped);
+            const uint32_t mneed = dry ? 0u : __ballot_sync(0xFFFFFFFFu, !have);
+            if ((ma | mneed) != 0u) {
+                const int leader = __ffs(ma | mneed) - 1;
+                if (lane == leader) wo = atomicAdd(ww, (unsigned long long)__popc(mneed) | ((unsigned long long)__popc(ma) << 32));
+                wo = __shfl_sync(0xFFFFFFFFu, wo, leader);
+            }
+            if (r.alive) {
+                const uint32_t pos = (uint32_t)(wo >> 32) + (uint32_t)__popc(ma & lt);
+                a.qA[pos] = make_float4(r.o.x, r.o.y, r.o.z, __uint_as_float(i));
+                a.qB[pos] = make_float4(r.d.x, r.d.y, r.d.z, r.beta.x);
+                a.qC[pos] = make_float2(r.beta.y, r.beta.z);
+            }
+            if (me != 0u) {
+                uint32_t eb = 0;
+                if (lane == __ffs(me) - 1) eb = atomicAdd(a.esc_count, (uint32_t)__popc(me));
+                eb = __shfl_sync(0xFFFFFFFFu, eb, __ffs(me) - 1);
+                if (r.escaped) {
+                    const uint32_t pos = eb + (uint32_t)__popc(me & lt);
+                    a.esc[pos] = make_float4(r.d.x, r.d.y, r.d.z, __uint_as_float(i));
+                    a.esc_beta[pos] = make_float4(r.beta.x, r.beta.y, r.beta.z, 0.0f);
+                }
+            }
+            if (mneed) refill((uint32_t)wo, mneed);
+            if (!__any_sync(0xFFFFFFFFu, have)) break;
+        }
+#pragma unroll
+        for (int k = 16; k > 0; k >>= 1) segs += __shfl_xor_sync(0xFFFFFFFFu, segs, k);
+        if (lane == 0) atomicAdd(a.seg_count, segs);
+        TAIL_STAMP(0);
+        return;
+    }
     if (lane == 0) wo = atomicAdd(ww, 32ull);
     uint32_t base = (uint32_t)__shfl_sync(0xFFFFFFFFu, wo, 0);
     while (base < n) {
@@ -914,113 +999,152 @@ __global__ void __launch_bounds__(128, PT_FB_MINB) first_bounce_kernel(ShadeArgs
 // Bounces 2.. (persistent): every lane carries one path from the first bounce's queue to its end,
 // and a lane whose path ends refills from the queue (one 64-bit atomic per warp iteration for all of the
 // warp's free lanes), so the warps stay full without a launch, a barrier or a state round trip through
-// HBM per bounce. Traversal with dynamic replacement (Aila & Laine 2009): a lane's traversal state
-// survives across rounds, and the warp interrupts its traversal rounds as soon as PT_TRACE_WAKE lanes are
-// waiting (traversal finished, or no path while the queue still has some) to shade those segments and
-// start the next ones -- so lanes with short traversals do not idle behind the warp's longest one.
-// Per-path results do not depend on the schedule: the RNG is keyed by (pixel, sample, depth) and every
-// path writes only its own slot.
-#ifndef PT_TRACE_WAKE
-#define PT_TRACE_WAKE 12
-#endif
-// PT_FUSED_PATHS=1: one kernel per wave -- lanes refill straight from the wave's camera slots (the S1
-// raygen of the refilled lanes only) and carry each path from its first segment to its end, so there is
-// no first-bounce pass and no alive queue (40 B written + 40 B read per surviving path)
-#ifndef PT_FUSED_PATHS
-#define PT_FUSED_PATHS 1
-#endif
-template <bool kFused>
+// HBM per bounce. Per-path results do not depend on the schedule: the RNG is keyed by (pixel, sample,
+// depth) and every path writes only its own slot.
+// kReplace (deep BVHs, launch_paths): traversal with dynamic replacement (Aila & Laine 2009) -- a lane's
+// traversal state survives across rounds, and the warp interrupts its traversal rounds as soon as
+// PT_TRACE_WAKE lanes are waiting (traversal finished, or no path while the queue still has some) to
+// shade those segments and start the next ones, so lanes with short traversals do not idle behind the
+// warp's longest one. Without it every warp iteration runs one whole closest-hit per lane (cheaper where
+// traversals are short: configs 0-2).
+template <bool kReplace>
 __global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
     pdl_wait();                       // first_bounce complete: its queue and counters are visible
     pdl_trigger();
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
-    // (escaped count, paths taken) word: taken counts alive-queue entries, or camera slots (fused); the
-    // alive queue's length is final once first_bounce is done
+    // (escaped count, paths taken) word; the alive queue's length is final once first_bounce is done
     unsigned long long* const qw = reinterpret_cast<unsigned long long*>(a.esc_count);
-    const int n_alive = kFused ? 0 : (int)*a.alive_count;
-    float4 cold[2];                   // local memory (ld/st.local asm): the ray's spilled constants
-    uint2 stk[kStackSize];            // local memory: the traversal stack
-    const uint32_t cold_a = (uint32_t)__cvta_generic_to_local(cold);
-    const uint32_t stk_a = (uint32_t)__cvta_generic_to_local(stk);
+    const int n_alive = (int)*a.alive_count;
     bool have = false, dry = false;
     uint32_t slot = 0;
     int depth = 0;
     float3 bt = make_float3(1, 1, 1);
-    Trav tv;
-    tv.tracing = false;
     uint32_t segs = 0;
-    // lanes without a path take queue entries r0 - 1 - (rank among them) while those are >= 0
-    auto refill = [&](unsigned long long old, uint32_t mneed) {
-        if (kFused && !have) {
-            // camera slots [taken, taken + popc(mneed)) for the free lanes, in lane order (coherent rays)
-            const uint32_t i = (uint32_t)(old >> 32) + (uint32_t)__popc(mneed & lt);
-            if (i < a.n_slots) {
-                slot = i;
-                bt = make_float3(1.0f, 1.0f, 1.0f);
-                depth = 1;
-                have = true;
-                trav_begin(tv, a.tp, make_float3(a.cam.eye[0], a.cam.eye[1], a.cam.eye[2]), camera_ray(a, i), cold_a);
+    if constexpr (kReplace) {
+        float4 cold[2];                   // local memory (ld/st.local asm): the ray's spilled constants
+        uint2 stk[kStackSize];            // local memory: the traversal stack
+        const uint32_t cold_a = (uint32_t)__cvta_generic_to_local(cold);
+        const uint32_t stk_a = (uint32_t)__cvta_generic_to_local(stk);
+        Trav tv;
+        tv.tracing = false;
+        // lanes without a path take queue entries r0 - 1 - (rank among them) while those are >= 0
+        auto refill = [&](unsigned long long old, uint32_t mneed) {
+            if (!have) {
+                const int idx = n_alive - 1 - (int)(uint32_t)(old >> 32) - __popc(mneed & lt);
+                if (idx >= 0) {
+                    const float4 qa = __ldg(a.qA + idx), qb = __ldg(a.qB + idx);
+                    const float2 qc = __ldg(a.qC + idx);
+                    slot = __float_as_uint(qa.w);
+                    bt = make_float3(qb.w, qc.x, qc.y);
+                    depth = 2;
+                    have = true;
+                    trav_begin(tv, a.tp, make_float3(qa.x, qa.y, qa.z), make_float3(qb.x, qb.y, qb.z), cold_a);
+                }
             }
-        } else if (!have) {
-            const int idx = n_alive - 1 - (int)(uint32_t)(old >> 32) - __popc(mneed & lt);
-            if (idx >= 0) {
-                const float4 qa = __ldg(a.qA + idx), qb = __ldg(a.qB + idx);
-                const float2 qc = __ldg(a.qC + idx);
-                slot = __float_as_uint(qa.w);
-                bt = make_float3(qb.w, qc.x, qc.y);
-                depth = 2;
-                have = true;
-                trav_begin(tv, a.tp, make_float3(qa.x, qa.y, qa.z), make_float3(qb.x, qb.y, qb.z), cold_a);
-            }
-        }
-        if (__any_sync(0xFFFFFFFFu, !have)) dry = true;   // the queue ran out (taken only grows)
-    };
-    {
-        unsigned long long old = 0;
-        if (lane == 0) old = atomicAdd(qw, 32ull << 32);
-        refill(__shfl_sync(0xFFFFFFFFu, old, 0), 0xFFFFFFFFu);
-    }
-    for (;;) {
-        // traversal rounds until enough lanes wait (or none traces)
-        for (;;) {
-            const uint32_t tr = __ballot_sync(0xFFFFFFFFu, tv.tracing);
-            const uint32_t wake = __ballot_sync(0xFFFFFFFFu, have ? !tv.tracing : !dry);
-            if (tr == 0u || __popc(wake) >= PT_TRACE_WAKE) break;
-            if (tv.tracing) trav_round(a.tp, tv, stk_a);
-        }
-        SegOut r;
-        r.escaped = false;
-        if (have && !tv.tracing) {
-            ++segs;
-            shade_hit(a, depth, slot, make_float3(tv.r.o[0], tv.r.o[1], tv.r.o[2]), ray_dir(tv.r), bt, tv.best, r);
-            write_radiance(a, r, slot);
-            if (r.alive) {
-                bt = r.beta;
-                ++depth;
-                trav_begin(tv, a.tp, r.o, r.d, cold_a);
-            } else {
-                have = false;
-            }
-        }
-        // one 64-bit atomic per warp iteration: append this iteration's escapes (low word) and take
-        // new paths for the free lanes (high word) while the queue has some
-        const uint32_t me = __ballot_sync(0xFFFFFFFFu, r.escaped);
-        const uint32_t mneed = dry ? 0u : __ballot_sync(0xFFFFFFFFu, !have);
-        if ((me | mneed) != 0u) {
-            const int leader = __ffs(me | mneed) - 1;
+            if (__any_sync(0xFFFFFFFFu, !have)) dry = true;   // the queue ran out (taken only grows)
+        };
+        {
             unsigned long long old = 0;
-            if (lane == leader)
-                old = atomicAdd(qw, ((unsigned long long)__popc(mneed) << 32) + (unsigned long long)__popc(me));
-            old = __shfl_sync(0xFFFFFFFFu, old, leader);
-            if (r.escaped) {
-                const uint32_t pos = (uint32_t)old + (uint32_t)__popc(me & lt);
-                a.esc[pos] = make_float4(r.d.x, r.d.y, r.d.z, __uint_as_float(slot));
-                a.esc_beta[pos] = make_float4(r.beta.x, r.beta.y, r.beta.z, 0.0f);
-            }
-            if (mneed) refill(old, mneed);
+            if (lane == 0) old = atomicAdd(qw, 32ull << 32);
+            refill(__shfl_sync(0xFFFFFFFFu, old, 0), 0xFFFFFFFFu);
         }
-        if (!__any_sync(0xFFFFFFFFu, have)) break;
+        for (;;) {
+            // traversal rounds until enough lanes wait (or none traces)
+            for (;;) {
+                const uint32_t tr = __ballot_sync(0xFFFFFFFFu, tv.tracing);
+                const uint32_t wake = __ballot_sync(0xFFFFFFFFu, have ? !tv.tracing : !dry);
+                if (tr == 0u || __popc(wake) >= PT_TRACE_WAKE) break;
+                if (tv.tracing) trav_round(a.tp, tv, stk_a);
+            }
+            SegOut r;
+            r.escaped = false;
+            if (have && !tv.tracing) {
+                ++segs;
+                shade_hit(a, depth, slot, make_float3(tv.r.o[0], tv.r.o[1], tv.r.o[2]), ray_dir(tv.r), bt, tv.best, r);
+                write_radiance(a, r, slot);
+                if (r.alive) {
+                    bt = r.beta;
+                    ++depth;
+                    trav_begin(tv, a.tp, r.o, r.d, cold_a);
+                } else {
+                    have = false;
+                }
+            }
+            // one 64-bit atomic per warp iteration: append this iteration's escapes (low word) and take
+            // new paths for the free lanes (high word) while the queue has some
+            const uint32_t me = __ballot_sync(0xFFFFFFFFu, r.escaped);
+            const uint32_t mneed = dry ? 0u : __ballot_sync(0xFFFFFFFFu, !have);
+            if ((me | mneed) != 0u) {
+                const int leader = __ffs(me | mneed) - 1;
+                unsigned long long old = 0;
+                if (lane == leader)
+                    old = atomicAdd(qw, ((unsigned long long)__popc(mneed) << 32) + (unsigned long long)__popc(me));
+                old = __shfl_sync(0xFFFFFFFFu, old, leader);
+                if (r.escaped) {
+                    const uint32_t pos = (uint32_t)old + (uint32_t)__popc(me & lt);
+                    a.esc[pos] = make_float4(r.d.x, r.d.y, r.d.z, __uint_as_float(slot));
+                    a.esc_beta[pos] = make_float4(r.beta.x, r.beta.y, r.beta.z, 0.0f);
+                }
+                if (mneed) refill(old, mneed);
+            }
+            if (!__any_sync(0xFFFFFFFFu, have)) break;
+        }
+    } else {
+        float3 o = make_float3(0, 0, 0), d = make_float3(0, 0, 1);
+        auto refill = [&](unsigned long long old, uint32_t mneed) {
+            if (!have) {
+                const int idx = n_alive - 1 - (int)(uint32_t)(old >> 32) - __popc(mneed & lt);
+                if (idx >= 0) {
+                    const float4 qa = __ldg(a.qA + idx), qb = __ldg(a.qB + idx);
+                    const float2 qc = __ldg(a.qC + idx);
+                    o = make_float3(qa.x, qa.y, qa.z);
+                    slot = __float_as_uint(qa.w);
+                    d = make_float3(qb.x, qb.y, qb.z);
+                    bt = make_float3(qb.w, qc.x, qc.y);
+                    depth = 2;
+                    have = true;
+                }
+            }
+        };
+        {
+            unsigned long long old = 0;
+            if (lane == 0) old = atomicAdd(qw, 32ull << 32);
+            refill(__shfl_sync(0xFFFFFFFFu, old, 0), 0xFFFFFFFFu);
+        }
+        for (;;) {
+            if (!__any_sync(0xFFFFFFFFu, have)) break;
+            SegOut r;
+            r.escaped = false;
+            if (have) {
+                ++segs;
+                shade_segment(a, depth, slot, o, d, bt, r);
+                write_radiance(a, r, slot);
+                if (r.alive) {
+                    o = r.o;
+                    d = r.d;
+                    bt = r.beta;
+                    ++depth;
+                } else {
+                    have = false;
+                }
+            }
+            const uint32_t me = __ballot_sync(0xFFFFFFFFu, r.escaped);
+            const uint32_t mneed = __ballot_sync(0xFFFFFFFFu, !have);
+            if ((me | mneed) != 0u) {
+                const int leader = __ffs(me | mneed) - 1;
+                unsigned long long old = 0;
+                if (lane == leader)
+                    old = atomicAdd(qw, ((unsigned long long)__popc(mneed) << 32) + (unsigned long long)__popc(me));
+                old = __shfl_sync(0xFFFFFFFFu, old, leader);
+                if (r.escaped) {
+                    const uint32_t pos = (uint32_t)old + (uint32_t)__popc(me & lt);
+                    a.esc[pos] = make_float4(r.d.x, r.d.y, r.d.z, __uint_as_float(slot));
+                    a.esc_beta[pos] = make_float4(r.beta.x, r.beta.y, r.beta.z, 0.0f);
+                }
+                refill(old, mneed);
+            }
+        }
     }
 #pragma unroll
     for (int k = 16; k > 0; k >>= 1) segs += __shfl_xor_sync(0xFFFFFFFFu, segs, k);
@@ -1174,17 +1298,20 @@ static int resident_grid(K kernel, int block) {
 }
 
 // resident grids of the two path kernels, per device (occupancy and SM count are per-device properties)
-static int2 path_grids() {
-    static std::atomic<int> g1[64], g2[64];
+static int3 path_grids() {
+    static std::atomic<int> g1[64], g2[64], g3[64];
     const int dev = current_device();
-    int a = g1[dev].load(std::memory_order_relaxed), b = g2[dev].load(std::memory_order_relaxed);
-    if (a <= 0 || b <= 0) {
-        a = resident_grid(first_bounce_kernel, 128);
-        b = resident_grid(path_kernel<PT_FUSED_PATHS != 0>, 128);
+    int a = g1[dev].load(std::memory_order_relaxed), b = g2[dev].load(std::memory_order_relaxed),
+        c = g3[dev].load(std::memory_order_relaxed);
+    if (a <= 0 || b <= 0 || c <= 0) {
+        a = resident_grid(first_bounce_kernel<false>, 128);   // (same occupancy with kReplace: 72-register cap)
+        b = resident_grid(path_kernel<false>, 128);
+        c = resident_grid(path_kernel<true>, 128);
         g1[dev].store(a, std::memory_order_relaxed);
         g2[dev].store(b, std::memory_order_relaxed);
+        g3[dev].store(c, std::memory_order_relaxed);
     }
-    return make_int2(a, b);
+    return make_int3(a, b, c);
 }
 
 void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int p0, int np, int first_sample, int n_slots,
@@ -1206,17 +1333,18 @@ void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int p0,
     a.use_nif = use_nif; a.env = env;
     a.qA = ws.rayA[0]; a.qB = ws.rayB[0]; a.qC = ws.rayC[0];
     a.esc = ws.esc; a.esc_beta = ws.esc_beta; a.wave_buf = ws.wave_buf;
-    const int2 grids = path_grids();
+    const int3 grids = path_grids();
     a.work = ws.counters + kCounterWork;
-    if (PT_FUSED_PATHS) {
-        launch_pdl(path_kernel<true>, dim3(grids.y), dim3(128), 0, st, a);
-    } else {
-        first_bounce_kernel<<<grids.x, 128, 0, st>>>(a);
-        if (max_depth > 1) launch_pdl(path_kernel<false>, dim3(grids.y), dim3(128), 0, st, a);
+    const bool replace = tp.bvh_depth >= PT_REPLACE_MIN_DEPTH;
+    if (replace && PT_FB_REPLACE) first_bounce_kernel<true><<<grids.x, 128, 0, st>>>(a);
+    else first_bounce_kernel<false><<<grids.x, 128, 0, st>>>(a);
+    if (max_depth > 1) {
+        if (replace) launch_pdl(path_kernel<true>, dim3(grids.z), dim3(128), 0, st, a);
+        else launch_pdl(path_kernel<false>, dim3(grids.y), dim3(128), 0, st, a);
     }
 }
 
-int path_launches(int max_depth) { return PT_FUSED_PATHS ? 1 : (max_depth > 1 ? 2 : 1); }
+int path_launches(int max_depth) { return max_depth > 1 ? 2 : 1; }
 
 void launch_accumulate(const float* wave_buf, int n_pix, int k, float* fb, const uint32_t* counters,
                        unsigned long long* stats, uint32_t paths, cudaStream_t st) {
