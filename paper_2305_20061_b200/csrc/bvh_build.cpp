@@ -123,7 +123,10 @@ struct Builder {
     int busy = 0;
     bool done = false;
     static constexpr int64_t kGrain = 2048;   // subtrees larger than this may move to another worker
-    static constexpr int NB = 16;
+    static constexpr int NB = 32;   // max bins (nb <= NB used)
+    int nb = 16;                    // SAH bins (PT_BVH_BINS)
+    double trav_cost = 1.5;         // node-traversal cost in primitive tests (PT_BVH_NODE_COST)
+    int max_leaf = kMaxLeafPrims;   // leaf size cap (PT_BVH_MAX_LEAF, <= 4)
 
     void build(int threads) {
         const int64_t n = (int64_t)refs.size();
@@ -280,13 +283,13 @@ struct Builder {
         if (cnt_all > 1 && ext > 0.0f) {
             int64_t cnt[NB] = {0};
             Box bins[NB], cbins[NB];
-            for (int k = 0; k < NB; ++k) { bins[k].empty(); cbins[k].empty(); }
-            const float scale = (float)(NB / (double)ext);
+            for (int k = 0; k < nb; ++k) { bins[k].empty(); cbins[k].empty(); }
+            const float scale = (float)(nb / (double)ext);
             const float c0 = it.cb.lo[axis];
             auto bin_of = [&](const Ref& r) {
                 const float c = 0.5f * (r.b.lo[axis] + r.b.hi[axis]);
                 const int k = (int)((c - c0) * scale);
-                return std::min(NB - 1, std::max(0, k));
+                return std::min(nb - 1, std::max(0, k));
             };
             for (int64_t i = 0; i < cnt_all; ++i) {
                 const Ref& r = r0[i];
@@ -302,7 +305,7 @@ struct Builder {
             Box acc;
             acc.empty();
             int64_t c = 0;
-            for (int k = NB - 1; k >= 1; --k) {
+            for (int k = nb - 1; k >= 1; --k) {
                 acc.grow(bins[k]);
                 c += cnt[k];
                 rarea[k] = acc.area();
@@ -312,26 +315,26 @@ struct Builder {
             int best_k = -1;
             acc.empty();
             c = 0;
-            for (int k = 0; k < NB - 1; ++k) {
+            for (int k = 0; k < nb - 1; ++k) {
                 acc.grow(bins[k]);
                 c += cnt[k];
                 if (c == 0 || rcnt[k + 1] == 0) continue;
                 const double cost = acc.area() * (double)c + rarea[k + 1] * (double)rcnt[k + 1];
                 if (cost < best) { best = cost; best_k = k; }
             }
-            constexpr double kTraversalCost = 1.5;
+            const double kTraversalCost = trav_cost;
             const double leaf_cost = it.bb.area() * (double)cnt_all;
             best += kTraversalCost * it.bb.area();
-            if (best_k >= 0 && (best < leaf_cost || cnt_all > kMaxLeafPrims)) {
+            if (best_k >= 0 && (best < leaf_cost || cnt_all > max_leaf)) {
                 Ref* mid = std::partition(r0, r0 + cnt_all, [&](const Ref& r) { return bin_of(r) <= best_k; });
                 split = it.first + (mid - r0);
                 lb.empty(); lcb.empty(); rb.empty(); rcb.empty();
-                for (int k = 0; k < NB; ++k) {
+                for (int k = 0; k < nb; ++k) {
                     if (k <= best_k) { lb.grow(bins[k]); lcb.grow(cbins[k]); }
                     else { rb.grow(bins[k]); rcb.grow(cbins[k]); }
                 }
             }
-        } else if (cnt_all > kMaxLeafPrims) {
+        } else if (cnt_all > max_leaf) {
             split = it.first + cnt_all / 2;   // coincident centroids
             lb.empty(); lcb.empty(); rb.empty(); rcb.empty();
             for (int64_t i = 0; i < cnt_all; ++i) {
@@ -453,6 +456,10 @@ int build_wide_bvh(const pt_triangle* tris, int64_t n_tris, const pt_sphere* sph
     };
     if (n >= (1ll << 30)) { *msg = "too many primitives for the BVH builder (< 2^30)"; return PT_ERR_INVALID_ARG; }
     Builder B;
+    // tuning knobs (experiments; defaults = the measured configuration)
+    if (const char* e = std::getenv("PT_BVH_BINS")) B.nb = std::max(2, std::min(Builder::NB, std::atoi(e)));
+    if (const char* e = std::getenv("PT_BVH_NODE_COST")) B.trav_cost = std::atof(e);
+    if (const char* e = std::getenv("PT_BVH_MAX_LEAF")) B.max_leaf = std::max(1, std::min(kMaxLeafPrims, std::atoi(e)));
     B.refs.resize(n);
     parallel_for(threads, n, [&](int64_t i) {
         Ref& r = B.refs[i];
