@@ -2,7 +2,8 @@
 //
 // The paper builds a BVH-2 on the host (Embree), compacts it into pointer-less nodes whose first
 // child is implicit, and stores box extents in fp16 with "round-to-nearest-not-lower" so no
-// intersection can be missed. Here: a binned-SAH BVH-2 (16 bins, leaves <= 4 primitives) is collapsed
+// intersection can be missed. Here: a binned-SAH BVH-2 (32 bins, node cost 1 primitive test, leaves <= 2
+// primitives; the node format holds up to 4) is collapsed
 // into 4-wide nodes (largest-area interior child expanded first), children are stored contiguously
 // behind one base index, leaf primitives are stored inline, and each child box is quantised to fp16
 // offsets from the node origin -- lo rounded down, hi rounded up, then corrected until the exact fp32
@@ -124,9 +125,11 @@ struct Builder {
     bool done = false;
     static constexpr int64_t kGrain = 2048;   // subtrees larger than this may move to another worker
     static constexpr int NB = 32;   // max bins (nb <= NB used)
-    int nb = 16;                    // SAH bins (PT_BVH_BINS)
-    double trav_cost = 1.5;         // node-traversal cost in primitive tests (PT_BVH_NODE_COST)
-    int max_leaf = kMaxLeafPrims;   // leaf size cap (PT_BVH_MAX_LEAF, <= 4)
+    // measured on configs 2-4 (profiles/round2/bvhparams_*.log): 32 bins, node cost 1.0 and leaves of at
+    // most 2 primitives beat round 1's 16 / 1.5 / 4 by 1-3.5 % samples/s
+    int nb = 32;                    // SAH bins (PT_BVH_BINS)
+    double trav_cost = 1.0;         // node-traversal cost in primitive tests (PT_BVH_NODE_COST)
+    int max_leaf = 2;               // leaf size cap (PT_BVH_MAX_LEAF, <= kMaxLeafPrims)
 
     void build(int threads) {
         const int64_t n = (int64_t)refs.size();
