@@ -688,6 +688,8 @@ struct ShadeArgs {
     float inv_np, inv_w;        // 1 / np, 1 / W for udiv_exact
     int np;                     // pixels of the rendered row range (W x rows)
     uint32_t p0;                // its first pixel (row0 W): slot i = (pixel p0 + i % np, sample first + i / np)
+    uint32_t tiles_x;           // > 0: the first bounce visits the slots in 8 x 4 pixel tiles (W % 8 == 0, rows % 4 == 0)
+    float inv_tiles_x;
     uint2 key;
     const uint32_t* counters;   // the wave's counters (pt_internal.h kCounters layout)
     uint32_t n_slots;           // paths of the wave
@@ -833,6 +835,18 @@ __device__ __forceinline__ void shade_segment(const ShadeArgs& a, int depth, uin
     shade_hit(a, depth, slot, o, d, bt, hh, r);
 }
 
+// The first bounce's visiting order: work index w -> slot, 32 consecutive w = one 8 x 4 pixel tile of one
+// sample (row-major tiles), so a warp's camera rays form a compact bundle (when the row range tiles
+// evenly; otherwise the identity). Slots keep their meaning (pixel-major), so nothing downstream changes.
+__device__ __forceinline__ uint32_t tile_slot(const ShadeArgs& a, uint32_t w) {
+    if (a.tiles_x == 0u) return w;
+    uint32_t q, tx;
+    const uint32_t s = udiv_exact(w, (uint32_t)a.np, a.inv_np, q);
+    const uint32_t t = q >> 5, k = q & 31u;
+    const uint32_t ty = udiv_exact(t, a.tiles_x, a.inv_tiles_x, tx);
+    return s * (uint32_t)a.np + (4u * ty + (k >> 3)) * (uint32_t)a.W + 8u * tx + (k & 7u);
+}
+
 // The camera ray of wave slot i = (pixel p0 + i % np, sample first + i / np) (S1, reading R22)
 __device__ __forceinline__ float3 camera_ray(const ShadeArgs& a, uint32_t i) {
     uint32_t pu, px;
@@ -848,6 +862,9 @@ __device__ __forceinline__ float3 camera_ray(const ShadeArgs& a, uint32_t i) {
 #endif
 #ifndef PT_REPLACE_MIN_DEPTH
 #define PT_REPLACE_MIN_DEPTH 6   // BVH depth (4-wide levels) from which the replacement kernel runs
+#endif
+#ifndef PT_TILE_ORDER
+#define PT_TILE_ORDER 1          // first-bounce slots in 8 x 4 pixel tiles (tile_slot)
 #endif
 #ifndef PT_TS_MINB
 #define PT_TS_MINB 7   // min resident blocks per SM for the path kernels: 72-register cap; tools/ts_tune.sh
@@ -881,10 +898,11 @@ __global__ void __launch_bounds__(128, PT_FB_MINB) first_bounce_kernel(ShadeArgs
     if (lane == 0) wo = atomicAdd(ww, 32ull);
     uint32_t base = (uint32_t)__shfl_sync(0xFFFFFFFFu, wo, 0);
     while (base < n) {
-        const uint32_t i = base + (uint32_t)lane;
+        const uint32_t w = base + (uint32_t)lane;
+        const uint32_t i = w < n ? tile_slot(a, w) : w;
         SegOut r;
         r.alive = r.escaped = false;
-        if (i < n) {
+        if (w < n) {
             ++segs;
             const float3 eye = make_float3(a.cam.eye[0], a.cam.eye[1], a.cam.eye[2]);
             shade_segment(a, 1, i, eye, camera_ray(a, i), make_float3(1.0f, 1.0f, 1.0f), r);
@@ -1245,6 +1263,8 @@ void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int p0,
     a.np = np;
     a.p0 = (uint32_t)p0;
     a.inv_np = 1.0f / (float)np;
+    a.tiles_x = (PT_TILE_ORDER && W % 8 == 0 && (np / W) % 4 == 0) ? (uint32_t)(W / 8) : 0u;
+    a.inv_tiles_x = a.tiles_x ? 1.0f / (float)a.tiles_x : 0.0f;
     a.inv_w = 1.0f / (float)W;
     a.key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
     a.counters = ws.counters;
