@@ -836,15 +836,20 @@ __device__ __forceinline__ void shade_segment(const ShadeArgs& a, int depth, uin
 }
 
 // The first bounce's visiting order: work index w -> slot, 32 consecutive w = one 8 x 4 pixel tile of one
+// sample (PT_TILE_W x 32 / PT_TILE_W; config 3: 2.60 -> 2.78 G samples/s, profiles/round2/tile_order.log)
 // sample (row-major tiles), so a warp's camera rays form a compact bundle (when the row range tiles
 // evenly; otherwise the identity). Slots keep their meaning (pixel-major), so nothing downstream changes.
+#ifndef PT_TILE_W
+#define PT_TILE_W 8              // tile width in pixels (height 32 / PT_TILE_W)
+#endif
+constexpr uint32_t kTileW = PT_TILE_W, kTileH = 32 / PT_TILE_W;
 __device__ __forceinline__ uint32_t tile_slot(const ShadeArgs& a, uint32_t w) {
     if (a.tiles_x == 0u) return w;
     uint32_t q, tx;
     const uint32_t s = udiv_exact(w, (uint32_t)a.np, a.inv_np, q);
     const uint32_t t = q >> 5, k = q & 31u;
     const uint32_t ty = udiv_exact(t, a.tiles_x, a.inv_tiles_x, tx);
-    return s * (uint32_t)a.np + (4u * ty + (k >> 3)) * (uint32_t)a.W + 8u * tx + (k & 7u);
+    return s * (uint32_t)a.np + (kTileH * ty + k / kTileW) * (uint32_t)a.W + kTileW * tx + (k % kTileW);
 }
 
 // The camera ray of wave slot i = (pixel p0 + i % np, sample first + i / np) (S1, reading R22)
@@ -1263,7 +1268,7 @@ void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int p0,
     a.np = np;
     a.p0 = (uint32_t)p0;
     a.inv_np = 1.0f / (float)np;
-    a.tiles_x = (PT_TILE_ORDER && W % 8 == 0 && (np / W) % 4 == 0) ? (uint32_t)(W / 8) : 0u;
+    a.tiles_x = (PT_TILE_ORDER && W % kTileW == 0 && (np / W) % kTileH == 0) ? (uint32_t)(W / kTileW) : 0u;
     a.inv_tiles_x = a.tiles_x ? 1.0f / (float)a.tiles_x : 0.0f;
     a.inv_w = 1.0f / (float)W;
     a.key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
