@@ -64,11 +64,19 @@ __device__ __forceinline__ float3 cam_dir(const Cam32& k, int W, int H, int x, i
 // ---------------------------------------------------------------------------------------------
 // Kept compact (14 registers) because it is live through the whole traversal under the path kernels'
 // 72-register cap; the shear matrix of the certified pre-test is rebuilt inside each triangle test.
+// PT_RAY_LOCAL=1: the origin and the slab reciprocals also live in the local-memory record (two 16-B
+// loads per node visit instead of registers the 72-register cap spills anyway)
+#ifndef PT_RAY_LOCAL
+#define PT_RAY_LOCAL 1
+#endif
+constexpr int kColdBytes = PT_RAY_LOCAL ? 64 : 32;
 struct RayT {
+#if !PT_RAY_LOCAL
     float o[3], inv[3];         // slab test
+#endif
     uint32_t kbits;             // kx | ky << 2 | kz << 4 | negmask << 8 (bit a: d[a] has its sign bit set)
-    uint32_t cold;              // local-memory address of (Sx, Sy, rz, |d[kz]|) (d.x, d.y, d.z, 0): only
-                                // primitive tests read them, so they are spilled by hand, not by ptxas
+    uint32_t cold;              // local-memory address of (Sx, Sy, rz, |d[kz]|) (d.x, d.y, d.z, 0) [(o, 0)
+                                // (inv, 0)]: spilled by hand, not by ptxas
 };
 __device__ __forceinline__ float4 ldl4(uint32_t a) {
     float4 v;
@@ -79,6 +87,22 @@ __device__ __forceinline__ void stl4(uint32_t a, float4 v) {
     asm volatile("st.local.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
 __device__ __forceinline__ float4 ray_shear_consts(const RayT& r) { return ldl4(r.cold); }   // Sx, Sy, rz, |d[kz]|
+__device__ __forceinline__ float3 ray_o(const RayT& r) {
+#if PT_RAY_LOCAL
+    const float4 v = ldl4(r.cold + 32);
+    return make_float3(v.x, v.y, v.z);
+#else
+    return make_float3(r.o[0], r.o[1], r.o[2]);
+#endif
+}
+__device__ __forceinline__ float3 ray_inv(const RayT& r) {
+#if PT_RAY_LOCAL
+    const float4 v = ldl4(r.cold + 48);
+    return make_float3(v.x, v.y, v.z);
+#else
+    return make_float3(r.inv[0], r.inv[1], r.inv[2]);
+#endif
+}
 __device__ __forceinline__ float3 ray_dir(const RayT& r) {
     const float4 v = ldl4(r.cold + 16);
     return make_float3(v.x, v.y, v.z);
@@ -152,9 +176,14 @@ __device__ __forceinline__ void ray_prepare(float3 o, float3 d, RayT& r, uint32_
     r.cold = cold;
     stl4(cold, make_float4(self3(d, kx) * rz, self3(d, ky) * rz, rz, fabsf(dkz)));
     stl4(cold + 16, make_float4(d.x, d.y, d.z, 0.0f));
-    r.o[0] = o.x; r.o[1] = o.y; r.o[2] = o.z;
     // slab reciprocals: the SFU approximation (<= 1 ulp); the slab bound below allows for its rounding
+#if PT_RAY_LOCAL
+    stl4(cold + 32, make_float4(o.x, o.y, o.z, 0.0f));
+    stl4(cold + 48, make_float4(rcp_approx(d.x), rcp_approx(d.y), rcp_approx(d.z), 0.0f));
+#else
+    r.o[0] = o.x; r.o[1] = o.y; r.o[2] = o.z;
     r.inv[0] = rcp_approx(d.x); r.inv[1] = rcp_approx(d.y); r.inv[2] = rcp_approx(d.z);
+#endif
     const uint32_t negmask = (signbit(d.x) ? 1u : 0u) | (signbit(d.y) ? 2u : 0u) | (signbit(d.z) ? 4u : 0u);
     r.kbits = (uint32_t)kx | ((uint32_t)ky << 2) | ((uint32_t)kz << 4) | (negmask << 8);
 }
@@ -172,9 +201,9 @@ __device__ __forceinline__ Shear64 shear64(const RayT& r) {
 // Shear one vertex into the ray's frame: D = v - o (world axes, one rounding each), then the products
 // with the 0/1/-S entries of the shear rows; at most two roundings per sheared coordinate (the -S
 // product and the sum), the same single-rounding Sz D[kz] for Az as the permuted form.
-__device__ __forceinline__ void shear_vertex(const RayT& r, const Shear32& m, float3 v, float& x, float& y, float& z) {
-    const float2 dxy = __fadd2_rn(make_float2(v.x, v.y), make_float2(-r.o[0], -r.o[1]));
-    const float dz = v.z - r.o[2];
+__device__ __forceinline__ void shear_vertex(float3 ro, const Shear32& m, float3 v, float& x, float& y, float& z) {
+    const float2 dxy = __fadd2_rn(make_float2(v.x, v.y), make_float2(-ro.x, -ro.y));
+    const float dz = v.z - ro.z;
     float2 a = __fmul2_rn(m.mxy[0], make_float2(dxy.x, dxy.x));
     a = __ffma2_rn(m.mxy[1], make_float2(dxy.y, dxy.y), a);
     a = __ffma2_rn(m.mxy[2], make_float2(dz, dz), a);
@@ -199,9 +228,10 @@ __device__ __forceinline__ int tri_test32(const RayT& r, float3 v0, float3 v1, f
     float Ax, Ay, Az, Bx, By, Bz, Cx, Cy, Cz;
     const float4 sc = ray_shear_consts(r);
     const Shear32 m = shear_matrix(r, sc);
-    shear_vertex(r, m, v0, Ax, Ay, Az);
-    shear_vertex(r, m, v1, Bx, By, Bz);
-    shear_vertex(r, m, v2, Cx, Cy, Cz);
+    const float3 ro = ray_o(r);
+    shear_vertex(ro, m, v0, Ax, Ay, Az);
+    shear_vertex(ro, m, v1, Bx, By, Bz);
+    shear_vertex(ro, m, v2, Cx, Cy, Cz);
     const float CyBx = Cy * Bx, AyCx = Ay * Cx, ByAx = By * Ax;
     const float U = fmaf(Cx, By, -CyBx);
     const float V = fmaf(Ax, Cy, -AyCx);
@@ -249,7 +279,7 @@ __device__ __forceinline__ int tri_test32(const RayT& r, float3 v0, float3 v1, f
 // fp64 watertight test in the oracle's operation order; true and t if hit with t > 0
 __device__ __forceinline__ bool tri_test64(RayT& r, float3 v0, float3 v1, float3 v2, double& t_out) {
     const Shear64 sh = shear64(r);
-    const float3 o32 = make_float3(r.o[0], r.o[1], r.o[2]);
+    const float3 o32 = ray_o(r);
     const int kx = ray_kx(r), ky = ray_ky(r), kz = ray_kz(r);
     const double ox = self3(o32, kx), oy = self3(o32, ky), oz = self3(o32, kz);
     const double A0 = __dsub_rn((double)self3(v0, kx), ox);
@@ -286,9 +316,10 @@ __device__ __forceinline__ bool tri_test64(RayT& r, float3 v0, float3 v1, float3
 __device__ __forceinline__ bool sph_test64(RayT& r, float3 c, float rad, double& t_out) {
     const float3 dd = ray_dir(r);
     const double d0 = dd.x, d1 = dd.y, d2 = dd.z;
-    const double oc0 = __dsub_rn((double)r.o[0], (double)c.x);
-    const double oc1 = __dsub_rn((double)r.o[1], (double)c.y);
-    const double oc2 = __dsub_rn((double)r.o[2], (double)c.z);
+    const float3 ro = ray_o(r);
+    const double oc0 = __dsub_rn((double)ro.x, (double)c.x);
+    const double oc1 = __dsub_rn((double)ro.y, (double)c.y);
+    const double oc2 = __dsub_rn((double)ro.z, (double)c.z);
     const double a = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
     const double b = __dadd_rn(__dadd_rn(__dmul_rn(oc0, d0), __dmul_rn(oc1, d1)), __dmul_rn(oc2, d2));
     const double cc = __dsub_rn(__dadd_rn(__dadd_rn(__dmul_rn(oc0, oc0), __dmul_rn(oc1, oc1)), __dmul_rn(oc2, oc2)),
@@ -308,7 +339,8 @@ __device__ __forceinline__ bool sph_test64(RayT& r, float3 c, float rad, double&
 // |dt| <= (db + d sqrt(disc)) / a + 5 eps |t|. Grazing rays and roots near 0 defer to fp64.
 __device__ __forceinline__ int sph_test32(const RayT& r, float3 c, float rad, float& t, float& dt) {
     constexpr float eps = 0x1p-24f;
-    const float ox = r.o[0] - c.x, oy = r.o[1] - c.y, oz = r.o[2] - c.z;
+    const float3 ro = ray_o(r);
+    const float ox = ro.x - c.x, oy = ro.y - c.y, oz = ro.z - c.z;
     const float3 dd = ray_dir(r);
     const float a = fmaf(dd.x, dd.x, fmaf(dd.y, dd.y, dd.z * dd.z));
     const float b = fmaf(ox, dd.x, fmaf(oy, dd.y, oz * dd.z));
@@ -538,6 +570,8 @@ __device__ __forceinline__ void trav_round(const TraceParams& tp, Trav& t, uint3
             ldg256(pool + t.cur + 2, q1, q2);
             const uint32_t w[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
             const float O[3] = {__uint_as_float(h.x), __uint_as_float(h.y), __uint_as_float(h.z)};
+            const float3 ro3 = ray_o(r), ri3 = ray_inv(r);
+            const float ro[3] = {ro3.x, ro3.y, ro3.z}, ri[3] = {ri3.x, ri3.y, ri3.z};
             // child sizes in units (nibbles: 0 none, 4 interior, 3 * count leaf), see pt_internal.h
             const uint32_t meta = (h.x & 15u) | ((h.y & 15u) << 4) | ((h.z & 15u) << 8) | ((h.w >> 28) << 12);
             uint32_t off = h.w & 0x0FFFFFFFu;
@@ -557,8 +591,8 @@ __device__ __forceinline__ void trav_round(const TraceParams& tp, Trav& t, uint3
                     const uint32_t ws = __byte_perm(w[3 * ci + a], 0u, swz[a]);
                     const float2 lh = __half22float2(*reinterpret_cast<const __half2*>(&ws));
                     const float2 b = __fadd2_rn(make_float2(O[a], O[a]), lh);
-                    const float2 tt = __fmul2_rn(__fadd2_rn(b, make_float2(-r.o[a], -r.o[a])),
-                                                 make_float2(r.inv[a], r.inv[a]));
+                    const float2 tt = __fmul2_rn(__fadd2_rn(b, make_float2(-ro[a], -ro[a])),
+                                                 make_float2(ri[a], ri[a]));
                     tn = fmaxf(tn, tt.x);
                     tf = fminf(tf, tt.y);
                 }
@@ -620,7 +654,7 @@ __device__ __forceinline__ void trav_round(const TraceParams& tp, Trav& t, uint3
 }
 
 __device__ Hit closest_hit(const TraceParams& tp, float3 o, float3 d) {
-    float4 cold[2];                   // local memory: written and read only through ld/st.local asm
+    float4 cold[kColdBytes / 16];                   // local memory: written and read only through ld/st.local asm
     uint2 stk[kStackSize];            // local memory: through ld/st.local asm
     Trav t;
     trav_begin(t, tp, o, d, (uint32_t)__cvta_generic_to_local(cold));
@@ -966,7 +1000,7 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
     float3 bt = make_float3(1, 1, 1);
     uint32_t segs = 0;
     if constexpr (kReplace) {
-        float4 cold[2];                   // local memory (ld/st.local asm): the ray's spilled constants
+        float4 cold[kColdBytes / 16];                   // local memory (ld/st.local asm): the ray's spilled constants
         uint2 stk[kStackSize];            // local memory: the traversal stack
         const uint32_t cold_a = (uint32_t)__cvta_generic_to_local(cold);
         const uint32_t stk_a = (uint32_t)__cvta_generic_to_local(stk);
@@ -1005,7 +1039,7 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
             r.escaped = false;
             if (have && !tv.tracing) {
                 ++segs;
-                shade_hit(a, depth, slot, make_float3(tv.r.o[0], tv.r.o[1], tv.r.o[2]), ray_dir(tv.r), bt, tv.best, r);
+                shade_hit(a, depth, slot, ray_o(tv.r), ray_dir(tv.r), bt, tv.best, r);
                 write_radiance(a, r, slot);
                 if (r.alive) {
                     bt = r.beta;
