@@ -67,7 +67,7 @@ __device__ __forceinline__ float3 cam_dir(const Cam32& k, int W, int H, int x, i
 // PT_RAY_LOCAL=1: the origin and the slab reciprocals also live in the local-memory record (two 16-B
 // loads per node visit instead of registers the 72-register cap spills anyway)
 #ifndef PT_RAY_LOCAL
-#define PT_RAY_LOCAL 1
+#define PT_RAY_LOCAL 0   // measured slower (2.72 vs 2.78 G samples/s on config 3, profiles/round2/raylocal.log)
 #endif
 constexpr int kColdBytes = PT_RAY_LOCAL ? 64 : 32;
 struct RayT {
