@@ -445,7 +445,6 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
                     if (stage == 0) pend[s] = true;
                 }
             }
-            rec += nslots;   // (trace records of the MMA's layer-5 steps)
         }
         hand_over();
         if (cb == 0)

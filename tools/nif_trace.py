@@ -1,6 +1,7 @@
 #!/usr/bin/env python
 """Run the trace build of the SIREN NIF kernel (PT_NIF_TRACE) and print the per-step timeline of CTA 0:
-MMA wait/issue stamps and epilogue wake/done stamps (cycles); 5 MMA stages per tile (the epilogue columns are empty for layer 5), 2 slots."""
+MMA wait/issue stamps and epilogue wake/done stamps (cycles); 4 MMA stages per tile (stage 0 = the previous
+tile's output layer + layer 1), 2 slots."""
 import ctypes as C
 import os
 import sys
@@ -26,11 +27,11 @@ nrec = int((tr[0, :, 1] > 0).sum())
 t0 = tr[0, 0, 0]
 print("rec  stage slot | mma_wait_done  mma_issued | epiA_wake epiA_done | epiB_wake epiB_done")
 for r in range(min(nrec, 60)):
-    layer, s = (r // 2) % 5, r % 2
+    layer, s = (r // 2) % 4, r % 2
     row = [tr[0, r, 0] - t0, tr[0, r, 1] - t0, tr[1, r, 0] - t0, tr[1, r, 1] - t0, tr[2, r, 0] - t0, tr[2, r, 1] - t0]
     print(f"{r:4d} {layer:5d} {s:4d} | " + " ".join(f"{v:10d}" for v in row))
 # per step averages over the steady state
 d = np.diff(tr[0, 10:nrec, 0])
-print("mean cycles between MMA issues:", d.mean(), " per tile:", (tr[0, nrec - 1, 0] - tr[0, 10, 0]) / ((nrec - 11) / 5))
+print("mean cycles between MMA issues:", d.mean(), " per tile:", (tr[0, nrec - 1, 0] - tr[0, 10, 0]) / ((nrec - 11) / 4))
 ep = tr[1, 10:nrec, 1] - tr[1, 10:nrec, 0]
 print("epilogue A busy per step:", ep.mean(), " wake latency after MMA issue:", (tr[1, 10:nrec, 0] - tr[0, 10:nrec, 1]).mean())
