@@ -37,3 +37,6 @@ for cfg in (3, 4):
             env["PT_BVH_THREADS"] = th
         p = subprocess.run([sys.executable, "-c", CODE, str(cfg)], env=env, capture_output=True, text=True)
         print(p.stdout.strip() or p.stderr[-500:], flush=True)
+        phases = [l for l in p.stderr.splitlines() if l.startswith("bvh ")]
+        if phases:   # PT_BVH_TIMING=1: the builder's phase times of the last build
+            print("   " + " | ".join(x[4:].strip() for x in phases[-6:]), flush=True)
