@@ -64,15 +64,19 @@ __device__ __forceinline__ float3 cam_dir(const Cam32& k, int W, int H, int x, i
 // ---------------------------------------------------------------------------------------------
 // Kept compact (14 registers) because it is live through the whole traversal under the path kernels'
 // 72-register cap; the shear matrix of the certified pre-test is rebuilt inside each triangle test.
-// (Keeping the origin and slab reciprocals in the local record too measured slower: 2.72 vs 2.78 G
-// samples/s on config 3, profiles/round2/raylocal.log.)
-constexpr int kColdBytes = 64;
+// PT_RAY_LOCAL=1: the origin and the slab reciprocals also live in the local-memory record (two 16-B
+// loads per node visit instead of registers the 72-register cap spills anyway)
+#ifndef PT_RAY_LOCAL
+#define PT_RAY_LOCAL 0   // measured slower (2.72 vs 2.78 G samples/s on config 3, profiles/round2/raylocal.log)
+#endif
+constexpr int kColdBytes = PT_RAY_LOCAL ? 64 : 32;
 struct RayT {
+#if !PT_RAY_LOCAL
     float o[3], inv[3];         // slab test
+#endif
     uint32_t kbits;             // kx | ky << 2 | kz << 4 | negmask << 8 (bit a: d[a] has its sign bit set)
-    uint32_t cold;              // local-memory address of (Sx, Sy, rz, |d[kz]|) (d.x, d.y, d.z, 0) and the
-                                // fp32 shear rows (mxy[0], mxy[1]) (mxy[2], 0, 0): only primitive tests
-                                // read them, so they are spilled by hand, not by ptxas
+    uint32_t cold;              // local-memory address of (Sx, Sy, rz, |d[kz]|) (d.x, d.y, d.z, 0) [(o, 0)
+                                // (inv, 0)]: spilled by hand, not by ptxas
 };
 __device__ __forceinline__ float4 ldl4(uint32_t a) {
     float4 v;
@@ -83,7 +87,22 @@ __device__ __forceinline__ void stl4(uint32_t a, float4 v) {
     asm volatile("st.local.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
 __device__ __forceinline__ float4 ray_shear_consts(const RayT& r) { return ldl4(r.cold); }   // Sx, Sy, rz, |d[kz]|
-__device__ __forceinline__ float3 ray_o(const RayT& r) { return make_float3(r.o[0], r.o[1], r.o[2]); }
+__device__ __forceinline__ float3 ray_o(const RayT& r) {
+#if PT_RAY_LOCAL
+    const float4 v = ldl4(r.cold + 32);
+    return make_float3(v.x, v.y, v.z);
+#else
+    return make_float3(r.o[0], r.o[1], r.o[2]);
+#endif
+}
+__device__ __forceinline__ float3 ray_inv(const RayT& r) {
+#if PT_RAY_LOCAL
+    const float4 v = ldl4(r.cold + 48);
+    return make_float3(v.x, v.y, v.z);
+#else
+    return make_float3(r.inv[0], r.inv[1], r.inv[2]);
+#endif
+}
 __device__ __forceinline__ float3 ray_dir(const RayT& r) {
     const float4 v = ldl4(r.cold + 16);
     return make_float3(v.x, v.y, v.z);
@@ -93,17 +112,21 @@ __device__ __forceinline__ int ray_ky(const RayT& r) { return (int)((r.kbits >> 
 __device__ __forceinline__ int ray_kz(const RayT& r) { return (int)((r.kbits >> 4) & 3u); }
 // fp32 shear as a matrix over the world axes a, so a vertex is sheared with packed FFMA2s instead of
 // permutation selects: (Ax, Ay) = sum_a mxy[a] (v - o)_a with mxy[a] = ((e_kx - Sx e_kz)_a,
-// (e_ky - Sy e_kz)_a); Az = Sz (v - o)_kz. The rows are built once per ray (ray_prepare) and read back
-// by each triangle test from the local record (2 loads instead of 12 selects per test).
+// (e_ky - Sy e_kz)_a), Az = sum_a mz[a] (v - o)_a with mz = Sz e_kz
 struct Shear32 {
     float2 mxy[3];
+    float mz[3];
 };
-__device__ __forceinline__ Shear32 shear_matrix(const RayT& r) {
-    const float4 a = ldl4(r.cold + 32), b = ldl4(r.cold + 48);
+__device__ __forceinline__ Shear32 shear_matrix(const RayT& r, float4 sc) {
+    uint32_t kb = r.kbits;
+    asm volatile("" : "+r"(kb));   // rebuilt per test: keep the compiler from hoisting it into registers
+    const int kx = (int)(kb & 3u), ky = (int)((kb >> 2) & 3u), kz = (int)((kb >> 4) & 3u);
     Shear32 m;
-    m.mxy[0] = make_float2(a.x, a.y);
-    m.mxy[1] = make_float2(a.z, a.w);
-    m.mxy[2] = make_float2(b.x, b.y);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        m.mxy[a] = make_float2(a == kx ? 1.0f : (a == kz ? -sc.x : 0.0f), a == ky ? 1.0f : (a == kz ? -sc.y : 0.0f));
+        m.mz[a] = a == kz ? sc.z : 0.0f;
+    }
     return m;
 }
 
@@ -151,18 +174,16 @@ __device__ __forceinline__ void ray_prepare(float3 o, float3 d, RayT& r, uint32_
     // six more registers live through the whole traversal
     const float rz = __frcp_rn(dkz);
     r.cold = cold;
-    const float Sx = self3(d, kx) * rz, Sy = self3(d, ky) * rz;
-    stl4(cold, make_float4(Sx, Sy, rz, fabsf(dkz)));
+    stl4(cold, make_float4(self3(d, kx) * rz, self3(d, ky) * rz, rz, fabsf(dkz)));
     stl4(cold + 16, make_float4(d.x, d.y, d.z, 0.0f));
-    float2 mxy[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-        mxy[a] = make_float2(a == kx ? 1.0f : (a == kz ? -Sx : 0.0f), a == ky ? 1.0f : (a == kz ? -Sy : 0.0f));
-    stl4(cold + 32, make_float4(mxy[0].x, mxy[0].y, mxy[1].x, mxy[1].y));
-    stl4(cold + 48, make_float4(mxy[2].x, mxy[2].y, 0.0f, 0.0f));
     // slab reciprocals: the SFU approximation (<= 1 ulp); the slab bound below allows for its rounding
+#if PT_RAY_LOCAL
+    stl4(cold + 32, make_float4(o.x, o.y, o.z, 0.0f));
+    stl4(cold + 48, make_float4(rcp_approx(d.x), rcp_approx(d.y), rcp_approx(d.z), 0.0f));
+#else
     r.o[0] = o.x; r.o[1] = o.y; r.o[2] = o.z;
     r.inv[0] = rcp_approx(d.x); r.inv[1] = rcp_approx(d.y); r.inv[2] = rcp_approx(d.z);
+#endif
     const uint32_t negmask = (signbit(d.x) ? 1u : 0u) | (signbit(d.y) ? 2u : 0u) | (signbit(d.z) ? 4u : 0u);
     r.kbits = (uint32_t)kx | ((uint32_t)ky << 2) | ((uint32_t)kz << 4) | (negmask << 8);
 }
@@ -180,8 +201,7 @@ __device__ __forceinline__ Shear64 shear64(const RayT& r) {
 // Shear one vertex into the ray's frame: D = v - o (world axes, one rounding each), then the products
 // with the 0/1/-S entries of the shear rows; at most two roundings per sheared coordinate (the -S
 // product and the sum), the same single-rounding Sz D[kz] for Az as the permuted form.
-__device__ __forceinline__ void shear_vertex(float3 ro, const Shear32& m, float Sz, int kz, float3 v, float& x, float& y,
-                                             float& z) {
+__device__ __forceinline__ void shear_vertex(float3 ro, const Shear32& m, float3 v, float& x, float& y, float& z) {
     const float2 dxy = __fadd2_rn(make_float2(v.x, v.y), make_float2(-ro.x, -ro.y));
     const float dz = v.z - ro.z;
     float2 a = __fmul2_rn(m.mxy[0], make_float2(dxy.x, dxy.x));
@@ -189,7 +209,7 @@ __device__ __forceinline__ void shear_vertex(float3 ro, const Shear32& m, float 
     a = __ffma2_rn(m.mxy[2], make_float2(dz, dz), a);
     x = a.x;
     y = a.y;
-    z = Sz * (kz == 0 ? dxy.x : (kz == 1 ? dxy.y : dz));   // the single rounding Sz D[kz]
+    z = fmaf(m.mz[2], dz, fmaf(m.mz[1], dxy.y, m.mz[0] * dxy.x));
 }
 
 // Certified fp32 watertight test. Returns 0 if the exact (hence the fp64 oracle's) test certainly
@@ -207,12 +227,11 @@ __device__ __forceinline__ int tri_test32(const RayT& r, float3 v0, float3 v1, f
     constexpr float eps = 0x1p-24f;
     float Ax, Ay, Az, Bx, By, Bz, Cx, Cy, Cz;
     const float4 sc = ray_shear_consts(r);
-    const Shear32 m = shear_matrix(r);
+    const Shear32 m = shear_matrix(r, sc);
     const float3 ro = ray_o(r);
-    const int kz = ray_kz(r);
-    shear_vertex(ro, m, sc.z, kz, v0, Ax, Ay, Az);
-    shear_vertex(ro, m, sc.z, kz, v1, Bx, By, Bz);
-    shear_vertex(ro, m, sc.z, kz, v2, Cx, Cy, Cz);
+    shear_vertex(ro, m, v0, Ax, Ay, Az);
+    shear_vertex(ro, m, v1, Bx, By, Bz);
+    shear_vertex(ro, m, v2, Cx, Cy, Cz);
     const float CyBx = Cy * Bx, AyCx = Ay * Cx, ByAx = By * Ax;
     const float U = fmaf(Cx, By, -CyBx);
     const float V = fmaf(Ax, Cy, -AyCx);
@@ -551,7 +570,8 @@ __device__ __forceinline__ void trav_round(const TraceParams& tp, Trav& t, uint3
             ldg256(pool + t.cur + 2, q1, q2);
             const uint32_t w[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
             const float O[3] = {__uint_as_float(h.x), __uint_as_float(h.y), __uint_as_float(h.z)};
-            const float ro[3] = {r.o[0], r.o[1], r.o[2]}, ri[3] = {r.inv[0], r.inv[1], r.inv[2]};
+            const float3 ro3 = ray_o(r), ri3 = ray_inv(r);
+            const float ro[3] = {ro3.x, ro3.y, ro3.z}, ri[3] = {ri3.x, ri3.y, ri3.z};
             // child sizes in units (nibbles: 0 none, 4 interior, 3 * count leaf), see pt_internal.h
             const uint32_t meta = (h.x & 15u) | ((h.y & 15u) << 4) | ((h.z & 15u) << 8) | ((h.w >> 28) << 12);
             uint32_t off = h.w & 0x0FFFFFFFu;
