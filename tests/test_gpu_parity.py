@@ -392,3 +392,26 @@ def test_render_identical_without_programmatic_dependent_launch(ptm, blob, tmp_p
                        capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stderr[-2000:]
     assert np.array_equal(np.load(out), img)
+
+
+def test_render_rows_equals_full_frame_rows(ptm, blob):
+    """pt_render_rows (the multi-GPU row-block split, reading R19) renders exactly the full frame's rows:
+    the same Philox counters (full-frame pixel index) and the same per-pixel sample order, so the rows are
+    bit-identical and every other row of the accumulator is left untouched."""
+    import torch
+    c = scenes.CONFIGS[0]
+    S = ptm.Scene(scenes.scene_for_config(0))
+    N = ptm.Nif(blob)
+    full = torch.zeros(c.width * c.height * 3, device="cuda")
+    ptm.render_samples(S, N, c.width, c.height, 0, c.spp, c.max_depth, 9, full, wave_samples=c.spp)
+    for r0, r1 in ((0, 64), (5, 6), (17, 43), (60, 64)):
+        part = torch.full((c.width * c.height * 3,), -1.0, device="cuda")
+        part.view(c.height, c.width, 3)[r0:r1] = 0.0
+        ptm.render_rows(S, N, c.width, c.height, r0, r1, 0, c.spp, c.max_depth, 9, part, wave_samples=c.spp)
+        torch.cuda.synchronize()
+        p3 = part.view(c.height, c.width, 3).cpu().numpy()
+        f3 = full.view(c.height, c.width, 3).cpu().numpy()
+        assert np.array_equal(p3[r0:r1], f3[r0:r1])
+        assert (p3[:r0] == -1).all() and (p3[r1:] == -1).all()
+    with pytest.raises(ptm.PtError):
+        ptm.render_rows(S, N, c.width, c.height, 10, 10, 0, 1, 2, 0, full)
