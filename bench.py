@@ -328,6 +328,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # logic test of the multi-rank path on a single-GPU box (never a measurement): every rank on cuda:0,
+    # gloo instead of NCCL (the ranks' kernels are independent; only the framebuffer reduce is shared)
+    shared_gpu_test = os.environ.get("PT_BENCH_SHARED_GPU_TEST") == "1"
+    if shared_gpu_test:
+        local = 0
     rows_cpu, rows_ref = ORACLE_ROWS[cfg.index]
     if args.oracle_rows_every > 0:
         rows_cpu = args.oracle_rows_every
@@ -353,7 +358,10 @@ def main():
     from paper_2305_20061_b200.dist import render_partitioned_rows
 
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared_gpu_test:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     if rank == 0:
         _build.build()

@@ -60,3 +60,30 @@ def test_own_arm_json_line_on_gpu():
     assert nr["peak"] == json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"] \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else True
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
+
+@__import__("pytest").mark.gpu
+@__import__("pytest").mark.parametrize("split", ["weak", "strong"])
+def test_own_arm_two_ranks_logic_on_one_gpu(split):
+    """bench.py's multi-rank path (partition, reduce, max-over-ranks timing, rank-0 line) under torchrun
+    with 2 ranks sharing cuda:0 over gloo (PT_BENCH_SHARED_GPU_TEST: a logic test, not a measurement);
+    configs[0] has 4 spp, so the strong split runs 2 samples per rank."""
+    import torch
+    if not torch.cuda.is_available():
+        __import__("pytest").skip("no CUDA device")
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, PT_BENCH_SHARED_GPU_TEST="1")
+    p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--gpus", "2", "--config", "0", "--steps", "2", "--warmup", "3", "--no-also", "--split", split],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [l for l in p.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == split and d["value"] > 0
+    assert d["config"]["frame_spp_total"] == (8 if split == "weak" else 4)
