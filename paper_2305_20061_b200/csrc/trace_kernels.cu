@@ -924,13 +924,6 @@ __device__ __forceinline__ void write_radiance(const ShadeArgs& a, const SegOut&
 #ifndef PT_FB_MINB
 #define PT_FB_MINB PT_TS_MINB   // the first bounce's own register cap (tools/ts_tune.sh)
 #endif
-// kReplace (PT_FB_REPLACE, deep BVHs): the lanes' traversals are interrupted once PT_TRACE_WAKE lanes
-// wait (as in path_kernel); the waiting lanes shade, append and take the next work indices (tile order)
-// while the others resume their traversal.
-#ifndef PT_FB_REPLACE
-#define PT_FB_REPLACE 0
-#endif
-template <bool kReplace>
 __global__ void __launch_bounds__(128, PT_FB_MINB) first_bounce_kernel(ShadeArgs a) {
     pdl_trigger();                    // all CTAs resident (grid = resident capacity): let path_kernel queue
     const uint32_t n = a.n_slots;
@@ -941,77 +934,6 @@ __global__ void __launch_bounds__(128, PT_FB_MINB) first_bounce_kernel(ShadeArgs
     // queue and fetches the next chunk of 32 slots
     unsigned long long* const ww = reinterpret_cast<unsigned long long*>(a.work);
     unsigned long long wo = 0;
-    if constexpr (kReplace) {
-        float4 cold[2];
-        uint2 stk[kStackSize];
-        const uint32_t cold_a = (uint32_t)__cvta_generic_to_local(cold);
-        const uint32_t stk_a = (uint32_t)__cvta_generic_to_local(stk);
-        const float3 eye = make_float3(a.cam.eye[0], a.cam.eye[1], a.cam.eye[2]);
-        Trav tv;
-        tv.tracing = false;
-        bool have = false, dry = false;
-        uint32_t i = 0;
-        // free lanes take work indices base + (rank among them) while those are < n
-        auto refill = [&](uint32_t base, uint32_t mneed) {
-            if (!have) {
-                const uint32_t k = base + (uint32_t)__popc(mneed & lt);
-                if (k < n) {
-                    i = tile_slot(a, k);
-                    have = true;
-                    trav_begin(tv, a.tp, eye, camera_ray(a, i), cold_a);
-                }
-            }
-            if (__any_sync(0xFFFFFFFFu, !have)) dry = true;
-        };
-        if (lane == 0) wo = atomicAdd(ww, 32ull);
-        refill((uint32_t)__shfl_sync(0xFFFFFFFFu, wo, 0), 0xFFFFFFFFu);
-        for (;;) {
-            for (;;) {
-                const uint32_t tr = __ballot_sync(0xFFFFFFFFu, tv.tracing);
-                const uint32_t wake = __ballot_sync(0xFFFFFFFFu, have ? !tv.tracing : !dry);
-                if (tr == 0u || __popc(wake) >= PT_TRACE_WAKE) break;
-                if (tv.tracing) trav_round(a.tp, tv, stk_a);
-            }
-            SegOut r;
-            r.alive = r.escaped = false;
-            if (have && !tv.tracing) {
-                ++segs;
-                shade_hit(a, 1, i, eye, ray_dir(tv.r), make_float3(1.0f, 1.0f, 1.0f), tv.best, r);
-                write_radiance(a, r, i);
-                have = false;
-            }
-            const uint32_t ma = __ballot_sync(0xFFFFFFFFu, r.alive), me = __ballot_sync(0xFFFFFFFFu, r.escaped);
-            const uint32_t mneed = dry ? 0u : __ballot_sync(0xFFFFFFFFu, !have);
-            if ((ma | mneed) != 0u) {
-                const int leader = __ffs(ma | mneed) - 1;
-                if (lane == leader) wo = atomicAdd(ww, (unsigned long long)__popc(mneed) | ((unsigned long long)__popc(ma) << 32));
-                wo = __shfl_sync(0xFFFFFFFFu, wo, leader);
-            }
-            if (r.alive) {
-                const uint32_t pos = (uint32_t)(wo >> 32) + (uint32_t)__popc(ma & lt);
-                a.qA[pos] = make_float4(r.o.x, r.o.y, r.o.z, __uint_as_float(i));
-                a.qB[pos] = make_float4(r.d.x, r.d.y, r.d.z, r.beta.x);
-                a.qC[pos] = make_float2(r.beta.y, r.beta.z);
-            }
-            if (me != 0u) {
-                uint32_t eb = 0;
-                if (lane == __ffs(me) - 1) eb = atomicAdd(a.esc_count, (uint32_t)__popc(me));
-                eb = __shfl_sync(0xFFFFFFFFu, eb, __ffs(me) - 1);
-                if (r.escaped) {
-                    const uint32_t pos = eb + (uint32_t)__popc(me & lt);
-                    a.esc[pos] = make_float4(r.d.x, r.d.y, r.d.z, __uint_as_float(i));
-                    a.esc_beta[pos] = make_float4(r.beta.x, r.beta.y, r.beta.z, 0.0f);
-                }
-            }
-            if (mneed) refill((uint32_t)wo, mneed);
-            if (!__any_sync(0xFFFFFFFFu, have)) break;
-        }
-#pragma unroll
-        for (int k = 16; k > 0; k >>= 1) segs += __shfl_xor_sync(0xFFFFFFFFu, segs, k);
-        if (lane == 0) atomicAdd(a.seg_count, segs);
-        TAIL_STAMP(0);
-        return;
-    }
     if (lane == 0) wo = atomicAdd(ww, 32ull);
     uint32_t base = (uint32_t)__shfl_sync(0xFFFFFFFFu, wo, 0);
     while (base < n) {
@@ -1360,7 +1282,7 @@ static int3 path_grids() {
     int a = g1[dev].load(std::memory_order_relaxed), b = g2[dev].load(std::memory_order_relaxed),
         c = g3[dev].load(std::memory_order_relaxed);
     if (a <= 0 || b <= 0 || c <= 0) {
-        a = resident_grid(first_bounce_kernel<false>, 128);
+        a = resident_grid(first_bounce_kernel, 128);
         b = resident_grid(path_kernel<false>, 128);
         c = resident_grid(path_kernel<true>, 128);
         g1[dev].store(a, std::memory_order_relaxed);
@@ -1396,8 +1318,7 @@ void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int p0,
     // (the first bounce's camera rays stay in whole coherent warps: replacement there measured slower,
     // 2.48 vs 2.58 G samples/s on config 3, profiles/round2/fb_replace.log)
     const bool replace = tp.bvh_depth >= PT_REPLACE_MIN_DEPTH;
-    if (PT_FB_REPLACE && replace) first_bounce_kernel<true><<<grids.x, 128, 0, st>>>(a);
-    else first_bounce_kernel<false><<<grids.x, 128, 0, st>>>(a);
+    first_bounce_kernel<<<grids.x, 128, 0, st>>>(a);
     if (max_depth > 1) {
         if (replace) launch_pdl(path_kernel<true>, dim3(grids.z), dim3(128), 0, st, a);
         else launch_pdl(path_kernel<false>, dim3(grids.y), dim3(128), 0, st, a);
