@@ -415,3 +415,38 @@ def test_render_rows_equals_full_frame_rows(ptm, blob):
         assert (p3[:r0] == -1).all() and (p3[r1:] == -1).all()
     with pytest.raises(ptm.PtError):
         ptm.render_rows(S, N, c.width, c.height, 10, 10, 0, 1, 2, 0, full)
+
+
+def test_concurrent_streams_match_sequential(ptm, blob):
+    """Library scratch shared across calls (the NIF query queue of pt_nif_infer, the pooled wave state of
+    the renders) is ordered by events across streams: two streams issuing interleaved NIF
+    queries and renders of two scene handles produce exactly the sequential results."""
+    import torch
+    nif = ptm.Nif(blob)
+    uv1 = torch.from_numpy(scenes.query_uv(300_000, 21)).cuda()
+    uv2 = torch.from_numpy(scenes.query_uv(200_000, 22)).cuda()
+    ref1 = ptm.nif_infer(nif, uv1).clone()
+    ref2 = ptm.nif_infer(nif, uv2).clone()
+    c = scenes.CONFIGS[0]
+    S1, S2 = ptm.Scene(scenes.scene_for_config(0)), ptm.Scene(scenes.box_scene(seed=3))
+    fr1 = torch.zeros(c.width * c.height * 3, device="cuda")
+    fr2 = torch.zeros(c.width * c.height * 3, device="cuda")
+    ptm.render_samples(S1, nif, c.width, c.height, 0, 4, 6, 1, fr1)
+    ptm.render_samples(S2, nif, c.width, c.height, 0, 4, 6, 2, fr2)
+    torch.cuda.synchronize()
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    o1 = torch.empty_like(ref1)
+    o2 = torch.empty_like(ref2)
+    g1 = torch.zeros_like(fr1)
+    g2 = torch.zeros_like(fr2)
+    for _ in range(3):
+        g1.zero_()
+        g2.zero_()
+        torch.cuda.synchronize()
+        ptm.nif_infer(nif, uv1, out=o1, stream=sa)
+        ptm.nif_infer(nif, uv2, out=o2, stream=sb)
+        ptm.render_samples(S1, nif, c.width, c.height, 0, 4, 6, 1, g1, stream=sa)
+        ptm.render_samples(S2, nif, c.width, c.height, 0, 4, 6, 2, g2, stream=sb)
+        torch.cuda.synchronize()
+        assert torch.equal(o1, ref1) and torch.equal(o2, ref2)
+        assert torch.equal(g1, fr1) and torch.equal(g2, fr2)
