@@ -54,11 +54,24 @@ __device__ __forceinline__ bool mbar_try_sleep(uint32_t bar, uint32_t phase) {
 #ifndef PT_MBAR_SPIN
 #define PT_MBAR_SPIN 0
 #endif
+// PT_MBAR_BACKOFF: 0 = check the trap deadline every retry; 1 = every 64th retry (the retry loop of the
+// warps that wait issues fewer instructions next to the epilogue warps that work); 2 = as 1 plus a
+// __nanosleep(PT_MBAR_NS) between retries
+#ifndef PT_MBAR_BACKOFF
+#define PT_MBAR_BACKOFF 1
+#endif
+#ifndef PT_MBAR_NS
+#define PT_MBAR_NS 32
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
     if (mbar_try(bar, phase)) return;
     const long long t0 = clock64();
+    uint32_t n = 0;
     while (!(PT_MBAR_SPIN ? mbar_try(bar, phase) : mbar_try_sleep(bar, phase))) {
-        if (clock64() - t0 > 4000000000ll) __trap();
+        if (PT_MBAR_BACKOFF == 2) __nanosleep(PT_MBAR_NS);
+        if (PT_MBAR_BACKOFF == 0 || (++n & 63u) == 0u) {
+            if (clock64() - t0 > 4000000000ll) __trap();
+        }
     }
 }
 
