@@ -444,6 +444,16 @@ def main():
             render_step(S2, N2)
     e2e_s = max_over_ranks(time.perf_counter() - te0, world)
     e2e_value = samples_per_step * e2e_steps / e2e_s
+    # the same steps without the pipelining (each step's inputs created, then rendered), for reference
+    serial_create = list(create_ms)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ts0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        render_step(*make_inputs())
+    e2e_serial = samples_per_step * e2e_steps / max_over_ranks(time.perf_counter() - ts0, world)
+    create_ms[:] = serial_create
 
     # ---- extra configs (not the headline): value only, same timing rules ----
     also = {}
@@ -533,7 +543,8 @@ def main():
                          "every step: pt_scene_create + pt_nif_load from host arrays, render, reduce, framebuffer "
                          "to pinned host") + "; pipelined: step i+1's inputs are created on a second host thread "
                                              "while step i renders",
-                "scene_create_ms_median": statistics.median(create_ms)},
+                "scene_create_ms_median": statistics.median(create_ms),
+                "serial_value": e2e_serial},
         "gpu_launches": int(round(prof["launches"] * K)),
         "roofline": roof,
         "nif": {"inferences_per_s": infers / (nif_ms / 1e3) if nif_ms > 0 else None,
