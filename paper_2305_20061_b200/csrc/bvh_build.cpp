@@ -124,6 +124,24 @@ struct Builder {
     int busy = 0;
     bool done = false;
     static constexpr int64_t kGrain = 2048;   // subtrees larger than this may move to another worker
+    // nodes of at least kBigNode references (the top levels of large scenes, where few workers are busy)
+    // are binned and partitioned by `helpers` threads over kChunks fixed chunks (fixed, so the result does
+    // not depend on the thread count); `scratch` is the partition's buffer
+    static constexpr int64_t kBigNode = 1 << 18;
+    static constexpr int kChunks = 64;
+    int helpers = 1;
+    std::vector<Ref> scratch;
+    template <typename F>
+    void chunked(int64_t n, F f) {
+        std::atomic<int> next{0};
+        auto run = [&] {
+            for (int ch; (ch = next.fetch_add(1)) < kChunks;) f(ch, n * ch / kChunks, n * (ch + 1) / kChunks);
+        };
+        std::vector<std::thread> ts;
+        for (int t = 1; t < helpers; ++t) ts.emplace_back(run);
+        run();
+        for (auto& t : ts) t.join();
+    }
     static constexpr int NB = 32;   // max bins (nb <= NB used)
     // measured on configs 2-4 (profiles/round2/bvhparams_*.log): 32 bins, node cost 1.0 and leaves of at
     // most 2 primitives beat round 1's 16 / 1.5 / 4 by 1-3.5 % samples/s
@@ -294,14 +312,41 @@ struct Builder {
                 const int k = (int)((c - c0) * scale);
                 return std::min(nb - 1, std::max(0, k));
             };
-            for (int64_t i = 0; i < cnt_all; ++i) {
-                const Ref& r = r0[i];
-                const int k = bin_of(r);
-                cnt[k]++;
-                bins[k].grow(r.b);
-                float c[3];
-                r.centroid(c);
-                cbins[k].grow_pt(c);
+            const bool big = cnt_all >= kBigNode;   // (for any thread count: the same partition order)
+            if (big) {
+                // the top splits: bin fixed chunks on helper threads, reduce in chunk order (exactly the
+                // serial bins: counts add, boxes unite)
+                std::vector<int64_t> ccnt((size_t)kChunks * NB, 0);
+                std::vector<Box> cb((size_t)kChunks * NB), ccb((size_t)kChunks * NB);
+                for (auto& b : cb) b.empty();
+                for (auto& b : ccb) b.empty();
+                chunked(cnt_all, [&](int ch, int64_t b0, int64_t b1) {
+                    for (int64_t i = b0; i < b1; ++i) {
+                        const Ref& r = r0[i];
+                        const int k = bin_of(r);
+                        ccnt[(size_t)ch * NB + k]++;
+                        cb[(size_t)ch * NB + k].grow(r.b);
+                        float c[3];
+                        r.centroid(c);
+                        ccb[(size_t)ch * NB + k].grow_pt(c);
+                    }
+                });
+                for (int ch = 0; ch < kChunks; ++ch)
+                    for (int k = 0; k < nb; ++k) {
+                        cnt[k] += ccnt[(size_t)ch * NB + k];
+                        bins[k].grow(cb[(size_t)ch * NB + k]);
+                        cbins[k].grow(ccb[(size_t)ch * NB + k]);
+                    }
+            } else {
+                for (int64_t i = 0; i < cnt_all; ++i) {
+                    const Ref& r = r0[i];
+                    const int k = bin_of(r);
+                    cnt[k]++;
+                    bins[k].grow(r.b);
+                    float c[3];
+                    r.centroid(c);
+                    cbins[k].grow_pt(c);
+                }
             }
             double rarea[NB];
             int64_t rcnt[NB];
@@ -329,8 +374,38 @@ struct Builder {
             const double leaf_cost = it.bb.area() * (double)cnt_all;
             best += kTraversalCost * it.bb.area();
             if (best_k >= 0 && (best < leaf_cost || cnt_all > max_leaf)) {
-                Ref* mid = std::partition(r0, r0 + cnt_all, [&](const Ref& r) { return bin_of(r) <= best_k; });
-                split = it.first + (mid - r0);
+                if (big) {
+                    // stable partition in fixed chunks: count, prefix, scatter into the scratch, copy back
+                    std::vector<int64_t> nl(kChunks, 0);
+                    chunked(cnt_all, [&](int ch, int64_t b0, int64_t b1) {
+                        int64_t m = 0;
+                        for (int64_t i = b0; i < b1; ++i) m += bin_of(r0[i]) <= best_k;
+                        nl[ch] = m;
+                    });
+                    int64_t left = 0;
+                    for (int ch = 0; ch < kChunks; ++ch) left += nl[ch];
+                    std::vector<int64_t> lo_at(kChunks), hi_at(kChunks);
+                    int64_t a = 0, b = left;
+                    for (int ch = 0; ch < kChunks; ++ch) {
+                        const int64_t b0 = cnt_all * ch / kChunks, b1 = cnt_all * (ch + 1) / kChunks;
+                        lo_at[ch] = a;
+                        hi_at[ch] = b;
+                        a += nl[ch];
+                        b += (b1 - b0) - nl[ch];
+                    }
+                    Ref* tmp = scratch.data() + it.first;
+                    chunked(cnt_all, [&](int ch, int64_t b0, int64_t b1) {
+                        int64_t pl = lo_at[ch], ph = hi_at[ch];
+                        for (int64_t i = b0; i < b1; ++i) tmp[bin_of(r0[i]) <= best_k ? pl++ : ph++] = r0[i];
+                    });
+                    chunked(cnt_all, [&](int, int64_t b0, int64_t b1) {
+                        std::memcpy(r0 + b0, tmp + b0, sizeof(Ref) * (size_t)(b1 - b0));
+                    });
+                    split = it.first + left;
+                } else {
+                    Ref* mid = std::partition(r0, r0 + cnt_all, [&](const Ref& r) { return bin_of(r) <= best_k; });
+                    split = it.first + (mid - r0);
+                }
                 lb.empty(); lcb.empty(); rb.empty(); rcb.empty();
                 for (int k = 0; k < nb; ++k) {
                     if (k <= best_k) { lb.grow(bins[k]); lcb.grow(cbins[k]); }
@@ -464,6 +539,8 @@ int build_wide_bvh(const pt_triangle* tris, int64_t n_tris, const pt_sphere* sph
     if (const char* e = std::getenv("PT_BVH_NODE_COST")) B.trav_cost = std::atof(e);
     if (const char* e = std::getenv("PT_BVH_MAX_LEAF")) B.max_leaf = std::max(1, std::min(kMaxLeafPrims, std::atoi(e)));
     B.refs.resize(n);
+    B.helpers = threads;
+    if (n >= Builder::kBigNode) B.scratch.resize(n);
     parallel_for(threads, n, [&](int64_t i) {
         Ref& r = B.refs[i];
         r.id = (uint32_t)i;

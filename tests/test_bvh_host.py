@@ -113,3 +113,28 @@ def test_library_exports_every_header_symbol(built):
     for n in names:
         assert hasattr(L, n), n
     assert set(names) == set(pt.EXPORTED)
+
+
+def test_parallel_build_is_thread_count_invariant(built):
+    """The parallel builder (worker pool, chunked binning/partition of the top splits) produces the same
+    pool for 1, 3 and the default number of threads (>= 2^18 primitives exercises the chunked splits)."""
+    import hashlib
+    import os
+    sc = scenes.random_soup(300_000, 0, 7)
+    digests = []
+    old = os.environ.get("PT_BVH_THREADS")
+    try:
+        for th in ("1", "3", None):
+            if th is None:
+                os.environ.pop("PT_BVH_THREADS", None)
+            else:
+                os.environ["PT_BVH_THREADS"] = th
+            st, pool = pt.debug_build_bvh(sc, with_pool=True)
+            digests.append(hashlib.sha1(pool.tobytes()).hexdigest())
+    finally:
+        if old is None:
+            os.environ.pop("PT_BVH_THREADS", None)
+        else:
+            os.environ["PT_BVH_THREADS"] = old
+    assert len(set(digests)) == 1
+    _check_pool(sc, pool) if st["units"] < 2_000_000 else None
