@@ -63,7 +63,8 @@ constexpr int kThreads = 32 * (kFirstEpiWarp + kNumEpiWarps);   // 640
 // the output warps read it before they arrive on a_ready(s) for the next tile's layer 4, which the
 // issuer waits for before it issues that tile's layer 5.)
 #ifndef PT_NIF_DIAG
-#define PT_NIF_DIAG 0   // diagnostic builds only (wrong results): 1 = no TMEM store of A, 2 = no sine
+#define PT_NIF_DIAG 0   // diagnostic builds only (wrong results): 1 = no TMEM store of A, 2 = no sine,
+                        // 3 = no epilogue TMEM traffic (neither the accumulator load nor the A store)
 #endif
 #ifndef PT_NIF_DEFER_ST
 #define PT_NIF_DEFER_ST 0   // measured slower (5.96 vs 7.25 G inferences/s, profiles/round2/nif_defer.log)
@@ -400,6 +401,16 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
                                 dbg[((size_t)stage * n_rows + row) * 128 + 32 * cb + j] = __uint_as_float(v[j]);
                         sine_half(v, 0, pk);
                         sine_half(v + 16, 1, pk + 8);
+                    } else if (PT_NIF_DIAG == 4) {
+                        // diagnostic (wrong results): the epilogue only hands over (MMA + hand-off latency)
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) pk[j] = (uint32_t)(j + lane);
+                    } else if (PT_NIF_DIAG == 3) {
+                        // diagnostic (wrong results): no TMEM traffic at all -- the sine on registers only
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) v[j] = __float_as_uint((float)(j + lane) * 0.01f);
+                        sine_half(v, 0, pk);
+                        sine_half(v + 16, 1, pk + 8);
                     } else if (PT_NIF_DIAG == 2) {
                         // diagnostic (wrong results): TMEM round trip without the sine
                         TMEM_LD32(tmem + d_col(s) + lane_addr + 32 * cb, v);
@@ -421,7 +432,7 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
 #endif
                     {
                         // -> A of the next layer (this warp's 32 columns)
-                        if (PT_NIF_DIAG != 1) {
+                        if (PT_NIF_DIAG != 1 && PT_NIF_DIAG != 3 && PT_NIF_DIAG != 4) {
                             TMEM_ST16(tmem + a_col(s) + lane_addr + 16 * cb, pk);
                         } else if (pk[0] == 0x7FFF7FFFu && pk[15] == 0x7FFF7FFFu) {   // diagnostic: keep pk live
                             out[0] = 0.0f;
