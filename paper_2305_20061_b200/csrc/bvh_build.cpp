@@ -113,7 +113,12 @@ struct WideTask {
 };
 
 struct Builder {
-    std::vector<Ref> refs;
+    // reference array and the partition scratch: uninitialised allocations (no serial zero fill of up to
+    // 2 x 160 MB); the parallel fill and the chunked partition touch them first
+    std::unique_ptr<Ref[]> refs_buf, scratch_buf;
+    Ref* refs = nullptr;
+    Ref* scratch = nullptr;
+    int64_t n_refs = 0;
     std::vector<Wide> wide;          // preallocated (at most one wide node per primitive)
     std::atomic<int32_t> next_wide{1};
     std::atomic<int64_t> n_leaves{0};
@@ -130,7 +135,6 @@ struct Builder {
     static constexpr int64_t kBigNode = 1 << 18;
     static constexpr int kChunks = 64;
     int helpers = 1;
-    std::vector<Ref> scratch;
     template <typename F>
     void chunked(int64_t n, F f) {
         std::atomic<int> next{0};
@@ -150,12 +154,13 @@ struct Builder {
     int max_leaf = 2;               // leaf size cap (PT_BVH_MAX_LEAF, <= kMaxLeafPrims)
 
     void build(int threads) {
-        const int64_t n = (int64_t)refs.size();
+        const int64_t n = n_refs;
         wide.resize((size_t)std::max<int64_t>(1, n));
         Item root{0, n, {}, {}};
         root.bb.empty();
         root.cb.empty();
-        for (const Ref& r : refs) {
+        for (int64_t i = 0; i < n; ++i) {
+            const Ref& r = refs[i];
             float c[3];
             r.centroid(c);
             root.bb.grow(r.b);
@@ -297,7 +302,7 @@ struct Builder {
         float ext = it.cb.hi[0] - it.cb.lo[0];
         for (int a = 1; a < 3; ++a)
             if (it.cb.hi[a] - it.cb.lo[a] > ext) { ext = it.cb.hi[a] - it.cb.lo[a]; axis = a; }
-        Ref* const r0 = refs.data() + it.first;
+        Ref* const r0 = refs + it.first;
         const int64_t cnt_all = it.count;
         int64_t split = -1;
         Box lb, lcb, rb, rcb;
@@ -393,7 +398,7 @@ struct Builder {
                         a += nl[ch];
                         b += (b1 - b0) - nl[ch];
                     }
-                    Ref* tmp = scratch.data() + it.first;
+                    Ref* tmp = scratch + it.first;
                     chunked(cnt_all, [&](int ch, int64_t b0, int64_t b1) {
                         int64_t pl = lo_at[ch], ph = hi_at[ch];
                         for (int64_t i = b0; i < b1; ++i) tmp[bin_of(r0[i]) <= best_k ? pl++ : ph++] = r0[i];
@@ -538,9 +543,14 @@ int build_wide_bvh(const pt_triangle* tris, int64_t n_tris, const pt_sphere* sph
     if (const char* e = std::getenv("PT_BVH_BINS")) B.nb = std::max(2, std::min(Builder::NB, std::atoi(e)));
     if (const char* e = std::getenv("PT_BVH_NODE_COST")) B.trav_cost = std::atof(e);
     if (const char* e = std::getenv("PT_BVH_MAX_LEAF")) B.max_leaf = std::max(1, std::min(kMaxLeafPrims, std::atoi(e)));
-    B.refs.resize(n);
+    B.refs_buf.reset(new Ref[(size_t)n]);
+    B.refs = B.refs_buf.get();
+    B.n_refs = n;
     B.helpers = threads;
-    if (n >= Builder::kBigNode) B.scratch.resize(n);
+    if (n >= Builder::kBigNode) {
+        B.scratch_buf.reset(new Ref[(size_t)n]);
+        B.scratch = B.scratch_buf.get();
+    }
     parallel_for(threads, n, [&](int64_t i) {
         Ref& r = B.refs[i];
         r.id = (uint32_t)i;
@@ -600,7 +610,7 @@ int build_wide_bvh(const pt_triangle* tris, int64_t n_tris, const pt_sphere* sph
     out->pool.reset(new uint4[(size_t)total]);
     out->units = total;
     uint4* pool = out->pool.get();
-    const Ref* refs = B.refs.data();
+    const Ref* refs = B.refs;
     lap("alloc");
 
     // ---- 4. records and inline primitives, in parallel ----
