@@ -20,12 +20,14 @@ __host__ __device__ constexpr uint32_t idesc(int n, uint32_t ta = 0, uint32_t tb
 
 // mode: 0 TS single N, 1 SS single N, 2 TS N=64 halves alternating D regions, 3 TS N=128 + SS bias / 8,
 // 4 TS with B MN-major (SWIZZLE_NONE, LBO = K stride 128 B, SBO = MN stride 2048 B; transpose-B bit),
-// 5 SS with A MN-major (same layout) and B K-major
+// 5 SS with A MN-major (same layout) and B K-major, 6 TS N=128 with a tcgen05.commit after every 9 MMAs
+// (the NIF's per-layer commit), 7 as 6 alternating two D regions (two slots)
 template <int mode, int n>
 __global__ void __launch_bounds__(128, 1) mma_rate(int iters, unsigned long long* out) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint32_t tslot;
     __shared__ __align__(8) uint64_t bar;
+    __shared__ __align__(8) uint64_t bar2;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
     if (warp == 0) {
@@ -34,6 +36,7 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int iters, unsigned long long
     }
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar2)));
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     asm volatile("fence.proxy.async.shared::cta;");
@@ -60,6 +63,16 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int iters, unsigned long long
                 asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem), "l"(am),
                              "l"(bk), "r"(idesc(n, 1, 0)), "r"(acc));
+            } else if (mode == 6 || mode == 7) {
+                const uint32_t d = mode == 7 ? tmem + 128u * ((it / 9) & 1) : tmem;
+                const uint32_t a = tmem + 384u + (uint32_t)(8 * (it % 8));
+                const uint32_t acc6 = (it % 9) != 0;
+                asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                             "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d), "r"(a),
+                             "l"(bd), "r"(idesc(n)), "r"(acc6));
+                if (it % 9 == 8)
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                        smem_u32(&bar2)));
             } else if (mode == 0 || mode == 2) {
                 const uint32_t d = mode == 2 ? tmem + 64u * (it & 1) : tmem;
                 const uint32_t a = tmem + 384u + (uint32_t)(8 * ((it >> (mode == 2 ? 1 : 0)) % 8));
@@ -94,14 +107,15 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int iters, unsigned long long
 int main() {
     unsigned long long* d_out;
     cudaMalloc(&d_out, 148 * 8);
-    const char* mname[6] = {"TS", "SS", "TS N64 halves", "TS + SS bias/8", "TS B MN-major", "SS A MN-major"};
+    const char* mname[8] = {"TS", "SS", "TS N64 halves", "TS + SS bias/8", "TS B MN-major", "SS A MN-major",
+                            "TS + commit/9", "TS + commit/9, 2 D"};
     struct { int mode, n; void (*k)(int, unsigned long long*); } cases[] = {
         {0, 16, mma_rate<0, 16>}, {0, 32, mma_rate<0, 32>}, {0, 64, mma_rate<0, 64>}, {0, 128, mma_rate<0, 128>},
         {0, 256, mma_rate<0, 256>}, {1, 16, mma_rate<1, 16>}, {1, 64, mma_rate<1, 64>}, {1, 128, mma_rate<1, 128>},
         {1, 256, mma_rate<1, 256>}, {2, 64, mma_rate<2, 64>}, {3, 128, mma_rate<3, 128>},
-        {4, 128, mma_rate<4, 128>}, {5, 16, mma_rate<5, 16>}};
+        {4, 128, mma_rate<4, 128>}, {5, 16, mma_rate<5, 16>}, {6, 128, mma_rate<6, 128>}, {7, 128, mma_rate<7, 128>}};
     for (auto c : cases) {
-        const int iters = 8192;
+        const int iters = 9 * 1024;
         cudaFuncSetAttribute(c.k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
         c.k<<<148, 128, 96 * 1024>>>(iters, d_out);
         cudaError_t e = cudaDeviceSynchronize();
