@@ -6,8 +6,13 @@
 //     (k = 1..3); y = W5 h4 + b5; radiance = beta * exp(y)   (written to the path's own wave slot)
 //
 // Design. One persistent CTA per SM keeps the weights resident in shared memory
-// (one bulk TMA copy per CTA). Two 128-ray tiles ("slots") are in flight: the tensor core runs one
-// slot's layer while 16 epilogue warps apply the sine to the other slot's accumulator.
+// (one bulk TMA copy per CTA). kSlots (3) 128-ray tiles ("slots") are in flight: the tensor core runs
+// one slot's layer while 16 epilogue warps apply the sine to another slot's accumulator. A layer's
+// MMA group takes ~1,300 cycles from issue to a visible commit against 576 cycles of tensor work
+// (tools/mma_shapes.cu "commit/9 + wait"), so with two slots each slot's chain (MMA latency + sine
+// epilogue) left the tensor pipe idle about half the time; three slots cover it. Accumulators are not
+// owned by slots: layer groups rotate over two D regions in issue order, and the epilogue frees a D
+// region (d_empty) as soon as its 32 columns are in registers, before the sine.
 //   * Layer 1 (2 -> 128): one SS MMA, K = 16, A = a shared-memory tile staged by two producer warps
 //     (equirect, hi/lo split of x0, constant-1 bias column), so no epilogue work is spent on inputs.
 //   * Layers 2-4 (128 -> 128): 9 TS MMAs, M = N = 128, K = 16 each; A = the previous layer's fp16
@@ -20,9 +25,10 @@
 //     warps owning TMEM lane quarters at column block 0 read O(prev tile) during the next tile's first
 //     sine stage (exp, beta, store). (On the FMA pipe inside the layer-4 epilogue it lengthened the
 //     epilogue, the bottleneck, by ~700 cycles per tile: tools/nif_trace.py.)
-// TMEM (512 columns): slot s: D at 256 s (128 fp32 columns), A at 256 s + 128 (64 columns of fp16
-// pairs + the constant K block 64..71), O at 256 s + 208 (16 columns). A is single-buffered: each
-// layer's epilogue starts after the layer's one commit, i.e. after the MMA finished reading A.
+// TMEM (512 columns): A(s) at 64 s (64 columns of fp16 pairs), O(s) at 192 + 16 s (16 columns), the
+// constant-1 K block shared by all slots at 240 (8 columns), D regions at 256 and 384 (128 fp32 columns
+// each). A is single-buffered: each layer's epilogue starts after the layer's one commit, i.e. after
+// the MMA finished reading A.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -46,38 +52,65 @@ constexpr int kOffBH = kB1Bytes;
 constexpr int kOffB5 = kOffBH + 3 * kBHBytes;   // layer 5: N = 16 (3 used), K = 128 + bias step
 constexpr int kB5Bytes = 16 * 144 * 2;
 constexpr int kImageBytes = kOffB5 + kB5Bytes;  // 119,296
-// after the image: barriers, staged layer-1 A tiles (2 slots)
+#ifndef PT_NIF_SLOTS
+#define PT_NIF_SLOTS 3
+#endif
+constexpr int kSlots = PT_NIF_SLOTS;            // tiles in flight (2 or 3: TMEM layout below)
+static_assert(kSlots == 2 || kSlots == 3, "TMEM holds at most three slots");
+constexpr int kDRegions = 2;
+// after the image: barriers, the TMEM base address, staged layer-1 A tiles (one per slot)
 constexpr int kOffBars = kImageBytes;
-constexpr int kOffA0 = ((kOffBars + 128 + 1023) / 1024) * 1024;
+// MMA issuers: warp j issues the layer groups of D region j (kIssuers = 2) or warp 0 all of them. A
+// tcgen05.mma the tensor pipe cannot take yet stalls its warp's SM sub-partition, which slowed that
+// sub-partition's epilogue warps by ~250 cycles per layer with one issuer (tools/nif_trace.py); two
+// issuers halve it. Every barrier an issuer waits on has that issuer as its only waiter, so each
+// waiter sees every phase in order (a_ready is per slot and per consuming issuer).
+#ifndef PT_NIF_ISSUERS
+#define PT_NIF_ISSUERS 2
+#endif
+constexpr int kIssuers = PT_NIF_ISSUERS;
+static_assert(kIssuers == 1 || kIssuers == kDRegions, "one issuer, or one per D region");
+constexpr int kNumBars = 1 + (3 + kIssuers) * kSlots + 2 * kDRegions;
+constexpr int kOffTmemSlot = kOffBars + 8 * kNumBars;
+constexpr int kOffA0 = ((kOffTmemSlot + 16 + 1023) / 1024) * 1024;
 constexpr int kA0Bytes = 128 * 16 * 2;
-constexpr int kSmemBytes = kOffA0 + 2 * kA0Bytes;
+constexpr int kSmemBytes = kOffA0 + kSlots * kA0Bytes;
 
-constexpr int kNumEpiWarps = 16;                // 4 per TMEM lane quarter, 32 columns each
+// Epilogue: two teams of 8 warps (2 per TMEM lane quarter, 64 columns each). Team t owns D region t,
+// i.e. every other layer group, so one team applies the sine while the other waits for its next
+// accumulator and the SM sub-partitions stay busy (with all 16 warps on every group, they all idled
+// together between groups and the slowest warp of each group gated the next; tools/nif_trace.py).
+constexpr int kNumEpiWarps = 16;
+constexpr int kTeamWarps = 8;
 constexpr int kFirstEpiWarp = 4;
 constexpr int kProducerWarp0 = 2;               // warps 2-3 stage the layer-1 inputs
 constexpr int kProducerThreads = 64;
 constexpr int kThreads = 32 * (kFirstEpiWarp + kNumEpiWarps);   // 640
-// barriers: [0] weights, [1..2] a_ready[slot] (16 epilogue warps: next layer's A written), [3..4] d_full[slot]
-// (commit of layers 1-4), [5..6] a0_full[slot] (64 producer threads), [7..8] a0_empty[slot] (commit),
-// [9..10] o_full[slot] (commit of layer 5); TMEM base address at +120. (O(s) needs no "free" barrier:
-// the output warps read it before they arrive on a_ready(s) for the next tile's layer 4, which the
-// issuer waits for before it issues that tile's layer 5.)
+// barriers: weights; per slot a_ready (the 8 warps of the team that ran the layer: next layer's A
+// written), a0_full (64 producer threads), a0_empty (commit), o_full (commit of layer 5); per D region
+// d_full (commit of a layer 1-4 group) and d_empty (the region's team: the accumulator is in registers).
+// (O(s) needs no "free" barrier: the output warps read it before they arrive on a_ready(s) for the
+// next tile's layer 2, and layer 5 of that tile is issued after its layer-4 epilogue.)
 #ifndef PT_NIF_DIAG
 #define PT_NIF_DIAG 0   // diagnostic builds only (wrong results): 1 = no TMEM store of A, 2 = no sine,
-                        // 3 = no epilogue TMEM traffic (neither the accumulator load nor the A store)
+                        // 3 = no epilogue TMEM traffic (neither the accumulator load nor the A store),
+                        // 4 = hand-off only, 5 = no output layer work (exp, stores, throughput loads)
 #endif
-#ifndef PT_NIF_DEFER_ST
-#define PT_NIF_DEFER_ST 0   // measured slower (5.96 vs 7.25 G inferences/s, profiles/round2/nif_defer.log)
-#endif
-#ifndef PT_NIF_OUT_EARLY
-#define PT_NIF_OUT_EARLY 0
-#endif
-enum { kBarW = 0, kBarAReady = 1, kBarDFull = 3, kBarA0Full = 5, kBarA0Empty = 7, kBarOFull = 9 };
+enum {
+    kBarW = 0,
+    kBarAReady = 1,
+    kBarA0Full = kBarAReady + kIssuers * kSlots,   // a_ready(s, consumer p) at kBarAReady + kIssuers s + p
+    kBarA0Empty = kBarA0Full + kSlots,
+    kBarOFull = kBarA0Empty + kSlots,
+    kBarDFull = kBarOFull + kSlots,
+    kBarDEmpty = kBarDFull + kDRegions
+};
 
 constexpr uint32_t kTmemCols = 512;
-__host__ __device__ constexpr uint32_t d_col(int s) { return 256u * s; }
-__host__ __device__ constexpr uint32_t a_col(int s) { return 256u * s + 128u; }
-__host__ __device__ constexpr uint32_t o_col(int s) { return 256u * s + 208u; }
+__host__ __device__ constexpr uint32_t a_col(int s) { return 64u * s; }
+__host__ __device__ constexpr uint32_t o_col(int s) { return 192u + 16u * s; }
+constexpr uint32_t kConstCol = 240u;
+__host__ __device__ constexpr uint32_t d_col(int j) { return 256u + 128u * j; }
 
 // instruction descriptor: D f32, A/B f16, K-major both, M = 128, N given
 __host__ __device__ constexpr uint32_t idesc(int n) {
@@ -133,17 +166,26 @@ void nif_build_smem_image(const uint16_t* blob, std::vector<uint8_t>* image) {
 }
 
 #ifdef PT_NIF_TRACE
-// timing trace of CTA 0 (variant builds only): [role][record][2] clock64 stamps
-__device__ unsigned long long g_nif_trace[3 * 4096 * 2];
+// timing trace of CTA 0 (variant builds only): [role][record][4] clock64 stamps. Issuer (role 0):
+// 3 group start, 2 slot input ready, 0 D region free, 1 issued. Epilogue warp e (role 1 + e):
+// 0 accumulator committed, 2 accumulator in registers (D released), 1 A stored, 3 A handed over
+__device__ unsigned long long g_nif_trace[17 * 4096 * 4];
 #define NIF_TRACE(role, rec, k)                                                                           \
     do {                                                                                                  \
-        if (blockIdx.x == 0 && (rec) < 4096) g_nif_trace[((role) * 4096 + (rec)) * 2 + (k)] = clock64(); \
+        if (blockIdx.x == 0 && (rec) < 4096) g_nif_trace[((role) * 4096 + (rec)) * 4 + (k)] = clock64(); \
     } while (0)
 #else
 #define NIF_TRACE(role, rec, k) \
     do {                        \
     } while (0)
 #endif
+
+// slots of the round starting at tile t0 (tiles t0 + s * gridDim.x, s < kSlots, that exist)
+__device__ __forceinline__ int slots_in_round(uint32_t t0, uint32_t n_tiles) {
+    int n = 1;
+    while (n < siren::kSlots && t0 + (uint32_t)n * gridDim.x < n_tiles) ++n;
+    return n;
+}
 
 template <bool kDebug>
 __global__ void __launch_bounds__(siren::kThreads, 1)
@@ -153,7 +195,7 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
     using namespace siren;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBars);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBars + 120);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmemSlot);
     auto bar = [&](int b) { return smem_u32(&bars[b]); };
 
     const int warp = threadIdx.x >> 5;
@@ -162,12 +204,15 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
 
     if (warp == 1 && lane == 0) {
         mbar_init(bar(kBarW), 1);
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(bar(kBarAReady + s), kNumEpiWarps);
-            mbar_init(bar(kBarDFull + s), 1);
+        for (int s = 0; s < kSlots; ++s) {
+            for (int p = 0; p < kIssuers; ++p) mbar_init(bar(kBarAReady + kIssuers * s + p), kTeamWarps);
             mbar_init(bar(kBarA0Full + s), kProducerThreads);
             mbar_init(bar(kBarA0Empty + s), 1);
             mbar_init(bar(kBarOFull + s), 1);
+        }
+        for (int j = 0; j < kDRegions; ++j) {
+            mbar_init(bar(kBarDFull + j), 1);
+            mbar_init(bar(kBarDEmpty + j), kTeamWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -200,18 +245,23 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
     const uint32_t n_rows = *count;
     const uint32_t n_tiles = (n_rows + kTileM - 1) / kTileM;
 
-    if (warp == 0) {
-        // ===== MMA issuer: warp 0 walks the schedule, one elected lane issues =====
+    if (warp < kIssuers) {
+        // ===== MMA issuers: each walks the whole schedule and issues (one elected lane) its groups =====
+        const uint32_t me = (uint32_t)warp;
         if (blockIdx.x < n_tiles) {
             mbar_wait(bar(kBarW), 0);
             const uint32_t img = smem_u32(smem);
-            uint32_t a_phase[2] = {0, 0}, f_phase[2] = {0, 0};
-            bool pend[2] = {false, false};   // a tile of this slot still needs its output layer
+            // per-slot / per-region barrier phases and flags as bit masks (bit s), so the dynamic slot
+            // index needs no local-memory array
+            uint32_t a_phase = 0, f_phase = 0, e_phase = 0;
+            uint32_t pend = 0;               // bit s: a tile of slot s still needs its output layer
+            uint32_t out_by_me = 0;          // bit s: that output layer is this warp's to issue
             int rec = 0;
+            uint32_t g = 0;                  // layer 1-4 groups (D region g % 2)
             // layer 5 of the slot's previous tile: after its layer-4 epilogue (a_ready), into O(s)
             auto issue_out = [&](int s) {
-                mbar_wait(bar(kBarAReady + s), a_phase[s]);
-                a_phase[s] ^= 1;
+                mbar_wait(bar(kBarAReady + kIssuers * s + (int)me), (a_phase >> s) & 1u);
+                a_phase ^= 1u << s;
                 tc_fence_after();
                 if (elect_one()) {
                     const uint32_t base = img + kOffB5;
@@ -223,46 +273,61 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
                 }
                 __syncwarp();
             };
-            for (uint32_t i = 0;; i += 2) {
+            for (uint32_t i = 0;; i += kSlots) {
                 const uint32_t t0 = blockIdx.x + i * gridDim.x;
                 if (t0 >= n_tiles) break;
-                const int nslots = (t0 + gridDim.x < n_tiles) ? 2 : 1;
+                const int nslots = slots_in_round(t0, n_tiles);
                 for (int stage = 0; stage < 4; ++stage) {
-                    for (int s = 0; s < nslots; ++s, ++rec) {
+                    for (int s = 0; s < nslots; ++s, ++rec, ++g) {
+                        const int j = (int)(g & 1u);
+                        // the consumer of this group's epilogue is group g + nslots (the slot's next layer,
+                        // or for stage 3 the output layer issued with the slot's next layer 1)
+                        if (stage == 3) {
+                            const bool mine_out = kIssuers == 1 || ((g + (uint32_t)nslots) & 1u) == me;
+                            out_by_me = mine_out ? (out_by_me | 1u << s) : (out_by_me & ~(1u << s));
+                        }
+                        if (stage == 0) pend |= 1u << s;
+                        if (kIssuers > 1 && (uint32_t)j != me) continue;
+                        if (lane == 0) NIF_TRACE(0, rec, 3);
                         if (stage == 0) {
-                            if (pend[s]) issue_out(s);                   // previous tile's output layer
-                            mbar_wait(bar(kBarA0Full + s), f_phase[s]);  // layer-1 inputs staged
-                            f_phase[s] ^= 1;
+                            if (i > 0) issue_out(s);                               // previous tile's output layer
+                            mbar_wait(bar(kBarA0Full + s), (f_phase >> s) & 1u);  // layer-1 inputs staged
+                            f_phase ^= 1u << s;
                         } else {
-                            mbar_wait(bar(kBarAReady + s), a_phase[s]);  // this layer's A written
-                            a_phase[s] ^= 1;
+                            mbar_wait(bar(kBarAReady + kIssuers * s + (int)me), (a_phase >> s) & 1u);  // A written
+                            a_phase ^= 1u << s;
+                        }
+                        if (lane == 0) NIF_TRACE(0, rec, 2);
+                        if (g >= (uint32_t)kDRegions) {
+                            mbar_wait(bar(kBarDEmpty + j), (e_phase >> j) & 1u);  // D region's last group loaded
+                            e_phase ^= 1u << j;
                         }
                         if (lane == 0) NIF_TRACE(0, rec, 0);
                         tc_fence_after();
-                        const uint32_t dt = tmem + d_col(s);
+                        const uint32_t dt = tmem + d_col(j);
                         if (elect_one()) {
                             if (stage == 0) {
                                 const uint64_t a0 = smem_desc(smem_u32(smem + kOffA0 + s * kA0Bytes), 2048, 128);
                                 mma_ss(dt, a0, smem_desc(img, 2048, 128), idesc(128), 0);
-                                mma_commit(bar(kBarDFull + s));
+                                mma_commit(bar(kBarDFull + j));
                                 mma_commit(bar(kBarA0Empty + s));   // staging tile free once layer 1 is done
                             } else {
                                 const uint32_t base = img + kOffBH + (stage - 1) * kBHBytes;
                                 const uint32_t at = tmem + a_col(s);
 #pragma unroll
                                 for (int k = 0; k < 9; ++k)
-                                    mma_ts(dt, at + 8 * k, smem_desc(base + k * 2 * 2048, 2048, 128), idesc(128), k > 0);
-                                mma_commit(bar(kBarDFull + s));
+                                    mma_ts(dt, k < 8 ? at + 8 * k : tmem + kConstCol, smem_desc(base + k * 2 * 2048, 2048, 128),
+                                           idesc(128), k > 0);
+                                mma_commit(bar(kBarDFull + j));
                             }
                         }
                         __syncwarp();
-                        if (stage == 0) pend[s] = true;
                         if (lane == 0) NIF_TRACE(0, rec, 1);
                     }
                 }
             }
-            for (int s = 0; s < 2; ++s)
-                if (pend[s]) issue_out(s);                           // the last tiles' output layers
+            for (int s = 0; s < kSlots; ++s)                          // the last tiles' output layers
+                if ((pend >> s) & (out_by_me >> s) & 1u) issue_out(s);
         }
     } else if (warp == kProducerWarp0 || warp == kProducerWarp0 + 1) {
         // ===== producers: layer-1 inputs of every tile, staged one tile ahead per slot =====
@@ -270,20 +335,20 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
         // -> x0 = (2u-1, 2v-1) split into fp16 hi + lo (reading R15), constant-1 bias column.
         const int p = threadIdx.x - 32 * kProducerWarp0;
         uint8_t* a0s = smem + kOffA0;
-        for (int i = p; i < 2 * kA0Bytes / 16; i += kProducerThreads)
+        for (int i = p; i < kSlots * kA0Bytes / 16; i += kProducerThreads)
             *reinterpret_cast<uint4*>(a0s + 16 * i) = make_uint4(0, 0, 0, 0);
-        uint32_t e_phase[2] = {0, 0};
-        uint32_t fills[2] = {0, 0};
-        for (uint32_t i = 0;; i += 2) {
+        uint32_t e_phase = 0, filled = 0;   // bit s
+        for (uint32_t i = 0;; i += kSlots) {
             const uint32_t t0 = blockIdx.x + i * gridDim.x;
             if (t0 >= n_tiles) break;
-            const int nslots = (t0 + gridDim.x < n_tiles) ? 2 : 1;
+            const int nslots = slots_in_round(t0, n_tiles);
             for (int s = 0; s < nslots; ++s) {
                 const uint32_t tile = t0 + s * gridDim.x;
-                if (fills[s]++ > 0) {
-                    mbar_wait(bar(kBarA0Empty + s), e_phase[s]);
-                    e_phase[s] ^= 1;
+                if ((filled >> s) & 1u) {
+                    mbar_wait(bar(kBarA0Empty + s), (e_phase >> s) & 1u);
+                    e_phase ^= 1u << s;
                 }
+                filled |= 1u << s;
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int m = p + 64 * h;
@@ -307,45 +372,48 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
             }
         }
     } else if (warp >= kFirstEpiWarp) {
-        // ===== epilogue warps =====
-        // All 16 work on one (slot, layer) at a time, in the MMA's issue order. Warp w owns TMEM lane
-        // quarter w % 4 (hardware rule) and the 32-column block cb of the 128 columns.
+        // ===== epilogue warps: team t = D region t = the groups g with g % 2 == t, in issue order =====
+        // Warp e of a team owns TMEM lane quarter warp % 4 (hardware rule) and the 64-column half h.
         const int e = warp - kFirstEpiWarp;
-        const int cb = e >> 2;
+        const int team = e >> 3;
+        const int h = (e >> 2) & 1;
         const int q = warp & 3;
         const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
-        // constant-1 K block (A columns 64..71 = fp16 (1, 0, ... 0) per row) of both slots' A buffers
-        if (cb == 0) {
+        // the constant-1 K block (fp16 (1, 0, ... 0) per row) every layer's 9th K step reads
+        if (team == 0 && h == 0) {
             const uint32_t one[8] = {0x00003C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-            tmem_st8(tmem + a_col(0) + 64 + lane_addr, one);
-            tmem_st8(tmem + a_col(1) + 64 + lane_addr, one);
+            tmem_st8(tmem + kConstCol + lane_addr, one);
         }
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        // b5 (fp16 in the image's bias step of B5: row n, k = 128), added by the output warps once the
-        // weight image has landed (the bulk copies complete on kBarW)
+        // Output duty: slot s's output layer (O(s) -> exp -> store) is read by the warps (team s % 2,
+        // half s / 2) after the layer-1 epilogue of the slot's next tile -- stage k of slot s is group
+        // 4 kSlots r + kSlots k + s, run by team (kSlots k + s) % 2, so stages 0 and 2 of slot s belong to
+        // team s % 2: the rows' throughput and queue slot are loaded at stage 2 for the output at the next
+        // tile's stage 0.
+        const int my_slot = 2 * h + team;            // the slot this warp outputs (if < kSlots)
+        const bool out_warp = my_slot < kSlots;
         float b5[3] = {0.0f, 0.0f, 0.0f};
-        if (cb == 0) {
+        if (out_warp) {
             mbar_wait(bar(kBarW), 0);
 #pragma unroll
             for (int n = 0; n < 3; ++n)
                 b5[n] = __half2float(*reinterpret_cast<const __half*>(smem + kOffB5 + (16 * 2) * 128 + n * 16));
         }
-        uint32_t d_phase[2] = {0, 0}, o_phase[2] = {0, 0};
-        // the output rows of each slot's previous tile (cb == 0 warps): slot id, throughput, validity
-        float4 beta[2] = {make_float4(0, 0, 0, 0), make_float4(0, 0, 0, 0)};
-        uint32_t oslot[2] = {0, 0};
-        bool ovalid[2] = {false, false}, pend[2] = {false, false};
-        // layer 5 of the slot's previous tile: y = O[:, 0:3] + b5; radiance = beta * exp(y)
-        auto output = [&](int s, uint32_t dbg_row) {
-            mbar_wait(bar(kBarOFull + s), o_phase[s]);
-            o_phase[s] ^= 1;
+        uint32_t d_phase = 0, o_phase = 0;
+        float4 beta = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        uint32_t oslot = 0, prow = 0;
+        bool ovalid = false, pend = false;
+        // layer 5 of the owned slot's previous tile: y = O[:, 0:3] + b5; radiance = beta * exp(y)
+        auto output = [&](uint32_t dbg_row) {
+            mbar_wait(bar(kBarOFull + my_slot), o_phase);
+            o_phase ^= 1;
             tc_fence_after();
             uint32_t v[4];
-            tmem_ld4(tmem + o_col(s) + lane_addr, v);
+            tmem_ld4(tmem + o_col(my_slot) + lane_addr, v);
             tmem_wait_ld_dep4(v);
-            if (ovalid[s]) {
+            if (ovalid) {
                 const float y0 = __uint_as_float(v[0]) + b5[0], y1 = __uint_as_float(v[1]) + b5[1],
                             y2 = __uint_as_float(v[2]) + b5[2];
                 if (kDebug) {
@@ -353,114 +421,88 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
                     dbg[((size_t)4 * n_rows + dbg_row) * 128 + 1] = y1;
                     dbg[((size_t)4 * n_rows + dbg_row) * 128 + 2] = y2;
                 }
-                out[3 * (size_t)oslot[s] + 0] = beta[s].x * __expf(y0);
-                out[3 * (size_t)oslot[s] + 1] = beta[s].y * __expf(y1);
-                out[3 * (size_t)oslot[s] + 2] = beta[s].z * __expf(y2);
+                out[3 * (size_t)oslot + 0] = beta.x * __expf(y0);
+                out[3 * (size_t)oslot + 1] = beta.y * __expf(y1);
+                out[3 * (size_t)oslot + 2] = beta.z * __expf(y2);
             }
         };
-        uint32_t prow[2] = {0, 0};
-        // PT_NIF_DEFER_ST: a stage's TMEM store of A is completed (wait::st, fence, a_ready arrive) only
-        // after the next stage's accumulator load is issued, so the store latency overlaps it; a pending
-        // output read of the slot (cb == 0, layer 1) follows the hand-over
-        int held = -1;                 // slot whose A store is still to be completed and signalled
-        bool held_out = false;         // ... and whose previous tile's output is to be read after it
-        auto hand_over = [&]() {
-            if (held < 0) return;
-            tmem_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar(kBarAReady + held));
-            if (held_out) output(held, prow[held]);
-            held = -1;
-            held_out = false;
-        };
+        const uint32_t dreg = tmem + d_col(team) + lane_addr + 64u * (uint32_t)h;
         int rec = 0;
-        for (uint32_t i = 0;; i += 2) {
+        uint32_t g = 0;
+        for (uint32_t i = 0;; i += kSlots) {
             const uint32_t t0 = blockIdx.x + i * gridDim.x;
             if (t0 >= n_tiles) break;
-            const int nslots = (t0 + gridDim.x < n_tiles) ? 2 : 1;
+            const int nslots = slots_in_round(t0, n_tiles);
             for (int stage = 0; stage < 4; ++stage) {
-                for (int s = 0; s < nslots; ++s, ++rec) {
+                for (int s = 0; s < nslots; ++s, ++rec, ++g) {
+                    if ((int)(g & 1u) != team) continue;
                     const uint32_t tile = t0 + s * gridDim.x;
                     const uint32_t row = tile * kTileM + 32 * q + lane;
                     const bool valid = row < n_rows;
-                    // complete the held hand-over now unless this stage's accumulator is already there
-                    if (held >= 0 && !mbar_try(bar(kBarDFull + s), d_phase[s])) hand_over();
-                    mbar_wait(bar(kBarDFull + s), d_phase[s]);
-                    d_phase[s] ^= 1;
-                    const int trole = (warp == kFirstEpiWarp) ? 1 : (warp == kFirstEpiWarp + kNumEpiWarps - 1 ? 2 : -1);
-                    if (trole > 0 && lane == 0) NIF_TRACE(trole, rec, 0);
+                    mbar_wait(bar(kBarDFull + team), d_phase);
+                    d_phase ^= 1;
+                    if (lane == 0) NIF_TRACE(1 + e, rec, 0);
                     tc_fence_after();
-                    uint32_t v[32];
-                    uint32_t pk[16];
-                    if (kDebug) {
-                        TMEM_LD32(tmem + d_col(s) + lane_addr + 32 * cb, v);
-                        tmem_wait_ld_dep(v);
-                        if (valid)
-                            for (int j = 0; j < 32; ++j)
-                                dbg[((size_t)stage * n_rows + row) * 128 + 32 * cb + j] = __uint_as_float(v[j]);
-                        sine_half(v, 0, pk);
-                        sine_half(v + 16, 1, pk + 8);
-                    } else if (PT_NIF_DIAG == 4) {
-                        // diagnostic (wrong results): the epilogue only hands over (MMA + hand-off latency)
+                    const uint32_t areg = tmem + a_col(s) + lane_addr + 32u * (uint32_t)h;
+                    // two 32-column chunks: D (fp32) -> registers (the region is released after the
+                    // second load) -> sin -> fp16 pairs -> A of the next layer
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) pk[j] = (uint32_t)(j + lane);
-                    } else if (PT_NIF_DIAG == 3) {
-                        // diagnostic (wrong results): no TMEM traffic at all -- the sine on registers only
+                    for (int c = 0; c < 2; ++c) {
+                        uint32_t v[32];
+                        uint32_t pk[16];
+                        if (PT_NIF_DIAG == 3 || PT_NIF_DIAG == 4) {
+                            // diagnostic (wrong results): no accumulator load
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) v[j] = __float_as_uint((float)(j + lane) * 0.01f);
-                        sine_half(v, 0, pk);
-                        sine_half(v + 16, 1, pk + 8);
-                    } else if (PT_NIF_DIAG == 2) {
-                        // diagnostic (wrong results): TMEM round trip without the sine
-                        TMEM_LD32(tmem + d_col(s) + lane_addr + 32 * cb, v);
-                        tmem_wait_ld_dep(v);
+                            for (int k = 0; k < 32; ++k) v[k] = __float_as_uint((float)(k + lane) * 0.01f);
+                        } else {
+                            TMEM_LD32(dreg + 32u * (uint32_t)c, v);
+                            tmem_wait_ld_dep(v);
+                        }
+                        if (c == 1) {
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(bar(kBarDEmpty + team));
+                            if (lane == 0) NIF_TRACE(1 + e, rec, 2);
+                        }
+                        if (kDebug && valid)
+                            for (int k = 0; k < 32; ++k)
+                                dbg[((size_t)stage * n_rows + row) * 128 + 64 * h + 32 * c + k] = __uint_as_float(v[k]);
+                        if (PT_NIF_DIAG == 2 || PT_NIF_DIAG == 4) {
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) pk[j] = v[2 * j] ^ v[2 * j + 1];
-                    } else {
-                        // D (fp32) -> sin -> fp16: the second 16 columns load while the first are computed
-                        TMEM_LD16(tmem + d_col(s) + lane_addr + 32 * cb, v);
-                        hand_over();   // (the previous stage's, if held)
-                        tmem_wait_ld_dep16(v);
-                        TMEM_LD16(tmem + d_col(s) + lane_addr + 32 * cb + 16, v + 16);
-                        sine_half(v, 0, pk);
-                        tmem_wait_ld_dep16(v + 16);
-                        sine_half(v + 16, 1, pk + 8);
-                    }
-#if PT_NIF_OUT_EARLY
-                    if (cb == 0 && stage == 0 && pend[s]) output(s, prow[s]);   // O(prev) committed with layer 1
-#endif
-                    {
-                        // -> A of the next layer (this warp's 32 columns)
+                            for (int k = 0; k < 16; ++k) pk[k] = v[2 * k] ^ v[2 * k + 1];
+                        } else {
+                            sine_half(v, 0, pk);
+                            sine_half(v + 16, 1, pk + 8);
+                        }
                         if (PT_NIF_DIAG != 1 && PT_NIF_DIAG != 3 && PT_NIF_DIAG != 4) {
-                            TMEM_ST16(tmem + a_col(s) + lane_addr + 16 * cb, pk);
+                            TMEM_ST16(areg + 16u * (uint32_t)c, pk);
                         } else if (pk[0] == 0x7FFF7FFFu && pk[15] == 0x7FFF7FFFu) {   // diagnostic: keep pk live
                             out[0] = 0.0f;
                         }
                     }
-                    if (trole > 0 && lane == 0) NIF_TRACE(trole, rec, 1);
-                    held = s;
+                    if (lane == 0) NIF_TRACE(1 + e, rec, 1);
+                    tmem_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(bar(kBarAReady + kIssuers * s + (kIssuers > 1 ? (int)((g + (uint32_t)nslots) & 1u) : 0)));
                     // O(prev) was committed with this layer 1: read it once this warp's share of the next
                     // layer's A is handed over, off the MMA's critical path
-                    held_out = !PT_NIF_OUT_EARLY && cb == 0 && stage == 0 && pend[s];
-                    if (!PT_NIF_DEFER_ST || kDebug || PT_NIF_DIAG) hand_over();
-                    if (cb == 0 && stage == 1) {
+                    if (PT_NIF_DIAG != 5 && stage == 0 && s == my_slot && pend) output(prow);
+                    if (lane == 0) NIF_TRACE(1 + e, rec, 3);
+                    if (PT_NIF_DIAG != 5 && stage == 2 && s == my_slot) {
                         // this tile's output rows (after the previous tile's output was written)
-                        ovalid[s] = valid;
-                        prow[s] = row;
+                        ovalid = valid;
+                        prow = row;
                         if (valid) {
-                            beta[s] = __ldg(esc_beta + row);
-                            oslot[s] = __float_as_uint(__ldg(esc + row).w);
+                            beta = __ldg(esc_beta + row);
+                            oslot = __float_as_uint(__ldg(esc + row).w);
                         }
+                        pend = true;
                     }
-                    if (stage == 0) pend[s] = true;
                 }
             }
         }
-        hand_over();
-        if (cb == 0)
-            for (int s = 0; s < 2; ++s)
-                if (pend[s]) output(s, prow[s]);   // the last tiles' output layers
+        if (PT_NIF_DIAG != 5 && out_warp && pend) output(prow);   // the last tile's output layer of the owned slot
     }
     // a CTA without tiles still owns the weight copies in flight into its shared memory
     if (warp == 1 && lane == 0 && blockIdx.x >= n_tiles) mbar_wait(bar(kBarW), 0);

@@ -142,6 +142,50 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int iters, unsigned long long
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// commit round trip: one thread issues k TS MMAs (N = 128), commits, waits on the barrier; repeated.
+// cycles per round = k * issue interval + the fixed MMA-completion + commit-notify latency
+__global__ void __launch_bounds__(128, 1) commit_rtt(int k, int rounds, unsigned long long* out) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint32_t tslot;
+    __shared__ __align__(8) uint64_t bar;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tslot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tslot;
+    if (warp == 0 && lane == 0) {
+        const uint64_t bd = sdesc(smem_u32(smem), 16 * 128, 128);
+        unsigned long long t0 = clock64();
+        for (int r = 0; r < rounds; ++r) {
+            for (int i = 0; i < k; ++i) {
+                const uint32_t a = tmem + 384u + (uint32_t)(8 * (i % 8));
+                asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                             "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem), "r"(a),
+                             "l"(bd), "r"(idesc(128)), "r"((uint32_t)(i > 0)));
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
+            uint32_t ok = 0;
+            while (!ok)
+                asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                             "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_u32(&bar)), "r"((uint32_t)(r & 1)));
+        }
+        out[blockIdx.x] = clock64() - t0;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
 int main() {
     unsigned long long* d_out;
     cudaMalloc(&d_out, 148 * 8);
@@ -169,6 +213,20 @@ int main() {
         const double clk = (double)mx / iters;
         printf("%-16s N=%3d: %6.1f clk/MMA  %6.0f FLOP/clk/SM (%.0f%% of 8192)\n", mname[c.mode], n, clk,
                2.0 * 128 * n * 16 / clk, 100.0 * 2.0 * 128 * n * 16 / clk / 8192);
+    }
+    cudaFuncSetAttribute(commit_rtt, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    for (int grid : {1, 148}) {
+        for (int k : {1, 2, 4, 9, 18, 36}) {
+            const int rounds = 256;
+            commit_rtt<<<grid, 128, 64 * 1024>>>(k, rounds, d_out);
+            cudaError_t e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
+            unsigned long long h[148], mx = 0;
+            cudaMemcpy(h, d_out, sizeof(unsigned long long) * grid, cudaMemcpyDeviceToHost);
+            for (int i = 0; i < grid; ++i) mx = h[i] > mx ? h[i] : mx;
+            printf("commit round trip, grid %3d, %2d MMAs (N=128) per commit: %7.1f clk per round (%.1f per MMA)\n",
+                   grid, k, (double)mx / rounds, (double)mx / rounds / k);
+        }
     }
     return 0;
 }
