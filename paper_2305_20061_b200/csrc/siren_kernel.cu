@@ -37,6 +37,11 @@
 #include <vector>
 
 #include "pt_internal.h"
+// SFU share of the sine (tc_ptx.cuh): 10 of 16 column pairs on MUFU.SIN measured best with the team
+// epilogue (8.31 vs 8.04 G inferences/s at 9, 8.27 at 11; profiles/round2/nif_slots.log)
+#ifndef PT_NIF_MUFU_PAIRS
+#define PT_NIF_MUFU_PAIRS 10
+#endif
 #include "tc_ptx.cuh"
 
 namespace pt {
@@ -91,6 +96,9 @@ constexpr int kThreads = 32 * (kFirstEpiWarp + kNumEpiWarps);   // 640
 // d_full (commit of a layer 1-4 group) and d_empty (the region's team: the accumulator is in registers).
 // (O(s) needs no "free" barrier: the output warps read it before they arrive on a_ready(s) for the
 // next tile's layer 2, and layer 5 of that tile is issued after its layer-4 epilogue.)
+#ifndef PT_NIF_ISSUE_SLEEP
+#define PT_NIF_ISSUE_SLEEP 0   // ns the issuing lane sleeps after MMAs 3 and 6 of a layer (A/B knob)
+#endif
 #ifndef PT_NIF_DIAG
 #define PT_NIF_DIAG 0   // diagnostic builds only (wrong results): 1 = no TMEM store of A, 2 = no sine,
                         // 3 = no epilogue TMEM traffic (neither the accumulator load nor the A store),
@@ -315,9 +323,11 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
                                 const uint32_t base = img + kOffBH + (stage - 1) * kBHBytes;
                                 const uint32_t at = tmem + a_col(s);
 #pragma unroll
-                                for (int k = 0; k < 9; ++k)
+                                for (int k = 0; k < 9; ++k) {
                                     mma_ts(dt, k < 8 ? at + 8 * k : tmem + kConstCol, smem_desc(base + k * 2 * 2048, 2048, 128),
                                            idesc(128), k > 0);
+                                    if (PT_NIF_ISSUE_SLEEP > 0 && (k == 2 || k == 5)) __nanosleep(PT_NIF_ISSUE_SLEEP);
+                                }
                                 mma_commit(bar(kBarDFull + j));
                             }
                         }
