@@ -177,11 +177,16 @@ PT_API int pt_trace_rays(const pt_scene* scene, const float* d_o, const float* d
 PT_API int pt_nif_infer(const pt_nif* nif, const float* d_uv, int64_t n, float* d_rgb, void* stream);
 
 /* Statistics of the last pt_render / pt_render_samples on this scene handle (counts are exact;
-   kernel times are CUDA-event times summed over launches and are filled only while profiling is on). */
+   kernel times are CUDA-event times summed over launches and are filled only while profiling is on).
+   node_visits, prim_tests, fp64_rechecks (interior-node visits, primitive tests, primitive tests decided
+   by the fp64 fallback; PAPER.md:103 / SURVEY 8(b)) are filled only by the counting build of the library
+   (-DPT_COUNT, tools/trace_count.py: process-wide counters of the last render); -1 otherwise, since
+   counting costs an atomic per visit. */
 typedef struct {
     int64_t paths, segments, escaped, waves, launches;
     double t_raygen_ms, t_traverse_ms, t_shade_ms, t_nif_ms, t_accum_ms;
     int64_t nif_launches, traverse_launches;
+    int64_t node_visits, prim_tests, fp64_rechecks;
 } pt_stats;
 PT_API int pt_get_stats(const pt_scene* scene, pt_stats* out);
 

@@ -254,6 +254,7 @@ int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, i
     if ((int64_t)W * H > (1ll << 31) / 2) return fail(PT_ERR_INVALID_ARG, "frame too large");
     const int64_t np = (int64_t)W * (row1 - row0);   // pixels rendered
     const int64_t p0 = (int64_t)W * row0;
+    pt::trav_counts_reset();                          // counting build only (pt_get_stats)
     int64_t k = wave_samples;
     // automatic wave: ~64 M paths (one wave per frame up to that size): fewer wave tails and NIF launches
     // (config 3: 2.19 -> 2.34 G samples/s from 8 to 66 M paths per wave, profiles/round2/wave_k_c3.log)
@@ -665,6 +666,8 @@ int pt_get_stats(const pt_scene* scene, pt_stats* out) {
         out->segments = (int64_t)h[1];
         out->escaped = (int64_t)h[2];
     }
+    out->node_visits = out->prim_tests = out->fp64_rechecks = -1;
+    if (pt::trav_counts(&out->node_visits, &out->prim_tests, &out->fp64_rechecks)) CU(cudaGetLastError());
     return PT_OK;
 }
 

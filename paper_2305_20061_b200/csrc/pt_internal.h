@@ -174,6 +174,9 @@ void launch_pack_queries(const float* uv, int64_t n, float4* esc, float4* esc_be
 
 // NIF (nif_kernel.cu)
 int64_t nif_smem_image_bytes();
+// counting build (-DPT_COUNT) traversal counters: false / no-op in the product build
+bool trav_counts(int64_t* visits, int64_t* prim_tests, int64_t* fp64);
+void trav_counts_reset();
 void nif_build_smem_image(const uint16_t* blob, std::vector<uint8_t>* image);
 void nif_build_smem_image_fr(const uint16_t* blob, std::vector<uint8_t>* image);
 cudaError_t launch_nif(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,

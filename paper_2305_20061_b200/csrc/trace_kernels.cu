@@ -480,6 +480,11 @@ __device__ __forceinline__ void test_prim(const uint4* __restrict__ pool, uint32
     best.thi = exact ? __double2float_ru(t64) : thi;
 }
 
+// child order at an interior node: 5 = full sorting network; 3 = nearest first, the other three only
+// partially ordered (A/B knob: the closest hit does not depend on the visit order, ties break on (t, id))
+#ifndef PT_CHILD_SORT
+#define PT_CHILD_SORT 5
+#endif
 __device__ __forceinline__ void cswap(float& ta, uint32_t& oa, float& tb, uint32_t& ob) {
     if (tb < ta) {
         const float t = ta; ta = tb; tb = t;
@@ -607,8 +612,10 @@ __device__ __forceinline__ void trav_round(const TraceParams& tp, Trav& t, uint3
             cswap(ctn[0], cent[0], ctn[1], cent[1]);
             cswap(ctn[2], cent[2], ctn[3], cent[3]);
             cswap(ctn[0], cent[0], ctn[2], cent[2]);
-            cswap(ctn[1], cent[1], ctn[3], cent[3]);
-            cswap(ctn[1], cent[1], ctn[2], cent[2]);
+            if (PT_CHILD_SORT == 5) {
+                cswap(ctn[1], cent[1], ctn[3], cent[3]);
+                cswap(ctn[1], cent[1], ctn[2], cent[2]);
+            }
             // (non-hit children carry +inf; the bound may be +inf, so test finiteness explicitly)
 #pragma unroll
             for (int ci = 3; ci >= 1; --ci)
@@ -1389,6 +1396,29 @@ extern "C" __attribute__((visibility("default"))) int pt_debug_trav_counts(unsig
     return 0;
 }
 #endif
+
+namespace pt {
+// traversal counters of the counting build (pt_get_stats): reset at the start of a render, read after it
+bool trav_counts(int64_t* visits, int64_t* prim_tests, int64_t* fp64) {
+#ifdef PT_COUNT
+    unsigned long long h[8];
+    if (cudaMemcpyFromSymbol(h, g_trav_count, sizeof(h)) != cudaSuccess) return false;
+    *visits = (int64_t)h[0];
+    *prim_tests = (int64_t)h[2];
+    *fp64 = (int64_t)h[3];
+    return true;
+#else
+    (void)visits; (void)prim_tests; (void)fp64;
+    return false;
+#endif
+}
+void trav_counts_reset() {
+#ifdef PT_COUNT
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_trav_count, z, sizeof(z));
+#endif
+}
+}  // namespace pt
 
 #ifdef PT_TAIL_TRACE
 extern "C" __attribute__((visibility("default"))) int pt_debug_tail(unsigned long long* host) {

@@ -26,7 +26,8 @@ class PtStats(C.Structure):
     _fields_ = [("paths", C.c_int64), ("segments", C.c_int64), ("escaped", C.c_int64), ("waves", C.c_int64),
                 ("launches", C.c_int64), ("t_raygen_ms", C.c_double), ("t_traverse_ms", C.c_double),
                 ("t_shade_ms", C.c_double), ("t_nif_ms", C.c_double), ("t_accum_ms", C.c_double),
-                ("nif_launches", C.c_int64), ("traverse_launches", C.c_int64)]
+                ("nif_launches", C.c_int64), ("traverse_launches", C.c_int64),
+                ("node_visits", C.c_int64), ("prim_tests", C.c_int64), ("fp64_rechecks", C.c_int64)]
 
 
 EXPORTED = ["pt_scene_create", "pt_scene_destroy", "pt_nif_load", "pt_nif_load_ex", "pt_nif_load_family",

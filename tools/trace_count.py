@@ -51,7 +51,11 @@ for cfg in (1, 2, 3, 4):
     counts()
     pt.render_samples(S, N, c.width, c.height, 0, spp, c.max_depth, 0, acc, env_rgb=None if c.use_nif else c.env_rgb,
                       wave_samples=min(c.wave_samples, spp))
+    st = S.stats()
     k = counts()
+    # the public statistics of the counting build carry the same counters (pt_get_stats)
+    assert (st["node_visits"], st["prim_tests"], st["fp64_rechecks"]) == (k["node_visits"], k["prim_tests"],
+                                                                          k["fp64_tests"]), (st, k)
     k["spp"] = spp
     k["per_segment"] = {"visits": k["node_visits"] / k["rays"], "prims": k["prim_tests"] / k["rays"],
                         "fp64": k["fp64_tests"] / k["rays"]}
