@@ -453,3 +453,28 @@ def test_concurrent_streams_match_sequential(ptm, blob):
         torch.cuda.synchronize()
         assert torch.equal(o1, ref1) and torch.equal(o2, ref2)
         assert torch.equal(g1, fr1) and torch.equal(g2, fr2)
+
+
+@pytest.mark.parametrize("n_tiles", [1, 149, 148 * 2 + 77, 148 * 3, 148 * 4 + 147, 148 * 5 + 1, 148 * 6 + 100, 148 * 8])
+def test_nif_schedule_rounds(ptm, orc, blob, n_tiles):
+    """The SIREN kernel runs three 128-row tiles per CTA round (tiles b + s * grid, s < 3) with the layer
+    groups rotating over two accumulator regions, two epilogue teams and two issuers; a CTA's last round
+    holds 1, 2 or 3 tiles. Query counts whose tile counts end every CTA on each of those cases (and a
+    ragged last tile): sampled rows (the first and last tile in full) against the oracle, and the whole
+    output bit-identical across two launches (a barrier-protocol race would show as a difference)."""
+    import torch
+    n = n_tiles * 128 - 37
+    uv = scenes.query_uv(n, 11)
+    nif = ptm.Nif(blob)
+    q = torch.from_numpy(uv).cuda()
+    a = ptm.nif_infer(nif, q).cpu().numpy()
+    b = ptm.nif_infer(nif, q).cpu().numpy()
+    assert np.array_equal(a, b)
+    rng = np.random.default_rng(n_tiles)
+    idx = np.unique(np.concatenate([np.arange(min(128, n)), np.arange(max(0, n - 128), n),
+                                    rng.integers(0, n, size=min(n, 1536))]))
+    y = orc.nif_eval(blob, uv[idx].astype(np.float64))
+    got = a[idx].astype(np.float64)
+    assert np.isfinite(got).all()
+    assert np.abs(np.log(got) - y).max() <= NIF_LOG_GATE
+    assert (np.abs(got - np.exp(y)) / np.exp(y)).max() <= NIF_REL_GATE
