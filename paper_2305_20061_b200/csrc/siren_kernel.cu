@@ -7,12 +7,13 @@
 //
 // Design. One persistent CTA per SM keeps the weights resident in shared memory
 // (one bulk TMA copy per CTA). kSlots (3) 128-ray tiles ("slots") are in flight: the tensor core runs
-// one slot's layer while 16 epilogue warps apply the sine to another slot's accumulator. A layer's
-// MMA group takes ~1,300 cycles from issue to a visible commit against 576 cycles of tensor work
-// (tools/mma_shapes.cu "commit/9 + wait"), so with two slots each slot's chain (MMA latency + sine
-// epilogue) left the tensor pipe idle about half the time; three slots cover it. Accumulators are not
-// owned by slots: layer groups rotate over two D regions in issue order, and the epilogue frees a D
-// region (d_empty) as soon as its 32 columns are in registers, before the sine.
+// one slot's layer while an 8-warp epilogue team applies the sine to another slot's accumulator. A
+// 9-MMA layer group takes ~880 cycles from issue to a visible commit (tools/mma_shapes.cu commit round
+// trip: ~240 fixed + ~71 per MMA) against 576 cycles of tensor work, and each slot's chain then adds its
+// sine epilogue, so with two slots the tensor pipe idled about half the time; three slots cover more
+// of it. Accumulators are not owned by slots: layer groups rotate over two D regions in issue order,
+// team t runs the groups of region t, and a warp frees the region (d_empty) as soon as its 64 columns
+// are in registers, before the sine.
 //   * Layer 1 (2 -> 128): one SS MMA, K = 16, A = a shared-memory tile staged by two producer warps
 //     (equirect, hi/lo split of x0, constant-1 bias column), so no epilogue work is spent on inputs.
 //   * Layers 2-4 (128 -> 128): 9 TS MMAs, M = N = 128, K = 16 each; A = the previous layer's fp16
@@ -21,10 +22,10 @@
 //     TMEM/SMEM A switch inside a layer (~50 cycles each).
 //   * Layer 5 (128 -> 3): 8 TS MMAs with N = 16 into the slot's own output columns O (b5 is added by the
 //     output warps). It is issued together with layer 1 of the slot's next tile (one commit group), so
-//     the tensor pipe never holds an output layer in front of the MMA the epilogue needs next; the 4
-//     warps owning TMEM lane quarters at column block 0 read O(prev tile) during the next tile's first
-//     sine stage (exp, beta, store). (On the FMA pipe inside the layer-4 epilogue it lengthened the
-//     epilogue, the bottleneck, by ~700 cycles per tile: tools/nif_trace.py.)
+//     the tensor pipe never holds an output layer in front of the MMA the epilogue needs next; the slot's
+//     4 output warps (team s % 2, column half s / 2, one per TMEM lane quarter) read O(prev tile) after
+//     handing over the next tile's layer-1 epilogue (exp, beta, store). (On the FMA pipe inside the
+//     layer-4 epilogue it lengthened the epilogue by ~700 cycles per tile in round 1.)
 // TMEM (512 columns): A(s) at 64 s (64 columns of fp16 pairs), O(s) at 192 + 16 s (16 columns), the
 // constant-1 K block shared by all slots at 240 (8 columns), D regions at 256 and 384 (128 fp32 columns
 // each). A is single-buffered: each layer's epilogue starts after the layer's one commit, i.e. after
