@@ -731,6 +731,11 @@ struct ShadeArgs {
     uint32_t p0;                // its first pixel (row0 W): slot i = (pixel p0 + i % np, sample first + i / np)
     uint32_t tiles_x;           // > 0: the first bounce visits the slots in 8 x 4 pixel tiles (W % 8 == 0, rows % 4 == 0)
     float inv_tiles_x;
+    uint32_t g_log2;            // PT_TILE_ORDER 2: a warp = 2^g_log2 samples x (32 >> g_log2) consecutive pixels
+    uint32_t npg;               // ... pixel groups (np / (32 >> g_log2)); 0: not in use
+    float inv_npg;
+    uint32_t k_wave;            // samples of the wave; with npg != 0 the wave buffer is pixel-major:
+                                // radiance of slot (pixel p, sample s) at index p * k_wave + s
     uint2 key;
     const uint32_t* counters;   // the wave's counters (pt_internal.h kCounters layout)
     uint32_t n_slots;           // paths of the wave
@@ -885,6 +890,16 @@ __device__ __forceinline__ void shade_segment(const ShadeArgs& a, int depth, uin
 #endif
 constexpr uint32_t kTileW = PT_TILE_W, kTileH = 32 / PT_TILE_W;
 __device__ __forceinline__ uint32_t tile_slot(const ShadeArgs& a, uint32_t w) {
+    if (a.npg != 0u) {
+        // 32 consecutive work indices = 2^g samples of (32 >> g) consecutive pixels (nearly the same
+        // camera ray: coherent traversal); consecutive warps walk the pixels, then the sample groups
+        uint32_t pg;
+        const uint32_t sg = udiv_exact(w >> 5, a.npg, a.inv_npg, pg);
+        const uint32_t k = w & 31u;
+        const uint32_t pix = (pg << (5u - a.g_log2)) + (k >> a.g_log2);
+        const uint32_t smp = (sg << a.g_log2) + (k & ((1u << a.g_log2) - 1u));
+        return smp * (uint32_t)a.np + pix;
+    }
     if (a.tiles_x == 0u) return w;
     uint32_t q, tx;
     const uint32_t s = udiv_exact(w, (uint32_t)a.np, a.inv_np, q);
@@ -910,18 +925,29 @@ __device__ __forceinline__ float3 camera_ray(const ShadeArgs& a, uint32_t i) {
 #define PT_REPLACE_MIN_DEPTH 6   // BVH depth (4-wide levels) from which the replacement kernel runs
 #endif
 #ifndef PT_TILE_ORDER
-#define PT_TILE_ORDER 1          // first-bounce slots in 8 x 4 pixel tiles (tile_slot)
+#define PT_TILE_ORDER 2          // first-bounce warps: 2 = a pixel's samples together (sample_group_log2),
+                                 // else 8 x 4 pixel tiles of one sample (1), or linear (0)
 #endif
 #ifndef PT_TS_MINB
 #define PT_TS_MINB 7   // min resident blocks per SM for the path kernels: 72-register cap; tools/ts_tune.sh
 #endif
 
-// Warp-aggregated append (one atomic per warp), returns this lane's position
+// Index of a slot's radiance in the wave buffer (and the NIF's output row): the slot itself
+// (sample-major), or pixel-major p * k + s when the first bounce runs a pixel's samples in one warp, so
+// the radiance stores of those lanes (and the NIF's, whose queue follows the same order) are contiguous
+__device__ __forceinline__ uint32_t buf_index(const ShadeArgs& a, uint32_t slot) {
+    if (a.npg == 0u) return slot;
+    uint32_t p;
+    const uint32_t sm = udiv_exact(slot, (uint32_t)a.np, a.inv_np, p);
+    return p * a.k_wave + sm;
+}
+
 __device__ __forceinline__ void write_radiance(const ShadeArgs& a, const SegOut& r, uint32_t slot) {
     if (r.done) {
-        a.wave_buf[3 * (size_t)slot + 0] = r.L.x;
-        a.wave_buf[3 * (size_t)slot + 1] = r.L.y;
-        a.wave_buf[3 * (size_t)slot + 2] = r.L.z;
+        const uint32_t b = buf_index(a, slot);
+        a.wave_buf[3 * (size_t)b + 0] = r.L.x;
+        a.wave_buf[3 * (size_t)b + 1] = r.L.y;
+        a.wave_buf[3 * (size_t)b + 2] = r.L.z;
     }
 }
 
@@ -969,7 +995,7 @@ __global__ void __launch_bounds__(128, PT_FB_MINB) first_bounce_kernel(ShadeArgs
             eb = __shfl_sync(0xFFFFFFFFu, eb, 0);
             if (r.escaped) {
                 const uint32_t pos = eb + (uint32_t)__popc(me & lt);
-                a.esc[pos] = make_float4(r.d.x, r.d.y, r.d.z, __uint_as_float(i));
+                a.esc[pos] = make_float4(r.d.x, r.d.y, r.d.z, __uint_as_float(buf_index(a, i)));
                 a.esc_beta[pos] = make_float4(r.beta.x, r.beta.y, r.beta.z, 0.0f);
             }
         }
@@ -1068,7 +1094,7 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
                 old = __shfl_sync(0xFFFFFFFFu, old, leader);
                 if (r.escaped) {
                     const uint32_t pos = (uint32_t)old + (uint32_t)__popc(me & lt);
-                    a.esc[pos] = make_float4(r.d.x, r.d.y, r.d.z, __uint_as_float(slot));
+                    a.esc[pos] = make_float4(r.d.x, r.d.y, r.d.z, __uint_as_float(buf_index(a, slot)));
                     a.esc_beta[pos] = make_float4(r.beta.x, r.beta.y, r.beta.z, 0.0f);
                 }
                 if (mneed) refill(old, mneed);
@@ -1124,7 +1150,7 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
                 old = __shfl_sync(0xFFFFFFFFu, old, leader);
                 if (r.escaped) {
                     const uint32_t pos = (uint32_t)old + (uint32_t)__popc(me & lt);
-                    a.esc[pos] = make_float4(r.d.x, r.d.y, r.d.z, __uint_as_float(slot));
+                    a.esc[pos] = make_float4(r.d.x, r.d.y, r.d.z, __uint_as_float(buf_index(a, slot)));
                     a.esc_beta[pos] = make_float4(r.beta.x, r.beta.y, r.beta.z, 0.0f);
                 }
                 refill(old, mneed);
@@ -1139,9 +1165,9 @@ __global__ void __launch_bounds__(128, PT_TS_MINB) path_kernel(ShadeArgs a) {
 
 // S6: fb += the wave's per-slot radiance, summed over its k samples in sample order (deterministic); one
 // thread also folds the wave's counters into the scene's statistics (paths, segments, escaped)
-__global__ void accumulate_kernel(const float* __restrict__ wave_buf, int n_elems, int k, float* __restrict__ fb,
-                                  const uint32_t* __restrict__ counters, unsigned long long* __restrict__ stats,
-                                  uint32_t paths) {
+__global__ void accumulate_kernel(const float* __restrict__ wave_buf, int n_elems, int k, int pixel_major,
+                                  float* __restrict__ fb, const uint32_t* __restrict__ counters,
+                                  unsigned long long* __restrict__ stats, uint32_t paths) {
     pdl_wait();
     if (blockIdx.x == 0 && threadIdx.x == 0 && stats) {
         stats[0] += paths;
@@ -1150,8 +1176,44 @@ __global__ void accumulate_kernel(const float* __restrict__ wave_buf, int n_elem
     }
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n_elems; e += gridDim.x * blockDim.x) {
         float s = fb[e];
-        for (int j = 0; j < k; ++j) s += __ldg(wave_buf + (size_t)j * n_elems + e);   // fixed sample order
+        if (pixel_major) {
+            const int p = e / 3, c = e - 3 * p;
+            const float* w = wave_buf + (size_t)3 * k * p + c;
+            for (int j = 0; j < k; ++j) s += __ldg(w + 3 * j);                         // fixed sample order
+        } else {
+            for (int j = 0; j < k; ++j) s += __ldg(wave_buf + (size_t)j * n_elems + e);   // fixed sample order
+        }
         fb[e] = s;
+    }
+}
+
+// Pixel-major wave buffer (PT_TILE_ORDER 2, k % 4 == 0): one thread per pixel reads its 3 k contiguous
+// floats as float4s and adds them per component in sample order (the same fixed order as the
+// sample-major path, so frames are bit-identical for any wave split)
+__global__ void accumulate_pm_kernel(const float4* __restrict__ wave_buf, int np, int k, float* __restrict__ fb,
+                                     const uint32_t* __restrict__ counters, unsigned long long* __restrict__ stats,
+                                     uint32_t paths) {
+    pdl_wait();
+    if (blockIdx.x == 0 && threadIdx.x == 0 && stats) {
+        stats[0] += paths;
+        stats[1] += counters[kCounterSeg];
+        stats[2] += counters[kCounterEsc];
+    }
+    const int n4 = 3 * k / 4;   // float4s per pixel
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < np; p += gridDim.x * blockDim.x) {
+        float acc[3] = {fb[3 * p + 0], fb[3 * p + 1], fb[3 * p + 2]};
+        const float4* w = wave_buf + (size_t)p * n4;
+        int c = 0;   // component of the next float
+        for (int q = 0; q < n4; ++q) {
+            const float4 v = __ldg(w + q);
+            acc[c] += v.x; c = c == 2 ? 0 : c + 1;
+            acc[c] += v.y; c = c == 2 ? 0 : c + 1;
+            acc[c] += v.z; c = c == 2 ? 0 : c + 1;
+            acc[c] += v.w; c = c == 2 ? 0 : c + 1;
+        }
+        fb[3 * p + 0] = acc[0];
+        fb[3 * p + 1] = acc[1];
+        fb[3 * p + 2] = acc[2];
     }
 }
 
@@ -1299,6 +1361,16 @@ static int3 path_grids() {
     return make_int3(a, b, c);
 }
 
+// PT_TILE_ORDER 2: a first-bounce warp takes 2^g samples of 32 / 2^g consecutive pixels, the largest
+// g <= 5 with 2^g dividing the wave's samples k and 32 / 2^g dividing np; -1 (8 x 4 tiles of one
+// sample, or linear order) when only g = 0 fits
+int sample_group_log2(int np, int k) {
+    if (PT_TILE_ORDER != 2) return -1;
+    for (int g = 5; g >= 1; --g)
+        if (k % (1 << g) == 0 && np % (32 >> g) == 0) return g;
+    return -1;
+}
+
 void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int p0, int np, int first_sample, int n_slots,
                   int max_depth, uint64_t seed, int use_nif, float3 env, Workspace& ws, cudaStream_t st) {
     ShadeArgs a;
@@ -1311,6 +1383,11 @@ void launch_paths(const TraceParams& tp, const Cam32& cam, int W, int H, int p0,
     a.inv_np = 1.0f / (float)np;
     a.tiles_x = (PT_TILE_ORDER && W % kTileW == 0 && (np / W) % kTileH == 0) ? (uint32_t)(W / kTileW) : 0u;
     a.inv_tiles_x = a.tiles_x ? 1.0f / (float)a.tiles_x : 0.0f;
+    a.k_wave = (uint32_t)(n_slots / np);
+    const int g = sample_group_log2(np, n_slots / np);
+    a.g_log2 = g > 0 ? (uint32_t)g : 0u;
+    a.npg = g > 0 ? (uint32_t)(np / (32 >> g)) : 0u;
+    a.inv_npg = g > 0 ? 1.0f / (float)a.npg : 0.0f;
     a.inv_w = 1.0f / (float)W;
     a.key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
     a.counters = ws.counters;
@@ -1337,8 +1414,14 @@ int path_launches(int max_depth) { return max_depth > 1 ? 2 : 1; }
 void launch_accumulate(const float* wave_buf, int n_pix, int k, float* fb, const uint32_t* counters,
                        unsigned long long* stats, uint32_t paths, cudaStream_t st) {
     const int n = 3 * n_pix;
-    launch_pdl(accumulate_kernel, dim3(grid_for(n, 256, 8)), dim3(256), 0, st, wave_buf, n, k, fb, counters, stats,
-               paths);
+    const int pixel_major = sample_group_log2(n_pix, k) > 0 ? 1 : 0;   // the layout launch_paths used
+    if (pixel_major && k % 4 == 0) {
+        launch_pdl(accumulate_pm_kernel, dim3(grid_for(n_pix, 256, 8)), dim3(256), 0, st,
+                   reinterpret_cast<const float4*>(wave_buf), n_pix, k, fb, counters, stats, paths);
+        return;
+    }
+    launch_pdl(accumulate_kernel, dim3(grid_for(n, 256, 8)), dim3(256), 0, st, wave_buf, n, k, pixel_major, fb,
+               counters, stats, paths);
 }
 
 void launch_primary(const TraceParams& tp, const Cam32& cam, int W, int H, int sample, uint64_t seed, int32_t* prim,
