@@ -393,7 +393,7 @@ def main():
     e2e_steps = max(3, min(2 * args.steps, 40))
     host_fb = torch.empty(W * H * 3, dtype=torch.float32, pin_memory=True)
     host_np = host_fb.numpy()
-    auto_k = max(1, min(spp, (64 << 20) // (W * H)))      # pt_render's wave size (pt_api.cu)
+    auto_k = max(1, min(spp, (1 << 28) // (W * H)))      # pt_render's wave size (pt_api.cu)
     host_render = world == 1 and auto_k == cfg.wave_samples
     src, blob, env = R.src, R.blob, R.env
     h2d = src.tris.nbytes + src.spheres.nbytes + src.materials.nbytes + src.camera.nbytes + (blob.nbytes if blob is not None else 0)

@@ -131,8 +131,8 @@ PT_API int pt_render(const pt_scene* scene, const pt_nif* nif, const float env_r
 
 /* Multi-GPU / framework path: ADD the per-pixel SUM over samples [first_sample, first_sample +
    n_samples) into the caller-owned DEVICE buffer d_accum[width*height*3] (fp32, row-major [H][W][3]).
-   wave_samples (k >= 1, or 0 = automatic) bounds how many consecutive samples share one wavefront
-   wave (k * width * height paths in flight). Results are bit-identical for any partition of the
+   wave_samples (k >= 1, or 0 = automatic: up to 2^28 paths, 108 B of device scratch each) bounds how
+   many consecutive samples share one wavefront wave (k * width * height paths in flight). Results are bit-identical for any partition of the
    sample range that keeps wave boundaries, and independent of k up to fp32 summation order.
    Asynchronous on `stream`. Errors: INVALID_ARG, CUDA, OOM. */
 PT_API int pt_render_samples(const pt_scene* scene, const pt_nif* nif, const float env_rgb[3], int32_t width,

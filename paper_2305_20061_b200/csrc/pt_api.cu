@@ -256,9 +256,11 @@ int render_samples_impl(pt_scene* sc, const pt_nif* nif, const float* env_rgb, i
     const int64_t p0 = (int64_t)W * row0;
     pt::trav_counts_reset();                          // counting build only (pt_get_stats)
     int64_t k = wave_samples;
-    // automatic wave: ~64 M paths (one wave per frame up to that size): fewer wave tails and NIF launches
-    // (config 3: 2.19 -> 2.34 G samples/s from 8 to 66 M paths per wave, profiles/round2/wave_k_c3.log)
-    if (k <= 0) k = std::max<int64_t>(1, std::min<int64_t>(n_samples, (int64_t)(64 << 20) / np));
+    // automatic wave: up to 2^28 paths (29 GB of wave state; one wave per frame up to that size): fewer
+    // wave tails and NIF launches, and the first bounce's sample groups reach 32 samples per pixel
+    // (config 3: 2.19 -> 2.34 G samples/s from 8 to 66 M paths per wave, profiles/round2/wave_k_c3.log;
+    // config 4: 2.66 -> 2.86 G from 66 to 265 M, profiles/round2/wavek.log)
+    if (k <= 0) k = std::max<int64_t>(1, std::min<int64_t>(n_samples, (int64_t)(1 << 28) / np));
     k = std::min<int64_t>(k, n_samples);
     while (k > 1 && k * np > (1ll << 31)) --k;
     int rc = ensure_ws(sc);

@@ -80,7 +80,7 @@ CONFIGS = [
     RenderConfig(1, "box_nif", 512, 512, 16, 8, True, wave_samples=16),
     RenderConfig(2, "spheres_nif", 1024, 1024, 64, 12, True, wave_samples=64),
     RenderConfig(3, "small_bvh_nif", 1920, 1080, 32, 8, True, wave_samples=32),
-    RenderConfig(4, "large_bvh", 3840, 2160, 64, 8, False, env_rgb=(1.0, 1.0, 1.0), wave_samples=8),
+    RenderConfig(4, "large_bvh", 3840, 2160, 64, 8, False, env_rgb=(1.0, 1.0, 1.0), wave_samples=32),
 ]
 
 
