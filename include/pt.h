@@ -129,6 +129,18 @@ PT_API int pt_nif_destroy(pt_nif* nif);
 PT_API int pt_render(const pt_scene* scene, const pt_nif* nif, const float env_rgb[3], int32_t width, int32_t height,
               int32_t spp, int32_t max_depth, uint64_t seed, float* out_rgb);
 
+/* pt_render enqueued on `stream` (a cudaStream_t; NULL = the legacy default stream) without waiting:
+   the frame, its scaling and the copy into out_rgb are ordered on the stream, and out_rgb holds the
+   frame once the stream reaches that point (cudaStreamSynchronize / an event). out_rgb should be
+   page-locked host memory (cudaHostAlloc or registered; pageable memory makes the copy synchronous).
+   The caller keeps scene, nif and out_rgb alive until then; calls on one scene handle are ordered only
+   when they use the same stream (the scene's framebuffer is reused). Successive frames on two streams
+   (with two scene handles) overlap one frame's read-back with the next frame's kernels.
+   Errors: INVALID_ARG, CUDA, OOM (launch errors; execution errors surface at the next synchronisation). */
+PT_API int pt_render_async(const pt_scene* scene, const pt_nif* nif, const float env_rgb[3], int32_t width,
+                           int32_t height, int32_t spp, int32_t max_depth, uint64_t seed, float* out_rgb,
+                           void* stream);
+
 /* Multi-GPU / framework path: ADD the per-pixel SUM over samples [first_sample, first_sample +
    n_samples) into the caller-owned DEVICE buffer d_accum[width*height*3] (fp32, row-major [H][W][3]).
    wave_samples (k >= 1, or 0 = automatic: up to 2^28 paths, 108 B of device scratch each) bounds how

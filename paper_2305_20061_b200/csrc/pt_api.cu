@@ -548,8 +548,11 @@ int pt_render_rows(const pt_scene* scene, const pt_nif* nif, const float env_rgb
                                wave_samples, d_accum, (cudaStream_t)stream);
 }
 
-int pt_render(const pt_scene* scene, const pt_nif* nif, const float env_rgb[3], int32_t width, int32_t height,
-              int32_t spp, int32_t max_depth, uint64_t seed, float* out_rgb) {
+namespace {
+// pt_render / pt_render_async: frame into the scene's device framebuffer, scale, copy to the host buffer
+// on `st` (the scene's own stream for pt_render); synchronous when `sync`
+int render_frame(const pt_scene* scene, const pt_nif* nif, const float env_rgb[3], int32_t width, int32_t height,
+                 int32_t spp, int32_t max_depth, uint64_t seed, float* out_rgb, void* stream, bool sync) {
     if (!scene || !out_rgb) return fail(PT_ERR_INVALID_ARG, "null argument");
     if (width < 1 || height < 1 || spp < 1 || max_depth < 1) return fail(PT_ERR_INVALID_ARG, "W, H, spp, max_depth >= 1");
     pt_scene* sc = const_cast<pt_scene*>(scene);
@@ -557,21 +560,34 @@ int pt_render(const pt_scene* scene, const pt_nif* nif, const float env_rgb[3], 
     int rc = ensure_ws(sc);
     if (rc) return rc;
     const int64_t n = (int64_t)width * height * 3;
+    cudaStream_t st = sync ? sc->ws.own_stream : (cudaStream_t)stream;
     if (sc->ws.fb_capacity < n) {
+        // the old framebuffer may still be read by an earlier asynchronous call: cache_free returns it only
+        // once the device is idle
         cache_free(sc->device, sc->ws.fb, sizeof(float) * sc->ws.fb_capacity);
         sc->ws.fb = nullptr;
         sc->ws.fb_capacity = 0;
         CU(cache_alloc(sc->device, sizeof(float) * n, reinterpret_cast<void**>(&sc->ws.fb)));
         sc->ws.fb_capacity = n;
     }
-    cudaStream_t st = sc->ws.own_stream;
     CU(cudaMemsetAsync(sc->ws.fb, 0, sizeof(float) * n, st));
     rc = render_samples_impl(sc, nif, env_rgb, width, height, 0, height, 0, spp, max_depth, seed, 0, sc->ws.fb, st);
     if (rc) return rc;
     pt::launch_scale(sc->ws.fb, n, 1.0f / (float)spp, st);
     CU(cudaMemcpyAsync(out_rgb, sc->ws.fb, sizeof(float) * n, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
+    if (sync) CU(cudaStreamSynchronize(st));
     return PT_OK;
+}
+}  // namespace
+
+int pt_render(const pt_scene* scene, const pt_nif* nif, const float env_rgb[3], int32_t width, int32_t height,
+              int32_t spp, int32_t max_depth, uint64_t seed, float* out_rgb) {
+    return render_frame(scene, nif, env_rgb, width, height, spp, max_depth, seed, out_rgb, nullptr, true);
+}
+
+int pt_render_async(const pt_scene* scene, const pt_nif* nif, const float env_rgb[3], int32_t width, int32_t height,
+                    int32_t spp, int32_t max_depth, uint64_t seed, float* out_rgb, void* stream) {
+    return render_frame(scene, nif, env_rgb, width, height, spp, max_depth, seed, out_rgb, stream, false);
 }
 
 int pt_trace_primary(const pt_scene* scene, int32_t width, int32_t height, uint64_t seed, int32_t sample,

@@ -31,7 +31,7 @@ class PtStats(C.Structure):
 
 
 EXPORTED = ["pt_scene_create", "pt_scene_destroy", "pt_nif_load", "pt_nif_load_ex", "pt_nif_load_family",
-            "pt_nif_load_family_ex", "pt_nif_destroy", "pt_render",
+            "pt_nif_load_family_ex", "pt_nif_destroy", "pt_render", "pt_render_async",
             "pt_render_samples", "pt_render_rows", "pt_trace_primary", "pt_trace_primary_aov", "pt_trace_rays", "pt_nif_infer", "pt_get_stats",
             "pt_set_profiling", "pt_last_error", "pt_version"]
 
@@ -53,6 +53,7 @@ def lib():
             L.pt_nif_load_family_ex.argtypes = [I32, I32, I32, P, I64, C.POINTER(P)]
             L.pt_nif_destroy.argtypes = [P]
             L.pt_render.argtypes = [P, P, P, I32, I32, I32, I32, U64, P]
+            L.pt_render_async.argtypes = [P, P, P, I32, I32, I32, I32, U64, P, P]
             L.pt_render_samples.argtypes = [P, P, P, I32, I32, I32, I32, I32, U64, I32, P, P]
             L.pt_render_rows.argtypes = [P, P, P, I32, I32, I32, I32, I32, I32, I32, U64, I32, P, P]
             L.pt_trace_primary.argtypes = [P, I32, I32, U64, I32, P, P, P]
@@ -168,6 +169,19 @@ def render(scene: Scene, nif: Nif | None, width, height, spp, max_depth, seed=0,
         raise PtError(-1, "out must be a C-contiguous float32 array of height * width * 3 elements")
     env = _env(env_rgb if env_rgb is not None else ((1.0, 1.0, 1.0) if nif is None else None))
     _check(lib().pt_render(scene.h, nif.h if nif else None, _p(env), width, height, spp, max_depth, seed, _p(out)))
+    return out
+
+
+def render_async(scene: Scene, nif: Nif | None, width, height, spp, max_depth, seed, out, env_rgb=None,
+                 stream=None):
+    """pt_render_async: enqueue a full frame (mean over spp) into the host array `out` (C-contiguous
+    float32, H*W*3 elements, page-locked for an asynchronous copy) on `stream` (a torch CUDA stream;
+    default: the current one). `out` holds the frame once the stream is synchronised."""
+    if out.dtype != np.float32 or not out.flags["C_CONTIGUOUS"] or out.size != height * width * 3:
+        raise PtError(-1, "out must be a C-contiguous float32 array of height * width * 3 elements")
+    env = _env(env_rgb if env_rgb is not None else ((1.0, 1.0, 1.0) if nif is None else None))
+    _check(lib().pt_render_async(scene.h, nif.h if nif else None, _p(env), width, height, spp, max_depth, seed,
+                                 _p(out), _stream(stream)))
     return out
 
 

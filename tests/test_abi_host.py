@@ -58,6 +58,7 @@ def test_nif_non_finite_weight(L):
 
 def test_null_arguments(L):
     assert L.pt_render(None, None, None, 4, 4, 1, 1, 0, None) == -1
+    assert L.pt_render_async(None, None, None, 4, 4, 1, 1, 0, None, None) == -1
     assert L.pt_render_samples(None, None, None, 4, 4, 0, 1, 1, 0, 0, None, None) == -1
     assert L.pt_get_stats(None, None) == -1
     assert L.pt_version().startswith(b"pt_b200")

@@ -478,3 +478,25 @@ def test_nif_schedule_rounds(ptm, orc, blob, n_tiles):
     assert np.isfinite(got).all()
     assert np.abs(np.log(got) - y).max() <= NIF_LOG_GATE
     assert (np.abs(got - np.exp(y)) / np.exp(y)).max() <= NIF_REL_GATE
+
+
+def test_render_async_matches_render(ptm, blob):
+    """pt_render_async on two streams with two scene handles (the overlapped read-back an application
+    uses) returns the frames pt_render returns, bit for bit."""
+    import torch
+    c = scenes.CONFIGS[1]
+    sc = scenes.scene_for_config(1)
+    W, H, spp = 96, 64, 4
+    nif = ptm.Nif(blob)
+    S1, S2 = ptm.Scene(sc), ptm.Scene(sc)
+    ref1 = ptm.render(S1, nif, W, H, spp, c.max_depth, seed=5)
+    ref2 = ptm.render(S1, nif, W, H, spp, c.max_depth, seed=6)
+    b1 = torch.empty(W * H * 3, dtype=torch.float32, pin_memory=True)
+    b2 = torch.empty(W * H * 3, dtype=torch.float32, pin_memory=True)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    ptm.render_async(S1, nif, W, H, spp, c.max_depth, 5, b1.numpy(), stream=s1)
+    ptm.render_async(S2, nif, W, H, spp, c.max_depth, 6, b2.numpy(), stream=s2)
+    s1.synchronize()
+    s2.synchronize()
+    assert np.array_equal(b1.numpy().reshape(H, W, 3), ref1)
+    assert np.array_equal(b2.numpy().reshape(H, W, 3), ref2)
