@@ -500,3 +500,23 @@ def test_render_async_matches_render(ptm, blob):
     s2.synchronize()
     assert np.array_equal(b1.numpy().reshape(H, W, 3), ref1)
     assert np.array_equal(b2.numpy().reshape(H, W, 3), ref2)
+
+
+@pytest.mark.parametrize("cfg", [0, 3])
+def test_wave_buffer_layouts_bit_identical(ptm, blob, cfg):
+    """Sample sums accumulated with waves of 1 and 3 samples (sample-major wave buffer, 8 x 4 tiles) and
+    of 4 / 32 samples (a pixel's samples per first-bounce warp, pixel-major buffer, float4 accumulate)
+    are bit-identical: every layout adds a pixel's samples in the same order."""
+    import torch
+    c = scenes.CONFIGS[cfg]
+    W, H, spp = (c.width, c.height, 4) if cfg == 0 else (320, 64, 32)
+    s = ptm.Scene(scenes.scene_for_config(cfg))
+    nif = ptm.Nif(blob)
+    outs = []
+    for k in (1, 3, spp):
+        acc = torch.zeros(W * H * 3, device="cuda")
+        ptm.render_samples(s, nif, W, H, 0, spp, c.max_depth, 7, acc, wave_samples=k)
+        torch.cuda.synchronize()
+        outs.append(acc.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[0], outs[2])
