@@ -269,20 +269,45 @@ __device__ __forceinline__ void sine_chunk(const uint32_t* v, uint32_t* p) {
 }
 
 
+// atan2 on the FMA pipe: octant reduction to a = min/max in [0, 1], a degree-15 odd polynomial (8
+// coefficients fitted for minimax error on [0, 1]: 3.7e-8 in exact arithmetic, <= 1.6e-7 rad evaluated in
+// fp32; tools/equirect_check.cu measures the whole map against fp64), then the octant's reflections; atan2(+-0, x < 0) = +-pi like atan2f. (y, x) = (0, 0) is the
+// caller's case.
+__device__ __forceinline__ float atan2_poly(float y, float x) {
+    const float ax = fabsf(x), ay = fabsf(y);
+    const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+    const float a = mx > 0.0f ? __fdividef(mn, mx) : 0.0f;   // 2 ulp: adds <= 2.4e-7 rad
+    const float s = a * a;
+    float p = -0.004054564982652664f;
+    p = fmaf(p, s, 0.021862955763936043f);
+    p = fmaf(p, s, -0.055912334471940994f);
+    p = fmaf(p, s, 0.0964219868183136f);
+    p = fmaf(p, s, -0.1390863060951233f);
+    p = fmaf(p, s, 0.19946566224098206f);
+    p = fmaf(p, s, -0.33329859375953674f);
+    p = fmaf(p, s, 0.9999993443489075f);
+    float r = p * a;
+    if (ay > ax) r = 1.57079637f - r;
+    if (x < 0.0f) r = 3.14159274f - r;
+    return copysignf(r, y);
+}
+
 // Equirect map of an escaped direction (S4 -> S5; moved here from the trace kernel so the divergent
-// atan2/acos run once per queued ray in the NIF prologue instead of in the traversal warps)
+// atan2/acos run once per queued ray in the NIF prologue instead of in the traversal warps).
+// v = acos(d.y / |d|) / pi is evaluated as atan2(|(d.x, d.z)|, d.y) / pi: the same angle, well conditioned
+// at the poles (acos of a rounded cosine near +-1 loses ~sqrt(eps) there), and both angles go through
+// atan2_poly (the producer warps' share of the NIF's issue slots).
 __device__ __forceinline__ void equirect_f32(float3 d, float& u, float& v) {
     // SPEC.md:438 convention (reading R14): u = 0.5 + atan2(d.x, -d.z)/2pi wrapped to [0,1); v = acos(d.y)/pi
-    const float len = sqrtf(d.x * d.x + d.y * d.y + d.z * d.z);
     float uu;
     if (d.x == 0.0f && d.z == 0.0f) uu = 0.5f;
     else {
-        uu = 0.5f + atan2f(d.x, -d.z) * (0.5f / CUDART_PI_F);
+        uu = 0.5f + atan2_poly(d.x, -d.z) * (0.5f / CUDART_PI_F);
         if (uu >= 1.0f) uu -= 1.0f;
     }
-    const float y = fminf(1.0f, fmaxf(-1.0f, d.y / len));
+    const float h = sqrtf(d.x * d.x + d.z * d.z);
     u = uu;
-    v = acosf(y) * (1.0f / CUDART_PI_F);
+    v = (h == 0.0f && d.y == 0.0f) ? 0.5f : atan2_poly(h, d.y) * (1.0f / CUDART_PI_F);
 }
 
 // ReLU epilogue of the paper's NIF: relu + fp16x2 pack in one cvt per pair
