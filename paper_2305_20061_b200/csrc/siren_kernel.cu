@@ -103,7 +103,8 @@ constexpr int kThreads = 32 * (kFirstEpiWarp + kNumEpiWarps);   // 640
 #ifndef PT_NIF_DIAG
 #define PT_NIF_DIAG 0   // diagnostic builds only (wrong results): 1 = no TMEM store of A, 2 = no sine,
                         // 3 = no epilogue TMEM traffic (neither the accumulator load nor the A store),
-                        // 4 = hand-off only, 5 = no output layer work (exp, stores, throughput loads)
+                        // 4 = hand-off only, 5 = no output layer work (exp, stores, throughput loads),
+                        // 6 = no equirect in the producers (the queue's direction read as (u, v))
 #endif
 enum {
     kBarW = 0,
@@ -369,7 +370,7 @@ __global__ void __launch_bounds__(siren::kThreads, 1)
                         const float4 en = __ldg(esc + row);
                         u = en.x;
                         v = en.y;
-                        if (dir_input) equirect_f32(make_float3(en.x, en.y, en.z), u, v);
+                        if (dir_input && PT_NIF_DIAG != 6) equirect_f32(make_float3(en.x, en.y, en.z), u, v);
                     }
                     const float x = 2.0f * u - 1.0f, y = 2.0f * v - 1.0f;
                     const __half xh = __float2half_rn(x), yh = __float2half_rn(y);
