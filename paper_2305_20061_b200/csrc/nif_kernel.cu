@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(nif::kThreads, 1)
     using namespace nif;
     constexpr int kImg = kFrImageBytes;
     constexpr uint32_t kOnesOff = kFrOffOnes;
-    extern __shared__ __align__(128) uint8_t smem[];
+    extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* image = smem;
     // [0] weights, [1..4] a_ready[slot][column half], [5..8] d_full[slot][column half]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kFrImageBytes);
@@ -470,6 +470,389 @@ cudaError_t ensure_dyn_smem(const void* kernel, int bytes) {
     return e;
 }
 
+// ---------------------------------------------------------------------------------------------
+// The paper's NIF on the SIREN kernel's schedule (round 2, PT_NIF_FR3): three 128-ray tiles in flight,
+// layer groups rotating over two accumulator regions, two 8-warp epilogue teams (team t = region t), one
+// MMA issuer per region with single-waiter barriers, full-N layers (one commit per layer). Layers:
+//   stage 0 (L0): the tile's 40 Fourier features from shared memory (SS, K' = 48) + bias -> 128 units
+//   stage 1 (L1): 128 -> 96 (88 used) TS + bias; its epilogue writes relu(h1) (88) and features 0..3
+//                 (sin/cos, the K step that straddles the concat boundary) into A
+//   stage 2 (L2): concat skip: 6 TS K steps (h1 + features 0..3) + 2 SS K steps (features 4..19 read
+//                 from the feature tile) + bias -> 128
+//   stage 3 (L3): 128 -> 128 TS + bias
+//   output  (L4): 128 -> 16 (Y, U, V used) TS + bias into O(s), issued with the slot's next L0; the
+//                 slot's 4 output warps apply BT.601 YUV -> RGB, exp, beta.
+// The producer warps compute the features (equirect of the queued direction, then sin/cos of
+// 2 pi B.(u, v) in turns) into the slot's feature tile, which stays live until L2 of the tile is done.
+// ---------------------------------------------------------------------------------------------
+#ifndef PT_NIF_FR3
+#define PT_NIF_FR3 1
+#endif
+namespace fr3 {
+using nif::kFrImageBytes;
+constexpr int kTileM = 128;
+constexpr int kSlots = 3;
+constexpr int kDRegions = 2;
+constexpr int kIssuers = 2;
+constexpr int kTeamWarps = 8;
+constexpr int kNumEpiWarps = 16;
+// four producer warps (one per SM sub-partition): 40 sin/cos per row are the producers' work, and two
+// warps measured too slow to keep three tiles in flight (6.4 G inferences/s)
+constexpr int kProducerWarp0 = 2;
+#ifndef PT_FR3_PRODUCERS
+#define PT_FR3_PRODUCERS 4
+#endif
+constexpr int kProducerWarps = PT_FR3_PRODUCERS;
+constexpr int kProducerThreads = 32 * kProducerWarps;
+constexpr int kFirstEpiWarp = kProducerWarp0 + kProducerWarps;   // 6
+constexpr int kThreads = 32 * (kFirstEpiWarp + kNumEpiWarps);     // 704
+constexpr int kFtBytes = 128 * 48 * 2;                          // feature tile: 128 rows x K' 48 (fp16)
+constexpr int kOffBars = ((kFrImageBytes + 1023) / 1024) * 1024;
+constexpr int kNumBars = 1 + (3 + kIssuers) * kSlots + 2 * kDRegions;
+constexpr int kOffTmemSlot = kOffBars + 8 * kNumBars;
+constexpr int kOffFt = ((kOffTmemSlot + 16 + 1023) / 1024) * 1024;
+constexpr int kSmemBytes = kOffFt + kSlots * kFtBytes;
+enum {
+    kBarW = 0,
+    kBarAReady = 1,   // a_ready(s, consumer p) at kBarAReady + kIssuers s + p
+    kBarFtFull = kBarAReady + kIssuers * kSlots,
+    kBarFtEmpty = kBarFtFull + kSlots,
+    kBarOFull = kBarFtEmpty + kSlots,
+    kBarDFull = kBarOFull + kSlots,
+    kBarDEmpty = kBarDFull + kDRegions
+};
+constexpr uint32_t kTmemCols = 512;
+__host__ __device__ constexpr uint32_t a_col(int s) { return 64u * s; }
+__host__ __device__ constexpr uint32_t o_col(int s) { return 192u + 16u * s; }
+__host__ __device__ constexpr uint32_t d_col(int j) { return 256u + 128u * j; }
+__device__ __forceinline__ int slots_in_round(uint32_t t0, uint32_t n_tiles) {
+    int n = 1;
+    while (n < kSlots && t0 + (uint32_t)n * gridDim.x < n_tiles) ++n;
+    return n;
+}
+}  // namespace fr3
+
+template <bool kDebug>
+__global__ void __launch_bounds__(fr3::kThreads, 1)
+    nif_fr3_kernel(const uint8_t* __restrict__ g_image, const float4* __restrict__ esc,
+                   const float4* __restrict__ esc_beta, const uint32_t* __restrict__ count, float* __restrict__ out,
+                   float* __restrict__ dbg, int dir_input) {
+    using namespace fr3;
+    using nif::idesc;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBars);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmemSlot);
+    auto bar = [&](int b) { return smem_u32(&bars[b]); };
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    pdl_trigger();
+
+    if (warp == 1 && lane == 0) {
+        mbar_init(bar(kBarW), 1);
+        for (int s = 0; s < kSlots; ++s) {
+            for (int p = 0; p < kIssuers; ++p) mbar_init(bar(kBarAReady + kIssuers * s + p), kTeamWarps);
+            mbar_init(bar(kBarFtFull + s), kProducerThreads);
+            mbar_init(bar(kBarFtEmpty + s), 1);
+            mbar_init(bar(kBarOFull + s), 1);
+        }
+        for (int j = 0; j < kDRegions; ++j) {
+            mbar_init(bar(kBarDFull + j), 1);
+            mbar_init(bar(kBarDEmpty + j), kTeamWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 1 && lane == 0) {
+        mbar_expect_tx(bar(kBarW), (uint32_t)kFrImageBytes);
+        constexpr int kChunk = 16384;
+        for (int off = 0; off < kFrImageBytes; off += kChunk) {
+            const int bytes = (kFrImageBytes - off) < kChunk ? (kFrImageBytes - off) : kChunk;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(smem + off)),
+                "l"(g_image + off), "r"(bytes), "r"(bar(kBarW))
+                : "memory");
+        }
+    }
+
+    pdl_wait();
+    const uint32_t n_rows = *count;
+    const uint32_t n_tiles = (n_rows + kTileM - 1) / kTileM;
+
+    if (warp < kIssuers) {
+        // ===== MMA issuers: warp j issues the layer groups of D region j =====
+        const uint32_t me = (uint32_t)warp;
+        if (blockIdx.x < n_tiles) {
+            mbar_wait(bar(kBarW), 0);
+            const uint32_t img = smem_u32(smem);
+            const uint64_t ones = smem_desc(img + nif::kFrOffOnes, 2048, 128);
+            uint32_t a_phase = 0, f_phase = 0, e_phase = 0, pend = 0, out_by_me = 0;
+            uint32_t g = 0;
+            auto issue_out = [&](int s) {
+                mbar_wait(bar(kBarAReady + kIssuers * s + (int)me), (a_phase >> s) & 1u);
+                a_phase ^= 1u << s;
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t base = img + nif::kFrOffB4;
+                    const uint32_t at = tmem + a_col(s);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        mma_ts(tmem + o_col(s), at + 8 * k, smem_desc(base + k * 2 * 256, 256, 128), idesc(16), k > 0);
+                    mma_ss(tmem + o_col(s), ones, smem_desc(base + 16 * 256, 256, 128), idesc(16), 1);   // + bias
+                    mma_commit(bar(kBarOFull + s));
+                }
+                __syncwarp();
+            };
+            for (uint32_t i = 0;; i += kSlots) {
+                const uint32_t t0 = blockIdx.x + i * gridDim.x;
+                if (t0 >= n_tiles) break;
+                const int nslots = slots_in_round(t0, n_tiles);
+                for (int stage = 0; stage < 4; ++stage) {
+                    for (int s = 0; s < nslots; ++s, ++g) {
+                        const int j = (int)(g & 1u);
+                        if (stage == 3) {
+                            const bool mine_out = ((g + (uint32_t)nslots) & 1u) == me;
+                            out_by_me = mine_out ? (out_by_me | 1u << s) : (out_by_me & ~(1u << s));
+                        }
+                        if (stage == 0) pend |= 1u << s;
+                        if ((uint32_t)j != me) continue;
+                        if (stage == 0) {
+                            if (i > 0) issue_out(s);
+                            mbar_wait(bar(kBarFtFull + s), (f_phase >> s) & 1u);   // features staged
+                            f_phase ^= 1u << s;
+                        } else {
+                            mbar_wait(bar(kBarAReady + kIssuers * s + (int)me), (a_phase >> s) & 1u);
+                            a_phase ^= 1u << s;
+                        }
+                        if (g >= (uint32_t)kDRegions) {
+                            mbar_wait(bar(kBarDEmpty + j), (e_phase >> j) & 1u);
+                            e_phase ^= 1u << j;
+                        }
+                        tc_fence_after();
+                        const uint32_t dt = tmem + d_col(j);
+                        const uint32_t ft = smem_u32(smem + kOffFt + s * kFtBytes);
+                        if (elect_one()) {
+                            const uint32_t at = tmem + a_col(s);
+                            if (stage == 0) {
+                                const uint32_t b0 = img + nif::kFrOffB0;
+#pragma unroll
+                                for (int k = 0; k < 3; ++k)
+                                    mma_ss(dt, smem_desc(ft + k * 2 * 2048, 2048, 128),
+                                           smem_desc(b0 + k * 2 * 2048, 2048, 128), idesc(128), k > 0);
+                                mma_ss(dt, ones, smem_desc(b0 + 6 * 2048, 2048, 128), idesc(128), 1);
+                            } else if (stage == 1) {
+                                const uint32_t b1 = img + nif::kFrOffB1;
+#pragma unroll
+                                for (int k = 0; k < 8; ++k)
+                                    mma_ts(dt, at + 8 * k, smem_desc(b1 + k * 2 * 1536, 1536, 128), idesc(96), k > 0);
+                                mma_ss(dt, ones, smem_desc(b1 + 16 * 1536, 1536, 128), idesc(96), 1);
+                            } else if (stage == 2) {
+                                const uint32_t b2 = img + nif::kFrOffB2;
+#pragma unroll
+                                for (int k = 0; k < 6; ++k)
+                                    mma_ts(dt, at + 8 * k, smem_desc(b2 + k * 2 * 2048, 2048, 128), idesc(128), k > 0);
+#pragma unroll
+                                for (int k = 6; k < 8; ++k)   // features 4..19: feature-tile K' 16..47
+                                    mma_ss(dt, smem_desc(ft + (2 * k - 10) * 2048, 2048, 128),
+                                           smem_desc(b2 + k * 2 * 2048, 2048, 128), idesc(128), 1);
+                                mma_ss(dt, ones, smem_desc(b2 + 16 * 2048, 2048, 128), idesc(128), 1);
+                            } else {
+                                const uint32_t b3 = img + nif::kFrOffB3;
+#pragma unroll
+                                for (int k = 0; k < 8; ++k)
+                                    mma_ts(dt, at + 8 * k, smem_desc(b3 + k * 2 * 2048, 2048, 128), idesc(128), k > 0);
+                                mma_ss(dt, ones, smem_desc(b3 + 16 * 2048, 2048, 128), idesc(128), 1);
+                            }
+                            mma_commit(bar(kBarDFull + j));
+                            if (stage == 2) mma_commit(bar(kBarFtEmpty + s));   // feature tile free after L2
+                        }
+                        __syncwarp();
+                    }
+                }
+            }
+            for (int s = 0; s < kSlots; ++s)
+                if ((pend >> s) & (out_by_me >> s) & 1u) issue_out(s);
+        }
+    } else if (warp >= kProducerWarp0 && warp < kFirstEpiWarp) {
+        // ===== producers: the Fourier features of each tile into the slot's feature tile =====
+        // row m, K' block kb (8 fp16) at kb * 2048 + 16 m; K' 0..7 zero, K' 8 + 2j / 9 + 2j = sin_j / cos_j
+        const int p = threadIdx.x - 32 * kProducerWarp0;
+        uint8_t* fts = smem + kOffFt;
+        for (int m = p; m < kSlots * 128; m += kProducerThreads)
+            *reinterpret_cast<uint4*>(fts + (m >> 7) * kFtBytes + 16 * (m & 127)) = make_uint4(0, 0, 0, 0);
+        if (blockIdx.x < n_tiles) mbar_wait(bar(kBarW), 0);   // the frequencies are in the image
+        const float* freq = reinterpret_cast<const float*>(smem + nif::kFrOffFreq);
+        uint32_t e_phase = 0, filled = 0;
+        for (uint32_t i = 0;; i += kSlots) {
+            const uint32_t t0 = blockIdx.x + i * gridDim.x;
+            if (t0 >= n_tiles) break;
+            const int nslots = slots_in_round(t0, n_tiles);
+            for (int s = 0; s < nslots; ++s) {
+                const uint32_t tile = t0 + s * gridDim.x;
+                if ((filled >> s) & 1u) {
+                    mbar_wait(bar(kBarFtEmpty + s), (e_phase >> s) & 1u);
+                    e_phase ^= 1u << s;
+                }
+                filled |= 1u << s;
+                for (int m = p; m < 128; m += kProducerThreads) {
+                    const uint32_t row = tile * kTileM + m;
+                    float u = 0.5f, v = 0.5f;
+                    if (row < n_rows) {
+                        const float4 en = __ldg(esc + row);
+                        u = en.x;
+                        v = en.y;
+                        if (dir_input) equirect_f32(make_float3(en.x, en.y, en.z), u, v);
+                    }
+                    uint32_t f[20];
+#pragma unroll
+                    for (int jj = 0; jj < 20; ++jj) {
+                        const float pp = fmaf(freq[2 * jj], u, freq[2 * jj + 1] * v);
+                        const float r = pp - rintf(pp);                  // exact-range turns in [-1/2, 1/2]
+                        float sn, cs;
+                        __sincosf(6.28318530717958647692f * r, &sn, &cs);
+                        f[jj] = pack_half2(sn, cs);
+                    }
+                    uint8_t* base = fts + s * kFtBytes + 16 * m;
+#pragma unroll
+                    for (int kb = 1; kb < 6; ++kb)
+                        *reinterpret_cast<uint4*>(base + kb * 2048) =
+                            make_uint4(f[4 * kb - 4], f[4 * kb - 3], f[4 * kb - 2], f[4 * kb - 1]);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic -> async proxy
+                mbar_arrive(bar(kBarFtFull + s));
+            }
+        }
+    } else if (warp >= kFirstEpiWarp) {
+        // ===== epilogue teams (see the SIREN kernel): team t runs the groups of D region t =====
+        const int e = warp - kFirstEpiWarp;
+        const int team = e >> 3;
+        const int h = (e >> 2) & 1;
+        const int q = warp & 3;
+        const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
+        const int my_slot = 2 * h + team;
+        const bool out_warp = my_slot < kSlots;
+        uint32_t d_phase = 0, o_phase = 0;
+        float4 beta = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        uint32_t oslot = 0, prow = 0;
+        bool ovalid = false, pend = false;
+        auto output = [&](uint32_t dbg_row) {
+            mbar_wait(bar(kBarOFull + my_slot), o_phase);
+            o_phase ^= 1;
+            tc_fence_after();
+            uint32_t v[4];
+            tmem_ld4(tmem + o_col(my_slot) + lane_addr, v);
+            tmem_wait_ld_dep4(v);
+            if (ovalid) {
+                float y0 = __uint_as_float(v[0]), y1 = __uint_as_float(v[1]), y2 = __uint_as_float(v[2]);
+                if (kDebug) {
+                    dbg[((size_t)4 * n_rows + dbg_row) * 128 + 0] = y0;
+                    dbg[((size_t)4 * n_rows + dbg_row) * 128 + 1] = y1;
+                    dbg[((size_t)4 * n_rows + dbg_row) * 128 + 2] = y2;
+                }
+                // fixed BT.601 YUV -> RGB colour layer, log space
+                const float Y = y0, U = y1, V = y2;
+                y0 = fmaf(1.13983f, V, Y);
+                y1 = fmaf(-0.58060f, V, fmaf(-0.39465f, U, Y));
+                y2 = fmaf(2.03211f, U, Y);
+                out[3 * (size_t)oslot + 0] = beta.x * __expf(y0);
+                out[3 * (size_t)oslot + 1] = beta.y * __expf(y1);
+                out[3 * (size_t)oslot + 2] = beta.z * __expf(y2);
+            }
+        };
+        const uint32_t dreg = tmem + d_col(team) + lane_addr + 64u * (uint32_t)h;
+        const int m_row = 32 * q + lane;   // this thread's row of the tile
+        uint32_t g = 0;
+        for (uint32_t i = 0;; i += kSlots) {
+            const uint32_t t0 = blockIdx.x + i * gridDim.x;
+            if (t0 >= n_tiles) break;
+            const int nslots = slots_in_round(t0, n_tiles);
+            for (int stage = 0; stage < 4; ++stage) {
+                for (int s = 0; s < nslots; ++s, ++g) {
+                    if ((int)(g & 1u) != team) continue;
+                    const uint32_t tile = t0 + s * gridDim.x;
+                    const uint32_t row = tile * kTileM + m_row;
+                    const bool valid = row < n_rows;
+                    mbar_wait(bar(kBarDFull + team), d_phase);
+                    d_phase ^= 1;
+                    tc_fence_after();
+                    const uint32_t areg = tmem + a_col(s) + lane_addr + 32u * (uint32_t)h;
+                    // L1 has 96 columns: the high half loads only its first 32 (units 64..87 + padding)
+                    const int nchunk = (stage == 1 && h == 1) ? 1 : 2;
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        if (c >= nchunk) break;
+                        uint32_t v[32];
+                        uint32_t pk[16];
+                        TMEM_LD32(dreg + 32u * (uint32_t)c, v);
+                        tmem_wait_ld_dep(v);
+                        if (c == nchunk - 1) {
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(bar(kBarDEmpty + team));
+                        }
+                        if (kDebug && valid)
+                            for (int k = 0; k < 32; ++k)
+                                dbg[((size_t)stage * n_rows + row) * 128 + 64 * h + 32 * c + k] = __uint_as_float(v[k]);
+#pragma unroll
+                        for (int k = 0; k < 16; ++k)
+                            pk[k] = relu_pack(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
+                        if (stage == 1 && h == 1) {
+                            // units 64..87 -> A columns 32..43; features 0..3 (feature-tile K' 8..15, the K
+                            // step straddling the concat boundary) -> A columns 44..47
+                            const uint4 fw = *reinterpret_cast<const uint4*>(smem + kOffFt + s * kFtBytes + 2048 + 16 * m_row);
+                            pk[12] = fw.x;
+                            pk[13] = fw.y;
+                            pk[14] = fw.z;
+                            pk[15] = fw.w;
+                        }
+                        TMEM_ST16(areg + 16u * (uint32_t)c, pk);
+                    }
+                    tmem_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(bar(kBarAReady + kIssuers * s + (int)((g + (uint32_t)nslots) & 1u)));
+                    if (stage == 0 && s == my_slot && pend) output(prow);
+                    if (stage == 2 && s == my_slot) {
+                        ovalid = valid;
+                        prow = row;
+                        if (valid) {
+                            beta = __ldg(esc_beta + row);
+                            oslot = __float_as_uint(__ldg(esc + row).w);
+                        }
+                        pend = true;
+                    }
+                }
+            }
+        }
+        if (out_warp && pend) output(prow);
+    }
+    if (warp == 1 && lane == 0 && blockIdx.x >= n_tiles) mbar_wait(bar(kBarW), 0);
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    }
+}
+
+template <bool kDebug>
+static cudaError_t nif_fr3_launch_t(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,
+                                    int grid, float* out, float* dbg, int dir_input, cudaStream_t st) {
+    cudaError_t e = ensure_dyn_smem((const void*)nif_fr3_kernel<kDebug>, fr3::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(nif_fr3_kernel<kDebug>, dim3(grid), dim3(fr3::kThreads), fr3::kSmemBytes, st,
+                      (const uint8_t*)nif->d_smem_image, esc, esc_beta, count, out, dbg, dir_input);
+}
+
 template <bool kDebug>
 static cudaError_t nif_fr_launch_t(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,
                                    int grid, float* out, float* dbg, int dir_input, cudaStream_t st) {
@@ -494,9 +877,13 @@ static cudaError_t nif_launch_impl(const pt_nif* nif, const float4* esc, const f
     int64_t tiles = (max_rows + 127) / 128;
     int grid = num_sms();
     if (tiles < grid) grid = (int)(tiles > 0 ? tiles : 1);
-    if (nif->kind == PT_NIF_FOURIER_RELU)
+    if (nif->kind == PT_NIF_FOURIER_RELU) {
+        if (PT_NIF_FR3)
+            return dbg ? nif_fr3_launch_t<true>(nif, esc, esc_beta, count, grid, out, dbg, dir_input, st)
+                       : nif_fr3_launch_t<false>(nif, esc, esc_beta, count, grid, out, dbg, dir_input, st);
         return dbg ? nif_fr_launch_t<true>(nif, esc, esc_beta, count, grid, out, dbg, dir_input, st)
                    : nif_fr_launch_t<false>(nif, esc, esc_beta, count, grid, out, dbg, dir_input, st);
+    }
     return launch_siren(nif, esc, esc_beta, count, grid, out, dbg, dir_input, st);
 }
 
