@@ -18,6 +18,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -870,13 +871,17 @@ cudaError_t launch_siren(const pt_nif* nif, const float4* esc, const float4* esc
 // one persistent CTA per SM (or per tile when there are fewer tiles); the row count is read on device
 static cudaError_t nif_launch_impl(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,
                                    int64_t max_rows, float* out, float* dbg, int dir_input, cudaStream_t st) {
-    if (nif->kind == PT_NIF_FR_FAMILY) {
-        if (dbg) return cudaErrorNotSupported;
-        return launch_mlp(const_cast<pt_nif*>(nif), esc, esc_beta, count, max_rows, out, dir_input, st);
-    }
     int64_t tiles = (max_rows + 127) / 128;
     int grid = num_sms();
     if (tiles < grid) grid = (int)(tiles > 0 ? tiles : 1);
+    if (nif->kind == PT_NIF_FR_FAMILY) {
+        if (dbg) return cudaErrorNotSupported;
+        // (128, 4) fp16 = the paper's network: the three-tile kernel (unless the tests force the layered path)
+        const char* env = std::getenv("PT_MLP_LAYERED");
+        if (PT_NIF_FR3 && nif->d_smem_image && !(env && env[0] == '1'))
+            return nif_fr3_launch_t<false>(nif, esc, esc_beta, count, grid, out, nullptr, dir_input, st);
+        return launch_mlp(const_cast<pt_nif*>(nif), esc, esc_beta, count, max_rows, out, dir_input, st);
+    }
     if (nif->kind == PT_NIF_FOURIER_RELU) {
         if (PT_NIF_FR3)
             return dbg ? nif_fr3_launch_t<true>(nif, esc, esc_beta, count, grid, out, dbg, dir_input, st)
