@@ -168,7 +168,7 @@ def oracle_sample(cfg, rows_every: int):
 
 
 # bounded oracle samples (rows every k): cpu_baseline ~3-5 s, one reference-arm step ~1-2 s on 16 cores
-ORACLE_ROWS = {0: (1, 1), 1: (8, 64), 2: (32, 256), 3: (54, 270), 4: (540, 1080)}
+ORACLE_ROWS = {0: (1, 1), 1: (8, 64), 2: (32, 256), 3: (12, 270), 4: (540, 1080)}   # cpu_baseline / reference-arm row strides (config 3: ~11 s of oracle work for the baseline)
 
 
 def run_oracle(cfg, steps: int, warmup: int, rows_every: int):
