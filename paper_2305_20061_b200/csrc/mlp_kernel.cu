@@ -667,6 +667,9 @@ namespace {
 
 int pick_bn(int n_valid) { return n_valid <= 16 ? 16 : n_valid <= 64 ? 64 : n_valid <= 128 ? 128 : 256; }
 
+}  // namespace
+
+// shared with the paper-NIF kernel's fp8 image (nif_kernel.cu): one e4m3 rounding of the weights
 float half_to_float(uint16_t h) {
     const int e = (h >> 10) & 31, m = h & 1023;
     float v = e == 0 ? std::ldexp((float)m, -24) : std::ldexp((float)(m | 1024), e - 25);
@@ -692,7 +695,6 @@ uint8_t float_to_e4m3(float x) {
     return sign | (uint8_t)(((ex + 7) << 3) | ((int)r - 8));
 }
 
-}  // namespace
 
 int mlp_concat_layer(int L) {
     int c = 0;

@@ -531,9 +531,84 @@ __device__ __forceinline__ int slots_in_round(uint32_t t0, uint32_t n_tiles) {
     while (n < kSlots && t0 + (uint32_t)n * gridDim.x < n_tiles) ++n;
     return n;
 }
+// fp8 image (reading R24: e4m3 weights, features and activations; fp32 biases): K-major 8-bit core
+// matrices (8 rows x 16 B = 16 K elements), K = 32 per tcgen05.mma kind::f8f6f4. L0's K' order is the
+// feature tile's: [g_8 .. g_39, g_0 .. g_7, 0 x 24] (g = sin_0..19, cos_0..19), so the concat layer's
+// last K step reads g_8..39 straight from the tile and g_0..7 ride in A after h1.
+constexpr int k8OffB0 = 0;                              // N = 128, K' = 64
+constexpr int k8OffB1 = k8OffB0 + 128 * 64;             // N = 96 (88 used), K = 128
+constexpr int k8OffB2 = k8OffB1 + 96 * 128;             // N = 128, K = [h1 (88), g (40)]
+constexpr int k8OffB3 = k8OffB2 + 128 * 128;
+constexpr int k8OffB4 = k8OffB3 + 128 * 128;            // N = 16 (3 used), K = 128
+constexpr int k8OffBias = k8OffB4 + 16 * 128;           // fp32: b0[128] b1[96] b2[128] b3[128] b4[16]
+constexpr int k8OffFreq = k8OffBias + 496 * 4;          // fp32 [20][2]
+constexpr int k8ImageBytes = k8OffFreq + 40 * 4;
+__host__ __device__ constexpr int k8bias(int l) {       // float offset of layer l's bias
+    return l == 0 ? 0 : l == 1 ? 128 : l == 2 ? 224 : l == 3 ? 352 : 480;
+}
+constexpr int k8FtBytes = 128 * 64;                     // feature tile: 128 rows x K' 64 (e4m3)
 }  // namespace fr3
 
-template <bool kDebug>
+// The paper's NIF -> the fp8 image of nif_fr3_kernel<kFp8 = true>
+void nif_build_smem_image_fr8(const uint16_t* blob, std::vector<uint8_t>* image) {
+    using namespace fr3;
+    std::vector<uint8_t>& img = *image;
+    img.assign(k8ImageBytes, 0);
+    auto put8 = [&](int base, int N, int n, int k, uint8_t v) {
+        img[base + ((k >> 4) * (N / 8) + (n >> 3)) * 128 + (n & 7) * 16 + (k & 15)] = v;
+    };
+    auto q8 = [&](uint16_t h) { return float_to_e4m3(half_to_float(h)); };
+    float* bias = reinterpret_cast<float*>(&img[k8OffBias]);
+    float* freq = reinterpret_cast<float*>(&img[k8OffFreq]);
+    size_t off = 0;
+    for (int i = 0; i < 40; ++i) freq[i] = half_to_float(blob[off++]);
+    // L0: W0 [128][40] over g = (sin_0..19, cos_0..19); K' k < 32 -> g_{k+8}, 32 <= k < 40 -> g_{k-32}
+    const uint16_t* W0 = blob + off; off += 128 * 40;
+    const uint16_t* b0 = blob + off; off += 128;
+    for (int n = 0; n < 128; ++n) {
+        for (int k = 0; k < 40; ++k) put8(k8OffB0, 128, n, k, q8(W0[n * 40 + (k < 32 ? k + 8 : k - 32)]));
+        bias[k8bias(0) + n] = half_to_float(b0[n]);
+    }
+    const uint16_t* W1 = blob + off; off += 88 * 128;
+    const uint16_t* b1 = blob + off; off += 88;
+    for (int n = 0; n < 88; ++n) {
+        for (int k = 0; k < 128; ++k) put8(k8OffB1, 96, n, k, q8(W1[n * 128 + k]));
+        bias[k8bias(1) + n] = half_to_float(b1[n]);
+    }
+    const uint16_t* W2 = blob + off; off += 128 * 128;
+    const uint16_t* b2 = blob + off; off += 128;
+    for (int n = 0; n < 128; ++n) {
+        for (int k = 0; k < 128; ++k) put8(k8OffB2, 128, n, k, q8(W2[n * 128 + k]));   // [h1, g] in order
+        bias[k8bias(2) + n] = half_to_float(b2[n]);
+    }
+    const uint16_t* W3 = blob + off; off += 128 * 128;
+    const uint16_t* b3 = blob + off; off += 128;
+    for (int n = 0; n < 128; ++n) {
+        for (int k = 0; k < 128; ++k) put8(k8OffB3, 128, n, k, q8(W3[n * 128 + k]));
+        bias[k8bias(3) + n] = half_to_float(b3[n]);
+    }
+    const uint16_t* W4 = blob + off; off += 3 * 128;
+    const uint16_t* b4 = blob + off; off += 3;
+    for (int n = 0; n < 3; ++n) {
+        for (int k = 0; k < 128; ++k) put8(k8OffB4, 16, n, k, q8(W4[n * 128 + k]));
+        bias[k8bias(4) + n] = half_to_float(b4[n]);
+    }
+}
+
+__device__ __forceinline__ uint32_t fr8_pack(float a, float b, float c, float d) {
+    uint16_t lo, hi;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(lo) : "f"(b), "f"(a));
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(hi) : "f"(d), "f"(c));
+    return (uint32_t)lo | ((uint32_t)hi << 16);
+}
+__device__ __forceinline__ uint32_t fr8_pack_relu(float a, float b, float c, float d) {
+    uint16_t lo, hi;
+    asm("cvt.rn.satfinite.relu.e4m3x2.f32 %0, %1, %2;" : "=h"(lo) : "f"(b), "f"(a));
+    asm("cvt.rn.satfinite.relu.e4m3x2.f32 %0, %1, %2;" : "=h"(hi) : "f"(d), "f"(c));
+    return (uint32_t)lo | ((uint32_t)hi << 16);
+}
+
+template <bool kDebug, bool kFp8>
 __global__ void __launch_bounds__(fr3::kThreads, 1)
     nif_fr3_kernel(const uint8_t* __restrict__ g_image, const float4* __restrict__ esc,
                    const float4* __restrict__ esc_beta, const uint32_t* __restrict__ count, float* __restrict__ out,
@@ -572,11 +647,13 @@ __global__ void __launch_bounds__(fr3::kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
+    constexpr int kImg = kFp8 ? k8ImageBytes : kFrImageBytes;
+    constexpr int kFt = kFp8 ? k8FtBytes : kFtBytes;
     if (warp == 1 && lane == 0) {
-        mbar_expect_tx(bar(kBarW), (uint32_t)kFrImageBytes);
+        mbar_expect_tx(bar(kBarW), (uint32_t)kImg);
         constexpr int kChunk = 16384;
-        for (int off = 0; off < kFrImageBytes; off += kChunk) {
-            const int bytes = (kFrImageBytes - off) < kChunk ? (kFrImageBytes - off) : kChunk;
+        for (int off = 0; off < kImg; off += kChunk) {
+            const int bytes = (kImg - off) < kChunk ? (kImg - off) : kChunk;
             asm volatile(
                 "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                     smem_u32(smem + off)),
@@ -603,12 +680,19 @@ __global__ void __launch_bounds__(fr3::kThreads, 1)
                 a_phase ^= 1u << s;
                 tc_fence_after();
                 if (elect_one()) {
-                    const uint32_t base = img + nif::kFrOffB4;
                     const uint32_t at = tmem + a_col(s);
+                    if (kFp8) {
+                        const uint32_t base = img + k8OffB4;   // b4 is added by the output warps
 #pragma unroll
-                    for (int k = 0; k < 8; ++k)
-                        mma_ts(tmem + o_col(s), at + 8 * k, smem_desc(base + k * 2 * 256, 256, 128), idesc(16), k > 0);
-                    mma_ss(tmem + o_col(s), ones, smem_desc(base + 16 * 256, 256, 128), idesc(16), 1);   // + bias
+                        for (int k = 0; k < 4; ++k)
+                            mma_ts_f8(tmem + o_col(s), at + 8 * k, smem_desc(base + k * 2 * 256, 256, 128), idesc(16), k > 0);
+                    } else {
+                        const uint32_t base = img + nif::kFrOffB4;
+#pragma unroll
+                        for (int k = 0; k < 8; ++k)
+                            mma_ts(tmem + o_col(s), at + 8 * k, smem_desc(base + k * 2 * 256, 256, 128), idesc(16), k > 0);
+                        mma_ss(tmem + o_col(s), ones, smem_desc(base + 16 * 256, 256, 128), idesc(16), 1);   // + bias
+                    }
                     mma_commit(bar(kBarOFull + s));
                 }
                 __syncwarp();
@@ -640,8 +724,36 @@ __global__ void __launch_bounds__(fr3::kThreads, 1)
                         }
                         tc_fence_after();
                         const uint32_t dt = tmem + d_col(j);
-                        const uint32_t ft = smem_u32(smem + kOffFt + s * kFtBytes);
-                        if (elect_one()) {
+                        const uint32_t ft = smem_u32(smem + kOffFt + s * kFt);
+                        if (kFp8 && elect_one()) {
+                            // e4m3, K = 32 per MMA, no bias steps (the epilogue adds the fp32 biases)
+                            const uint32_t at = tmem + a_col(s);
+                            if (stage == 0) {
+#pragma unroll
+                                for (int k = 0; k < 2; ++k)
+                                    mma_ss_f8(dt, smem_desc(ft + k * 2 * 2048, 2048, 128),
+                                              smem_desc(img + k8OffB0 + k * 2 * 2048, 2048, 128), idesc(128), k > 0);
+                            } else if (stage == 1) {
+#pragma unroll
+                                for (int k = 0; k < 4; ++k)
+                                    mma_ts_f8(dt, at + 8 * k, smem_desc(img + k8OffB1 + k * 2 * 1536, 1536, 128), idesc(96),
+                                              k > 0);
+                            } else if (stage == 2) {
+#pragma unroll
+                                for (int k = 0; k < 3; ++k)   // h1 (88) and g_0..7 from A
+                                    mma_ts_f8(dt, at + 8 * k, smem_desc(img + k8OffB2 + k * 2 * 2048, 2048, 128), idesc(128),
+                                              k > 0);
+                                mma_ss_f8(dt, smem_desc(ft, 2048, 128), smem_desc(img + k8OffB2 + 3 * 2 * 2048, 2048, 128),
+                                          idesc(128), 1);     // g_8..39: feature-tile K' 0..31
+                            } else {
+#pragma unroll
+                                for (int k = 0; k < 4; ++k)
+                                    mma_ts_f8(dt, at + 8 * k, smem_desc(img + k8OffB3 + k * 2 * 2048, 2048, 128), idesc(128),
+                                              k > 0);
+                            }
+                            mma_commit(bar(kBarDFull + j));
+                            if (stage == 2) mma_commit(bar(kBarFtEmpty + s));
+                        } else if (!kFp8 && elect_one()) {
                             const uint32_t at = tmem + a_col(s);
                             if (stage == 0) {
                                 const uint32_t b0 = img + nif::kFrOffB0;
@@ -688,10 +800,18 @@ __global__ void __launch_bounds__(fr3::kThreads, 1)
         // row m, K' block kb (8 fp16) at kb * 2048 + 16 m; K' 0..7 zero, K' 8 + 2j / 9 + 2j = sin_j / cos_j
         const int p = threadIdx.x - 32 * kProducerWarp0;
         uint8_t* fts = smem + kOffFt;
-        for (int m = p; m < kSlots * 128; m += kProducerThreads)
-            *reinterpret_cast<uint4*>(fts + (m >> 7) * kFtBytes + 16 * (m & 127)) = make_uint4(0, 0, 0, 0);
+        for (int m = p; m < kSlots * 128; m += kProducerThreads) {
+            // the K blocks no feature lands in: fp16 K' 0..7; fp8 K' 40..47 (second half of block 2), 48..63
+            uint8_t* t = fts + (m >> 7) * kFt + 16 * (m & 127);
+            if (kFp8) {
+                *reinterpret_cast<uint4*>(t + 2 * 2048) = make_uint4(0, 0, 0, 0);
+                *reinterpret_cast<uint4*>(t + 3 * 2048) = make_uint4(0, 0, 0, 0);
+            } else {
+                *reinterpret_cast<uint4*>(t) = make_uint4(0, 0, 0, 0);
+            }
+        }
         if (blockIdx.x < n_tiles) mbar_wait(bar(kBarW), 0);   // the frequencies are in the image
-        const float* freq = reinterpret_cast<const float*>(smem + nif::kFrOffFreq);
+        const float* freq = reinterpret_cast<const float*>(smem + (kFp8 ? k8OffFreq : nif::kFrOffFreq));
         uint32_t e_phase = 0, filled = 0;
         for (uint32_t i = 0;; i += kSlots) {
             const uint32_t t0 = blockIdx.x + i * gridDim.x;
@@ -713,20 +833,39 @@ __global__ void __launch_bounds__(fr3::kThreads, 1)
                         v = en.y;
                         if (dir_input) equirect_f32(make_float3(en.x, en.y, en.z), u, v);
                     }
-                    uint32_t f[20];
+                    uint8_t* base = fts + s * kFt + 16 * m;
+                    if (kFp8) {
+                        // g = (sin_0..19, cos_0..19) in e4m3; tile row = [g_8 .. g_39 | g_0 .. g_7 | 0]
+                        float g[40];
 #pragma unroll
-                    for (int jj = 0; jj < 20; ++jj) {
-                        const float pp = fmaf(freq[2 * jj], u, freq[2 * jj + 1] * v);
-                        const float r = pp - rintf(pp);                  // exact-range turns in [-1/2, 1/2]
-                        float sn, cs;
-                        __sincosf(6.28318530717958647692f * r, &sn, &cs);
-                        f[jj] = pack_half2(sn, cs);
+                        for (int jj = 0; jj < 20; ++jj) {
+                            const float pp = fmaf(freq[2 * jj], u, freq[2 * jj + 1] * v);
+                            const float r = pp - rintf(pp);
+                            __sincosf(6.28318530717958647692f * r, &g[jj], &g[20 + jj]);
+                        }
+                        uint32_t w[10];
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) w[t] = fr8_pack(g[8 + 4 * t], g[9 + 4 * t], g[10 + 4 * t], g[11 + 4 * t]);
+                        w[8] = fr8_pack(g[0], g[1], g[2], g[3]);
+                        w[9] = fr8_pack(g[4], g[5], g[6], g[7]);
+                        *reinterpret_cast<uint4*>(base) = make_uint4(w[0], w[1], w[2], w[3]);
+                        *reinterpret_cast<uint4*>(base + 2048) = make_uint4(w[4], w[5], w[6], w[7]);
+                        *reinterpret_cast<uint2*>(base + 2 * 2048) = make_uint2(w[8], w[9]);
+                    } else {
+                        uint32_t f[20];
+#pragma unroll
+                        for (int jj = 0; jj < 20; ++jj) {
+                            const float pp = fmaf(freq[2 * jj], u, freq[2 * jj + 1] * v);
+                            const float r = pp - rintf(pp);                  // exact-range turns in [-1/2, 1/2]
+                            float sn, cs;
+                            __sincosf(6.28318530717958647692f * r, &sn, &cs);
+                            f[jj] = pack_half2(sn, cs);
+                        }
+#pragma unroll
+                        for (int kb = 1; kb < 6; ++kb)
+                            *reinterpret_cast<uint4*>(base + kb * 2048) =
+                                make_uint4(f[4 * kb - 4], f[4 * kb - 3], f[4 * kb - 2], f[4 * kb - 1]);
                     }
-                    uint8_t* base = fts + s * kFtBytes + 16 * m;
-#pragma unroll
-                    for (int kb = 1; kb < 6; ++kb)
-                        *reinterpret_cast<uint4*>(base + kb * 2048) =
-                            make_uint4(f[4 * kb - 4], f[4 * kb - 3], f[4 * kb - 2], f[4 * kb - 1]);
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic -> async proxy
                 mbar_arrive(bar(kBarFtFull + s));
@@ -754,6 +893,12 @@ __global__ void __launch_bounds__(fr3::kThreads, 1)
             tmem_wait_ld_dep4(v);
             if (ovalid) {
                 float y0 = __uint_as_float(v[0]), y1 = __uint_as_float(v[1]), y2 = __uint_as_float(v[2]);
+                if (kFp8) {
+                    const float* b4 = reinterpret_cast<const float*>(smem + k8OffBias) + k8bias(4);
+                    y0 += b4[0];
+                    y1 += b4[1];
+                    y2 += b4[2];
+                }
                 if (kDebug) {
                     dbg[((size_t)4 * n_rows + dbg_row) * 128 + 0] = y0;
                     dbg[((size_t)4 * n_rows + dbg_row) * 128 + 1] = y1;
@@ -785,7 +930,7 @@ __global__ void __launch_bounds__(fr3::kThreads, 1)
                     mbar_wait(bar(kBarDFull + team), d_phase);
                     d_phase ^= 1;
                     tc_fence_after();
-                    const uint32_t areg = tmem + a_col(s) + lane_addr + 32u * (uint32_t)h;
+                    const uint32_t areg = tmem + a_col(s) + lane_addr + (kFp8 ? 16u : 32u) * (uint32_t)h;
                     // L1 has 96 columns: the high half loads only its first 32 (units 64..87 + padding)
                     const int nchunk = (stage == 1 && h == 1) ? 1 : 2;
 #pragma unroll
@@ -803,13 +948,35 @@ __global__ void __launch_bounds__(fr3::kThreads, 1)
                         if (kDebug && valid)
                             for (int k = 0; k < 32; ++k)
                                 dbg[((size_t)stage * n_rows + row) * 128 + 64 * h + 32 * c + k] = __uint_as_float(v[k]);
+                        if (kFp8) {
+                            // + the layer's fp32 bias, ReLU, e4m3 (4 per A column)
+                            const float4* bp = reinterpret_cast<const float4*>(smem + k8OffBias) +
+                                               (k8bias(stage) + 64 * h + 32 * c) / 4;
+#pragma unroll
+                            for (int t = 0; t < 8; ++t) {
+                                const float4 b = bp[t];
+                                const float2 x01 = __fadd2_rn(make_float2(__uint_as_float(v[4 * t]), __uint_as_float(v[4 * t + 1])),
+                                                              make_float2(b.x, b.y));
+                                const float2 x23 = __fadd2_rn(make_float2(__uint_as_float(v[4 * t + 2]), __uint_as_float(v[4 * t + 3])),
+                                                              make_float2(b.z, b.w));
+                                pk[t] = fr8_pack_relu(x01.x, x01.y, x23.x, x23.y);
+                            }
+                            if (stage == 1 && h == 1) {
+                                // units 64..87 -> A columns 16..21; g_0..7 (feature-tile K' 32..39) -> 22..23
+                                const uint2 fw = *reinterpret_cast<const uint2*>(smem + kOffFt + s * kFt + 2 * 2048 + 16 * m_row);
+                                pk[6] = fw.x;
+                                pk[7] = fw.y;
+                            }
+                            tmem_st8(areg + 8u * (uint32_t)c, pk);
+                            continue;
+                        }
 #pragma unroll
                         for (int k = 0; k < 16; ++k)
                             pk[k] = relu_pack(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
                         if (stage == 1 && h == 1) {
                             // units 64..87 -> A columns 32..43; features 0..3 (feature-tile K' 8..15, the K
                             // step straddling the concat boundary) -> A columns 44..47
-                            const uint4 fw = *reinterpret_cast<const uint4*>(smem + kOffFt + s * kFtBytes + 2048 + 16 * m_row);
+                            const uint4 fw = *reinterpret_cast<const uint4*>(smem + kOffFt + s * kFt + 2048 + 16 * m_row);
                             pk[12] = fw.x;
                             pk[13] = fw.y;
                             pk[14] = fw.z;
@@ -845,12 +1012,12 @@ __global__ void __launch_bounds__(fr3::kThreads, 1)
     }
 }
 
-template <bool kDebug>
+template <bool kDebug, bool kFp8 = false>
 static cudaError_t nif_fr3_launch_t(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,
                                     int grid, float* out, float* dbg, int dir_input, cudaStream_t st) {
-    cudaError_t e = ensure_dyn_smem((const void*)nif_fr3_kernel<kDebug>, fr3::kSmemBytes);
+    cudaError_t e = ensure_dyn_smem((const void*)nif_fr3_kernel<kDebug, kFp8>, fr3::kSmemBytes);
     if (e != cudaSuccess) return e;
-    return launch_pdl(nif_fr3_kernel<kDebug>, dim3(grid), dim3(fr3::kThreads), fr3::kSmemBytes, st,
+    return launch_pdl(nif_fr3_kernel<kDebug, kFp8>, dim3(grid), dim3(fr3::kThreads), fr3::kSmemBytes, st,
                       (const uint8_t*)nif->d_smem_image, esc, esc_beta, count, out, dbg, dir_input);
 }
 
@@ -879,7 +1046,8 @@ static cudaError_t nif_launch_impl(const pt_nif* nif, const float4* esc, const f
         // (128, 4) fp16 = the paper's network: the three-tile kernel (unless the tests force the layered path)
         const char* env = std::getenv("PT_MLP_LAYERED");
         if (PT_NIF_FR3 && nif->d_smem_image && !(env && env[0] == '1'))
-            return nif_fr3_launch_t<false>(nif, esc, esc_beta, count, grid, out, nullptr, dir_input, st);
+            return nif->mlp_fp8 ? nif_fr3_launch_t<false, true>(nif, esc, esc_beta, count, grid, out, nullptr, dir_input, st)
+                                : nif_fr3_launch_t<false, false>(nif, esc, esc_beta, count, grid, out, nullptr, dir_input, st);
         return launch_mlp(const_cast<pt_nif*>(nif), esc, esc_beta, count, max_rows, out, dir_input, st);
     }
     if (nif->kind == PT_NIF_FOURIER_RELU) {

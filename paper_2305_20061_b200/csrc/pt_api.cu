@@ -512,11 +512,13 @@ int pt_nif_load_family_ex(int32_t hidden, int32_t layers, int32_t precision, con
         pt_nif_destroy(n);
         return fail(rc, msg);
     }
-    if (hidden == 128 && layers == 4 && precision == PT_NIF_FP16) {
-        // (128, 4) is the paper's network (reading R23): its fused path is the three-tile paper-NIF kernel,
-        // which reads this shared-memory image (the streamed-weight family kernel serves the other sizes)
+    if (hidden == 128 && layers == 4) {
+        // (128, 4) is the paper's network (reading R23): its fused path is the three-tile paper-NIF kernel
+        // (fp16, or e4m3 with kind::f8f6f4), which reads this shared-memory image (the streamed-weight
+        // family kernel serves the other sizes)
         std::vector<uint8_t> img;
-        pt::nif_build_smem_image_fr(blob, &img);
+        if (precision == PT_NIF_FP8) pt::nif_build_smem_image_fr8(blob, &img);
+        else pt::nif_build_smem_image_fr(blob, &img);
         n->smem_bytes = (int64_t)img.size();
         n->d_alloc_bytes = img.size();
         cudaError_t e = cache_alloc(n->device, img.size(), &n->d_smem_image);

@@ -179,6 +179,9 @@ bool trav_counts(int64_t* visits, int64_t* prim_tests, int64_t* fp64);
 void trav_counts_reset();
 void nif_build_smem_image(const uint16_t* blob, std::vector<uint8_t>* image);
 void nif_build_smem_image_fr(const uint16_t* blob, std::vector<uint8_t>* image);
+void nif_build_smem_image_fr8(const uint16_t* blob, std::vector<uint8_t>* image);   // e4m3 variant (R24)
+float half_to_float(uint16_t h);
+uint8_t float_to_e4m3(float x);   // OCP e4m3, RN, saturating (cvt.rn.satfinite.e4m3x2.f32 on the host)
 cudaError_t launch_nif(const pt_nif* nif, const float4* esc, const float4* esc_beta, const uint32_t* count,
                        int64_t max_rows, float* out, int dir_input, cudaStream_t st);
 int num_sms();   // SM count of the current device (cached per device)
