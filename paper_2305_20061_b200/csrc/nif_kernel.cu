@@ -500,6 +500,9 @@ constexpr int kNumEpiWarps = 16;
 // four producer warps (one per SM sub-partition): 40 sin/cos per row are the producers' work, and two
 // warps measured too slow to keep three tiles in flight (6.4 G inferences/s)
 constexpr int kProducerWarp0 = 2;
+#ifndef PT_FR3_DIAG
+#define PT_FR3_DIAG 0   // diagnostic builds only: 1 = producers skip the sin/cos
+#endif
 #ifndef PT_FR3_PRODUCERS
 #define PT_FR3_PRODUCERS 4
 #endif
@@ -813,22 +816,36 @@ __global__ void __launch_bounds__(fr3::kThreads, 1)
         if (blockIdx.x < n_tiles) mbar_wait(bar(kBarW), 0);   // the frequencies are in the image
         const float* freq = reinterpret_cast<const float*>(smem + (kFp8 ? k8OffFreq : nif::kFrOffFreq));
         uint32_t e_phase = 0, filled = 0;
+        // one row per producer thread: its queue entry for each slot's next tile is loaded a round ahead,
+        // so the global-load latency overlaps the waits instead of each tile's production
+        static_assert(kProducerThreads == 128, "one row per producer thread");
+        auto load_row = [&](uint32_t tile) {
+            const uint32_t row = tile * kTileM + (uint32_t)p;
+            return (tile < n_tiles && row < n_rows) ? __ldg(esc + row) : make_float4(0.5f, 0.5f, 0.0f, 0.0f);
+        };
+        float4 en_pf[kSlots];
+#pragma unroll
+        for (int s = 0; s < kSlots; ++s) en_pf[s] = load_row(blockIdx.x + s * gridDim.x);
         for (uint32_t i = 0;; i += kSlots) {
             const uint32_t t0 = blockIdx.x + i * gridDim.x;
             if (t0 >= n_tiles) break;
             const int nslots = slots_in_round(t0, n_tiles);
-            for (int s = 0; s < nslots; ++s) {
+#pragma unroll
+            for (int s = 0; s < kSlots; ++s) {
+                if (s >= nslots) break;
                 const uint32_t tile = t0 + s * gridDim.x;
                 if ((filled >> s) & 1u) {
                     mbar_wait(bar(kBarFtEmpty + s), (e_phase >> s) & 1u);
                     e_phase ^= 1u << s;
                 }
                 filled |= 1u << s;
-                for (int m = p; m < 128; m += kProducerThreads) {
+                const float4 en = en_pf[s];
+                en_pf[s] = load_row(tile + kSlots * gridDim.x);
+                {
+                    const int m = p;
                     const uint32_t row = tile * kTileM + m;
                     float u = 0.5f, v = 0.5f;
                     if (row < n_rows) {
-                        const float4 en = __ldg(esc + row);
                         u = en.x;
                         v = en.y;
                         if (dir_input) equirect_f32(make_float3(en.x, en.y, en.z), u, v);
@@ -858,7 +875,8 @@ __global__ void __launch_bounds__(fr3::kThreads, 1)
                             const float pp = fmaf(freq[2 * jj], u, freq[2 * jj + 1] * v);
                             const float r = pp - rintf(pp);                  // exact-range turns in [-1/2, 1/2]
                             float sn, cs;
-                            __sincosf(6.28318530717958647692f * r, &sn, &cs);
+                            if (PT_FR3_DIAG == 1) { sn = r; cs = pp; }   // diagnostic: no sin/cos (wrong results)
+                            else __sincosf(6.28318530717958647692f * r, &sn, &cs);
                             f[jj] = pack_half2(sn, cs);
                         }
 #pragma unroll
