@@ -511,17 +511,27 @@ constexpr int kProducerThreads = 32 * kProducerWarps;
 constexpr int kFirstEpiWarp = kProducerWarp0 + kProducerWarps;   // 6
 constexpr int kThreads = 32 * (kFirstEpiWarp + kNumEpiWarps);     // 704
 constexpr int kFtBytes = 128 * 48 * 2;                          // feature tile: 128 rows x K' 48 (fp16)
+// feature tiles per slot: 2 = double-buffered by round parity, so the producers can stage a slot's next
+// tile before the current one's concat layer (L2) has read its features
+#ifndef PT_FR3_FT_BUFS
+#define PT_FR3_FT_BUFS 2
+#endif
+constexpr int kFtBufs = PT_FR3_FT_BUFS;
+constexpr int kNumFt = kSlots * kFtBufs;
 constexpr int kOffBars = ((kFrImageBytes + 1023) / 1024) * 1024;
-constexpr int kNumBars = 1 + (3 + kIssuers) * kSlots + 2 * kDRegions;
+constexpr int kNumBars = 1 + (1 + kIssuers) * kSlots + 2 * kNumFt + 2 * kDRegions;
 constexpr int kOffTmemSlot = kOffBars + 8 * kNumBars;
 constexpr int kOffFt = ((kOffTmemSlot + 16 + 1023) / 1024) * 1024;
-constexpr int kSmemBytes = kOffFt + kSlots * kFtBytes;
+constexpr int kSmemBytes = kOffFt + kNumFt * kFtBytes;
+__host__ __device__ constexpr int ft_buf(int s, uint32_t i) {   // slot s in the round starting at i (i += kSlots)
+    return s + kSlots * (int)((i / kSlots) % kFtBufs);
+}
 enum {
     kBarW = 0,
     kBarAReady = 1,   // a_ready(s, consumer p) at kBarAReady + kIssuers s + p
-    kBarFtFull = kBarAReady + kIssuers * kSlots,
-    kBarFtEmpty = kBarFtFull + kSlots,
-    kBarOFull = kBarFtEmpty + kSlots,
+    kBarFtFull = kBarAReady + kIssuers * kSlots,   // per feature tile (kNumFt)
+    kBarFtEmpty = kBarFtFull + kNumFt,
+    kBarOFull = kBarFtEmpty + kNumFt,
     kBarDFull = kBarOFull + kSlots,
     kBarDEmpty = kBarDFull + kDRegions
 };
@@ -630,9 +640,11 @@ __global__ void __launch_bounds__(fr3::kThreads, 1)
         mbar_init(bar(kBarW), 1);
         for (int s = 0; s < kSlots; ++s) {
             for (int p = 0; p < kIssuers; ++p) mbar_init(bar(kBarAReady + kIssuers * s + p), kTeamWarps);
-            mbar_init(bar(kBarFtFull + s), kProducerThreads);
-            mbar_init(bar(kBarFtEmpty + s), 1);
             mbar_init(bar(kBarOFull + s), 1);
+        }
+        for (int b = 0; b < kNumFt; ++b) {
+            mbar_init(bar(kBarFtFull + b), kProducerThreads);
+            mbar_init(bar(kBarFtEmpty + b), 1);
         }
         for (int j = 0; j < kDRegions; ++j) {
             mbar_init(bar(kBarDFull + j), 1);
@@ -715,8 +727,9 @@ __global__ void __launch_bounds__(fr3::kThreads, 1)
                         if ((uint32_t)j != me) continue;
                         if (stage == 0) {
                             if (i > 0) issue_out(s);
-                            mbar_wait(bar(kBarFtFull + s), (f_phase >> s) & 1u);   // features staged
-                            f_phase ^= 1u << s;
+                            const int fb = ft_buf(s, i);
+                            mbar_wait(bar(kBarFtFull + fb), (f_phase >> fb) & 1u);   // features staged
+                            f_phase ^= 1u << fb;
                         } else {
                             mbar_wait(bar(kBarAReady + kIssuers * s + (int)me), (a_phase >> s) & 1u);
                             a_phase ^= 1u << s;
@@ -727,7 +740,7 @@ __global__ void __launch_bounds__(fr3::kThreads, 1)
                         }
                         tc_fence_after();
                         const uint32_t dt = tmem + d_col(j);
-                        const uint32_t ft = smem_u32(smem + kOffFt + s * kFt);
+                        const uint32_t ft = smem_u32(smem + kOffFt + ft_buf(s, i) * kFt);
                         if (kFp8 && elect_one()) {
                             // e4m3, K = 32 per MMA, no bias steps (the epilogue adds the fp32 biases)
                             const uint32_t at = tmem + a_col(s);
@@ -755,7 +768,7 @@ __global__ void __launch_bounds__(fr3::kThreads, 1)
                                               k > 0);
                             }
                             mma_commit(bar(kBarDFull + j));
-                            if (stage == 2) mma_commit(bar(kBarFtEmpty + s));
+                            if (stage == 2) mma_commit(bar(kBarFtEmpty + ft_buf(s, i)));
                         } else if (!kFp8 && elect_one()) {
                             const uint32_t at = tmem + a_col(s);
                             if (stage == 0) {
@@ -789,7 +802,7 @@ __global__ void __launch_bounds__(fr3::kThreads, 1)
                                 mma_ss(dt, ones, smem_desc(b3 + 16 * 2048, 2048, 128), idesc(128), 1);
                             }
                             mma_commit(bar(kBarDFull + j));
-                            if (stage == 2) mma_commit(bar(kBarFtEmpty + s));   // feature tile free after L2
+                            if (stage == 2) mma_commit(bar(kBarFtEmpty + ft_buf(s, i)));   // feature tile free after L2
                         }
                         __syncwarp();
                     }
@@ -803,7 +816,7 @@ __global__ void __launch_bounds__(fr3::kThreads, 1)
         // row m, K' block kb (8 fp16) at kb * 2048 + 16 m; K' 0..7 zero, K' 8 + 2j / 9 + 2j = sin_j / cos_j
         const int p = threadIdx.x - 32 * kProducerWarp0;
         uint8_t* fts = smem + kOffFt;
-        for (int m = p; m < kSlots * 128; m += kProducerThreads) {
+        for (int m = p; m < kNumFt * 128; m += kProducerThreads) {
             // the K blocks no feature lands in: fp16 K' 0..7; fp8 K' 40..47 (second half of block 2), 48..63
             uint8_t* t = fts + (m >> 7) * kFt + 16 * (m & 127);
             if (kFp8) {
@@ -834,11 +847,12 @@ __global__ void __launch_bounds__(fr3::kThreads, 1)
             for (int s = 0; s < kSlots; ++s) {
                 if (s >= nslots) break;
                 const uint32_t tile = t0 + s * gridDim.x;
-                if ((filled >> s) & 1u) {
-                    mbar_wait(bar(kBarFtEmpty + s), (e_phase >> s) & 1u);
-                    e_phase ^= 1u << s;
+                const int fb = ft_buf(s, i);
+                if ((filled >> fb) & 1u) {
+                    mbar_wait(bar(kBarFtEmpty + fb), (e_phase >> fb) & 1u);
+                    e_phase ^= 1u << fb;
                 }
-                filled |= 1u << s;
+                filled |= 1u << fb;
                 const float4 en = en_pf[s];
                 en_pf[s] = load_row(tile + kSlots * gridDim.x);
                 {
@@ -850,7 +864,7 @@ __global__ void __launch_bounds__(fr3::kThreads, 1)
                         v = en.y;
                         if (dir_input) equirect_f32(make_float3(en.x, en.y, en.z), u, v);
                     }
-                    uint8_t* base = fts + s * kFt + 16 * m;
+                    uint8_t* base = fts + fb * kFt + 16 * m;
                     if (kFp8) {
                         // g = (sin_0..19, cos_0..19) in e4m3; tile row = [g_8 .. g_39 | g_0 .. g_7 | 0]
                         float g[40];
@@ -886,7 +900,7 @@ __global__ void __launch_bounds__(fr3::kThreads, 1)
                     }
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic -> async proxy
-                mbar_arrive(bar(kBarFtFull + s));
+                mbar_arrive(bar(kBarFtFull + fb));
             }
         }
     } else if (warp >= kFirstEpiWarp) {
@@ -981,7 +995,7 @@ __global__ void __launch_bounds__(fr3::kThreads, 1)
                             }
                             if (stage == 1 && h == 1) {
                                 // units 64..87 -> A columns 16..21; g_0..7 (feature-tile K' 32..39) -> 22..23
-                                const uint2 fw = *reinterpret_cast<const uint2*>(smem + kOffFt + s * kFt + 2 * 2048 + 16 * m_row);
+                                const uint2 fw = *reinterpret_cast<const uint2*>(smem + kOffFt + ft_buf(s, i) * kFt + 2 * 2048 + 16 * m_row);
                                 pk[6] = fw.x;
                                 pk[7] = fw.y;
                             }
@@ -994,7 +1008,7 @@ __global__ void __launch_bounds__(fr3::kThreads, 1)
                         if (stage == 1 && h == 1) {
                             // units 64..87 -> A columns 32..43; features 0..3 (feature-tile K' 8..15, the K
                             // step straddling the concat boundary) -> A columns 44..47
-                            const uint4 fw = *reinterpret_cast<const uint4*>(smem + kOffFt + s * kFt + 2048 + 16 * m_row);
+                            const uint4 fw = *reinterpret_cast<const uint4*>(smem + kOffFt + ft_buf(s, i) * kFt + 2048 + 16 * m_row);
                             pk[12] = fw.x;
                             pk[13] = fw.y;
                             pk[14] = fw.z;
